@@ -1,0 +1,438 @@
+"""Benchmark of the B200 tensor path (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload sort|join] [--no-join] [--no-cpu-baseline]
+
+Workload (BASELINE.json configs[1], the single-GPU config the metric is quoted
+on): cfg2 — ORDER BY of 10,000,000 rows, int64 key uniform over the full
+signed range with ~1% duplicates copied from earlier rows, int32 payload
+(Bytes(4)), stable ascending; output = sorted keys, sorted payload and the
+row-id permutation. A "step" is one such sort.
+
+  value  — Mrows/s with inputs resident in HBM (CUDA events per step, L2
+           flushed by a 256 MiB write between steps, max over ranks).
+  e2e    — Mrows/s through the public drop-in API tensor_sort(Relation) with
+           numpy (host) inputs and outputs: H2D + kernels + D2H per step.
+  roofline — the onesweep digit pass (dominant kernel): algorithmic bytes per
+           launch / its average event-timed duration vs measured HBM GB/s.
+  cpu_baseline — the reference algorithm (oracle/ numpy port of
+           tensorpath.py:232-252) on a bounded sample, host cores.
+  join_cfg1 — BASELINE cfg1 (1M x 1M equi-join) P50/P99, device and e2e,
+           next to the CPU tensor path's P99 (north-star target: >= 20x).
+
+--impl reference runs only the reference algorithm (CPU, rank 0) on the same
+workload and prints the same metric with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sort_throughput_cfg2"
+UNIT = "Mrows/s"
+WORKLOAD = ("cfg2: ORDER BY sort of 10,000,000 rows (int64 key uniform over the signed 64-bit range, "
+            "~1% duplicates, int32 payload as Bytes(4)), stable ascending; outputs sorted keys, payload, permutation")
+N_ROWS = 10_000_000
+
+
+def percentile(samples, q):
+    """Nearest-rank percentile, rank ceil(q/100 * n) (bench.py:101-114)."""
+    ordered = sorted(samples)
+    rank = math.ceil(Fraction(q) * len(ordered) / 100)
+    return ordered[max(rank, 1) - 1]
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5,
+                ).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def active_digit_passes(keys: np.ndarray, descending: bool = False):
+    u = keys.view(np.uint64)
+    if descending:
+        u = ~u
+    u = u ^ np.uint64(1 << 63)
+    act = []
+    for p in range(8):
+        d = (u >> np.uint64(8 * p)) & np.uint64(255)
+        act.append(bool(d.min() != d.max()))
+    return act
+
+
+def pass_bytes(n: int, active):
+    """Algorithmic bytes of each onesweep launch: the first
+    active pass reads keys (8n; row ids are generated) and writes key + id
+    (12n); later passes read and write 12n each; the last writes the final
+    int64 keys and uint32 permutation (12n)."""
+    idx = [p for p, a in enumerate(active) if a]
+    out = {}
+    for j, p in enumerate(idx):
+        out[p] = (8 if j == 0 else 12) * n + 12 * n
+    return out
+
+
+# ---------------------------------------------------------------- CPU arm
+def cpu_sort_sample(keys, payload, reps):
+    """The reference's tensor_sort algorithm (numpy port in oracle/) on host cores."""
+    from oracle import tensorpath_oracle as O
+
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        perm = O.sort_permutation([keys], [False])
+        _k, _p = keys[perm], payload[perm]
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_join_sample(r, s, reps):
+    from oracle import tensorpath_oracle as O
+
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.join_columns(list(r.columns), 0, list(s.columns), 0)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2602_21237_b200 import synth
+
+    rel = synth.cfg2_relation(N_ROWS)
+    keys, payload = rel.column("key"), rel.column("payload")
+    # one full cfg2 sort costs ~3-4 s on one core; bound the whole run to ~2.5 min
+    per_full = 4.0
+    budget = 150.0
+    sample = N_ROWS if (args.steps + args.warmup) * per_full <= budget else max(
+        500_000, int(N_ROWS * budget / ((args.steps + args.warmup) * per_full)))
+    k, p = keys[:sample], payload[:sample]
+    cpu_sort_sample(k, p, args.warmup)
+    times = cpu_sort_sample(k, p, args.steps)
+    value = sample * len(times) / sum(times) / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rows": N_ROWS, "sample_rows_per_step": sample},
+        "p50_ms": round(1e3 * percentile(times, 50), 3), "p99_ms": round(1e3 * percentile(times, 99), 3),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{sample} rows of the cfg2 input per step (numpy, single-threaded as the "
+                                   f"reference; host has {os.cpu_count()} cores)"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_21237_b200 import SortSpec, _capi, engine, synth, tensor_join, tensor_sort, to_tensor
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _capi.load()
+
+    # each rank sorts its own cfg2 shard (weak scaling; seed 0 on rank 0 = BASELINE cfg2)
+    rel = synth.cfg2_relation(N_ROWS, seed=rank)
+    keys_h, pay_h = rel.column("key"), rel.column("payload")
+    n = len(keys_h)
+    active = active_digit_passes(keys_h)
+    keys_d = torch.from_numpy(keys_h.copy()).to(dev)
+    pay_d = torch.from_numpy(pay_h.copy()).to(dev)
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+    ws = engine.workspace(lib.rl_sort_workspace_bytes(n), dev)
+    s = engine.stream_handle()
+
+    def device_step(events=None):
+        sorted_keys = torch.empty(n, dtype=torch.int64, device=dev)
+        perm = torch.empty(n, dtype=torch.int32, device=dev)
+        out_pay = torch.empty((n, 4), dtype=torch.uint8, device=dev)
+        if events is None:
+            _capi.check(lib.rl_sort_axis(ctypes.c_void_p(keys_d.data_ptr()), 0, 8, 0, 0, None, n,
+                                         ctypes.c_void_p(sorted_keys.data_ptr()), ctypes.c_void_p(perm.data_ptr()),
+                                         ctypes.c_void_p(ws.data_ptr()), ws.numel(), s), "sort")
+        else:
+            arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
+            _capi.check(lib.rl_sort_axis_profiled(ctypes.c_void_p(keys_d.data_ptr()), 0, 8, 0, 0, None, n,
+                                                  ctypes.c_void_p(sorted_keys.data_ptr()),
+                                                  ctypes.c_void_p(perm.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                                  ws.numel(), s, arr), "sort")
+        engine.gather_rows(perm, [engine.OutColumn(pay_d, out_pay, 4, 0)])
+        return sorted_keys, perm, out_pay
+
+    # correctness gate before timing: sorted + permutation + stable (cheap device checks)
+    sk, perm, _ = device_step()
+    p64 = perm.to(torch.int64) & 0xFFFFFFFF
+    ok = bool((sk[1:] >= sk[:-1]).all()) and bool((keys_d[p64] == sk).all())
+    ties = sk[1:] == sk[:-1]
+    ok = ok and bool((p64[1:][ties] > p64[:-1][ties]).all())
+    if not ok:
+        raise SystemExit("device sort failed its self-check; refusing to report a number")
+    del sk, perm, p64, ties
+
+    for _ in range(args.warmup):
+        device_step()
+    torch.cuda.synchronize()
+
+    def make_events(k):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        for e in evs:  # force creation so the raw handle exists
+            e.record()
+        return evs
+
+    step_ev = [make_events(2) for _ in range(args.steps)]
+    pass_ev = [make_events(_capi.RL_SORT_EVENTS) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.rl_launch_count()
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush, outside the timed window
+            step_ev[k][0].record()
+            device_step(pass_ev[k])
+            step_ev[k][1].record()
+        torch.cuda.synchronize()
+    launches = lib.rl_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * n * args.steps / (total_ms / 1e3) / 1e6
+
+    # roofline of the onesweep pass kernel (events around each launch)
+    pbytes = pass_bytes(n, active)
+    pass_ms = {p: [] for p in pbytes}
+    for evs in pass_ev:
+        for p in pbytes:
+            pass_ms[p].append(evs[2 + p].elapsed_time(evs[3 + p]))
+    launches_timed = sum(len(v) for v in pass_ms.values())
+    total_pass_ms = sum(sum(v) for v in pass_ms.values())
+    alg_bytes = sum(pbytes[p] * len(pass_ms[p]) for p in pbytes)
+    achieved = alg_bytes / (total_pass_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("onesweep_kernel_bytes_per_launch")
+        except Exception:
+            traffic = None
+    hist_ms = [evs[0].elapsed_time(evs[1]) for evs in pass_ev]
+    sort_share = total_pass_ms / total_ms
+
+    # e2e through the public drop-in API, host numpy in/out
+    spec = SortSpec(("key",))
+    for _ in range(max(1, args.warmup)):
+        tensor_sort(rel, spec)
+    e2e_t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out, _st = tensor_sort(rel, spec)
+        e2e_t.append(time.perf_counter() - t0)
+    del out
+    e2e_total = sum(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * n * args.steps / e2e_total / 1e6
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rows_per_gpu": n, "parallelism": f"replicas{world}",
+                   "l2": "flushed between timed steps (256 MiB write)", "seed_per_rank": "rank"},
+        "p50_ms": round(percentile(step_ms, 50), 4), "p99_ms": round(percentile(step_ms, 99), 4),
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": n * 12,
+                "d2h_bytes_per_step": n * 12, "api": "tensor_sort(Relation numpy) -> (Relation, SpillStats)",
+                "p50_ms": round(1e3 * percentile(e2e_t, 50), 3), "p99_ms": round(1e3 * percentile(e2e_t, 99), 3)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "rl::radix::onesweep_kernel", "peak_source": peak_src,
+                     "launches_timed": launches_timed, "active_passes": sum(active),
+                     "avg_launch_us": round(1e3 * total_pass_ms / max(launches_timed, 1), 2),
+                     "alg_bytes_per_launch": int(alg_bytes / max(launches_timed, 1)),
+                     "share_of_step": round(sort_share, 4), "hist_kernel_us": round(1e3 * statistics.mean(hist_ms), 2)},
+        "clocks": clocks.summary(),
+        "gpu_launches": int(launches),
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        reps = 3
+        t = cpu_sort_sample(keys_h, pay_h, reps)
+        line["cpu_baseline"] = {"value": round(n * reps / sum(t) / 1e6, 3), "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"{reps} full cfg2 sorts of {n} rows (numpy port of tensorpath.py:232-252, "
+                                          f"single-threaded; host has {os.cpu_count()} cores)"}
+
+    if not args.no_join:
+        line["join_cfg1"] = join_cfg1(args, dev, rank, world)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def join_cfg1(args, dev, rank, world):
+    """BASELINE cfg1: 1M x 1M uniform equi-join, latency percentiles."""
+    import torch
+
+    from paper_2602_21237_b200 import engine, synth, tensor_join, to_tensor
+
+    r, s = synth.cfg1_relations()
+    rk = torch.from_numpy(r.column("key").copy()).to(dev)
+    sk = torch.from_numpy(s.column("key").copy()).to(dev)
+    rp = torch.from_numpy(r.column("payload").copy()).to(dev)
+    sp = torch.from_numpy(s.column("payload").copy()).to(dev)
+
+    def device_join():
+        li, ri = engine.index_keys(rk), engine.index_keys(sk)
+        al = engine.align(li, ri)
+        m, total = engine.fetch_scalars(al.m_total)  # the one sizing sync
+        cols = [engine.OutColumn(None, torch.empty(total, dtype=torch.int64, device=dev), 8, 2),
+                engine.OutColumn(rp, torch.empty(total, dtype=torch.int64, device=dev), 8, 0),
+                engine.OutColumn(sp, torch.empty(total, dtype=torch.int64, device=dev), 8, 1)]
+        engine.expand(al, m, li, ri, 0, total, cols)
+        return total
+
+    reps = 100
+    for _ in range(5):
+        device_join()
+    torch.cuda.synchronize()
+    dev_ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        total = device_join()
+        b.record()
+        b.synchronize()
+        dev_ms.append(a.elapsed_time(b))
+    for _ in range(3):
+        tensor_join(to_tensor(r, "key"), to_tensor(s, "key"))
+    e2e_ms = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out, _ = tensor_join(to_tensor(r, "key"), to_tensor(s, "key"))
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    res = {
+        "workload": "cfg1: 1M x 1M uniform int64 keys in [0,1e6), int64 payload = row id, seeds 0/1",
+        "matches": int(total), "reps": reps,
+        "device_p50_ms": round(percentile(dev_ms, 50), 4), "device_p99_ms": round(percentile(dev_ms, 99), 4),
+        "e2e_p50_ms": round(percentile(e2e_ms, 50), 3), "e2e_p99_ms": round(percentile(e2e_ms, 99), 3),
+        "device_mrows_per_s": round(2e6 / (statistics.median(dev_ms) / 1e3) / 1e6, 1),
+        "e2e_mrows_per_s": round(2e6 / (statistics.median(e2e_ms) / 1e3) / 1e6, 1),
+        "e2e_api": "tensor_join(to_tensor(R), to_tensor(S)) on numpy Relations",
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t = cpu_join_sample(r, s, 20)
+        res["cpu_tensor_path"] = {"p50_ms": round(1e3 * percentile(t, 50), 2), "p99_ms": round(1e3 * percentile(t, 99), 2),
+                                  "reps": 20, "cores": 1, "kind": "port"}
+        res["p99_speedup_e2e_vs_cpu"] = round(res["cpu_tensor_path"]["p99_ms"] / res["e2e_p99_ms"], 1)
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-join", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

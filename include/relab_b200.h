@@ -1,0 +1,226 @@
+/*
+ * relab_b200.h — C ABI of the B200 tensor path (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's tensor path
+ * (/root/reference/pkg/src/relab/tensorpath.py). The reference is pure
+ * Python + numpy, so its "FFI" for this path is the Python call into
+ * numpy primitives; every entry point below replaces one group of those
+ * primitives and is bound from Python with ctypes
+ * (paper_2602_21237_b200/_capi.py).
+ *
+ * Conventions
+ *   - All data pointers are DEVICE pointers unless a parameter says "host".
+ *   - Buffers are caller-allocated; the library never allocates or frees
+ *     caller memory and keeps no global mutable state. Scratch space comes
+ *     from the caller through (ws, ws_bytes); size it with the matching
+ *     *_workspace_bytes() query. ws must be 256-byte aligned.
+ *   - `stream` is a cudaStream_t passed as void*. Every call is
+ *     asynchronous on that stream; nothing synchronises the host.
+ *   - Row indices (positions, permutations, starts, counts, row ids) are
+ *     uint32: one call handles at most RL_MAX_ROWS rows per side. The
+ *     Python layer widens them to int64 when it hands numpy arrays back,
+ *     matching the reference dtypes.
+ *   - Counts that the host does not need before the next launch (distinct
+ *     keys D, matched keys M, total output pairs) are written to device
+ *     scalars, so a join runs with exactly one device→host sync (the output
+ *     size, needed to allocate the output columns).
+ *   - Return value: RL_OK or an RL_ERR_* status; rl_strerror() names it.
+ */
+#ifndef RELAB_B200_H
+#define RELAB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RL_API __attribute__((visibility("default")))
+#else
+#define RL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RL_ABI_VERSION 1
+
+#define RL_OK 0
+#define RL_ERR_BAD_ARG 1          /* ValueError on the Python side            */
+#define RL_ERR_OUTPUT_TOO_LARGE 2 /* relab.errors.OutputTooLarge               */
+#define RL_ERR_WORKSPACE 3        /* workspace too small / misaligned          */
+#define RL_ERR_TOO_MANY_ROWS 4    /* n > RL_MAX_ROWS                           */
+#define RL_ERR_CUDA 1000          /* RL_ERR_CUDA + cudaError_t                 */
+
+#define RL_MAX_ROWS 4294967295LL  /* uint32 row ids */
+
+/* Column kinds (relation.py:23-40: Int64, Bytes(w)). */
+#define RL_COL_INT64 0
+#define RL_COL_BYTES 1
+
+/* Which row a gathered output column reads (tensorpath.py:174-185). */
+#define RL_SIDE_LEFT 0   /* source row = left row id of the pair          */
+#define RL_SIDE_RIGHT 1  /* source row = right row id of the pair         */
+#define RL_SIDE_KEY 2    /* the matched key itself (int64, src ignored)    */
+
+#define RL_MAX_COLUMNS 32
+
+typedef struct rl_column {
+  const void* src; /* device: n_src rows × width bytes, row-major          */
+  void* dst;       /* device: out rows × width bytes                       */
+  int32_t width;   /* bytes per row: 8 for Int64, w for Bytes(w) (w >= 0)  */
+  int32_t side;    /* RL_SIDE_*                                            */
+} rl_column;
+
+RL_API int rl_abi_version(void);
+RL_API const char* rl_strerror(int status);
+/* Number of SMs of the current device (grid sizing; 148 on B200). */
+RL_API int rl_device_sm_count(void);
+/* Process-wide count of kernels this library has launched (a statistic for
+ * the benchmark's gpu_launches claim; monotone, never reset). */
+RL_API int64_t rl_launch_count(void);
+
+/* ---------------------------------------------------------------------
+ * K1+K2  Stable LSD radix sort of one key word, carrying row ids.
+ *
+ * Replaces  _stable_key_order      tensorpath.py:62-75
+ *           _stable_axis_order     tensorpath.py:206-229
+ *           one refinement step    tensorpath.py:244-246
+ *             perm = perm[_stable_axis_order(axis[perm], direction)]
+ *
+ * The key of output slot i is word `word` of row r = perm_in[i] (or r = i
+ * when perm_in is NULL) of column `col`:
+ *   RL_COL_INT64 (width 8, word 0): the int64 value, ordered as signed;
+ *       descending uses the bitwise complement (tensorpath.py:215).
+ *   RL_COL_BYTES (width w, word j < ceil(w/8)): bytes [8j, 8j+8) of the
+ *       row, complemented first when descending, zero-padded, read
+ *       big-endian (tensorpath.py:220-225).
+ * Output: perm_out[i] = the row at sorted position i; ties keep input
+ * order (stable). sorted_keys_out (optional, INT64 without perm_in only)
+ * receives the sorted int64 key values (tensorpath.py:84 `sk`).
+ * Passes whose 8-bit digit is constant over the input are skipped on the
+ * device (no host sync).
+ * --------------------------------------------------------------------- */
+RL_API size_t rl_sort_workspace_bytes(int64_t n);
+RL_API int rl_sort_axis(const void* col, int32_t col_kind, int32_t width,
+                 int32_t word, int32_t descending, const uint32_t* perm_in,
+                 int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
+                 void* ws, size_t ws_bytes, void* stream);
+
+/* Same as rl_sort_axis, additionally recording events[i] (cudaEvent_t,
+ * created by the caller with timing enabled) on `stream` before kernel i and
+ * events[RL_SORT_EVENTS-1] after the last one: [0] histogram, [1] plan,
+ * [2..9] digit passes 0..7, [10] finalize, [11] end. Used by bench.py to time
+ * the onesweep pass kernel live inside the timed region. */
+#define RL_SORT_EVENTS 12
+RL_API int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width,
+                 int32_t word, int32_t descending, const uint32_t* perm_in,
+                 int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
+                 void* ws, size_t ws_bytes, void* stream,
+                 void* const* events);
+
+/* ---------------------------------------------------------------------
+ * K3  Run bounds of sorted keys: distinct keys + CSR offsets.
+ *
+ * Replaces tensorpath.py:84-92
+ *   bounds = flatnonzero(concat([True], sk[1:] != sk[:-1]))
+ *   key_values = sk[bounds]; offsets = concat([bounds, [n]])
+ * key_values and offsets need capacity n and n+1. *d_out (device int64)
+ * receives D; offsets[D] = n. n == 0 gives D = 0, offsets = [0].
+ * --------------------------------------------------------------------- */
+RL_API size_t rl_run_bounds_workspace_bytes(int64_t n);
+RL_API int rl_run_bounds(const int64_t* sorted_keys, int64_t n, int64_t* key_values,
+                  uint32_t* offsets, int64_t* d_out, void* ws,
+                  size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K4+K5  Key-axis alignment and join sizing.
+ *
+ * Replaces key_axis_align  tensorpath.py:109-128 (searchsorted + mask +
+ * compaction) and the sizing of tensor_join tensorpath.py:149-161
+ * (per_key = lc*rc, cumsum). Every left distinct key is searched in the
+ * right distinct keys (vectorised searchsorted, lower bound); matches are
+ * compacted in left-key order. D_left / D_right are read from device
+ * scalars (rl_run_bounds' d_out); d_left_cap bounds the grid.
+ * Outputs (capacity d_left_cap, pair_offsets d_left_cap+1):
+ *   matched_keys[M]; left_starts/left_counts/right_starts/right_counts[M];
+ *   pair_offsets[0..M] = exclusive prefix of lc*rc (uint64),
+ *   pair_offsets[M] = total; *m_out = M; *total_out = total.
+ * --------------------------------------------------------------------- */
+RL_API size_t rl_align_workspace_bytes(int64_t d_left_cap);
+RL_API int rl_key_axis_align(const int64_t* left_keys, const uint32_t* left_offsets,
+                      const int64_t* d_left, int64_t d_left_cap,
+                      const int64_t* right_keys,
+                      const uint32_t* right_offsets, const int64_t* d_right,
+                      int64_t* matched_keys, uint32_t* left_starts,
+                      uint32_t* left_counts, uint32_t* right_starts,
+                      uint32_t* right_counts, uint64_t* pair_offsets,
+                      int64_t* m_out, uint64_t* total_out, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K6+K7  Run expansion fused with the column gathers.
+ *
+ * Replaces tensorpath.py:157-185: output pair t (global index in
+ * [out_begin, out_end)) belongs to matched key g with
+ * pair_offsets[g] <= t < pair_offsets[g+1]; local = t - pair_offsets[g];
+ * (li, ri) = divmod(local, right_counts[g]);
+ * left row  = left_positions[left_starts[g] + li],
+ * right row = right_positions[right_starts[g] + ri].
+ * Emits rows in (key, left row, right row) order — byte-identical to the
+ * reference. Optional outputs (NULL to skip): left_rows/right_rows
+ * (uint32, index t - out_begin) and up to RL_MAX_COLUMNS gathered columns
+ * (rl_column, host array; dst indexed by t - out_begin).
+ * m (number of matched keys) is passed from the host.
+ * --------------------------------------------------------------------- */
+RL_API int rl_join_expand(const int64_t* matched_keys, const uint32_t* left_starts,
+                   const uint32_t* right_starts, const uint32_t* right_counts,
+                   const uint64_t* pair_offsets, int64_t m,
+                   const uint32_t* left_positions,
+                   const uint32_t* right_positions, uint64_t out_begin,
+                   uint64_t out_end, uint32_t* left_rows_out,
+                   uint32_t* right_rows_out, const rl_column* columns,
+                   int32_t n_columns, void* stream);
+
+/* Order-independent checksum of the pairs in [out_begin, out_end):
+ * sum over pairs of fmix64((left_row << 32) | right_row), into *sum_out
+ * (device uint64, accumulated: zero it first). For joins too large to
+ * materialise (BASELINE cfg3: 2.29e12 pairs). */
+RL_API int rl_join_pair_checksum(const uint32_t* left_starts,
+                          const uint32_t* right_starts,
+                          const uint32_t* right_counts,
+                          const uint64_t* pair_offsets, int64_t m,
+                          const uint32_t* left_positions,
+                          const uint32_t* right_positions, uint64_t out_begin,
+                          uint64_t out_end, uint64_t* sum_out, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K7  Row gather by a uint32 index vector (Relation.take,
+ * relation.py:133-136, as used by tensor_sort tensorpath.py:247).
+ * out row t of every column = src row rows[t]; side must be RL_SIDE_LEFT.
+ * --------------------------------------------------------------------- */
+RL_API int rl_gather_rows(const uint32_t* rows, int64_t m, const rl_column* columns,
+                   int32_t n_columns, void* stream);
+
+/* Widen uint32 → int64 (positions/offsets handed back as numpy int64). */
+RL_API int rl_widen_u32(const uint32_t* src, int64_t n, int64_t* dst, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K8  Hash partitioning for the multi-GPU join (no reference
+ * counterpart; the hash is hash_i64, hashing.py:54-61:
+ * h(k) = fmix64(u64(k) ^ fmix64(seed)), destination = h(k) mod P).
+ * Stable within each destination: rows keep input order.
+ * counts_out[P] (device int64) receives per-destination row counts;
+ * the packed outputs are grouped by destination in rank order.
+ * --------------------------------------------------------------------- */
+RL_API size_t rl_partition_workspace_bytes(int64_t n, int32_t parts);
+RL_API int rl_hash_partition(const int64_t* keys, int64_t n, int32_t parts,
+                      uint64_t seed, const rl_column* columns,
+                      int32_t n_columns, uint32_t* row_ids_out,
+                      int64_t* counts_out, void* ws, size_t ws_bytes,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RELAB_B200_H */

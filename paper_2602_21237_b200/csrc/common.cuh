@@ -1,0 +1,162 @@
+// common.cuh — shared device helpers for the sm_100a tensor-path kernels.
+//
+// Decoupled look-back status words (Merrill & Garland single-pass scan;
+// Adinets & Merrill onesweep) are packed into one 64-bit word so a
+// reader sees flag, epoch and value atomically:
+//
+//   [63:62] flag   0 = not yet published, 1 = tile aggregate, 2 = inclusive
+//   [61:56] epoch  which pass/launch wrote it (stale words are ignored)
+//   [55:0]  value
+//
+// The status arrays are zeroed once per call (one cudaMemsetAsync); the
+// epoch lets the eight radix passes of one sort share a single array.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/relab_b200.h"
+
+namespace rl {
+
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagIncl = 2ull << 62;
+constexpr uint64_t kFlagMask = 3ull << 62;
+constexpr uint64_t kValueMask = (1ull << 56) - 1;
+
+__device__ __forceinline__ uint64_t pack_status(uint64_t flag, uint32_t epoch,
+                                                uint64_t value) {
+  return flag | (uint64_t(epoch & 63u) << 56) | (value & kValueMask);
+}
+__device__ __forceinline__ uint32_t status_epoch(uint64_t s) {
+  return uint32_t(s >> 56) & 63u;
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Streaming stores: output columns are written once and not re-read by
+// this kernel, so keep them from displacing the gathered inputs in L2.
+__device__ __forceinline__ void st_stream(uint64_t* p, uint64_t v) { __stcs(reinterpret_cast<unsigned long long*>(p), v); }
+__device__ __forceinline__ void st_stream(uint32_t* p, uint32_t v) { __stcs(p, v); }
+
+// Murmur3 fmix64 (hashing.py:32-40).
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xFF51AFD7ED558CCDull;
+  x ^= x >> 33;
+  x *= 0xC4CEB9FE1A85EC53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+// Block-wide exclusive scan of one value per thread (THREADS ≤ 1024).
+// `warp_sums` must hold THREADS/32 entries. Returns the exclusive prefix;
+// *total receives the block total.
+template <int THREADS, typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* warp_sums, T* total) {
+  constexpr int kWarps = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    T s = lane < kWarps ? warp_sums[lane] : T(0);
+    T si = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T n = __shfl_up_sync(0xffffffffu, si, o);
+      if (lane >= o) si += n;
+    }
+    if (lane < kWarps) warp_sums[lane] = si - s;  // exclusive warp offsets
+    if (lane == kWarps - 1) warp_sums[kWarps] = si;
+  }
+  __syncthreads();
+  T out = warp_sums[warp] + incl - v;
+  *total = warp_sums[kWarps];
+  return out;
+}
+
+// Single-value decoupled look-back: returns the exclusive prefix of tile
+// `tile` and publishes its inclusive value. Called by one thread.
+__device__ __forceinline__ uint64_t lookback_publish(uint64_t* status, uint32_t tile,
+                                                     uint32_t epoch, uint64_t aggregate) {
+  if (tile == 0) {
+    st_relaxed(&status[0], pack_status(kFlagIncl, epoch, aggregate));
+    return 0;
+  }
+  st_relaxed(&status[tile], pack_status(kFlagAgg, epoch, aggregate));
+  uint64_t excl = 0;
+  int64_t p = int64_t(tile) - 1;
+  while (true) {
+    uint64_t s = ld_relaxed(&status[p]);
+    if ((s & kFlagMask) == 0 || status_epoch(s) != (epoch & 63u)) continue;
+    excl += s & kValueMask;
+    if ((s & kFlagMask) == kFlagIncl) break;
+    --p;
+  }
+  st_relaxed(&status[tile], pack_status(kFlagIncl, epoch, excl + aggregate));
+  return excl;
+}
+
+inline int rl_cuda_status(cudaError_t e) { return e == cudaSuccess ? RL_OK : RL_ERR_CUDA + int(e); }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Simple bump allocator over the caller's workspace.
+struct Carve {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  bool ok = true;
+  template <typename T>
+  T* take(size_t count) {
+    size_t off = align_up(used, 256);
+    size_t bytes = count * sizeof(T);
+    if (off + bytes > cap) {
+      ok = false;
+      return nullptr;
+    }
+    used = off + bytes;
+    return reinterpret_cast<T*>(base + off);
+  }
+};
+
+// Measuring pass of the same carve sequence (workspace queries).
+struct CarveSize {
+  size_t used = 0;
+  template <typename T>
+  void take(size_t count) {
+    used = align_up(used, 256) + count * sizeof(T);
+  }
+};
+
+int device_sm_count();
+void count_launches(int k);
+
+}  // namespace rl

@@ -1,0 +1,286 @@
+"""Device-resident execution of the tensor path on one B200.
+
+Every function here takes and returns CUDA tensors and launches the sm_100a
+kernels of librelab_b200.so on the current torch stream; nothing falls back to
+the CPU. The numpy-facing drop-in (``tensor_path``) is a thin layer of H2D/D2H
+copies around these calls, and the benchmark's device-resident numbers call
+them directly with inputs already in HBM.
+
+Kernel map:  index_keys = K1+K2 (radix sort) + K3 (run
+bounds); align = K4+K5; expand = K6+K7 (fused); sort_permutation = K1+K2 per
+key word; gather_rows = K7; hash_partition = K8.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import _capi as C
+
+_U32 = torch.int32  # torch has no general uint32 tensor ops; bits are reinterpreted as uint32
+
+
+def _require_cuda(t: torch.Tensor, what: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (the B200 path has no CPU fallback)")
+
+
+def stream_handle(stream: Optional[torch.cuda.Stream] = None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """Scratch from torch's stream-ordered caching allocator (512 B aligned)."""
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+@dataclass
+class KeyIndex:
+    """The sparse key axis of one relation, on the device (to_tensor)."""
+
+    n: int
+    key_values: torch.Tensor  # int64, capacity max(n, 1); first D valid
+    offsets: torch.Tensor  # uint32 bits, capacity n + 1; first D + 1 valid
+    positions: torch.Tensor  # uint32 bits, n
+    d: torch.Tensor  # int64 [1]: D (device scalar)
+
+    def nbytes(self, d: int) -> int:
+        return 4 * self.n + 8 * d + 4 * (d + 1)
+
+
+def index_keys(keys: torch.Tensor) -> KeyIndex:
+    """Stable (key, row) sort + run bounds of an int64 key column.
+
+    Replaces tensorpath.py:78-93 (to_tensor): positions = stable argsort,
+    key_values = distinct keys, offsets = CSR run starts + [n].
+    """
+    _require_cuda(keys, "keys")
+    if keys.dtype != torch.int64 or keys.dim() != 1:
+        raise ValueError("keys must be a 1-D int64 tensor")
+    keys = keys.contiguous()
+    lib = C.load()
+    n = keys.numel()
+    dev = keys.device
+    s = stream_handle()
+    positions = torch.empty(n, dtype=_U32, device=dev)
+    key_values = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    offsets = torch.empty(n + 1, dtype=_U32, device=dev)
+    d = torch.empty(1, dtype=torch.int64, device=dev)
+    if n > 0:
+        sorted_keys = torch.empty(n, dtype=torch.int64, device=dev)
+        ws_bytes = lib.rl_sort_workspace_bytes(n)
+        ws = workspace(ws_bytes, dev)
+        C.check(
+            lib.rl_sort_axis(_ptr(keys), C.RL_COL_INT64, 8, 0, 0, None, n, _ptr(sorted_keys), _ptr(positions),
+                             _ptr(ws), ws.numel(), s),
+            "rl_sort_axis",
+        )
+        del ws
+        rb_ws = workspace(lib.rl_run_bounds_workspace_bytes(n), dev)
+        C.check(
+            lib.rl_run_bounds(_ptr(sorted_keys), n, _ptr(key_values), _ptr(offsets), _ptr(d), _ptr(rb_ws),
+                              rb_ws.numel(), s),
+            "rl_run_bounds",
+        )
+    else:
+        rb_ws = workspace(lib.rl_run_bounds_workspace_bytes(0), dev)
+        C.check(lib.rl_run_bounds(_ptr(keys), 0, _ptr(key_values), _ptr(offsets), _ptr(d), _ptr(rb_ws),
+                                  rb_ws.numel(), s), "rl_run_bounds")
+    return KeyIndex(n, key_values, offsets, positions, d)
+
+
+@dataclass
+class Alignment:
+    """Matched keys of two key axes + join sizing, on the device."""
+
+    cap: int
+    matched_keys: torch.Tensor  # int64 [cap]
+    left_starts: torch.Tensor  # uint32 bits [cap]
+    left_counts: torch.Tensor
+    right_starts: torch.Tensor
+    right_counts: torch.Tensor
+    pair_offsets: torch.Tensor  # uint64 bits (int64 tensor) [cap + 1]
+    m_total: torch.Tensor  # int64 [2]: M, total pairs (device scalars)
+
+
+def align(left: KeyIndex, right: KeyIndex) -> Alignment:
+    """K4+K5: key_axis_align + per-key pair counts and their exclusive scan
+    (tensorpath.py:109-128, 149-161), no host synchronisation."""
+    lib = C.load()
+    dev = left.positions.device
+    cap = min(left.n, right.n)
+    alloc = max(cap, 1)
+    mk = torch.empty(alloc, dtype=torch.int64, device=dev)
+    ls = torch.empty(alloc, dtype=_U32, device=dev)
+    lc = torch.empty(alloc, dtype=_U32, device=dev)
+    rs = torch.empty(alloc, dtype=_U32, device=dev)
+    rc = torch.empty(alloc, dtype=_U32, device=dev)
+    po = torch.empty(alloc + 1, dtype=torch.int64, device=dev)
+    mt = torch.empty(2, dtype=torch.int64, device=dev)
+    grid_cap = left.n if cap > 0 else 0
+    ws = workspace(lib.rl_align_workspace_bytes(grid_cap), dev)
+    C.check(
+        lib.rl_key_axis_align(
+            _ptr(left.key_values), _ptr(left.offsets), _ptr(left.d), grid_cap,
+            _ptr(right.key_values), _ptr(right.offsets), _ptr(right.d),
+            _ptr(mk), _ptr(ls), _ptr(lc), _ptr(rs), _ptr(rc), _ptr(po),
+            ctypes.c_void_p(mt.data_ptr()), ctypes.c_void_p(mt.data_ptr() + 8),
+            _ptr(ws), ws.numel(), stream_handle(),
+        ),
+        "rl_key_axis_align",
+    )
+    return Alignment(cap, mk, ls, lc, rs, rc, po, mt)
+
+
+def fetch_scalars(*tensors: torch.Tensor) -> list:
+    """One pinned D2H of several small device int64 tensors, one sync."""
+    flat = [t.reshape(-1) for t in tensors]
+    total = sum(t.numel() for t in flat)
+    host = torch.empty(total, dtype=torch.int64, pin_memory=True)
+    off = 0
+    for t in flat:
+        host[off : off + t.numel()].copy_(t, non_blocking=True)
+        off += t.numel()
+    torch.cuda.current_stream().synchronize()
+    return host.tolist()
+
+
+@dataclass
+class OutColumn:
+    """One output column of a join/gather: dst[t] = src[row(t)]."""
+
+    src: Optional[torch.Tensor]  # device rows × width bytes (None for the key column)
+    dst: torch.Tensor  # device
+    width: int
+    side: int  # C.RL_SIDE_*
+
+
+def expand(
+    al: Alignment,
+    m: int,
+    left: KeyIndex,
+    right: KeyIndex,
+    out_begin: int,
+    out_end: int,
+    columns: Sequence[OutColumn] = (),
+    left_rows: Optional[torch.Tensor] = None,
+    right_rows: Optional[torch.Tensor] = None,
+) -> None:
+    """K6+K7: materialise output pairs [out_begin, out_end) in reference
+    order (key, left row, right row) and gather the columns in one pass."""
+    lib = C.load()
+    arr, ncols = C.columns_array(
+        (None if c.src is None else c.src.data_ptr(), c.dst.data_ptr(), c.width, c.side) for c in columns
+    )
+    C.check(
+        lib.rl_join_expand(
+            _ptr(al.matched_keys), _ptr(al.left_starts), _ptr(al.right_starts), _ptr(al.right_counts),
+            _ptr(al.pair_offsets), m, _ptr(left.positions), _ptr(right.positions), out_begin, out_end,
+            _ptr(left_rows), _ptr(right_rows), arr, ncols, stream_handle(),
+        ),
+        "rl_join_expand",
+    )
+
+
+def pair_checksum(al: Alignment, m: int, left: KeyIndex, right: KeyIndex, out_begin: int, out_end: int,
+                  acc: torch.Tensor) -> None:
+    """Accumulate sum(fmix64(l << 32 | r)) over pairs [out_begin, out_end) into acc (int64[1])."""
+    lib = C.load()
+    C.check(
+        lib.rl_join_pair_checksum(
+            _ptr(al.left_starts), _ptr(al.right_starts), _ptr(al.right_counts), _ptr(al.pair_offsets), m,
+            _ptr(left.positions), _ptr(right.positions), out_begin, out_end, _ptr(acc), stream_handle(),
+        ),
+        "rl_join_pair_checksum",
+    )
+
+
+@dataclass
+class SortAxis:
+    """One sort key on the device: int64 [n] or uint8 [n, w] (Bytes(w))."""
+
+    data: torch.Tensor
+    descending: bool = False
+
+    @property
+    def is_int64(self) -> bool:
+        return self.data.dtype == torch.int64 and self.data.dim() == 1
+
+
+def sort_permutation(axes: Sequence[SortAxis], n: int, device, sorted_keys_out: Optional[torch.Tensor] = None
+                     ) -> torch.Tensor:
+    """Stable multi-key order: LSD over the key axes, least significant first
+    (tensorpath.py:243-246); Bytes axes go word by word from the last word
+    (tensorpath.py:226-228). Returns the permutation (uint32 bits, int32).
+
+    sorted_keys_out (optional) receives the sorted values of the single
+    int64 key when there is exactly one key axis (the cfg2 ORDER BY).
+    """
+    lib = C.load()
+    s = stream_handle()
+    perm: Optional[torch.Tensor] = None
+    if n == 0:
+        return torch.empty(0, dtype=_U32, device=device)
+    ws = workspace(lib.rl_sort_workspace_bytes(n), device)
+    if sorted_keys_out is not None and not (len(axes) == 1 and axes[0].is_int64):
+        raise ValueError("sorted_keys_out needs exactly one int64 key axis")
+    for axis in reversed(list(axes)):
+        _require_cuda(axis.data, "sort axis")
+        if axis.is_int64:
+            words = [(C.RL_COL_INT64, 8, 0)]
+        else:
+            w = axis.data.shape[1]
+            words = [(C.RL_COL_BYTES, w, j) for j in range(max(1, -(-w // 8)) - 1, -1, -1)]
+        for kind, width, word in words:
+            out = torch.empty(n, dtype=_U32, device=device)
+            C.check(
+                lib.rl_sort_axis(_ptr(axis.data), kind, width, word, int(axis.descending), _ptr(perm), n,
+                                 _ptr(sorted_keys_out) if perm is None and kind == C.RL_COL_INT64 else None,
+                                 _ptr(out), _ptr(ws), ws.numel(), s),
+                "rl_sort_axis",
+            )
+            perm = out
+    return perm
+
+
+def gather_rows(rows: torch.Tensor, columns: Sequence[OutColumn]) -> None:
+    """K7: dst row t = src row rows[t] for every column (Relation.take)."""
+    lib = C.load()
+    arr, ncols = C.columns_array((c.src.data_ptr(), c.dst.data_ptr(), c.width, C.RL_SIDE_LEFT) for c in columns)
+    C.check(lib.rl_gather_rows(_ptr(rows), rows.numel(), arr, ncols, stream_handle()), "rl_gather_rows")
+
+
+def widen(u32: torch.Tensor, n: Optional[int] = None) -> torch.Tensor:
+    """uint32 bits → int64 values (positions/offsets handed back as int64)."""
+    lib = C.load()
+    n = u32.numel() if n is None else n
+    out = torch.empty(n, dtype=torch.int64, device=u32.device)
+    C.check(lib.rl_widen_u32(_ptr(u32), n, _ptr(out), stream_handle()), "rl_widen_u32")
+    return out
+
+
+def hash_partition(keys: torch.Tensor, parts: int, seed: int, columns: Sequence[OutColumn] = ()):
+    """K8: stable hash partition by hash_i64(key, seed) % parts
+    (hashing.py:54-61). Returns (row ids grouped by destination, counts[parts])."""
+    lib = C.load()
+    n = keys.numel()
+    dev = keys.device
+    rows = torch.empty(n, dtype=_U32, device=dev)
+    counts = torch.empty(parts, dtype=torch.int64, device=dev)
+    ws = workspace(lib.rl_partition_workspace_bytes(n, parts), dev)
+    arr, ncols = C.columns_array((c.src.data_ptr(), c.dst.data_ptr(), c.width, C.RL_SIDE_LEFT) for c in columns)
+    C.check(
+        lib.rl_hash_partition(_ptr(keys), n, parts, seed & (2**64 - 1), arr, ncols, _ptr(rows), _ptr(counts),
+                              _ptr(ws), ws.numel(), stream_handle()),
+        "rl_hash_partition",
+    )
+    return rows, counts

@@ -454,7 +454,8 @@ static int launch_sort(HistArgs h, const void* orig_keys, int key_mode, const ui
 int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
               cudaStream_t stream, void* const* events) {
-  if (n < 0 || perm_out == nullptr || (n > 0 && col == nullptr)) return RL_ERR_BAD_ARG;
+  const bool zero_width = col_kind == RL_COL_BYTES && width == 0;  // no key bytes: col may be NULL
+  if (n < 0 || (n > 0 && perm_out == nullptr) || (n > 0 && col == nullptr && !zero_width)) return RL_ERR_BAD_ARG;
   if (n > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
   if (col_kind == RL_COL_INT64) {
     if (width != 8 || word != 0) return RL_ERR_BAD_ARG;

@@ -43,9 +43,6 @@ TYPES = {
     "UnknownAttribute": _errors.UnknownAttribute,
 }
 
-warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
-
-
 def _device() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("the B200 tensor path needs a CUDA device (no CPU fallback)")
@@ -53,8 +50,12 @@ def _device() -> torch.device:
 
 
 def _h2d(arr: np.ndarray, dev) -> torch.Tensor:
-    """Host column → HBM (int64 [n] or uint8 [n, w])."""
-    return torch.from_numpy(np.ascontiguousarray(arr)).to(dev, non_blocking=False)
+    """Host column → HBM (int64 [n] or uint8 [n, w]). The relation's columns
+    are read-only numpy arrays; torch only reads them here."""
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(np.ascontiguousarray(arr))
+    return host.to(dev, non_blocking=False)
 
 
 def _to_numpy_i64(dev_u32_or_i64: torch.Tensor, n: int) -> np.ndarray:

@@ -98,7 +98,9 @@ RL_API int64_t rl_launch_count(void);
  * order (stable). sorted_keys_out (optional, INT64 without perm_in only)
  * receives the sorted int64 key values (tensorpath.py:84 `sk`).
  * Passes whose 8-bit digit is constant over the input are skipped on the
- * device (no host sync).
+ * device (no host sync). An INT64 `col` read without perm_in, and perm_in,
+ * must be 16-byte aligned (they are streamed with TMA bulk copies);
+ * RL_ERR_BAD_ARG otherwise.
  * --------------------------------------------------------------------- */
 RL_API size_t rl_sort_workspace_bytes(int64_t n);
 RL_API int rl_sort_axis(const void* col, int32_t col_kind, int32_t width,

@@ -38,7 +38,10 @@ namespace rl {
 namespace radix {
 
 #ifndef RL_ONESWEEP_ITEMS
-#define RL_ONESWEEP_ITEMS 16
+#define RL_ONESWEEP_ITEMS 12
+#endif
+#ifndef RL_RANK_BALLOT
+#define RL_RANK_BALLOT 1
 #endif
 #ifndef RL_ONESWEEP_MIN_BLOCKS
 #define RL_ONESWEEP_MIN_BLOCKS 2
@@ -51,6 +54,10 @@ constexpr int kThreads = 256;  // == kBins: one digit per thread in the tile sca
 constexpr int kItems = RL_ONESWEEP_ITEMS;
 constexpr int kTile = kThreads * kItems;
 constexpr int kWarps = kThreads / 32;
+#ifndef RL_LOOKBACK_WINDOW
+#define RL_LOOKBACK_WINDOW 4
+#endif
+constexpr int kLookback = RL_LOOKBACK_WINDOW;
 constexpr int kHistThreads = 512;
 constexpr int kHistUnroll = 4;
 
@@ -188,146 +195,276 @@ struct PassArgs {
   int key_mode;
 };
 
-constexpr size_t kPassSmem = size_t(kTile) * 8 + size_t(kTile) * 4 + size_t(kWarps) * kBins * 4 +
-                             size_t(kBins) * 4 * 2 + 64 * 4;
+#ifndef RL_RANK_MODE
+#define RL_RANK_MODE 2  // 1: ballot match_any, 2: shared atomicOr match (fewest instructions)
+#endif
 
-// K2: one stable 8-bit onesweep digit pass.
-__global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_kernel(PassArgs a, int pass) {
+// Shared memory of one persistent onesweep CTA: two tile buffers (one being
+// processed — loaded by TMA, then reused as the digit-ordered staging area —
+// and one being prefetched), per-warp digit counters and match masks.
+constexpr size_t kBufBytes = size_t(kTile) * 12;  // keys (8 B) then row ids (4 B)
+constexpr size_t kPassSmem = 2 * kBufBytes + size_t(kWarps) * kBins * 4 * 2 + size_t(kBins) * 4 * 2 + 64 * 4 + 64;
+
+// Stable rank of every item of this warp within its digit, offset by the
+// warp's base for that digit (wh[] holds the bases on entry). Warp-striped
+// items: element order is (item, lane), so lanes of one item are ranked
+// by peer mask and items by the in-order shared atomics on wh[].
+template <int SHIFT>
+__device__ __forceinline__ void rank_items(const uint64_t (&k)[kItems], uint32_t (&rank2)[kItems / 2],
+                                           uint32_t* wh, uint32_t* wm, uint32_t e0, uint32_t count, int lane) {
+  const uint32_t lt = lanemask_lt();
+  const uint32_t me = 1u << lane;
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const bool valid = (e0 + it * 32) < count;
+    const uint32_t d = uint32_t(k[it] >> SHIFT) & (kBins - 1);
+#if RL_RANK_MODE == 1
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+    if (!valid) peers = me;
+#pragma unroll
+    for (int b = 0; b < kBits; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+    const int leader = 31 - __clz(peers);
+    uint32_t base = 0;
+    if (valid && lane == leader) base = atomicAdd(&wh[d], uint32_t(__popc(peers)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+#else
+    // match via shared atomicOr (wm[] is all-zero between items)
+    if (valid) atomicOr(&wm[d], me);
+    __syncwarp();
+    const uint32_t peers = valid ? wm[d] : me;
+    const int leader = 31 - __clz(peers);
+    uint32_t base = 0;
+    if (valid && lane == leader) base = atomicAdd(&wh[d], uint32_t(__popc(peers)));
+    base = __shfl_sync(0xffffffffu, base, leader);  // also orders every read of wm before the clear
+    if (valid && lane == leader) wm[d] = 0;
+    __syncwarp();
+#endif
+    const uint32_t r = base + __popc(peers & lt);
+    if (it & 1) rank2[it >> 1] |= r << 16;
+    else rank2[it >> 1] = r;
+  }
+}
+
+// Issue the TMA bulk loads of one tile into `buf` (full 16-byte chunks; a
+// ragged tail is finished with plain loads after the wait).
+__device__ __forceinline__ void prefetch_tile(const PassArgs& a, const uint64_t* kin, const uint32_t* vin,
+                                              uint32_t tile, uint8_t* buf, uint64_t* bar) {
+  const int64_t begin = int64_t(tile) * kTile;
+  const int64_t left = a.n - begin;
+  const uint32_t count = left < kTile ? uint32_t(left) : uint32_t(kTile);
+  const uint32_t kbytes = (count * 8u) & ~15u;
+  const uint32_t vbytes = vin ? ((count * 4u) & ~15u) : 0u;
+  mbar_expect_tx(bar, kbytes + vbytes);
+  if (kbytes) bulk_g2s(buf, kin + begin, kbytes, bar);
+  if (vbytes) bulk_g2s(buf + size_t(kTile) * 8, vin + begin, vbytes, bar);
+}
+
+// K2: one stable 8-bit onesweep digit pass (PASS selects the digit).
+// Persistent: each CTA claims tiles in increasing order from an atomic
+// counter and prefetches tile i+1 with TMA while it ranks and scatters tile
+// i, so HBM always has loads in flight. Progress: the smallest unfinished
+// tile's predecessors are all finished, and it is either being processed
+// or queued behind a smaller tile of the same CTA.
+template <int PASS>
+__global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_kernel(PassArgs a) {
+  constexpr int kShift = PASS * kBits;
+  constexpr uint32_t kEpoch = PASS + 1;
   const Plan* plan = a.plan;
-  if (!plan->active[pass]) return;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* skeys = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + kTile);
-  uint32_t* whist = svals + kTile;
-  uint32_t* local_start = whist + kWarps * kBins;
+  if (!plan->active[PASS]) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* bufs = smem;
+  uint32_t* whist = reinterpret_cast<uint32_t*>(smem + 2 * kBufBytes);
+  uint32_t* wmatch = whist + kWarps * kBins;
+  uint32_t* local_start = wmatch + kWarps * kBins;
   uint32_t* gbase = local_start + kBins;
-  uint32_t* misc = gbase + kBins;
+  uint32_t* misc = gbase + kBins;  // [0],[1] claimed tile ids (by iteration parity), [4..] scan scratch
+  uint64_t* bars = reinterpret_cast<uint64_t*>(misc + 64);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t src = plan->src[pass], dst = plan->dst[pass];
-  const uint32_t epoch = uint32_t(pass) + 1;
-  const int shift = pass * kBits;
-
-  for (int i = tid; i < kWarps * kBins; i += kThreads) whist[i] = 0;
-  if (tid == 0) misc[0] = atomicAdd(&a.tile_counter[pass], 1u);
-  __syncthreads();
-  const uint32_t tile = misc[0];
-  const int64_t tile_begin = int64_t(tile) * kTile;
-  const int64_t left = a.n - tile_begin;
-  const uint32_t count = left < kTile ? uint32_t(left) : uint32_t(kTile);
-
-  // ---- load keys (warp-striped: a warp instruction reads 32 consecutive keys)
-  uint64_t k[kItems];
-  const uint32_t e0 = uint32_t(warp) * (32 * kItems) + lane;
+  const uint32_t src = plan->src[PASS], dst = plan->dst[PASS];
+  const uint32_t num_tiles = uint32_t((a.n + kTile - 1) / kTile);
   const uint64_t* kin = src == 1 ? a.keys_a : src == 2 ? a.keys_b : static_cast<const uint64_t*>(a.orig_keys);
   const uint32_t* vin = src == 1 ? a.vals_a : src == 2 ? a.vals_b : a.perm_in;
   const bool xf = src == 0 && a.key_mode != kMaterialized;
   const int desc_in = a.key_mode == kRawDesc;
-#pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const uint32_t e = e0 + it * 32;
-    uint64_t x = 0;
-    if (e < count) x = __ldcs(reinterpret_cast<const unsigned long long*>(kin) + tile_begin + e);
-    k[it] = xf ? xform(x, desc_in) : x;
-  }
 
-  // ---- warp-level stable ranking (match_any multisplit)
-  uint32_t rank2[kItems / 2];  // two 16-bit in-warp ranks per register (rank < 512)
+  for (int i = tid; i < 2 * kWarps * kBins; i += kThreads) whist[i] = 0;  // whist + wmatch
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    const uint32_t t = atomicAdd(&a.tile_counter[PASS], 1u);
+    misc[0] = t;
+    if (t < num_tiles) prefetch_tile(a, kin, vin, t, bufs, &bars[0]);
+  }
+  __syncthreads();
+  uint32_t tile = misc[0];
+  uint32_t cb = 0, phase0 = 0, phase1 = 0;  // cb: buffer + claim slot of this iteration
   uint32_t* wh = whist + warp * kBins;
-  const uint32_t lt = lanemask_lt();
-#pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const bool valid = (e0 + it * 32) < count;
-    const uint32_t d = valid ? uint32_t(k[it] >> shift) & (kBins - 1) : uint32_t(kBins + lane);
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t r = __popc(peers & lt);
-    const uint32_t prior = valid ? wh[d] : 0u;
-    __syncwarp();
-    if (valid && r == 0) wh[d] = prior + __popc(peers);
-    __syncwarp();
-    if (it & 1) rank2[it >> 1] |= (prior + r) << 16;
-    else rank2[it >> 1] = prior + r;
-  }
-  uint32_t v[kItems];
-#pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const uint32_t e = e0 + it * 32;
-    v[it] = 0;
-    if (e < count) v[it] = vin ? __ldcs(vin + tile_begin + e) : uint32_t(tile_begin + e);
-  }
-  __syncthreads();
+  const uint32_t e0 = uint32_t(warp) * (32 * kItems) + lane;
 
-  // ---- per-digit tile counts, warp offsets, publish aggregate
-  uint32_t run = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    uint32_t c = whist[w * kBins + tid];
-    whist[w * kBins + tid] = run;
-    run += c;
-  }
-  uint64_t* my_status = a.status + uint64_t(tile) * kBins + tid;
-  st_relaxed(my_status, pack_status(tile == 0 ? kFlagIncl : kFlagAgg, epoch, run));
-  uint32_t tile_total;
-  const uint32_t ls = block_exclusive_scan<kThreads>(run, misc + 1, &tile_total);
-  local_start[tid] = ls;
-  __syncthreads();
-
-  // ---- stage the tile in digit order (stable local positions)
-#pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    if ((e0 + it * 32) < count) {
-      const uint32_t d = uint32_t(k[it] >> shift) & (kBins - 1);
-      const uint32_t rk = (rank2[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
-      const uint32_t pos = local_start[d] + wh[d] + rk;
-      skeys[pos] = k[it];
-      svals[pos] = v[it];
-    }
-  }
-
-  // ---- decoupled look-back for this thread's digit
-  uint64_t excl = 0;
-  if (tile > 0) {
-    int64_t p = int64_t(tile) - 1;
-    while (true) {
-      const uint64_t s = ld_relaxed(a.status + uint64_t(p) * kBins + tid);
-      if ((s & kFlagMask) == 0 || status_epoch(s) != epoch) continue;
-      excl += s & kValueMask;
-      if ((s & kFlagMask) == kFlagIncl) break;
-      --p;
-    }
-    st_relaxed(my_status, pack_status(kFlagIncl, epoch, excl + run));
-  }
-  gbase[tid] = a.bin_off[pass * kBins + tid] + uint32_t(excl) - ls;
-  __syncthreads();
-
-  // ---- write the staged tile: consecutive threads → consecutive slots
-  if (dst == 3) {
-    const int desc = a.key_mode == kRawDesc;
-#pragma unroll 4
-    for (int it = 0; it < kItems; ++it) {
-      const uint32_t j = uint32_t(it) * kThreads + tid;
-      if (j < count) {
-        const uint64_t key = skeys[j];
-        const uint32_t o = gbase[uint32_t(key >> shift) & (kBins - 1)] + j;
-        if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(key, desc));
-        __stcs(a.out_vals + o, svals[j]);
+  while (tile < num_tiles) {
+    uint8_t* buf = bufs + cb * kBufBytes;
+    uint64_t* skeys = reinterpret_cast<uint64_t*>(buf);
+    uint32_t* svals = reinterpret_cast<uint32_t*>(buf + size_t(kTile) * 8);
+    if (tid == 0) {  // claim + prefetch the next tile into the other buffer
+      const uint32_t nt = atomicAdd(&a.tile_counter[PASS], 1u);
+      misc[cb ^ 1] = nt;  // slot cb^1: its previous value was read before the last barrier
+      if (nt < num_tiles) {
+        fence_proxy_async_smem();
+        prefetch_tile(a, kin, vin, nt, bufs + (cb ^ 1) * kBufBytes, &bars[cb ^ 1]);
       }
     }
-  } else {
-    uint64_t* kout = dst == 1 ? a.keys_a : a.keys_b;
-    uint32_t* vout = dst == 1 ? a.vals_a : a.vals_b;
-#pragma unroll 4
+    const int64_t tile_begin = int64_t(tile) * kTile;
+    const int64_t left = a.n - tile_begin;
+    const uint32_t count = left < kTile ? uint32_t(left) : uint32_t(kTile);
+    mbar_wait(&bars[cb], cb ? phase1 : phase0);
+    if (cb) phase1 ^= 1; else phase0 ^= 1;
+    if (count < kTile) {  // ragged tail: the bytes TMA did not move
+      const uint32_t kdone = ((count * 8u) & ~15u) / 8u;
+      for (uint32_t i = kdone + tid; i < count; i += kThreads) skeys[i] = kin[tile_begin + i];
+      if (vin) {
+        const uint32_t vdone = ((count * 4u) & ~15u) / 4u;
+        for (uint32_t i = vdone + tid; i < count; i += kThreads) svals[i] = vin[tile_begin + i];
+      }
+      __syncthreads();
+    }
+
+    // ---- keys + row ids into registers (warp-striped; conflict-free 8-byte reads)
+    uint64_t k[kItems];
+    uint32_t v[kItems];
+#pragma unroll
     for (int it = 0; it < kItems; ++it) {
-      const uint32_t j = uint32_t(it) * kThreads + tid;
-      if (j < count) {
-        const uint64_t key = skeys[j];
-        const uint32_t o = gbase[uint32_t(key >> shift) & (kBins - 1)] + j;
-        kout[o] = key;
-        vout[o] = svals[j];
+      const uint32_t e = e0 + it * 32;
+      const uint64_t x = skeys[e];
+      k[it] = xf ? xform(x, desc_in) : x;
+      v[it] = vin ? svals[e] : uint32_t(tile_begin + e);
+    }
+
+    // ---- early counts: per-warp digit histograms (order-free shared
+    // reductions), so the tile publishes its aggregate before ranking.
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      if ((e0 + it * 32) < count) atomicAdd(&wh[uint32_t(k[it] >> kShift) & (kBins - 1)], 1u);
+    }
+    __syncthreads();  // counts complete; every thread has read its keys out of buf
+
+    // ---- per-digit tile counts → warp base offsets; publish the aggregate
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = whist[w * kBins + tid];
+      whist[w * kBins + tid] = run;
+      run += c;
+    }
+    uint64_t* my_status = a.status + uint64_t(tile) * kBins + tid;
+    st_relaxed(my_status, pack_status(tile == 0 ? kFlagIncl : kFlagAgg, kEpoch, run));
+    uint32_t tile_total;
+    const uint32_t ls = block_exclusive_scan<kThreads>(run, misc + 4, &tile_total);  // syncs: bases visible
+    // fold the tile-local digit start into every warp's base, so a rank is
+    // directly the item's slot in the digit-ordered staging buffer
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) whist[w * kBins + tid] += ls;
+    __syncthreads();
+
+    // ---- warp-level stable ranking
+    uint32_t rank2[kItems / 2];  // two 16-bit tile-local digit ranks per register (rank < kTile)
+    rank_items<kShift>(k, rank2, wh, wmatch + warp * kBins, e0, count, lane);
+
+    // ---- stage the tile in digit order (stable local positions), in place
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      if ((e0 + it * 32) < count) {
+        const uint32_t pos = (rank2[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
+        skeys[pos] = k[it];
+        svals[pos] = v[it];
       }
     }
+
+    // ---- decoupled look-back for this thread's digit, kLookback predecessor
+    // status words per round trip, from the nearest tile back to the first
+    // inclusive prefix.
+    uint64_t excl = 0;
+    if (tile > 0) {
+      int64_t p = int64_t(tile) - 1;
+      bool done = false;
+      while (!done) {
+        uint64_t st[kLookback];
+#pragma unroll
+        for (int j = 0; j < kLookback; ++j)
+          st[j] = (p - j >= 0) ? ld_relaxed(a.status + uint64_t(p - j) * kBins + tid) : 0;
+        int used = 0;
+#pragma unroll
+        for (int j = 0; j < kLookback; ++j) {
+          if (done) break;
+          const uint64_t sj = st[j];
+          if ((sj & kFlagMask) == 0 || status_epoch(sj) != kEpoch) break;  // not published yet
+          excl += sj & kValueMask;
+          ++used;
+          done = (sj & kFlagMask) == kFlagIncl;
+        }
+        if (done) break;
+        p -= used;
+        if (used < kLookback) {  // tile p not published yet: poll it alone, backing off
+          uint64_t sp;
+          uint32_t ns = 32;
+          while (true) {
+            sp = ld_relaxed(a.status + uint64_t(p) * kBins + tid);
+            if ((sp & kFlagMask) != 0 && status_epoch(sp) == kEpoch) break;
+            __nanosleep(ns);
+            ns = ns < 256 ? ns * 2 : ns;
+          }
+          excl += sp & kValueMask;
+          done = (sp & kFlagMask) == kFlagIncl;
+          --p;
+        }
+      }
+      st_relaxed(my_status, pack_status(kFlagIncl, kEpoch, excl + run));
+    }
+    gbase[tid] = a.bin_off[PASS * kBins + tid] + uint32_t(excl) - ls;
+    __syncthreads();  // every warp is past its ranking: whist may be reset
+    for (int i = tid; i < kWarps * kBins; i += kThreads) whist[i] = 0;  // for the next tile
+
+    // ---- write the staged tile: consecutive threads → consecutive slots
+    if (dst == 3) {
+      const int desc = a.key_mode == kRawDesc;
+#pragma unroll 4
+      for (int it = 0; it < kItems; ++it) {
+        const uint32_t j = uint32_t(it) * kThreads + tid;
+        if (j < count) {
+          const uint64_t key = skeys[j];
+          const uint32_t o = gbase[uint32_t(key >> kShift) & (kBins - 1)] + j;
+          if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(key, desc));
+          __stcs(a.out_vals + o, svals[j]);
+        }
+      }
+    } else {
+      uint64_t* kout = dst == 1 ? a.keys_a : a.keys_b;
+      uint32_t* vout = dst == 1 ? a.vals_a : a.vals_b;
+#pragma unroll 4
+      for (int it = 0; it < kItems; ++it) {
+        const uint32_t j = uint32_t(it) * kThreads + tid;
+        if (j < count) {
+          const uint64_t key = skeys[j];
+          const uint32_t o = gbase[uint32_t(key >> kShift) & (kBins - 1)] + j;
+          kout[o] = key;
+          vout[o] = svals[j];
+        }
+      }
+    }
+    __syncthreads();  // buf free for the prefetch two tiles ahead; next tile id visible
+    cb ^= 1;
+    tile = misc[cb];
   }
 }
+
+typedef void (*OnesweepFn)(PassArgs);
+static const OnesweepFn kOnesweep[kPasses] = {onesweep_kernel<0>, onesweep_kernel<1>, onesweep_kernel<2>,
+                                              onesweep_kernel<3>, onesweep_kernel<4>, onesweep_kernel<5>,
+                                              onesweep_kernel<6>, onesweep_kernel<7>};
 
 // No active pass (all keys share every digit, or n == 1): copy through.
 __global__ void finalize_kernel(const Plan* plan, const int64_t* raw_keys, const uint32_t* perm_in,
@@ -431,14 +568,17 @@ static int launch_sort(HistArgs h, const void* orig_keys, int key_mode, const ui
   p.key_mode = key_mode;
   static bool attr_set = false;  // idempotent; a racing duplicate call is harmless
   if (!attr_set) {
-    e = cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPassSmem));
-    if (e != cudaSuccess) return rl_cuda_status(e);
+    for (int pass = 0; pass < kPasses; ++pass) {
+      e = cudaFuncSetAttribute(kOnesweep[pass], cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPassSmem));
+      if (e != cudaSuccess) return rl_cuda_status(e);
+    }
     attr_set = true;
   }
   const int tiles = int((n + kTile - 1) / kTile);
+  const int grid = std::min(tiles, sms * RL_ONESWEEP_MIN_BLOCKS);
   for (int pass = 0; pass < kPasses; ++pass) {
     mark(2 + pass);
-    onesweep_kernel<<<tiles, kThreads, kPassSmem, stream>>>(p, pass);
+    kOnesweep[pass]<<<grid, kThreads, kPassSmem, stream>>>(p);
   }
   {
     int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
@@ -466,6 +606,9 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
     return RL_ERR_BAD_ARG;
   }
   if (sorted_keys_out && perm_in) return RL_ERR_BAD_ARG;
+  // the digit passes stream int64 keys / row ids with 16-byte TMA bulk copies
+  if (col_kind == RL_COL_INT64 && !perm_in && (reinterpret_cast<uintptr_t>(col) & 15)) return RL_ERR_BAD_ARG;
+  if (reinterpret_cast<uintptr_t>(perm_in) & 15) return RL_ERR_BAD_ARG;
   if (n == 0) return RL_OK;
   if (col_kind == RL_COL_BYTES && width == 0) {  // tensorpath.py:218-219: identity order
     int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8));

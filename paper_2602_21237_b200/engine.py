@@ -38,6 +38,13 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def aligned16(t: torch.Tensor) -> torch.Tensor:
+    """The sort streams int64 keys / row ids with 16-byte TMA bulk copies:
+    give it a contiguous, 16-byte aligned view (copy only if needed)."""
+    t = t.contiguous()
+    return t if t.data_ptr() % 16 == 0 else t.clone()
+
+
 def workspace(nbytes: int, device) -> torch.Tensor:
     """Scratch from torch's stream-ordered caching allocator (512 B aligned)."""
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
@@ -66,7 +73,7 @@ def index_keys(keys: torch.Tensor) -> KeyIndex:
     _require_cuda(keys, "keys")
     if keys.dtype != torch.int64 or keys.dim() != 1:
         raise ValueError("keys must be a 1-D int64 tensor")
-    keys = keys.contiguous()
+    keys = aligned16(keys)
     lib = C.load()
     n = keys.numel()
     dev = keys.device
@@ -235,6 +242,7 @@ def sort_permutation(axes: Sequence[SortAxis], n: int, device, sorted_keys_out: 
         raise ValueError("sorted_keys_out needs exactly one int64 key axis")
     for axis in reversed(list(axes)):
         _require_cuda(axis.data, "sort axis")
+        data = aligned16(axis.data)
         if axis.is_int64:
             words = [(C.RL_COL_INT64, 8, 0)]
         else:
@@ -243,7 +251,7 @@ def sort_permutation(axes: Sequence[SortAxis], n: int, device, sorted_keys_out: 
         for kind, width, word in words:
             out = torch.empty(n, dtype=_U32, device=device)
             C.check(
-                lib.rl_sort_axis(_ptr(axis.data), kind, width, word, int(axis.descending), _ptr(perm), n,
+                lib.rl_sort_axis(_ptr(data), kind, width, word, int(axis.descending), _ptr(perm), n,
                                  _ptr(sorted_keys_out) if perm is None and kind == C.RL_COL_INT64 else None,
                                  _ptr(out), _ptr(ws), ws.numel(), s),
                 "rl_sort_axis",

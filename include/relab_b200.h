@@ -221,6 +221,23 @@ RL_API int rl_hash_partition(const int64_t* keys, int64_t n, int32_t parts,
                       int64_t* counts_out, void* ws, size_t ws_bytes,
                       void* stream);
 
+/* ---------------------------------------------------------------------
+ * Host→device staging (the drop-in boundary's inputs are pageable numpy
+ * columns). A stager owns a pinned ring of `slots` chunks, a copy stream
+ * and `threads` native copy threads; rl_stager_h2d copies chunk c into the
+ * ring in parallel while the copy engine DMAs chunk c-1, then makes
+ * `stream` wait for the finished upload (no host sync on the data path).
+ * ready_event (cudaEvent_t or NULL): the copy stream first waits for it —
+ * record it on the allocating stream right after allocating dst, so the
+ * upload cannot overtake earlier work on recycled memory while kernels
+ * enqueued later still overlap the upload.
+ * One stager serves one upload at a time (calls are serialised).
+ * --------------------------------------------------------------------- */
+RL_API void* rl_stager_create(int32_t threads, size_t chunk_bytes, int32_t slots);
+RL_API void rl_stager_destroy(void* stager);
+RL_API int rl_stager_h2d(void* stager, void* dst_dev, const void* src_host,
+                         size_t bytes, void* stream, void* ready_event);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,168 @@
+// stager.cu — pipelined host→device staging for the drop-in boundary.
+//
+// The reference's relations are ordinary (pageable) numpy columns. A plain
+// cudaMemcpy from pageable memory runs at ~11 GB/s on the B200 box, while a
+// copy from pinned memory reaches ~55 GB/s and 8 host threads copy memory at
+// ~50 GB/s. The stager overlaps the two: a pool of native threads copies
+// chunk c of the source into a pinned ring slot while the copy engine DMAs
+// chunk c-1 to HBM on the stager's own copy stream. The caller's compute
+// stream is made to wait (cudaStreamWaitEvent) for the finished upload, so
+// kernels that consume the column are ordered after it while unrelated
+// kernels already queued keep running — uploading the payload columns
+// overlaps the key sort.
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rl {
+namespace stage {
+
+class Pool {
+ public:
+  explicit Pool(int n) {
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  int size() const { return int(workers_.size()); }
+  // run fn(i) for i in [0, size()) on the workers; returns when all finished
+  void parallel(const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> lk(m_);
+    job_ = &fn;
+    pending_ = int(workers_.size());
+    ++gen_;
+    cv_.notify_all();
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int idx) {
+    uint64_t seen = 0;
+    while (true) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        job = job_;
+      }
+      if (job) (*job)(idx);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
+struct Stager {
+  Pool pool;
+  size_t chunk;
+  int slots;
+  char* ring = nullptr;
+  std::vector<cudaEvent_t> slot_free;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t done = nullptr;
+  int next_slot = 0;
+  std::mutex call_mu;  // one upload at a time per stager
+
+  Stager(int threads, size_t chunk_bytes, int n_slots) : pool(threads), chunk(chunk_bytes), slots(n_slots) {}
+};
+
+}  // namespace stage
+}  // namespace rl
+
+using rl::stage::Stager;
+
+extern "C" {
+
+RL_API void* rl_stager_create(int32_t threads, size_t chunk_bytes, int32_t slots) {
+  if (threads < 1 || slots < 2 || chunk_bytes < 4096) return nullptr;
+  Stager* s = new Stager(threads, chunk_bytes, slots);
+  bool ok = cudaHostAlloc(reinterpret_cast<void**>(&s->ring), chunk_bytes * size_t(slots), cudaHostAllocDefault) ==
+                cudaSuccess &&
+            cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming) == cudaSuccess;
+  s->slot_free.resize(slots);
+  for (int i = 0; ok && i < slots; ++i)
+    ok = cudaEventCreateWithFlags(&s->slot_free[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    delete s;
+    return nullptr;
+  }
+  for (int i = 0; i < slots; ++i) cudaEventRecord(s->slot_free[i], s->copy_stream);
+  return s;
+}
+
+RL_API void rl_stager_destroy(void* handle) {
+  Stager* s = static_cast<Stager*>(handle);
+  if (!s) return;
+  if (s->copy_stream) cudaStreamSynchronize(s->copy_stream);
+  for (auto e : s->slot_free)
+    if (e) cudaEventDestroy(e);
+  if (s->done) cudaEventDestroy(s->done);
+  if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+  if (s->ring) cudaFreeHost(s->ring);
+  delete s;
+}
+
+RL_API int rl_stager_h2d(void* handle, void* dst_dev, const void* src_host, size_t bytes, void* stream,
+                         void* ready_event) {
+  Stager* s = static_cast<Stager*>(handle);
+  if (!s || (bytes && (!dst_dev || !src_host))) return RL_ERR_BAD_ARG;
+  if (bytes == 0) return RL_OK;
+  std::lock_guard<std::mutex> g(s->call_mu);
+  if (ready_event) {  // dst may have been freed by work queued before the event: wait for it
+    cudaError_t e = cudaStreamWaitEvent(s->copy_stream, static_cast<cudaEvent_t>(ready_event), 0);
+    if (e != cudaSuccess) return rl::rl_cuda_status(e);
+  }
+  const int nt = s->pool.size();
+  for (size_t off = 0; off < bytes; off += s->chunk) {
+    const size_t len = std::min(s->chunk, bytes - off);
+    const int slot = s->next_slot;
+    s->next_slot = (s->next_slot + 1) % s->slots;
+    cudaError_t e = cudaEventSynchronize(s->slot_free[slot]);  // its previous DMA has drained
+    if (e != cudaSuccess) return rl::rl_cuda_status(e);
+    char* dst = s->ring + size_t(slot) * s->chunk;
+    const char* src = static_cast<const char*>(src_host) + off;
+    if (len >= (size_t(1) << 20) && nt > 1) {
+      const size_t piece = (len + nt - 1) / nt;
+      s->pool.parallel([&](int i) {
+        const size_t a = std::min(len, size_t(i) * piece), b = std::min(len, a + piece);
+        if (b > a) std::memcpy(dst + a, src + a, b - a);
+      });
+    } else {
+      std::memcpy(dst, src, len);
+    }
+    e = cudaMemcpyAsync(static_cast<char*>(dst_dev) + off, dst, len, cudaMemcpyHostToDevice, s->copy_stream);
+    if (e != cudaSuccess) return rl::rl_cuda_status(e);
+    cudaEventRecord(s->slot_free[slot], s->copy_stream);
+  }
+  cudaEventRecord(s->done, s->copy_stream);
+  return rl::rl_cuda_status(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), s->done, 0));
+}
+
+}  // extern "C"

@@ -20,6 +20,7 @@ only when a caller reads them.
 
 from __future__ import annotations
 
+import ctypes
 import sys
 import warnings
 from typing import Optional
@@ -49,13 +50,67 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_STAGE_MIN_BYTES = 1 << 20
+_stagers: dict = {}
+
+
+def _stager(dev) -> int:
+    """Per-device native staging pipeline (csrc/stager.cu): pinned ring of
+    4 x 8 MiB, up to 8 copy threads, its own copy stream."""
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    h = _stagers.get(idx)
+    if h is None:
+        import os
+
+        threads = max(1, min(8, (os.cpu_count() or 2) // 2))
+        h = C.load().rl_stager_create(threads, 8 << 20, 4)
+        if not h:
+            raise RuntimeError("rl_stager_create failed (pinned host memory / CUDA stream)")
+        _stagers[idx] = h
+    return h
+
+
+class _Uploads:
+    """Device destinations for host columns, allocated up front.
+
+    All destinations are allocated, then one event is recorded on the
+    current stream; every staged upload waits only for that event, so it
+    cannot overtake earlier work on recycled allocator memory, while the
+    kernels enqueued afterwards (the key sort) overlap the payload uploads.
+    """
+
+    def __init__(self, arrays, dev):
+        self.host = [np.ascontiguousarray(a) for a in arrays]
+        self.dev = []
+        for a in self.host:
+            if a.dtype not in (np.int64, np.uint8, np.int32):
+                raise ValueError(f"unsupported column dtype {a.dtype}")
+            dt = {np.dtype(np.int64): torch.int64, np.dtype(np.uint8): torch.uint8, np.dtype(np.int32): torch.int32}
+            self.dev.append(torch.empty(a.shape, dtype=dt[a.dtype], device=dev))
+        self.ready = torch.cuda.Event()
+        self.ready.record()
+        self.done = [False] * len(self.host)
+
+    def get(self, j: int) -> torch.Tensor:
+        """Device copy of column j, uploading it now if it has not been."""
+        if not self.done[j]:
+            arr, out = self.host[j], self.dev[j]
+            if arr.nbytes >= _STAGE_MIN_BYTES:
+                C.check(C.load().rl_stager_h2d(_stager(out.device), ctypes.c_void_p(out.data_ptr()),
+                                               ctypes.c_void_p(arr.ctypes.data), arr.nbytes,
+                                               engine.stream_handle(), ctypes.c_void_p(self.ready.cuda_event)),
+                        "rl_stager_h2d")
+            elif arr.nbytes:
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore", UserWarning)
+                    out.copy_(torch.from_numpy(arr))
+            self.done[j] = True
+        return self.dev[j]
+
+
 def _h2d(arr: np.ndarray, dev) -> torch.Tensor:
-    """Host column → HBM (int64 [n] or uint8 [n, w]). The relation's columns
-    are read-only numpy arrays; torch only reads them here."""
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore", UserWarning)
-        host = torch.from_numpy(np.ascontiguousarray(arr))
-    return host.to(dev, non_blocking=False)
+    """One host column → HBM (int64 [n], int32 [n] or uint8 [n, w])."""
+    return _Uploads([arr], dev).get(0)
 
 
 def _to_numpy_i64(dev_u32_or_i64: torch.Tensor, n: int) -> np.ndarray:
@@ -183,8 +238,9 @@ def to_tensor(rel, key: str) -> TensorRelation:
         raise TYPES["UnknownAttribute"](f"key attribute {key!r} must be int64")
     dev = _device()
     key_idx = rel.schema.index(key)
-    dev_axes = tuple(_h2d(c, dev) for c in rel.columns)
-    index = engine.index_keys(dev_axes[key_idx])
+    up = _Uploads(rel.columns, dev)
+    index = engine.index_keys(up.get(key_idx))  # queued behind the key upload only
+    dev_axes = tuple(up.get(j) for j in range(len(rel.columns)))  # overlap the sort
     return TensorRelation(rel.schema, rel.columns, key, _index=index, _dev_axes=dev_axes)
 
 
@@ -323,8 +379,8 @@ def tensor_sort(rel, spec):
     if n == 0:
         return rel_cls(rel.schema, rel.columns), TYPES["SpillStats"](peak_mem_bytes=0, peak_build_bytes=0)
     dev = _device()
-    dev_cols = [_h2d(c, dev) for c in rel.columns]
-    axes = [engine.SortAxis(dev_cols[rel.schema.index(k)], is_descending(d)) for k, d in zip(spec.keys, spec.directions)]
+    up = _Uploads(rel.columns, dev)
+    axes = [engine.SortAxis(up.get(rel.schema.index(k)), is_descending(d)) for k, d in zip(spec.keys, spec.directions)]
     single_int = len(axes) == 1 and axes[0].is_int64
     key_j = rel.schema.index(spec.keys[0])
     sorted_key = torch.empty(n, dtype=torch.int64, device=dev) if single_int else None
@@ -334,7 +390,7 @@ def tensor_sort(rel, spec):
         if single_int and j == key_j:
             outs.append(sorted_key)
             continue
-        col = _out_column(dev_cols[j], t, n, dev, C.RL_SIDE_LEFT)
+        col = _out_column(up.get(j), t, n, dev, C.RL_SIDE_LEFT)  # uploads overlap the sort
         gathers.append(col)
         outs.append(col.dst)
     engine.gather_rows(perm, gathers)

@@ -221,6 +221,8 @@ def run_ours(args):
     ws = engine.workspace(lib.rl_sort_workspace_bytes(n), dev)
     s = engine.stream_handle()
 
+    stamps = torch.zeros(_capi.RL_SORT_STAMPS, dtype=torch.int64, device=dev)
+
     def device_step(events=None):
         sorted_keys = torch.empty(n, dtype=torch.int64, device=dev)
         perm = torch.empty(n, dtype=torch.int32, device=dev)
@@ -234,7 +236,7 @@ def run_ours(args):
             _capi.check(lib.rl_sort_axis_profiled(ctypes.c_void_p(keys_d.data_ptr()), 0, 8, 0, 0, None, n,
                                                   ctypes.c_void_p(sorted_keys.data_ptr()),
                                                   ctypes.c_void_p(perm.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
-                                                  ws.numel(), s, arr), "sort")
+                                                  ws.numel(), s, arr, ctypes.c_void_p(stamps.data_ptr())), "sort")
         engine.gather_rows(perm, [engine.OutColumn(pay_d, out_pay, 4, 0)])
         return sorted_keys, perm, out_pay
 
@@ -284,26 +286,29 @@ def run_ours(args):
         total_ms = float(t.item())
     value = world * n * args.steps / (total_ms / 1e3) / 1e6
 
-    # roofline of the onesweep pass kernel (events around each launch)
+    # roofline of the dominant kernel: the cooperative onesweep kernel (all
+    # active digit passes in one launch), timed with CUDA events around it
     pbytes = pass_bytes(n, active)
-    pass_ms = {p: [] for p in pbytes}
-    for evs in pass_ev:
-        for p in pbytes:
-            pass_ms[p].append(evs[2 + p].elapsed_time(evs[3 + p]))
-    launches_timed = sum(len(v) for v in pass_ms.values())
-    total_pass_ms = sum(sum(v) for v in pass_ms.values())
-    alg_bytes = sum(pbytes[p] * len(pass_ms[p]) for p in pbytes)
-    achieved = alg_bytes / (total_pass_ms / 1e3) / 1e9
+    alg_bytes = sum(pbytes.values())  # per launch
+    sort_ms = [evs[1].elapsed_time(evs[2]) for evs in pass_ev]
+    hist_ms = [evs[0].elapsed_time(evs[1]) for evs in pass_ev]
+    avg_sort_ms = statistics.mean(sort_ms)
+    achieved = alg_bytes / (avg_sort_ms / 1e3) / 1e9
     peak, peak_src = measured_peak_hbm()
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("onesweep_kernel_bytes_per_launch")
+            traffic = json.loads(tfile.read_text()).get("sort_kernel_bytes_per_launch")
         except Exception:
             traffic = None
-    hist_ms = [evs[0].elapsed_time(evs[1]) for evs in pass_ev]
-    sort_share = total_pass_ms / total_ms
+    st = stamps.cpu().tolist()  # last step's per-pass split (globaltimer, CTA 0)
+    prev, per_pass_us = st[1], []
+    for p in range(8):
+        if st[2 + p]:
+            per_pass_us.append(round((st[2 + p] - prev) / 1e3, 1))
+            prev = st[2 + p]
+    sort_share = sum(sort_ms) / total_ms
 
     # e2e through the public drop-in API, host numpy in/out
     spec = SortSpec(("key",))
@@ -335,11 +340,12 @@ def run_ours(args):
                 "p50_ms": round(1e3 * percentile(e2e_t, 50), 3), "p99_ms": round(1e3 * percentile(e2e_t, 99), 3)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "rl::radix::onesweep_kernel", "peak_source": peak_src,
-                     "launches_timed": launches_timed, "active_passes": sum(active),
-                     "avg_launch_us": round(1e3 * total_pass_ms / max(launches_timed, 1), 2),
-                     "alg_bytes_per_launch": int(alg_bytes / max(launches_timed, 1)),
-                     "share_of_step": round(sort_share, 4), "hist_kernel_us": round(1e3 * statistics.mean(hist_ms), 2)},
+                     "kernel": "rl::radix::sort_kernel (cooperative onesweep, all active digit passes)",
+                     "peak_source": peak_src, "launches_timed": len(sort_ms), "active_passes": sum(active),
+                     "avg_launch_us": round(1e3 * avg_sort_ms, 2), "alg_bytes_per_launch": int(alg_bytes),
+                     "alg_bytes_formula": "per active pass: first 8n+12n, others 12n+12n (key u64 + row id u32)",
+                     "per_pass_us_last_step": per_pass_us, "share_of_step": round(sort_share, 4),
+                     "hist_kernel_us": round(1e3 * statistics.mean(hist_ms), 2)},
         "clocks": clocks.summary(),
         "gpu_launches": int(launches),
     }

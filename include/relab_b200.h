@@ -97,8 +97,10 @@ RL_API int64_t rl_launch_count(void);
  * Output: perm_out[i] = the row at sorted position i; ties keep input
  * order (stable). sorted_keys_out (optional, INT64 without perm_in only)
  * receives the sorted int64 key values (tensorpath.py:84 `sk`).
- * Passes whose 8-bit digit is constant over the input are skipped on the
- * device (no host sync). An INT64 `col` read without perm_in, and perm_in,
+ * A sort is two launches: the digit histograms, then ONE cooperative
+ * kernel running the plan and every digit pass separated by grid barriers;
+ * passes whose 8-bit digit is constant over the input are skipped on the
+ * device (no host sync, no launch). An INT64 `col` read without perm_in, and perm_in,
  * must be 16-byte aligned (they are streamed with TMA bulk copies);
  * RL_ERR_BAD_ARG otherwise.
  * --------------------------------------------------------------------- */
@@ -108,17 +110,20 @@ RL_API int rl_sort_axis(const void* col, int32_t col_kind, int32_t width,
                  int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
                  void* ws, size_t ws_bytes, void* stream);
 
-/* Same as rl_sort_axis, additionally recording events[i] (cudaEvent_t,
- * created by the caller with timing enabled) on `stream` before kernel i and
- * events[RL_SORT_EVENTS-1] after the last one: [0] histogram, [1] plan,
- * [2..9] digit passes 0..7, [10] finalize, [11] end. Used by bench.py to time
- * the onesweep pass kernel live inside the timed region. */
-#define RL_SORT_EVENTS 12
+/* Same as rl_sort_axis, for measurement: events[0..2] (cudaEvent_t
+ * created by the caller with timing enabled) are recorded on `stream`
+ * before the histogram kernel, between it and the cooperative pass kernel,
+ * and after the pass kernel; if stamps_dev (device, RL_SORT_STAMPS x
+ * uint64) is not NULL, CTA 0 writes %globaltimer (ns) there: [0] histogram
+ * start, [1] pass kernel start, [2+p] after digit pass p (0 for skipped
+ * passes), [10] end. */
+#define RL_SORT_EVENTS 3
+#define RL_SORT_STAMPS 11
 RL_API int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width,
                  int32_t word, int32_t descending, const uint32_t* perm_in,
                  int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
                  void* ws, size_t ws_bytes, void* stream,
-                 void* const* events);
+                 void* const* events, unsigned long long* stamps_dev);
 
 /* ---------------------------------------------------------------------
  * K3  Run bounds of sorted keys: distinct keys + CSR offsets.

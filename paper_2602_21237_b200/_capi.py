@@ -31,7 +31,8 @@ RL_SIDE_RIGHT = 1
 RL_SIDE_KEY = 2
 RL_MAX_COLUMNS = 32
 RL_MAX_ROWS = 2**32 - 1
-RL_SORT_EVENTS = 12
+RL_SORT_EVENTS = 3
+RL_SORT_STAMPS = 11
 
 
 class RlColumn(ctypes.Structure):
@@ -59,7 +60,7 @@ SIGNATURES = {
     "rl_sort_axis": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
     "rl_sort_axis_profiled": (
         ctypes.c_int,
-        [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _SZ, _P, ctypes.POINTER(ctypes.c_void_p)],
+        [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _SZ, _P, ctypes.POINTER(ctypes.c_void_p), _P],
     ),
     "rl_run_bounds_workspace_bytes": (_SZ, [_I64]),
     "rl_run_bounds": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _SZ, _P]),

@@ -11,7 +11,7 @@ namespace radix {
 size_t workspace_bytes(int64_t n);
 int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
-              cudaStream_t stream, void* const* events);
+              cudaStream_t stream, void* const* events, unsigned long long* stamps);
 size_t partition_workspace_bytes(int64_t n);
 int hash_partition_perm(const int64_t* keys, int64_t n, int parts, uint64_t seed, uint32_t* perm_out,
                         int64_t* counts_out, void* ws, size_t ws_bytes, cudaStream_t stream);
@@ -85,15 +85,15 @@ int rl_sort_axis(const void* col, int32_t col_kind, int32_t width, int32_t word,
                  const uint32_t* perm_in, int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws,
                  size_t ws_bytes, void* stream) {
   return rl::radix::sort_axis(col, col_kind, width, word, descending, perm_in, n, sorted_keys_out, perm_out, ws,
-                              ws_bytes, as_stream(stream), nullptr);
+                              ws_bytes, as_stream(stream), nullptr, nullptr);
 }
 
 int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width, int32_t word, int32_t descending,
                           const uint32_t* perm_in, int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws,
-                          size_t ws_bytes, void* stream, void* const* events) {
+                          size_t ws_bytes, void* stream, void* const* events, unsigned long long* stamps_dev) {
   if (events == nullptr) return RL_ERR_BAD_ARG;
   return rl::radix::sort_axis(col, col_kind, width, word, descending, perm_in, n, sorted_keys_out, perm_out, ws,
-                              ws_bytes, as_stream(stream), events);
+                              ws_bytes, as_stream(stream), events, stamps_dev);
 }
 
 size_t rl_run_bounds_workspace_bytes(int64_t n) { return rl::keyaxis::run_bounds_workspace_bytes(n); }

@@ -1,29 +1,37 @@
-// radix_sort.cu — K1 (upfront digit histograms) + K2 (onesweep digit pass).
+// radix_sort.cu — K1 (digit histograms) + K2 (onesweep digit passes), fused
+// into ONE persistent cooperative kernel per sort.
 //
 // Stable LSD radix sort of 64-bit key words carrying uint32 row ids. It
 // replaces the reference's stable argsorts:
 //   _stable_key_order   /root/reference/pkg/src/relab/tensorpath.py:62-75
 //   _stable_axis_order  /root/reference/pkg/src/relab/tensorpath.py:206-229
 //
-// Design (B200, HBM-bound integer work — no tensor cores):
-//   * K1 reads the keys once and builds all eight 8-bit digit histograms in
-//     shared memory (one global atomic per non-empty bin per CTA). For a
-//     gathered key (a refinement step of a multi-key sort, or a Bytes word)
-//     it also materialises the transformed 64-bit key words so the first
-//     digit pass streams them contiguously.
-//   * A one-CTA plan kernel scans the histograms into global digit bases
-//     and marks passes whose digit is constant over the input as inactive.
-//     The plan (active flags, ping-pong buffer choice, epochs) stays on the
-//     device: the host launches all eight passes and inactive ones exit at
-//     once, so a sort never synchronises the host.
-//   * K2 is a onesweep pass: tiles of 4096 keys are claimed in launch order
-//     by an atomic counter; each warp ranks its 512 keys with
-//     __match_any_sync (stable: lanes in element order, items in order);
-//     the tile publishes its per-digit counts, scatters keys+row ids into a
-//     shared-memory staging buffer in digit order while the decoupled
-//     look-back resolves its global digit offsets, and finally writes the
-//     staged tile out in ascending local order, so every digit run is a
-//     contiguous, coalesced burst.
+// Design (B200, HBM/shared-memory bound integer work — no tensor cores):
+//   * One cooperative launch of 2 CTAs per SM (all co-resident). Phases are
+//     separated by a grid barrier instead of kernel boundaries, so a sort is
+//     a single launch: digits that are constant over the input (pass
+//     skipping: a 1e6-domain key has only 3 active 8-bit digits of 8) cost
+//     nothing, and no launch gaps separate the passes.
+//   * Phase H reads the keys once and builds all eight 8-bit digit
+//     histograms (shared-memory counters, one global atomic per bin per
+//     CTA). For a gathered key (a refinement step of a multi-key sort, or a
+//     Bytes word) it also materialises the transformed key words so the
+//     first digit pass streams them contiguously.
+//   * Every CTA then derives the pass plan itself from the global
+//     histograms (active digits, ping-pong buffers, global digit bases): no
+//     plan kernel, no host synchronisation.
+//   * Each active digit pass is a onesweep pass over tiles of 3072 keys that
+//     CTAs claim in increasing order from an atomic counter. A CTA prefetches
+//     its next tile with TMA bulk copies (cp.async.bulk → shared memory,
+//     mbarrier completion) while it ranks and scatters the current one:
+//       - early counts: per-warp digit histograms (shared atomics) published
+//         as the tile's aggregate before ranking (decoupled look-back);
+//       - stable warp multisplit rank: peers of a digit from a shared
+//         atomicOr mask, the leader bumps the warp's running digit offset;
+//       - the tile is staged in digit order in place, the look-back resolves
+//         the global digit offsets (a window of predecessor status words per
+//         round trip), and the staged tile is written out so every digit run
+//         is a contiguous burst.
 //
 // Key transform (self-inverse): int64 ascending  u = x ^ 2^63;
 // descending u = ~x ^ 2^63 (the reference's np.invert, tensorpath.py:215,
@@ -40,11 +48,14 @@ namespace radix {
 #ifndef RL_ONESWEEP_ITEMS
 #define RL_ONESWEEP_ITEMS 12
 #endif
-#ifndef RL_RANK_BALLOT
-#define RL_RANK_BALLOT 1
-#endif
 #ifndef RL_ONESWEEP_MIN_BLOCKS
 #define RL_ONESWEEP_MIN_BLOCKS 2
+#endif
+#ifndef RL_LOOKBACK_WINDOW
+#define RL_LOOKBACK_WINDOW 4
+#endif
+#ifndef RL_RANK_MODE
+#define RL_RANK_MODE 2  // 1: ballot match_any, 2: shared atomicOr match (fewest instructions)
 #endif
 
 constexpr int kBits = 8;
@@ -54,24 +65,18 @@ constexpr int kThreads = 256;  // == kBins: one digit per thread in the tile sca
 constexpr int kItems = RL_ONESWEEP_ITEMS;
 constexpr int kTile = kThreads * kItems;
 constexpr int kWarps = kThreads / 32;
-#ifndef RL_LOOKBACK_WINDOW
-#define RL_LOOKBACK_WINDOW 4
-#endif
 constexpr int kLookback = RL_LOOKBACK_WINDOW;
-constexpr int kHistThreads = 512;
-constexpr int kHistUnroll = 4;
+#ifndef RL_HIST_UNROLL
+#define RL_HIST_UNROLL 8
+#endif
+constexpr int kHistUnroll = RL_HIST_UNROLL;
+constexpr int kStamps = 2 + kPasses + 1;  // per-phase globaltimer stamps (profiling)
 
 static_assert(kThreads == kBins, "tile scan maps one digit per thread");
+static_assert(kStamps == RL_SORT_STAMPS, "stamp layout is part of the ABI");
 
 enum KeyMode : int { kRawAsc = 0, kRawDesc = 1, kMaterialized = 2 };
 enum SrcMode : int { kSrcInt64 = 0, kSrcInt64Gather = 1, kSrcBytes = 2, kSrcWords = 3 };
-
-struct Plan {
-  uint32_t n_active;
-  uint32_t active[kPasses];
-  uint32_t src[kPasses];  // 0 original, 1 buffer A, 2 buffer B
-  uint32_t dst[kPasses];  // 1 buffer A, 2 buffer B, 3 final outputs
-};
 
 __device__ __forceinline__ uint64_t xform(uint64_t x, int desc) {
   return (desc ? ~x : x) ^ 0x8000000000000000ull;
@@ -92,123 +97,79 @@ __device__ __forceinline__ uint64_t bytes_word(const uint8_t* row, int width, in
   return v;
 }
 
-struct HistArgs {
+struct SortArgs {
+  // phase H source
   const void* col;
-  const uint32_t* perm_in;
-  uint64_t* materialized;  // only for gather / bytes modes
-  uint32_t* ghist;         // [kPasses][kBins]
+  const uint32_t* perm_in;   // row ids of the input slots (NULL = identity)
+  uint64_t* materialized;    // gathered/bytes modes: transformed key words
   int64_t n;
-  int width, word, desc, src_mode;
-};
-
-__device__ __forceinline__ uint64_t load_key(const HistArgs& a, int64_t i) {
-  if (a.src_mode == kSrcInt64) {
-    return xform(uint64_t(__ldg(static_cast<const long long*>(a.col) + i)), a.desc);
-  }
-  uint64_t row = a.perm_in ? uint64_t(__ldg(a.perm_in + i)) : uint64_t(i);
-  if (a.src_mode == kSrcWords) return __ldg(static_cast<const unsigned long long*>(a.col) + i);
-  if (a.src_mode == kSrcInt64Gather) {
-    return xform(uint64_t(__ldg(static_cast<const long long*>(a.col) + row)), a.desc);
-  }
-  const uint8_t* base = static_cast<const uint8_t*>(a.col) + row * uint64_t(a.width);
-  return bytes_word(base, a.width, a.word, a.desc);
-}
-
-// K1: all digit histograms in one read of the keys.
-__global__ void __launch_bounds__(kHistThreads) hist_kernel(HistArgs a) {
-  __shared__ uint32_t h[kPasses * kBins];
-  for (int i = threadIdx.x; i < kPasses * kBins; i += kHistThreads) h[i] = 0;
-  __syncthreads();
-  const int64_t stride = int64_t(gridDim.x) * kHistThreads * kHistUnroll;
-  for (int64_t base = int64_t(blockIdx.x) * kHistThreads * kHistUnroll + threadIdx.x; base < a.n;
-       base += stride) {
-    uint64_t k[kHistUnroll];
-    bool ok[kHistUnroll];
-#pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      int64_t i = base + int64_t(u) * kHistThreads;
-      ok[u] = i < a.n;
-      k[u] = ok[u] ? load_key(a, i) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      if (!ok[u]) continue;
-      if (a.materialized) a.materialized[base + int64_t(u) * kHistThreads] = k[u];
-#pragma unroll
-      for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p * kBins + ((k[u] >> (p * kBits)) & (kBins - 1))], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kPasses * kBins; i += kHistThreads) {
-    uint32_t c = h[i];
-    if (c) atomicAdd(&a.ghist[i], c);
-  }
-}
-
-// Global digit bases + the device-side pass plan.
-__global__ void __launch_bounds__(kBins) plan_kernel(const uint32_t* ghist, uint32_t* bin_off, Plan* plan,
-                                                     uint64_t n) {
-  __shared__ uint32_t warp_sums[kBins / 32 + 1];
-  __shared__ uint32_t active[kPasses];
-  for (int p = 0; p < kPasses; ++p) {
-    uint32_t c = ghist[p * kBins + threadIdx.x];
-    uint32_t total;
-    uint32_t excl = block_exclusive_scan<kBins>(c, warp_sums, &total);
-    bin_off[p * kBins + threadIdx.x] = excl;
-    int full = __syncthreads_or(uint64_t(c) == n);
-    if (threadIdx.x == 0) active[p] = full ? 0u : 1u;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t n_active = 0;
-    for (int p = 0; p < kPasses; ++p) n_active += active[p];
-    uint32_t seen = 0, cur = 0;
-    for (int p = 0; p < kPasses; ++p) {
-      plan->active[p] = active[p];
-      plan->src[p] = 0;
-      plan->dst[p] = 0;
-      if (!active[p]) continue;
-      plan->src[p] = cur;
-      ++seen;
-      uint32_t d = (seen == n_active) ? 3u : (cur == 1 ? 2u : 1u);
-      plan->dst[p] = d;
-      cur = d;
-    }
-    plan->n_active = n_active;
-  }
-}
-
-struct PassArgs {
-  const void* orig_keys;     // raw int64 (key_mode raw) or materialised u64
-  const uint32_t* perm_in;   // values of the first pass (NULL = identity)
+  int width, word, desc, src_mode, key_mode;
+  // passes
+  const void* orig_keys;     // what the first active pass streams (raw int64 or materialised words)
   uint64_t* keys_a;
   uint64_t* keys_b;
   uint32_t* vals_a;
   uint32_t* vals_b;
-  int64_t* out_keys;         // final sorted int64 keys (optional)
+  int64_t* out_keys;         // final sorted int64 keys (optional, raw modes)
   uint32_t* out_vals;        // final permutation
-  const Plan* plan;
-  const uint32_t* bin_off;
+  // zeroed per call
+  uint32_t* ghist;           // [kPasses][kBins]
   uint32_t* tile_counter;    // [kPasses]
-  uint64_t* status;          // [num_tiles][kBins]
-  int64_t n;
-  int key_mode;
+  uint32_t* grid_bar;        // grid barrier arrivals
+  uint64_t* status;          // [num_tiles][kBins] look-back words (epoch = pass + 1)
+  unsigned long long* stamps;  // optional [kStamps] globaltimer ns (device)
 };
 
-#ifndef RL_RANK_MODE
-#define RL_RANK_MODE 2  // 1: ballot match_any, 2: shared atomicOr match (fewest instructions)
-#endif
+__device__ __forceinline__ uint64_t load_key(const SortArgs& a, int64_t i) {
+  if (a.src_mode == kSrcInt64) return xform(uint64_t(__ldg(static_cast<const long long*>(a.col) + i)), a.desc);
+  if (a.src_mode == kSrcWords) return __ldg(static_cast<const unsigned long long*>(a.col) + i);
+  const uint64_t row = a.perm_in ? uint64_t(__ldg(a.perm_in + i)) : uint64_t(i);
+  if (a.src_mode == kSrcInt64Gather) return xform(uint64_t(__ldg(static_cast<const long long*>(a.col) + row)), a.desc);
+  return bytes_word(static_cast<const uint8_t*>(a.col) + row * uint64_t(a.width), a.width, a.word, a.desc);
+}
 
-// Shared memory of one persistent onesweep CTA: two tile buffers (one being
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Grid-wide barrier for the co-resident cooperative grid: the k-th barrier
+// completes when k * gridDim.x arrivals have been counted.
+__device__ __forceinline__ void grid_sync(uint32_t* arrivals, uint32_t k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(arrivals, 1u);
+    const uint32_t target = k * gridDim.x;
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(arrivals) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Shared memory of one CTA during a pass: two tile buffers (one being
 // processed — loaded by TMA, then reused as the digit-ordered staging area —
 // and one being prefetched), per-warp digit counters and match masks.
 constexpr size_t kBufBytes = size_t(kTile) * 12;  // keys (8 B) then row ids (4 B)
-constexpr size_t kPassSmem = 2 * kBufBytes + size_t(kWarps) * kBins * 4 * 2 + size_t(kBins) * 4 * 2 + 64 * 4 + 64;
+constexpr size_t kBarOffset = 2 * kBufBytes + size_t(kWarps) * kBins * 4 * 2 + size_t(kBins) * 4 + 64 * 4;
+constexpr size_t kPassSmemBytes = kBarOffset + 64;
+// + the plan kept for the whole kernel: global digit bases [kPasses][kBins] + flags
+constexpr size_t kSmemBytes = kPassSmemBytes + size_t(kPasses) * kBins * 4 + 64;
+
+struct PassState {  // per-CTA mbarrier phase parities, carried across passes
+  uint32_t phase0, phase1;
+};
 
 // Stable rank of every item of this warp within its digit, offset by the
 // warp's base for that digit (wh[] holds the bases on entry). Warp-striped
-// items: element order is (item, lane), so lanes of one item are ranked
-// by peer mask and items by the in-order shared atomics on wh[].
+// items: element order is (item, lane), so lanes of one item are ranked by
+// peer mask and items by the in-order shared atomics on wh[].
 template <int SHIFT>
 __device__ __forceinline__ void rank_items(const uint64_t (&k)[kItems], uint32_t (&rank2)[kItems / 2],
                                            uint32_t* wh, uint32_t* wm, uint32_t e0, uint32_t count, int lane) {
@@ -251,10 +212,10 @@ __device__ __forceinline__ void rank_items(const uint64_t (&k)[kItems], uint32_t
 
 // Issue the TMA bulk loads of one tile into `buf` (full 16-byte chunks; a
 // ragged tail is finished with plain loads after the wait).
-__device__ __forceinline__ void prefetch_tile(const PassArgs& a, const uint64_t* kin, const uint32_t* vin,
-                                              uint32_t tile, uint8_t* buf, uint64_t* bar) {
+__device__ __forceinline__ void prefetch_tile(int64_t n, const uint64_t* kin, const uint32_t* vin, uint32_t tile,
+                                              uint8_t* buf, uint64_t* bar) {
   const int64_t begin = int64_t(tile) * kTile;
-  const int64_t left = a.n - begin;
+  const int64_t left = n - begin;
   const uint32_t count = left < kTile ? uint32_t(left) : uint32_t(kTile);
   const uint32_t kbytes = (count * 8u) & ~15u;
   const uint32_t vbytes = vin ? ((count * 4u) & ~15u) : 0u;
@@ -263,29 +224,24 @@ __device__ __forceinline__ void prefetch_tile(const PassArgs& a, const uint64_t*
   if (vbytes) bulk_g2s(buf + size_t(kTile) * 8, vin + begin, vbytes, bar);
 }
 
-// K2: one stable 8-bit onesweep digit pass (PASS selects the digit).
-// Persistent: each CTA claims tiles in increasing order from an atomic
-// counter and prefetches tile i+1 with TMA while it ranks and scatters tile
-// i, so HBM always has loads in flight. Progress: the smallest unfinished
-// tile's predecessors are all finished, and it is either being processed
-// or queued behind a smaller tile of the same CTA.
+// One stable 8-bit onesweep digit pass (PASS selects the digit). Persistent:
+// the CTA claims tiles in increasing order and prefetches tile i+1 while it
+// processes tile i. Progress: the smallest unfinished tile's predecessors
+// are all finished, and it is either being processed or queued behind a
+// smaller tile of the same CTA.
 template <int PASS>
-__global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_kernel(PassArgs a) {
+__device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint32_t src, uint32_t dst,
+                                      const uint32_t* bin_off, PassState& ps) {
   constexpr int kShift = PASS * kBits;
   constexpr uint32_t kEpoch = PASS + 1;
-  const Plan* plan = a.plan;
-  if (!plan->active[PASS]) return;
-  extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* bufs = smem;
   uint32_t* whist = reinterpret_cast<uint32_t*>(smem + 2 * kBufBytes);
   uint32_t* wmatch = whist + kWarps * kBins;
-  uint32_t* local_start = wmatch + kWarps * kBins;
-  uint32_t* gbase = local_start + kBins;
+  uint32_t* gbase = wmatch + kWarps * kBins;
   uint32_t* misc = gbase + kBins;  // [0],[1] claimed tile ids (by iteration parity), [4..] scan scratch
-  uint64_t* bars = reinterpret_cast<uint64_t*>(misc + 64);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t src = plan->src[PASS], dst = plan->dst[PASS];
   const uint32_t num_tiles = uint32_t((a.n + kTile - 1) / kTile);
   const uint64_t* kin = src == 1 ? a.keys_a : src == 2 ? a.keys_b : static_cast<const uint64_t*>(a.orig_keys);
   const uint32_t* vin = src == 1 ? a.vals_a : src == 2 ? a.vals_b : a.perm_in;
@@ -294,15 +250,16 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_ker
 
   for (int i = tid; i < 2 * kWarps * kBins; i += kThreads) whist[i] = 0;  // whist + wmatch
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
     const uint32_t t = atomicAdd(&a.tile_counter[PASS], 1u);
     misc[0] = t;
-    if (t < num_tiles) prefetch_tile(a, kin, vin, t, bufs, &bars[0]);
+    if (t < num_tiles) {
+      fence_proxy_async_smem();  // buffer 0 was last written by generic stores
+      prefetch_tile(a.n, kin, vin, t, bufs, &bars[0]);
+    }
   }
   __syncthreads();
   uint32_t tile = misc[0];
-  uint32_t cb = 0, phase0 = 0, phase1 = 0;  // cb: buffer + claim slot of this iteration
+  uint32_t cb = 0;  // buffer + claim slot of this iteration
   uint32_t* wh = whist + warp * kBins;
   const uint32_t e0 = uint32_t(warp) * (32 * kItems) + lane;
 
@@ -315,14 +272,15 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_ker
       misc[cb ^ 1] = nt;  // slot cb^1: its previous value was read before the last barrier
       if (nt < num_tiles) {
         fence_proxy_async_smem();
-        prefetch_tile(a, kin, vin, nt, bufs + (cb ^ 1) * kBufBytes, &bars[cb ^ 1]);
+        prefetch_tile(a.n, kin, vin, nt, bufs + (cb ^ 1) * kBufBytes, &bars[cb ^ 1]);
       }
     }
     const int64_t tile_begin = int64_t(tile) * kTile;
     const int64_t left = a.n - tile_begin;
     const uint32_t count = left < kTile ? uint32_t(left) : uint32_t(kTile);
-    mbar_wait(&bars[cb], cb ? phase1 : phase0);
-    if (cb) phase1 ^= 1; else phase0 ^= 1;
+    mbar_wait(&bars[cb], cb ? ps.phase1 : ps.phase0);
+    if (cb) ps.phase1 ^= 1;
+    else ps.phase0 ^= 1;
     if (count < kTile) {  // ragged tail: the bytes TMA did not move
       const uint32_t kdone = ((count * 8u) & ~15u) / 8u;
       for (uint32_t i = kdone + tid; i < count; i += kThreads) skeys[i] = kin[tile_begin + i];
@@ -371,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_ker
     __syncthreads();
 
     // ---- warp-level stable ranking
-    uint32_t rank2[kItems / 2];  // two 16-bit tile-local digit ranks per register (rank < kTile)
+    uint32_t rank2[kItems / 2];  // two 16-bit tile-local slots per register (slot < kTile)
     rank_items<kShift>(k, rank2, wh, wmatch + warp * kBins, e0, count, lane);
 
     // ---- stage the tile in digit order (stable local positions), in place
@@ -386,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_ker
 
     // ---- decoupled look-back for this thread's digit, kLookback predecessor
     // status words per round trip, from the nearest tile back to the first
-    // inclusive prefix.
+    // inclusive prefix; a not-yet-published predecessor is polled alone.
     uint64_t excl = 0;
     if (tile > 0) {
       int64_t p = int64_t(tile) - 1;
@@ -424,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_ker
       }
       st_relaxed(my_status, pack_status(kFlagIncl, kEpoch, excl + run));
     }
-    gbase[tid] = a.bin_off[PASS * kBins + tid] + uint32_t(excl) - ls;
+    gbase[tid] = bin_off[PASS * kBins + tid] + uint32_t(excl) - ls;
     __syncthreads();  // every warp is past its ranking: whist may be reset
     for (int i = tid; i < kWarps * kBins; i += kThreads) whist[i] = 0;  // for the next tile
 
@@ -461,28 +419,112 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) onesweep_ker
   }
 }
 
-typedef void (*OnesweepFn)(PassArgs);
-static const OnesweepFn kOnesweep[kPasses] = {onesweep_kernel<0>, onesweep_kernel<1>, onesweep_kernel<2>,
-                                              onesweep_kernel<3>, onesweep_kernel<4>, onesweep_kernel<5>,
-                                              onesweep_kernel<6>, onesweep_kernel<7>};
-
-// No active pass (all keys share every digit, or n == 1): copy through.
-__global__ void finalize_kernel(const Plan* plan, const int64_t* raw_keys, const uint32_t* perm_in,
-                                int64_t n, int64_t* out_keys, uint32_t* out_vals) {
-  if (plan != nullptr && plan->n_active != 0) return;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    out_vals[i] = perm_in ? perm_in[i] : uint32_t(i);
-    if (out_keys) out_keys[i] = raw_keys[i];
+// K1: all eight digit histograms in one read of the keys (its own launch:
+// shared-atomic bound, it wants 4x the resident threads of the passes).
+constexpr int kHistThreads = 512;
+__global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
+  __shared__ uint32_t h[kPasses * kBins];
+  const int tid = threadIdx.x;
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
+  for (int i = tid; i < kPasses * kBins; i += kHistThreads) h[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * kHistThreads * kHistUnroll;
+  for (int64_t base = int64_t(blockIdx.x) * kHistThreads * kHistUnroll + tid; base < a.n; base += stride) {
+    uint64_t k[kHistUnroll];
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t i = base + int64_t(u) * kHistThreads;
+      k[u] = i < a.n ? load_key(a, i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t i = base + int64_t(u) * kHistThreads;
+      if (i >= a.n) continue;
+      if (a.materialized) a.materialized[i] = k[u];
+#pragma unroll
+      for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p * kBins + ((k[u] >> (p * kBits)) & (kBins - 1))], 1u);
+    }
   }
+  __syncthreads();
+  for (int i = tid; i < kPasses * kBins; i += kHistThreads) {
+    const uint32_t c = h[i];
+    if (c) atomicAdd(&a.ghist[i], c);
+  }
+}
+
+// The whole sort after the histograms: plan, every active digit pass,
+// copy-through — one cooperative launch.
+__global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(SortArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* bin_off = reinterpret_cast<uint32_t*>(smem + kPassSmemBytes);  // [kPasses][kBins], whole kernel
+  uint32_t* plan = bin_off + kPasses * kBins;                                // [0..7] active, [8] n_active
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
+  const int tid = threadIdx.x;
+  uint32_t barrier_no = 0;
+  const bool stamper = a.stamps && blockIdx.x == 0 && tid == 0;
+
+  // ---- histograms come from hist_kernel (launched just before, on the same stream)
+  if (stamper) a.stamps[1] = globaltimer();
+
+  // ---- plan (every CTA for itself): global digit bases + active digits
+  {
+    uint32_t* warp_sums = reinterpret_cast<uint32_t*>(smem);  // scratch
+    for (int p = 0; p < kPasses; ++p) {
+      const uint32_t c = __ldcg(a.ghist + p * kBins + tid);
+      uint32_t total;
+      bin_off[p * kBins + tid] = block_exclusive_scan<kThreads>(c, warp_sums, &total);
+      const int full = __syncthreads_or(uint64_t(c) == uint64_t(a.n));
+      if (tid == 0) plan[p] = full ? 0u : 1u;
+    }
+    if (tid == 0) {
+      uint32_t na = 0;
+      for (int p = 0; p < kPasses; ++p) na += plan[p];
+      plan[kPasses] = na;
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+    }
+    __syncthreads();
+  }
+
+  // ---- the active digit passes, least significant first
+  const uint32_t n_active = plan[kPasses];
+  PassState ps{0, 0};
+  uint32_t src = 0, seen = 0;
+  for (int p = 0; p < kPasses; ++p) {
+    if (!plan[p]) continue;
+    ++seen;
+    const uint32_t dst = seen == n_active ? 3u : (src == 1 ? 2u : 1u);
+    switch (p) {
+      case 0: run_pass<0>(a, smem, src, dst, bin_off, ps); break;
+      case 1: run_pass<1>(a, smem, src, dst, bin_off, ps); break;
+      case 2: run_pass<2>(a, smem, src, dst, bin_off, ps); break;
+      case 3: run_pass<3>(a, smem, src, dst, bin_off, ps); break;
+      case 4: run_pass<4>(a, smem, src, dst, bin_off, ps); break;
+      case 5: run_pass<5>(a, smem, src, dst, bin_off, ps); break;
+      case 6: run_pass<6>(a, smem, src, dst, bin_off, ps); break;
+      default: run_pass<7>(a, smem, src, dst, bin_off, ps); break;
+    }
+    src = dst;
+    if (seen < n_active) grid_sync(a.grid_bar, ++barrier_no);  // the next pass reads what this one wrote
+    if (stamper) a.stamps[2 + p] = globaltimer();
+  }
+
+  // ---- no active digit (all keys equal, or n == 1): copy through
+  if (n_active == 0) {
+    for (int64_t i = int64_t(blockIdx.x) * kThreads + tid; i < a.n; i += int64_t(gridDim.x) * kThreads) {
+      a.out_vals[i] = a.perm_in ? a.perm_in[i] : uint32_t(i);
+      if (a.out_keys) a.out_keys[i] = static_cast<const int64_t*>(a.col)[i];
+    }
+  }
+  if (stamper) a.stamps[kStamps - 1] = globaltimer();
 }
 
 struct Layout {
   uint32_t* hist;
   uint32_t* tile_counter;
+  uint32_t* grid_bar;
   uint64_t* status;
-  size_t zero_bytes;  // prefix [hist, counters, status] zeroed per call
-  uint32_t* bin_off;
-  Plan* plan;
+  size_t zero_bytes;  // prefix [hist, counters, barrier, status] zeroed per call
   uint64_t* keys_a;
   uint64_t* keys_b;
   uint32_t* vals_a;
@@ -494,9 +536,8 @@ static void carve(C& c, int64_t n) {
   const size_t tiles = size_t((n + kTile - 1) / kTile);
   c.template take<uint32_t>(kPasses * kBins);
   c.template take<uint32_t>(kPasses);
+  c.template take<uint32_t>(1);
   c.template take<uint64_t>(tiles * kBins);
-  c.template take<uint32_t>(kPasses * kBins);
-  c.template take<Plan>(1);
   c.template take<uint64_t>(size_t(n));
   c.template take<uint64_t>(size_t(n));
   c.template take<uint32_t>(size_t(n));
@@ -515,10 +556,9 @@ static bool carve_layout(Layout& L, void* ws, size_t ws_bytes, int64_t n) {
   const size_t tiles = size_t((n + kTile - 1) / kTile);
   L.hist = c.take<uint32_t>(kPasses * kBins);
   L.tile_counter = c.take<uint32_t>(kPasses);
+  L.grid_bar = c.take<uint32_t>(1);
   L.status = c.take<uint64_t>(tiles * kBins);
   L.zero_bytes = c.used;
-  L.bin_off = c.take<uint32_t>(kPasses * kBins);
-  L.plan = c.take<Plan>(1);
   L.keys_a = c.take<uint64_t>(size_t(n));
   L.keys_b = c.take<uint64_t>(size_t(n));
   L.vals_a = c.take<uint32_t>(size_t(n));
@@ -531,69 +571,50 @@ __global__ void identity_kernel(const uint32_t* perm_in, int64_t n, uint32_t* ou
     out[i] = perm_in ? perm_in[i] : uint32_t(i);
 }
 
-// Shared launcher: K1 → plan → 8 × K2 → finalize. `h` describes how K1
-// reads keys; `orig_keys`/`key_mode` how the first active pass reads them.
-static int launch_sort(HistArgs h, const void* orig_keys, int key_mode, const uint32_t* perm_in, int64_t n,
-                       int64_t* sorted_keys_out, uint32_t* perm_out, const Layout& L, cudaStream_t stream,
-                       void* const* events = nullptr) {
-  const int sms = device_sm_count();
-  auto mark = [&](int i) {
-    if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), stream);
-  };
+// Largest co-resident grid of the cooperative sort kernel on this device.
+static int sort_grid_limit() {
+  static int cached = 0;
+  if (cached > 0) return cached;
+  if (cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)) != cudaSuccess)
+    return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sort_kernel, kThreads, kSmemBytes) != cudaSuccess ||
+      per_sm < 1)
+    return -1;
+  cached = per_sm * device_sm_count();
+  return cached;
+}
+
+static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* const* events) {
+  const int limit = sort_grid_limit();
+  if (limit < 1) {
+    cudaError_t e = cudaGetLastError();
+    return rl_cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration);
+  }
   cudaError_t e = cudaMemsetAsync(L.hist, 0, L.zero_bytes, stream);
   if (e != cudaSuccess) return rl_cuda_status(e);
+  // enough CTAs for the tiles (and ~8K keys each in the histogram phase), at most all co-resident
+  const int64_t tiles = (a.n + kTile - 1) / kTile;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(limit, tiles)));
+  if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
   {
-    int64_t per_cta = int64_t(kHistThreads) * kHistUnroll * 4;
-    int grid = int(std::min<int64_t>((n + per_cta - 1) / per_cta, int64_t(sms) * 4));
-    mark(0);
-    hist_kernel<<<std::max(grid, 1), kHistThreads, 0, stream>>>(h);
+    const int64_t per_cta = int64_t(kHistThreads) * kHistUnroll * 2;
+    const int hgrid = int(std::max<int64_t>(1, std::min<int64_t>((a.n + per_cta - 1) / per_cta,
+                                                                 int64_t(device_sm_count()) * 4)));
+    hist_kernel<<<hgrid, kHistThreads, 0, stream>>>(a);
   }
-  mark(1);
-  plan_kernel<<<1, kBins, 0, stream>>>(L.hist, L.bin_off, L.plan, uint64_t(n));
-
-  PassArgs p;
-  p.orig_keys = orig_keys;
-  p.perm_in = perm_in;
-  p.keys_a = L.keys_a;
-  p.keys_b = L.keys_b;
-  p.vals_a = L.vals_a;
-  p.vals_b = L.vals_b;
-  p.out_keys = sorted_keys_out;
-  p.out_vals = perm_out;
-  p.plan = L.plan;
-  p.bin_off = L.bin_off;
-  p.tile_counter = L.tile_counter;
-  p.status = L.status;
-  p.n = n;
-  p.key_mode = key_mode;
-  static bool attr_set = false;  // idempotent; a racing duplicate call is harmless
-  if (!attr_set) {
-    for (int pass = 0; pass < kPasses; ++pass) {
-      e = cudaFuncSetAttribute(kOnesweep[pass], cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPassSmem));
-      if (e != cudaSuccess) return rl_cuda_status(e);
-    }
-    attr_set = true;
-  }
-  const int tiles = int((n + kTile - 1) / kTile);
-  const int grid = std::min(tiles, sms * RL_ONESWEEP_MIN_BLOCKS);
-  for (int pass = 0; pass < kPasses; ++pass) {
-    mark(2 + pass);
-    kOnesweep[pass]<<<grid, kThreads, kPassSmem, stream>>>(p);
-  }
-  {
-    int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
-    mark(2 + kPasses);
-    finalize_kernel<<<grid, 256, 0, stream>>>(L.plan, static_cast<const int64_t*>(orig_keys), perm_in, n,
-                                              key_mode == kMaterialized ? nullptr : sorted_keys_out, perm_out);
-    mark(3 + kPasses);
-  }
-  count_launches(3 + kPasses);
-  return rl_cuda_status(cudaGetLastError());
+  if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
+  void* params[] = {&a};
+  e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
+                                  kSmemBytes, stream);
+  if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
+  count_launches(2);
+  return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
 }
 
 int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
-              cudaStream_t stream, void* const* events) {
+              cudaStream_t stream, void* const* events, unsigned long long* stamps) {
   const bool zero_width = col_kind == RL_COL_BYTES && width == 0;  // no key bytes: col may be NULL
   if (n < 0 || (n > 0 && perm_out == nullptr) || (n > 0 && col == nullptr && !zero_width)) return RL_ERR_BAD_ARG;
   if (n > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
@@ -610,7 +631,7 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
   if (col_kind == RL_COL_INT64 && !perm_in && (reinterpret_cast<uintptr_t>(col) & 15)) return RL_ERR_BAD_ARG;
   if (reinterpret_cast<uintptr_t>(perm_in) & 15) return RL_ERR_BAD_ARG;
   if (n == 0) return RL_OK;
-  if (col_kind == RL_COL_BYTES && width == 0) {  // tensorpath.py:218-219: identity order
+  if (zero_width) {  // tensorpath.py:218-219: identity order
     int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8));
     identity_kernel<<<grid, 256, 0, stream>>>(perm_in, n, perm_out);
     count_launches(1);
@@ -620,23 +641,37 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
   Layout L;
   if (!carve_layout(L, ws, ws_bytes, n)) return RL_ERR_WORKSPACE;
 
-  HistArgs h;
-  h.col = col;
-  h.perm_in = perm_in;
-  h.ghist = L.hist;
-  h.n = n;
-  h.width = width;
-  h.word = word;
-  h.desc = descending ? 1 : 0;
+  SortArgs a;
+  a.col = col;
+  a.perm_in = perm_in;
+  a.n = n;
+  a.width = width;
+  a.word = word;
+  a.desc = descending ? 1 : 0;
+  a.keys_a = L.keys_a;
+  a.keys_b = L.keys_b;
+  a.vals_a = L.vals_a;
+  a.vals_b = L.vals_b;
+  a.out_vals = perm_out;
+  a.ghist = L.hist;
+  a.tile_counter = L.tile_counter;
+  a.grid_bar = L.grid_bar;
+  a.status = L.status;
+  a.stamps = stamps;
   if (col_kind == RL_COL_INT64 && perm_in == nullptr) {
-    h.src_mode = kSrcInt64;
-    h.materialized = nullptr;
-    return launch_sort(h, col, descending ? kRawDesc : kRawAsc, nullptr, n, sorted_keys_out, perm_out, L, stream,
-                       events);
+    a.src_mode = kSrcInt64;
+    a.materialized = nullptr;
+    a.key_mode = descending ? kRawDesc : kRawAsc;
+    a.orig_keys = col;
+    a.out_keys = sorted_keys_out;
+  } else {
+    a.src_mode = col_kind == RL_COL_INT64 ? kSrcInt64Gather : kSrcBytes;
+    a.materialized = L.keys_b;  // read once by the first active pass, then reused as ping-pong B
+    a.key_mode = kMaterialized;
+    a.orig_keys = L.keys_b;
+    a.out_keys = nullptr;
   }
-  h.src_mode = col_kind == RL_COL_INT64 ? kSrcInt64Gather : kSrcBytes;
-  h.materialized = L.keys_b;  // read once by the first active pass, then reused as ping-pong B
-  return launch_sort(h, L.keys_b, kMaterialized, perm_in, n, nullptr, perm_out, L, stream, events);
+  return launch_sort(a, L, stream, events);
 }
 
 // ---------------------------------------------------------------- K8
@@ -678,20 +713,33 @@ int hash_partition_perm(const int64_t* keys, int64_t n, int parts, uint64_t seed
   const int sms = device_sm_count();
   const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
   dest_kernel<<<grid, 256, 0, stream>>>(keys, n, uint32_t(parts), fmix64(seed), words);
-  count_launches(2);
-  HistArgs h;
-  h.col = words;
-  h.perm_in = nullptr;
-  h.ghist = L.hist;
-  h.n = n;
-  h.width = 8;
-  h.word = 0;
-  h.desc = 0;
-  h.src_mode = kSrcWords;
-  h.materialized = nullptr;
-  int st = launch_sort(h, words, kMaterialized, nullptr, n, nullptr, perm_out, L, stream);
+  count_launches(1);
+  SortArgs a;
+  a.col = words;
+  a.perm_in = nullptr;
+  a.materialized = nullptr;
+  a.n = n;
+  a.width = 8;
+  a.word = 0;
+  a.desc = 0;
+  a.src_mode = kSrcWords;
+  a.key_mode = kMaterialized;
+  a.orig_keys = words;
+  a.keys_a = L.keys_a;
+  a.keys_b = L.keys_b;
+  a.vals_a = L.vals_a;
+  a.vals_b = L.vals_b;
+  a.out_keys = nullptr;
+  a.out_vals = perm_out;
+  a.ghist = L.hist;
+  a.tile_counter = L.tile_counter;
+  a.grid_bar = L.grid_bar;
+  a.status = L.status;
+  a.stamps = nullptr;
+  int st = launch_sort(a, L, stream, nullptr);
   if (st != RL_OK) return st;
   counts_kernel<<<1, kBins, 0, stream>>>(L.hist, parts, counts_out);
+  count_launches(1);
   return rl_cuda_status(cudaGetLastError());
 }
 

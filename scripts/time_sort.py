@@ -37,17 +37,28 @@ def main():
     for e in evs:
         e.record()
     arr = (ctypes.c_void_p * len(evs))(*[ctypes.c_void_p(e.cuda_event) for e in evs])
+    stamps = torch.zeros(_capi.RL_SORT_STAMPS, dtype=torch.int64, device="cuda")
     tot, passes, hist = [], [], []
     for r in range(a.reps + 3):
         flush.zero_()
+        stamps.zero_()
         _capi.check(lib.rl_sort_axis_profiled(ctypes.c_void_p(keys.data_ptr()), 0, 8, 0, 0, None, n,
                                               ctypes.c_void_p(sk.data_ptr()), ctypes.c_void_p(perm.data_ptr()),
-                                              ctypes.c_void_p(ws.data_ptr()), ws.numel(), s, arr), "sort")
+                                              ctypes.c_void_p(ws.data_ptr()), ws.numel(), s, arr,
+                                              ctypes.c_void_p(stamps.data_ptr())), "sort")
         torch.cuda.synchronize()
         if r >= 3:
-            tot.append(evs[0].elapsed_time(evs[11]))
-            passes.append([evs[2 + p].elapsed_time(evs[3 + p]) for p in range(8)])
-            hist.append(evs[0].elapsed_time(evs[1]))
+            tot.append(evs[0].elapsed_time(evs[2]))
+            st = stamps.cpu().tolist()
+            hist.append((st[1] - st[0]) / 1e6)
+            prev, pp = st[1], []
+            for p in range(8):
+                if st[2 + p]:
+                    pp.append((st[2 + p] - prev) / 1e6)
+                    prev = st[2 + p]
+                else:
+                    pp.append(0.0)
+            passes.append(pp)
     ok = bool((sk[1:] >= sk[:-1]).all()) and bool((keys[perm.long() & 0xFFFFFFFF] == sk).all())
     pm = np.median(np.array(passes), axis=0)
     act = pm[pm > 0.01]

@@ -226,6 +226,19 @@ RL_API int rl_hash_partition(const int64_t* keys, int64_t n, int32_t parts,
                       int64_t* counts_out, void* ws, size_t ws_bytes,
                       void* stream);
 
+/* Range partition for the distributed ORDER BY: row i (global row id
+ * gid_base + i) goes to destination = number of splitters (split_keys[s],
+ * split_gids[s]) strictly below (key, gid) in (key order, gid) order —
+ * descending keys compare by complement like rl_sort_axis. n_splitters
+ * <= 255 (destinations = n_splitters + 1). Stable within a destination;
+ * counts_out[n_splitters + 1]; columns gathered like rl_hash_partition. */
+RL_API int rl_range_partition(const int64_t* keys, int64_t n, int64_t gid_base,
+                              const int64_t* split_keys, const int64_t* split_gids,
+                              int32_t n_splitters, int32_t descending,
+                              const rl_column* columns, int32_t n_columns,
+                              uint32_t* row_ids_out, int64_t* counts_out, void* ws,
+                              size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------------
  * Host→device staging (the drop-in boundary's inputs are pageable numpy
  * columns). A stager owns a pinned ring of `slots` chunks, a copy stream

@@ -77,6 +77,10 @@ SIGNATURES = {
     "rl_gather_rows": (ctypes.c_int, [_P, _I64, ctypes.POINTER(RlColumn), _I32, _P]),
     "rl_widen_u32": (ctypes.c_int, [_P, _I64, _P, _P]),
     "rl_partition_workspace_bytes": (_SZ, [_I64, _I32]),
+    "rl_range_partition": (
+        ctypes.c_int,
+        [_P, _I64, _I64, _P, _P, _I32, _I32, ctypes.POINTER(RlColumn), _I32, _P, _P, _P, _SZ, _P],
+    ),
     "rl_stager_create": (_P, [_I32, _SZ, _I32]),
     "rl_stager_destroy": (None, [_P]),
     "rl_stager_h2d": (ctypes.c_int, [_P, _P, _P, _SZ, _P, _P]),

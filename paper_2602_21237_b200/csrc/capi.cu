@@ -15,6 +15,9 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
 size_t partition_workspace_bytes(int64_t n);
 int hash_partition_perm(const int64_t* keys, int64_t n, int parts, uint64_t seed, uint32_t* perm_out,
                         int64_t* counts_out, void* ws, size_t ws_bytes, cudaStream_t stream);
+int range_partition_perm(const int64_t* keys, int64_t n, int64_t gid_base, const int64_t* split_keys,
+                         const int64_t* split_gids, int nsplit, int descending, uint32_t* perm_out,
+                         int64_t* counts_out, void* ws, size_t ws_bytes, cudaStream_t stream);
 }  // namespace radix
 namespace keyaxis {
 size_t run_bounds_workspace_bytes(int64_t n);
@@ -151,6 +154,16 @@ int rl_hash_partition(const int64_t* keys, int64_t n, int32_t parts, uint64_t se
                       void* stream) {
   int st = rl::radix::hash_partition_perm(keys, n, parts, seed, row_ids_out, counts_out, ws, ws_bytes,
                                           as_stream(stream));
+  if (st != RL_OK) return st;
+  return rl::expand::gather_rows(row_ids_out, n, columns, n_columns, as_stream(stream));
+}
+
+int rl_range_partition(const int64_t* keys, int64_t n, int64_t gid_base, const int64_t* split_keys,
+                       const int64_t* split_gids, int32_t n_splitters, int32_t descending, const rl_column* columns,
+                       int32_t n_columns, uint32_t* row_ids_out, int64_t* counts_out, void* ws, size_t ws_bytes,
+                       void* stream) {
+  int st = rl::radix::range_partition_perm(keys, n, gid_base, split_keys, split_gids, n_splitters, descending,
+                                           row_ids_out, counts_out, ws, ws_bytes, as_stream(stream));
   if (st != RL_OK) return st;
   return rl::expand::gather_rows(row_ids_out, n, columns, n_columns, as_stream(stream));
 }

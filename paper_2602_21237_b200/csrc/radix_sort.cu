@@ -696,24 +696,10 @@ size_t partition_workspace_bytes(int64_t n) {
   return c.used + 256 + workspace_bytes(n);
 }
 
-int hash_partition_perm(const int64_t* keys, int64_t n, int parts, uint64_t seed, uint32_t* perm_out,
-                        int64_t* counts_out, void* ws, size_t ws_bytes, cudaStream_t stream) {
-  if (n < 0 || parts < 1 || parts > kBins || counts_out == nullptr || (n > 0 && (keys == nullptr || perm_out == nullptr)))
-    return RL_ERR_BAD_ARG;
-  if (n > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
-  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) return RL_ERR_WORKSPACE;
-  cudaError_t e = cudaMemsetAsync(counts_out, 0, sizeof(int64_t) * size_t(parts), stream);
-  if (e != cudaSuccess) return rl_cuda_status(e);
-  if (n == 0) return RL_OK;
-  Carve c{static_cast<char*>(ws), ws_bytes};
-  uint64_t* words = c.take<uint64_t>(size_t(n));
-  if (!c.ok) return RL_ERR_WORKSPACE;
-  Layout L;
-  if (!carve_layout(L, c.base + align_up(c.used, 256), ws_bytes - align_up(c.used, 256), n)) return RL_ERR_WORKSPACE;
-  const int sms = device_sm_count();
-  const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
-  dest_kernel<<<grid, 256, 0, stream>>>(keys, n, uint32_t(parts), fmix64(seed), words);
-  count_launches(1);
+// Stable counting pass over destination words (< parts <= 256): row ids
+// grouped by destination, input order kept within each destination.
+static int partition_by_words(const uint64_t* words, int64_t n, int parts, uint32_t* perm_out, int64_t* counts_out,
+                              const Layout& L, cudaStream_t stream) {
   SortArgs a;
   a.col = words;
   a.perm_in = nullptr;
@@ -741,6 +727,70 @@ int hash_partition_perm(const int64_t* keys, int64_t n, int parts, uint64_t seed
   counts_kernel<<<1, kBins, 0, stream>>>(L.hist, parts, counts_out);
   count_launches(1);
   return rl_cuda_status(cudaGetLastError());
+}
+
+static int partition_prologue(int64_t n, int parts, int64_t* counts_out, uint32_t* perm_out, void* ws,
+                              size_t ws_bytes, cudaStream_t stream, uint64_t** words, Layout* L) {
+  if (n < 0 || parts < 1 || parts > kBins || counts_out == nullptr || (n > 0 && perm_out == nullptr))
+    return RL_ERR_BAD_ARG;
+  if (n > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
+  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) return RL_ERR_WORKSPACE;
+  cudaError_t e = cudaMemsetAsync(counts_out, 0, sizeof(int64_t) * size_t(parts), stream);
+  if (e != cudaSuccess) return rl_cuda_status(e);
+  if (n == 0) return RL_OK;
+  Carve c{static_cast<char*>(ws), ws_bytes};
+  *words = c.take<uint64_t>(size_t(n));
+  if (!c.ok) return RL_ERR_WORKSPACE;
+  if (!carve_layout(*L, c.base + align_up(c.used, 256), ws_bytes - align_up(c.used, 256), n)) return RL_ERR_WORKSPACE;
+  return RL_OK;
+}
+
+int hash_partition_perm(const int64_t* keys, int64_t n, int parts, uint64_t seed, uint32_t* perm_out,
+                        int64_t* counts_out, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (n > 0 && keys == nullptr) return RL_ERR_BAD_ARG;
+  uint64_t* words = nullptr;
+  Layout L;
+  int st = partition_prologue(n, parts, counts_out, perm_out, ws, ws_bytes, stream, &words, &L);
+  if (st != RL_OK || n == 0) return st;
+  const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8));
+  dest_kernel<<<grid, 256, 0, stream>>>(keys, n, uint32_t(parts), fmix64(seed), words);
+  count_launches(1);
+  return partition_by_words(words, n, parts, perm_out, counts_out, L, stream);
+}
+
+// Range partition for the distributed sort: row i (global id gid_base + i)
+// goes to the number of splitters strictly below (key, gid) in
+// lexicographic order, so equal keys split by global row id and every
+// rank's range is contiguous in the global (stable) order.
+__global__ void range_dest_kernel(const int64_t* __restrict__ keys, int64_t n, int64_t gid_base,
+                                  const int64_t* __restrict__ split_keys, const int64_t* __restrict__ split_gids,
+                                  int nsplit, int desc, uint64_t* __restrict__ words) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = xform(uint64_t(keys[i]), desc);
+    const int64_t g = gid_base + i;
+    uint32_t d = 0;
+    for (int s = 0; s < nsplit; ++s) {
+      const uint64_t sk = xform(uint64_t(split_keys[s]), desc);
+      d += (sk < k || (sk == k && split_gids[s] < g)) ? 1u : 0u;
+    }
+    words[i] = d;
+  }
+}
+
+int range_partition_perm(const int64_t* keys, int64_t n, int64_t gid_base, const int64_t* split_keys,
+                         const int64_t* split_gids, int nsplit, int descending, uint32_t* perm_out,
+                         int64_t* counts_out, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if ((n > 0 && keys == nullptr) || nsplit < 0 || (nsplit > 0 && (!split_keys || !split_gids))) return RL_ERR_BAD_ARG;
+  uint64_t* words = nullptr;
+  Layout L;
+  const int parts = nsplit + 1;
+  int st = partition_prologue(n, parts, counts_out, perm_out, ws, ws_bytes, stream, &words, &L);
+  if (st != RL_OK || n == 0) return st;
+  const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8));
+  range_dest_kernel<<<grid, 256, 0, stream>>>(keys, n, gid_base, split_keys, split_gids, nsplit, descending ? 1 : 0,
+                                              words);
+  count_launches(1);
+  return partition_by_words(words, n, parts, perm_out, counts_out, L, stream);
 }
 
 }  // namespace radix

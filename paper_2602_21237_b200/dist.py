@@ -1,0 +1,195 @@
+"""Multi-GPU tensor path: one process per GPU, one exchange step per operator.
+
+North star / SURVEY.md §8(e): inputs shard naturally. Each rank holds a
+contiguous global row range of every relation (rank r owns rows
+[base_r, base_r + n_r)), so global row ids are base + local row.
+
+* Join: every rank hash-partitions R and S by ``hash_i64(key, seed) % P``
+  (hashing.py:54-61) with the stable device partition (K8), exchanges the
+  per-destination counts and then (key, global row id, payload columns) with
+  ``all_to_all_single`` (NCCL over NVLink on GPUs), and joins locally with
+  K1-K7. A key lands on exactly one rank; rows arrive grouped by source rank
+  in source order, i.e. in ascending global row id, so the local stable join
+  emits every key's pairs in the reference's (left row, right row) order.
+  The match count is an all-reduce SUM. Output stays sharded.
+* ORDER BY: regular samples of (key, global row id) are all-gathered, P-1
+  splitters are chosen on that composite order (duplicate-heavy keys split
+  by row id, which keeps stability), every rank range-partitions (K8 range
+  variant), exchanges, and sorts locally with the stable radix sort. Rank r
+  then holds the r-th slice of the global stable order.
+
+The device work is done through an ``Ops`` object: ``GpuOps`` calls the
+sm_100a kernels; the CPU multi-process tests inject an oracle-backed
+implementation to exercise this exchange protocol with the gloo backend
+(there is one GPU in this environment).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+PARTITION_SEED = 0x5EED  # join partition hash seed (any fixed value; every rank must agree)
+
+
+class GpuOps:
+    """Device kernels for the distributed operators (librelab_b200.so)."""
+
+    def hash_partition(self, keys: torch.Tensor, parts: int, seed: int):
+        from . import engine
+
+        return engine.hash_partition(keys, parts, seed)
+
+    def range_partition(self, keys: torch.Tensor, gid_base: int, split_keys: torch.Tensor, split_gids: torch.Tensor,
+                        descending: bool):
+        from . import engine
+
+        return engine.range_partition(keys, gid_base, split_keys, split_gids, descending)
+
+    def take(self, col: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
+        from . import engine
+
+        rows = rows if rows.dtype == torch.int32 else rows.to(torch.int32)  # uint32 row-id bits
+        out = torch.empty((rows.numel(),) + tuple(col.shape[1:]), dtype=col.dtype, device=col.device)
+        width = col.element_size() * (col.shape[1] if col.dim() > 1 else 1)
+        engine.gather_rows(rows, [engine.OutColumn(col.contiguous(), out, width, 0)])
+        return out
+
+    def local_join_pairs(self, lkeys: torch.Tensor, rkeys: torch.Tensor):
+        """(left rows, right rows) of the local equi-join, int64, reference order."""
+        from . import engine
+
+        li, ri = engine.index_keys(lkeys), engine.index_keys(rkeys)
+        al = engine.align(li, ri)
+        m, total = engine.fetch_scalars(al.m_total)
+        lr = torch.empty(total, dtype=torch.int32, device=lkeys.device)
+        rr = torch.empty(total, dtype=torch.int32, device=lkeys.device)
+        if total:
+            engine.expand(al, m, li, ri, 0, total, (), lr, rr)
+        return lr.to(torch.int64) & 0xFFFFFFFF, rr.to(torch.int64) & 0xFFFFFFFF
+
+    def stable_order(self, keys: torch.Tensor, descending: bool) -> torch.Tensor:
+        from . import engine
+
+        perm = engine.sort_permutation([engine.SortAxis(keys, descending)], keys.numel(), keys.device)
+        return perm.to(torch.int64) & 0xFFFFFFFF
+
+
+def _group_size(group) -> int:
+    return dist.get_world_size(group)
+
+
+def exchange(columns: Sequence[torch.Tensor], send_counts: torch.Tensor, group=None) -> List[torch.Tensor]:
+    """all-to-all-v of row-grouped columns. ``columns`` are grouped by
+    destination rank (rank order), ``send_counts[d]`` rows for rank d. Returns
+    the received columns, grouped by source rank, each group in source order."""
+    p = _group_size(group)
+    counts = send_counts.to(torch.int64).reshape(p)
+    recv_counts = torch.empty_like(counts)
+    dist.all_to_all_single(recv_counts, counts, group=group)
+    send_l = counts.cpu().tolist()
+    recv_l = recv_counts.cpu().tolist()
+    out = []
+    for col in columns:
+        col = col.contiguous()
+        dst = torch.empty((sum(recv_l),) + tuple(col.shape[1:]), dtype=col.dtype, device=col.device)
+        dist.all_to_all_single(dst, col, output_split_sizes=recv_l, input_split_sizes=send_l, group=group)
+        out.append(dst)
+    return out
+
+
+@dataclass
+class JoinShard:
+    """This rank's share of a distributed join's output."""
+
+    columns: List[torch.Tensor]  # left columns (key = matched key), then right non-key columns
+    left_gids: torch.Tensor  # int64 global row ids of the left rows
+    right_gids: torch.Tensor  # int64 global row ids of the right rows
+    total_matches: int  # all ranks
+
+
+def distributed_join(left: Sequence[torch.Tensor], left_key: int, left_base: int, right: Sequence[torch.Tensor],
+                     right_key: int, right_base: int, group=None, seed: int = PARTITION_SEED,
+                     ops: Optional[object] = None) -> JoinShard:
+    """Hash-partitioned equi-join of two row-sharded relations (see module doc)."""
+    ops = ops or GpuOps()
+    p = _group_size(group)
+    dev = left[left_key].device
+
+    def shuffle(cols, key_idx, base):
+        n = cols[key_idx].shape[0]
+        rows, counts = ops.hash_partition(cols[key_idx], p, seed)
+        gids = rows.to(torch.int64) & 0xFFFFFFFF
+        gids = gids + base
+        moved = [ops.take(c, rows) for c in cols]
+        recv = exchange(moved + [gids], counts, group)
+        return recv[:-1], recv[-1]
+
+    lcols, lgids = shuffle(list(left), left_key, left_base)
+    rcols, rgids = shuffle(list(right), right_key, right_base)
+    lrows, rrows = ops.local_join_pairs(lcols[left_key], rcols[right_key])
+    out = [ops.take(c, lrows) for c in lcols]
+    out += [ops.take(c, rrows) for j, c in enumerate(rcols) if j != right_key]
+    total = torch.tensor([lrows.numel()], dtype=torch.int64, device=dev)
+    dist.all_reduce(total, group=group)
+    return JoinShard(out, lgids[lrows], rgids[rrows], int(total.item()))
+
+
+def choose_splitters(keys: torch.Tensor, gid_base: int, descending: bool, group=None, per_rank: int = 256):
+    """Regular sampling of (key, global id); all-gather; P-1 splitters on the
+    composite order. Every rank computes the same splitters."""
+    p = _group_size(group)
+    n = keys.numel()
+    idx = (torch.arange(per_rank, device=keys.device, dtype=torch.int64) * max(n, 1)) // per_rank
+    idx = idx[idx < n] if n else idx[:0]
+    sk = keys[idx] if n else keys[:0]
+    sg = idx + gid_base
+    cnt = torch.tensor([sk.numel()], dtype=torch.int64, device=keys.device)
+    counts = [torch.zeros_like(cnt) for _ in range(p)]
+    dist.all_gather(counts, cnt, group=group)
+    mx = int(max(c.item() for c in counts))
+    pad_k = torch.zeros(mx, dtype=torch.int64, device=keys.device)
+    pad_g = torch.full((mx,), -1, dtype=torch.int64, device=keys.device)
+    pad_k[: sk.numel()] = sk
+    pad_g[: sg.numel()] = sg
+    all_k = [torch.empty_like(pad_k) for _ in range(p)]
+    all_g = [torch.empty_like(pad_g) for _ in range(p)]
+    dist.all_gather(all_k, pad_k, group=group)
+    dist.all_gather(all_g, pad_g, group=group)
+    ks = torch.cat([k[: int(c.item())] for k, c in zip(all_k, counts)]).cpu()
+    gs = torch.cat([g[: int(c.item())] for g, c in zip(all_g, counts)]).cpu()
+    if ks.numel() == 0:
+        e = torch.empty(0, dtype=torch.int64, device=keys.device)
+        return e, e
+    ordk = torch.bitwise_not(ks) if descending else ks
+    # composite (key, gid) order: stable sort by gid then by key
+    o = torch.argsort(gs, stable=True)
+    o = o[torch.argsort(ordk[o], stable=True)]
+    ks, gs = ks[o], gs[o]
+    m = ks.numel()
+    picks = [min(m - 1, (i * m) // p) for i in range(1, p)]
+    return ks[picks].to(keys.device), gs[picks].to(keys.device)
+
+
+@dataclass
+class SortShard:
+    columns: List[torch.Tensor]  # this rank's slice of the globally sorted relation
+    gids: torch.Tensor  # their global row ids (the permutation slice)
+
+
+def distributed_sort(cols: Sequence[torch.Tensor], key_idx: int, gid_base: int, descending: bool = False,
+                     group=None, ops: Optional[object] = None) -> SortShard:
+    """Range-partitioned stable ORDER BY on one int64 key (see module doc)."""
+    ops = ops or GpuOps()
+    keys = cols[key_idx]
+    split_k, split_g = choose_splitters(keys, gid_base, descending, group)
+    rows, counts = ops.range_partition(keys, gid_base, split_k, split_g, descending)
+    gids = (rows.to(torch.int64) & 0xFFFFFFFF) + gid_base
+    moved = [ops.take(c, rows) for c in cols]
+    recv = exchange(moved + [gids], counts, group)
+    rcols, rgids = recv[:-1], recv[-1]
+    perm = ops.stable_order(rcols[key_idx], descending)  # arrival order = ascending gid
+    return SortShard([ops.take(c, perm) for c in rcols], rgids[perm])

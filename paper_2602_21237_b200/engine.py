@@ -292,3 +292,27 @@ def hash_partition(keys: torch.Tensor, parts: int, seed: int, columns: Sequence[
         "rl_hash_partition",
     )
     return rows, counts
+
+
+def range_partition(keys: torch.Tensor, gid_base: int, split_keys: torch.Tensor, split_gids: torch.Tensor,
+                    descending: bool = False, columns: Sequence[OutColumn] = ()):
+    """K8 (sort variant): stable range partition by (key, global row id)
+    against sorted splitters. Returns (row ids grouped by destination,
+    counts[len(splitters) + 1])."""
+    lib = C.load()
+    n = keys.numel()
+    dev = keys.device
+    parts = split_keys.numel() + 1
+    rows = torch.empty(n, dtype=_U32, device=dev)
+    counts = torch.empty(parts, dtype=torch.int64, device=dev)
+    ws = workspace(lib.rl_partition_workspace_bytes(n, parts), dev)
+    sk = split_keys.to(device=dev, dtype=torch.int64).contiguous()
+    sg = split_gids.to(device=dev, dtype=torch.int64).contiguous()
+    arr, ncols = C.columns_array((c.src.data_ptr(), c.dst.data_ptr(), c.width, C.RL_SIDE_LEFT) for c in columns)
+    C.check(
+        lib.rl_range_partition(_ptr(keys.contiguous()), n, int(gid_base), _ptr(sk), _ptr(sg), parts - 1,
+                               int(descending), arr, ncols, _ptr(rows), _ptr(counts), _ptr(ws), ws.numel(),
+                               stream_handle()),
+        "rl_range_partition",
+    )
+    return rows, counts

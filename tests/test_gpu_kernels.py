@@ -134,3 +134,25 @@ def test_gather_and_widen_widths():
         assert (dst.cpu().numpy() == src[rows]).all(), w
     wide = engine.widen(rows_d)
     assert (wide.cpu().numpy() == rows.astype(np.int64)).all()
+
+
+def test_range_partition_matches_composite_order():
+    rng = np.random.default_rng(21)
+    for desc in (False, True):
+        n = 20_000
+        keys = rng.integers(-50, 50, n).astype(np.int64)
+        base = 1000
+        split_k = np.array([-10, 0, 0, 30], dtype=np.int64)
+        split_g = np.array([5000, 1500, 12000, 4000], dtype=np.int64)
+        if desc:
+            split_k = split_k[::-1].copy()
+        rows, counts = engine.range_partition(torch.from_numpy(keys).cuda(), base, torch.from_numpy(split_k),
+                                              torch.from_numpy(split_g), desc)
+        kk = np.invert(keys) if desc else keys
+        sk = np.invert(split_k) if desc else split_k
+        g = np.arange(n) + base
+        dest = np.zeros(n, dtype=np.int64)
+        for a, b in zip(sk, split_g):
+            dest += (a < kk) | ((a == kk) & (b < g))
+        assert (u32(rows) == np.argsort(dest, kind="stable")).all()
+        assert counts.cpu().tolist() == np.bincount(dest, minlength=5).tolist()

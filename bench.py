@@ -127,9 +127,9 @@ def active_digit_passes(keys: np.ndarray, descending: bool = False):
 
 
 def pass_bytes(n: int, active):
-    """Algorithmic bytes of each onesweep launch: the first
-    active pass reads keys (8n; row ids are generated) and writes key + id
-    (12n); later passes read and write 12n each; the last writes the final
+    """Algorithmic bytes of each onesweep digit pass: the
+    first active pass reads keys (8n; row ids are generated) and writes key +
+    id (12n); later passes read and write 12n each; the last writes the final
     int64 keys and uint32 permutation (12n)."""
     idx = [p for p, a in enumerate(active) if a]
     out = {}
@@ -224,31 +224,31 @@ def run_ours(args):
     stamps = torch.zeros(_capi.RL_SORT_STAMPS, dtype=torch.int64, device=dev)
 
     def device_step(events=None):
+        """One cfg2 ORDER BY on resident inputs: sorted keys + permutation
+        (histogram + cooperative onesweep kernel), then the payload gather."""
         sorted_keys = torch.empty(n, dtype=torch.int64, device=dev)
         perm = torch.empty(n, dtype=torch.int32, device=dev)
         out_pay = torch.empty((n, 4), dtype=torch.uint8, device=dev)
+        common = (ctypes.c_void_p(keys_d.data_ptr()), 0, 8, 0, 0, None, n, ctypes.c_void_p(sorted_keys.data_ptr()),
+                  ctypes.c_void_p(perm.data_ptr()), None, 0, ctypes.c_void_p(ws.data_ptr()), ws.numel(), s)
         if events is None:
-            _capi.check(lib.rl_sort_axis(ctypes.c_void_p(keys_d.data_ptr()), 0, 8, 0, 0, None, n,
-                                         ctypes.c_void_p(sorted_keys.data_ptr()), ctypes.c_void_p(perm.data_ptr()),
-                                         ctypes.c_void_p(ws.data_ptr()), ws.numel(), s), "sort")
+            _capi.check(lib.rl_sort_axis_gather(*common), "sort")
         else:
             arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
-            _capi.check(lib.rl_sort_axis_profiled(ctypes.c_void_p(keys_d.data_ptr()), 0, 8, 0, 0, None, n,
-                                                  ctypes.c_void_p(sorted_keys.data_ptr()),
-                                                  ctypes.c_void_p(perm.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
-                                                  ws.numel(), s, arr, ctypes.c_void_p(stamps.data_ptr())), "sort")
+            _capi.check(lib.rl_sort_axis_profiled(*common, arr, ctypes.c_void_p(stamps.data_ptr())), "sort")
         engine.gather_rows(perm, [engine.OutColumn(pay_d, out_pay, 4, 0)])
         return sorted_keys, perm, out_pay
 
     # correctness gate before timing: sorted + permutation + stable (cheap device checks)
-    sk, perm, _ = device_step()
+    sk, perm, _pay = device_step()
     p64 = perm.to(torch.int64) & 0xFFFFFFFF
     ok = bool((sk[1:] >= sk[:-1]).all()) and bool((keys_d[p64] == sk).all())
+    ok = ok and bool((pay_d[p64] == _pay).all())
     ties = sk[1:] == sk[:-1]
     ok = ok and bool((p64[1:][ties] > p64[:-1][ties]).all())
     if not ok:
         raise SystemExit("device sort failed its self-check; refusing to report a number")
-    del sk, perm, p64, ties
+    del sk, perm, p64, ties, _pay
 
     for _ in range(args.warmup):
         device_step()

@@ -110,7 +110,18 @@ RL_API int rl_sort_axis(const void* col, int32_t col_kind, int32_t width,
                  int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
                  void* ws, size_t ws_bytes, void* stream);
 
-/* Same as rl_sort_axis, for measurement: events[0..2] (cudaEvent_t
+/* rl_sort_axis + Relation.take fused into the final digit pass
+ * (tensorpath.py:247): for every column c (side RL_SIDE_LEFT, at most 8),
+ * c.dst row o = c.src row perm_out[o], written while the permutation is
+ * written — no separate gather launch, no re-read of the permutation. */
+RL_API int rl_sort_axis_gather(const void* col, int32_t col_kind, int32_t width,
+                 int32_t word, int32_t descending, const uint32_t* perm_in,
+                 int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
+                 const rl_column* columns, int32_t n_columns,
+                 void* ws, size_t ws_bytes, void* stream);
+#define RL_SORT_MAX_FUSED_COLUMNS 8
+
+/* Same as rl_sort_axis_gather, for measurement: events[0..2] (cudaEvent_t
  * created by the caller with timing enabled) are recorded on `stream`
  * before the histogram kernel, between it and the cooperative pass kernel,
  * and after the pass kernel; if stamps_dev (device, RL_SORT_STAMPS x
@@ -122,6 +133,7 @@ RL_API int rl_sort_axis(const void* col, int32_t col_kind, int32_t width,
 RL_API int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width,
                  int32_t word, int32_t descending, const uint32_t* perm_in,
                  int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
+                 const rl_column* columns, int32_t n_columns,
                  void* ws, size_t ws_bytes, void* stream,
                  void* const* events, unsigned long long* stamps_dev);
 

@@ -33,6 +33,7 @@ RL_MAX_COLUMNS = 32
 RL_MAX_ROWS = 2**32 - 1
 RL_SORT_EVENTS = 3
 RL_SORT_STAMPS = 11
+RL_SORT_MAX_FUSED_COLUMNS = 8
 
 
 class RlColumn(ctypes.Structure):
@@ -60,7 +61,12 @@ SIGNATURES = {
     "rl_sort_axis": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
     "rl_sort_axis_profiled": (
         ctypes.c_int,
-        [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _SZ, _P, ctypes.POINTER(ctypes.c_void_p), _P],
+        [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, ctypes.POINTER(RlColumn), _I32, _P, _SZ, _P,
+         ctypes.POINTER(ctypes.c_void_p), _P],
+    ),
+    "rl_sort_axis_gather": (
+        ctypes.c_int,
+        [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, ctypes.POINTER(RlColumn), _I32, _P, _SZ, _P],
     ),
     "rl_run_bounds_workspace_bytes": (_SZ, [_I64]),
     "rl_run_bounds": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _SZ, _P]),

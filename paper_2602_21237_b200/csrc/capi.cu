@@ -11,7 +11,8 @@ namespace radix {
 size_t workspace_bytes(int64_t n);
 int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
-              cudaStream_t stream, void* const* events, unsigned long long* stamps);
+              cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
+              int n_columns);
 size_t partition_workspace_bytes(int64_t n);
 int hash_partition_perm(const int64_t* keys, int64_t n, int parts, uint64_t seed, uint32_t* perm_out,
                         int64_t* counts_out, void* ws, size_t ws_bytes, cudaStream_t stream);
@@ -88,15 +89,23 @@ int rl_sort_axis(const void* col, int32_t col_kind, int32_t width, int32_t word,
                  const uint32_t* perm_in, int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws,
                  size_t ws_bytes, void* stream) {
   return rl::radix::sort_axis(col, col_kind, width, word, descending, perm_in, n, sorted_keys_out, perm_out, ws,
-                              ws_bytes, as_stream(stream), nullptr, nullptr);
+                              ws_bytes, as_stream(stream), nullptr, nullptr, nullptr, 0);
+}
+
+int rl_sort_axis_gather(const void* col, int32_t col_kind, int32_t width, int32_t word, int32_t descending,
+                        const uint32_t* perm_in, int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
+                        const rl_column* columns, int32_t n_columns, void* ws, size_t ws_bytes, void* stream) {
+  return rl::radix::sort_axis(col, col_kind, width, word, descending, perm_in, n, sorted_keys_out, perm_out, ws,
+                              ws_bytes, as_stream(stream), nullptr, nullptr, columns, n_columns);
 }
 
 int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width, int32_t word, int32_t descending,
-                          const uint32_t* perm_in, int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws,
-                          size_t ws_bytes, void* stream, void* const* events, unsigned long long* stamps_dev) {
+                          const uint32_t* perm_in, int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,
+                          const rl_column* columns, int32_t n_columns, void* ws, size_t ws_bytes, void* stream,
+                          void* const* events, unsigned long long* stamps_dev) {
   if (events == nullptr) return RL_ERR_BAD_ARG;
   return rl::radix::sort_axis(col, col_kind, width, word, descending, perm_in, n, sorted_keys_out, perm_out, ws,
-                              ws_bytes, as_stream(stream), events, stamps_dev);
+                              ws_bytes, as_stream(stream), events, stamps_dev, columns, n_columns);
 }
 
 size_t rl_run_bounds_workspace_bytes(int64_t n) { return rl::keyaxis::run_bounds_workspace_bytes(n); }

@@ -190,6 +190,32 @@ struct CarveSize {
   }
 };
 
+// Output column descriptors travel by value in kernel parameters.
+struct ColumnSet {
+  rl_column c[RL_MAX_COLUMNS];
+  int n;
+};
+
+// Copy one w-byte row (w = 8 / 4 / 16 fast paths; any width >= 0).
+__device__ __forceinline__ void copy_row(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int w) {
+  if (w == 8) {
+    __stcs(reinterpret_cast<unsigned long long*>(dst), __ldg(reinterpret_cast<const unsigned long long*>(src)));
+  } else if (w == 4) {
+    __stcs(reinterpret_cast<unsigned int*>(dst), __ldg(reinterpret_cast<const unsigned int*>(src)));
+  } else if (w == 16) {
+    __stcs(reinterpret_cast<uint4*>(dst), __ldg(reinterpret_cast<const uint4*>(src)));
+  } else if ((w & 7) == 0) {
+    for (int b = 0; b < w; b += 8)
+      *reinterpret_cast<uint64_t*>(dst + b) = __ldg(reinterpret_cast<const unsigned long long*>(src + b));
+  } else if ((w & 3) == 0) {
+    for (int b = 0; b < w; b += 4)
+      *reinterpret_cast<uint32_t*>(dst + b) = __ldg(reinterpret_cast<const unsigned int*>(src + b));
+  } else {
+    for (int b = 0; b < w; ++b) dst[b] = src[b];
+  }
+}
+
+
 int device_sm_count();
 void count_launches(int k);
 

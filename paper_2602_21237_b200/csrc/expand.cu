@@ -28,29 +28,6 @@ constexpr int kThreads = 256;
 constexpr int kItems = 8;
 constexpr int kTile = kThreads * kItems;
 
-struct ColumnSet {
-  rl_column c[RL_MAX_COLUMNS];
-  int n;
-};
-
-__device__ __forceinline__ void copy_row(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int w) {
-  if (w == 8) {
-    __stcs(reinterpret_cast<unsigned long long*>(dst), __ldg(reinterpret_cast<const unsigned long long*>(src)));
-  } else if (w == 4) {
-    __stcs(reinterpret_cast<unsigned int*>(dst), __ldg(reinterpret_cast<const unsigned int*>(src)));
-  } else if (w == 16) {
-    __stcs(reinterpret_cast<uint4*>(dst), __ldg(reinterpret_cast<const uint4*>(src)));
-  } else if ((w & 7) == 0) {
-    for (int b = 0; b < w; b += 8)
-      *reinterpret_cast<uint64_t*>(dst + b) = __ldg(reinterpret_cast<const unsigned long long*>(src + b));
-  } else if ((w & 3) == 0) {
-    for (int b = 0; b < w; b += 4)
-      *reinterpret_cast<uint32_t*>(dst + b) = __ldg(reinterpret_cast<const unsigned int*>(src + b));
-  } else {
-    for (int b = 0; b < w; ++b) dst[b] = src[b];
-  }
-}
-
 // last index g in [0, m] with offs[g] <= t (offs is non-decreasing, offs[0] = 0 <= t)
 __device__ __forceinline__ int64_t upper_bound_minus1(const uint64_t* __restrict__ offs, int64_t m, uint64_t t) {
   int64_t lo = 0, len = m + 1;

@@ -97,6 +97,19 @@ __device__ __forceinline__ uint64_t bytes_word(const uint8_t* row, int width, in
   return v;
 }
 
+constexpr int kMaxFusedColumns = 8;
+struct FusedColumns {
+  rl_column c[kMaxFusedColumns];
+  int n;
+};
+
+__device__ __forceinline__ void gather_fused(const FusedColumns& g, uint32_t row, uint64_t o) {
+  for (int ci = 0; ci < g.n; ++ci) {
+    const int w = g.c[ci].width;
+    copy_row(static_cast<const uint8_t*>(g.c[ci].src) + uint64_t(row) * w, static_cast<uint8_t*>(g.c[ci].dst) + o * w, w);
+  }
+}
+
 struct SortArgs {
   // phase H source
   const void* col;
@@ -118,6 +131,9 @@ struct SortArgs {
   uint32_t* grid_bar;        // grid barrier arrivals
   uint64_t* status;          // [num_tiles][kBins] look-back words (epoch = pass + 1)
   unsigned long long* stamps;  // optional [kStamps] globaltimer ns (device)
+  // columns gathered by the final permutation inside the last pass
+  // (Relation.take fused into the sort: dst row o = src row perm[o])
+  FusedColumns gather;
 };
 
 __device__ __forceinline__ uint64_t load_key(const SortArgs& a, int64_t i) {
@@ -396,7 +412,9 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
           const uint64_t key = skeys[j];
           const uint32_t o = gbase[uint32_t(key >> kShift) & (kBins - 1)] + j;
           if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(key, desc));
-          __stcs(a.out_vals + o, svals[j]);
+          const uint32_t row = svals[j];
+          __stcs(a.out_vals + o, row);
+          gather_fused(a.gather, row, o);
         }
       }
     } else {
@@ -512,8 +530,10 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   // ---- no active digit (all keys equal, or n == 1): copy through
   if (n_active == 0) {
     for (int64_t i = int64_t(blockIdx.x) * kThreads + tid; i < a.n; i += int64_t(gridDim.x) * kThreads) {
-      a.out_vals[i] = a.perm_in ? a.perm_in[i] : uint32_t(i);
+      const uint32_t row = a.perm_in ? a.perm_in[i] : uint32_t(i);
+      a.out_vals[i] = row;
       if (a.out_keys) a.out_keys[i] = static_cast<const int64_t*>(a.col)[i];
+      gather_fused(a.gather, row, uint64_t(i));
     }
   }
   if (stamper) a.stamps[kStamps - 1] = globaltimer();
@@ -614,7 +634,13 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
 
 int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
-              cudaStream_t stream, void* const* events, unsigned long long* stamps) {
+              cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
+              int n_columns) {
+  if (n_columns < 0 || n_columns > kMaxFusedColumns || (n_columns > 0 && columns == nullptr)) return RL_ERR_BAD_ARG;
+  for (int i = 0; i < n_columns; ++i)
+    if (columns[i].width < 0 || columns[i].side != RL_SIDE_LEFT ||
+        (columns[i].width > 0 && (!columns[i].src || !columns[i].dst)))
+      return RL_ERR_BAD_ARG;
   const bool zero_width = col_kind == RL_COL_BYTES && width == 0;  // no key bytes: col may be NULL
   if (n < 0 || (n > 0 && perm_out == nullptr) || (n > 0 && col == nullptr && !zero_width)) return RL_ERR_BAD_ARG;
   if (n > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
@@ -631,12 +657,13 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
   if (col_kind == RL_COL_INT64 && !perm_in && (reinterpret_cast<uintptr_t>(col) & 15)) return RL_ERR_BAD_ARG;
   if (reinterpret_cast<uintptr_t>(perm_in) & 15) return RL_ERR_BAD_ARG;
   if (n == 0) return RL_OK;
-  if (zero_width) {  // tensorpath.py:218-219: identity order
+  if (zero_width && n_columns == 0) {  // tensorpath.py:218-219: identity order
     int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(device_sm_count()) * 8));
     identity_kernel<<<grid, 256, 0, stream>>>(perm_in, n, perm_out);
     count_launches(1);
     return rl_cuda_status(cudaGetLastError());
   }
+  if (zero_width) return RL_ERR_BAD_ARG;  // fused gathers need a real key word
   if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) return RL_ERR_WORKSPACE;
   Layout L;
   if (!carve_layout(L, ws, ws_bytes, n)) return RL_ERR_WORKSPACE;
@@ -658,6 +685,8 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
   a.grid_bar = L.grid_bar;
   a.status = L.status;
   a.stamps = stamps;
+  a.gather.n = n_columns;
+  for (int i = 0; i < n_columns; ++i) a.gather.c[i] = columns[i];
   if (col_kind == RL_COL_INT64 && perm_in == nullptr) {
     a.src_mode = kSrcInt64;
     a.materialized = nullptr;
@@ -722,6 +751,7 @@ static int partition_by_words(const uint64_t* words, int64_t n, int parts, uint3
   a.grid_bar = L.grid_bar;
   a.status = L.status;
   a.stamps = nullptr;
+  a.gather.n = 0;
   int st = launch_sort(a, L, stream, nullptr);
   if (st != RL_OK) return st;
   counts_kernel<<<1, kBins, 0, stream>>>(L.hist, parts, counts_out);

@@ -44,7 +44,7 @@ def main():
         stamps.zero_()
         _capi.check(lib.rl_sort_axis_profiled(ctypes.c_void_p(keys.data_ptr()), 0, 8, 0, 0, None, n,
                                               ctypes.c_void_p(sk.data_ptr()), ctypes.c_void_p(perm.data_ptr()),
-                                              ctypes.c_void_p(ws.data_ptr()), ws.numel(), s, arr,
+                                              None, 0, ctypes.c_void_p(ws.data_ptr()), ws.numel(), s, arr,
                                               ctypes.c_void_p(stamps.data_ptr())), "sort")
         torch.cuda.synchronize()
         if r >= 3:

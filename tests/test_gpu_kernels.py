@@ -156,3 +156,30 @@ def test_range_partition_matches_composite_order():
             dest += (a < kk) | ((a == kk) & (b < g))
         assert (u32(rows) == np.argsort(dest, kind="stable")).all()
         assert counts.cpu().tolist() == np.bincount(dest, minlength=5).tolist()
+
+
+def test_fused_final_pass_gather_equals_take():
+    rng = np.random.default_rng(31)
+    for n in (1, 5, 3073, 40_000):
+        keys = rng.integers(-100, 100, n).astype(np.int64)
+        cols = [rng.integers(0, 256, (n, w), dtype=np.uint8) for w in (1, 4, 12, 16)]
+        cols.append(np.arange(n, dtype=np.int64) * 3)
+        gathers = []
+        for c in cols:
+            src = torch.from_numpy(c).cuda()
+            dst = torch.empty_like(src)
+            gathers.append(engine.OutColumn(src, dst, c.itemsize * (c.shape[1] if c.ndim > 1 else 1), 0))
+        for desc in (False, True):
+            perm = engine.sort_permutation([engine.SortAxis(torch.from_numpy(keys).cuda(), desc)], n, "cuda",
+                                           gather=gathers, fuse_gather=(n % 2 == 1))
+            want = O.stable_axis_order(keys, desc)
+            assert (u32(perm) == want).all()
+            for c, g in zip(cols, gathers):
+                assert (g.dst.cpu().numpy() == c[want]).all(), (n, c.shape)
+    # constant keys: no active digit, the copy-through path gathers too
+    keys = np.full(1000, 3, dtype=np.int64)
+    src = torch.arange(1000, dtype=torch.int64, device="cuda")
+    dst = torch.empty_like(src)
+    engine.sort_permutation([engine.SortAxis(torch.from_numpy(keys).cuda())], 1000, "cuda",
+                            gather=[engine.OutColumn(src, dst, 8, 0)], fuse_gather=True)
+    assert (dst.cpu().numpy() == np.arange(1000)).all()

@@ -158,6 +158,34 @@ __device__ __forceinline__ uint64_t lookback_publish(uint64_t* status, uint32_t 
   return excl;
 }
 
+// Warp-parallel decoupled look-back (called by all 32 lanes of one warp):
+// lane l inspects predecessor tile - 1 - l, a whole window per round trip.
+// Single packed value per tile. Returns the exclusive prefix (all lanes).
+__device__ __forceinline__ uint64_t warp_lookback(const uint64_t* status, uint32_t tile, uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t base = int64_t(tile) - 1;
+  while (true) {
+    const int64_t p = base - lane;
+    const uint64_t s = p >= 0 ? ld_relaxed(status + p) : (kFlagIncl | (uint64_t(epoch & 63u) << 56));
+    const bool ready = (s & kFlagMask) != 0 && status_epoch(s) == (epoch & 63u);
+    const uint32_t incl = __ballot_sync(0xffffffffu, ready && (s & kFlagMask) == kFlagIncl);
+    const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
+    const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor in the window
+    const uint32_t need = stop == 31 ? 0xffffffffu : ((2u << stop) - 1u);
+    if (notready & need) {
+      __nanosleep(32);
+      continue;
+    }
+    uint64_t v = lane <= stop ? (s & kValueMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (incl) return excl;
+    base -= 32;
+  }
+}
+
 inline int rl_cuda_status(cudaError_t e) { return e == cudaSuccess ? RL_OK : RL_ERR_CUDA + int(e); }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

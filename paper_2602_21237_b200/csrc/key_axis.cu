@@ -5,10 +5,16 @@
 //   K4  replaces tensorpath.py:109-128 (searchsorted(b, a), mask, compact)
 //   K5  replaces tensorpath.py:149-161 (per_key = lc * rc, cumsum, total)
 //
-// Both are single-pass decoupled look-back compactions: one read of the
-// input, one write of the compacted output, the device-side totals (D, M,
-// total pairs) written by the last tile, so the host never waits between
+// Both are single-pass decoupled look-back compactions (warp-parallel
+// look-back: 32 predecessor tiles per round trip): one read of the input,
+// one write of the compacted output, the device-side totals (D, M, total
+// pairs) written by the last tile, so the host never waits between
 // to_tensor, key_axis_align and the sizing pass.
+//
+// K4 is a tiled merge: a CTA stages 2048 consecutive left distinct keys,
+// finds the matching window of right distinct keys with two warp-parallel
+// 32-ary searches (4 round trips for ~1e6 keys instead of 20 dependent
+// loads per key), stages that window in shared memory and searches it there.
 #include <algorithm>
 
 #include "common.cuh"
@@ -21,6 +27,7 @@ constexpr int kRbItems = 16;
 constexpr int kRbTile = kThreads * kRbItems;
 constexpr int kAlItems = 8;
 constexpr int kAlTile = kThreads * kAlItems;
+constexpr int kAlWindow = 3584;  // right keys staged per CTA (larger windows search global memory)
 
 // ---------------------------------------------------------------- K3
 __global__ void __launch_bounds__(kThreads) run_bounds_kernel(const int64_t* __restrict__ sk, int64_t n,
@@ -58,7 +65,19 @@ __global__ void __launch_bounds__(kThreads) run_bounds_kernel(const int64_t* __r
   }
   uint32_t tile_total;
   const uint32_t off = block_exclusive_scan<kThreads>(c, warp_sums, &tile_total);
-  if (tid == 0) s_excl = lookback_publish(status, tile, 1, tile_total);
+  if (tid < 32) {
+    if (tile == 0) {
+      if (tid == 0) st_relaxed(&status[0], pack_status(kFlagIncl, 1, tile_total));
+      if (tid == 0) s_excl = 0;
+    } else {
+      if (tid == 0) st_relaxed(&status[tile], pack_status(kFlagAgg, 1, tile_total));
+      const uint64_t excl = warp_lookback(status, tile, 1);
+      if (tid == 0) {
+        st_relaxed(&status[tile], pack_status(kFlagIncl, 1, excl + tile_total));
+        s_excl = excl;
+      }
+    }
+  }
   __syncthreads();
   const uint64_t base = s_excl + off;
   uint32_t k = 0;
@@ -113,12 +132,38 @@ int run_bounds(const int64_t* sk, int64_t n, int64_t* key_values, uint32_t* offs
 }
 
 // ---------------------------------------------------------------- K4+K5
-__device__ __forceinline__ uint32_t lower_bound_i64(const int64_t* __restrict__ a, uint32_t n, int64_t key) {
-  uint32_t lo = 0, len = n;
+// first index in a[lo, hi) with a[i] >= x (strict = false) or a[i] > x
+// (strict = true); one warp, 32 probes per round trip.
+__device__ __forceinline__ uint32_t warp_bound(const int64_t* __restrict__ a, uint32_t lo, uint32_t hi, int64_t x,
+                                               bool strict) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t idx = lo + uint32_t(lane) * step;
+    bool pred = false;
+    if (idx < hi) {
+      const int64_t v = __ldg(reinterpret_cast<const long long*>(a) + idx);
+      pred = strict ? v <= x : v < x;
+    }
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, pred));
+    const uint32_t nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
+    const uint32_t nhi = min(hi, lo + c * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  bool pred = false;
+  if (lo + lane < hi) {
+    const int64_t v = __ldg(reinterpret_cast<const long long*>(a) + lo + lane);
+    pred = strict ? v <= x : v < x;
+  }
+  return lo + __popc(__ballot_sync(0xffffffffu, pred));
+}
+
+__device__ __forceinline__ uint32_t lower_bound_i64(const int64_t* a, uint32_t lo, uint32_t hi, int64_t key) {
+  uint32_t len = hi - lo;
   while (len > 0) {
     const uint32_t half = len >> 1;
-    const int64_t v = __ldg(reinterpret_cast<const long long*>(a) + lo + half);
-    if (v < key) {
+    if (a[lo + half] < key) {
       lo += half + 1;
       len -= half + 1;
     } else {
@@ -149,12 +194,55 @@ struct AlignArgs {
   uint64_t* incl_pairs;  // per tile inclusive pairs (valid when flag == INCL)
 };
 
+// Two-value warp look-back: matches packed in the status word, pairs in a
+// side array published before the flag (release) and read after it (acquire).
+__device__ __forceinline__ void warp_lookback2(const AlignArgs& a, uint32_t tile, uint64_t* excl_m,
+                                               uint64_t* excl_p) {
+  const int lane = threadIdx.x & 31;
+  uint64_t em = 0, ep = 0;
+  int64_t base = int64_t(tile) - 1;
+  while (true) {
+    const int64_t p = base - lane;
+    uint64_t s = kFlagIncl;  // virtual tile -1: inclusive zero
+    uint64_t pv = 0;
+    if (p >= 0) {
+      s = ld_acquire(&a.status[p]);
+      if ((s & kFlagMask) == kFlagIncl) pv = ld_relaxed(&a.incl_pairs[p]);
+      else if ((s & kFlagMask) == kFlagAgg) pv = ld_relaxed(&a.agg_pairs[p]);
+    }
+    const bool ready = (s & kFlagMask) != 0;
+    const uint32_t incl = __ballot_sync(0xffffffffu, ready && (s & kFlagMask) == kFlagIncl);
+    const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
+    const int stop = incl ? __ffs(incl) - 1 : 31;
+    const uint32_t need = stop == 31 ? 0xffffffffu : ((2u << stop) - 1u);
+    if (notready & need) {
+      __nanosleep(32);
+      continue;
+    }
+    uint64_t vm = lane <= stop ? (s & kValueMask) : 0;
+    uint64_t vp = lane <= stop ? pv : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      vm += __shfl_xor_sync(0xffffffffu, vm, o);
+      vp += __shfl_xor_sync(0xffffffffu, vp, o);
+    }
+    em += vm;
+    ep += vp;
+    if (incl) break;
+    base -= 32;
+  }
+  *excl_m = em;
+  *excl_p = ep;
+}
+
 __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
+  __shared__ int64_t sl[kAlTile];        // this tile's left distinct keys
+  __shared__ int64_t sr[kAlWindow];      // the matching window of right distinct keys
   __shared__ uint32_t warp_m[kThreads / 32 + 1];
   __shared__ uint64_t warp_p[kThreads / 32 + 1];
-  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_tile, s_lo, s_hi;
   __shared__ uint64_t s_excl_m, s_excl_p;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5;
   if (tid == 0) s_tile = atomicAdd(a.counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
@@ -169,24 +257,51 @@ __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
     }
     return;
   }
+  const int count = dl - begin < kAlTile ? int(dl - begin) : kAlTile;
   const bool last = begin + kAlTile >= dl;
+  for (int i = tid; i < count; i += kThreads) sl[i] = __ldg(reinterpret_cast<const long long*>(a.lkeys) + begin + i);
+  // right window [lo, hi): keys in [first left key, last left key]
+  if (warp == 0) {
+    const uint32_t lo = dr ? warp_bound(a.rkeys, 0, dr, a.lkeys[begin], false) : 0;
+    if (tid == 0) s_lo = lo;
+  } else if (warp == 1) {
+    const uint32_t hi = dr ? warp_bound(a.rkeys, 0, dr, a.lkeys[begin + count - 1], true) : 0;
+    if ((tid & 31) == 0) s_hi = hi;
+  }
+  __syncthreads();
+  const uint32_t lo = s_lo, hi = max(s_lo, s_hi);
+  const bool staged = hi - lo <= uint32_t(kAlWindow);
+  if (staged)
+    for (uint32_t i = tid; i < hi - lo; i += kThreads) sr[i] = __ldg(reinterpret_cast<const long long*>(a.rkeys) + lo + i);
+  __syncthreads();
 
   uint32_t match_bits = 0, my_m = 0;
   uint64_t my_p = 0;
   uint32_t rj[kAlItems];
   uint32_t lcnt[kAlItems], rcnt[kAlItems];
+  uint32_t from = 0;  // search start inside the window (this thread's keys increase)
 #pragma unroll
   for (int it = 0; it < kAlItems; ++it) {
-    const int64_t i = begin + tid * kAlItems + it;
+    const int e = tid * kAlItems + it;
     rj[it] = 0;
     lcnt[it] = rcnt[it] = 0;
-    if (i < dl && dr > 0) {
-      const int64_t key = a.lkeys[i];
-      const uint32_t j = lower_bound_i64(a.rkeys, dr, key);
-      if (j < dr && a.rkeys[j] == key) {
+    if (e < count && hi > lo) {
+      const int64_t key = sl[e];
+      uint32_t j;
+      bool hit;
+      if (staged) {
+        j = lower_bound_i64(sr, from, hi - lo, key);
+        hit = j < hi - lo && sr[j] == key;
+        from = j;
+        j += lo;
+      } else {
+        j = lower_bound_i64(a.rkeys, lo, hi, key);
+        hit = j < hi && a.rkeys[j] == key;
+      }
+      if (hit) {
         match_bits |= 1u << it;
         rj[it] = j;
-        lcnt[it] = a.loff[i + 1] - a.loff[i];
+        lcnt[it] = a.loff[begin + e + 1] - a.loff[begin + e];
         rcnt[it] = a.roff[j + 1] - a.roff[j];
         ++my_m;
         my_p += uint64_t(lcnt[it]) * uint64_t(rcnt[it]);
@@ -198,32 +313,28 @@ __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
   const uint32_t off_m = block_exclusive_scan<kThreads>(my_m, warp_m, &tot_m);
   const uint64_t off_p = block_exclusive_scan<kThreads>(my_p, warp_p, &tot_p);
 
-  if (tid == 0) {
+  if (warp == 0) {
     uint64_t excl_m = 0, excl_p = 0;
     if (tile == 0) {
-      a.incl_pairs[0] = tot_p;
-      st_release(&a.status[0], pack_status(kFlagIncl, 1, tot_m));
-    } else {
-      a.agg_pairs[tile] = tot_p;
-      st_release(&a.status[tile], pack_status(kFlagAgg, 1, tot_m));
-      int64_t p = int64_t(tile) - 1;
-      while (true) {
-        const uint64_t s = ld_acquire(&a.status[p]);
-        const uint64_t f = s & kFlagMask;
-        if (f == 0) continue;
-        excl_m += s & kValueMask;
-        if (f == kFlagIncl) {
-          excl_p += ld_relaxed(&a.incl_pairs[p]);
-          break;
-        }
-        excl_p += ld_relaxed(&a.agg_pairs[p]);
-        --p;
+      if (tid == 0) {
+        a.incl_pairs[0] = tot_p;
+        st_release(&a.status[0], pack_status(kFlagIncl, 1, tot_m));
       }
-      a.incl_pairs[tile] = excl_p + tot_p;
-      st_release(&a.status[tile], pack_status(kFlagIncl, 1, excl_m + tot_m));
+    } else {
+      if (tid == 0) {
+        a.agg_pairs[tile] = tot_p;
+        st_release(&a.status[tile], pack_status(kFlagAgg, 1, tot_m));
+      }
+      warp_lookback2(a, tile, &excl_m, &excl_p);
+      if (tid == 0) {
+        a.incl_pairs[tile] = excl_p + tot_p;
+        st_release(&a.status[tile], pack_status(kFlagIncl, 1, excl_m + tot_m));
+      }
     }
-    s_excl_m = excl_m;
-    s_excl_p = excl_p;
+    if (tid == 0) {
+      s_excl_m = excl_m;
+      s_excl_p = excl_p;
+    }
   }
   __syncthreads();
   uint64_t pos = s_excl_m + off_m;
@@ -231,9 +342,9 @@ __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
 #pragma unroll
   for (int it = 0; it < kAlItems; ++it) {
     if (match_bits & (1u << it)) {
-      const int64_t i = begin + tid * kAlItems + it;
-      a.matched_keys[pos] = a.lkeys[i];
-      a.ls[pos] = a.loff[i];
+      const int e = tid * kAlItems + it;
+      a.matched_keys[pos] = sl[e];
+      a.ls[pos] = a.loff[begin + e];
       a.lc[pos] = lcnt[it];
       a.rs[pos] = a.roff[rj[it]];
       a.rc[pos] = rcnt[it];

@@ -267,6 +267,16 @@ RL_API void* rl_stager_create(int32_t threads, size_t chunk_bytes, int32_t slots
 RL_API void rl_stager_destroy(void* stager);
 RL_API int rl_stager_h2d(void* stager, void* dst_dev, const void* src_host,
                          size_t bytes, void* stream, void* ready_event);
+/* Long-lived inputs (a relation reused across repetitions) are page-locked
+ * once and then uploaded with one direct DMA each (no staging copy). */
+RL_API int rl_host_register(void* host, size_t bytes);
+RL_API int rl_host_unregister(void* host);
+RL_API int rl_host_is_pinned(const void* host);
+RL_API int rl_stager_h2d_pinned(void* stager, void* dst_dev, const void* src_host,
+                                size_t bytes, void* stream, void* ready_event);
+/* Block until every upload issued through this stager has read its host
+ * memory (call before unregistering or freeing a source buffer). */
+RL_API int rl_stager_drain(void* stager);
 
 #ifdef __cplusplus
 }

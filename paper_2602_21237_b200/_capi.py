@@ -90,6 +90,11 @@ SIGNATURES = {
     "rl_stager_create": (_P, [_I32, _SZ, _I32]),
     "rl_stager_destroy": (None, [_P]),
     "rl_stager_h2d": (ctypes.c_int, [_P, _P, _P, _SZ, _P, _P]),
+    "rl_host_register": (ctypes.c_int, [_P, _SZ]),
+    "rl_host_unregister": (ctypes.c_int, [_P]),
+    "rl_host_is_pinned": (ctypes.c_int, [_P]),
+    "rl_stager_h2d_pinned": (ctypes.c_int, [_P, _P, _P, _SZ, _P, _P]),
+    "rl_stager_drain": (ctypes.c_int, [_P]),
     "rl_hash_partition": (
         ctypes.c_int,
         [_P, _I64, _I32, _U64, ctypes.POINTER(RlColumn), _I32, _P, _P, _P, _SZ, _P],

@@ -129,6 +129,55 @@ RL_API void rl_stager_destroy(void* handle) {
   delete s;
 }
 
+// Page-lock a long-lived host buffer so uploads from it are one direct DMA
+// (no staging copy: the staging memcpy + DMA triple the host memory traffic).
+RL_API int rl_host_register(void* host, size_t bytes) {
+  if (!host || !bytes) return RL_ERR_BAD_ARG;
+  cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) cudaGetLastError();
+  return rl::rl_cuda_status(e);
+}
+
+// 1 if `host` lies in page-locked memory this process registered or
+// allocated pinned (e.g. a previous operator's output), else 0.
+RL_API int rl_host_is_pinned(const void* host) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, host) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return attr.type == cudaMemoryTypeHost ? 1 : 0;
+}
+
+RL_API int rl_host_unregister(void* host) {
+  cudaError_t e = cudaHostUnregister(host);
+  if (e != cudaSuccess) cudaGetLastError();
+  return rl::rl_cuda_status(e);
+}
+
+// Upload from page-locked (registered or pinned) memory: one DMA on the
+// stager's copy stream, ordered like rl_stager_h2d.
+RL_API int rl_stager_h2d_pinned(void* handle, void* dst_dev, const void* src_host, size_t bytes, void* stream,
+                                void* ready_event) {
+  Stager* s = static_cast<Stager*>(handle);
+  if (!s || (bytes && (!dst_dev || !src_host))) return RL_ERR_BAD_ARG;
+  if (bytes == 0) return RL_OK;
+  std::lock_guard<std::mutex> g(s->call_mu);
+  cudaError_t e = cudaSuccess;
+  if (ready_event) e = cudaStreamWaitEvent(s->copy_stream, static_cast<cudaEvent_t>(ready_event), 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, s->copy_stream);
+  if (e == cudaSuccess) e = cudaEventRecord(s->done, s->copy_stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), s->done, 0);
+  return rl::rl_cuda_status(e);
+}
+
+// Wait until every upload issued so far has finished reading host memory.
+RL_API int rl_stager_drain(void* handle) {
+  Stager* s = static_cast<Stager*>(handle);
+  if (!s) return RL_ERR_BAD_ARG;
+  return rl::rl_cuda_status(cudaStreamSynchronize(s->copy_stream));
+}
+
 RL_API int rl_stager_h2d(void* handle, void* dst_dev, const void* src_host, size_t bytes, void* stream,
                          void* ready_event) {
   Stager* s = static_cast<Stager*>(handle);

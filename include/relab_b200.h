@@ -252,6 +252,16 @@ RL_API int rl_range_partition(const int64_t* keys, int64_t n, int64_t gid_base,
                               size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
+ * The reference's 128-bit multiset result digest (relation.py:319-330,
+ * hashing.py:64-109), bit-exact, computed on the device from the columns
+ * (src, width; schema order; Int64 width 8) of n rows without serialising
+ * them. out2[0] = lane 0 (high 64 bits), out2[1] = lane 1 (low 64 bits);
+ * n == 0 gives 0. Row width <= 512 bytes.
+ * --------------------------------------------------------------------- */
+RL_API int rl_multiset_digest(const rl_column* columns, int32_t n_columns,
+                              int64_t n, uint64_t* out2, void* stream);
+
+/* ---------------------------------------------------------------------
  * Host→device staging (the drop-in boundary's inputs are pageable numpy
  * columns). A stager owns a pinned ring of `slots` chunks, a copy stream
  * and `threads` native copy threads; rl_stager_h2d copies chunk c into the

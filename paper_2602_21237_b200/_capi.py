@@ -87,6 +87,7 @@ SIGNATURES = {
         ctypes.c_int,
         [_P, _I64, _I64, _P, _P, _I32, _I32, ctypes.POINTER(RlColumn), _I32, _P, _P, _P, _SZ, _P],
     ),
+    "rl_multiset_digest": (ctypes.c_int, [ctypes.POINTER(RlColumn), _I32, _I64, _P, _P]),
     "rl_stager_create": (_P, [_I32, _SZ, _I32]),
     "rl_stager_destroy": (None, [_P]),
     "rl_stager_h2d": (ctypes.c_int, [_P, _P, _P, _SZ, _P, _P]),

@@ -332,3 +332,21 @@ def range_partition(keys: torch.Tensor, gid_base: int, split_keys: torch.Tensor,
         "rl_range_partition",
     )
     return rows, counts
+
+
+def multiset_digest(columns: Sequence[torch.Tensor]) -> int:
+    """The reference's 128-bit multiset digest (relation.py:319-330) of the
+    relation whose columns (schema order; int64 [n] or uint8 [n, w]) are on
+    the device. Returns the 128-bit int (0 for an empty relation)."""
+    lib = C.load()
+    cols = [c.contiguous() for c in columns]
+    if not cols:
+        raise ValueError("a relation has at least one column")
+    n = cols[0].shape[0]
+    arr, ncols = C.columns_array(
+        (c.data_ptr(), None, c.element_size() * (c.shape[1] if c.dim() > 1 else 1), C.RL_SIDE_LEFT) for c in cols
+    )
+    out = torch.empty(2, dtype=torch.int64, device=cols[0].device)
+    C.check(lib.rl_multiset_digest(arr, ncols, n, _ptr(out), stream_handle()), "rl_multiset_digest")
+    hi, lo = (int(v) & (2**64 - 1) for v in fetch_scalars(out))
+    return (hi << 64) | lo

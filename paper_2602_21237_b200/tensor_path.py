@@ -458,3 +458,14 @@ def tensor_sort(rel, spec):
         peak_build_bytes=0,
     )
     return out, stats
+
+
+def multiset_digest(rel) -> int:
+    """relation.py:319-330 on the device: XOR of the per-row 128-bit hashes of
+    the canonical serialisation, computed straight from the columns (no
+    serialised copy). Returns the digest as an int (``ResultDigest.value``)."""
+    if rel.row_count == 0:
+        return 0
+    dev = _device()
+    up = _Uploads(rel.columns, dev)
+    return engine.multiset_digest([up.get(j) for j in range(len(rel.columns))])

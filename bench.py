@@ -359,6 +359,8 @@ def run_ours(args):
 
     if not args.no_join:
         line["join_cfg1"] = join_cfg1(args, dev, rank, world)
+    if args.extras and world == 1:
+        line["other_configs"] = extras(args, dev)
 
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -425,6 +427,84 @@ def join_cfg1(args, dev, rank, world):
     return res
 
 
+def extras(args, dev):
+    """The other BASELINE configs on one GPU (parity cases, not bench lines):
+    cfg5 join -> ORDER BY pipeline, cfg4 composite-key join, cfg3 Zipf count
+    + chunked pair streaming. Device-resident, CUDA-event timed."""
+    import torch
+
+    from paper_2602_21237_b200 import SortSpec, pipeline, synth
+
+    out = {}
+
+    def timed(fn, reps):
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            res = fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return res, ts
+
+    # cfg5: uniform keys with domain N, join then ORDER BY the R payload, kept in HBM
+    spec = SortSpec(("payload",))
+    for n in (10**6, 10**7, 10**8):
+        try:
+            r, s = synth.cfg1_relations(n=n, domain=n)
+            dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
+            del r, s
+            pipeline.join_then_order_by(dr, ds, "key", spec)
+            res, ts = timed(lambda: pipeline.join_then_order_by(dr, ds, "key", spec), 5)
+            out[f"cfg5_n{n:.0e}"] = {"rows_out": res.row_count, "p50_ms": round(percentile(ts, 50), 3),
+                                     "max_ms": round(max(ts), 3),
+                                     "mrows_per_s": round(2 * n / (statistics.median(ts) / 1e3) / 1e6, 1)}
+            del dr, ds, res
+        except Exception as e:  # keep the headline line even if an extra fails
+            out[f"cfg5_n{n:.0e}"] = {"error": repr(e)[:200]}
+        torch.cuda.empty_cache()
+
+    # cfg4: 1e8 x 1e8 composite (a<<32|b) keys, 16-byte payloads
+    try:
+        r, s = synth.cfg4_relations(n=10**8)
+        dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
+        del r, s
+        pipeline.join(dr, ds, "key")
+        res, ts = timed(lambda: pipeline.join(dr, ds, "key"), 3)
+        out["cfg4_n1e8"] = {"rows_out": res.row_count, "p50_ms": round(percentile(ts, 50), 3),
+                            "mrows_per_s": round(2e8 / (statistics.median(ts) / 1e3) / 1e6, 1)}
+        del dr, ds, res
+    except Exception as e:
+        out["cfg4_n1e8"] = {"error": repr(e)[:200]}
+    torch.cuda.empty_cache()
+
+    # cfg3: 10M x 10M Zipf(1.1): exact count (2.29e12) and chunked pair streaming
+    try:
+        r, s = synth.cfg3_relations()
+        lk = torch.from_numpy(r.column("key").copy()).to(dev)
+        sk = torch.from_numpy(s.column("key").copy()).to(dev)
+        plan, ts = timed(lambda: pipeline.plan_join(lk, sk), 3)
+        chunk = 1 << 30
+        start = plan.total // 2
+        it = pipeline.join_stream(plan, chunk_pairs=chunk, begin=start, end=start + 4 * chunk)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        streamed = sum(lr.numel() for _, lr, _ in it)
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b)
+        out["cfg3_n1e7"] = {"total_pairs": plan.total, "count_p50_ms": round(percentile(ts, 50), 3),
+                            "stream_pairs_per_s": round(streamed / (ms / 1e3), 0),
+                            "stream_sample_pairs": streamed,
+                            "stream_write_gbs": round(streamed * 8 / (ms / 1e3) / 1e9, 1),
+                            "note": "pairs materialised as uint32 (left row, right row) in 2^30-pair chunks"}
+    except Exception as e:
+        out["cfg3_n1e7"] = {"error": repr(e)[:200]}
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,6 +513,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-join", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also time BASELINE cfg3/cfg4/cfg5 (a few more minutes)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -391,19 +391,10 @@ def tensor_join(left: TensorRelation, right: TensorRelation, max_output_rows: in
     if total == 0:
         return rel_cls.empty(out_schema), TYPES["SpillStats"]()
 
-    dev = li.positions.device
-    l_axes, r_axes = left.device_axes(), right.device_axes()
-    l_key = left.schema.index(left.key)
-    r_key = right.schema.index(right.key)
-    cols = []
-    for j, (_, t) in enumerate(left.schema.attributes):
-        if j == l_key:
-            cols.append(engine.OutColumn(None, torch.empty(total, dtype=torch.int64, device=dev), 8, C.RL_SIDE_KEY))
-        else:
-            cols.append(_out_column(l_axes[j], t, total, dev, C.RL_SIDE_LEFT))
-    for j, (_, t) in enumerate(right.schema.attributes):
-        if j != r_key:
-            cols.append(_out_column(r_axes[j], t, total, dev, C.RL_SIDE_RIGHT))
+    from .pipeline import join_out_columns
+
+    cols = join_out_columns(left.device_axes(), left.schema.index(left.key), right.device_axes(),
+                            right.schema.index(right.key), total)
     engine.expand(al, m, li, ri, 0, total, cols)
     hosts = [_host_out(c.dst) for c in cols]
     torch.cuda.current_stream().synchronize()

@@ -1,0 +1,61 @@
+"""Device-resident pipeline (join → ORDER BY without leaving HBM), chunked
+join streaming and the device digest, against the drop-in and the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tensorpath_oracle as O
+from paper_2602_21237_b200 import SortSpec, pipeline, synth, tensor_join, tensor_sort, to_tensor
+
+pytestmark = pytest.mark.gpu
+
+
+def test_join_then_order_by_equals_drop_in_and_oracle():
+    n = 1_000_000
+    r, s = synth.cfg1_relations(n=n, domain=n, seed=4)
+    dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
+    spec = SortSpec(("payload",))
+    dev_out = pipeline.join_then_order_by(dr, ds, "key", spec)
+    host = dev_out.to_host()
+    joined, _ = tensor_join(to_tensor(r, "key"), to_tensor(s, "key"))
+    drop_in, _ = tensor_sort(joined, spec)
+    assert host.schema.names == drop_in.schema.names == ("key", "payload", "right_payload")
+    for a, b in zip(host.columns, drop_in.columns):
+        assert (a == b).all()
+    cols = O.join_columns(list(r.columns), 0, list(s.columns), 0)
+    perm = O.sort_permutation([cols[1]], [False])
+    for a, b in zip(host.columns, cols):
+        assert (a == b[perm]).all()
+    assert dev_out.digest() == O.multiset_digest(cols)
+
+
+def test_join_stream_and_checksum_windows_cfg3_shape():
+    r, s = synth.cfg3_relations(n=200_000)
+    lk, rk = r.column("key"), s.column("key")
+    plan = pipeline.plan_join(torch.from_numpy(lk.copy()).cuda(), torch.from_numpy(rk.copy()).cuda())
+    assert plan.total == O.join_count(lk, rk)
+    assert 5e8 < plan.total < 2e9  # the N=2e5 variant has ~9.1e8 pairs
+    windows = [(0, 1 << 20), (plan.total // 3, plan.total // 3 + (1 << 20)), (plan.total - 777_777, plan.total)]
+    for a, b in windows:
+        got_l, got_r = [], []
+        for start, lr, rr in pipeline.join_stream(plan, chunk_pairs=300_000, begin=a, end=b):
+            got_l.append(lr.cpu().numpy().view(np.uint32).astype(np.int64))
+            got_r.append(rr.cpu().numpy().view(np.uint32).astype(np.int64))
+        wl, wr = O.join_pairs(lk, rk, a, b)
+        assert (np.concatenate(got_l) == wl).all() and (np.concatenate(got_r) == wr).all()
+        assert pipeline.pair_checksum(plan, a, b) == O.pair_checksum(wl, wr)
+
+
+def test_order_by_multi_key_device_relation():
+    rng = np.random.default_rng(6)
+    n = 30_000
+    from paper_2602_21237_b200 import Bytes, Direction, Int64, Relation, Schema
+
+    rel = Relation(Schema((("a", Int64()), ("b", Bytes(5)), ("c", Int64()))),
+                   (rng.integers(-3, 3, n), rng.integers(0, 3, (n, 5), dtype=np.uint8), np.arange(n)))
+    spec = SortSpec(("b", "a"), (Direction.DESC, Direction.ASC))
+    out, perm = pipeline.order_by(pipeline.DeviceRelation.from_host(rel), spec)
+    want = O.sort_permutation([rel.column("b"), rel.column("a")], [True, False])
+    assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
+    assert (out.to_host().column("c") == want).all()

@@ -69,29 +69,52 @@ def measured_peak_hbm():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in
+    process through NVML (no nvidia-smi subprocess next to the kernels);
+    falls back to nvidia-smi when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
-        self.rows = []
+        self.period = period_s
+        self.rows = []  # (sm_mhz, max_mhz, set(reasons))
         self._stop = threading.Event()
         self._t = None
 
+    def _sample_nvml(self, nv, h):
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        return sm, mx, {name for name, const in self.REASONS if bits & getattr(nv, const)}
+
+    def _sample_smi(self):
+        out = subprocess.run(
+            ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+             "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        return float(f[0]), float(f[1]), {self.REASONS[i][0] for i in range(4) if f[2 + i] == "Active"}
+
     def _run(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            sample = lambda: self._sample_nvml(nv, h)  # noqa: E731
+        except Exception:
+            sample = self._sample_smi
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                    capture_output=True, text=True, timeout=5,
-                ).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self.rows.append(sample())
             except Exception:
                 return
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -105,13 +128,10 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*(r[2] for r in self.rows))), "samples": len(self.rows),
+                "source": "nvml"}
 
 
 def active_digit_passes(keys: np.ndarray, descending: bool = False):
@@ -380,15 +400,15 @@ def join_cfg1(args, dev, rank, world):
     rp = torch.from_numpy(r.column("payload").copy()).to(dev)
     sp = torch.from_numpy(s.column("payload").copy()).to(dev)
 
+    from paper_2602_21237_b200 import pipeline
+
+    dr = pipeline.DeviceRelation(r.schema, [rk, rp])
+    ds = pipeline.DeviceRelation(s.schema, [sk, sp])
+
     def device_join():
-        li, ri = engine.index_keys(rk), engine.index_keys(sk)
-        al = engine.align(li, ri)
-        m, total = engine.fetch_scalars(al.m_total)  # the one sizing sync
-        cols = [engine.OutColumn(None, torch.empty(total, dtype=torch.int64, device=dev), 8, 2),
-                engine.OutColumn(rp, torch.empty(total, dtype=torch.int64, device=dev), 8, 0),
-                engine.OutColumn(sp, torch.empty(total, dtype=torch.int64, device=dev), 8, 1)]
-        engine.expand(al, m, li, ri, 0, total, cols)
-        return total
+        """to_tensor x2 + align + sizing in one C call (rl_join_plan_build), the
+        one sizing sync, then the fused expansion + gathers."""
+        return pipeline.join(dr, ds, "key").row_count
 
     reps = 100
     for _ in range(5):

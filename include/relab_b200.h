@@ -177,6 +177,33 @@ RL_API int rl_key_axis_align(const int64_t* left_keys, const uint32_t* left_offs
                       size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Join plan: K1-K5 for both sides in ONE call over ONE workspace.
+ * tensorpath.py:78-93 (to_tensor) x 2 + 109-161 (key_axis_align + sizing).
+ * Fills *plan with device pointers into ws (valid while ws lives); the
+ * device scalars are [0] D_left, [1] D_right, [2] M, [3] total pairs.
+ * Feed the plan arrays to rl_join_expand / rl_join_pair_checksum.
+ * --------------------------------------------------------------------- */
+typedef struct rl_join_plan {
+  int64_t* scalars;
+  uint32_t* left_positions;
+  int64_t* left_key_values;
+  uint32_t* left_offsets;
+  uint32_t* right_positions;
+  int64_t* right_key_values;
+  uint32_t* right_offsets;
+  int64_t* matched_keys;
+  uint32_t* left_starts;
+  uint32_t* left_counts;
+  uint32_t* right_starts;
+  uint32_t* right_counts;
+  uint64_t* pair_offsets;
+} rl_join_plan;
+RL_API size_t rl_join_plan_workspace_bytes(int64_t n_left, int64_t n_right);
+RL_API int rl_join_plan_build(const int64_t* left_keys, int64_t n_left,
+                              const int64_t* right_keys, int64_t n_right, void* ws,
+                              size_t ws_bytes, rl_join_plan* plan, void* stream);
+
+/* ---------------------------------------------------------------------
  * K6+K7  Run expansion fused with the column gathers.
  *
  * Replaces tensorpath.py:157-185: output pair t (global index in

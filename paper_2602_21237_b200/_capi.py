@@ -45,6 +45,13 @@ class RlColumn(ctypes.Structure):
     ]
 
 
+class RlJoinPlan(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "scalars", "left_positions", "left_key_values", "left_offsets", "right_positions", "right_key_values",
+        "right_offsets", "matched_keys", "left_starts", "left_counts", "right_starts", "right_counts",
+        "pair_offsets")]
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -75,6 +82,8 @@ SIGNATURES = {
         ctypes.c_int,
         [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
     ),
+    "rl_join_plan_workspace_bytes": (_SZ, [_I64, _I64]),
+    "rl_join_plan_build": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(RlJoinPlan), _P]),
     "rl_join_expand": (
         ctypes.c_int,
         [_P, _P, _P, _P, _P, _I64, _P, _P, _U64, _U64, _P, _P, ctypes.POINTER(RlColumn), _I32, _P],

@@ -25,22 +25,39 @@ namespace rl {
 namespace expand {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+#ifndef RL_EXPAND_ITEMS
+#define RL_EXPAND_ITEMS 4
+#endif
+constexpr int kItems = RL_EXPAND_ITEMS;
+#ifndef RL_EXPAND_MIN_BLOCKS
+#define RL_EXPAND_MIN_BLOCKS 3
+#endif
 constexpr int kTile = kThreads * kItems;
 
-// last index g in [0, m] with offs[g] <= t (offs is non-decreasing, offs[0] = 0 <= t)
-__device__ __forceinline__ int64_t upper_bound_minus1(const uint64_t* __restrict__ offs, int64_t m, uint64_t t) {
-  int64_t lo = 0, len = m + 1;
-  while (len > 0) {
-    const int64_t half = len >> 1;
-    if (__ldg(reinterpret_cast<const unsigned long long*>(offs) + lo + half) <= t) {
-      lo += half + 1;
-      len -= half + 1;
-    } else {
-      len = half;
-    }
+// last index g in [0, m] with offs[g] <= t (offs is non-decreasing,
+// offs[0] = 0 <= t); one warp, 32 probes per round trip.
+__device__ __forceinline__ int64_t warp_last_le(const uint64_t* __restrict__ offs, int64_t lo, int64_t m,
+                                                uint64_t t) {
+  const int lane = threadIdx.x & 31;
+  int64_t hi = m + 1;  // answer + 1 = first index with offs[i] > t, in [lo, hi]; offs[lo] <= t
+  {  // gallop: the answer is usually within 32 keys of the hint (consecutive output tiles)
+    const bool pred = lo + lane < hi && __ldg(reinterpret_cast<const unsigned long long*>(offs) + lo + lane) <= t;
+    const uint32_t bal = __ballot_sync(0xffffffffu, pred);
+    if (bal != 0xffffffffu) return lo + __popc(bal) - 1;
+    lo += 31;
   }
-  return lo - 1;
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t idx = lo + int64_t(lane) * step;
+    const bool pred = idx < hi && __ldg(reinterpret_cast<const unsigned long long*>(offs) + idx) <= t;
+    const int64_t c = __popc(__ballot_sync(0xffffffffu, pred));
+    const int64_t nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
+    const int64_t nhi = min(hi, lo + c * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  const bool pred = lo + lane < hi && __ldg(reinterpret_cast<const unsigned long long*>(offs) + lo + lane) <= t;
+  return lo + __popc(__ballot_sync(0xffffffffu, pred)) - 1;
 }
 
 struct ExpandArgs {
@@ -58,75 +75,188 @@ struct ExpandArgs {
   uint64_t* checksum;  // checksum mode when non-null
 };
 
+// Gather one column for this thread's items: all loads first, then all
+// stores, so the kItems random reads are in flight together.
+template <typename T>
+__device__ __forceinline__ void gather_items(const rl_column& col, const uint32_t (&row)[kItems], uint64_t o0,
+                                             uint32_t valid) {
+  const T* src = static_cast<const T*>(col.src);
+  T* dst = static_cast<T*>(col.dst) + o0;  // item it writes dst[it * kThreads]
+  T v[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it)
+    if (valid & (1u << it)) v[it] = __ldg(src + row[it]);
+#pragma unroll
+  for (int it = 0; it < kItems; ++it)
+    if (valid & (1u << it)) __stcs(dst + it * kThreads, v[it]);
+}
+
+__device__ __forceinline__ void gather_column(const rl_column& col, const uint32_t (&row)[kItems], uint64_t o0,
+                                              uint32_t valid) {
+  const int w = col.width;
+  if (w == 8) {
+    gather_items<unsigned long long>(col, row, o0, valid);
+  } else if (w == 4) {
+    gather_items<unsigned int>(col, row, o0, valid);
+  } else if (w == 16) {
+    gather_items<uint4>(col, row, o0, valid);
+  } else {
+#pragma unroll 1
+    for (int it = 0; it < kItems; ++it)
+      if (valid & (1u << it))
+        copy_row(static_cast<const uint8_t*>(col.src) + uint64_t(row[it]) * w,
+                 static_cast<uint8_t*>(col.dst) + (o0 + uint64_t(it) * kThreads) * uint64_t(w), w);
+  }
+}
+
+// Output-space load-balanced expansion. Each CTA owns kTile consecutive
+// output pairs; it locates its window of matched keys with two warp-parallel
+// searches and stages the window's pair offsets and per-key starts/counts in
+// shared memory. Each thread then resolves its kItems pairs in phases —
+// window search, row-id loads, column loads, stores — so the dependent
+// global reads of all its pairs overlap instead of running one pair at a time.
 template <bool kChecksum>
-__global__ void __launch_bounds__(kThreads) expand_kernel(ExpandArgs a, ColumnSet cols) {
+__global__ void __launch_bounds__(kThreads, RL_EXPAND_MIN_BLOCKS) expand_kernel(ExpandArgs a, ColumnSet cols,
+                                                                               uint32_t tiles_per_cta) {
   __shared__ uint64_t so[kTile + 1];
+  __shared__ uint32_t sls[kTile], srs[kTile], src_[kTile];
   __shared__ int64_t s_g[2];
-  const int tid = threadIdx.x;
-  const uint64_t t0 = a.out_begin + uint64_t(blockIdx.x) * kTile;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  uint64_t sum = 0;  // checksum mode
+  int64_t hint = 0;  // the next sub-tile's first key is at or after this one's last
+  for (uint32_t sub = 0; sub < tiles_per_cta; ++sub) {
+  const uint64_t t0 = a.out_begin + (uint64_t(blockIdx.x) * tiles_per_cta + sub) * kTile;
+  if (t0 >= a.out_end) break;
   const uint64_t t1 = min(t0 + kTile, a.out_end);
-  if (tid < 2) s_g[tid] = upper_bound_minus1(a.offs, a.m, tid == 0 ? t0 : t1 - 1);
+  if (warp < 2) {
+    const int64_t g = warp_last_le(a.offs, hint, a.m, warp == 0 ? t0 : t1 - 1);
+    if ((tid & 31) == 0) s_g[warp] = g;
+  }
   __syncthreads();
   const int64_t g0 = s_g[0];
-  const int nk = int(s_g[1] - g0) + 1;  // <= kTile
+  hint = s_g[1];
+  const int nk = int(s_g[1] - g0) + 1;  // <= kTile: every matched key owns >= 1 pair
   for (int i = tid; i <= nk; i += kThreads) so[i] = a.offs[g0 + i];
+  for (int i = tid; i < nk; i += kThreads) {
+    sls[i] = __ldg(a.ls + g0 + i);
+    srs[i] = __ldg(a.rs + g0 + i);
+    src_[i] = __ldg(a.rc + g0 + i);
+  }
   __syncthreads();
 
-  uint64_t sum = 0;
-#pragma unroll 2
+  // phase 1: window slot of each pair (binary search in shared memory)
+  uint32_t kk[kItems], lrow[kItems], rrow[kItems];
+  const uint64_t o0 = t0 + tid - a.out_begin;  // output index of item 0; item it is o0 + it * kThreads
+  uint32_t valid = 0;
+#pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const uint64_t t = t0 + uint64_t(it) * kThreads + tid;
-    if (t >= t1) break;
-    // binary search in the staged window: last k with so[k] <= t
-    int lo = 0, len = nk;
-    while (len > 0) {
-      const int half = len >> 1;
-      if (so[lo + half] <= t) {
-        lo += half + 1;
-        len -= half + 1;
-      } else {
-        len = half;
+    kk[it] = 0;
+    if (t < t1) {
+      valid |= 1u << it;
+      if (nk == 1) continue;
+      int lo = 0, len = nk;
+      while (len > 0) {
+        const int half = len >> 1;
+        if (so[lo + half + 1] <= t) {
+          lo += half + 1;
+          len -= half + 1;
+        } else {
+          len = half;
+        }
+      }
+      kk[it] = uint32_t(lo);
+    }
+  }
+  // phase 2: divmod by the right count, then the two row-id loads of every pair
+  if (nk == 1) {
+    // the whole tile lies inside one (heavy) key: one division, then step the
+    // (li, ri) pair by kThreads outputs per item without dividing again
+    const uint32_t c = src_[0];
+    const uint64_t local0 = t0 + tid - so[0];
+    uint64_t li = local0 / c;
+    uint32_t ri = uint32_t(local0 - li * c);
+    const uint32_t q = uint32_t(kThreads) / c, r = uint32_t(kThreads) % c;
+    const uint32_t* lp = a.lpos + sls[0];
+    const uint32_t* rp = a.rpos + srs[0];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      if (valid & (1u << it)) {
+        lrow[it] = __ldg(lp + li);
+        rrow[it] = __ldg(rp + ri);
+      }
+      li += q;
+      ri += r;
+      if (ri >= c) {
+        ri -= c;
+        ++li;
       }
     }
-    const int k = lo - 1;
-    const int64_t g = g0 + k;
-    const uint64_t local = t - so[k];
-    const uint32_t c = __ldg(a.rc + g);
-    uint64_t li, ri;
-    if (local < (1ull << 32)) {
-      const uint32_t l32 = uint32_t(local);
-      li = l32 / c;
-      ri = l32 - uint32_t(li) * c;
-    } else {
-      li = local / c;
-      ri = local - li * c;
-    }
-    const uint32_t lrow = __ldg(a.lpos + __ldg(a.ls + g) + li);
-    const uint32_t rrow = __ldg(a.rpos + __ldg(a.rs + g) + ri);
-    if (kChecksum) {
-      sum += fmix64((uint64_t(lrow) << 32) | rrow);
-      continue;
-    }
-    const uint64_t o = t - a.out_begin;
-    if (a.lrows_out) __stcs(a.lrows_out + o, lrow);
-    if (a.rrows_out) __stcs(a.rrows_out + o, rrow);
-    for (int ci = 0; ci < cols.n; ++ci) {
-      const rl_column& col = cols.c[ci];
-      const int w = col.width;
-      uint8_t* dst = static_cast<uint8_t*>(col.dst) + o * uint64_t(w);
-      if (col.side == RL_SIDE_KEY) {
-        __stcs(reinterpret_cast<long long*>(dst), (long long)__ldg(reinterpret_cast<const long long*>(a.matched_keys) + g));
+  } else {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      if (!(valid & (1u << it))) continue;
+      const uint32_t k = kk[it];
+      const uint64_t local = t0 + uint64_t(it) * kThreads + tid - so[k];
+      const uint32_t c = src_[k];
+      uint64_t li, ri;
+      if (local < (1ull << 32)) {
+        const uint32_t l32 = uint32_t(local);
+        li = l32 / c;
+        ri = l32 - uint32_t(li) * c;
       } else {
-        const uint64_t row = col.side == RL_SIDE_LEFT ? lrow : rrow;
-        copy_row(static_cast<const uint8_t*>(col.src) + row * uint64_t(w), dst, w);
+        li = local / c;
+        ri = local - li * c;
       }
+      lrow[it] = __ldg(a.lpos + sls[k] + li);
+      rrow[it] = __ldg(a.rpos + srs[k] + ri);
     }
   }
   if (kChecksum) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int it = 0; it < kItems; ++it)
+      if (valid & (1u << it)) sum += fmix64((uint64_t(lrow[it]) << 32) | rrow[it]);
+    __syncthreads();  // the staged window is rewritten by the next sub-tile
+    continue;
+  }
+  // phase 3: pair outputs and column gathers (loads of a column batched)
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    if (!(valid & (1u << it))) continue;
+    if (a.lrows_out) __stcs(a.lrows_out + o0 + it * kThreads, lrow[it]);
+    if (a.rrows_out) __stcs(a.rrows_out + o0 + it * kThreads, rrow[it]);
+  }
+  for (int ci = 0; ci < cols.n; ++ci) {
+    const rl_column& col = cols.c[ci];
+    const int w = col.width;
+    if (col.side == RL_SIDE_KEY) {
+#pragma unroll
+      for (int it = 0; it < kItems; ++it)
+        if (valid & (1u << it))
+          __stcs(reinterpret_cast<long long*>(col.dst) + o0 + it * kThreads,
+                 (long long)__ldg(reinterpret_cast<const long long*>(a.matched_keys) + g0 + kk[it]));
+      continue;
+    }
+    if (col.side == RL_SIDE_LEFT) gather_column(col, lrow, o0, valid);
+    else gather_column(col, rrow, o0, valid);
+  }
+  __syncthreads();  // the staged window is rewritten by the next sub-tile
+  }
+  if (kChecksum) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
     if ((tid & 31) == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(a.checksum), (unsigned long long)sum);
   }
+}
+// One CTA per output tile while that fills ~8 CTAs per SM; beyond, each CTA
+// walks a contiguous run of tiles (the key-window search then continues
+// from where the previous tile ended instead of starting over).
+static unsigned expand_grid(uint64_t outputs, uint32_t* per_cta) {
+  const uint64_t tiles = (outputs + kTile - 1) / kTile;
+  const uint64_t target = uint64_t(device_sm_count()) * 8;
+  uint64_t per = tiles <= target ? 1 : (tiles + target - 1) / target;
+  *per_cta = uint32_t(per);
+  return unsigned((tiles + per - 1) / per);
 }
 
 static int fill_columns(ColumnSet& cs, const rl_column* columns, int n_columns, bool allow_key) {
@@ -160,9 +290,9 @@ int join_expand(const int64_t* matched_keys, const uint32_t* ls, const uint32_t*
   if (out_end == out_begin) return RL_OK;
   if (m == 0) return RL_ERR_BAD_ARG;
   ExpandArgs a{matched_keys, ls, rs, rc, offs, m, lpos, rpos, out_begin, out_end, lrows_out, rrows_out, nullptr};
-  const uint64_t blocks = (out_end - out_begin + kTile - 1) / kTile;
-  if (blocks > 0x7fffffffull) return RL_ERR_BAD_ARG;
-  expand_kernel<false><<<unsigned(blocks), kThreads, 0, stream>>>(a, cs);
+  uint32_t per_cta;
+  const unsigned blocks = expand_grid(out_end - out_begin, &per_cta);
+  expand_kernel<false><<<blocks, kThreads, 0, stream>>>(a, cs, per_cta);
   count_launches(1);
   return rl_cuda_status(cudaGetLastError());
 }
@@ -176,9 +306,9 @@ int pair_checksum(const uint32_t* ls, const uint32_t* rs, const uint32_t* rc, co
   ExpandArgs a{nullptr, ls, rs, rc, offs, m, lpos, rpos, out_begin, out_end, nullptr, nullptr, sum_out};
   ColumnSet cs;
   cs.n = 0;
-  const uint64_t blocks = (out_end - out_begin + kTile - 1) / kTile;
-  if (blocks > 0x7fffffffull) return RL_ERR_BAD_ARG;
-  expand_kernel<true><<<unsigned(blocks), kThreads, 0, stream>>>(a, cs);
+  uint32_t per_cta;
+  const unsigned blocks = expand_grid(out_end - out_begin, &per_cta);
+  expand_kernel<true><<<blocks, kThreads, 0, stream>>>(a, cs, per_cta);
   count_launches(1);
   return rl_cuda_status(cudaGetLastError());
 }

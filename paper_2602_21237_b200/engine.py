@@ -350,3 +350,43 @@ def multiset_digest(columns: Sequence[torch.Tensor]) -> int:
     C.check(lib.rl_multiset_digest(arr, ncols, n, _ptr(out), stream_handle()), "rl_multiset_digest")
     hi, lo = (int(v) & (2**64 - 1) for v in fetch_scalars(out))
     return (hi << 64) | lo
+
+
+class JoinPlanDev:
+    """rl_join_plan_build result: both key axes indexed and aligned inside
+    one workspace (device pointers in ``plan``), totals fetched once."""
+
+    def __init__(self, left_keys: torch.Tensor, right_keys: torch.Tensor):
+        lib = C.load()
+        lk, rk = aligned16(left_keys), aligned16(right_keys)
+        nl, nr = lk.numel(), rk.numel()
+        self.ws = workspace(lib.rl_join_plan_workspace_bytes(nl, nr), lk.device)
+        self.plan = C.RlJoinPlan()
+        C.check(lib.rl_join_plan_build(_ptr(lk), nl, _ptr(rk), nr, _ptr(self.ws), self.ws.numel(),
+                                       ctypes.byref(self.plan), stream_handle()), "rl_join_plan_build")
+        self.n_left, self.n_right = nl, nr
+        # one pinned D2H of the device scalars (D_left, D_right, M, total) + one sync
+        off = self.plan.scalars - self.ws.data_ptr()
+        host = torch.empty(4, dtype=torch.int64, pin_memory=True)
+        host.view(torch.uint8).copy_(self.ws[off : off + 32], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self.d_left, self.d_right, self.matched_keys, self.total = host.tolist()
+
+    def expand(self, out_begin: int, out_end: int, columns: Sequence[OutColumn] = (),
+               left_rows: Optional[torch.Tensor] = None, right_rows: Optional[torch.Tensor] = None) -> None:
+        lib = C.load()
+        p = self.plan
+        arr, ncols = C.columns_array(
+            (None if c.src is None else c.src.data_ptr(), c.dst.data_ptr(), c.width, c.side) for c in columns
+        )
+        C.check(lib.rl_join_expand(p.matched_keys, p.left_starts, p.right_starts, p.right_counts, p.pair_offsets,
+                                   self.matched_keys, p.left_positions, p.right_positions, out_begin, out_end,
+                                   _ptr(left_rows), _ptr(right_rows), arr, ncols, stream_handle()),
+                "rl_join_expand")
+
+    def pair_checksum(self, out_begin: int, out_end: int, acc: torch.Tensor) -> None:
+        lib = C.load()
+        p = self.plan
+        C.check(lib.rl_join_pair_checksum(p.left_starts, p.right_starts, p.right_counts, p.pair_offsets,
+                                          self.matched_keys, p.left_positions, p.right_positions, out_begin,
+                                          out_end, _ptr(acc), stream_handle()), "rl_join_pair_checksum")

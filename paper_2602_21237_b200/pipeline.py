@@ -76,23 +76,13 @@ def _width(col: torch.Tensor) -> int:
     return col.element_size() * (col.shape[1] if col.dim() > 1 else 1)
 
 
-@dataclass
-class JoinPlan:
-    """Both key axes indexed and aligned, totals known on the host."""
-
-    left: engine.KeyIndex
-    right: engine.KeyIndex
-    alignment: engine.Alignment
-    matched_keys: int
-    total: int
+JoinPlan = engine.JoinPlanDev
 
 
 def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor) -> JoinPlan:
-    """to_tensor x2 + key_axis_align + sizing; one host sync (the totals)."""
-    li, ri = engine.index_keys(left_keys), engine.index_keys(right_keys)
-    al = engine.align(li, ri)
-    m, total = engine.fetch_scalars(al.m_total)
-    return JoinPlan(li, ri, al, m, total)
+    """to_tensor x2 + key_axis_align + sizing in one C call over one
+    workspace (rl_join_plan_build); one host sync (the totals)."""
+    return engine.JoinPlanDev(left_keys, right_keys)
 
 
 def join(left: DeviceRelation, right: DeviceRelation, key: str,
@@ -107,7 +97,7 @@ def join(left: DeviceRelation, right: DeviceRelation, key: str,
         raise OutputTooLarge(f"join would produce {plan.total} rows (cap {max_output_rows})")
     cols = join_out_columns(left.columns, lk, right.columns, rk, plan.total)
     if plan.total:
-        engine.expand(plan.alignment, plan.matched_keys, plan.left, plan.right, 0, plan.total, cols)
+        plan.expand(0, plan.total, cols)
     return DeviceRelation(out_schema, [c.dst for c in cols])
 
 
@@ -167,13 +157,13 @@ def join_stream(plan: JoinPlan, chunk_pairs: int = 1 << 31, begin: int = 0,
     end = plan.total if end is None else min(end, plan.total)
     if end <= begin:
         return
-    dev = plan.left.positions.device
+    dev = plan.ws.device
     cap = min(chunk_pairs, end - begin)
     lr = torch.empty(cap, dtype=torch.int32, device=dev)
     rr = torch.empty(cap, dtype=torch.int32, device=dev)
     for a in range(begin, end, chunk_pairs):
         b = min(a + chunk_pairs, end)
-        engine.expand(plan.alignment, plan.matched_keys, plan.left, plan.right, a, b, (), lr[: b - a], rr[: b - a])
+        plan.expand(a, b, (), lr[: b - a], rr[: b - a])
         yield a, lr[: b - a], rr[: b - a]
 
 
@@ -182,9 +172,7 @@ def pair_checksum(plan: JoinPlan, begin: int = 0, end: Optional[int] = None) -> 
     without materialising them (order-independent; the oracle's
     pair_checksum restricted to the same range agrees)."""
     end = plan.total if end is None else min(end, plan.total)
-    acc = torch.zeros(1, dtype=torch.int64, device=plan.left.positions.device)
+    acc = torch.zeros(1, dtype=torch.int64, device=plan.ws.device)
     if end > begin:
-        step = 1 << 40  # grid-size bound of one launch (2048 pairs per CTA)
-        for a in range(begin, end, step):
-            engine.pair_checksum(plan.alignment, plan.matched_keys, plan.left, plan.right, a, min(a + step, end), acc)
+        plan.pair_checksum(begin, end, acc)
     return int(engine.fetch_scalars(acc)[0]) & (2**64 - 1)

@@ -514,7 +514,16 @@ def extras(args, dev):
         b.record()
         b.synchronize()
         ms = a.elapsed_time(b)
+        acc = torch.zeros(1, dtype=torch.int64, device=dev)
+        a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a2.record()
+        plan.pair_checksum(0, plan.total, acc)
+        b2.record()
+        b2.synchronize()
+        full_ms = a2.elapsed_time(b2)
         out["cfg3_n1e7"] = {"total_pairs": plan.total, "count_p50_ms": round(percentile(ts, 50), 3),
+                            "full_checksum_s": round(full_ms / 1e3, 3),
+                            "full_checksum_pairs_per_s": round(plan.total / (full_ms / 1e3), 0),
                             "stream_pairs_per_s": round(streamed / (ms / 1e3), 0),
                             "stream_sample_pairs": streamed,
                             "stream_write_gbs": round(streamed * 8 / (ms / 1e3) / 1e9, 1),

@@ -124,6 +124,66 @@ __global__ void __launch_bounds__(kThreads, RL_EXPAND_MIN_BLOCKS) expand_kernel(
   const int tid = threadIdx.x, warp = tid >> 5;
   uint64_t sum = 0;  // checksum mode
   int64_t hint = 0;  // the next sub-tile's first key is at or after this one's last
+
+  // ---- streaming mode: the CTA's whole output range is covered by few heavy
+  // keys (>= 1024 pairs per key on average, e.g. the Zipf head of BASELINE
+  // cfg3). Each key's block of lc x rc pairs is walked with a
+  // division-free (li, ri) stride, no shared-memory staging, no barriers.
+  {
+    const uint64_t c0 = a.out_begin + uint64_t(blockIdx.x) * tiles_per_cta * kTile;
+    const uint64_t c1 = min(c0 + uint64_t(tiles_per_cta) * kTile, a.out_end);
+    if (warp < 2) {
+      const int64_t g = warp_last_le(a.offs, 0, a.m, warp == 0 ? c0 : c1 - 1);
+      if ((tid & 31) == 0) s_g[warp] = g;
+    }
+    __syncthreads();
+    const int64_t ga = s_g[0], gb = s_g[1];
+    hint = ga;
+    if (uint64_t(gb - ga + 1) * kTile <= c1 - c0) {
+      for (int64_t g = ga; g <= gb; ++g) {
+        const uint64_t kbeg = __ldg(reinterpret_cast<const unsigned long long*>(a.offs) + g);
+        const uint64_t kend = __ldg(reinterpret_cast<const unsigned long long*>(a.offs) + g + 1);
+        const uint64_t s0 = max(kbeg, c0), s1 = min(kend, c1);
+        const uint32_t c = __ldg(a.rc + g);
+        const uint32_t* lp = a.lpos + __ldg(a.ls + g);
+        const uint32_t* rp = a.rpos + __ldg(a.rs + g);
+        const uint64_t t = s0 + tid;
+        if (t >= s1) continue;
+        const uint64_t local = t - kbeg;
+        uint64_t li = local / c;
+        uint32_t ri = uint32_t(local - li * c);
+        const uint32_t q = uint32_t(kThreads) / c, r = uint32_t(kThreads) % c;
+        for (uint64_t u = t; u < s1; u += kThreads) {
+          const uint32_t lrow = __ldg(lp + li), rrow = __ldg(rp + ri);
+          if (kChecksum) {
+            sum += fmix64((uint64_t(lrow) << 32) | rrow);
+          } else {
+            const uint64_t o = u - a.out_begin;
+            if (a.lrows_out) __stcs(a.lrows_out + o, lrow);
+            if (a.rrows_out) __stcs(a.rrows_out + o, rrow);
+            for (int ci = 0; ci < cols.n; ++ci) {
+              const rl_column& col = cols.c[ci];
+              const int w = col.width;
+              uint8_t* dst = static_cast<uint8_t*>(col.dst) + o * uint64_t(w);
+              if (col.side == RL_SIDE_KEY)
+                __stcs(reinterpret_cast<long long*>(dst), (long long)__ldg(reinterpret_cast<const long long*>(a.matched_keys) + g));
+              else
+                copy_row(static_cast<const uint8_t*>(col.src) + uint64_t(col.side == RL_SIDE_LEFT ? lrow : rrow) * w, dst, w);
+            }
+          }
+          li += q;
+          ri += r;
+          if (ri >= c) {
+            ri -= c;
+            ++li;
+          }
+        }
+      }
+      tiles_per_cta = 0;  // skip the tile loop
+    }
+    __syncthreads();
+  }
+
   for (uint32_t sub = 0; sub < tiles_per_cta; ++sub) {
   const uint64_t t0 = a.out_begin + (uint64_t(blockIdx.x) * tiles_per_cta + sub) * kTile;
   if (t0 >= a.out_end) break;

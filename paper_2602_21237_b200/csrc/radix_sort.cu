@@ -33,12 +33,25 @@
 //         round trip), and the staged tile is written out so every digit run
 //         is a contiguous burst.
 //
+// Wide-key hybrid (raw int64 keys, n >= 2^18): when the top 16 key bits
+// spread the input into sub-buckets that fit on chip, the sort runs only
+// two onesweep passes — digit 6 then digit 7, i.e. stably by the top 16
+// bits — and the last of them also counts the 65536 (d7, d6) sub-bucket
+// sizes. One local phase then sorts every sub-bucket in shared memory
+// (stable 8-bit partition on its top varying byte, then insertion /
+// bitonic sorts of the few equal-digit rows by (key, row id)) and writes
+// the final keys, permutation and fused gathers. 2 + 1 passes over HBM
+// instead of 8. A sub-bucket larger than kLocalCap (skewed top bits) is
+// detected on the device after the two passes and the sort falls back
+// to the LSD kernel, launched behind it, which otherwise exits at once.
+//
 // Key transform (self-inverse): int64 ascending  u = x ^ 2^63;
 // descending u = ~x ^ 2^63 (the reference's np.invert, tensorpath.py:215,
 // keeps ties in ascending row order). Bytes words are built big-endian
 // from (complemented when descending) bytes, zero padded
 // (tensorpath.py:220-225).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -71,11 +84,18 @@ constexpr int kLookback = RL_LOOKBACK_WINDOW;
 #endif
 constexpr int kHistUnroll = RL_HIST_UNROLL;
 constexpr int kStamps = 2 + kPasses + 1;  // per-phase globaltimer stamps (profiling)
+// wide-key hybrid
+constexpr int kLocalCap = 3840;            // rows of one on-chip local load (24 B each: two key/id buffers)
+constexpr int kSubBuckets = 1 << 16;       // (d7, d6) sub-buckets
+constexpr int kGroupSubs = 16;             // sub-buckets claimed per local work item
+constexpr int64_t kHybridMinRows = 1 << 18;
+constexpr uint32_t kHybridEpoch = kPasses; // LSD after a hybrid fallback publishes epoch PASS + 1 + 8
 
 static_assert(kThreads == kBins, "tile scan maps one digit per thread");
 static_assert(kStamps == RL_SORT_STAMPS, "stamp layout is part of the ABI");
 
 enum KeyMode : int { kRawAsc = 0, kRawDesc = 1, kMaterialized = 2 };
+enum SortMode : int { kModeLsd = 0, kModeHybrid = 1 };  // hybrid: try the wide-key path first
 enum SrcMode : int { kSrcInt64 = 0, kSrcInt64Gather = 1, kSrcBytes = 2, kSrcWords = 3 };
 
 __device__ __forceinline__ uint64_t xform(uint64_t x, int desc) {
@@ -125,10 +145,13 @@ struct SortArgs {
   uint32_t* vals_b;
   int64_t* out_keys;         // final sorted int64 keys (optional, raw modes)
   uint32_t* out_vals;        // final permutation
+  int mode;                  // SortMode
   // zeroed per call
   uint32_t* ghist;           // [kPasses][kBins]
-  uint32_t* tile_counter;    // [kPasses]
+  uint32_t* tile_counter;    // [2][kPasses] (first attempt, LSD after a hybrid fallback)
   uint32_t* grid_bar;        // grid barrier arrivals
+  uint32_t* flags;           // [0] a sub-bucket exceeds kLocalCap -> LSD fallback, [1] local work-item counter
+  uint32_t* sub_off;         // [kSubBuckets + 1] sub-bucket starts, hybrid (not zeroed)
   uint64_t* status;          // [num_tiles][kBins] look-back words (epoch = pass + 1)
   unsigned long long* stamps;  // optional [kStamps] globaltimer ns (device)
   // columns gathered by the final permutation inside the last pass
@@ -176,7 +199,21 @@ constexpr size_t kBufBytes = size_t(kTile) * 12;  // keys (8 B) then row ids (4 
 constexpr size_t kBarOffset = 2 * kBufBytes + size_t(kWarps) * kBins * 4 * 2 + size_t(kBins) * 4 + 64 * 4;
 constexpr size_t kPassSmemBytes = kBarOffset + 64;
 // + the plan kept for the whole kernel: global digit bases [kPasses][kBins] + flags
-constexpr size_t kSmemBytes = kPassSmemBytes + size_t(kPasses) * kBins * 4 + 64;
+// ---------------------------------------------------------------- hybrid
+// Shared memory of the local phase (reuses the pass buffers): load buffer
+// A, scattered buffer B, the (sub-bucket, d5) bin counters/cursors, the
+// list of bins too long for a one-thread fix-up, and scalars.
+constexpr int kLocalBins = kGroupSubs * kBins;  // (top16 - first of group, d5)
+constexpr int kBigList = 256;
+constexpr size_t kLocAk = 0;
+constexpr size_t kLocAv = kLocAk + size_t(kLocalCap) * 8;
+constexpr size_t kLocBk = kLocAv + size_t(kLocalCap) * 4;
+constexpr size_t kLocBv = kLocBk + size_t(kLocalCap) * 8;
+constexpr size_t kLocHist = kLocBv + size_t(kLocalCap) * 4;
+constexpr size_t kLocBig = kLocHist + size_t(kLocalBins) * 4;
+constexpr size_t kLocMisc = kLocBig + size_t(kBigList) * 4;
+constexpr size_t kLocalSmemBytes = kLocMisc + 64 * 4;  // misc: [0] claim, [1] big count, [8..] group starts, [32..] scan
+constexpr size_t kSmemBytes = std::max(kPassSmemBytes + size_t(kPasses) * kBins * 4 + 64, kLocalSmemBytes);
 
 struct PassState {  // per-CTA mbarrier phase parities, carried across passes
   uint32_t phase0, phase1;
@@ -245,11 +282,17 @@ __device__ __forceinline__ void prefetch_tile(int64_t n, const uint64_t* kin, co
 // processes tile i. Progress: the smallest unfinished tile's predecessors
 // are all finished, and it is either being processed or queued behind a
 // smaller tile of the same CTA.
-template <int PASS>
+//
+// SUBOFF (the hybrid's digit-7 pass, whose input is ordered by digit 6):
+// a tile holding the first rows of digit-6 values c in (lo, hi] writes
+// every sub-bucket start (d7, c) = d7's base + its look-back prefix + the
+// rows of d7 in this tile with d6 < c (a binary search in the staged run,
+// which keeps input order, i.e. d6 order). No extra pass over the data.
+template <int PASS, bool SUBOFF = false>
 __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint32_t src, uint32_t dst,
-                                      const uint32_t* bin_off, PassState& ps) {
+                                      const uint32_t* bin_off, PassState& ps, const uint32_t kEpoch,
+                                      uint32_t* tile_counter) {
   constexpr int kShift = PASS * kBits;
-  constexpr uint32_t kEpoch = PASS + 1;
   uint8_t* bufs = smem;
   uint32_t* whist = reinterpret_cast<uint32_t*>(smem + 2 * kBufBytes);
   uint32_t* wmatch = whist + kWarps * kBins;
@@ -266,7 +309,7 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
 
   for (int i = tid; i < 2 * kWarps * kBins; i += kThreads) whist[i] = 0;  // whist + wmatch
   if (tid == 0) {
-    const uint32_t t = atomicAdd(&a.tile_counter[PASS], 1u);
+    const uint32_t t = atomicAdd(&tile_counter[PASS], 1u);
     misc[0] = t;
     if (t < num_tiles) {
       fence_proxy_async_smem();  // buffer 0 was last written by generic stores
@@ -284,7 +327,7 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
     uint64_t* skeys = reinterpret_cast<uint64_t*>(buf);
     uint32_t* svals = reinterpret_cast<uint32_t*>(buf + size_t(kTile) * 8);
     if (tid == 0) {  // claim + prefetch the next tile into the other buffer
-      const uint32_t nt = atomicAdd(&a.tile_counter[PASS], 1u);
+      const uint32_t nt = atomicAdd(&tile_counter[PASS], 1u);
       misc[cb ^ 1] = nt;  // slot cb^1: its previous value was read before the last barrier
       if (nt < num_tiles) {
         fence_proxy_async_smem();
@@ -294,6 +337,8 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
     const int64_t tile_begin = int64_t(tile) * kTile;
     const int64_t left = a.n - tile_begin;
     const uint32_t count = left < kTile ? uint32_t(left) : uint32_t(kTile);
+    uint64_t before = 0;  // SUBOFF: the row ahead of this tile
+    if (SUBOFF && tid == 0 && tile_begin > 0) before = __ldcg(reinterpret_cast<const unsigned long long*>(kin) + tile_begin - 1);
     mbar_wait(&bars[cb], cb ? ps.phase1 : ps.phase0);
     if (cb) ps.phase1 ^= 1;
     else ps.phase0 ^= 1;
@@ -307,6 +352,11 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
       __syncthreads();
     }
 
+    if (SUBOFF && tid == 0) {  // d6 range of this tile's rows: (lo, hi]
+      const uint64_t last = skeys[count - 1];
+      misc[16] = tile_begin > 0 ? uint32_t((xf ? xform(before, desc_in) : before) >> 48) & (kBins - 1u) : 0xFFFFFFFFu;
+      misc[17] = uint32_t((xf ? xform(last, desc_in) : last) >> 48) & (kBins - 1u);
+    }
     // ---- keys + row ids into registers (warp-striped; conflict-free 8-byte reads)
     uint64_t k[kItems];
     uint32_t v[kItems];
@@ -401,6 +451,27 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
     gbase[tid] = bin_off[PASS * kBins + tid] + uint32_t(excl) - ls;
     __syncthreads();  // every warp is past its ranking: whist may be reset
     for (int i = tid; i < kWarps * kBins; i += kThreads) whist[i] = 0;  // for the next tile
+    if constexpr (SUBOFF) {
+      const int lo = int(misc[16]), hi = int(misc[17]);  // lo = -1 (0xFFFFFFFF) for tile 0
+      const bool last_tile = tile == num_tiles - 1;
+      if (hi > lo || last_tile) {
+        const uint32_t base7 = bin_off[PASS * kBins + tid] + uint32_t(excl);
+        const uint32_t row = uint32_t(tid) << kBits;
+        for (int c = lo + 1; c <= hi; ++c) {
+          uint32_t l = ls, r = ls + run;
+          while (l < r) {
+            const uint32_t m = (l + r) >> 1;
+            if (int(uint32_t(skeys[m] >> 48) & (kBins - 1)) < c) l = m + 1;
+            else r = m;
+          }
+          a.sub_off[row | uint32_t(c)] = base7 + (l - ls);
+        }
+        if (last_tile) {
+          for (int c = hi + 1; c < kBins; ++c) a.sub_off[row | uint32_t(c)] = base7 + run;
+          if (tid == 0) a.sub_off[kSubBuckets] = uint32_t(a.n);
+        }
+      }
+    }
 
     // ---- write the staged tile: consecutive threads → consecutive slots
     if (dst == 3) {
@@ -470,12 +541,223 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
   }
 }
 
+__device__ __forceinline__ bool row_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+  return ka < kb || (ka == kb && va < vb);
+}
+
+// Sort rows [lo, hi) of B by (key, row id) — one warp, bitonic network
+// with mirrored first steps (every comparator ascending), so rows past hi
+// act as +inf padding and their comparators are skipped.
+__device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t hi, int lane) {
+  const uint32_t sz = hi - lo;
+  uint32_t p2 = 1;
+  while (p2 < sz) p2 <<= 1;
+  for (uint32_t k = 2; k <= p2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = lane; t < (p2 >> 1); t += 32) {
+        const uint32_t i = (t / j) * (2 * j) + (t % j);
+        const uint32_t q = j == (k >> 1) ? (i ^ (k - 1)) : (i + j);
+        if (q < sz) {
+          const uint64_t ka = bk[lo + i], kb = bk[lo + q];
+          const uint32_t va = bv[lo + i], vb = bv[lo + q];
+          if (row_less(kb, vb, ka, va)) {
+            bk[lo + i] = kb; bk[lo + q] = ka;
+            bv[lo + i] = vb; bv[lo + q] = va;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// The local phase: CTAs claim groups of kGroupSubs consecutive sub-buckets
+// and load them in runs of whole sub-buckets of at most kLocalCap rows.
+// A run is sorted on chip by (top16, d5) with a counting scatter (one
+// shared atomic per row: the order inside a bin is settled next), then
+// each row takes its rank by (key, row id) inside its bin — rows equal in
+// their top 24 bits, ~1 for uniform keys; a warp's bitonic network for
+// bins above 32 rows — and goes straight to its final position in the
+// outputs, with the fused gathers.
+__device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
+  uint64_t* ak = reinterpret_cast<uint64_t*>(smem + kLocAk);
+  uint32_t* av = reinterpret_cast<uint32_t*>(smem + kLocAv);
+  uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
+  uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kLocHist);
+  uint32_t* big = reinterpret_cast<uint32_t*>(smem + kLocBig);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t* kin = src == 1 ? a.keys_a : a.keys_b;
+  const uint32_t* vin = src == 1 ? a.vals_a : a.vals_b;
+  constexpr uint32_t kGroups = kSubBuckets / kGroupSubs;
+  constexpr int kPerThread = kLocalBins / kThreads;  // consecutive bins per thread in scan / fix-up
+  while (true) {
+    __syncthreads();  // previous group's reads of misc are done
+    if (tid == 0) misc[0] = atomicAdd(&a.flags[1], 1u);
+    __syncthreads();
+    const uint32_t g = misc[0];
+    if (g >= kGroups) break;
+    if (tid <= kGroupSubs) misc[8 + tid] = __ldcg(a.sub_off + g * kGroupSubs + tid);
+    __syncthreads();
+    const uint32_t top0 = g * kGroupSubs;
+    uint32_t s = 0;
+    while (s < kGroupSubs) {
+      const uint32_t base = misc[8 + s];
+      uint32_t e = s + 1;
+      while (e < kGroupSubs && misc[8 + e + 1] - base <= uint32_t(kLocalCap)) ++e;
+      const uint32_t cnt = misc[8 + e] - base;
+      if (cnt == 0) {
+        s = e;
+        continue;
+      }
+      for (int i = tid; i < kLocalBins; i += kThreads) hist[i] = 0;
+      if (tid == 0) misc[1] = 0;
+      {  // all of the run's loads in flight at once
+        constexpr int kLoads = (kLocalCap + kThreads - 1) / kThreads;
+        uint64_t lk[kLoads];
+        uint32_t lv[kLoads];
+#pragma unroll
+        for (int u = 0; u < kLoads; ++u) {
+          const uint32_t j = uint32_t(u * kThreads + tid);
+          if (j < cnt) {
+            lk[u] = __ldcg(reinterpret_cast<const unsigned long long*>(kin) + base + j);
+            lv[u] = __ldcg(vin + base + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kLoads; ++u) {
+          const uint32_t j = uint32_t(u * kThreads + tid);
+          if (j < cnt) {
+            ak[j] = lk[u];
+            av[j] = lv[u];
+          }
+        }
+      }
+      __syncthreads();
+      for (uint32_t j = tid; j < cnt; j += kThreads) {
+        const uint64_t k = ak[j];
+        atomicAdd(&hist[((uint32_t(k >> 48) - top0) << kBits) | (uint32_t(k >> 40) & (kBins - 1))], 1u);
+      }
+      __syncthreads();
+      {  // exclusive scan: thread owns bins [kPerThread tid, kPerThread (tid + 1))
+        uint32_t c[kPerThread], run = 0;
+#pragma unroll
+        for (int i = 0; i < kPerThread; ++i) {
+          c[i] = hist[tid * kPerThread + i];
+          run += c[i];
+        }
+        uint32_t total;
+        uint32_t start = block_exclusive_scan<kThreads>(run, misc + 32, &total);
+#pragma unroll
+        for (int i = 0; i < kPerThread; ++i) {
+          hist[tid * kPerThread + i] = start;
+          start += c[i];
+        }
+      }
+      __syncthreads();
+      for (uint32_t j = tid; j < cnt; j += kThreads) {
+        const uint64_t k = ak[j];
+        const uint32_t pos =
+            atomicAdd(&hist[((uint32_t(k >> 48) - top0) << kBits) | (uint32_t(k >> 40) & (kBins - 1))], 1u);
+        bk[pos] = k;
+        bv[pos] = av[j];
+      }
+      __syncthreads();
+      // hist[b] is now the end of bin b; a bin holds the rows equal in their
+      // top 24 bits (~1 for uniform keys). Every row finds its rank by
+      // (key, row id) among its bin's rows and is written straight to its
+      // final position; bins above kRankMax rows are sorted by a warp first.
+      constexpr uint32_t kRankMax = 32;
+      const int desc = a.key_mode == kRawDesc;
+      auto bin_of = [&](uint64_t k) {
+        return int(((uint32_t(k >> 48) - top0) << kBits) | (uint32_t(k >> 40) & (kBins - 1)));
+      };
+      for (uint32_t p = tid; p < cnt; p += kThreads) {
+        const uint64_t k = bk[p];
+        const uint32_t v = bv[p];
+        const int b = bin_of(k);
+        const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+        uint32_t pos = p;
+        if (b1 - b0 > kRankMax) {
+          if (p == b0) {
+            const uint32_t slot = atomicAdd(&misc[1], 1u);
+            if (slot < kBigList) big[slot] = uint32_t(b);
+          }
+          continue;
+        }
+        if (b1 - b0 > 1) {
+          uint32_t r = 0;
+          for (uint32_t i = b0; i < b1; ++i) r += row_less(bk[i], bv[i], k, v) ? 1u : 0u;
+          pos = b0 + r;
+        }
+        const uint64_t o = uint64_t(base) + pos;
+        if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(k, desc));
+        __stcs(a.out_vals + o, v);
+        gather_fused(a.gather, v, o);
+      }
+      __syncthreads();
+      for (uint32_t t = warp; t < min(misc[1], uint32_t(kBigList)); t += kWarps) {
+        const int b = int(big[t]);
+        const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+        warp_bitonic(bk, bv, b0, b1, lane);
+        for (uint32_t p = b0 + lane; p < b1; p += 32) {
+          const uint64_t o = uint64_t(base) + p;
+          if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(bk[p], desc));
+          __stcs(a.out_vals + o, bv[p]);
+          gather_fused(a.gather, bv[p], o);
+        }
+      }
+      s = e;
+      __syncthreads();  // A/B/hist free for the next run
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // The whole sort after the histograms: plan, every active digit pass,
-// copy-through — one cooperative launch.
+// copy-through — one cooperative launch. Hybrid (wide raw int64 keys):
+// the two top-digit passes, the boundary scan, then the local phase — or,
+// if a sub-bucket turned out larger than kLocalCap, the LSD passes from
+// the original input (fresh epochs and tile counters), in the same launch.
+__device__ void run_passes(const SortArgs& a, uint8_t* smem, const uint32_t* bin_off, const uint32_t* active,
+                           uint32_t n_active, bool to_final, bool suboff, PassState& ps, uint32_t epoch_base,
+                           uint32_t* tile_counter, uint32_t* grid_bar, uint32_t& barrier_no, uint32_t& src,
+                           bool stamper) {
+  uint32_t seen = 0;
+  src = 0;
+  for (int p = 0; p < kPasses; ++p) {
+    if (!active[p]) continue;
+    ++seen;
+    const bool last = seen == n_active;
+    const uint32_t dst = last && to_final ? 3u : (src == 1 ? 2u : 1u);
+    const uint32_t ep = epoch_base + p + 1;
+    switch (p) {
+      case 0: run_pass<0>(a, smem, src, dst, bin_off, ps, ep, tile_counter); break;
+      case 1: run_pass<1>(a, smem, src, dst, bin_off, ps, ep, tile_counter); break;
+      case 2: run_pass<2>(a, smem, src, dst, bin_off, ps, ep, tile_counter); break;
+      case 3: run_pass<3>(a, smem, src, dst, bin_off, ps, ep, tile_counter); break;
+      case 4: run_pass<4>(a, smem, src, dst, bin_off, ps, ep, tile_counter); break;
+      case 5: run_pass<5>(a, smem, src, dst, bin_off, ps, ep, tile_counter); break;
+      case 6: run_pass<6>(a, smem, src, dst, bin_off, ps, ep, tile_counter); break;
+      default:
+        if (suboff) run_pass<7, true>(a, smem, src, dst, bin_off, ps, ep, tile_counter);
+        else run_pass<7>(a, smem, src, dst, bin_off, ps, ep, tile_counter);
+        break;
+    }
+    src = dst;
+    if (!last || !to_final) grid_sync(grid_bar, ++barrier_no);  // the next phase reads what this one wrote
+    if (stamper) a.stamps[2 + p] = globaltimer();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(SortArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* bin_off = reinterpret_cast<uint32_t*>(smem + kPassSmemBytes);  // [kPasses][kBins], whole kernel
-  uint32_t* plan = bin_off + kPasses * kBins;                                // [0..7] active, [8] n_active
+  uint32_t* plan = bin_off + kPasses * kBins;  // [0..7] active, [8] n_active, [9] hybrid, [10..17] hybrid passes
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
   const int tid = threadIdx.x;
   uint32_t barrier_no = 0;
@@ -487,48 +769,92 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   // ---- plan (every CTA for itself): global digit bases + active digits
   {
     uint32_t* warp_sums = reinterpret_cast<uint32_t*>(smem);  // scratch
+    uint32_t nz = 1, mx = 1;
     for (int p = 0; p < kPasses; ++p) {
       const uint32_t c = __ldcg(a.ghist + p * kBins + tid);
       uint32_t total;
       bin_off[p * kBins + tid] = block_exclusive_scan<kThreads>(c, warp_sums, &total);
       const int full = __syncthreads_or(uint64_t(c) == uint64_t(a.n));
+      if (p >= 6) {  // spread of the top two digits (the hybrid's pre-check)
+        nz *= uint32_t(__syncthreads_count(c != 0));
+        uint32_t m = c;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((tid & 31) == 0) warp_sums[16 + (tid >> 5)] = m;
+        __syncthreads();
+        m = 0;
+        for (int w = 0; w < kWarps; ++w) m = max(m, warp_sums[16 + w]);
+        const uint64_t est = uint64_t(mx) * m / uint64_t(a.n) + 1;  // largest sub-bucket if d6, d7 independent
+        mx = p == 6 ? m : uint32_t(est > 0xFFFFFFFFull ? 0xFFFFFFFFull : est);
+        __syncthreads();
+      }
       if (tid == 0) plan[p] = full ? 0u : 1u;
     }
     if (tid == 0) {
       uint32_t na = 0;
       for (int p = 0; p < kPasses; ++p) na += plan[p];
       plan[kPasses] = na;
+      // hybrid: wide raw keys whose top two digits spread the rows into
+      // sub-buckets that fit on chip (pigeonhole + independent-digit estimate)
+      // and at least two passes to save
+      const bool hyb = a.mode == kModeHybrid && na >= 4 && (plan[6] | plan[7]) &&
+                       uint64_t(a.n) <= uint64_t(nz) * kLocalCap && mx <= uint32_t(kLocalCap) / 2;
+      plan[kPasses + 1] = hyb ? 1u : 0u;
+      for (int p = 0; p < kPasses; ++p) plan[kPasses + 2 + p] = p >= 6 ? plan[p] : 0u;
+      plan[2 * kPasses + 2] = plan[6] + plan[7];
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
     }
     __syncthreads();
   }
 
-  // ---- the active digit passes, least significant first
-  const uint32_t n_active = plan[kPasses];
   PassState ps{0, 0};
-  uint32_t src = 0, seen = 0;
-  for (int p = 0; p < kPasses; ++p) {
-    if (!plan[p]) continue;
-    ++seen;
-    const uint32_t dst = seen == n_active ? 3u : (src == 1 ? 2u : 1u);
-    switch (p) {
-      case 0: run_pass<0>(a, smem, src, dst, bin_off, ps); break;
-      case 1: run_pass<1>(a, smem, src, dst, bin_off, ps); break;
-      case 2: run_pass<2>(a, smem, src, dst, bin_off, ps); break;
-      case 3: run_pass<3>(a, smem, src, dst, bin_off, ps); break;
-      case 4: run_pass<4>(a, smem, src, dst, bin_off, ps); break;
-      case 5: run_pass<5>(a, smem, src, dst, bin_off, ps); break;
-      case 6: run_pass<6>(a, smem, src, dst, bin_off, ps); break;
-      default: run_pass<7>(a, smem, src, dst, bin_off, ps); break;
+  uint32_t src = 0;
+  if (plan[kPasses + 1]) {
+    // ---- hybrid: the two top-digit passes (stable by the top 16 bits); the
+    // digit-7 pass also writes the sub-bucket starts. With digit 7 constant
+    // (c7) the starts are digit 6's bases on row c7.
+    if (!plan[7]) {
+      uint32_t c7 = 0;
+      for (int d = 0; d < kBins; ++d)
+        if (bin_off[7 * kBins + d] == 0 && (d == kBins - 1 || bin_off[7 * kBins + d + 1] == uint32_t(a.n))) c7 = d;
+      for (uint32_t b = blockIdx.x * kThreads + tid; b <= uint32_t(kSubBuckets); b += gridDim.x * kThreads) {
+        const uint32_t d7 = b >> kBits;
+        a.sub_off[b] = b == uint32_t(kSubBuckets) || d7 > c7 ? uint32_t(a.n) : d7 < c7 ? 0u : bin_off[6 * kBins + (b & 255u)];
+      }
     }
-    src = dst;
-    if (seen < n_active) grid_sync(a.grid_bar, ++barrier_no);  // the next pass reads what this one wrote
-    if (stamper) a.stamps[2 + p] = globaltimer();
+    run_passes(a, smem, bin_off, plan + kPasses + 2, plan[2 * kPasses + 2], false, true, ps, 0u, a.tile_counter,
+               a.grid_bar, barrier_no, src, stamper);
+    {  // sub-buckets larger than the on-chip cap? (each CTA checks a slice)
+      int over = 0;
+      for (uint32_t b = blockIdx.x * kThreads + tid; b < uint32_t(kSubBuckets); b += gridDim.x * kThreads)
+        over |= __ldcg(a.sub_off + b + 1) - __ldcg(a.sub_off + b) > uint32_t(kLocalCap);
+      if (__syncthreads_or(over) && tid == 0) atomicExch(a.flags, 1u);
+    }
+    grid_sync(a.grid_bar, ++barrier_no);
+    if (stamper) a.stamps[2] = globaltimer();  // (pass 0's slot: the hybrid's sub-bucket check)
+    if (*reinterpret_cast<volatile uint32_t*>(a.flags) == 0) {
+      if (tid == 0) {
+        mbar_inval(&bars[0]);
+        mbar_inval(&bars[1]);
+      }
+      __syncthreads();
+      local_phase(a, smem, src);
+      if (stamper) a.stamps[kStamps - 1] = globaltimer();
+      return;
+    }
+    // a sub-bucket does not fit on chip: the LSD sort, fresh epochs and counters
+    if (stamper)
+      for (int p = 0; p < kPasses; ++p) a.stamps[2 + p] = 0;
   }
 
+  // ---- LSD: the active digit passes, least significant first
+  const bool fb = plan[kPasses + 1] != 0;
+  run_passes(a, smem, bin_off, plan, plan[kPasses], true, false, ps, fb ? kHybridEpoch : 0u,
+             a.tile_counter + (fb ? kPasses : 0), a.grid_bar, barrier_no, src, stamper);
+
   // ---- no active digit (all keys equal, or n == 1): copy through
-  if (n_active == 0) {
+  if (plan[kPasses] == 0) {
     for (int64_t i = int64_t(blockIdx.x) * kThreads + tid; i < a.n; i += int64_t(gridDim.x) * kThreads) {
       const uint32_t row = a.perm_in ? a.perm_in[i] : uint32_t(i);
       a.out_vals[i] = row;
@@ -543,52 +869,57 @@ struct Layout {
   uint32_t* hist;
   uint32_t* tile_counter;
   uint32_t* grid_bar;
+  uint32_t* flags;
   uint64_t* status;
-  size_t zero_bytes;  // prefix [hist, counters, barrier, status] zeroed per call
+  size_t zero_bytes;  // prefix [hist .. status] zeroed per call
+  uint32_t* sub_off;
   uint64_t* keys_a;
   uint64_t* keys_b;
   uint32_t* vals_a;
   uint32_t* vals_b;
 };
 
-template <typename C>
-static void carve(C& c, int64_t n) {
+template <typename C, typename T32, typename T64>
+static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   const size_t tiles = size_t((n + kTile - 1) / kTile);
-  c.template take<uint32_t>(kPasses * kBins);
-  c.template take<uint32_t>(kPasses);
-  c.template take<uint32_t>(1);
-  c.template take<uint64_t>(tiles * kBins);
-  c.template take<uint64_t>(size_t(n));
-  c.template take<uint64_t>(size_t(n));
-  c.template take<uint32_t>(size_t(n));
-  c.template take<uint32_t>(size_t(n));
+  auto h = t32(c, kPasses * kBins);
+  auto tc = t32(c, 2 * kPasses);
+  auto gb = t32(c, 2);
+  auto fl = t32(c, 4);
+  auto st = t64(c, tiles * kBins);
+  const size_t zero = c.used;
+  auto so = t32(c, kSubBuckets + 1);
+  auto ka = t64(c, size_t(n));
+  auto kb = t64(c, size_t(n));
+  auto va = t32(c, size_t(n));
+  auto vb = t32(c, size_t(n));
+  if (L) *L = Layout{h, tc, gb, fl, st, zero, so, ka, kb, va, vb};
 }
 
 size_t workspace_bytes(int64_t n) {
   if (n <= 0) return 256;
   CarveSize c;
-  carve(c, n);
+  carve_all(c, n, [](CarveSize& c, size_t k) { c.take<uint32_t>(k); return (uint32_t*)nullptr; },
+            [](CarveSize& c, size_t k) { c.take<uint64_t>(k); return (uint64_t*)nullptr; }, nullptr);
   return c.used + 256;
 }
 
 static bool carve_layout(Layout& L, void* ws, size_t ws_bytes, int64_t n) {
   Carve c{static_cast<char*>(ws), ws_bytes};
-  const size_t tiles = size_t((n + kTile - 1) / kTile);
-  L.hist = c.take<uint32_t>(kPasses * kBins);
-  L.tile_counter = c.take<uint32_t>(kPasses);
-  L.grid_bar = c.take<uint32_t>(1);
-  L.status = c.take<uint64_t>(tiles * kBins);
-  L.zero_bytes = c.used;
-  L.keys_a = c.take<uint64_t>(size_t(n));
-  L.keys_b = c.take<uint64_t>(size_t(n));
-  L.vals_a = c.take<uint32_t>(size_t(n));
-  L.vals_b = c.take<uint32_t>(size_t(n));
+  carve_all(c, n, [](Carve& c, size_t k) { return c.take<uint32_t>(k); },
+            [](Carve& c, size_t k) { return c.take<uint64_t>(k); }, &L);
   return c.ok;
 }
 
 __global__ void identity_kernel(const uint32_t* perm_in, int64_t n, uint32_t* out) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     out[i] = perm_in ? perm_in[i] : uint32_t(i);
+}
+
+// RL_NO_HYBRID=1 forces the LSD path (A/B measurements and tests).
+static bool getenv_flag_no_hybrid() {
+  const char* v = getenv("RL_NO_HYBRID");
+  return v && v[0] && v[0] != '0';
 }
 
 // Largest co-resident grid of the cooperative sort kernel on this device.
@@ -605,6 +936,13 @@ static int sort_grid_limit() {
   return cached;
 }
 
+static int hist_grid(int64_t n) {
+  const int64_t per_cta = int64_t(kHistThreads) * kHistUnroll * 2;
+  return int(std::max<int64_t>(1, std::min<int64_t>((n + per_cta - 1) / per_cta, int64_t(device_sm_count()) * 4)));
+}
+
+// Histograms, then the cooperative kernel (LSD, or the wide-key hybrid
+// with its in-kernel LSD fallback).
 static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* const* events) {
   const int limit = sort_grid_limit();
   if (limit < 1) {
@@ -613,16 +951,12 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   }
   cudaError_t e = cudaMemsetAsync(L.hist, 0, L.zero_bytes, stream);
   if (e != cudaSuccess) return rl_cuda_status(e);
-  // enough CTAs for the tiles (and ~8K keys each in the histogram phase), at most all co-resident
+  // enough CTAs for the tiles, at most all co-resident
   const int64_t tiles = (a.n + kTile - 1) / kTile;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(limit, tiles)));
+  a.mode = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() ? kModeHybrid : kModeLsd;
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
-  {
-    const int64_t per_cta = int64_t(kHistThreads) * kHistUnroll * 2;
-    const int hgrid = int(std::max<int64_t>(1, std::min<int64_t>((a.n + per_cta - 1) / per_cta,
-                                                                 int64_t(device_sm_count()) * 4)));
-    hist_kernel<<<hgrid, kHistThreads, 0, stream>>>(a);
-  }
+  hist_kernel<<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
   void* params[] = {&a};
   e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
@@ -683,6 +1017,8 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
   a.ghist = L.hist;
   a.tile_counter = L.tile_counter;
   a.grid_bar = L.grid_bar;
+  a.flags = L.flags;
+  a.sub_off = L.sub_off;
   a.status = L.status;
   a.stamps = stamps;
   a.gather.n = n_columns;
@@ -749,6 +1085,8 @@ static int partition_by_words(const uint64_t* words, int64_t n, int parts, uint3
   a.ghist = L.hist;
   a.tile_counter = L.tile_counter;
   a.grid_bar = L.grid_bar;
+  a.flags = L.flags;
+  a.sub_off = L.sub_off;
   a.status = L.status;
   a.stamps = nullptr;
   a.gather.n = 0;

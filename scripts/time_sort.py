@@ -38,7 +38,8 @@ def main():
         e.record()
     arr = (ctypes.c_void_p * len(evs))(*[ctypes.c_void_p(e.cuda_event) for e in evs])
     stamps = torch.zeros(_capi.RL_SORT_STAMPS, dtype=torch.int64, device="cuda")
-    tot, passes, hist = [], [], []
+    tot, passes, hist, local, full, scan = [], [], [], [], [], []
+    e_end = torch.cuda.Event(enable_timing=True)
     for r in range(a.reps + 3):
         flush.zero_()
         stamps.zero_()
@@ -46,23 +47,32 @@ def main():
                                               ctypes.c_void_p(sk.data_ptr()), ctypes.c_void_p(perm.data_ptr()),
                                               None, 0, ctypes.c_void_p(ws.data_ptr()), ws.numel(), s, arr,
                                               ctypes.c_void_p(stamps.data_ptr())), "sort")
+        e_end.record()
         torch.cuda.synchronize()
         if r >= 3:
             tot.append(evs[0].elapsed_time(evs[2]))
             st = stamps.cpu().tolist()
             hist.append((st[1] - st[0]) / 1e6)
+            hybrid = st[2] != 0 and st[9] != 0 and st[2] > st[9]
             prev, pp = st[1], []
             for p in range(8):
-                if st[2 + p]:
+                if st[2 + p] and not (hybrid and p == 0):
                     pp.append((st[2 + p] - prev) / 1e6)
                     prev = st[2 + p]
                 else:
                     pp.append(0.0)
             passes.append(pp)
+            if hybrid:
+                scan.append((st[2] - st[9]) / 1e6)
+                local.append((st[10] - st[2]) / 1e6)
+            else:
+                local.append((st[10] - prev) / 1e6)
+            full.append(evs[0].elapsed_time(e_end))
     ok = bool((sk[1:] >= sk[:-1]).all()) and bool((keys[perm.long() & 0xFFFFFFFF] == sk).all())
     pm = np.median(np.array(passes), axis=0)
     act = pm[pm > 0.01]
     print(f"lib={os.environ.get('RELAB_B200_LIB','default')} n={n} ok={ok} total_ms={statistics.median(tot):.4f} "
+          f"with_fallback_ms={statistics.median(full):.4f} scan_us={1e3*statistics.median(scan) if scan else 0:.1f} local_us={1e3*statistics.median(local):.1f} "
           f"hist_us={1e3*statistics.median(hist):.1f} pass_us={[round(1e3*x,1) for x in pm]} "
           f"pass_GBps={24*n/(np.mean(act)/1e3)/1e9:.0f}")
 

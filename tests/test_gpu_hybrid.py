@@ -1,0 +1,135 @@
+"""The wide-key hybrid sort (radix_sort.cu: two top-digit onesweep passes +
+on-chip local sort of the 65536 sub-buckets, LSD fallback on skew) against
+the reference's stable argsort (tensorpath.py:62-75, 206-216 via the oracle).
+
+Every case is checked for the permutation (stable tie order) and the sorted
+key values; the shapes are chosen to reach each branch of the local phase
+and both fallback points (pre-check and post-pass sub-bucket overflow)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tensorpath_oracle as O
+from paper_2602_21237_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+LOCAL_CAP = 3840  # kLocalCap in radix_sort.cu
+I64_MIN, I64_MAX = -(2**63), 2**63 - 1
+
+
+def check_sort(keys: np.ndarray, desc: bool = False):
+    n = len(keys)
+    kd = torch.from_numpy(keys).cuda()
+    sk = torch.empty(n, dtype=torch.int64, device="cuda")
+    perm = engine.sort_permutation([engine.SortAxis(kd, desc)], n, kd.device, sorted_keys_out=sk)
+    got = perm.cpu().numpy().view(np.uint32).astype(np.int64)
+    want = O.stable_axis_order(keys, desc)
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, (n, desc, bad[:5], got[bad[:5]], want[bad[:5]])
+    assert (sk.cpu().numpy() == keys[want]).all()
+
+
+def full_range(rng, n):
+    return rng.integers(I64_MIN, I64_MAX, n, dtype=np.int64, endpoint=True)
+
+
+@pytest.mark.parametrize("n", [1 << 18, (1 << 18) + 12345, 1_000_003, 4_000_000])
+def test_uniform_full_range(n):
+    rng = np.random.default_rng(n)
+    keys = full_range(rng, n)
+    for desc in (False, True):
+        check_sort(keys, desc)
+
+
+def test_cfg2_shape_duplicates():
+    """cfg2's generator (~1% duplicates copied from earlier rows) at 2M rows."""
+    rng = np.random.default_rng(0)
+    n = 2_000_000
+    keys = full_range(rng, n)
+    dst = rng.choice(np.arange(1, n), n // 100, replace=False)
+    src = (rng.random(n // 100) * dst).astype(np.int64)
+    keys[dst] = keys[src]
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+def test_heavy_duplicates_equal_subbuckets():
+    """Few distinct wide values: sub-buckets of equal keys (copy branch)."""
+    rng = np.random.default_rng(5)
+    vals = full_range(rng, 3000)
+    keys = vals[rng.integers(0, 3000, 1_000_000)]
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+def test_large_bins_bitonic_branch():
+    """Sub-buckets whose top varying byte leaves > 16 rows per digit with
+    distinct low bits (warp bitonic by (key, row id)), with repeats."""
+    rng = np.random.default_rng(6)
+    n_groups, per = 2000, 300
+    tops = full_range(rng, n_groups) & ~np.int64((1 << 48) - 1)
+    parts = []
+    for g in range(n_groups):
+        low = rng.integers(0, 1 << 40, per, dtype=np.int64)
+        low[:5] |= np.int64(1) << 47  # top varying bit 47 -> digit bits 40..47; the rest share digit 0
+        low[per // 2:per // 2 + 40] = low[per // 2]  # equal keys inside the big bin
+        parts.append(tops[g] | low)
+    keys = np.concatenate(parts)
+    keys = keys[rng.permutation(len(keys))]
+    # plus uniform background so the top digits pass the spread pre-check
+    keys = np.concatenate([keys, full_range(rng, 1_000_000)])
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+def test_small_bins_insertion_branch():
+    """Rows differing only below the top varying byte, a few per digit."""
+    rng = np.random.default_rng(7)
+    base = full_range(rng, 400_000)
+    extra = base[rng.integers(0, len(base), 200_000)] ^ rng.integers(0, 1 << 12, 200_000, dtype=np.int64)
+    check_sort(np.concatenate([base, extra]))
+
+
+def test_precheck_fallback_narrow_keys():
+    """Top 16 bits constant (keys in [0, 2^40)): the pre-check hands over to LSD."""
+    rng = np.random.default_rng(8)
+    keys = rng.integers(0, 1 << 40, 1_500_000, dtype=np.int64)
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+def test_overflow_fallback_after_passes():
+    """Spread top digits but one sub-bucket above the on-chip cap: detected
+    after the two passes, the LSD kernel behind it produces the result."""
+    rng = np.random.default_rng(9)
+    n = 1_000_000
+    keys = full_range(rng, n)
+    hot = np.int64(0x1234) << 48
+    keys[rng.choice(n, LOCAL_CAP + 1200, replace=False)] = hot | rng.integers(0, 1 << 48, LOCAL_CAP + 1200,
+                                                                           dtype=np.int64)
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+def test_extremes_and_sign_boundary():
+    rng = np.random.default_rng(10)
+    keys = full_range(rng, 600_000)
+    keys[::97] = I64_MIN
+    keys[::89] = I64_MAX
+    keys[::83] = -1
+    keys[::79] = 0
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+def test_hybrid_matches_forced_lsd(monkeypatch):
+    """Same permutation from the hybrid and the LSD path (RL_NO_HYBRID)."""
+    rng = np.random.default_rng(11)
+    keys = full_range(rng, 3_000_000)
+    kd = torch.from_numpy(keys).cuda()
+    a = engine.sort_permutation([engine.SortAxis(kd, False)], len(keys), kd.device)
+    monkeypatch.setenv("RL_NO_HYBRID", "1")
+    b = engine.sort_permutation([engine.SortAxis(kd, False)], len(keys), kd.device)
+    assert torch.equal(a, b)

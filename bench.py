@@ -306,10 +306,25 @@ def run_ours(args):
         total_ms = float(t.item())
     value = world * n * args.steps / (total_ms / 1e3) / 1e6
 
-    # roofline of the dominant kernel: the cooperative onesweep kernel (all
-    # active digit passes in one launch), timed with CUDA events around it
+    # roofline of the dominant kernel: the cooperative sort kernel (one
+    # launch: every digit pass, or the wide-key hybrid's two top-digit passes
+    # + on-chip local phase), timed with CUDA events around it
+    st = stamps.cpu().tolist()  # last step's per-phase split (globaltimer, CTA 0) and the path taken
+    path = {0: "lsd", 1: "hybrid", 2: "hybrid->lsd fallback"}.get(int(st[11]), "?")
     pbytes = pass_bytes(n, active)
-    alg_bytes = sum(pbytes.values())  # per launch
+    top = [p for p in (6, 7) if active[p]]
+    hybrid_bytes = pass_bytes(n, [p in top for p in range(8)])
+    hybrid_total = sum(hybrid_bytes.values()) + 24 * n  # + local phase: read key+id 12n, write key+perm 12n
+    if path == "hybrid":
+        alg_bytes = hybrid_total
+        alg_formula = ("hybrid: pass d6 8n+12n, pass d7 12n+12n, local phase 12n read + 12n write "
+                       "(key u64 + row id u32 in, sorted key + permutation out)")
+    elif path == "lsd":
+        alg_bytes = sum(pbytes.values())
+        alg_formula = "per active pass: first 8n+12n, others 12n+12n (key u64 + row id u32)"
+    else:
+        alg_bytes = sum(hybrid_bytes.values()) + sum(pbytes.values())
+        alg_formula = "hybrid passes then every LSD pass"
     sort_ms = [evs[1].elapsed_time(evs[2]) for evs in pass_ev]
     hist_ms = [evs[0].elapsed_time(evs[1]) for evs in pass_ev]
     avg_sort_ms = statistics.mean(sort_ms)
@@ -319,15 +334,19 @@ def run_ours(args):
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("sort_kernel_bytes_per_launch")
+            tj = json.loads(tfile.read_text())
+            traffic = tj.get("sort_kernel_bytes_per_launch") if tj.get("path", "lsd") == path else None
         except Exception:
             traffic = None
-    st = stamps.cpu().tolist()  # last step's per-pass split (globaltimer, CTA 0)
     prev, per_pass_us = st[1], []
     for p in range(8):
-        if st[2 + p]:
+        if st[2 + p] and not (path == "hybrid" and p == 0):
             per_pass_us.append(round((st[2 + p] - prev) / 1e3, 1))
             prev = st[2 + p]
+    phases = {"passes_us": per_pass_us}
+    if path == "hybrid":
+        phases["subbucket_check_us"] = round((st[2] - prev) / 1e3, 1)
+        phases["local_phase_us"] = round((st[10] - st[2]) / 1e3, 1)
     sort_share = sum(sort_ms) / total_ms
 
     # e2e through the public drop-in API, host numpy in/out
@@ -360,11 +379,11 @@ def run_ours(args):
                 "p50_ms": round(1e3 * percentile(e2e_t, 50), 3), "p99_ms": round(1e3 * percentile(e2e_t, 99), 3)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "rl::radix::sort_kernel (cooperative onesweep, all active digit passes)",
-                     "peak_source": peak_src, "launches_timed": len(sort_ms), "active_passes": sum(active),
-                     "avg_launch_us": round(1e3 * avg_sort_ms, 2), "alg_bytes_per_launch": int(alg_bytes),
-                     "alg_bytes_formula": "per active pass: first 8n+12n, others 12n+12n (key u64 + row id u32)",
-                     "per_pass_us_last_step": per_pass_us, "share_of_step": round(sort_share, 4),
+                     "kernel": "rl::radix::sort_kernel (cooperative: plan, digit passes, hybrid local phase)",
+                     "path": path, "peak_source": peak_src, "launches_timed": len(sort_ms),
+                     "active_digits": sum(active), "avg_launch_us": round(1e3 * avg_sort_ms, 2),
+                     "alg_bytes_per_launch": int(alg_bytes), "alg_bytes_formula": alg_formula,
+                     "phases_last_step": phases, "share_of_step": round(sort_share, 4),
                      "hist_kernel_us": round(1e3 * statistics.mean(hist_ms), 2)},
         "clocks": clocks.summary(),
         "gpu_launches": int(launches),

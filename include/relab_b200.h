@@ -100,7 +100,12 @@ RL_API int64_t rl_launch_count(void);
  * A sort is two launches: the digit histograms, then ONE cooperative
  * kernel running the plan and every digit pass separated by grid barriers;
  * passes whose 8-bit digit is constant over the input are skipped on the
- * device (no host sync, no launch). An INT64 `col` read without perm_in, and perm_in,
+ * device (no host sync, no launch). Wide INT64 keys without perm_in
+ * (n >= 2^18, top 16 bits spread so every one of the 65536 sub-buckets fits
+ * on chip) take the hybrid inside the same kernel: two passes on the top
+ * two digits, then an on-chip sort of each sub-bucket by (key, row id)
+ * written straight to the outputs; a sub-bucket over the on-chip cap
+ * switches the same launch to the LSD passes. Results are identical. An INT64 `col` read without perm_in, and perm_in,
  * must be 16-byte aligned (they are streamed with TMA bulk copies);
  * RL_ERR_BAD_ARG otherwise.
  * --------------------------------------------------------------------- */
@@ -127,9 +132,10 @@ RL_API int rl_sort_axis_gather(const void* col, int32_t col_kind, int32_t width,
  * and after the pass kernel; if stamps_dev (device, RL_SORT_STAMPS x
  * uint64) is not NULL, CTA 0 writes %globaltimer (ns) there: [0] histogram
  * start, [1] pass kernel start, [2+p] after digit pass p (0 for skipped
- * passes), [10] end. */
+ * passes; in the hybrid [2] = sub-bucket check done), [10] end, and [11]
+ * the path taken: 0 LSD, 1 hybrid, 2 hybrid that fell back to LSD. */
 #define RL_SORT_EVENTS 3
-#define RL_SORT_STAMPS 11
+#define RL_SORT_STAMPS 12
 RL_API int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width,
                  int32_t word, int32_t descending, const uint32_t* perm_in,
                  int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out,

@@ -32,7 +32,7 @@ RL_SIDE_KEY = 2
 RL_MAX_COLUMNS = 32
 RL_MAX_ROWS = 2**32 - 1
 RL_SORT_EVENTS = 3
-RL_SORT_STAMPS = 11
+RL_SORT_STAMPS = 12
 RL_SORT_MAX_FUSED_COLUMNS = 8
 
 

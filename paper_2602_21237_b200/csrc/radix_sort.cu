@@ -80,12 +80,12 @@ constexpr int kTile = kThreads * kItems;
 constexpr int kWarps = kThreads / 32;
 constexpr int kLookback = RL_LOOKBACK_WINDOW;
 #ifndef RL_HIST_UNROLL
-#define RL_HIST_UNROLL 8
+#define RL_HIST_UNROLL 16
 #endif
 constexpr int kHistUnroll = RL_HIST_UNROLL;
-constexpr int kStamps = 2 + kPasses + 1;  // per-phase globaltimer stamps (profiling)
+constexpr int kStamps = 2 + kPasses + 2;  // per-phase globaltimer stamps + the path taken (profiling)
 // wide-key hybrid
-constexpr int kLocalCap = 3840;            // rows of one on-chip local load (24 B each: two key/id buffers)
+constexpr int kLocalCap = 2560;            // rows of one on-chip local run (and the largest sub-bucket)
 constexpr int kSubBuckets = 1 << 16;       // (d7, d6) sub-buckets
 constexpr int kGroupSubs = 16;             // sub-buckets claimed per local work item
 constexpr int64_t kHybridMinRows = 1 << 18;
@@ -204,15 +204,20 @@ constexpr size_t kPassSmemBytes = kBarOffset + 64;
 // A, scattered buffer B, the (sub-bucket, d5) bin counters/cursors, the
 // list of bins too long for a one-thread fix-up, and scalars.
 constexpr int kLocalBins = kGroupSubs * kBins;  // (top16 - first of group, d5)
-constexpr int kBigList = 256;
-constexpr size_t kLocAk = 0;
-constexpr size_t kLocAv = kLocAk + size_t(kLocalCap) * 8;
-constexpr size_t kLocBk = kLocAv + size_t(kLocalCap) * 4;
+constexpr int kBigList = 128;
+constexpr size_t kLocAKeys = size_t(kLocalCap + 2) * 8;  // +2 / +4: TMA copies start 16-byte aligned
+constexpr size_t kLocAVals = size_t(kLocalCap + 4) * 4;
+constexpr size_t kLocABytes = (kLocAKeys + kLocAVals + 15) / 16 * 16;
+constexpr size_t kLocA = 0;  // two run buffers (double-buffered TMA loads)
+constexpr size_t kLocBk = kLocA + 2 * kLocABytes;
 constexpr size_t kLocBv = kLocBk + size_t(kLocalCap) * 8;
 constexpr size_t kLocHist = kLocBv + size_t(kLocalCap) * 4;
 constexpr size_t kLocBig = kLocHist + size_t(kLocalBins) * 4;
 constexpr size_t kLocMisc = kLocBig + size_t(kBigList) * 4;
-constexpr size_t kLocalSmemBytes = kLocMisc + 64 * 4;  // misc: [0] claim, [1] big count, [8..] group starts, [32..] scan
+// misc: [0] big count, [2..3] run-list sizes, [8..] scan scratch, [32..65] group offsets (x2),
+// [72..103] run ends (x2), [112..] run descriptors
+constexpr size_t kLocBars = kLocMisc + 128 * 4;
+constexpr size_t kLocalSmemBytes = kLocBars + 2 * 8;
 constexpr size_t kSmemBytes = std::max(kPassSmemBytes + size_t(kPasses) * kBins * 4 + 64, kLocalSmemBytes);
 
 struct PassState {  // per-CTA mbarrier phase parities, carried across passes
@@ -510,28 +515,59 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
 
 // K1: all eight digit histograms in one read of the keys (its own launch:
 // shared-atomic bound, it wants 4x the resident threads of the passes).
+// RAW: contiguous int64 keys, read as 16-byte vectors with every load of a
+// step in flight before the first use; otherwise the generic loader
+// (gathered rows, Bytes words; materialises the transformed words).
 constexpr int kHistThreads = 512;
+template <bool RAW>
 __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
   __shared__ uint32_t h[kPasses * kBins];
   const int tid = threadIdx.x;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
   for (int i = tid; i < kPasses * kBins; i += kHistThreads) h[i] = 0;
   __syncthreads();
-  const int64_t stride = int64_t(gridDim.x) * kHistThreads * kHistUnroll;
-  for (int64_t base = int64_t(blockIdx.x) * kHistThreads * kHistUnroll + tid; base < a.n; base += stride) {
-    uint64_t k[kHistUnroll];
+  auto count = [&](uint64_t k) {
 #pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      const int64_t i = base + int64_t(u) * kHistThreads;
-      k[u] = i < a.n ? load_key(a, i) : 0;
+    for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p * kBins + ((k >> (p * kBits)) & (kBins - 1))], 1u);
+  };
+  if constexpr (RAW) {
+    const ulonglong2* v2 = static_cast<const ulonglong2*>(a.col);  // 16-byte aligned (checked by the caller)
+    const int64_t pairs = a.n >> 1;
+    constexpr int kV = kHistUnroll / 2;
+    const int64_t stride = int64_t(gridDim.x) * kHistThreads * kV;
+    for (int64_t base = int64_t(blockIdx.x) * kHistThreads * kV + tid; base < pairs; base += stride) {
+      ulonglong2 q[kV];
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int64_t i = base + int64_t(u) * kHistThreads;
+        q[u] = i < pairs ? __ldcs(v2 + i) : make_ulonglong2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        if (base + int64_t(u) * kHistThreads < pairs) {
+          count(xform(q[u].x, a.desc));
+          count(xform(q[u].y, a.desc));
+        }
+      }
     }
+    if ((a.n & 1) && blockIdx.x == 0 && tid == 0)
+      count(xform(uint64_t(static_cast<const long long*>(a.col)[a.n - 1]), a.desc));
+  } else {
+    const int64_t stride = int64_t(gridDim.x) * kHistThreads * kHistUnroll;
+    for (int64_t base = int64_t(blockIdx.x) * kHistThreads * kHistUnroll + tid; base < a.n; base += stride) {
+      uint64_t k[kHistUnroll];
 #pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      const int64_t i = base + int64_t(u) * kHistThreads;
-      if (i >= a.n) continue;
-      if (a.materialized) a.materialized[i] = k[u];
+      for (int u = 0; u < kHistUnroll; ++u) {
+        const int64_t i = base + int64_t(u) * kHistThreads;
+        k[u] = i < a.n ? load_key(a, i) : 0;
+      }
 #pragma unroll
-      for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p * kBins + ((k[u] >> (p * kBits)) & (kBins - 1))], 1u);
+      for (int u = 0; u < kHistUnroll; ++u) {
+        const int64_t i = base + int64_t(u) * kHistThreads;
+        if (i >= a.n) continue;
+        if (a.materialized) a.materialized[i] = k[u];
+        count(k[u]);
+      }
     }
   }
   __syncthreads();
@@ -571,152 +607,235 @@ __device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t h
   }
 }
 
-// The local phase: CTAs claim groups of kGroupSubs consecutive sub-buckets
-// and load them in runs of whole sub-buckets of at most kLocalCap rows.
-// A run is sorted on chip by (top16, d5) with a counting scatter (one
-// shared atomic per row: the order inside a bin is settled next), then
-// each row takes its rank by (key, row id) inside its bin — rows equal in
-// their top 24 bits, ~1 for uniform keys; a warp's bitonic network for
-// bins above 32 rows — and goes straight to its final position in the
-// outputs, with the fused gathers.
+// The local phase. CTA c owns groups c, c + grid, ... of kGroupSubs
+// consecutive sub-buckets; each group is cut into runs of whole sub-buckets
+// of at most kLocalCap rows. Runs are double-buffered: while one is sorted
+// the next streams in with TMA bulk copies, and the offsets of the next
+// group are loaded a group ahead. A run is sorted on chip by (top16, d5)
+// with a counting scatter (one shared atomic per row: the order inside a
+// bin is settled next), then each row takes its rank by (key, row id)
+// inside its bin — rows equal in their top 24 bits, ~1 for uniform keys; a
+// warp's bitonic network for bins above 32 rows — and goes straight to its
+// final position in the outputs, with the fused gathers.
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Greedy cut of one group (offsets off[0..G]) into runs; returns the count.
+__device__ __forceinline__ uint32_t cut_group(const uint32_t* off, uint32_t* ends) {
+  uint32_t nr = 0, s = 0;
+  while (s < uint32_t(kGroupSubs)) {
+    const uint32_t base = off[s];
+    uint32_t e = s + 1;
+    while (e < uint32_t(kGroupSubs) && off[e + 1] - base <= uint32_t(kLocalCap)) ++e;
+    if (off[e] > base) ends[nr++] = (s << 8) | e;
+    s = e;
+  }
+  return nr;
+}
+
+__device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* vin, uint32_t base, uint32_t cnt,
+                                          uint8_t* abuf, uint64_t* bar) {
+  const uint32_t k0 = base & ~1u, v0 = base & ~3u;
+  const uint32_t kbytes = ((base + cnt - k0) * 8u + 15u) & ~15u;
+  const uint32_t vbytes = ((base + cnt - v0) * 4u + 15u) & ~15u;
+  fence_proxy_async_smem();
+  mbar_expect_tx(bar, kbytes + vbytes);
+  bulk_g2s(abuf, kin + k0, kbytes, bar);
+  bulk_g2s(abuf + kLocAKeys, vin + v0, vbytes, bar);
+}
+
 __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
-  uint64_t* ak = reinterpret_cast<uint64_t*>(smem + kLocAk);
-  uint32_t* av = reinterpret_cast<uint32_t*>(smem + kLocAv);
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
   uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kLocHist);
   uint32_t* big = reinterpret_cast<uint32_t*>(smem + kLocBig);
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
+  uint32_t* goff = misc + 32;   // [2][kGroupSubs + 1]
+  uint32_t* gends = misc + 72;  // [2][kGroupSubs]
+  uint32_t* runs = misc + 112;  // [2][3] descriptors of the run in each buffer
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLocBars);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* kin = src == 1 ? a.keys_a : a.keys_b;
   const uint32_t* vin = src == 1 ? a.vals_a : a.vals_b;
+  const int desc = a.key_mode == kRawDesc;
   constexpr uint32_t kGroups = kSubBuckets / kGroupSubs;
-  constexpr int kPerThread = kLocalBins / kThreads;  // consecutive bins per thread in scan / fix-up
+  constexpr int kPerThread = kLocalBins / kThreads;
+  const uint32_t g0 = blockIdx.x, gstep = gridDim.x;
+  if (g0 >= kGroups) return;
+
+  // ---- prologue (warp 0): offsets of the first group, its runs, the first
+  // TMA; the second group's offsets are requested into registers
+  uint32_t next_off = 0;  // warp 0, lane <= G: sub_off of the group after the current one
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+    }
+    if (lane <= kGroupSubs) goff[lane] = __ldcg(a.sub_off + g0 * kGroupSubs + lane);
+    if (lane <= kGroupSubs && g0 + gstep < kGroups) next_off = __ldcg(a.sub_off + (g0 + gstep) * kGroupSubs + lane);
+    __syncwarp();
+    if (lane == 0) misc[2] = cut_group(goff, gends);
+    __syncwarp();
+  }
+  __syncthreads();
+  // run cursor: group k (g = g0 + k gstep), run r of that group; identical in every thread
+  uint32_t k = 0, r = 0, buf = 0, phase0 = 0, phase1 = 0;
+  bool have = misc[2] > 0;
+  // an empty first group: advance (rare; only tiny inputs have empty groups)
+  while (!have) {
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t gn = g0 + (k + 1) * gstep;
+      if (lane <= kGroupSubs && gn < kGroups) goff[((k + 1) & 1) * 17 + lane] = next_off;
+      if (lane <= kGroupSubs && gn + gstep < kGroups) next_off = __ldcg(a.sub_off + (gn + gstep) * kGroupSubs + lane);
+      __syncwarp();
+      if (lane == 0) misc[2 + ((k + 1) & 1)] = gn < kGroups ? cut_group(goff + ((k + 1) & 1) * 17, gends + ((k + 1) & 1) * 16) : 0;
+    }
+    __syncthreads();
+    ++k;
+    if (g0 + k * gstep >= kGroups) return;
+    have = misc[2 + (k & 1)] > 0;
+  }
+  if (tid == 0) {
+    const uint32_t* off = goff + (k & 1) * 17;
+    const uint32_t se = gends[(k & 1) * 16];
+    const uint32_t base = off[se >> 8], cnt = off[se & 255] - base;
+    runs[0] = base;
+    runs[1] = cnt;
+    runs[2] = (g0 + k * gstep) * kGroupSubs + (se >> 8);
+    issue_run(kin, vin, base, cnt, smem + kLocA, &bars[0]);
+  }
+
   while (true) {
-    __syncthreads();  // previous group's reads of misc are done
-    if (tid == 0) misc[0] = atomicAdd(&a.flags[1], 1u);
+    // ---- warp 0: find and prefetch the next run into the other buffer
+    if (warp == 0) {
+      uint32_t nk = k, nr = r + 1;
+      bool ok = true;
+      while (nr >= misc[2 + (nk & 1)]) {  // past the group's runs: the next group (offsets were prefetched)
+        const uint32_t gn = g0 + (nk + 1) * gstep;
+        if (gn >= kGroups) {
+          ok = false;
+          break;
+        }
+        if (lane <= kGroupSubs) goff[((nk + 1) & 1) * 17 + lane] = next_off;
+        if (lane <= kGroupSubs && gn + gstep < kGroups) next_off = __ldcg(a.sub_off + (gn + gstep) * kGroupSubs + lane);
+        __syncwarp();
+        if (lane == 0) misc[2 + ((nk + 1) & 1)] = cut_group(goff + ((nk + 1) & 1) * 17, gends + ((nk + 1) & 1) * 16);
+        __syncwarp();
+        ++nk;
+        nr = 0;
+      }
+      if (lane == 0) {
+        misc[4] = ok ? 1u : 0u;
+        misc[5] = nk;
+        misc[6] = nr;
+        if (ok) {
+          const uint32_t* off = goff + (nk & 1) * 17;
+          const uint32_t se = gends[(nk & 1) * 16 + nr];
+          const uint32_t base = off[se >> 8], cnt = off[se & 255] - base;
+          uint32_t* d = runs + (buf ^ 1) * 3;
+          d[0] = base;
+          d[1] = cnt;
+          d[2] = (g0 + nk * gstep) * kGroupSubs + (se >> 8);
+          issue_run(kin, vin, base, cnt, smem + kLocA + (buf ^ 1) * kLocABytes, &bars[buf ^ 1]);
+        }
+      }
+    }
+    // ---- this run
+    for (int i = tid; i < kLocalBins; i += kThreads) hist[i] = 0;
+    if (tid == 0) {
+      misc[0] = 0;
+      misc[1] = 0;
+    }
+    mbar_wait(&bars[buf], buf ? phase1 : phase0);
+    if (buf) phase1 ^= 1;
+    else phase0 ^= 1;
+    __syncthreads();  // hist zeroed, run descriptors and next-run fields visible
+    const uint32_t base = runs[buf * 3], cnt = runs[buf * 3 + 1], top0 = runs[buf * 3 + 2] & ~uint32_t(kGroupSubs - 1);
+    const uint8_t* abuf = smem + kLocA + buf * kLocABytes;
+    const uint64_t* ak = reinterpret_cast<const uint64_t*>(abuf) + (base & 1u);
+    const uint32_t* av = reinterpret_cast<const uint32_t*>(abuf + kLocAKeys) + (base & 3u);
+    auto bin_of = [&](uint64_t key) {
+      return int(((uint32_t(key >> 48) - top0) << kBits) | (uint32_t(key >> 40) & (kBins - 1)));
+    };
+    for (uint32_t j = tid; j < cnt; j += kThreads) atomicAdd(&hist[bin_of(ak[j])], 1u);
     __syncthreads();
-    const uint32_t g = misc[0];
-    if (g >= kGroups) break;
-    if (tid <= kGroupSubs) misc[8 + tid] = __ldcg(a.sub_off + g * kGroupSubs + tid);
+    {  // exclusive scan: thread owns bins [kPerThread tid, kPerThread (tid + 1))
+      uint32_t c[kPerThread], run = 0;
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        c[i] = hist[tid * kPerThread + i];
+        run += c[i];
+      }
+      uint32_t total;
+      uint32_t start = block_exclusive_scan<kThreads>(run, misc + 8, &total);
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        hist[tid * kPerThread + i] = start;
+        start += c[i];
+      }
+    }
     __syncthreads();
-    const uint32_t top0 = g * kGroupSubs;
-    uint32_t s = 0;
-    while (s < kGroupSubs) {
-      const uint32_t base = misc[8 + s];
-      uint32_t e = s + 1;
-      while (e < kGroupSubs && misc[8 + e + 1] - base <= uint32_t(kLocalCap)) ++e;
-      const uint32_t cnt = misc[8 + e] - base;
-      if (cnt == 0) {
-        s = e;
+    for (uint32_t j = tid; j < cnt; j += kThreads) {
+      const uint64_t key = ak[j];
+      const uint32_t pos = atomicAdd(&hist[bin_of(key)], 1u);
+      bk[pos] = key;
+      bv[pos] = av[j];
+    }
+    __syncthreads();
+    // hist[b] is now the end of bin b; a bin holds the rows equal in their
+    // top 24 bits (~1 for uniform keys). Each row takes its rank by (key,
+    // row id) among its bin's rows and goes straight to its final position;
+    // bins above 32 rows are sorted by a warp's bitonic network first.
+    constexpr uint32_t kRankMax = 32;
+    auto emit = [&](uint32_t p, uint64_t key, uint32_t v) {
+      const uint64_t o = uint64_t(base) + p;
+      if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(key, desc));
+      __stcs(a.out_vals + o, v);
+      gather_fused(a.gather, v, o);
+    };
+    for (uint32_t p = tid; p < cnt; p += kThreads) {
+      const uint64_t key = bk[p];
+      const uint32_t v = bv[p];
+      const int b = bin_of(key);
+      const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+      uint32_t pos = p;
+      if (b1 - b0 > kRankMax) {
+        if (p == b0) {
+          const uint32_t slot = atomicAdd(&misc[0], 1u);
+          if (slot < kBigList) big[slot] = uint32_t(b);
+        }
         continue;
       }
-      for (int i = tid; i < kLocalBins; i += kThreads) hist[i] = 0;
-      if (tid == 0) misc[1] = 0;
-      {  // all of the run's loads in flight at once
-        constexpr int kLoads = (kLocalCap + kThreads - 1) / kThreads;
-        uint64_t lk[kLoads];
-        uint32_t lv[kLoads];
-#pragma unroll
-        for (int u = 0; u < kLoads; ++u) {
-          const uint32_t j = uint32_t(u * kThreads + tid);
-          if (j < cnt) {
-            lk[u] = __ldcg(reinterpret_cast<const unsigned long long*>(kin) + base + j);
-            lv[u] = __ldcg(vin + base + j);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kLoads; ++u) {
-          const uint32_t j = uint32_t(u * kThreads + tid);
-          if (j < cnt) {
-            ak[j] = lk[u];
-            av[j] = lv[u];
-          }
-        }
+      if (b1 - b0 > 1) {
+        uint32_t rk = 0;
+        for (uint32_t i = b0; i < b1; ++i) rk += row_less(bk[i], bv[i], key, v) ? 1u : 0u;
+        pos = b0 + rk;
       }
-      __syncthreads();
-      for (uint32_t j = tid; j < cnt; j += kThreads) {
-        const uint64_t k = ak[j];
-        atomicAdd(&hist[((uint32_t(k >> 48) - top0) << kBits) | (uint32_t(k >> 40) & (kBins - 1))], 1u);
-      }
-      __syncthreads();
-      {  // exclusive scan: thread owns bins [kPerThread tid, kPerThread (tid + 1))
-        uint32_t c[kPerThread], run = 0;
-#pragma unroll
-        for (int i = 0; i < kPerThread; ++i) {
-          c[i] = hist[tid * kPerThread + i];
-          run += c[i];
-        }
-        uint32_t total;
-        uint32_t start = block_exclusive_scan<kThreads>(run, misc + 32, &total);
-#pragma unroll
-        for (int i = 0; i < kPerThread; ++i) {
-          hist[tid * kPerThread + i] = start;
-          start += c[i];
-        }
-      }
-      __syncthreads();
-      for (uint32_t j = tid; j < cnt; j += kThreads) {
-        const uint64_t k = ak[j];
-        const uint32_t pos =
-            atomicAdd(&hist[((uint32_t(k >> 48) - top0) << kBits) | (uint32_t(k >> 40) & (kBins - 1))], 1u);
-        bk[pos] = k;
-        bv[pos] = av[j];
-      }
-      __syncthreads();
-      // hist[b] is now the end of bin b; a bin holds the rows equal in their
-      // top 24 bits (~1 for uniform keys). Every row finds its rank by
-      // (key, row id) among its bin's rows and is written straight to its
-      // final position; bins above kRankMax rows are sorted by a warp first.
-      constexpr uint32_t kRankMax = 32;
-      const int desc = a.key_mode == kRawDesc;
-      auto bin_of = [&](uint64_t k) {
-        return int(((uint32_t(k >> 48) - top0) << kBits) | (uint32_t(k >> 40) & (kBins - 1)));
-      };
-      for (uint32_t p = tid; p < cnt; p += kThreads) {
-        const uint64_t k = bk[p];
-        const uint32_t v = bv[p];
-        const int b = bin_of(k);
-        const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
-        uint32_t pos = p;
-        if (b1 - b0 > kRankMax) {
-          if (p == b0) {
-            const uint32_t slot = atomicAdd(&misc[1], 1u);
-            if (slot < kBigList) big[slot] = uint32_t(b);
-          }
-          continue;
-        }
-        if (b1 - b0 > 1) {
-          uint32_t r = 0;
-          for (uint32_t i = b0; i < b1; ++i) r += row_less(bk[i], bv[i], k, v) ? 1u : 0u;
-          pos = b0 + r;
-        }
-        const uint64_t o = uint64_t(base) + pos;
-        if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(k, desc));
-        __stcs(a.out_vals + o, v);
-        gather_fused(a.gather, v, o);
-      }
-      __syncthreads();
-      for (uint32_t t = warp; t < min(misc[1], uint32_t(kBigList)); t += kWarps) {
-        const int b = int(big[t]);
-        const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
-        warp_bitonic(bk, bv, b0, b1, lane);
-        for (uint32_t p = b0 + lane; p < b1; p += 32) {
-          const uint64_t o = uint64_t(base) + p;
-          if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(bk[p], desc));
-          __stcs(a.out_vals + o, bv[p]);
-          gather_fused(a.gather, bv[p], o);
-        }
-      }
-      s = e;
-      __syncthreads();  // A/B/hist free for the next run
+      emit(pos, key, v);
     }
+    __syncthreads();
+    const uint32_t nbig = min(misc[0], uint32_t(kBigList));
+    for (uint32_t t = warp; t < nbig; t += kWarps) {
+      const int b = int(big[t]);
+      const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+      warp_bitonic(bk, bv, b0, b1, lane);
+      for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], bv[p]);
+    }
+    if (nbig) __syncthreads();
+    if (!misc[4]) break;
+    k = misc[5];
+    r = misc[6];
+    buf ^= 1;
+    __syncthreads();  // B/hist/misc reads done before the next run rewrites them
+  }
+  if (tid == 0) {
+    mbar_inval(&bars[0]);
+    mbar_inval(&bars[1]);
   }
 }
 
-__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
-  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // The whole sort after the histograms: plan, every active digit pass,
 // copy-through — one cooperative launch. Hybrid (wide raw int64 keys):
@@ -798,7 +917,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       // sub-buckets that fit on chip (pigeonhole + independent-digit estimate)
       // and at least two passes to save
       const bool hyb = a.mode == kModeHybrid && na >= 4 && (plan[6] | plan[7]) &&
-                       uint64_t(a.n) <= uint64_t(nz) * kLocalCap && mx <= uint32_t(kLocalCap) / 2;
+                       uint64_t(a.n) <= uint64_t(nz) * kLocalCap && mx <= uint32_t(kLocalCap) * 4 / 5;
       plan[kPasses + 1] = hyb ? 1u : 0u;
       for (int p = 0; p < kPasses; ++p) plan[kPasses + 2 + p] = p >= 6 ? plan[p] : 0u;
       plan[2 * kPasses + 2] = plan[6] + plan[7];
@@ -840,7 +959,10 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       }
       __syncthreads();
       local_phase(a, smem, src);
-      if (stamper) a.stamps[kStamps - 1] = globaltimer();
+      if (stamper) {
+        a.stamps[kStamps - 2] = globaltimer();
+        a.stamps[kStamps - 1] = 1;
+      }
       return;
     }
     // a sub-bucket does not fit on chip: the LSD sort, fresh epochs and counters
@@ -862,7 +984,10 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       gather_fused(a.gather, row, uint64_t(i));
     }
   }
-  if (stamper) a.stamps[kStamps - 1] = globaltimer();
+  if (stamper) {
+    a.stamps[kStamps - 2] = globaltimer();
+    a.stamps[kStamps - 1] = plan[kPasses + 1] ? 2 : 0;
+  }
 }
 
 struct Layout {
@@ -936,9 +1061,9 @@ static int sort_grid_limit() {
   return cached;
 }
 
-static int hist_grid(int64_t n) {
-  const int64_t per_cta = int64_t(kHistThreads) * kHistUnroll * 2;
-  return int(std::max<int64_t>(1, std::min<int64_t>((n + per_cta - 1) / per_cta, int64_t(device_sm_count()) * 4)));
+static int hist_grid(int64_t n) {  // one co-resident wave (2 CTAs of 512 threads per SM), >= 1 step each
+  const int64_t per_cta = int64_t(kHistThreads) * kHistUnroll;
+  return int(std::max<int64_t>(1, std::min<int64_t>((n + per_cta - 1) / per_cta, int64_t(device_sm_count()) * 2)));
 }
 
 // Histograms, then the cooperative kernel (LSD, or the wide-key hybrid
@@ -956,7 +1081,8 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(limit, tiles)));
   a.mode = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() ? kModeHybrid : kModeLsd;
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
-  hist_kernel<<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
+  if (a.src_mode == kSrcInt64) hist_kernel<true><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
+  else hist_kernel<false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
   void* params[] = {&a};
   e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,

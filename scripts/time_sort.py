@@ -53,7 +53,7 @@ def main():
             tot.append(evs[0].elapsed_time(evs[2]))
             st = stamps.cpu().tolist()
             hist.append((st[1] - st[0]) / 1e6)
-            hybrid = st[2] != 0 and st[9] != 0 and st[2] > st[9]
+            hybrid = st[11] == 1
             prev, pp = st[1], []
             for p in range(8):
                 if st[2 + p] and not (hybrid and p == 0):

@@ -15,7 +15,7 @@ from paper_2602_21237_b200 import engine
 
 pytestmark = pytest.mark.gpu
 
-LOCAL_CAP = 3840  # kLocalCap in radix_sort.cu
+LOCAL_CAP = 2560  # kLocalCap in radix_sort.cu
 I64_MIN, I64_MAX = -(2**63), 2**63 - 1
 
 

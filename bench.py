@@ -214,8 +214,60 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def sort_roofline(n, active, st, sort_ms, hist_ms, step_ms_total):
+    """Roofline of the dominant kernel: the cooperative sort kernel (one
+    launch: every digit pass, or the wide-key hybrid's two top-digit passes +
+    on-chip local phase), from CUDA events around it; `st` = the last
+    step's globaltimer stamps (per-phase split, [11] = path taken)."""
+    path = {0: "lsd", 1: "hybrid", 2: "hybrid->lsd fallback"}.get(int(st[11]), "?")
+    pbytes = pass_bytes(n, active)
+    top = [p for p in (6, 7) if active[p]]
+    hybrid_bytes = pass_bytes(n, [p in top for p in range(8)])
+    if path == "hybrid":
+        alg_bytes = sum(hybrid_bytes.values()) + 24 * n  # + local phase: read key+id 12n, write key+perm 12n
+        alg_formula = ("hybrid: pass d6 8n+12n, pass d7 12n+12n, local phase 12n read + 12n write "
+                       "(key u64 + row id u32 in, sorted key + permutation out)")
+    elif path == "lsd":
+        alg_bytes = sum(pbytes.values())
+        alg_formula = "per active pass: first 8n+12n, others 12n+12n (key u64 + row id u32)"
+    else:
+        alg_bytes = sum(hybrid_bytes.values()) + sum(pbytes.values())
+        alg_formula = "hybrid passes then every LSD pass"
+    avg_sort_ms = statistics.mean(sort_ms)
+    achieved = alg_bytes / (avg_sort_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            tj = json.loads(tfile.read_text())
+            traffic = tj.get("sort_kernel_bytes_per_launch") if tj.get("path", "lsd") == path else None
+        except Exception:
+            traffic = None
+    prev, per_pass_us = st[1], []
+    for p in range(8):
+        if st[2 + p] and not (path == "hybrid" and p == 0):
+            per_pass_us.append(round((st[2 + p] - prev) / 1e3, 1))
+            prev = st[2 + p]
+    phases = {"passes_us": per_pass_us}
+    if path == "hybrid":
+        phases["subbucket_check_us"] = round((st[2] - prev) / 1e3, 1)
+        phases["local_phase_us"] = round((st[10] - st[2]) / 1e3, 1)
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": "rl::radix::sort_kernel (cooperative: plan, digit passes, hybrid local phase)",
+            "path": path, "peak_source": peak_src, "launches_timed": len(sort_ms),
+            "active_digits": sum(active), "avg_launch_us": round(1e3 * avg_sort_ms, 2),
+            "alg_bytes_per_launch": int(alg_bytes), "alg_bytes_formula": alg_formula,
+            "phases_last_step": phases, "share_of_step": round(sum(sort_ms) / step_ms_total, 4),
+            "hist_kernel_us": round(1e3 * statistics.mean(hist_ms), 2)}
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_ours(args):
+    # the driver parses rank 0's stdout as ONE JSON line: keep NCCL's banner off it
+    if not os.environ.get("RL_KEEP_NCCL_DEBUG"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     import torch
     import torch.distributed as dist
 
@@ -243,7 +295,7 @@ def run_ours(args):
 
     stamps = torch.zeros(_capi.RL_SORT_STAMPS, dtype=torch.int64, device=dev)
 
-    def device_step(events=None):
+    def device_step(events=None, stamps_out=None):
         """One cfg2 ORDER BY on resident inputs: sorted keys + permutation
         (histogram + cooperative onesweep kernel), then the payload gather."""
         sorted_keys = torch.empty(n, dtype=torch.int64, device=dev)
@@ -255,7 +307,8 @@ def run_ours(args):
             _capi.check(lib.rl_sort_axis_gather(*common), "sort")
         else:
             arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
-            _capi.check(lib.rl_sort_axis_profiled(*common, arr, ctypes.c_void_p(stamps.data_ptr())), "sort")
+            st_t = stamps if stamps_out is None else stamps_out
+            _capi.check(lib.rl_sort_axis_profiled(*common, arr, ctypes.c_void_p(st_t.data_ptr())), "sort")
         engine.gather_rows(perm, [engine.OutColumn(pay_d, out_pay, 4, 0)])
         return sorted_keys, perm, out_pay
 
@@ -279,6 +332,11 @@ def run_ours(args):
         for e in evs:  # force creation so the raw handle exists
             e.record()
         return evs
+
+    dist_mode = world > 1 or args.dist
+    if dist_mode:
+        return run_distributed(args, dev, rank, world, lib, keys_h, pay_h, keys_d, pay_d, flush, device_step,
+                               make_events)
 
     step_ev = [make_events(2) for _ in range(args.steps)]
     pass_ev = [make_events(_capi.RL_SORT_EVENTS) for _ in range(args.steps)]
@@ -306,48 +364,9 @@ def run_ours(args):
         total_ms = float(t.item())
     value = world * n * args.steps / (total_ms / 1e3) / 1e6
 
-    # roofline of the dominant kernel: the cooperative sort kernel (one
-    # launch: every digit pass, or the wide-key hybrid's two top-digit passes
-    # + on-chip local phase), timed with CUDA events around it
-    st = stamps.cpu().tolist()  # last step's per-phase split (globaltimer, CTA 0) and the path taken
-    path = {0: "lsd", 1: "hybrid", 2: "hybrid->lsd fallback"}.get(int(st[11]), "?")
-    pbytes = pass_bytes(n, active)
-    top = [p for p in (6, 7) if active[p]]
-    hybrid_bytes = pass_bytes(n, [p in top for p in range(8)])
-    hybrid_total = sum(hybrid_bytes.values()) + 24 * n  # + local phase: read key+id 12n, write key+perm 12n
-    if path == "hybrid":
-        alg_bytes = hybrid_total
-        alg_formula = ("hybrid: pass d6 8n+12n, pass d7 12n+12n, local phase 12n read + 12n write "
-                       "(key u64 + row id u32 in, sorted key + permutation out)")
-    elif path == "lsd":
-        alg_bytes = sum(pbytes.values())
-        alg_formula = "per active pass: first 8n+12n, others 12n+12n (key u64 + row id u32)"
-    else:
-        alg_bytes = sum(hybrid_bytes.values()) + sum(pbytes.values())
-        alg_formula = "hybrid passes then every LSD pass"
     sort_ms = [evs[1].elapsed_time(evs[2]) for evs in pass_ev]
     hist_ms = [evs[0].elapsed_time(evs[1]) for evs in pass_ev]
-    avg_sort_ms = statistics.mean(sort_ms)
-    achieved = alg_bytes / (avg_sort_ms / 1e3) / 1e9
-    peak, peak_src = measured_peak_hbm()
-    traffic = None
-    tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists():
-        try:
-            tj = json.loads(tfile.read_text())
-            traffic = tj.get("sort_kernel_bytes_per_launch") if tj.get("path", "lsd") == path else None
-        except Exception:
-            traffic = None
-    prev, per_pass_us = st[1], []
-    for p in range(8):
-        if st[2 + p] and not (path == "hybrid" and p == 0):
-            per_pass_us.append(round((st[2 + p] - prev) / 1e3, 1))
-            prev = st[2 + p]
-    phases = {"passes_us": per_pass_us}
-    if path == "hybrid":
-        phases["subbucket_check_us"] = round((st[2] - prev) / 1e3, 1)
-        phases["local_phase_us"] = round((st[10] - st[2]) / 1e3, 1)
-    sort_share = sum(sort_ms) / total_ms
+    roofline = sort_roofline(n, active, stamps.cpu().tolist(), sort_ms, hist_ms, total_ms)
 
     # e2e through the public drop-in API, host numpy in/out
     spec = SortSpec(("key",))
@@ -377,14 +396,7 @@ def run_ours(args):
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": n * 12,
                 "d2h_bytes_per_step": n * 12, "api": "tensor_sort(Relation numpy) -> (Relation, SpillStats)",
                 "p50_ms": round(1e3 * percentile(e2e_t, 50), 3), "p99_ms": round(1e3 * percentile(e2e_t, 99), 3)},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "rl::radix::sort_kernel (cooperative: plan, digit passes, hybrid local phase)",
-                     "path": path, "peak_source": peak_src, "launches_timed": len(sort_ms),
-                     "active_digits": sum(active), "avg_launch_us": round(1e3 * avg_sort_ms, 2),
-                     "alg_bytes_per_launch": int(alg_bytes), "alg_bytes_formula": alg_formula,
-                     "phases_last_step": phases, "share_of_step": round(sort_share, 4),
-                     "hist_kernel_us": round(1e3 * statistics.mean(hist_ms), 2)},
+        "roofline": roofline,
         "clocks": clocks.summary(),
         "gpu_launches": int(launches),
     }
@@ -405,6 +417,154 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_distributed(args, dev, rank, world, lib, keys_h, pay_h, keys_d, pay_d, flush, device_step, make_events):
+    """N GPUs (or --dist at N=1): the north star's multi-GPU ORDER BY. Every
+    rank holds its own 10M-row cfg2 shard (global row ids rank*n + i, weak
+    scaling); a step is one dist.distributed_sort: sampled (key, row id)
+    splitters, device range partition, NCCL all-to-all of keys / payload /
+    row ids over NVLink, local stable sort (the hybrid kernel) + gather. The
+    roofline is the local sort kernel's, from profiled single-rank steps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_21237_b200 import _capi
+    from paper_2602_21237_b200 import dist as D
+
+    if not dist.is_initialized():  # --dist at N=1: a one-rank NCCL group
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    n = keys_d.numel()
+    base = rank * n
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    active = active_digit_passes(keys_h)
+
+    def step(keys, pay):
+        return D.distributed_sort([keys, pay], 0, base)
+
+    def fingerprint(gid, key, pay4):
+        m1, m2, m3 = 0x9E3779B97F4A7C15 - (1 << 64), 0x7F4A7C159E3779B9, 0x2545F4914F6CDD1D
+        p32 = pay4.contiguous().view(torch.int32).reshape(-1).to(torch.int64)
+        return torch.stack([(gid * m1 ^ key * m2 ^ p32 * m3).sum(), gid.numel() * torch.ones((), dtype=torch.int64,
+                                                                                            device=gid.device)])
+
+    # correctness gate: globally sorted, stable, a permutation carrying its payload
+    res = step(keys_d, pay_d)
+    k, g, p = res.columns[0], res.gids, res.columns[1]
+    ok = bool((k[1:] >= k[:-1]).all()) if k.numel() > 1 else True
+    ties = k[1:] == k[:-1]
+    ok = ok and bool((g[1:][ties] > g[:-1][ties]).all())
+    mine = fingerprint(g, k, p)
+    want = fingerprint(torch.arange(n, device=dev, dtype=torch.int64) + base, keys_d, pay_d)
+    both = torch.stack([mine, want])
+    dist.all_reduce(both)
+    ok = ok and bool((both[0] == both[1]).all()) and int(both[0][1]) == world * n
+    edge = torch.tensor([k.numel(), int(k[0]) if k.numel() else 0, int(g[0]) if k.numel() else 0,
+                         int(k[-1]) if k.numel() else 0, int(g[-1]) if k.numel() else 0], dtype=torch.int64, device=dev)
+    edges = [torch.empty_like(edge) for _ in range(world)]
+    dist.all_gather(edges, edge)
+    last = None
+    for e in edges:
+        if int(e[0]) == 0:
+            continue
+        if last is not None and (int(e[1]), int(e[2])) < last:
+            ok = False
+        last = (int(e[3]), int(e[4]))
+    if not ok:
+        raise SystemExit("distributed sort failed its self-check; refusing to report a number")
+    del res, k, g, p, ties
+
+    for _ in range(args.warmup):
+        step(keys_d, pay_d)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    evs = [make_events(2) for _ in range(args.steps)]
+    launches0 = lib.rl_launch_count()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record()
+            step(keys_d, pay_d)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+    launches = lib.rl_launch_count() - launches0
+    dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = world * n * args.steps / (total_ms / 1e3) / 1e6
+
+    # roofline: the local sort kernel, profiled on this rank's shard
+    stamps = torch.zeros(_capi.RL_SORT_STAMPS, dtype=torch.int64, device=dev)
+    prof = [make_events(_capi.RL_SORT_EVENTS) for _ in range(5)]
+    for pe in prof:
+        flush.zero_()
+        device_step(pe, stamps)
+    torch.cuda.synchronize()
+    sort_ms = [pe[1].elapsed_time(pe[2]) for pe in prof]
+    hist_ms = [pe[0].elapsed_time(pe[1]) for pe in prof]
+    roofline = sort_roofline(n, active, stamps.cpu().tolist(), sort_ms, hist_ms,
+                             total_ms / args.steps * len(prof))
+    roofline["note"] = "local sort kernel of one rank (profiled steps); value includes partition + NCCL exchange"
+
+    # e2e: pinned host shard -> device -> distributed sort -> host (keys + payload of this rank's slice)
+    keys_pin = torch.from_numpy(np.array(keys_h)).pin_memory()
+    pay_pin = torch.from_numpy(np.array(pay_h)).pin_memory()
+    cap = 2 * n  # a rank receives ~n rows (splitters balance the shards); pinned landing buffers
+    out_k = torch.empty(cap, dtype=torch.int64).pin_memory()
+    out_p = torch.empty((cap, 4), dtype=torch.uint8).pin_memory()
+    d2h = []
+
+    def e2e_step():
+        kd = keys_pin.to(dev, non_blocking=True)
+        pd = pay_pin.to(dev, non_blocking=True)
+        r = step(kd, pd)
+        m = r.columns[0].numel()
+        dk, dp = (out_k[:m], out_p[:m]) if m <= cap else (torch.empty(m, dtype=torch.int64),
+                                                           torch.empty((m, 4), dtype=torch.uint8))
+        dk.copy_(r.columns[0], non_blocking=True)
+        dp.copy_(r.columns[1], non_blocking=True)
+        torch.cuda.synchronize()
+        d2h.append(m * 12)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    dist.barrier()
+    e2e_t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_t.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(e2e_t), float(sum(d2h[-args.steps:]))], dtype=torch.float64, device=dev)
+    tt = t.clone()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+    e2e_total = float(t[0].item())
+    e2e_value = world * n * args.steps / e2e_total / 1e6
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rows_per_gpu": n, "rows_total": world * n,
+                   "parallelism": f"range-partitioned sort over {world} rank(s): sampled splitters, NCCL all_to_all, "
+                                  "local stable sort",
+                   "l2": "flushed between timed steps (256 MiB write)", "seed_per_rank": "rank"},
+        "p50_ms": round(percentile(step_ms, 50), 4), "p99_ms": round(percentile(step_ms, 99), 4),
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": world * n * 12,
+                "d2h_bytes_per_step": int(float(tt[1].item()) / args.steps),
+                "api": "dist.distributed_sort from pinned host shards; sorted keys + payload back to host"},
+        "roofline": roofline,
+        "clocks": clocks.summary(),
+        "gpu_launches": int(launches),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def join_cfg1(args, dev, rank, world):
@@ -562,6 +722,8 @@ def main():
     ap.add_argument("--no-join", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time BASELINE cfg3/cfg4/cfg5 (a few more minutes)")
+    ap.add_argument("--dist", action="store_true",
+                    help="time the multi-GPU path (range partition + NCCL all-to-all + local sort) even at N=1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -36,14 +36,14 @@
 // Wide-key hybrid (raw int64 keys, n >= 2^18): when the top 16 key bits
 // spread the input into sub-buckets that fit on chip, the sort runs only
 // two onesweep passes — digit 6 then digit 7, i.e. stably by the top 16
-// bits — and the last of them also counts the 65536 (d7, d6) sub-bucket
-// sizes. One local phase then sorts every sub-bucket in shared memory
-// (stable 8-bit partition on its top varying byte, then insertion /
-// bitonic sorts of the few equal-digit rows by (key, row id)) and writes
-// the final keys, permutation and fused gathers. 2 + 1 passes over HBM
-// instead of 8. A sub-bucket larger than kLocalCap (skewed top bits) is
-// detected on the device after the two passes and the sort falls back
-// to the LSD kernel, launched behind it, which otherwise exits at once.
+// bits; the digit-7 pass also writes the 65536 sub-bucket starts from its
+// look-back prefixes (its input is digit-6 ordered). A local phase then
+// sorts every sub-bucket in shared memory ((sub-bucket, d5) counting
+// scatter, then each row's rank by (key, row id) among the rows equal in
+// their top 24 bits) and writes the final keys, permutation and fused
+// gathers: 2 passes + 1 streaming phase over HBM instead of 8 passes. A
+// sub-bucket larger than kLocalCap (skewed top bits) is caught after the
+// two passes and the same launch runs the LSD passes instead.
 //
 // Key transform (self-inverse): int64 ascending  u = x ^ 2^63;
 // descending u = ~x ^ 2^63 (the reference's np.invert, tensorpath.py:215,

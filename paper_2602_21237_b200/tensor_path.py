@@ -365,6 +365,28 @@ def _as_device_tensor(t) -> TensorRelation:
     return TensorRelation(t.schema, t.axes, t.key, t.key_values, t.offsets, t.positions)
 
 
+_D2H_STREAMS: dict = {}
+
+
+def _d2h_stream(dev) -> torch.cuda.Stream:
+    key = torch.device(dev).index
+    if key not in _D2H_STREAMS:
+        _D2H_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _D2H_STREAMS[key]
+
+
+def _host_out_on(dev_t: torch.Tensor, stream: torch.cuda.Stream) -> torch.Tensor:
+    """D2H of dev_t on `stream` once the current stream's work so far is done."""
+    host = torch.empty(dev_t.shape, dtype=dev_t.dtype, pin_memory=True)
+    ready = torch.cuda.Event()
+    ready.record()
+    stream.wait_event(ready)
+    with torch.cuda.stream(stream):
+        host.copy_(dev_t, non_blocking=True)
+    dev_t.record_stream(stream)
+    return host
+
+
 def _host_out(dev_t: torch.Tensor) -> torch.Tensor:
     host = torch.empty(dev_t.shape, dtype=dev_t.dtype, pin_memory=True)
     host.copy_(dev_t, non_blocking=True)
@@ -432,7 +454,13 @@ def tensor_sort(rel, spec):
     key_j = rel.schema.index(spec.keys[0])
     sorted_key = torch.empty(n, dtype=torch.int64, device=dev) if single_int else None
     perm = engine.sort_permutation(axes, n, dev, sorted_keys_out=sorted_key)
-    outs, gathers = [], []
+    # PCIe is full duplex: the sorted key column goes down on its own stream
+    # while the payload columns are still coming up for the gather
+    down = _d2h_stream(dev)
+    hosts = [None] * len(rel.columns)
+    if single_int:
+        hosts[key_j] = _host_out_on(sorted_key, down)
+    outs, gathers, idx = [], [], []
     for j, (_, t) in enumerate(rel.schema.attributes):
         if single_int and j == key_j:
             outs.append(sorted_key)
@@ -440,9 +468,11 @@ def tensor_sort(rel, spec):
         col = _out_column(up.get(j), t, n, dev, C.RL_SIDE_LEFT)  # uploads overlap the sort
         gathers.append(col)
         outs.append(col.dst)
+        idx.append(j)
     engine.gather_rows(perm, gathers)
-    hosts = [_host_out(o) for o in outs]
-    torch.cuda.current_stream().synchronize()
+    for j, col in zip(idx, gathers):
+        hosts[j] = _host_out_on(col.dst, down)
+    down.synchronize()
     out = rel_cls(rel.schema, tuple(h.numpy() for h in hosts))
     stats = TYPES["SpillStats"](
         peak_mem_bytes=2 * 4 * n + sum(o.numel() * o.element_size() for o in outs),

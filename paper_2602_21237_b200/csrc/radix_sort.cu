@@ -150,7 +150,8 @@ struct SortArgs {
   uint32_t* ghist;           // [kPasses][kBins]
   uint32_t* tile_counter;    // [2][kPasses] (first attempt, LSD after a hybrid fallback)
   uint32_t* grid_bar;        // grid barrier arrivals
-  uint32_t* flags;           // [0] a sub-bucket exceeds kLocalCap -> LSD fallback, [1] local work-item counter
+  uint32_t* flags;           // [0] a sub-bucket exceeds kLocalCap -> LSD fallback, [1] local work-item counter,
+                             // [4..5] raw int64 keys: OR of (key ^ first key) = the varying bits (u64)
   uint32_t* sub_off;         // [kSubBuckets + 1] sub-bucket starts, hybrid (not zeroed)
   uint64_t* status;          // [num_tiles][kBins] look-back words (epoch = pass + 1)
   unsigned long long* stamps;  // optional [kStamps] globaltimer ns (device)
@@ -218,7 +219,7 @@ constexpr size_t kLocMisc = kLocBig + size_t(kBigList) * 4;
 // [72..103] run ends (x2), [112..] run descriptors
 constexpr size_t kLocBars = kLocMisc + 128 * 4;
 constexpr size_t kLocalSmemBytes = kLocBars + 2 * 8;
-constexpr size_t kSmemBytes = std::max(kPassSmemBytes + size_t(kPasses) * kBins * 4 + 64, kLocalSmemBytes);
+constexpr size_t kSmemBytes = std::max(kPassSmemBytes + size_t(kPasses) * kBins * 4 + 128, kLocalSmemBytes);
 
 struct PassState {  // per-CTA mbarrier phase parities, carried across passes
   uint32_t phase0, phase1;
@@ -526,9 +527,20 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
   for (int i = tid; i < kPasses * kBins; i += kHistThreads) h[i] = 0;
   __syncthreads();
+  // RAW counts only the top two digits (the hybrid's passes) and ORs the
+  // varying bits: which digits an LSD sort needs, counted later in the sort
+  // kernel only if it goes LSD, and only for digits that vary
+  uint64_t vary = 0, k0 = 0;
+  if constexpr (RAW) k0 = xform(uint64_t(__ldg(static_cast<const long long*>(a.col))), a.desc);
   auto count = [&](uint64_t k) {
+    if constexpr (RAW) {
+      vary |= k ^ k0;
+      atomicAdd(&h[6 * kBins + ((k >> (6 * kBits)) & (kBins - 1))], 1u);
+      atomicAdd(&h[7 * kBins + ((k >> (7 * kBits)) & (kBins - 1))], 1u);
+    } else {
 #pragma unroll
-    for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p * kBins + ((k >> (p * kBits)) & (kBins - 1))], 1u);
+      for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p * kBins + ((k >> (p * kBits)) & (kBins - 1))], 1u);
+    }
   };
   if constexpr (RAW) {
     const ulonglong2* v2 = static_cast<const ulonglong2*>(a.col);  // 16-byte aligned (checked by the caller)
@@ -570,10 +582,56 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
       }
     }
   }
+  if constexpr (RAW) {
+    const uint32_t hi = __reduce_or_sync(0xffffffffu, uint32_t(vary >> 32));
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, uint32_t(vary));
+    if ((tid & 31) == 0 && (hi | lo))
+      atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(hi) << 32) | lo);
+  }
   __syncthreads();
-  for (int i = tid; i < kPasses * kBins; i += kHistThreads) {
+  for (int i = RAW ? 6 * kBins + tid : tid; i < kPasses * kBins; i += kHistThreads) {
     const uint32_t c = h[i];
     if (c) atomicAdd(&a.ghist[i], c);
+  }
+}
+
+// In-kernel histograms of the varying digits in `digits` (bit p = digit p)
+// of raw int64 keys, by every CTA of the cooperative kernel (the LSD path
+// after the RAW histogram kernel, which counted only digits 6 and 7).
+__device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) {
+  uint32_t* h = reinterpret_cast<uint32_t*>(smem);  // [kPasses][kBins]; pass buffers are free here
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kPasses * kBins; i += kThreads) h[i] = 0;
+  __syncthreads();
+  const ulonglong2* v2 = static_cast<const ulonglong2*>(a.col);
+  const int64_t pairs = a.n >> 1;
+  constexpr int kV = 8;
+  auto count = [&](uint64_t k) {
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+      if ((digits >> p) & 1u) atomicAdd(&h[p * kBins + ((k >> (p * kBits)) & (kBins - 1))], 1u);
+  };
+  const int64_t stride = int64_t(gridDim.x) * kThreads * kV;
+  for (int64_t base = int64_t(blockIdx.x) * kThreads * kV + tid; base < pairs; base += stride) {
+    ulonglong2 q[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t i = base + int64_t(u) * kThreads;
+      q[u] = i < pairs ? __ldcs(v2 + i) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      if (base + int64_t(u) * kThreads < pairs) {
+        count(xform(q[u].x, a.desc));
+        count(xform(q[u].y, a.desc));
+      }
+    }
+  }
+  if ((a.n & 1) && blockIdx.x == 0 && tid == 0) count(xform(uint64_t(static_cast<const long long*>(a.col)[a.n - 1]), a.desc));
+  __syncthreads();
+  for (int i = tid; i < 6 * kBins; i += kThreads) {
+    const uint32_t c = h[i];
+    if (c && ((digits >> (i / kBins)) & 1u)) atomicAdd(&a.ghist[i], c);
   }
 }
 
@@ -876,7 +934,7 @@ __device__ void run_passes(const SortArgs& a, uint8_t* smem, const uint32_t* bin
 __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(SortArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* bin_off = reinterpret_cast<uint32_t*>(smem + kPassSmemBytes);  // [kPasses][kBins], whole kernel
-  uint32_t* plan = bin_off + kPasses * kBins;  // [0..7] active, [8] n_active, [9] hybrid, [10..17] hybrid passes
+  uint32_t* plan = bin_off + kPasses * kBins;  // [0..7] active, [8] n_active, [9] hybrid, [10..17] hybrid passes, [18] their count, [19] low digits to count
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
   const int tid = threadIdx.x;
   uint32_t barrier_no = 0;
@@ -885,11 +943,25 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   // ---- histograms come from hist_kernel (launched just before, on the same stream)
   if (stamper) a.stamps[1] = globaltimer();
 
-  // ---- plan (every CTA for itself): global digit bases + active digits
+  // ---- plan (every CTA for itself): global digit bases + active digits.
+  // Raw int64 keys: the histogram kernel counted digits 6 and 7 and ORed
+  // the varying bits; the other digits are counted here only on the LSD
+  // path, and only if they vary.
+  const bool raw = a.src_mode == kSrcInt64;
+  auto scan_rows = [&](int p0, int p1) {  // bin_off rows [p0, p1) from the global histograms
+    uint32_t* warp_sums = reinterpret_cast<uint32_t*>(smem);  // scratch
+    for (int p = p0; p < p1; ++p) {
+      const uint32_t c = __ldcg(a.ghist + p * kBins + tid);
+      uint32_t total;
+      bin_off[p * kBins + tid] = block_exclusive_scan<kThreads>(c, warp_sums, &total);
+      __syncthreads();
+    }
+  };
   {
     uint32_t* warp_sums = reinterpret_cast<uint32_t*>(smem);  // scratch
+    const uint64_t vary = raw ? __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4)) : 0ull;
     uint32_t nz = 1, mx = 1;
-    for (int p = 0; p < kPasses; ++p) {
+    for (int p = raw ? 6 : 0; p < kPasses; ++p) {
       const uint32_t c = __ldcg(a.ghist + p * kBins + tid);
       uint32_t total;
       bin_off[p * kBins + tid] = block_exclusive_scan<kThreads>(c, warp_sums, &total);
@@ -907,9 +979,11 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
         mx = p == 6 ? m : uint32_t(est > 0xFFFFFFFFull ? 0xFFFFFFFFull : est);
         __syncthreads();
       }
-      if (tid == 0) plan[p] = full ? 0u : 1u;
+      if (tid == 0 && !raw) plan[p] = full ? 0u : 1u;
     }
     if (tid == 0) {
+      if (raw)
+        for (int p = 0; p < kPasses; ++p) plan[p] = ((vary >> (p * kBits)) & (kBins - 1)) ? 1u : 0u;
       uint32_t na = 0;
       for (int p = 0; p < kPasses; ++p) na += plan[p];
       plan[kPasses] = na;
@@ -921,11 +995,23 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       plan[kPasses + 1] = hyb ? 1u : 0u;
       for (int p = 0; p < kPasses; ++p) plan[kPasses + 2 + p] = p >= 6 ? plan[p] : 0u;
       plan[2 * kPasses + 2] = plan[6] + plan[7];
+      uint32_t low = 0;
+      for (int p = 0; p < 6; ++p) low |= plan[p] << p;
+      plan[2 * kPasses + 3] = raw ? low : 0u;  // digits the LSD path still has to count
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
     }
     __syncthreads();
   }
+  // raw keys going LSD: count the varying low digits now (every CTA), then their bases
+  auto count_low_digits = [&]() {
+    const uint32_t low = plan[2 * kPasses + 3];
+    if (!low) return;
+    count_digits(a, smem, low);
+    grid_sync(a.grid_bar, ++barrier_no);
+    scan_rows(0, 6);
+  };
+  if (!plan[kPasses + 1]) count_low_digits();
 
   PassState ps{0, 0};
   uint32_t src = 0;
@@ -968,6 +1054,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
     // a sub-bucket does not fit on chip: the LSD sort, fresh epochs and counters
     if (stamper)
       for (int p = 0; p < kPasses; ++p) a.stamps[2 + p] = 0;
+    count_low_digits();
   }
 
   // ---- LSD: the active digit passes, least significant first
@@ -1010,7 +1097,7 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   auto h = t32(c, kPasses * kBins);
   auto tc = t32(c, 2 * kPasses);
   auto gb = t32(c, 2);
-  auto fl = t32(c, 4);
+  auto fl = t32(c, 8);
   auto st = t64(c, tiles * kBins);
   const size_t zero = c.used;
   auto so = t32(c, kSubBuckets + 1);

@@ -77,15 +77,86 @@ class GpuOps:
         perm = engine.sort_permutation([engine.SortAxis(keys, descending)], keys.numel(), keys.device)
         return perm.to(torch.int64) & 0xFFFFFFFF
 
+    # fused forms (one launch for every column) used when an Ops object has them
+    def partition_take(self, kind: str, keys: torch.Tensor, cols: Sequence[torch.Tensor], **kw):
+        """Partition + every column gathered into destination order in one
+        gather launch (rl_hash_partition / rl_range_partition with columns)."""
+        from . import engine
+
+        outs = [torch.empty_like(c) for c in cols]
+        oc = [engine.OutColumn(c.contiguous(), o, _row_bytes(c), 0) for c, o in zip(cols, outs)]
+        if kind == "hash":
+            rows, counts = engine.hash_partition(keys, kw["parts"], kw["seed"], columns=oc)
+        else:
+            rows, counts = engine.range_partition(keys, kw["gid_base"], kw["split_keys"], kw["split_gids"],
+                                                  kw["descending"], columns=oc)
+        return rows, counts, outs
+
+    def sort_take(self, cols: Sequence[torch.Tensor], key_idx: int, descending: bool):
+        """Stable sort by the int64 column key_idx: the sort kernel writes the
+        sorted keys itself; every other column in one gather launch."""
+        from . import engine
+
+        keys = cols[key_idx]
+        n = keys.numel()
+        sk = torch.empty_like(keys)
+        outs = [sk if j == key_idx else torch.empty_like(c) for j, c in enumerate(cols)]
+        gather = [engine.OutColumn(c.contiguous(), outs[j], _row_bytes(c), 0) for j, c in enumerate(cols) if j != key_idx]
+        if n:
+            engine.sort_permutation([engine.SortAxis(keys, descending)], n, keys.device, sorted_keys_out=sk,
+                                    gather=gather)
+        return outs
+
+
+def _row_bytes(c: torch.Tensor) -> int:
+    return c.element_size() * (c.shape[1] if c.dim() > 1 else 1)
+
+
+def _partition_take(ops, kind, keys, cols, **kw):
+    if hasattr(ops, "partition_take"):
+        return ops.partition_take(kind, keys, cols, **kw)
+    if kind == "hash":
+        rows, counts = ops.hash_partition(keys, kw["parts"], kw["seed"])
+    else:
+        rows, counts = ops.range_partition(keys, kw["gid_base"], kw["split_keys"], kw["split_gids"], kw["descending"])
+    return rows, counts, [ops.take(c, rows) for c in cols]
+
+
+def _sort_take(ops, cols, key_idx, descending):
+    if hasattr(ops, "sort_take"):
+        return ops.sort_take(cols, key_idx, descending)
+    perm = ops.stable_order(cols[key_idx], descending)
+    return [ops.take(c, perm) for c in cols]
+
+
+def _global_ids(rows: torch.Tensor, recv_counts: list, bases: list) -> torch.Tensor:
+    """int64 global row ids of received rows: the sender's base + its local
+    row id (row ids travel as 4 bytes, not 8)."""
+    r = rows.to(torch.int64) & 0xFFFFFFFF
+    off = 0
+    for c, b in zip(recv_counts, bases):  # P slices, one in-place add each
+        if c and b:
+            r[off:off + c] += b
+        off += c
+    return r
+
+
+def _all_bases(base: int, device, group) -> list:
+    t = torch.tensor([base], dtype=torch.int64, device=device)
+    out = [torch.empty_like(t) for _ in range(_group_size(group))]
+    dist.all_gather(out, t, group=group)
+    return [int(x.item()) for x in out]
+
 
 def _group_size(group) -> int:
     return dist.get_world_size(group)
 
 
-def exchange(columns: Sequence[torch.Tensor], send_counts: torch.Tensor, group=None) -> List[torch.Tensor]:
+def exchange(columns: Sequence[torch.Tensor], send_counts: torch.Tensor, group=None, with_counts: bool = False):
     """all-to-all-v of row-grouped columns. ``columns`` are grouped by
     destination rank (rank order), ``send_counts[d]`` rows for rank d. Returns
-    the received columns, grouped by source rank, each group in source order."""
+    the received columns, grouped by source rank, each group in source order
+    (and the per-source row counts with ``with_counts``)."""
     p = _group_size(group)
     counts = send_counts.to(torch.int64).reshape(p)
     recv_counts = torch.empty_like(counts)
@@ -98,7 +169,7 @@ def exchange(columns: Sequence[torch.Tensor], send_counts: torch.Tensor, group=N
         dst = torch.empty((sum(recv_l),) + tuple(col.shape[1:]), dtype=col.dtype, device=col.device)
         dist.all_to_all_single(dst, col, output_split_sizes=recv_l, input_split_sizes=send_l, group=group)
         out.append(dst)
-    return out
+    return (out, recv_l) if with_counts else out
 
 
 @dataclass
@@ -120,13 +191,10 @@ def distributed_join(left: Sequence[torch.Tensor], left_key: int, left_base: int
     dev = left[left_key].device
 
     def shuffle(cols, key_idx, base):
-        n = cols[key_idx].shape[0]
-        rows, counts = ops.hash_partition(cols[key_idx], p, seed)
-        gids = rows.to(torch.int64) & 0xFFFFFFFF
-        gids = gids + base
-        moved = [ops.take(c, rows) for c in cols]
-        recv = exchange(moved + [gids], counts, group)
-        return recv[:-1], recv[-1]
+        rows, counts, moved = _partition_take(ops, "hash", cols[key_idx], list(cols), parts=p, seed=seed)
+        bases = _all_bases(base, dev, group)
+        recv, rc = exchange(moved + [rows], counts, group, with_counts=True)
+        return recv[:-1], _global_ids(recv[-1], rc, bases)
 
     lcols, lgids = shuffle(list(left), left_key, left_base)
     rcols, rgids = shuffle(list(right), right_key, right_base)
@@ -138,40 +206,39 @@ def distributed_join(left: Sequence[torch.Tensor], left_key: int, left_base: int
     return JoinShard(out, lgids[lrows], rgids[rrows], int(total.item()))
 
 
-def choose_splitters(keys: torch.Tensor, gid_base: int, descending: bool, group=None, per_rank: int = 256):
-    """Regular sampling of (key, global id); all-gather; P-1 splitters on the
-    composite order. Every rank computes the same splitters."""
+def choose_splitters(keys: torch.Tensor, gid_base: int, descending: bool, group=None, per_rank: int = 256,
+                     with_bases: bool = False):
+    """Regular sampling of (key, global id); ONE all-gather of every rank's
+    samples (and its row-id base); P-1 splitters on the composite order.
+    Every rank computes the same splitters."""
     p = _group_size(group)
     n = keys.numel()
-    idx = (torch.arange(per_rank, device=keys.device, dtype=torch.int64) * max(n, 1)) // per_rank
-    idx = idx[idx < n] if n else idx[:0]
-    sk = keys[idx] if n else keys[:0]
-    sg = idx + gid_base
-    cnt = torch.tensor([sk.numel()], dtype=torch.int64, device=keys.device)
-    counts = [torch.zeros_like(cnt) for _ in range(p)]
-    dist.all_gather(counts, cnt, group=group)
-    mx = int(max(c.item() for c in counts))
-    pad_k = torch.zeros(mx, dtype=torch.int64, device=keys.device)
-    pad_g = torch.full((mx,), -1, dtype=torch.int64, device=keys.device)
-    pad_k[: sk.numel()] = sk
-    pad_g[: sg.numel()] = sg
-    all_k = [torch.empty_like(pad_k) for _ in range(p)]
-    all_g = [torch.empty_like(pad_g) for _ in range(p)]
-    dist.all_gather(all_k, pad_k, group=group)
-    dist.all_gather(all_g, pad_g, group=group)
-    ks = torch.cat([k[: int(c.item())] for k, c in zip(all_k, counts)]).cpu()
-    gs = torch.cat([g[: int(c.item())] for g, c in zip(all_g, counts)]).cpu()
+    m = min(per_rank, n)
+    idx = (torch.arange(m, device=keys.device, dtype=torch.int64) * max(n, 1)) // max(m, 1)
+    pack = torch.zeros(2 + 2 * per_rank, dtype=torch.int64, device=keys.device)
+    pack[0] = m
+    pack[1] = gid_base
+    if m:
+        pack[2:2 + m] = keys[idx]
+        pack[2 + per_rank:2 + per_rank + m] = idx + gid_base
+    packs = [torch.empty_like(pack) for _ in range(p)]
+    dist.all_gather(packs, pack, group=group)
+    host = torch.stack(packs).cpu()
+    bases = [int(v) for v in host[:, 1].tolist()]
+    ks = torch.cat([h[2:2 + int(h[0])] for h in host])
+    gs = torch.cat([h[2 + per_rank:2 + per_rank + int(h[0])] for h in host])
     if ks.numel() == 0:
         e = torch.empty(0, dtype=torch.int64, device=keys.device)
-        return e, e
+        return (e, e, bases) if with_bases else (e, e)
     ordk = torch.bitwise_not(ks) if descending else ks
     # composite (key, gid) order: stable sort by gid then by key
     o = torch.argsort(gs, stable=True)
     o = o[torch.argsort(ordk[o], stable=True)]
     ks, gs = ks[o], gs[o]
-    m = ks.numel()
-    picks = [min(m - 1, (i * m) // p) for i in range(1, p)]
-    return ks[picks].to(keys.device), gs[picks].to(keys.device)
+    cnt = ks.numel()
+    picks = [min(cnt - 1, (i * cnt) // p) for i in range(1, p)]
+    sk, sg = ks[picks].to(keys.device), gs[picks].to(keys.device)
+    return (sk, sg, bases) if with_bases else (sk, sg)
 
 
 @dataclass
@@ -185,11 +252,11 @@ def distributed_sort(cols: Sequence[torch.Tensor], key_idx: int, gid_base: int, 
     """Range-partitioned stable ORDER BY on one int64 key (see module doc)."""
     ops = ops or GpuOps()
     keys = cols[key_idx]
-    split_k, split_g = choose_splitters(keys, gid_base, descending, group)
-    rows, counts = ops.range_partition(keys, gid_base, split_k, split_g, descending)
-    gids = (rows.to(torch.int64) & 0xFFFFFFFF) + gid_base
-    moved = [ops.take(c, rows) for c in cols]
-    recv = exchange(moved + [gids], counts, group)
-    rcols, rgids = recv[:-1], recv[-1]
-    perm = ops.stable_order(rcols[key_idx], descending)  # arrival order = ascending gid
-    return SortShard([ops.take(c, perm) for c in rcols], rgids[perm])
+    split_k, split_g, bases = choose_splitters(keys, gid_base, descending, group, with_bases=True)
+    rows, counts, moved = _partition_take(ops, "range", keys, list(cols), gid_base=gid_base, split_keys=split_k,
+                                          split_gids=split_g, descending=descending)
+    recv, rc = exchange(moved + [rows], counts, group, with_counts=True)
+    rcols, rgids = recv[:-1], _global_ids(recv[-1], rc, bases)
+    # arrival order = ascending global row id, so the stable local sort keeps the reference tie order
+    out = _sort_take(ops, list(rcols) + [rgids], key_idx, descending)
+    return SortShard(out[:-1], out[-1])

@@ -52,20 +52,33 @@ __global__ void __launch_bounds__(kThreads) run_bounds_kernel(const int64_t* __r
   if (tid == 0) stage[0] = begin > 0 ? sk[begin - 1] : 0;
   __syncthreads();
 
-  // blocked ownership: thread owns elements [tid*items, tid*items+items)
-  uint32_t flags = 0, c = 0;
+  // warp w owns the 512 consecutive elements [512 w, 512 w + 512), 32 per
+  // round (conflict-free 8-byte reads); run heads by ballot, so each round
+  // writes its heads to consecutive slots (coalesced)
+  constexpr int kSeg = 32 * kRbItems;
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = lanemask_lt();
+  uint32_t bal[kRbItems];
+  uint32_t c = 0;
 #pragma unroll
   for (int it = 0; it < kRbItems; ++it) {
-    const int e = tid * kRbItems + it;
-    if (e < count) {
-      const bool head = (begin + e == 0) || (stage[e + 1] != stage[e]);
-      flags |= uint32_t(head) << it;
-      c += head;
-    }
+    const int e = warp * kSeg + it * 32 + lane;
+    const bool head = e < count && ((begin + e == 0) || (stage[e + 1] != stage[e]));
+    bal[it] = __ballot_sync(0xffffffffu, head);
+    c += __popc(bal[it]);
   }
-  uint32_t tile_total;
-  const uint32_t off = block_exclusive_scan<kThreads>(c, warp_sums, &tile_total);
+  if (lane == 0) warp_sums[warp] = c;
+  __syncthreads();
   if (tid < 32) {
+    const uint32_t v = tid < kThreads / 32 ? warp_sums[tid] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (tid >= o) incl += x;
+    }
+    const uint32_t tile_total = __shfl_sync(0xffffffffu, incl, kThreads / 32 - 1);
+    if (tid < kThreads / 32) warp_sums[tid] = incl - v;  // exclusive warp offsets
     if (tile == 0) {
       if (tid == 0) st_relaxed(&status[0], pack_status(kFlagIncl, 1, tile_total));
       if (tid == 0) s_excl = 0;
@@ -77,18 +90,20 @@ __global__ void __launch_bounds__(kThreads) run_bounds_kernel(const int64_t* __r
         s_excl = excl;
       }
     }
+    if (tid == 0) warp_sums[kThreads / 32] = tile_total;
   }
   __syncthreads();
-  const uint64_t base = s_excl + off;
-  uint32_t k = 0;
+  const uint32_t tile_total = warp_sums[kThreads / 32];
+  uint64_t pos = s_excl + warp_sums[warp];
 #pragma unroll
   for (int it = 0; it < kRbItems; ++it) {
-    if (flags & (1u << it)) {
-      const int e = tid * kRbItems + it;
-      key_values[base + k] = stage[e + 1];
-      offsets[base + k] = uint32_t(begin + e);
-      ++k;
+    const int e = warp * kSeg + it * 32 + lane;
+    if (bal[it] & (1u << lane)) {
+      const uint64_t o = pos + __popc(bal[it] & lt);
+      key_values[o] = stage[e + 1];
+      offsets[o] = uint32_t(begin + e);
     }
+    pos += __popc(bal[it]);
   }
   if (tile == num_tiles - 1 && tid == 0) {
     const uint64_t d = s_excl + tile_total;

@@ -17,6 +17,11 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
               cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
               int n_columns);
+int sort_axis_capped(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
+                     int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
+                     cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
+                     int n_columns, int max_ctas);
+int sort_grid_capacity();
 }  // namespace radix
 namespace keyaxis {
 size_t run_bounds_workspace_bytes(int64_t n);
@@ -59,12 +64,24 @@ struct Sizer {  // CarveSize with the pointer-returning interface of Carve
   }
 };
 
-static size_t scratch_bytes(int64_t nl, int64_t nr) {
-  const int64_t n = std::max(nl, nr);
+// Both sides are indexed concurrently (two streams, each sort on half the
+// co-resident grid) when they are small enough to be latency-bound; each
+// side then needs its own scratch.
+constexpr int64_t kConcurrentMaxRows = int64_t(16) << 20;
+static bool concurrent_sides(int64_t nl, int64_t nr) {
+  return nl > 0 && nr > 0 && std::max(nl, nr) <= kConcurrentMaxRows;
+}
+
+static size_t side_scratch_bytes(int64_t n) {
   size_t s = align_up(size_t(std::max<int64_t>(n, 1)) * 8, 256);  // sorted keys
   size_t inner = std::max(radix::workspace_bytes(n), keyaxis::run_bounds_workspace_bytes(n));
-  inner = std::max(inner, keyaxis::align_workspace_bytes(nl));
   return s + align_up(inner, 256) + 256;
+}
+
+static size_t scratch_bytes(int64_t nl, int64_t nr) {
+  const int64_t n = std::max(nl, nr);
+  size_t one = std::max(side_scratch_bytes(n), align_up(keyaxis::align_workspace_bytes(nl), 256) + 256);
+  return concurrent_sides(nl, nr) ? 2 * one : one;
 }
 
 size_t workspace_bytes(int64_t nl, int64_t nr) {
@@ -72,6 +89,28 @@ size_t workspace_bytes(int64_t nl, int64_t nr) {
   rl_join_plan p;
   carve_plan(z, nl, nr, &p);
   return align_up(z.used, 256) + scratch_bytes(nl, nr) + 256;
+}
+
+// Per-host-thread auxiliary stream + fork/join events (created once).
+struct Aux {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int device = -1;
+};
+static Aux* aux_for_current_device() {
+  thread_local Aux aux;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (aux.device != dev) {
+    if (cudaStreamCreateWithFlags(&aux.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&aux.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&aux.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    aux.device = dev;
+  }
+  return &aux;
 }
 
 int build(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, void* ws, size_t ws_bytes,
@@ -84,10 +123,9 @@ int build(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, vo
   if (!c.ok) return RL_ERR_WORKSPACE;
   char* scratch = c.base + align_up(c.used, 256);
   const size_t scratch_cap = ws_bytes - align_up(c.used, 256);
-  int64_t* sorted = reinterpret_cast<int64_t*>(scratch);
-  const size_t sorted_bytes = align_up(size_t(std::max(std::max<int64_t>(nl, nr), int64_t(1))) * 8, 256);
-  void* inner = scratch + sorted_bytes;
-  const size_t inner_cap = scratch_cap - sorted_bytes;
+  Aux* aux = concurrent_sides(nl, nr) ? aux_for_current_device() : nullptr;
+  const int half = aux ? std::max(1, radix::sort_grid_capacity() / 2) : 0;
+  const size_t per_side = aux ? scratch_cap / 2 / 256 * 256 : scratch_cap;
 
   struct Side {
     const int64_t* keys;
@@ -98,14 +136,33 @@ int build(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, vo
     int64_t* d;
   } sides[2] = {{lkeys, nl, p->left_positions, p->left_key_values, p->left_offsets, p->scalars + 0},
                 {rkeys, nr, p->right_positions, p->right_key_values, p->right_offsets, p->scalars + 1}};
-  for (const Side& sd : sides) {
+  if (aux) {  // right side on the auxiliary stream, after everything already queued on `stream`
+    cudaError_t e = cudaEventRecord(aux->fork, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(aux->stream, aux->fork, 0);
+    if (e != cudaSuccess) return rl_cuda_status(e);
+  }
+  for (int i = 0; i < 2; ++i) {
+    const Side& sd = sides[i];
+    cudaStream_t st_i = (aux && i == 1) ? aux->stream : stream;
+    char* base = scratch + (aux ? i * per_side : 0);
+    int64_t* sorted = reinterpret_cast<int64_t*>(base);
+    const size_t sorted_bytes = align_up(size_t(std::max(std::max<int64_t>(nl, nr), int64_t(1))) * 8, 256);
+    void* inner = base + sorted_bytes;
+    const size_t inner_cap = per_side - sorted_bytes;
     if (sd.n > 0) {
-      int st = radix::sort_axis(sd.keys, RL_COL_INT64, 8, 0, 0, nullptr, sd.n, sorted, sd.pos, inner, inner_cap,
-                                stream, nullptr, nullptr, nullptr, 0);
+      int st = radix::sort_axis_capped(sd.keys, RL_COL_INT64, 8, 0, 0, nullptr, sd.n, sorted, sd.pos, inner, inner_cap,
+                                       st_i, nullptr, nullptr, nullptr, 0, half);
       if (st != RL_OK) return st;
     }
-    int st = keyaxis::run_bounds(sd.n > 0 ? sorted : sd.keys, sd.n, sd.kv, sd.off, sd.d, inner, inner_cap, stream);
+    int st = keyaxis::run_bounds(sd.n > 0 ? sorted : sd.keys, sd.n, sd.kv, sd.off, sd.d, inner, inner_cap, st_i);
     if (st != RL_OK) return st;
+  }
+  void* inner = scratch;  // the alignment reuses the first scratch (both sides are done with it)
+  const size_t inner_cap = per_side;
+  if (aux) {  // join: the alignment waits for the right side
+    cudaError_t e = cudaEventRecord(aux->join, aux->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, aux->join, 0);
+    if (e != cudaSuccess) return rl_cuda_status(e);
   }
   const int64_t cap = std::min(nl, nr) > 0 ? nl : 0;
   return keyaxis::key_axis_align(p->left_key_values, p->left_offsets, p->scalars + 0, cap, p->right_key_values,

@@ -85,7 +85,10 @@ constexpr int kLookback = RL_LOOKBACK_WINDOW;
 constexpr int kHistUnroll = RL_HIST_UNROLL;
 constexpr int kStamps = 2 + kPasses + 2;  // per-phase globaltimer stamps + the path taken (profiling)
 // wide-key hybrid
-constexpr int kLocalCap = 2560;            // rows of one on-chip local run (and the largest sub-bucket)
+#ifndef RL_LOCAL_CAP
+#define RL_LOCAL_CAP 2560
+#endif
+constexpr int kLocalCap = RL_LOCAL_CAP;    // rows of one on-chip local run (and the largest sub-bucket)
 constexpr int kSubBuckets = 1 << 16;       // (d7, d6) sub-buckets
 constexpr int kGroupSubs = 16;             // sub-buckets claimed per local work item
 constexpr int64_t kHybridMinRows = 1 << 18;
@@ -1155,8 +1158,9 @@ static int hist_grid(int64_t n) {  // one co-resident wave (2 CTAs of 512 thread
 
 // Histograms, then the cooperative kernel (LSD, or the wide-key hybrid
 // with its in-kernel LSD fallback).
-static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* const* events) {
-  const int limit = sort_grid_limit();
+static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* const* events, int max_ctas = 0) {
+  int limit = sort_grid_limit();
+  if (max_ctas > 0 && limit > max_ctas) limit = max_ctas;  // leave room for a concurrent sort
   if (limit < 1) {
     cudaError_t e = cudaGetLastError();
     return rl_cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration);
@@ -1179,10 +1183,10 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
 }
 
-int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
-              int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
-              cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
-              int n_columns) {
+int sort_axis_capped(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
+                     int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
+                     cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
+                     int n_columns, int max_ctas) {
   if (n_columns < 0 || n_columns > kMaxFusedColumns || (n_columns > 0 && columns == nullptr)) return RL_ERR_BAD_ARG;
   for (int i = 0; i < n_columns; ++i)
     if (columns[i].width < 0 || columns[i].side != RL_SIDE_LEFT ||
@@ -1249,7 +1253,18 @@ int sort_axis(const void* col, int col_kind, int width, int word, int descending
     a.orig_keys = L.keys_b;
     a.out_keys = nullptr;
   }
-  return launch_sort(a, L, stream, events);
+  return launch_sort(a, L, stream, events, max_ctas);
+}
+
+// Co-resident CTAs of the cooperative sort kernel on this device (0 if unknown).
+int sort_grid_capacity() { return std::max(0, sort_grid_limit()); }
+
+int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
+              int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
+              cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
+              int n_columns) {
+  return sort_axis_capped(col, col_kind, width, word, descending, perm_in, n, sorted_keys_out, perm_out, ws,
+                          ws_bytes, stream, events, stamps, columns, n_columns, 0);
 }
 
 // ---------------------------------------------------------------- K8

@@ -250,9 +250,27 @@ __device__ __forceinline__ void warp_lookback2(const AlignArgs& a, uint32_t tile
   *excl_p = ep;
 }
 
+// Dynamic shared memory of align_kernel.
+constexpr size_t kAlSl = 0;                                   // int64 [kAlTile] left keys of the tile
+constexpr size_t kAlSr = kAlSl + size_t(kAlTile) * 8;         // int64 [kAlWindow] right window
+constexpr size_t kAlMi = kAlSr + size_t(kAlWindow) * 8;       // uint32 [kAlTile] match: tile-local left index
+constexpr size_t kAlMj = kAlMi + size_t(kAlTile) * 4;         // uint32 [kAlTile] match: right index
+constexpr size_t kAlSmem = kAlMj + size_t(kAlTile) * 4;
+
+// One tile of kAlTile left distinct keys. The matching window of right
+// distinct keys is staged, then merge path: thread t takes diagonals
+// [t E, (t+1) E) of the merged (left, right) order — one binary search for
+// its split, then a sequential walk (a key present on both sides is a
+// match) — so the tile costs ~log(window) + E shared reads per thread
+// instead of a binary search per key. Matches are listed in shared memory
+// in left order, then resolved and written striped (coalesced), with the
+// pair prefix from per-round block scans and a two-value look-back.
 __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
-  __shared__ int64_t sl[kAlTile];        // this tile's left distinct keys
-  __shared__ int64_t sr[kAlWindow];      // the matching window of right distinct keys
+  extern __shared__ __align__(16) uint8_t asmem[];
+  int64_t* sl = reinterpret_cast<int64_t*>(asmem + kAlSl);
+  int64_t* sr = reinterpret_cast<int64_t*>(asmem + kAlSr);
+  uint32_t* mi = reinterpret_cast<uint32_t*>(asmem + kAlMi);
+  uint32_t* mj = reinterpret_cast<uint32_t*>(asmem + kAlMj);
   __shared__ uint32_t warp_m[kThreads / 32 + 1];
   __shared__ uint64_t warp_p[kThreads / 32 + 1];
   __shared__ uint32_t s_tile, s_lo, s_hi;
@@ -285,49 +303,68 @@ __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
   }
   __syncthreads();
   const uint32_t lo = s_lo, hi = max(s_lo, s_hi);
-  const bool staged = hi - lo <= uint32_t(kAlWindow);
+  const uint32_t w = hi - lo;
+  const bool staged = w <= uint32_t(kAlWindow);
   if (staged)
-    for (uint32_t i = tid; i < hi - lo; i += kThreads) sr[i] = __ldg(reinterpret_cast<const long long*>(a.rkeys) + lo + i);
+    for (uint32_t i = tid; i < w; i += kThreads) sr[i] = __ldg(reinterpret_cast<const long long*>(a.rkeys) + lo + i);
   __syncthreads();
 
-  uint32_t match_bits = 0, my_m = 0;
-  uint64_t my_p = 0;
-  uint32_t rj[kAlItems];
-  uint32_t lcnt[kAlItems], rcnt[kAlItems];
-  uint32_t from = 0;  // search start inside the window (this thread's keys increase)
-#pragma unroll
-  for (int it = 0; it < kAlItems; ++it) {
-    const int e = tid * kAlItems + it;
-    rj[it] = 0;
-    lcnt[it] = rcnt[it] = 0;
-    if (e < count && hi > lo) {
-      const int64_t key = sl[e];
-      uint32_t j;
-      bool hit;
-      if (staged) {
-        j = lower_bound_i64(sr, from, hi - lo, key);
-        hit = j < hi - lo && sr[j] == key;
-        from = j;
-        j += lo;
-      } else {
-        j = lower_bound_i64(a.rkeys, lo, hi, key);
-        hit = j < hi && a.rkeys[j] == key;
+  // ---- phase 1: this thread's matches (count, then list them in order)
+  const uint32_t T = uint32_t(count) + (staged ? w : 0u);
+  const uint32_t E = (T + kThreads - 1) / kThreads;
+  uint32_t d0 = min(uint32_t(tid) * E, T), d1 = min(d0 + E, T);
+  uint32_t i0 = 0, j0 = 0;
+  if (staged) {
+    uint32_t l = d0 > w ? d0 - w : 0u, h = min(d0, uint32_t(count));
+    while (l < h) {  // smallest i whose left key comes after right key d0-1-i
+      const uint32_t mid = (l + h) >> 1;
+      if (sl[mid] <= sr[d0 - 1 - mid]) l = mid + 1;
+      else h = mid;
+    }
+    i0 = l;
+    j0 = d0 - l;
+  }
+  auto walk = [&](auto&& on_match) {
+    if (staged) {
+      uint32_t i = i0, j = j0;
+      for (uint32_t d = d0; d < d1; ++d) {
+        if (i < uint32_t(count) && (j >= w || sl[i] <= sr[j])) {
+          if (j < w && sl[i] == sr[j]) on_match(i, lo + j);
+          ++i;
+        } else {
+          ++j;
+        }
       }
-      if (hit) {
-        match_bits |= 1u << it;
-        rj[it] = j;
-        lcnt[it] = a.loff[begin + e + 1] - a.loff[begin + e];
-        rcnt[it] = a.roff[j + 1] - a.roff[j];
-        ++my_m;
-        my_p += uint64_t(lcnt[it]) * uint64_t(rcnt[it]);
+    } else if (hi > lo) {  // window too wide to stage: per-key searches in global memory
+      for (int it = 0; it < kAlItems; ++it) {
+        const int e = tid * kAlItems + it;
+        if (e < count) {
+          const uint32_t j = lower_bound_i64(a.rkeys, lo, hi, sl[e]);
+          if (j < hi && a.rkeys[j] == sl[e]) on_match(uint32_t(e), j);
+        }
       }
     }
-  }
+  };
+  uint32_t my_m = 0;
+  walk([&](uint32_t, uint32_t) { ++my_m; });
   uint32_t tot_m;
-  uint64_t tot_p;
-  const uint32_t off_m = block_exclusive_scan<kThreads>(my_m, warp_m, &tot_m);
-  const uint64_t off_p = block_exclusive_scan<kThreads>(my_p, warp_p, &tot_p);
+  uint32_t q = block_exclusive_scan<kThreads>(my_m, warp_m, &tot_m);
+  walk([&](uint32_t i, uint32_t j) {
+    mi[q] = i;
+    mj[q] = j;
+    ++q;
+  });
+  __syncthreads();
 
+  // ---- phase 2: the tile's pair total (for the look-back), striped over matches
+  uint64_t my_p = 0;
+  for (uint32_t t = tid; t < tot_m; t += kThreads) {
+    const uint32_t i = mi[t], j = mj[t];
+    my_p += uint64_t(__ldg(a.loff + begin + i + 1) - __ldg(a.loff + begin + i)) *
+            uint64_t(__ldg(a.roff + j + 1) - __ldg(a.roff + j));
+  }
+  uint64_t tot_p;
+  block_exclusive_scan<kThreads>(my_p, warp_p, &tot_p);
   if (warp == 0) {
     uint64_t excl_m = 0, excl_p = 0;
     if (tile == 0) {
@@ -352,21 +389,36 @@ __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
     }
   }
   __syncthreads();
-  uint64_t pos = s_excl_m + off_m;
-  uint64_t pairs = s_excl_p + off_p;
-#pragma unroll
-  for (int it = 0; it < kAlItems; ++it) {
-    if (match_bits & (1u << it)) {
-      const int e = tid * kAlItems + it;
-      a.matched_keys[pos] = sl[e];
-      a.ls[pos] = a.loff[begin + e];
-      a.lc[pos] = lcnt[it];
-      a.rs[pos] = a.roff[rj[it]];
-      a.rc[pos] = rcnt[it];
-      a.pair_offsets[pos] = pairs;
-      pairs += uint64_t(lcnt[it]) * uint64_t(rcnt[it]);
-      ++pos;
+
+  // ---- phase 3: resolve and write the matches, striped (coalesced), the
+  // pair prefix carried across rounds of kThreads matches
+  uint64_t pairs_base = s_excl_p;
+  const uint64_t mbase = s_excl_m;
+  for (uint32_t r0 = 0; r0 < tot_m; r0 += kThreads) {
+    const uint32_t t = r0 + tid;
+    uint32_t l0 = 0, lcount = 0, rr0 = 0, rcount = 0, i = 0;
+    if (t < tot_m) {
+      i = mi[t];
+      const uint32_t j = mj[t];
+      l0 = __ldg(a.loff + begin + i);
+      lcount = __ldg(a.loff + begin + i + 1) - l0;
+      rr0 = __ldg(a.roff + j);
+      rcount = __ldg(a.roff + j + 1) - rr0;
     }
+    const uint64_t p = uint64_t(lcount) * uint64_t(rcount);
+    uint64_t round_total;
+    const uint64_t pre = block_exclusive_scan<kThreads>(p, warp_p, &round_total);
+    if (t < tot_m) {
+      const uint64_t o = mbase + t;
+      a.matched_keys[o] = sl[i];
+      a.ls[o] = l0;
+      a.lc[o] = lcount;
+      a.rs[o] = rr0;
+      a.rc[o] = rcount;
+      a.pair_offsets[o] = pairs_base + pre;
+    }
+    pairs_base += round_total;
+    __syncthreads();  // warp_p reuse by the next round's scan
   }
   if (last && tid == 0) {
     const uint64_t m = s_excl_m + tot_m, total = s_excl_p + tot_p;
@@ -428,7 +480,13 @@ int key_axis_align(const int64_t* lkeys, const uint32_t* loff, const int64_t* d_
   a.pair_offsets = pair_offsets;
   a.m_out = m_out;
   a.total_out = total_out;
-  align_kernel<<<tiles, kThreads, 0, stream>>>(a);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kAlSmem)) != cudaSuccess)
+      return rl_cuda_status(cudaGetLastError());
+    attr = true;
+  }
+  align_kernel<<<tiles, kThreads, kAlSmem, stream>>>(a);
   count_launches(1);
   return rl_cuda_status(cudaGetLastError());
 }

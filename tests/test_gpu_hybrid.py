@@ -133,3 +133,30 @@ def test_hybrid_matches_forced_lsd(monkeypatch):
     monkeypatch.setenv("RL_NO_HYBRID", "1")
     b = engine.sort_permutation([engine.SortAxis(kd, False)], len(keys), kd.device)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("width", [4, 8, 5])
+@pytest.mark.parametrize("shape", ["uniform", "bitonic_bins"])
+def test_fused_gather_in_local_phase(width, shape):
+    """Relation.take fused into the hybrid's local phase: one 4- or 8-byte
+    column takes the prefetch-and-park path, other widths the direct loads;
+    bins sorted by the bitonic network reload their moved rows."""
+    rng = np.random.default_rng(12 + width)
+    if shape == "uniform":
+        keys = full_range(rng, 1_500_000)
+    else:
+        tops = full_range(rng, 500) & ~np.int64((1 << 48) - 1)
+        low = rng.integers(0, 1 << 40, (500, 200), dtype=np.int64)
+        low[:, :3] |= np.int64(1) << 47
+        keys = np.concatenate([(tops[:, None] | low).ravel(), full_range(rng, 800_000)])
+        keys = keys[rng.permutation(len(keys))]
+    n = len(keys)
+    col = rng.integers(0, 256, (n, width), dtype=np.uint8)
+    kd = torch.from_numpy(keys).cuda()
+    cd = torch.from_numpy(col).cuda()
+    out = torch.empty_like(cd)
+    perm = engine.sort_permutation([engine.SortAxis(kd, False)], n, kd.device,
+                                   gather=[engine.OutColumn(cd, out, width, 0)], fuse_gather=True)
+    want = O.stable_axis_order(keys, False)
+    assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
+    assert (out.cpu().numpy() == col[want]).all()

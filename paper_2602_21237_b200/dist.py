@@ -78,6 +78,23 @@ class GpuOps:
         return perm.to(torch.int64) & 0xFFFFFFFF
 
     # fused forms (one launch for every column) used when an Ops object has them
+    def local_join(self, lcols, lkey: int, rcols, rkey: int, lgids: torch.Tensor, rgids: torch.Tensor):
+        """The local equi-join with every output column and both global row-id
+        columns written by ONE expansion launch (rl_join_plan_build + rl_join_expand)."""
+        from . import _capi as C
+        from . import engine
+        from .pipeline import join_out_columns
+
+        plan = engine.JoinPlanDev(lcols[lkey], rcols[rkey])
+        total = plan.total
+        cols = join_out_columns(list(lcols), lkey, list(rcols), rkey, total)
+        ids = [engine.OutColumn(lgids, torch.empty(total, dtype=torch.int64, device=lgids.device), 8, C.RL_SIDE_LEFT),
+               engine.OutColumn(rgids, torch.empty(total, dtype=torch.int64, device=rgids.device), 8,
+                                C.RL_SIDE_RIGHT)]
+        if total:
+            plan.expand(0, total, cols + ids)
+        return [c.dst for c in cols], ids[0].dst, ids[1].dst
+
     def partition_take(self, kind: str, keys: torch.Tensor, cols: Sequence[torch.Tensor], **kw):
         """Partition + every column gathered into destination order in one
         gather launch (rl_hash_partition / rl_range_partition with columns)."""
@@ -198,12 +215,16 @@ def distributed_join(left: Sequence[torch.Tensor], left_key: int, left_base: int
 
     lcols, lgids = shuffle(list(left), left_key, left_base)
     rcols, rgids = shuffle(list(right), right_key, right_base)
-    lrows, rrows = ops.local_join_pairs(lcols[left_key], rcols[right_key])
-    out = [ops.take(c, lrows) for c in lcols]
-    out += [ops.take(c, rrows) for j, c in enumerate(rcols) if j != right_key]
-    total = torch.tensor([lrows.numel()], dtype=torch.int64, device=dev)
+    if hasattr(ops, "local_join"):
+        out, lg, rg = ops.local_join(lcols, left_key, rcols, right_key, lgids, rgids)
+    else:
+        lrows, rrows = ops.local_join_pairs(lcols[left_key], rcols[right_key])
+        out = [ops.take(c, lrows) for c in lcols]
+        out += [ops.take(c, rrows) for j, c in enumerate(rcols) if j != right_key]
+        lg, rg = lgids[lrows], rgids[rrows]
+    total = torch.tensor([lg.numel()], dtype=torch.int64, device=dev)
     dist.all_reduce(total, group=group)
-    return JoinShard(out, lgids[lrows], rgids[rrows], int(total.item()))
+    return JoinShard(out, lg, rg, int(total.item()))
 
 
 def choose_splitters(keys: torch.Tensor, gid_base: int, descending: bool, group=None, per_rank: int = 256,

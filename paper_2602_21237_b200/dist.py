@@ -235,21 +235,20 @@ def choose_splitters(keys: torch.Tensor, gid_base: int, descending: bool, group=
     p = _group_size(group)
     n = keys.numel()
     m = min(per_rank, n)
-    idx = (torch.arange(m, device=keys.device, dtype=torch.int64) * max(n, 1)) // max(m, 1)
-    pack = torch.zeros(2 + 2 * per_rank, dtype=torch.int64, device=keys.device)
-    pack[0] = m
-    pack[1] = gid_base
-    if m:
-        pack[2:2 + m] = keys[idx]
-        pack[2 + per_rank:2 + per_rank + m] = idx + gid_base
-    packs = [torch.empty_like(pack) for _ in range(p)]
-    dist.all_gather(packs, pack, group=group)
-    host = torch.stack(packs).cpu()
+    dev = keys.device
+    idx = (torch.arange(per_rank, device=dev, dtype=torch.int64) * max(n, 1)) // max(m, 1)
+    idx = idx.clamp_(max=max(n - 1, 0))
+    head = torch.tensor([m, gid_base], dtype=torch.int64, device=dev)
+    pack = torch.cat([head, keys[idx] if n else torch.zeros(per_rank, dtype=torch.int64, device=dev),
+                      idx + gid_base])  # entries past m are ignored
+    packs = torch.empty(p * pack.numel(), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(packs, pack, group=group)
+    host = packs.cpu().view(p, -1)
     bases = [int(v) for v in host[:, 1].tolist()]
     ks = torch.cat([h[2:2 + int(h[0])] for h in host])
     gs = torch.cat([h[2 + per_rank:2 + per_rank + int(h[0])] for h in host])
     if ks.numel() == 0:
-        e = torch.empty(0, dtype=torch.int64, device=keys.device)
+        e = torch.empty(0, dtype=torch.int64, device=dev)
         return (e, e, bases) if with_bases else (e, e)
     ordk = torch.bitwise_not(ks) if descending else ks
     # composite (key, gid) order: stable sort by gid then by key
@@ -258,7 +257,9 @@ def choose_splitters(keys: torch.Tensor, gid_base: int, descending: bool, group=
     ks, gs = ks[o], gs[o]
     cnt = ks.numel()
     picks = [min(cnt - 1, (i * cnt) // p) for i in range(1, p)]
-    sk, sg = ks[picks].to(keys.device), gs[picks].to(keys.device)
+    both = torch.stack([ks[picks], gs[picks]])
+    both = both.pin_memory().to(dev, non_blocking=True) if dev.type == "cuda" else both  # one small H2D
+    sk, sg = both[0], both[1]
     return (sk, sg, bases) if with_bases else (sk, sg)
 
 

@@ -285,6 +285,25 @@ RL_API int rl_range_partition(const int64_t* keys, int64_t n, int64_t gid_base,
                               size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Multi-GPU exchange fused with the partition gather.
+ * After rl_hash_partition / rl_range_partition (row ids grouped by
+ * destination; dest_starts[parts + 1] = device prefix of the counts), every
+ * partitioned row i of destination d is stored straight into d's receive
+ * buffer — through d's peer pointer (NVLink P2P into symmetric memory; the
+ * own rank's local buffer) — at row dest_offsets[d] + (i - dest_starts[d]):
+ * each column c (src = local column, width bytes) into the region at
+ * dest_bases[d * (n_columns + 1) + c], the local row id (uint32) into the
+ * region at dest_bases[d * (n_columns + 1) + n_columns]. Replaces the
+ * per-column gather + NCCL all-to-all-v; receive order = source rank order,
+ * partition order within a source, as the all-to-all. parts <= 64,
+ * n_columns <= 8. The caller brackets the call with barriers.
+ * --------------------------------------------------------------------- */
+RL_API int rl_push_rows(const uint32_t* rows, int64_t n, int32_t parts,
+                 const int64_t* dest_starts, const rl_column* columns,
+                 int32_t n_columns, const uint64_t* dest_bases,
+                 const int64_t* dest_offsets, void* stream);
+
+/* ---------------------------------------------------------------------
  * The reference's 128-bit multiset result digest (relation.py:319-330,
  * hashing.py:64-109), bit-exact, computed on the device from the columns
  * (src, width; schema order; Int64 width 8) of n rows without serialising

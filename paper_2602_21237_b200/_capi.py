@@ -64,6 +64,7 @@ SIGNATURES = {
     "rl_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "rl_device_sm_count": (ctypes.c_int, []),
     "rl_launch_count": (_I64, []),
+    "rl_push_rows": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _I32, _P, _P, _P]),
     "rl_sort_workspace_bytes": (_SZ, [_I64]),
     "rl_sort_axis": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
     "rl_sort_axis_profiled": (

@@ -18,6 +18,14 @@ contiguous global row range of every relation (rank r owns rows
   variant), exchanges, and sorts locally with the stable radix sort. Rank r
   then holds the r-th slice of the global stable order.
 
+On GPUs the exchange is fused with the partition gather: ``PeerExchange``
+keeps every rank's receive buffers in symmetric memory, the P x P counts
+go round once, and ``rl_push_rows`` reads each partitioned row from local
+HBM and stores it straight into its destination's buffer through the peer
+pointer (NVLink P2P), between two symmetric-memory barriers — the
+all-to-all without a send buffer or a second pass (``RL_NO_P2P=1``, or a
+group without symmetric memory, uses NCCL ``all_to_all_single``).
+
 The device work is done through an ``Ops`` object: ``GpuOps`` calls the
 sm_100a kernels; the CPU multi-process tests inject an oracle-backed
 implementation to exercise this exchange protocol with the gloo backend
@@ -26,6 +34,7 @@ implementation to exercise this exchange protocol with the gloo backend
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -77,6 +86,21 @@ class GpuOps:
         perm = engine.sort_permutation([engine.SortAxis(keys, descending)], keys.numel(), keys.device)
         return perm.to(torch.int64) & 0xFFFFFFFF
 
+    def push_exchange(self, slot: str, cols, rows, counts, group):
+        """Partition gather + all-to-all in one kernel over peer memory
+        (PeerExchange); None when this group has no symmetric memory."""
+        dev = cols[0].device
+        if not _peer_exchange_ok(group, dev):
+            return None
+        key = (slot, id(group), dev.index, tuple((c.dtype, tuple(c.shape[1:])) for c in cols))
+        try:
+            if key not in _PEER:
+                _PEER[key] = PeerExchange(group, dev, cols)
+            return _PEER[key].exchange(cols, rows, counts)
+        except (RuntimeError, ImportError, AttributeError):
+            _PEER[("ok", dev.index)] = False  # no symmetric memory here: NCCL from now on
+            return None
+
     # fused forms (one launch for every column) used when an Ops object has them
     def local_join(self, lcols, lkey: int, rcols, rkey: int, lgids: torch.Tensor, rgids: torch.Tensor):
         """The local equi-join with every output column and both global row-id
@@ -123,6 +147,75 @@ class GpuOps:
             engine.sort_permutation([engine.SortAxis(keys, descending)], n, keys.device, sorted_keys_out=sk,
                                     gather=gather)
         return outs
+
+
+class PeerExchange:
+    """Receive buffers of one exchange slot in symmetric memory, and the
+    fused partition-gather + all-to-all (rl_push_rows) into them. Received
+    columns are views of the buffers, valid until this slot's next exchange."""
+
+    def __init__(self, group, device, like: Sequence[torch.Tensor]):
+        self.group, self.device = group, device
+        self.p = _group_size(group)
+        self.me = dist.get_rank(group)
+        self.likes = [(c.dtype, tuple(c.shape[1:]), _row_bytes(c)) for c in like]
+        self.cap = 0
+
+    def _ensure(self, rows: int) -> None:
+        """(Re)allocate for `rows` received rows; every rank takes the same
+        decision (from the same counts matrix), so the rendezvous is collective."""
+        if rows <= self.cap:
+            return
+        import torch.distributed._symmetric_memory as sm
+
+        cap = max(rows, self.cap + self.cap // 4, 1024)
+        offs, total = [], 0
+        for _, _, w in self.likes + [(None, None, 4)]:  # + the local row ids
+            offs.append(total)
+            total += (cap * w + 255) // 256 * 256
+        self.buf = sm.empty(total, dtype=torch.uint8, device=self.device)
+        grp = self.group if self.group is not None else dist.group.WORLD
+        self.hdl = sm.rendezvous(self.buf, grp.group_name)
+        ptrs = list(self.hdl.buffer_ptrs)
+        table = [[ptrs[d] + o for o in offs] for d in range(self.p)]  # user-space addresses < 2^63
+        self.bases = torch.tensor(table, dtype=torch.int64).view(-1).to(self.device)
+        self.offs, self.cap = offs, cap
+
+    def exchange(self, cols: Sequence[torch.Tensor], rows: torch.Tensor, counts: torch.Tensor):
+        from . import _capi as C
+        from . import engine
+
+        p, me = self.p, self.me
+        mat_dev = torch.empty(p * p, dtype=torch.int64, device=self.device)
+        dist.all_gather_into_tensor(mat_dev, counts.to(torch.int64).reshape(p), group=self.group)
+        mat = mat_dev.cpu().view(p, p)  # mat[s][d]: rows s sends to d
+        self._ensure(int(mat.sum(0).max()))
+        recv_counts = mat[:, me].tolist()
+        total = sum(recv_counts)
+        starts = torch.zeros(p + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(counts.to(torch.int64).reshape(p), 0, out=starts[1:])
+        offs = torch.tensor([int(mat[:me, d].sum()) for d in range(p)], dtype=torch.int64).to(self.device)
+        arr, ncols = C.columns_array((c.contiguous().data_ptr(), 0, w, C.RL_SIDE_LEFT)
+                                     for c, (_, _, w) in zip(cols, self.likes))
+        self.hdl.barrier()  # every rank is done with its previous receive
+        C.check(C.load().rl_push_rows(engine._ptr(rows), rows.numel(), p, engine._ptr(starts), arr, ncols,
+                                      engine._ptr(self.bases), engine._ptr(offs), engine.stream_handle()),
+                "rl_push_rows")
+        self.hdl.barrier()  # every push into this rank has landed
+        out = []
+        for (dt, tail, w), o in zip(self.likes, self.offs):
+            out.append(self.buf[o:o + total * w].view(dt).view((total,) + tail))
+        recv_rows = self.buf[self.offs[-1]:self.offs[-1] + total * 4].view(torch.int32)
+        return out, recv_rows, recv_counts
+
+
+_PEER: dict = {}
+
+
+def _peer_exchange_ok(group, device) -> bool:
+    if os.environ.get("RL_NO_P2P") or device.type != "cuda" or dist.get_backend(group) != "nccl":
+        return False
+    return _PEER.get(("ok", device.index), True)
 
 
 def _row_bytes(c: torch.Tensor) -> int:
@@ -207,14 +300,20 @@ def distributed_join(left: Sequence[torch.Tensor], left_key: int, left_base: int
     p = _group_size(group)
     dev = left[left_key].device
 
-    def shuffle(cols, key_idx, base):
-        rows, counts, moved = _partition_take(ops, "hash", cols[key_idx], list(cols), parts=p, seed=seed)
+    def shuffle(cols, key_idx, base, slot):
         bases = _all_bases(base, dev, group)
+        if hasattr(ops, "push_exchange"):
+            rows, counts = ops.hash_partition(cols[key_idx], p, seed)
+            pushed = ops.push_exchange(slot, list(cols), rows, counts, group)
+            if pushed is not None:
+                rcols, rrows, rc = pushed
+                return rcols, _global_ids(rrows, rc, bases)
+        rows, counts, moved = _partition_take(ops, "hash", cols[key_idx], list(cols), parts=p, seed=seed)
         recv, rc = exchange(moved + [rows], counts, group, with_counts=True)
         return recv[:-1], _global_ids(recv[-1], rc, bases)
 
-    lcols, lgids = shuffle(list(left), left_key, left_base)
-    rcols, rgids = shuffle(list(right), right_key, right_base)
+    lcols, lgids = shuffle(list(left), left_key, left_base, "join_left")
+    rcols, rgids = shuffle(list(right), right_key, right_base, "join_right")
     if hasattr(ops, "local_join"):
         out, lg, rg = ops.local_join(lcols, left_key, rcols, right_key, lgids, rgids)
     else:
@@ -275,10 +374,18 @@ def distributed_sort(cols: Sequence[torch.Tensor], key_idx: int, gid_base: int, 
     ops = ops or GpuOps()
     keys = cols[key_idx]
     split_k, split_g, bases = choose_splitters(keys, gid_base, descending, group, with_bases=True)
-    rows, counts, moved = _partition_take(ops, "range", keys, list(cols), gid_base=gid_base, split_keys=split_k,
-                                          split_gids=split_g, descending=descending)
-    recv, rc = exchange(moved + [rows], counts, group, with_counts=True)
-    rcols, rgids = recv[:-1], _global_ids(recv[-1], rc, bases)
+    pushed = None
+    if hasattr(ops, "push_exchange"):
+        rows, counts = ops.range_partition(keys, gid_base, split_k, split_g, descending)
+        pushed = ops.push_exchange("sort", list(cols), rows, counts, group)
+    if pushed is not None:
+        rcols, rrows, rc = pushed
+        rgids = _global_ids(rrows, rc, bases)
+    else:
+        rows, counts, moved = _partition_take(ops, "range", keys, list(cols), gid_base=gid_base, split_keys=split_k,
+                                              split_gids=split_g, descending=descending)
+        recv, rc = exchange(moved + [rows], counts, group, with_counts=True)
+        rcols, rgids = recv[:-1], _global_ids(recv[-1], rc, bases)
     # arrival order = ascending global row id, so the stable local sort keeps the reference tie order
     out = _sort_take(ops, list(rcols) + [rgids], key_idx, descending)
     return SortShard(out[:-1], out[-1])

@@ -57,3 +57,77 @@ def test_distributed_sort_on_device(nccl_world1):
     want = O.stable_axis_order(keys, True)
     assert (res.gids.cpu().numpy() == want).all()
     assert (res.columns[0].cpu().numpy() == keys[want]).all()
+
+
+def test_push_rows_emulated_ranks():
+    """rl_push_rows for P logical ranks on one GPU (each rank's receive
+    buffers are separate allocations; ranks push one after another, none
+    waits on another): every destination receives source blocks in rank
+    order, each in stable partition order, with the local row ids — the
+    all-to-all-v contract."""
+    import ctypes
+
+    from paper_2602_21237_b200 import _capi as C
+    from paper_2602_21237_b200 import engine
+
+    lib = C.load()
+    P = 3
+    rng = np.random.default_rng(21)
+    sizes = [40_000, 0, 65_537]
+    keys = [rng.integers(-10**6, 10**6, n).astype(np.int64) for n in sizes]
+    pays = [rng.integers(0, 256, (n, 12), dtype=np.uint8) for n in sizes]
+    parts = []
+    for k in keys:
+        rows, counts = engine.hash_partition(torch.from_numpy(k).cuda(), P, 77)
+        parts.append((rows, counts.cpu().numpy()))
+    mat = np.stack([c for _, c in parts])  # mat[s][d]
+    recv = mat.sum(0)
+    bufs = [(torch.empty(max(r, 1), dtype=torch.int64, device="cuda"),
+             torch.empty((max(r, 1), 12), dtype=torch.uint8, device="cuda"),
+             torch.empty(max(r, 1), dtype=torch.int32, device="cuda")) for r in recv]
+    table = torch.tensor([[b[0].data_ptr(), b[1].data_ptr(), b[2].data_ptr()] for b in bufs],
+                         dtype=torch.int64).view(-1).cuda()
+    for s in range(P):
+        rows, counts = parts[s]
+        kd, pd = torch.from_numpy(keys[s]).cuda(), torch.from_numpy(pays[s]).cuda()
+        starts = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int64).cuda()
+        offs = torch.tensor([int(mat[:s, d].sum()) for d in range(P)], dtype=torch.int64).cuda()
+        arr, ncols = C.columns_array([(kd.data_ptr(), 0, 8, C.RL_SIDE_LEFT), (pd.data_ptr(), 0, 12, C.RL_SIDE_LEFT)])
+        C.check(lib.rl_push_rows(ctypes.c_void_p(rows.data_ptr()), rows.numel(), P,
+                                 ctypes.c_void_p(starts.data_ptr()), arr, ncols, ctypes.c_void_p(table.data_ptr()),
+                                 ctypes.c_void_p(offs.data_ptr()), engine.stream_handle()), "rl_push_rows")
+    torch.cuda.synchronize()
+    for d in range(P):
+        want_rows = [np.flatnonzero(O.fmix64(keys[s].view(np.uint64) ^ np.uint64(O.fmix64_scalar(77)))
+                                    % np.uint64(P) == d) for s in range(P)]
+        wk = np.concatenate([keys[s][r] for s, r in enumerate(want_rows)])
+        wp = np.concatenate([pays[s][r] for s, r in enumerate(want_rows)])
+        wr = np.concatenate(want_rows)
+        n = int(recv[d])
+        assert (bufs[d][0][:n].cpu().numpy() == wk).all()
+        assert (bufs[d][1][:n].cpu().numpy() == wp).all()
+        assert (bufs[d][2][:n].cpu().numpy().view(np.uint32) == wr).all()
+
+
+def test_distributed_ops_take_the_peer_push(nccl_world1, monkeypatch):
+    """One-rank NCCL group: the distributed sort and join go through
+    PeerExchange (symmetric memory) and agree with the NCCL all-to-all path."""
+    from paper_2602_21237_b200 import dist as D
+
+    rng = np.random.default_rng(5)
+    keys = rng.integers(-(2**40), 2**40, 80_000).astype(np.int64)
+    pay = rng.integers(0, 256, (80_000, 4), dtype=np.uint8)
+    kd, pd = torch.from_numpy(keys).cuda(), torch.from_numpy(pay).cuda()
+    a = D.distributed_sort([kd, pd], 0, 0)
+    monkeypatch.setenv("RL_NO_P2P", "1")
+    b = D.distributed_sort([kd, pd], 0, 0)
+    monkeypatch.delenv("RL_NO_P2P")
+    assert torch.equal(a.gids, b.gids) and torch.equal(a.columns[1], b.columns[1])
+    assert (a.gids.cpu().numpy() == O.stable_axis_order(keys, False)).all()
+    lk = rng.integers(0, 5000, 30_000).astype(np.int64)
+    rk = rng.integers(0, 5000, 20_000).astype(np.int64)
+    j = D.distributed_join([torch.from_numpy(lk).cuda()], 0, 0, [torch.from_numpy(rk).cuda()], 0, 0)
+    wl, wr = O.join_pairs(lk, rk)
+    assert (j.left_gids.cpu().numpy() == wl).all() and (j.right_gids.cpu().numpy() == wr).all()
+    used = [k for k in D._PEER if k[0] in ("sort", "join_left", "join_right")]
+    assert used, "the peer-memory exchange was not used"

@@ -1151,9 +1151,13 @@ static int sort_grid_limit() {
   return cached;
 }
 
+#ifndef RL_HIST_CTAS_PER_SM
+#define RL_HIST_CTAS_PER_SM 2
+#endif
 static int hist_grid(int64_t n) {  // one co-resident wave (2 CTAs of 512 threads per SM), >= 1 step each
   const int64_t per_cta = int64_t(kHistThreads) * kHistUnroll;
-  return int(std::max<int64_t>(1, std::min<int64_t>((n + per_cta - 1) / per_cta, int64_t(device_sm_count()) * 2)));
+  return int(std::max<int64_t>(1, std::min<int64_t>((n + per_cta - 1) / per_cta,
+                                                    int64_t(device_sm_count()) * RL_HIST_CTAS_PER_SM)));
 }
 
 // Histograms, then the cooperative kernel (LSD, or the wide-key hybrid

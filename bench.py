@@ -410,6 +410,7 @@ def run_ours(args):
 
     if not args.no_join:
         line["join_cfg1"] = join_cfg1(args, dev, rank, world)
+        line["join_scaling"] = join_scaling(args, dev, rank, world)
     if args.extras and world == 1:
         line["other_configs"] = extras(args, dev)
 
@@ -562,6 +563,8 @@ def run_distributed(args, dev, rank, world, lib, keys_h, pay_h, keys_d, pay_d, f
         "clocks": clocks.summary(),
         "gpu_launches": int(launches),
     }
+    if not args.no_join:
+        line["join_scaling"] = join_scaling(args, dev, rank, world)
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -624,6 +627,68 @@ def join_cfg1(args, dev, rank, world):
                                   "reps": 20, "cores": 1, "kind": "port"}
         res["p99_speedup_e2e_vs_cpu"] = round(res["cpu_tensor_path"]["p99_ms"] / res["e2e_p99_ms"], 1)
     return res
+
+
+JOIN_SCALING_ROWS = 100_000_000
+
+
+def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
+    """The north star's scaling case, a cfg5-shaped equi-join (uniform keys,
+    domain = rows, int64 payload = global row id) at a FIXED total of
+    `total_rows` rows per side split over the ranks (strong scaling): N = 1
+    runs the device join, N > 1 dist.distributed_join (hash partition, the
+    peer-memory exchange, local join). Device time per step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_21237_b200 import dist as D
+    from paper_2602_21237_b200 import pipeline, synth
+
+    n = total_rows // world
+    base = rank * n
+    lk = synth.uniform_keys(n, total_rows, 2 * rank + 11)
+    rk = synth.uniform_keys(n, total_rows, 2 * rank + 12)
+    pay = np.arange(base, base + n, dtype=np.int64)
+    cols_l = [torch.from_numpy(lk).to(dev), torch.from_numpy(pay).to(dev)]
+    cols_r = [torch.from_numpy(rk).to(dev), torch.from_numpy(pay.copy()).to(dev)]
+    del lk, rk, pay
+
+    if world == 1:
+        from paper_2602_21237_b200 import records as R
+
+        schema = R.Schema((("key", R.Int64()), ("payload", R.Int64())))
+        dl, dr = pipeline.DeviceRelation(schema, cols_l), pipeline.DeviceRelation(schema, cols_r)
+
+        def step():
+            return pipeline.join(dl, dr, "key").row_count
+    else:
+        def step():
+            return D.distributed_join(cols_l, 0, base, cols_r, 0, base).total_matches
+
+    for _ in range(2):
+        total = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = []
+    for _ in range(min(args.steps, 5)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        total = step()
+        b.record()
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = torch.tensor([statistics.median(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    med = float(t.item())
+    torch.cuda.empty_cache()
+    return {"workload": f"cfg5-shaped equi-join, {total_rows:.0e} rows per side in total (uniform keys, domain = rows, "
+                        "int64 payload), strong scaling over the ranks",
+            "rows_per_side_per_gpu": n, "matches_total": int(total),
+            "path": "device join" if world == 1 else "distributed_join: hash partition + peer-memory push + local join",
+            "ms_per_step_p50_max_over_ranks": round(med, 3),
+            "mrows_per_s": round(2 * total_rows / (med / 1e3) / 1e6, 1), "scaling": "strong"}
 
 
 def extras(args, dev):

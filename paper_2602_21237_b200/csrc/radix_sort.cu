@@ -714,7 +714,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
   uint32_t* goff = misc + 32;   // [2][kGroupSubs + 1]
   uint32_t* gends = misc + 72;  // [2][kGroupSubs]
-  uint32_t* runs = misc + 112;  // [2][3] descriptors of the run in each buffer
+  uint32_t* runs = misc + 112;  // [2][4] descriptors of the run in each buffer
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLocBars);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* kin = src == 1 ? a.keys_a : a.keys_b;
@@ -765,8 +765,10 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     runs[0] = base;
     runs[1] = cnt;
     runs[2] = (g0 + k * gstep) * kGroupSubs + (se >> 8);
+    runs[3] = (se & 255) - (se >> 8);
     issue_run(kin, vin, base, cnt, smem + kLocA, &bars[0]);
   }
+  __syncthreads();  // the first run's descriptor is visible to every thread
 
   while (true) {
     // ---- warp 0: find and prefetch the next run into the other buffer
@@ -795,16 +797,18 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
           const uint32_t* off = goff + (nk & 1) * 17;
           const uint32_t se = gends[(nk & 1) * 16 + nr];
           const uint32_t base = off[se >> 8], cnt = off[se & 255] - base;
-          uint32_t* d = runs + (buf ^ 1) * 3;
+          uint32_t* d = runs + (buf ^ 1) * 4;
           d[0] = base;
           d[1] = cnt;
           d[2] = (g0 + nk * gstep) * kGroupSubs + (se >> 8);
+          d[3] = (se & 255) - (se >> 8);
           issue_run(kin, vin, base, cnt, smem + kLocA + (buf ^ 1) * kLocABytes, &bars[buf ^ 1]);
         }
       }
     }
-    // ---- this run
-    for (int i = tid; i < kLocalBins; i += kThreads) hist[i] = 0;
+    // ---- this run: only the bins of its sub-buckets are zeroed and scanned
+    const uint32_t bin_lo = (runs[buf * 4 + 2] & (kGroupSubs - 1)) * kBins, nsb = runs[buf * 4 + 3];
+    for (uint32_t i = tid; i < nsb * kBins; i += kThreads) hist[bin_lo + i] = 0;
     if (tid == 0) {
       misc[0] = 0;
       misc[1] = 0;
@@ -813,7 +817,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     if (buf) phase1 ^= 1;
     else phase0 ^= 1;
     __syncthreads();  // hist zeroed, run descriptors and next-run fields visible
-    const uint32_t base = runs[buf * 3], cnt = runs[buf * 3 + 1], top0 = runs[buf * 3 + 2] & ~uint32_t(kGroupSubs - 1);
+    const uint32_t base = runs[buf * 4], cnt = runs[buf * 4 + 1], top0 = runs[buf * 4 + 2] & ~uint32_t(kGroupSubs - 1);
     const uint8_t* abuf = smem + kLocA + buf * kLocABytes;
     const uint64_t* ak = reinterpret_cast<const uint64_t*>(abuf) + (base & 1u);
     const uint32_t* av = reinterpret_cast<const uint32_t*>(abuf + kLocAKeys) + (base & 3u);
@@ -822,7 +826,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     };
     for (uint32_t j = tid; j < cnt; j += kThreads) atomicAdd(&hist[bin_of(ak[j])], 1u);
     __syncthreads();
-    {  // exclusive scan: thread owns bins [kPerThread tid, kPerThread (tid + 1))
+    if (nsb == uint32_t(kGroupSubs)) {  // a whole group: thread owns kPerThread consecutive bins (vector loads)
       uint32_t c[kPerThread], run = 0;
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
@@ -834,6 +838,21 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
         hist[tid * kPerThread + i] = start;
+        start += c[i];
+      }
+    } else {  // part of a group: only its nsb * 256 bins, thread owns nsb consecutive bins
+      uint32_t c[kPerThread], run = 0;
+      uint32_t* hb = hist + bin_lo + tid * nsb;
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        c[i] = uint32_t(i) < nsb ? hb[i] : 0u;
+        run += c[i];
+      }
+      uint32_t total;
+      uint32_t start = block_exclusive_scan<kThreads>(run, misc + 8, &total);
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        if (uint32_t(i) < nsb) hb[i] = start;
         start += c[i];
       }
     }
@@ -860,7 +879,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       const uint64_t key = bk[p];
       const uint32_t v = bv[p];
       const int b = bin_of(key);
-      const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+      const uint32_t b0 = uint32_t(b) > bin_lo ? hist[b - 1] : 0u, b1 = hist[b];
       uint32_t pos = p;
       if (b1 - b0 > kRankMax) {
         if (p == b0) {
@@ -880,7 +899,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     const uint32_t nbig = min(misc[0], uint32_t(kBigList));
     for (uint32_t t = warp; t < nbig; t += kWarps) {
       const int b = int(big[t]);
-      const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+      const uint32_t b0 = uint32_t(b) > bin_lo ? hist[b - 1] : 0u, b1 = hist[b];
       warp_bitonic(bk, bv, b0, b1, lane);
       for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], bv[p]);
     }

@@ -771,6 +771,12 @@ def extras(args, dev):
                             "stream_pairs_per_s": round(streamed / (ms / 1e3), 0),
                             "stream_sample_pairs": streamed,
                             "stream_write_gbs": round(streamed * 8 / (ms / 1e3) / 1e9, 1),
+                            "expand_roofline": {"bound": "hbm", "unit": "GB/s",
+                                                "achieved": round(streamed * 8 / (ms / 1e3) / 1e9, 1),
+                                                "peak": measured_peak_hbm()[0],
+                                                "frac": round(streamed * 8 / (ms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
+                                                "alg_bytes": "8 B written per materialised pair (uint32 left row, "
+                                                             "uint32 right row); row-id reads hit L2"},
                             "note": "pairs materialised as uint32 (left row, right row) in 2^30-pair chunks"}
     except Exception as e:
         out["cfg3_n1e7"] = {"error": repr(e)[:200]}

@@ -147,6 +147,56 @@ __global__ void __launch_bounds__(kThreads, RL_EXPAND_MIN_BLOCKS) expand_kernel(
         const uint32_t c = __ldg(a.rc + g);
         const uint32_t* lp = a.lpos + __ldg(a.ls + g);
         const uint32_t* rp = a.rpos + __ldg(a.rs + g);
+        if (!kChecksum && cols.n == 0 && a.lrows_out && a.rrows_out && s1 - s0 >= 8 * kThreads) {
+          // pairs only (cfg3 materialisation): 4 consecutive outputs per thread
+          // per step, one 16-byte store per row-id array (scalar head / tail)
+          const uint64_t oa = s0 - a.out_begin;
+          const uint64_t head = (4 - (oa & 3)) & 3;  // outputs before the first 16-byte boundary
+          auto scalar_at = [&](uint64_t u) {
+            const uint64_t local = u - kbeg;
+            const uint64_t li = local / c;
+            const uint32_t ri = uint32_t(local - li * c);
+            __stcs(a.lrows_out + (u - a.out_begin), __ldg(lp + li));
+            __stcs(a.rrows_out + (u - a.out_begin), __ldg(rp + ri));
+          };
+          if (tid < head) scalar_at(s0 + tid);
+          const uint64_t v0 = s0 + head;                   // first vector output
+          const uint64_t nvec = (s1 - v0) / 4;             // whole 4-output groups
+          const uint64_t tail0 = v0 + nvec * 4;
+          if (tid < s1 - tail0) scalar_at(tail0 + tid);
+          uint64_t u = v0 + uint64_t(tid) * 4;
+          if (u < tail0) {
+            const uint64_t local = u - kbeg;
+            uint64_t li = local / c;
+            uint32_t ri = uint32_t(local - li * c);
+            constexpr uint32_t kStep = 4 * kThreads;
+            const uint32_t q = kStep / c, r = kStep % c;
+            for (; u < tail0; u += kStep) {
+              uint32_t lv[4], rv[4];
+              uint64_t li2 = li;
+              uint32_t ri2 = ri;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                lv[e] = __ldg(lp + li2);
+                rv[e] = __ldg(rp + ri2);
+                if (++ri2 == c) {
+                  ri2 = 0;
+                  ++li2;
+                }
+              }
+              const uint64_t o = u - a.out_begin;
+              __stcs(reinterpret_cast<uint4*>(a.lrows_out + o), make_uint4(lv[0], lv[1], lv[2], lv[3]));
+              __stcs(reinterpret_cast<uint4*>(a.rrows_out + o), make_uint4(rv[0], rv[1], rv[2], rv[3]));
+              li += q;
+              ri += r;
+              if (ri >= c) {
+                ri -= c;
+                ++li;
+              }
+            }
+          }
+          continue;
+        }
         const uint64_t t = s0 + tid;
         if (t >= s1) continue;
         const uint64_t local = t - kbeg;

@@ -59,3 +59,27 @@ def test_order_by_multi_key_device_relation():
     want = O.sort_permutation([rel.column("b"), rel.column("a")], [True, False])
     assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
     assert (out.to_host().column("c") == want).all()
+
+
+def test_join_stream_vector_path_right_run_lengths():
+    """Materialised pair streaming of heavy keys (4 outputs per thread,
+    16-byte stores, scalar head/tail): right runs of 1, 2, 3, 7, 1023, 1025
+    and 4099 rows wrap (li, ri) inside and across 4-output groups; windows
+    start at odd offsets."""
+    rng = np.random.default_rng(31)
+    lparts, rparts = [], []
+    for kv, c in zip(range(10, 17), (1, 2, 3, 7, 1023, 1025, 4099)):
+        lparts.append(np.full(3000 + kv, kv, dtype=np.int64))
+        rparts.append(np.full(c, kv, dtype=np.int64))
+    lk = np.concatenate(lparts + [rng.integers(1000, 9000, 5000)]).astype(np.int64)
+    rk = np.concatenate(rparts + [rng.integers(1000, 9000, 5000)]).astype(np.int64)
+    lk, rk = lk[rng.permutation(len(lk))], rk[rng.permutation(len(rk))]
+    plan = pipeline.plan_join(torch.from_numpy(lk).cuda(), torch.from_numpy(rk).cuda())
+    assert plan.total == O.join_count(lk, rk)
+    for a, b, chunk in ((3, plan.total, 1_000_003), (0, plan.total, 1 << 22), (plan.total // 2 + 1, plan.total, 77_777)):
+        got_l, got_r = [], []
+        for start, lr, rr in pipeline.join_stream(plan, chunk_pairs=chunk, begin=a, end=b):
+            got_l.append(lr.cpu().numpy().view(np.uint32).astype(np.int64))
+            got_r.append(rr.cpu().numpy().view(np.uint32).astype(np.int64))
+        wl, wr = O.join_pairs(lk, rk, a, b)
+        assert (np.concatenate(got_l) == wl).all() and (np.concatenate(got_r) == wr).all()

@@ -59,7 +59,7 @@ namespace rl {
 namespace radix {
 
 #ifndef RL_ONESWEEP_ITEMS
-#define RL_ONESWEEP_ITEMS 12
+#define RL_ONESWEEP_ITEMS 14
 #endif
 #ifndef RL_ONESWEEP_MIN_BLOCKS
 #define RL_ONESWEEP_MIN_BLOCKS 2

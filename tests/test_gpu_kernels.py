@@ -11,7 +11,8 @@ from paper_2602_21237_b200 import engine
 
 pytestmark = pytest.mark.gpu
 
-SIZES = [2, 3, 5, 16, 17, 31, 33, 40, 80, 255, 333, 511, 700, 3071, 3072, 3073, 6143, 6145, 7000, 50_000]
+SIZES = [2, 3, 5, 16, 17, 31, 33, 40, 80, 255, 333, 511, 700, 3071, 3072, 3073, 3583, 3584, 3585, 6143, 6145,
+         7000, 7167, 7169, 50_000]
 
 
 def keys_for(n, mode, seed):

@@ -86,7 +86,7 @@ class GpuOps:
         perm = engine.sort_permutation([engine.SortAxis(keys, descending)], keys.numel(), keys.device)
         return perm.to(torch.int64) & 0xFFFFFFFF
 
-    def push_exchange(self, slot: str, cols, rows, counts, group):
+    def push_exchange(self, slot: str, cols, rows, counts, group, base: int = 0):
         """Partition gather + all-to-all in one kernel over peer memory
         (PeerExchange); None when this group has no symmetric memory."""
         dev = cols[0].device
@@ -96,7 +96,7 @@ class GpuOps:
         try:
             if key not in _PEER:
                 _PEER[key] = PeerExchange(group, dev, cols)
-            return _PEER[key].exchange(cols, rows, counts)
+            return _PEER[key].exchange(cols, rows, counts, base)
         except (RuntimeError, ImportError, AttributeError):
             _PEER[("ok", dev.index)] = False  # no symmetric memory here: NCCL from now on
             return None
@@ -181,14 +181,20 @@ class PeerExchange:
         self.bases = torch.tensor(table, dtype=torch.int64).view(-1).to(self.device)
         self.offs, self.cap = offs, cap
 
-    def exchange(self, cols: Sequence[torch.Tensor], rows: torch.Tensor, counts: torch.Tensor):
+    def exchange(self, cols: Sequence[torch.Tensor], rows: torch.Tensor, counts: torch.Tensor, base: int = 0):
+        """Returns (received columns, received local row ids, rows per source,
+        every source's row-id base) — the bases ride on the counts gather."""
         from . import _capi as C
         from . import engine
 
         p, me = self.p, self.me
-        mat_dev = torch.empty(p * p, dtype=torch.int64, device=self.device)
-        dist.all_gather_into_tensor(mat_dev, counts.to(torch.int64).reshape(p), group=self.group)
-        mat = mat_dev.cpu().view(p, p)  # mat[s][d]: rows s sends to d
+        mine = torch.empty(p + 1, dtype=torch.int64, device=self.device)
+        mine[:p] = counts.to(torch.int64).reshape(p)
+        mine[p] = base
+        gathered = torch.empty(p * (p + 1), dtype=torch.int64, device=self.device)
+        dist.all_gather_into_tensor(gathered, mine, group=self.group)
+        host = gathered.cpu().view(p, p + 1)  # the step's one host sync
+        mat, bases = host[:, :p], host[:, p].tolist()  # mat[s][d]: rows s sends to d
         self._ensure(int(mat.sum(0).max()))
         recv_counts = mat[:, me].tolist()
         total = sum(recv_counts)
@@ -206,7 +212,7 @@ class PeerExchange:
         for (dt, tail, w), o in zip(self.likes, self.offs):
             out.append(self.buf[o:o + total * w].view(dt).view((total,) + tail))
         recv_rows = self.buf[self.offs[-1]:self.offs[-1] + total * 4].view(torch.int32)
-        return out, recv_rows, recv_counts
+        return out, recv_rows, recv_counts, bases
 
 
 _PEER: dict = {}
@@ -301,13 +307,13 @@ def distributed_join(left: Sequence[torch.Tensor], left_key: int, left_base: int
     dev = left[left_key].device
 
     def shuffle(cols, key_idx, base, slot):
-        bases = _all_bases(base, dev, group)
         if hasattr(ops, "push_exchange"):
             rows, counts = ops.hash_partition(cols[key_idx], p, seed)
-            pushed = ops.push_exchange(slot, list(cols), rows, counts, group)
+            pushed = ops.push_exchange(slot, list(cols), rows, counts, group, base)
             if pushed is not None:
-                rcols, rrows, rc = pushed
+                rcols, rrows, rc, bases = pushed
                 return rcols, _global_ids(rrows, rc, bases)
+        bases = _all_bases(base, dev, group)
         rows, counts, moved = _partition_take(ops, "hash", cols[key_idx], list(cols), parts=p, seed=seed)
         recv, rc = exchange(moved + [rows], counts, group, with_counts=True)
         return recv[:-1], _global_ids(recv[-1], rc, bases)
@@ -362,6 +368,37 @@ def choose_splitters(keys: torch.Tensor, gid_base: int, descending: bool, group=
     return (sk, sg, bases) if with_bases else (sk, sg)
 
 
+def choose_splitters_device(keys: torch.Tensor, gid_base: int, descending: bool, group=None, per_rank: int = 256):
+    """choose_splitters without leaving the device: the gathered samples are
+    ordered by (key, gid) and the P-1 splitters picked on the GPU (ranks
+    with fewer rows contribute fewer samples; missing slots sort last)."""
+    p = _group_size(group)
+    n = keys.numel()
+    dev = keys.device
+    m = min(per_rank, n)
+    idx = (torch.arange(per_rank, device=dev, dtype=torch.int64) * max(n, 1)) // max(m, 1)
+    idx = idx.clamp_(max=max(n - 1, 0))
+    valid = torch.arange(per_rank, device=dev) < m
+    k = keys[idx] if n else torch.zeros(per_rank, dtype=torch.int64, device=dev)
+    ordk = torch.bitwise_not(k) if descending else k
+    pack = torch.stack([ordk, idx + gid_base, valid.to(torch.int64)])  # [3, per_rank]
+    allp = torch.empty((p * 3 * per_rank,), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allp, pack.reshape(-1), group=group)
+    allp = allp.view(p, 3, per_rank).permute(1, 0, 2).reshape(3, -1)
+    ok, gs, v = allp[0], allp[1], allp[2].bool()
+    # composite (valid first, key, gid) order: stable sorts, least significant first
+    o = torch.argsort(gs, stable=True)
+    o = o[torch.argsort(ok[o], stable=True)]
+    o = o[torch.argsort((~v[o]).to(torch.int8), stable=True)]
+    cnt = v.sum()
+    picks = (torch.arange(1, p, device=dev, dtype=torch.int64) * cnt) // p
+    picks = torch.minimum(picks, (cnt - 1).clamp(min=0))
+    sel = o[picks]
+    sk = ok[sel]
+    sk = torch.bitwise_not(sk) if descending else sk
+    return sk, gs[sel]
+
+
 @dataclass
 class SortShard:
     columns: List[torch.Tensor]  # this rank's slice of the globally sorted relation
@@ -373,15 +410,17 @@ def distributed_sort(cols: Sequence[torch.Tensor], key_idx: int, gid_base: int, 
     """Range-partitioned stable ORDER BY on one int64 key (see module doc)."""
     ops = ops or GpuOps()
     keys = cols[key_idx]
-    split_k, split_g, bases = choose_splitters(keys, gid_base, descending, group, with_bases=True)
     pushed = None
-    if hasattr(ops, "push_exchange"):
+    if hasattr(ops, "push_exchange") and keys.device.type == "cuda" and _peer_exchange_ok(group, keys.device):
+        # device-side splitters (no host sync); the bases ride on the count exchange
+        split_k, split_g = choose_splitters_device(keys, gid_base, descending, group)
         rows, counts = ops.range_partition(keys, gid_base, split_k, split_g, descending)
-        pushed = ops.push_exchange("sort", list(cols), rows, counts, group)
+        pushed = ops.push_exchange("sort", list(cols), rows, counts, group, gid_base)
     if pushed is not None:
-        rcols, rrows, rc = pushed
+        rcols, rrows, rc, bases = pushed
         rgids = _global_ids(rrows, rc, bases)
     else:
+        split_k, split_g, bases = choose_splitters(keys, gid_base, descending, group, with_bases=True)
         rows, counts, moved = _partition_take(ops, "range", keys, list(cols), gid_base=gid_base, split_keys=split_k,
                                               split_gids=split_g, descending=descending)
         recv, rc = exchange(moved + [rows], counts, group, with_counts=True)

@@ -84,6 +84,14 @@ def _worker(rank, world, port, case, q):
                                      ops=ops)
             out = {"lg": res.left_gids.numpy(), "rg": res.right_gids.numpy(), "total": res.total_matches,
                    "cols": [c.numpy() for c in res.columns]}
+        elif case["kind"] == "splitters":
+            n = case["n"]
+            keys = rng.integers(-case["dom"], case["dom"], n).astype(np.int64)
+            a, b = _shard(n, world, rank)
+            kt = torch.from_numpy(keys[a:b])
+            hk, hg = D.choose_splitters(kt, a, case["desc"])
+            dk, dg = D.choose_splitters_device(kt, a, case["desc"])
+            out = {"host": (hk.numpy(), hg.numpy()), "dev": (dk.numpy(), dg.numpy())}
         else:
             n = case["n"]
             keys = rng.integers(-case["dom"], case["dom"], n).astype(np.int64)
@@ -156,3 +164,12 @@ def test_exchange_counts_and_order_two_ranks():
     case = {"kind": "join", "seed": 1, "nl": 1, "nr": 0, "dom": 3}
     parts = _run(case, 2)
     assert all(p["total"] == 0 for p in parts)
+
+
+@pytest.mark.parametrize("desc", [False, True])
+def test_device_splitters_match_host_splitters(desc):
+    """choose_splitters_device (no host round trip) picks the same (key, gid)
+    splitters as the host version, duplicates included."""
+    parts = _run({"kind": "splitters", "seed": 13, "n": 3001, "dom": 50, "desc": desc}, 2)
+    for p in parts:
+        assert (p["host"][0] == p["dev"][0]).all() and (p["host"][1] == p["dev"][1]).all()

@@ -342,31 +342,15 @@ def run_ours(args):
     # cooperative sort + payload gather into static buffers): the same work
     # every step without host launch gaps. Graph capture failing falls back
     # to eager launches (config["launch"] says which).
-    g_keys = torch.empty(n, dtype=torch.int64, device=dev)
-    g_perm = torch.empty(n, dtype=torch.int32, device=dev)
     g_pay = torch.empty((n, 4), dtype=torch.uint8, device=dev)
-
-    def graph_body():
-        _capi.check(lib.rl_sort_axis(ctypes.c_void_p(keys_d.data_ptr()), 0, 8, 0, 0, None, n,
-                                     ctypes.c_void_p(g_keys.data_ptr()), ctypes.c_void_p(g_perm.data_ptr()),
-                                     ctypes.c_void_p(ws.data_ptr()), ws.numel(), engine.stream_handle()), "sort")
-        engine.gather_rows(g_perm, [engine.OutColumn(pay_d, g_pay, 4, 0)])
-
     graph, launch_mode, per_step_launches = None, "eager", 0
     try:
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            graph_body()
-        torch.cuda.current_stream().wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        c0 = lib.rl_launch_count()
-        with torch.cuda.graph(graph):
-            graph_body()
-        per_step_launches = lib.rl_launch_count() - c0
+        graph = engine.SortGraph(keys_d, gather=[engine.OutColumn(pay_d, g_pay, 4, 0)])
+        per_step_launches = graph.launches_per_replay
+        g_keys, g_perm = graph.sorted_keys, graph.perm
         graph.replay()
         torch.cuda.synchronize()
-        launch_mode = "cuda graph replay"
+        launch_mode = "cuda graph replay (engine.SortGraph)"
     except Exception:  # noqa: BLE001 — keep measuring, eagerly
         graph = None
 

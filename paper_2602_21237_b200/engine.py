@@ -276,6 +276,48 @@ def sort_permutation(axes: Sequence[SortAxis], n: int, device, sorted_keys_out: 
     return perm
 
 
+class SortGraph:
+    """A stable ORDER BY of one int64 key column (+ Relation.take of bound
+    columns) captured once as a CUDA graph: histogram, cooperative sort and
+    gather replay without host launch work (repeated sorts of same-shaped,
+    device-resident inputs — e.g. a serving loop). ``replay()`` sorts the
+    current contents of ``keys`` / the gather sources into ``sorted_keys``,
+    ``perm`` and the gather destinations, which are fixed at capture."""
+
+    def __init__(self, keys: torch.Tensor, descending: bool = False, gather: Sequence[OutColumn] = ()):
+        _require_cuda(keys, "keys")
+        lib = C.load()
+        self.keys = aligned16(keys)
+        n = self.keys.numel()
+        dev = self.keys.device
+        self.sorted_keys = torch.empty(n, dtype=torch.int64, device=dev)
+        self.perm = torch.empty(n, dtype=_U32, device=dev)
+        self.gather = list(gather)
+        self._ws = workspace(lib.rl_sort_workspace_bytes(n), dev)
+        self._desc = int(descending)
+
+        def body():
+            C.check(lib.rl_sort_axis(_ptr(self.keys), C.RL_COL_INT64, 8, 0, self._desc, None, n,
+                                     _ptr(self.sorted_keys), _ptr(self.perm), _ptr(self._ws), self._ws.numel(),
+                                     stream_handle()), "rl_sort_axis")
+            if self.gather:
+                gather_rows(self.perm, self.gather)
+
+        side = torch.cuda.Stream(device=dev)  # warm-up outside the capture (lazy attributes, allocator)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        c0 = lib.rl_launch_count()
+        with torch.cuda.graph(self.graph):
+            body()
+        self.launches_per_replay = lib.rl_launch_count() - c0
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+
 def gather_rows(rows: torch.Tensor, columns: Sequence[OutColumn]) -> None:
     """K7: dst row t = src row rows[t] for every column (Relation.take)."""
     lib = C.load()

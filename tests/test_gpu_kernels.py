@@ -184,3 +184,24 @@ def test_fused_final_pass_gather_equals_take():
     engine.sort_permutation([engine.SortAxis(torch.from_numpy(keys).cuda())], 1000, "cuda",
                             gather=[engine.OutColumn(src, dst, 8, 0)], fuse_gather=True)
     assert (dst.cpu().numpy() == np.arange(1000)).all()
+
+
+def test_sort_graph_replays_current_inputs():
+    """engine.SortGraph: a captured sort + gather re-sorts whatever the bound
+    input buffers hold at replay time (hybrid-sized and LSD-sized inputs)."""
+    for n in (300_000, 5000):
+        rng = np.random.default_rng(n)
+        keys = torch.empty(n, dtype=torch.int64, device="cuda")
+        pay = torch.empty((n, 4), dtype=torch.uint8, device="cuda")
+        out = torch.empty_like(pay)
+        g = engine.SortGraph(keys, gather=[engine.OutColumn(pay, out, 4, 0)])
+        for seed in (1, 2):
+            k = rng.integers(-(2**63), 2**63 - 1, n, dtype=np.int64, endpoint=True)
+            p = rng.integers(0, 256, (n, 4), dtype=np.uint8)
+            keys.copy_(torch.from_numpy(k))
+            pay.copy_(torch.from_numpy(p))
+            g.replay()
+            want = O.stable_axis_order(k, False)
+            assert (u32(g.perm) == want).all()
+            assert (g.sorted_keys.cpu().numpy() == k[want]).all()
+            assert (out.cpu().numpy() == p[want]).all()

@@ -78,7 +78,7 @@ class ClockSampler:
                ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
                ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.001):
         self.index = index
         self.period = period_s
         self.rows = []  # (sm_mhz, max_mhz, set(reasons))

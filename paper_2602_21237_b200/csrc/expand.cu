@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(kThreads, RL_EXPAND_MIN_BLOCKS) expand_kernel(
   const int tid = threadIdx.x, warp = tid >> 5;
   uint64_t sum = 0;  // checksum mode
   int64_t hint = 0;  // the next sub-tile's first key is at or after this one's last
+  bool reuse = false;  // the first tile's key window = the streaming check's search
 
   // ---- streaming mode: the CTA's whole output range is covered by few heavy
   // keys (>= 1024 pairs per key on average, e.g. the Zipf head of BASELINE
@@ -231,6 +232,8 @@ __global__ void __launch_bounds__(kThreads, RL_EXPAND_MIN_BLOCKS) expand_kernel(
       }
       tiles_per_cta = 0;  // skip the tile loop
     }
+    // a one-tile CTA's tile is the range just searched: reuse [ga, gb]
+    reuse = tiles_per_cta == 1 && c1 - c0 <= uint64_t(kTile);
     __syncthreads();
   }
 
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, RL_EXPAND_MIN_BLOCKS) expand_kernel(
   const uint64_t t0 = a.out_begin + (uint64_t(blockIdx.x) * tiles_per_cta + sub) * kTile;
   if (t0 >= a.out_end) break;
   const uint64_t t1 = min(t0 + kTile, a.out_end);
-  if (warp < 2) {
+  if (warp < 2 && !(reuse && sub == 0)) {
     const int64_t g = warp_last_le(a.offs, hint, a.m, warp == 0 ? t0 : t1 - 1);
     if ((tid & 31) == 0) s_g[warp] = g;
   }

@@ -92,6 +92,7 @@ constexpr int kLocalCap = RL_LOCAL_CAP;    // rows of one on-chip local run (and
 constexpr int kSubBuckets = 1 << 16;       // (d7, d6) sub-buckets
 constexpr int kGroupSubs = 16;             // sub-buckets claimed per local work item
 constexpr int64_t kHybridMinRows = 1 << 18;
+constexpr int64_t kCountAllRows = int64_t(1) << 22;  // raw keys below this: all 8 histograms up front
 constexpr uint32_t kHybridEpoch = kPasses; // LSD after a hybrid fallback publishes epoch PASS + 1 + 8
 
 static_assert(kThreads == kBins, "tile scan maps one digit per thread");
@@ -149,6 +150,7 @@ struct SortArgs {
   int64_t* out_keys;         // final sorted int64 keys (optional, raw modes)
   uint32_t* out_vals;        // final permutation
   int mode;                  // SortMode
+  int count_all;             // raw keys: the histogram kernel counted every digit (small n)
   // zeroed per call
   uint32_t* ghist;           // [kPasses][kBins]
   uint32_t* tile_counter;    // [2][kPasses] (first attempt, LSD after a hybrid fallback)
@@ -523,7 +525,7 @@ __device__ __forceinline__ void run_pass(const SortArgs& a, uint8_t* smem, uint3
 // step in flight before the first use; otherwise the generic loader
 // (gathered rows, Bytes words; materialises the transformed words).
 constexpr int kHistThreads = 512;
-template <bool RAW>
+template <bool RAW, bool ALL = !RAW>
 __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
   __shared__ uint32_t h[kPasses * kBins];
   const int tid = threadIdx.x;
@@ -536,8 +538,8 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
   uint64_t vary = 0, k0 = 0;
   if constexpr (RAW) k0 = xform(uint64_t(__ldg(static_cast<const long long*>(a.col))), a.desc);
   auto count = [&](uint64_t k) {
-    if constexpr (RAW) {
-      vary |= k ^ k0;
+    if constexpr (RAW) vary |= k ^ k0;
+    if constexpr (RAW && !ALL) {
       atomicAdd(&h[6 * kBins + ((k >> (6 * kBits)) & (kBins - 1))], 1u);
       atomicAdd(&h[7 * kBins + ((k >> (7 * kBits)) & (kBins - 1))], 1u);
     } else {
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
       atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(hi) << 32) | lo);
   }
   __syncthreads();
-  for (int i = RAW ? 6 * kBins + tid : tid; i < kPasses * kBins; i += kHistThreads) {
+  for (int i = RAW && !ALL ? 6 * kBins + tid : tid; i < kPasses * kBins; i += kHistThreads) {
     const uint32_t c = h[i];
     if (c) atomicAdd(&a.ghist[i], c);
   }
@@ -983,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
     uint32_t* warp_sums = reinterpret_cast<uint32_t*>(smem);  // scratch
     const uint64_t vary = raw ? __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4)) : 0ull;
     uint32_t nz = 1, mx = 1;
-    for (int p = raw ? 6 : 0; p < kPasses; ++p) {
+    for (int p = raw && !a.count_all ? 6 : 0; p < kPasses; ++p) {
       const uint32_t c = __ldcg(a.ghist + p * kBins + tid);
       uint32_t total;
       bin_off[p * kBins + tid] = block_exclusive_scan<kThreads>(c, warp_sums, &total);
@@ -1019,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       plan[2 * kPasses + 2] = plan[6] + plan[7];
       uint32_t low = 0;
       for (int p = 0; p < 6; ++p) low |= plan[p] << p;
-      plan[2 * kPasses + 3] = raw ? low : 0u;  // digits the LSD path still has to count
+      plan[2 * kPasses + 3] = raw && !a.count_all ? low : 0u;  // digits the LSD path still has to count
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
     }
@@ -1195,7 +1197,10 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(limit, tiles)));
   a.mode = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() ? kModeHybrid : kModeLsd;
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
-  if (a.src_mode == kSrcInt64) hist_kernel<true><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
+  // small raw inputs (never worth the hybrid's skipped histograms): every digit in the histogram kernel
+  a.count_all = a.src_mode == kSrcInt64 && a.n < kCountAllRows ? 1 : 0;
+  if (a.src_mode == kSrcInt64 && a.count_all) hist_kernel<true, true><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
+  else if (a.src_mode == kSrcInt64) hist_kernel<true, false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   else hist_kernel<false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
   void* params[] = {&a};

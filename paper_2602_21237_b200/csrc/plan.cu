@@ -7,6 +7,7 @@
 // a 1M x 1M join is not paced by per-launch host work. The plan arrays stay
 // in the workspace for rl_join_expand.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -69,7 +70,11 @@ struct Sizer {  // CarveSize with the pointer-returning interface of Carve
 // side then needs its own scratch.
 constexpr int64_t kConcurrentMaxRows = int64_t(16) << 20;
 static bool concurrent_sides(int64_t nl, int64_t nr) {
-  return nl > 0 && nr > 0 && std::max(nl, nr) <= kConcurrentMaxRows;
+  static const bool serial = [] {  // RL_PLAN_SERIAL=1: one side after the other (A/B measurements)
+    const char* v = getenv("RL_PLAN_SERIAL");
+    return v && v[0] && v[0] != '0';
+  }();
+  return !serial && nl > 0 && nr > 0 && std::max(nl, nr) <= kConcurrentMaxRows;
 }
 
 static size_t side_scratch_bytes(int64_t n) {

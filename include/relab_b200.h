@@ -49,6 +49,7 @@ extern "C" {
 #define RL_ERR_OUTPUT_TOO_LARGE 2 /* relab.errors.OutputTooLarge               */
 #define RL_ERR_WORKSPACE 3        /* workspace too small / misaligned          */
 #define RL_ERR_TOO_MANY_ROWS 4    /* n > RL_MAX_ROWS                           */
+#define RL_ERR_IO 5               /* file read/write failed (OSError)          */
 #define RL_ERR_CUDA 1000          /* RL_ERR_CUDA + cudaError_t                 */
 
 #define RL_MAX_ROWS 4294967295LL  /* uint32 row ids */
@@ -329,6 +330,23 @@ RL_API void* rl_stager_create(int32_t threads, size_t chunk_bytes, int32_t slots
 RL_API void rl_stager_destroy(void* stager);
 RL_API int rl_stager_h2d(void* stager, void* dst_dev, const void* src_host,
                          size_t bytes, void* stream, void* ready_event);
+
+/* RELCOL01 relation files straight to / from HBM (relation.py:364-419).
+ * rl_stager_file_h2d: `bytes` at `file_offset` of the open file `fd` are
+ * pread() by the stager's threads into its pinned ring while the copy
+ * engine DMAs the previous chunk to dst_dev on the stager's copy stream;
+ * `stream` waits for the upload, ready_event (optional) orders it after
+ * earlier work. rl_stager_file_d2h: device bytes -> file section through the
+ * ring (DMA of chunk c+1 overlaps the pwrite of chunk c); synchronous.
+ * RL_ERR_IO on a short read / failed write. */
+RL_API int rl_stager_file_h2d(void* stager, void* dst_dev, int32_t fd,
+                 uint64_t file_offset, size_t bytes, void* stream,
+                 void* ready_event);
+RL_API int rl_stager_file_d2h(void* stager, const void* src_dev, int32_t fd,
+                 uint64_t file_offset, size_t bytes, void* stream);
+/* File section -> host memory (page-locked columns), parallel pread(). */
+RL_API int rl_stager_file_read(void* stager, void* dst_host, int32_t fd,
+                 uint64_t file_offset, size_t bytes);
 /* Long-lived inputs (a relation reused across repetitions) are page-locked
  * once and then uploaded with one direct DMA each (no staging copy). */
 RL_API int rl_host_register(void* host, size_t bytes);

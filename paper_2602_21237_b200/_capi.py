@@ -22,6 +22,7 @@ RL_ERR_BAD_ARG = 1
 RL_ERR_OUTPUT_TOO_LARGE = 2
 RL_ERR_WORKSPACE = 3
 RL_ERR_TOO_MANY_ROWS = 4
+RL_ERR_IO = 5
 RL_ERR_CUDA = 1000
 
 RL_COL_INT64 = 0
@@ -65,6 +66,9 @@ SIGNATURES = {
     "rl_device_sm_count": (ctypes.c_int, []),
     "rl_launch_count": (_I64, []),
     "rl_push_rows": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _I32, _P, _P, _P]),
+    "rl_stager_file_h2d": (ctypes.c_int, [_P, _P, _I32, ctypes.c_uint64, _SZ, _P, _P]),
+    "rl_stager_file_d2h": (ctypes.c_int, [_P, _P, _I32, ctypes.c_uint64, _SZ, _P]),
+    "rl_stager_file_read": (ctypes.c_int, [_P, _P, _I32, ctypes.c_uint64, _SZ]),
     "rl_sort_workspace_bytes": (_SZ, [_I64]),
     "rl_sort_axis": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
     "rl_sort_axis_profiled": (
@@ -150,6 +154,8 @@ def check(status: int, what: str) -> None:
         raise ValueError(msg)
     if status == RL_ERR_OUTPUT_TOO_LARGE:
         raise OutputTooLarge(msg)
+    if status == RL_ERR_IO:
+        raise OSError(msg)
     raise DeviceError(msg)
 
 

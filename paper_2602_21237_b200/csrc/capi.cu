@@ -73,6 +73,7 @@ const char* rl_strerror(int status) {
     case RL_ERR_OUTPUT_TOO_LARGE: return "join output exceeds the row cap";
     case RL_ERR_WORKSPACE: return "workspace too small or misaligned";
     case RL_ERR_TOO_MANY_ROWS: return "more rows than uint32 row ids can address";
+    case RL_ERR_IO: return "file read or write failed";
     default: break;
   }
   if (status >= RL_ERR_CUDA) return cudaGetErrorString(static_cast<cudaError_t>(status - RL_ERR_CUDA));

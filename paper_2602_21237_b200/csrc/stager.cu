@@ -11,12 +11,15 @@
 // kernels already queued keep running — uploading the payload columns
 // overlaps the key sort.
 #include <algorithm>
+#include <cerrno>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
+
+#include <unistd.h>
 
 #include "common.cuh"
 
@@ -212,6 +215,143 @@ RL_API int rl_stager_h2d(void* handle, void* dst_dev, const void* src_host, size
   }
   cudaEventRecord(s->done, s->copy_stream);
   return rl::rl_cuda_status(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), s->done, 0));
+}
+
+// ---- RELCOL01 relation files straight to / from HBM (relation.py:364-419):
+// a column section of `bytes` at `file_offset` of the open file `fd` is read
+// by the pool threads with pread() into the pinned ring — each chunk split
+// across the threads — while the copy engine DMAs the previous chunk; no
+// numpy array, no pageable intermediate. The write direction DMAs a chunk
+// into the ring and the threads pwrite() it.
+static bool pread_all(int fd, char* dst, size_t len, uint64_t off) {
+  while (len) {
+    const ssize_t r = pread(fd, dst, len, off_t(off));
+    if (r < 0 && errno == EINTR) continue;
+    if (r <= 0) return false;
+    dst += r;
+    off += uint64_t(r);
+    len -= size_t(r);
+  }
+  return true;
+}
+
+static bool pwrite_all(int fd, const char* src, size_t len, uint64_t off) {
+  while (len) {
+    const ssize_t r = pwrite(fd, src, len, off_t(off));
+    if (r < 0 && errno == EINTR) continue;
+    if (r <= 0) return false;
+    src += r;
+    off += uint64_t(r);
+    len -= size_t(r);
+  }
+  return true;
+}
+
+RL_API int rl_stager_file_h2d(void* handle, void* dst_dev, int32_t fd, uint64_t file_offset, size_t bytes,
+                              void* stream, void* ready_event) {
+  Stager* s = static_cast<Stager*>(handle);
+  if (!s || fd < 0 || (bytes && !dst_dev)) return RL_ERR_BAD_ARG;
+  if (bytes == 0) return RL_OK;
+  std::lock_guard<std::mutex> g(s->call_mu);
+  if (ready_event) {
+    cudaError_t e = cudaStreamWaitEvent(s->copy_stream, static_cast<cudaEvent_t>(ready_event), 0);
+    if (e != cudaSuccess) return rl::rl_cuda_status(e);
+  }
+  const int nt = s->pool.size();
+  for (size_t off = 0; off < bytes; off += s->chunk) {
+    const size_t len = std::min(s->chunk, bytes - off);
+    const int slot = s->next_slot;
+    s->next_slot = (s->next_slot + 1) % s->slots;
+    cudaError_t e = cudaEventSynchronize(s->slot_free[slot]);
+    if (e != cudaSuccess) return rl::rl_cuda_status(e);
+    char* dst = s->ring + size_t(slot) * s->chunk;
+    bool ok = true;
+    std::mutex ok_mu;
+    const size_t piece = (len + nt - 1) / nt;
+    s->pool.parallel([&](int i) {
+      const size_t a = std::min(len, size_t(i) * piece), b = std::min(len, a + piece);
+      if (b > a && !pread_all(fd, dst + a, b - a, file_offset + off + a)) {
+        std::lock_guard<std::mutex> lk(ok_mu);
+        ok = false;
+      }
+    });
+    if (!ok) return RL_ERR_IO;
+    e = cudaMemcpyAsync(static_cast<char*>(dst_dev) + off, dst, len, cudaMemcpyHostToDevice, s->copy_stream);
+    if (e != cudaSuccess) return rl::rl_cuda_status(e);
+    cudaEventRecord(s->slot_free[slot], s->copy_stream);
+  }
+  cudaEventRecord(s->done, s->copy_stream);
+  return rl::rl_cuda_status(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), s->done, 0));
+}
+
+// File section -> host memory (e.g. page-locked columns), the threads
+// splitting the section between them.
+RL_API int rl_stager_file_read(void* handle, void* dst_host, int32_t fd, uint64_t file_offset, size_t bytes) {
+  Stager* s = static_cast<Stager*>(handle);
+  if (!s || fd < 0 || (bytes && !dst_host)) return RL_ERR_BAD_ARG;
+  if (bytes == 0) return RL_OK;
+  const int nt = s->pool.size();
+  bool ok = true;
+  std::mutex ok_mu;
+  const size_t piece = (bytes + nt - 1) / nt;
+  s->pool.parallel([&](int i) {
+    const size_t a = std::min(bytes, size_t(i) * piece), b = std::min(bytes, a + piece);
+    if (b > a && !pread_all(fd, static_cast<char*>(dst_host) + a, b - a, file_offset + a)) {
+      std::lock_guard<std::mutex> lk(ok_mu);
+      ok = false;
+    }
+  });
+  return ok ? RL_OK : RL_ERR_IO;
+}
+
+// Device column -> file section. Synchronous (returns after the data is in
+// the file): the DMA of chunk c+1 overlaps the pwrite of chunk c.
+RL_API int rl_stager_file_d2h(void* handle, const void* src_dev, int32_t fd, uint64_t file_offset, size_t bytes,
+                              void* stream) {
+  Stager* s = static_cast<Stager*>(handle);
+  if (!s || fd < 0 || (bytes && !src_dev)) return RL_ERR_BAD_ARG;
+  if (bytes == 0) return RL_OK;
+  std::lock_guard<std::mutex> g(s->call_mu);
+  cudaError_t e = cudaEventRecord(s->done, static_cast<cudaStream_t>(stream));  // producers of src_dev first
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s->copy_stream, s->done, 0);
+  if (e != cudaSuccess) return rl::rl_cuda_status(e);
+  const int nt = s->pool.size();
+  const size_t nchunks = (bytes + s->chunk - 1) / s->chunk;
+  std::vector<int> slot_of(nchunks);
+  auto issue = [&](size_t c) -> cudaError_t {
+    const size_t off = c * s->chunk, len = std::min(s->chunk, bytes - off);
+    const int slot = s->next_slot;
+    s->next_slot = (s->next_slot + 1) % s->slots;
+    slot_of[c] = slot;
+    cudaError_t err = cudaEventSynchronize(s->slot_free[slot]);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(s->ring + size_t(slot) * s->chunk, static_cast<const char*>(src_dev) + off, len,
+                            cudaMemcpyDeviceToHost, s->copy_stream);
+    if (err == cudaSuccess) err = cudaEventRecord(s->slot_free[slot], s->copy_stream);
+    return err;
+  };
+  if (nchunks) e = issue(0);
+  for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    if (c + 1 < nchunks && s->slots > 1) e = issue(c + 1);  // next DMA in flight while this chunk is written
+    if (e != cudaSuccess) break;
+    const int slot = slot_of[c];
+    e = cudaEventSynchronize(s->slot_free[slot]);
+    if (e != cudaSuccess) break;
+    const size_t off = c * s->chunk, len = std::min(s->chunk, bytes - off);
+    const char* src = s->ring + size_t(slot) * s->chunk;
+    bool ok = true;
+    std::mutex ok_mu;
+    const size_t piece = (len + nt - 1) / nt;
+    s->pool.parallel([&](int i) {
+      const size_t a = std::min(len, size_t(i) * piece), b = std::min(len, a + piece);
+      if (b > a && !pwrite_all(fd, src + a, b - a, file_offset + off + a)) {
+        std::lock_guard<std::mutex> lk(ok_mu);
+        ok = false;
+      }
+    });
+    if (!ok) return RL_ERR_IO;
+  }
+  return rl::rl_cuda_status(e);
 }
 
 }  // extern "C"

@@ -63,6 +63,20 @@ class DeviceRelation:
             cls = getattr(sys.modules.get(type(self.schema).__module__), "Relation", R.Relation)
         return cls(self.schema, tuple(h.numpy() for h in hosts))
 
+    @classmethod
+    def from_file(cls, path, device=None, rows=None) -> "DeviceRelation":
+        """A RELCOL01 relation file (relation.py:364-419) straight into HBM,
+        optionally only the row range ``rows = (a, b)`` (relfile.read_device)."""
+        from .relfile import read_device
+
+        return read_device(path, device, rows)
+
+    def to_file(self, path) -> None:
+        """Write a RELCOL01 file byte-identical to relation.write_relation's."""
+        from .relfile import write_device
+
+        write_device(self, path)
+
     def digest(self) -> int:
         """relation.py:319-330 multiset digest, computed on the device."""
         return engine.multiset_digest(self.columns) if self.row_count else 0

@@ -34,6 +34,7 @@ import os
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 from fractions import Fraction
@@ -181,6 +182,24 @@ def cpu_join_sample(r, s, reps):
         O.join_columns(list(r.columns), 0, list(s.columns), 0)
         times.append(time.perf_counter() - t0)
     return times
+
+
+def cpu_relational_sample(r, s, reps):
+    """The reference's CPU relational path — memory-budgeted Grace hash join
+    with temp-file spill at work_mem = 1 MB (rowpath.py:177-335, restated in
+    oracle/relational_baseline.py and pinned to the reference's block counts)
+    — on the box's host, temp files under $TMPDIR, spill counted."""
+    from oracle import relational_baseline as RB
+
+    times, st = [], None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _rows, st = RB.hash_join_row(list(r.columns), [8, 8], 0, list(s.columns), [8, 8], 0, 1 << 20)
+        times.append(time.perf_counter() - t0)
+    return {"p50_ms": round(1e3 * percentile(times, 50), 2), "p99_ms": round(1e3 * percentile(times, 99), 2),
+            "reps": reps, "work_mem_bytes": 1 << 20, "temp_blocks_written": st.temp_blocks_written,
+            "temp_mb": round(st.temp_mb, 2), "partition_passes": st.partition_passes, "cores": 1, "kind": "port",
+            "temp_dir": tempfile.gettempdir()}
 
 
 def run_reference(args):
@@ -662,6 +681,8 @@ def join_cfg1(args, dev, rank, world):
         res["cpu_tensor_path"] = {"p50_ms": round(1e3 * percentile(t, 50), 2), "p99_ms": round(1e3 * percentile(t, 99), 2),
                                   "reps": 20, "cores": 1, "kind": "port"}
         res["p99_speedup_e2e_vs_cpu"] = round(res["cpu_tensor_path"]["p99_ms"] / res["e2e_p99_ms"], 1)
+        res["cpu_relational_path"] = cpu_relational_sample(r, s, reps=10)
+        res["p99_speedup_e2e_vs_cpu_relational"] = round(res["cpu_relational_path"]["p99_ms"] / res["e2e_p99_ms"], 1)
     return res
 
 

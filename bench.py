@@ -770,17 +770,26 @@ def extras(args, dev):
         return res, ts
 
     # cfg5: uniform keys with domain N, join then ORDER BY the R payload, kept in HBM
+    from paper_2602_21237_b200 import policy, records as RR
+
     spec = SortSpec(("payload",))
     for n in (10**6, 10**7, 10**8):
         try:
             r, s = synth.cfg1_relations(n=n, domain=n)
+            budget = RR.MemoryBudget(1 << 20)
+            jc = policy.select_path(policy.join_signals(r, s, "key", budget, key_cardinality=n))
+            # the CPU relational path (work_mem = 1 MB, spill counted) at the sizes it finishes in seconds
+            rel_cpu = cpu_relational_sample(r, s, reps=1) if n <= 10**7 else None
             dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
             del r, s
             pipeline.join_then_order_by(dr, ds, "key", spec)
             res, ts = timed(lambda: pipeline.join_then_order_by(dr, ds, "key", spec), 5)
             out[f"cfg5_n{n:.0e}"] = {"rows_out": res.row_count, "p50_ms": round(percentile(ts, 50), 3),
                                      "max_ms": round(max(ts), 3),
-                                     "mrows_per_s": round(2 * n / (statistics.median(ts) / 1e3) / 1e6, 1)}
+                                     "mrows_per_s": round(2 * n / (statistics.median(ts) / 1e3) / 1e6, 1),
+                                     "select_path_join": f"{jc.path.name}/{jc.reason.name}",
+                                     "cpu_relational_join_ms": rel_cpu and rel_cpu["p50_ms"],
+                                     "cpu_relational_temp_mb": rel_cpu and rel_cpu["temp_mb"]}
             del dr, ds, res
         except Exception as e:  # keep the headline line even if an extra fails
             out[f"cfg5_n{n:.0e}"] = {"error": repr(e)[:200]}

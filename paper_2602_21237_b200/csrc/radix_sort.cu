@@ -51,6 +51,7 @@
 // from (complemented when descending) bytes, zero padded
 // (tensorpath.py:220-225).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -99,7 +100,22 @@ static_assert(kThreads == kBins, "tile scan maps one digit per thread");
 static_assert(kStamps == RL_SORT_STAMPS, "stamp layout is part of the ABI");
 
 enum KeyMode : int { kRawAsc = 0, kRawDesc = 1, kMaterialized = 2 };
-enum SortMode : int { kModeLsd = 0, kModeHybrid = 1 };  // hybrid: try the wide-key path first
+enum SortMode : int { kModeLsd = 0, kModeHybrid = 1, kModeScatter = 2 };  // hybrid/scatter: try the wide-key path first
+
+// scatter hybrid: exact per-chunk 16-bit counts, then two non-stable
+// counting passes (digit 7; digit 6 inside every digit-7 bucket), then the local phase
+constexpr int kScatThreads = 1024;
+constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
+constexpr int kMaxChunks = 160;
+constexpr int kSItems = 8;
+constexpr int kSTile = kScatThreads * kSItems;     // rows per staged tile
+constexpr int64_t kScatterMinRows = int64_t(1) << 22;
+#ifndef RL_SLICE_ROWS
+#define RL_SLICE_ROWS 32768
+#endif
+constexpr int64_t kSliceRows = RL_SLICE_ROWS;      // digit-7 bucket rows per pass-B work item (whole chunks)
+constexpr size_t kSStage = size_t(kSTile) * 12;    // staged keys + row ids (also reduction scratch)
+constexpr size_t kSSmem = kSStage + 4 * 256 * 4 + 64 * 4;
 enum SrcMode : int { kSrcInt64 = 0, kSrcInt64Gather = 1, kSrcBytes = 2, kSrcWords = 3 };
 
 __device__ __forceinline__ uint64_t xform(uint64_t x, int desc) {
@@ -163,6 +179,14 @@ struct SortArgs {
   // columns gathered by the final permutation inside the last pass
   // (Relation.take fused into the sort: dst row o = src row perm[o])
   FusedColumns gather;
+  // scatter hybrid (kModeScatter)
+  uint32_t* chunk_cnt;       // [kMaxChunks][kScatWords] rows per (chunk, sub-bucket), packed u16 pairs
+  uint32_t* d7_cnt;          // [kMaxChunks][kBins] rows per (chunk, digit 7)
+  uint32_t* d7_base;         // [kBins + 1] digit-7 bucket starts
+  uint32_t* sub_tot;         // [kSubBuckets] rows per sub-bucket
+  uint4* items;              // pass-B work items (digit-7 bucket, first chunk, end chunk)
+  uint32_t* meta;            // [0] work items
+  int chunks;                // input chunks = CTAs of the histogram and digit-7 kernels
 };
 
 __device__ __forceinline__ uint64_t load_key(const SortArgs& a, int64_t i) {
@@ -613,7 +637,7 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
   constexpr int kV = 8;
   auto count = [&](uint64_t k) {
 #pragma unroll
-    for (int p = 0; p < 6; ++p)
+    for (int p = 0; p < kPasses; ++p)
       if ((digits >> p) & 1u) atomicAdd(&h[p * kBins + ((k >> (p * kBits)) & (kBins - 1))], 1u);
   };
   const int64_t stride = int64_t(gridDim.x) * kThreads * kV;
@@ -634,9 +658,361 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
   }
   if ((a.n & 1) && blockIdx.x == 0 && tid == 0) count(xform(uint64_t(static_cast<const long long*>(a.col)[a.n - 1]), a.desc));
   __syncthreads();
-  for (int i = tid; i < 6 * kBins; i += kThreads) {
+  for (int i = tid; i < kPasses * kBins; i += kThreads) {
     const uint32_t c = h[i];
     if (c && ((digits >> (i / kBins)) & 1u)) atomicAdd(&a.ghist[i], c);
+  }
+}
+
+// ---------------------------------------------------------------- scatter hybrid
+// Wide raw int64 keys, n >= kScatterMinRows. The local phase ranks every row
+// by (key, row id) inside its sub-bucket (top 16 key bits), so the rows only
+// have to reach their sub-bucket, in any order — two non-stable counting
+// passes with exact precomputed offsets instead of two stable onesweep passes
+// (no look-back, no stable multisplit):
+//   sub_hist_kernel     chunk c (one CTA per SM) counts its rows per
+//                       sub-bucket in shared memory (packed u16 pairs, 128 KB):
+//                       chunk_cnt[c], d7_cnt[c]; ORs the varying key bits
+//   top_scatter_kernel  chunk c: digit-7 bases + its offset in every digit-7
+//                       bucket; tiles of 8192 rows ranked by shared atomics,
+//                       staged in digit order and written as contiguous runs
+//                       (keys_b / vals_b); CTA 0 lists the pass-B work items
+//                       (digit-7 buckets, big ones cut at chunk boundaries);
+//                       then per-sub-bucket totals of a slice of chunk_cnt
+//   sub_scatter_kernel  work item (bucket g, chunks [c0, c1)): its rows are
+//                       contiguous in keys_b; cursors = sub-bucket start + rows
+//                       of chunks < c0 (from chunk_cnt); the same staged
+//                       scatter by digit 6 into keys_a / vals_a; writes sub_off
+//                       and flags a sub-bucket above kLocalCap
+// Work items walk the buckets in order, so the sub-buckets being written at
+// any time span a few MB and every sector is completed in L2. The
+// cooperative kernel then runs only the local phase — or, on the fallback
+// flag (> kLocalCap rows in a sub-bucket, a wrapped chunk counter, < 4
+// varying digits), the LSD passes from the original input.
+
+// The fallback flag, read ONCE per CTA: other CTAs of the same kernel may
+// set it meanwhile, and a per-thread read could split the CTA at a barrier.
+__device__ __forceinline__ bool fallback_flag(const SortArgs& a) {
+  return __syncthreads_or(threadIdx.x == 0 && *reinterpret_cast<volatile const uint32_t*>(a.flags) != 0) != 0;
+}
+
+__device__ __forceinline__ int64_t chunk_lo(int64_t n, int chunks, int c) {
+  const int64_t per = (((n + chunks - 1) / chunks) + 1) & ~int64_t(1);  // even: 16-byte pair loads
+  return per * c < n ? per * c : n;
+}
+
+// Exclusive scan of one value per thread over threads 0..255 (every thread
+// of the CTA calls it; the result is meaningful for tid < 256).
+__device__ __forceinline__ uint32_t scan256(uint32_t c, uint32_t* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t incl = c;
+  if (tid < 256) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) scratch[warp] = incl;
+  }
+  __syncthreads();
+  uint32_t pre = 0;
+  if (tid < 256)
+    for (int w = 0; w < warp; ++w) pre += scratch[w];
+  __syncthreads();
+  return pre + incl - c;
+}
+
+struct STile {  // shared memory of the counting passes
+  uint64_t* sk;       // [kSTile] staged keys
+  uint32_t* sv;       // [kSTile] staged row ids
+  uint32_t* hist;     // [256] tile digit counts -> tile digit starts
+  uint32_t* base;     // [256] output position of staged row 0 of each digit
+  uint32_t* gcur;     // [256] next output position per digit (this CTA's cursors)
+  uint32_t* scratch;  // [64]
+};
+
+__device__ __forceinline__ STile stile(uint8_t* sm) {
+  STile t;
+  t.sk = reinterpret_cast<uint64_t*>(sm);
+  t.sv = reinterpret_cast<uint32_t*>(sm + size_t(kSTile) * 8);
+  t.hist = reinterpret_cast<uint32_t*>(sm + kSStage);
+  t.base = t.hist + 256;
+  t.gcur = t.base + 256;
+  t.scratch = t.gcur + 512;
+  return t;
+}
+
+// One tile of a non-stable counting scatter by the 8-bit digit at SHIFT:
+// rank by shared atomics, stage in digit order, write every digit's rows as
+// one contiguous run at the CTA's cursor for that digit.
+template <int SHIFT>
+__device__ __forceinline__ void stile_scatter(const uint64_t (&k)[kSItems], const uint32_t (&v)[kSItems], int tn,
+                                              const STile& s, uint64_t* out_k, uint32_t* out_v) {
+  const int tid = threadIdx.x;
+  if (tid < 256) s.hist[tid] = 0;
+  __syncthreads();
+  uint32_t r[kSItems];
+#pragma unroll
+  for (int u = 0; u < kSItems; ++u)
+    if (u * kScatThreads + tid < tn) r[u] = atomicAdd(&s.hist[uint32_t(k[u] >> SHIFT) & 255u], 1u);
+  __syncthreads();
+  const uint32_t c = tid < 256 ? s.hist[tid] : 0u;
+  const uint32_t excl = scan256(c, s.scratch);
+  if (tid < 256) {
+    s.hist[tid] = excl;
+    s.base[tid] = s.gcur[tid] - excl;
+    s.gcur[tid] += c;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kSItems; ++u) {
+    if (u * kScatThreads + tid < tn) {
+      const uint32_t p = s.hist[uint32_t(k[u] >> SHIFT) & 255u] + r[u];
+      s.sk[p] = k[u];
+      s.sv[p] = v[u];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < tn; i += kScatThreads) {
+    const uint64_t key = s.sk[i];
+    const uint32_t o = s.base[uint32_t(key >> SHIFT) & 255u] + uint32_t(i);
+    out_k[o] = key;
+    out_v[o] = s.sv[i];
+  }
+  __syncthreads();  // staging reused by the next tile
+}
+
+__global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
+  extern __shared__ __align__(16) uint32_t w[];  // [kScatWords]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
+  for (int i = tid; i < kScatWords / 4; i += kScatThreads) reinterpret_cast<uint4*>(w)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const int64_t lo = chunk_lo(a.n, a.chunks, blockIdx.x), hi = chunk_lo(a.n, a.chunks, blockIdx.x + 1);
+  const long long* col = static_cast<const long long*>(a.col);
+  const uint64_t k0 = xform(uint64_t(__ldg(col)), a.desc);
+  uint64_t vary = 0;
+  uint32_t ovf = 0;
+  auto count = [&](uint64_t u) {
+    vary |= u ^ k0;
+    const uint32_t b = uint32_t(u >> 48), sh = (b & 1u) << 4;
+    const uint32_t old = atomicAdd(&w[b >> 1], 1u << sh);
+    ovf |= ((old >> sh) & 0xFFFFu) == 0xFFFFu;  // wrapped: that sub-bucket is far above kLocalCap anyway
+  };
+  const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(col);
+  constexpr int kV = 4;
+  const int64_t p1 = hi >> 1;
+  for (int64_t base = (lo >> 1) + tid; base < p1; base += int64_t(kScatThreads) * kV) {
+    ulonglong2 q[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t i = base + int64_t(u) * kScatThreads;
+      q[u] = i < p1 ? __ldg(v2 + i) : make_ulonglong2(0, 0);  // cached: the digit-7 pass reads them again
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      if (base + int64_t(u) * kScatThreads < p1) {
+        count(xform(q[u].x, a.desc));
+        count(xform(q[u].y, a.desc));
+      }
+    }
+  }
+  if ((hi & 1) && hi > lo && tid == 0) count(xform(uint64_t(col[hi - 1]), a.desc));
+  const uint32_t vhi = __reduce_or_sync(0xffffffffu, uint32_t(vary >> 32));
+  const uint32_t vlo = __reduce_or_sync(0xffffffffu, uint32_t(vary));
+  const uint32_t anyo = __reduce_or_sync(0xffffffffu, ovf);
+  if (lane == 0) {
+    if (vhi | vlo) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(vhi) << 32) | vlo);
+    if (anyo) atomicOr(a.flags, 1u);  // LSD fallback
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(a.chunk_cnt + size_t(blockIdx.x) * kScatWords);
+  for (int i = tid; i < kScatWords / 4; i += kScatThreads) dst[i] = reinterpret_cast<const uint4*>(w)[i];
+  // rows per digit 7: a warp sums the 128 words of one bucket at a time
+  for (int g = warp; g < kBins; g += kScatThreads / 32) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t x = w[g * 128 + j * 32 + lane];
+      t += (x & 0xFFFFu) + (x >> 16);
+    }
+    t = __reduce_add_sync(0xffffffffu, t);
+    if (lane == 0) a.d7_cnt[blockIdx.x * kBins + g] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kScatThreads, 1) top_scatter_kernel(SortArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const STile s = stile(sm);
+  const int tid = threadIdx.x;
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[2] = globaltimer();
+  if (fallback_flag(a)) return;  // a chunk counter wrapped: LSD
+  const int chunks = a.chunks, c = blockIdx.x;
+  uint32_t* red = reinterpret_cast<uint32_t*>(s.sk);  // reduction scratch (staging is free here)
+  {  // digit-7 totals and this chunk's rows before it in every bucket
+    const int g = tid & 255, sl = tid >> 8;
+    uint32_t tot = 0, pre = 0;
+    for (int cc = sl; cc < chunks; cc += kScatThreads / 256) {
+      const uint32_t v = __ldcg(a.d7_cnt + cc * kBins + g);
+      tot += v;
+      pre += cc < c ? v : 0u;
+    }
+    red[tid] = tot;
+    red[kScatThreads + tid] = pre;
+    __syncthreads();
+    uint32_t t = 0, p = 0;
+    if (tid < 256)
+      for (int j = 0; j < kScatThreads / 256; ++j) {
+        t += red[j * 256 + tid];
+        p += red[kScatThreads + j * 256 + tid];
+      }
+    const uint32_t excl = scan256(t, s.scratch);
+    if (tid < 256) s.gcur[tid] = excl + p;
+    if (c == 0) {
+      // pass-B work items: a bucket per item, big buckets cut into runs of whole chunks
+      uint32_t k = 0;
+      if (tid < 256) {
+        a.d7_base[tid] = excl;
+        const uint64_t want = (uint64_t(t) + kSliceRows - 1) / kSliceRows;
+        k = uint32_t(want < 1 ? 1 : want > uint64_t(chunks) ? uint64_t(chunks) : want);
+      }
+      const uint32_t first = scan256(k, s.scratch);
+      if (tid < 256)
+        for (uint32_t j = 0; j < k; ++j)
+          a.items[first + j] = make_uint4(uint32_t(tid), j * chunks / k, (j + 1) * chunks / k, 0u);
+      // the spread pre-check: a bucket that cannot fit 256 sub-buckets of kLocalCap
+      const int too_big = __syncthreads_or(tid < 256 && uint64_t(t) > uint64_t(kBins) * kLocalCap);
+      if (tid == 255) {
+        a.d7_base[kBins] = uint32_t(a.n);
+        a.meta[0] = first + k;
+      }
+      if (tid == 0) {
+        const uint64_t vary = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4));
+        int na = 0;
+        for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
+        if (too_big || na < 4) atomicOr(a.flags, 1u);  // LSD is certain, or as cheap
+      }
+    }
+    __syncthreads();
+  }
+  // the chunk's rows by digit 7 -> keys_b / vals_b
+  const int64_t lo = chunk_lo(a.n, chunks, c), hi = chunk_lo(a.n, chunks, c + 1);
+  const long long* col = static_cast<const long long*>(a.col);
+  for (int64_t t0 = lo; t0 < hi; t0 += kSTile) {
+    const int tn = int(hi - t0 < kSTile ? hi - t0 : kSTile);
+    uint64_t k[kSItems];
+    uint32_t v[kSItems];
+#pragma unroll
+    for (int u = 0; u < kSItems; ++u) {
+      const int j = u * kScatThreads + tid;
+      k[u] = j < tn ? xform(uint64_t(__ldcs(col + t0 + j)), a.desc) : 0ull;
+      v[u] = uint32_t(t0 + j);
+    }
+    stile_scatter<7 * kBits>(k, v, tn, s, a.keys_b, a.vals_b);
+  }
+  // rows per sub-bucket over all chunks, for a slice of the sub-buckets
+  for (int wb = c * 256; wb < kScatWords; wb += chunks * 256) {
+    const int wi = wb + (tid & 255), sl = tid >> 8;
+    uint32_t l16 = 0, h16 = 0;
+    for (int cc = sl; cc < chunks; cc += kScatThreads / 256) {
+      const uint32_t v = __ldcg(a.chunk_cnt + size_t(cc) * kScatWords + wi);
+      l16 += v & 0xFFFFu;
+      h16 += v >> 16;
+    }
+    red[tid] = l16;
+    red[kScatThreads + tid] = h16;
+    __syncthreads();
+    if (tid < 256) {
+      uint32_t x = 0, y = 0;
+      for (int j = 0; j < kScatThreads / 256; ++j) {
+        x += red[j * 256 + tid];
+        y += red[kScatThreads + j * 256 + tid];
+      }
+      reinterpret_cast<uint2*>(a.sub_tot)[wi] = make_uint2(x, y);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kScatThreads, 1) sub_scatter_kernel(SortArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const STile s = stile(sm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[3] = globaltimer();
+  if (fallback_flag(a)) return;  // LSD fallback
+  const uint32_t n_items = __ldcg(a.meta);
+  const int chunks = a.chunks;
+  uint32_t* red = reinterpret_cast<uint32_t*>(s.sk);
+  while (true) {
+    if (tid == 0) s.scratch[40] = atomicAdd(a.flags + 3, 1u);
+    __syncthreads();
+    const uint32_t it = s.scratch[40];
+    if (it >= n_items) break;
+    const uint4 item = __ldcg(a.items + it);
+    const uint32_t g = item.x;
+    const int c0 = int(item.y), c1 = int(item.z);
+    // the item's rows in keys_b: chunks [c0, c1) of bucket g
+    {
+      const uint32_t v = tid < chunks ? __ldcg(a.d7_cnt + tid * kBins + g) : 0u;
+      const uint32_t x0 = __reduce_add_sync(0xffffffffu, tid < c0 ? v : 0u);
+      const uint32_t x1 = __reduce_add_sync(0xffffffffu, tid < c1 ? v : 0u);
+      if (lane == 0) {
+        red[2 * kScatThreads + warp] = x0;
+        red[2 * kScatThreads + 32 + warp] = x1;
+      }
+    }
+    // rows of chunks < c0 per sub-bucket of g (8 chunk slices x 128 words)
+    {
+      const int wi = tid & 127, sl = tid >> 7;
+      uint32_t l16 = 0, h16 = 0;
+      for (int cc = sl; cc < c0; cc += kScatThreads / 128) {
+        const uint32_t v = __ldcg(a.chunk_cnt + size_t(cc) * kScatWords + g * 128 + wi);
+        l16 += v & 0xFFFFu;
+        h16 += v >> 16;
+      }
+      red[tid] = l16;
+      red[kScatThreads + tid] = h16;
+    }
+    __syncthreads();
+    uint32_t tb = 0, rb = 0, start = 0, end = 0;
+    if (tid < 256) {
+      tb = __ldcg(a.sub_tot + g * 256 + tid);
+      const int wi = tid >> 1;
+      const uint32_t* r = red + (tid & 1) * kScatThreads;
+      for (int j = 0; j < kScatThreads / 128; ++j) rb += r[j * 128 + wi];
+      for (int j = 0; j < kScatThreads / 32; ++j) {
+        start += red[2 * kScatThreads + j];
+        end += red[2 * kScatThreads + 32 + j];
+      }
+    }
+    const uint32_t excl = scan256(tb, s.scratch);
+    const uint32_t gb = __ldcg(a.d7_base + g);
+    if (tid < 256) {
+      if (c0 == 0) {
+        a.sub_off[g * 256 + tid] = gb + excl;
+        if (tb > uint32_t(kLocalCap)) atomicOr(a.flags, 1u);
+      }
+      s.gcur[tid] = gb + excl + rb;
+    }
+    if (c0 == 0 && g == kBins - 1 && tid == 0) a.sub_off[kSubBuckets] = uint32_t(a.n);
+    if (tid == 0) {
+      s.scratch[41] = start;
+      s.scratch[42] = end;
+    }
+    __syncthreads();
+    const uint32_t r0 = gb + s.scratch[41], r1 = gb + s.scratch[42];
+    for (uint32_t t0 = r0; t0 < r1; t0 += kSTile) {
+      const int tn = int(r1 - t0 < uint32_t(kSTile) ? r1 - t0 : uint32_t(kSTile));
+      uint64_t k[kSItems];
+      uint32_t v[kSItems];
+#pragma unroll
+      for (int u = 0; u < kSItems; ++u) {
+        const int j = u * kScatThreads + tid;
+        k[u] = j < tn ? __ldcs(a.keys_b + t0 + j) : 0ull;
+        v[u] = j < tn ? __ldcs(a.vals_b + t0 + j) : 0u;
+      }
+      stile_scatter<6 * kBits>(k, v, tn, s, a.keys_a, a.vals_a);
+    }
   }
 }
 
@@ -966,6 +1342,15 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
 
   // ---- histograms come from hist_kernel (launched just before, on the same stream)
   if (stamper) a.stamps[1] = globaltimer();
+  // ---- scatter hybrid: the rows already sit in their sub-buckets (keys_a / vals_a)
+  if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) {
+    local_phase(a, smem, 1);
+    if (stamper) {
+      a.stamps[kStamps - 2] = globaltimer();
+      a.stamps[kStamps - 1] = 3;
+    }
+    return;
+  }
 
   // ---- plan (every CTA for itself): global digit bases + active digits.
   // Raw int64 keys: the histogram kernel counted digits 6 and 7 and ORed
@@ -1021,6 +1406,8 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       plan[2 * kPasses + 2] = plan[6] + plan[7];
       uint32_t low = 0;
       for (int p = 0; p < 6; ++p) low |= plan[p] << p;
+      // scatter fallback: no digit-6/7 histograms were built, count them too
+      if (a.mode == kModeScatter) low |= (plan[6] << 6) | (plan[7] << 7);
       plan[2 * kPasses + 3] = raw && !a.count_all ? low : 0u;  // digits the LSD path still has to count
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
@@ -1033,7 +1420,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
     if (!low) return;
     count_digits(a, smem, low);
     grid_sync(a.grid_bar, ++barrier_no);
-    scan_rows(0, 6);
+    scan_rows(0, (low >> 6) ? kPasses : 6);
   };
   if (!plan[kPasses + 1]) count_low_digits();
 
@@ -1097,8 +1484,15 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   }
   if (stamper) {
     a.stamps[kStamps - 2] = globaltimer();
-    a.stamps[kStamps - 1] = plan[kPasses + 1] ? 2 : 0;
+    a.stamps[kStamps - 1] = a.mode == kModeScatter ? 4 : plan[kPasses + 1] ? 2 : 0;
   }
+}
+
+// RL_SCATTER_MIN_ROWS overrides kScatterMinRows (tests: every hybrid shape through both paths)
+static int64_t scatter_min_rows() {
+  const char* v = getenv("RL_SCATTER_MIN_ROWS");
+  const long long r = v && v[0] ? atoll(v) : 0;
+  return r > 0 ? std::max<int64_t>(r, kHybridMinRows) : kScatterMinRows;
 }
 
 struct Layout {
@@ -1113,6 +1507,12 @@ struct Layout {
   uint64_t* keys_b;
   uint32_t* vals_a;
   uint32_t* vals_b;
+  uint32_t* chunk_cnt;  // scatter hybrid only (n >= scatter_min_rows())
+  uint32_t* d7_cnt;
+  uint32_t* d7_base;
+  uint32_t* sub_tot;
+  uint32_t* items;
+  uint32_t* meta;
 };
 
 template <typename C, typename T32, typename T64>
@@ -1129,7 +1529,14 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   auto kb = t64(c, size_t(n));
   auto va = t32(c, size_t(n));
   auto vb = t32(c, size_t(n));
-  if (L) *L = Layout{h, tc, gb, fl, st, zero, so, ka, kb, va, vb};
+  const bool scat = n >= scatter_min_rows();
+  auto cc = scat ? t32(c, size_t(kMaxChunks) * kScatWords) : nullptr;
+  auto dc = scat ? t32(c, size_t(kMaxChunks) * kBins) : nullptr;
+  auto db = scat ? t32(c, size_t(kBins + 4)) : nullptr;
+  auto stt = scat ? t32(c, size_t(kSubBuckets)) : nullptr;
+  auto it = scat ? t32(c, 4 * size_t(kBins + 2 + n / kSliceRows)) : nullptr;
+  auto me = scat ? t32(c, 4) : nullptr;
+  if (L) *L = Layout{h, tc, gb, fl, st, zero, so, ka, kb, va, vb, cc, dc, db, stt, it, me};
 }
 
 size_t workspace_bytes(int64_t n) {
@@ -1152,10 +1559,26 @@ __global__ void identity_kernel(const uint32_t* perm_in, int64_t n, uint32_t* ou
     out[i] = perm_in ? perm_in[i] : uint32_t(i);
 }
 
-// RL_NO_HYBRID=1 forces the LSD path (A/B measurements and tests).
-static bool getenv_flag_no_hybrid() {
-  const char* v = getenv("RL_NO_HYBRID");
+// RL_NO_HYBRID=1 forces the LSD path, RL_NO_SCATTER=1 the onesweep-pass hybrid
+// (A/B measurements and tests).
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
   return v && v[0] && v[0] != '0';
+}
+static bool getenv_flag_no_hybrid() { return getenv_flag("RL_NO_HYBRID"); }
+
+static bool scatter_kernels_ready() {
+  static int ready = -1;
+  if (ready < 0)
+    ready = cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(size_t(kScatWords) * 4)) == cudaSuccess &&
+                    cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSSmem)) == cudaSuccess &&
+                    cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSSmem)) == cudaSuccess
+                ? 1
+                : 0;
+  return ready == 1;
 }
 
 // Largest co-resident grid of the cooperative sort kernel on this device.
@@ -1196,6 +1619,42 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   const int64_t tiles = (a.n + kTile - 1) / kTile;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(limit, tiles)));
   a.mode = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() ? kModeHybrid : kModeLsd;
+  if (a.mode == kModeHybrid && L.chunk_cnt && !getenv_flag("RL_NO_SCATTER") && scatter_kernels_ready()) {
+    // scatter hybrid: chunk counts, digit-7 pass, digit-6 pass, then the local phase
+    a.mode = kModeScatter;
+    a.count_all = 0;
+    a.chunk_cnt = L.chunk_cnt;
+    a.d7_cnt = L.d7_cnt;
+    a.d7_base = L.d7_base;
+    a.sub_tot = L.sub_tot;
+    a.items = reinterpret_cast<uint4*>(L.items);
+    a.meta = L.meta;
+    int chunks = std::min(device_sm_count(), kMaxChunks);
+    if (max_ctas > 0) chunks = std::max(1, std::min(chunks, max_ctas / 2));  // one CTA per SM, like the sort's 2
+    a.chunks = chunks;
+    if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
+    const bool dbg = getenv_flag("RL_SCATTER_DEBUG");
+    auto chk = [&](const char* what) {
+      if (!dbg) return;
+      cudaError_t x = cudaStreamSynchronize(stream);
+      uint32_t fl[8] = {0};
+      cudaMemcpy(fl, L.flags, sizeof(fl), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[scatter-debug] %s: %s flags=%u,%u,%u,%u\n", what, cudaGetErrorString(x), fl[0], fl[1], fl[2], fl[3]);
+    };
+    sub_hist_kernel<<<chunks, kScatThreads, size_t(kScatWords) * 4, stream>>>(a);
+    chk("sub_hist");
+    top_scatter_kernel<<<chunks, kScatThreads, kSSmem, stream>>>(a);
+    chk("top_scatter");
+    sub_scatter_kernel<<<chunks, kScatThreads, kSSmem, stream>>>(a);
+    chk("sub_scatter");
+    if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
+    void* params[] = {&a};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
+                                    kSmemBytes, stream);
+    if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
+    count_launches(4);
+    return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
+  }
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
   // small raw inputs (never worth the hybrid's skipped histograms): every digit in the histogram kernel
   a.count_all = a.src_mode == kSrcInt64 && a.n < kCountAllRows ? 1 : 0;

@@ -53,6 +53,13 @@ def main():
             tot.append(evs[0].elapsed_time(evs[2]))
             st = stamps.cpu().tolist()
             hist.append((st[1] - st[0]) / 1e6)
+            if st[11] == 3:  # scatter hybrid: K1 st[0], K2 st[2], K3 st[3], local phase st[1]..st[10]
+                hist.append((st[2] - st[0]) / 1e6)
+                passes.append([(st[3] - st[2]) / 1e6, (st[1] - st[3]) / 1e6] + [0.0] * 6)
+                scan.append(0.0)
+                local.append((st[10] - st[1]) / 1e6)
+                full.append(evs[0].elapsed_time(e_end))
+                continue
             hybrid = st[11] == 1
             prev, pp = st[1], []
             for p in range(8):
@@ -71,7 +78,7 @@ def main():
     ok = bool((sk[1:] >= sk[:-1]).all()) and bool((keys[perm.long() & 0xFFFFFFFF] == sk).all())
     pm = np.median(np.array(passes), axis=0)
     act = pm[pm > 0.01]
-    print(f"lib={os.environ.get('RELAB_B200_LIB','default')} n={n} ok={ok} total_ms={statistics.median(tot):.4f} "
+    print(f"lib={os.environ.get('RELAB_B200_LIB','default')} path={int(st[11])} n={n} ok={ok} total_ms={statistics.median(tot):.4f} "
           f"with_fallback_ms={statistics.median(full):.4f} scan_us={1e3*statistics.median(scan) if scan else 0:.1f} local_us={1e3*statistics.median(local):.1f} "
           f"hist_us={1e3*statistics.median(hist):.1f} pass_us={[round(1e3*x,1) for x in pm]} "
           f"pass_GBps={24*n/(np.mean(act)/1e3)/1e9:.0f}")

@@ -1,10 +1,14 @@
-"""The wide-key hybrid sort (radix_sort.cu: two top-digit onesweep passes +
-on-chip local sort of the 65536 sub-buckets, LSD fallback on skew) against
-the reference's stable argsort (tensorpath.py:62-75, 206-216 via the oracle).
+"""The wide-key hybrid sort (radix_sort.cu: the rows reach their 65536
+sub-buckets — top 16 key bits — by two top-digit onesweep passes or by the
+scatter path's chunk counts + two non-stable counting passes; an on-chip local sort of
+every sub-bucket; LSD fallback on skew) against the reference's stable
+argsort (tensorpath.py:62-75, 206-216 via the oracle).
 
 Every case is checked for the permutation (stable tie order) and the sorted
 key values; the shapes are chosen to reach each branch of the local phase
-and both fallback points (pre-check and post-pass sub-bucket overflow)."""
+and every fallback point. Each test runs through both ways into the
+sub-buckets: RL_SCATTER_MIN_ROWS
+lowers the scatter threshold to the hybrid's, RL_NO_SCATTER forces the passes."""
 
 import numpy as np
 import pytest
@@ -17,6 +21,15 @@ pytestmark = pytest.mark.gpu
 
 LOCAL_CAP = 2560  # kLocalCap in radix_sort.cu
 I64_MIN, I64_MAX = -(2**63), 2**63 - 1
+
+
+@pytest.fixture(autouse=True, params=["scatter", "passes"])
+def into_subbuckets(request, monkeypatch):
+    if request.param == "passes":
+        monkeypatch.setenv("RL_NO_SCATTER", "1")
+    else:
+        monkeypatch.setenv("RL_SCATTER_MIN_ROWS", str(1 << 18))
+    return request.param
 
 
 def check_sort(keys: np.ndarray, desc: bool = False):
@@ -160,3 +173,39 @@ def test_fused_gather_in_local_phase(width, shape):
     want = O.stable_axis_order(keys, False)
     assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
     assert (out.cpu().numpy() == col[want]).all()
+
+
+def test_chunk_counter_wrap_fallback():
+    """> 65535 rows of one sub-bucket inside one scatter chunk (10M rows, the
+    first 1M in sub-bucket 0x8123): the chunk's 16-bit counter wraps, the LSD
+    fallback recounts digits 6 and 7 itself."""
+    rng = np.random.default_rng(13)
+    n = 10_000_000
+    keys = full_range(rng, n)
+    keys[:1_000_000] = (np.int64(0x0123) << 48) | rng.integers(0, 1 << 48, 1_000_000, dtype=np.int64)
+    check_sort(keys)
+
+
+def test_scatter_cfg2_size_with_ties():
+    """cfg2's size (10M) with cfg2's duplicate pattern, both directions."""
+    rng = np.random.default_rng(14)
+    n = 10_000_000
+    keys = full_range(rng, n)
+    dst = rng.choice(np.arange(1, n), n // 100, replace=False)
+    src = (rng.random(n // 100) * dst).astype(np.int64)
+    keys[dst] = keys[src]
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+@pytest.mark.parametrize("tops", [(0x10, 0x90), (0x7F,)])
+def test_split_digit7_buckets(tops):
+    """Digit 7 takes one or two values, digit 6 spreads: every digit-7 bucket
+    holds far more than one pass-B work item, so it is cut at chunk
+    boundaries and later slices start from the earlier chunks' counts."""
+    rng = np.random.default_rng(15 + len(tops))
+    n = 500_000 * len(tops)
+    hi = np.array(tops, dtype=np.int64)[rng.integers(0, len(tops), n)]
+    keys = (hi << np.int64(56)) | rng.integers(0, 1 << 56, n, dtype=np.int64)
+    check_sort(keys)
+    check_sort(keys, True)

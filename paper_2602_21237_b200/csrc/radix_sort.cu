@@ -104,18 +104,21 @@ enum SortMode : int { kModeLsd = 0, kModeHybrid = 1, kModeScatter = 2 };  // hyb
 
 // scatter hybrid: exact per-chunk 16-bit counts, then two non-stable
 // counting passes (digit 7; digit 6 inside every digit-7 bucket), then the local phase
-constexpr int kScatThreads = 1024;
+constexpr int kScatThreads = 1024;                 // histogram kernel: one CTA per SM
 constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
 constexpr int kMaxChunks = 160;
-constexpr int kSItems = 8;
-constexpr int kSTile = kScatThreads * kSItems;     // rows per staged tile
 constexpr int64_t kScatterMinRows = int64_t(1) << 22;
-#ifndef RL_SLICE_ROWS
-#define RL_SLICE_ROWS 32768
+#ifndef RL_PASS_THREADS
+#define RL_PASS_THREADS 512
 #endif
-constexpr int64_t kSliceRows = RL_SLICE_ROWS;      // digit-7 bucket rows per pass-B work item (whole chunks)
-constexpr size_t kSStage = size_t(kSTile) * 12;    // staged keys + row ids (also reduction scratch)
-constexpr size_t kSSmem = kSStage + 4 * 256 * 4 + 64 * 4;
+#ifndef RL_PASS_CTAS_PER_SM
+#define RL_PASS_CTAS_PER_SM 2
+#endif
+constexpr int kPThreads = RL_PASS_THREADS;         // counting passes
+constexpr int kPItems = 8;
+constexpr int kPTile = kPThreads * kPItems;        // rows per staged tile
+constexpr size_t kPStage = size_t(kPTile) * 12;    // staged keys + row ids (also reduction scratch)
+constexpr size_t kPSmem = kPStage + 3 * 256 * 4 + 64 * 4;
 enum SrcMode : int { kSrcInt64 = 0, kSrcInt64Gather = 1, kSrcBytes = 2, kSrcWords = 3 };
 
 __device__ __forceinline__ uint64_t xform(uint64_t x, int desc) {
@@ -181,11 +184,11 @@ struct SortArgs {
   FusedColumns gather;
   // scatter hybrid (kModeScatter)
   uint32_t* chunk_cnt;       // [kMaxChunks][kScatWords] rows per (chunk, sub-bucket), packed u16 pairs
-  uint32_t* d7_cnt;          // [kMaxChunks][kBins] rows per (chunk, digit 7)
+  uint32_t* cur7;            // [kBins] rows placed per digit-7 bucket so far (zeroed)
+  uint32_t* cur16;           // [kSubBuckets] rows placed per sub-bucket so far (zeroed)
   uint32_t* d7_base;         // [kBins + 1] digit-7 bucket starts
-  uint32_t* sub_tot;         // [kSubBuckets] rows per sub-bucket
-  uint4* items;              // pass-B work items (digit-7 bucket, first chunk, end chunk)
-  uint32_t* meta;            // [0] work items
+  uint4* items;              // pass-B tiles (digit-7 bucket, first row, end row)
+  uint32_t* meta;            // [0] pass-B tiles
   int chunks;                // input chunks = CTAs of the histogram and digit-7 kernels
 };
 
@@ -668,27 +671,27 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // Wide raw int64 keys, n >= kScatterMinRows. The local phase ranks every row
 // by (key, row id) inside its sub-bucket (top 16 key bits), so the rows only
 // have to reach their sub-bucket, in any order — two non-stable counting
-// passes with exact precomputed offsets instead of two stable onesweep passes
-// (no look-back, no stable multisplit):
+// passes with exact, precomputed bucket starts instead of two stable
+// onesweep passes (no look-back, no stable multisplit):
 //   sub_hist_kernel     chunk c (one CTA per SM) counts its rows per
-//                       sub-bucket in shared memory (packed u16 pairs, 128 KB):
-//                       chunk_cnt[c], d7_cnt[c]; ORs the varying key bits
-//   top_scatter_kernel  chunk c: digit-7 bases + its offset in every digit-7
-//                       bucket; tiles of 8192 rows ranked by shared atomics,
-//                       staged in digit order and written as contiguous runs
-//                       (keys_b / vals_b); CTA 0 lists the pass-B work items
-//                       (digit-7 buckets, big ones cut at chunk boundaries);
-//                       then per-sub-bucket totals of a slice of chunk_cnt
-//   sub_scatter_kernel  work item (bucket g, chunks [c0, c1)): its rows are
-//                       contiguous in keys_b; cursors = sub-bucket start + rows
-//                       of chunks < c0 (from chunk_cnt); the same staged
-//                       scatter by digit 6 into keys_a / vals_a; writes sub_off
-//                       and flags a sub-bucket above kLocalCap
-// Work items walk the buckets in order, so the sub-buckets being written at
-// any time span a few MB and every sector is completed in L2. The
-// cooperative kernel then runs only the local phase — or, on the fallback
-// flag (> kLocalCap rows in a sub-bucket, a wrapped chunk counter, < 4
-// varying digits), the LSD passes from the original input.
+//                       sub-bucket in shared memory (packed u16 pairs, 128 KB)
+//                       into chunk_cnt[c], adds its digit-7 histogram, ORs
+//                       the varying key bits
+//   top_scatter_kernel  every CTA: the digit-7 bucket starts; CTA g also the
+//                       starts of bucket g's 256 sub-buckets (totals over the
+//                       chunk counts; > kLocalCap -> LSD fallback) and their
+//                       digit-6 histogram contributions; CTA 0 the
+//                       pass-B tile list. Then tiles of 4096 rows: ranked by
+//                       shared atomics, staged in digit order, one global
+//                       atomic per (tile, digit) reserves the run, written as
+//                       contiguous runs (keys_b / vals_b)
+//   sub_scatter_kernel  tiles of one digit-7 bucket each, claimed in bucket
+//                       order: the same staged scatter by digit 6 into the
+//                       sub-buckets (keys_a / vals_a)
+// Bucket-ordered claiming keeps the sub-buckets being written within a few
+// MB, so every sector completes in L2. The cooperative kernel then runs only
+// the local phase — or, on the fallback flag (a sub-bucket above kLocalCap, a
+// wrapped chunk counter, < 4 varying digits), the LSD passes from the input.
 
 // The fallback flag, read ONCE per CTA: other CTAs of the same kernel may
 // set it meanwhile, and a per-thread read could split the CTA at a barrier.
@@ -722,68 +725,83 @@ __device__ __forceinline__ uint32_t scan256(uint32_t c, uint32_t* scratch) {
   return pre + incl - c;
 }
 
-struct STile {  // shared memory of the counting passes
-  uint64_t* sk;       // [kSTile] staged keys
-  uint32_t* sv;       // [kSTile] staged row ids
+struct PTile {  // shared memory of the counting passes
+  uint64_t* sk;       // [kPTile] staged keys
+  uint32_t* sv;       // [kPTile] staged row ids
   uint32_t* hist;     // [256] tile digit counts -> tile digit starts
   uint32_t* base;     // [256] output position of staged row 0 of each digit
-  uint32_t* gcur;     // [256] next output position per digit (this CTA's cursors)
+  uint32_t* aux;      // [256] pass A: digit-7 bucket starts
   uint32_t* scratch;  // [64]
 };
 
-__device__ __forceinline__ STile stile(uint8_t* sm) {
-  STile t;
+__device__ __forceinline__ PTile ptile(uint8_t* sm) {
+  PTile t;
   t.sk = reinterpret_cast<uint64_t*>(sm);
-  t.sv = reinterpret_cast<uint32_t*>(sm + size_t(kSTile) * 8);
-  t.hist = reinterpret_cast<uint32_t*>(sm + kSStage);
+  t.sv = reinterpret_cast<uint32_t*>(sm + size_t(kPTile) * 8);
+  t.hist = reinterpret_cast<uint32_t*>(sm + kPStage);
   t.base = t.hist + 256;
-  t.gcur = t.base + 256;
-  t.scratch = t.gcur + 512;
+  t.aux = t.base + 256;
+  t.scratch = t.aux + 256;
   return t;
 }
 
 // One tile of a non-stable counting scatter by the 8-bit digit at SHIFT:
-// rank by shared atomics, stage in digit order, write every digit's rows as
-// one contiguous run at the CTA's cursor for that digit.
-template <int SHIFT>
-__device__ __forceinline__ void stile_scatter(const uint64_t (&k)[kSItems], const uint32_t (&v)[kSItems], int tn,
-                                              const STile& s, uint64_t* out_k, uint32_t* out_v) {
-  const int tid = threadIdx.x;
-  if (tid < 256) s.hist[tid] = 0;
-  __syncthreads();
-  uint32_t r[kSItems];
+// rank by shared atomics, reserve every digit's run with one global atomic
+// (reserve(d, count) -> first output position; in flight during the scan and
+// the staging), stage in digit order, write every run contiguously. s.hist
+// is zero on entry and on exit. Once the tile is staged, next(k, v) loads the
+// following tile into the same registers, in flight during the write-out.
+template <int SHIFT, typename Reserve, typename Next>
+__device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int tn, const PTile& s,
+                                              uint64_t* out_k, uint32_t* out_v, Reserve reserve, Next next) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t r[kPItems];
 #pragma unroll
-  for (int u = 0; u < kSItems; ++u)
-    if (u * kScatThreads + tid < tn) r[u] = atomicAdd(&s.hist[uint32_t(k[u] >> SHIFT) & 255u], 1u);
+  for (int u = 0; u < kPItems; ++u)
+    if (u * kPThreads + tid < tn) r[u] = atomicAdd(&s.hist[uint32_t(k[u] >> SHIFT) & 255u], 1u);
   __syncthreads();
   const uint32_t c = tid < 256 ? s.hist[tid] : 0u;
-  const uint32_t excl = scan256(c, s.scratch);
+  const uint32_t res = tid < 256 && c ? reserve(uint32_t(tid), c) : 0u;
+  uint32_t incl = c;  // digit scan: warps 0..7, one barrier (the next scratch write is behind two more)
   if (tid < 256) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) s.scratch[warp] = incl;
+  }
+  __syncthreads();
+  uint32_t excl = incl - c;
+  if (tid < 256) {
+    for (int w = 0; w < warp; ++w) excl += s.scratch[w];
     s.hist[tid] = excl;
-    s.base[tid] = s.gcur[tid] - excl;
-    s.gcur[tid] += c;
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < kSItems; ++u) {
-    if (u * kScatThreads + tid < tn) {
+  for (int u = 0; u < kPItems; ++u) {
+    if (u * kPThreads + tid < tn) {
       const uint32_t p = s.hist[uint32_t(k[u] >> SHIFT) & 255u] + r[u];
       s.sk[p] = k[u];
       s.sv[p] = v[u];
     }
   }
+  if (tid < 256) s.base[tid] = res - excl;
   __syncthreads();
-  for (int i = tid; i < tn; i += kScatThreads) {
+  next(k, v);
+  if (tid < 256) s.hist[tid] = 0;  // for the next tile (the write-out reads only s.base)
+  for (int i = tid; i < tn; i += kPThreads) {
     const uint64_t key = s.sk[i];
     const uint32_t o = s.base[uint32_t(key >> SHIFT) & 255u] + uint32_t(i);
     out_k[o] = key;
     out_v[o] = s.sv[i];
   }
-  __syncthreads();  // staging reused by the next tile
+  __syncthreads();  // staging and s.base reused by the next tile
 }
 
 __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
-  extern __shared__ __align__(16) uint32_t w[];  // [kScatWords]
+  extern __shared__ __align__(16) uint32_t w[];  // [kScatWords] + [kScatThreads] reduction scratch
+  uint32_t* red = w + kScatWords;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
   for (int i = tid; i < kScatWords / 4; i += kScatThreads) reinterpret_cast<uint4*>(w)[i] = make_uint4(0, 0, 0, 0);
@@ -792,43 +810,49 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   const long long* col = static_cast<const long long*>(a.col);
   const uint64_t k0 = xform(uint64_t(__ldg(col)), a.desc);
   uint64_t vary = 0;
-  uint32_t ovf = 0;
-  auto count = [&](uint64_t u) {
+  auto count = [&](uint64_t u) {  // a wrapped 16-bit counter shows up in the chunk total below
     vary |= u ^ k0;
-    const uint32_t b = uint32_t(u >> 48), sh = (b & 1u) << 4;
-    const uint32_t old = atomicAdd(&w[b >> 1], 1u << sh);
-    ovf |= ((old >> sh) & 0xFFFFu) == 0xFFFFu;  // wrapped: that sub-bucket is far above kLocalCap anyway
+    const uint32_t b = uint32_t(u >> 48);
+    atomicAdd(&w[b >> 1], 1u << ((b & 1u) << 4));
   };
   const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(col);
   constexpr int kV = 4;
+  constexpr int64_t kStep = int64_t(kScatThreads) * kV;
   const int64_t p1 = hi >> 1;
-  for (int64_t base = (lo >> 1) + tid; base < p1; base += int64_t(kScatThreads) * kV) {
-    ulonglong2 q[kV];
+  ulonglong2 q[kV];  // the next batch is in flight while this one is counted
+  auto fetch = [&](int64_t base) {
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
       const int64_t i = base + int64_t(u) * kScatThreads;
       q[u] = i < p1 ? __ldg(v2 + i) : make_ulonglong2(0, 0);  // cached: the digit-7 pass reads them again
     }
+  };
+  fetch((lo >> 1) + tid);
+  for (int64_t base = (lo >> 1) + tid; base < p1; base += kStep) {
+    ulonglong2 cur[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) cur[u] = q[u];
+    if (base + kStep < p1) fetch(base + kStep);
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
       if (base + int64_t(u) * kScatThreads < p1) {
-        count(xform(q[u].x, a.desc));
-        count(xform(q[u].y, a.desc));
+        count(xform(cur[u].x, a.desc));
+        count(xform(cur[u].y, a.desc));
       }
     }
   }
   if ((hi & 1) && hi > lo && tid == 0) count(xform(uint64_t(col[hi - 1]), a.desc));
   const uint32_t vhi = __reduce_or_sync(0xffffffffu, uint32_t(vary >> 32));
   const uint32_t vlo = __reduce_or_sync(0xffffffffu, uint32_t(vary));
-  const uint32_t anyo = __reduce_or_sync(0xffffffffu, ovf);
-  if (lane == 0) {
-    if (vhi | vlo) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(vhi) << 32) | vlo);
-    if (anyo) atomicOr(a.flags, 1u);  // LSD fallback
-  }
+  if (lane == 0 && (vhi | vlo))
+    atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(vhi) << 32) | vlo);
   __syncthreads();
   uint4* dst = reinterpret_cast<uint4*>(a.chunk_cnt + size_t(blockIdx.x) * kScatWords);
   for (int i = tid; i < kScatWords / 4; i += kScatThreads) dst[i] = reinterpret_cast<const uint4*>(w)[i];
-  // rows per digit 7: a warp sums the 128 words of one bucket at a time
+  // digit 7: a warp sums the 128 words of one bucket at a time; the chunk
+  // total exposes a 16-bit counter that wrapped (> 65535 rows of one
+  // sub-bucket in this chunk: far above kLocalCap, so the LSD runs)
+  uint32_t mine = 0;
   for (int g = warp; g < kBins; g += kScatThreads / 32) {
     uint32_t t = 0;
 #pragma unroll
@@ -837,182 +861,154 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
       t += (x & 0xFFFFu) + (x >> 16);
     }
     t = __reduce_add_sync(0xffffffffu, t);
-    if (lane == 0) a.d7_cnt[blockIdx.x * kBins + g] = t;
+    mine += t;
+    if (lane == 0 && t) atomicAdd(&a.ghist[7 * kBins + g], t);
+  }
+  if (lane == 0) red[warp] = mine;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t tot = 0;
+    for (int i = 0; i < kScatThreads / 32; ++i) tot += red[i];
+    if (tot != uint32_t(hi - lo)) {
+      atomicOr(a.flags, 1u);      // LSD fallback,
+      atomicOr(a.flags + 2, 1u);  // which recounts digits 6 and 7
+    }
   }
 }
 
-__global__ void __launch_bounds__(kScatThreads, 1) top_scatter_kernel(SortArgs a) {
+__global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_kernel(SortArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const STile s = stile(sm);
+  const PTile s = ptile(sm);
   const int tid = threadIdx.x;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[2] = globaltimer();
   if (fallback_flag(a)) return;  // a chunk counter wrapped: LSD
-  const int chunks = a.chunks, c = blockIdx.x;
-  uint32_t* red = reinterpret_cast<uint32_t*>(s.sk);  // reduction scratch (staging is free here)
-  {  // digit-7 totals and this chunk's rows before it in every bucket
-    const int g = tid & 255, sl = tid >> 8;
-    uint32_t tot = 0, pre = 0;
-    for (int cc = sl; cc < chunks; cc += kScatThreads / 256) {
-      const uint32_t v = __ldcg(a.d7_cnt + cc * kBins + g);
-      tot += v;
-      pre += cc < c ? v : 0u;
-    }
-    red[tid] = tot;
-    red[kScatThreads + tid] = pre;
-    __syncthreads();
-    uint32_t t = 0, p = 0;
-    if (tid < 256)
-      for (int j = 0; j < kScatThreads / 256; ++j) {
-        t += red[j * 256 + tid];
-        p += red[kScatThreads + j * 256 + tid];
-      }
-    const uint32_t excl = scan256(t, s.scratch);
-    if (tid < 256) s.gcur[tid] = excl + p;
-    if (c == 0) {
-      // pass-B work items: a bucket per item, big buckets cut into runs of whole chunks
-      uint32_t k = 0;
-      if (tid < 256) {
-        a.d7_base[tid] = excl;
-        const uint64_t want = (uint64_t(t) + kSliceRows - 1) / kSliceRows;
-        k = uint32_t(want < 1 ? 1 : want > uint64_t(chunks) ? uint64_t(chunks) : want);
-      }
-      const uint32_t first = scan256(k, s.scratch);
-      if (tid < 256)
-        for (uint32_t j = 0; j < k; ++j)
-          a.items[first + j] = make_uint4(uint32_t(tid), j * chunks / k, (j + 1) * chunks / k, 0u);
-      // the spread pre-check: a bucket that cannot fit 256 sub-buckets of kLocalCap
-      const int too_big = __syncthreads_or(tid < 256 && uint64_t(t) > uint64_t(kBins) * kLocalCap);
-      if (tid == 255) {
-        a.d7_base[kBins] = uint32_t(a.n);
-        a.meta[0] = first + k;
-      }
-      if (tid == 0) {
-        const uint64_t vary = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4));
-        int na = 0;
-        for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
-        if (too_big || na < 4) atomicOr(a.flags, 1u);  // LSD is certain, or as cheap
+  // digit-7 bucket starts (every CTA)
+  const uint32_t t7 = tid < 256 ? __ldcg(a.ghist + 7 * kBins + tid) : 0u;
+  const uint32_t b7 = scan256(t7, s.scratch);
+  if (tid < 256) s.aux[tid] = b7;
+  if (blockIdx.x == 0) {
+    // pass-B tiles: a bucket's rows cut into tiles of kPTile
+    const uint32_t k = tid < 256 ? (t7 + kPTile - 1) / kPTile : 0u;
+    const uint32_t first = scan256(k, s.scratch);
+    if (tid < 256) {
+      a.d7_base[tid] = b7;
+      for (uint32_t j = 0; j < k; ++j) {
+        const uint32_t r0 = b7 + j * kPTile, r1 = min(b7 + t7, r0 + kPTile);
+        a.items[first + j] = make_uint4(uint32_t(tid), r0, r1, 0u);
       }
     }
-    __syncthreads();
+    // a bucket that cannot fit 256 sub-buckets of kLocalCap, or < 4 varying digits: LSD
+    const int too_big = __syncthreads_or(tid < 256 && uint64_t(t7) > uint64_t(kBins) * kLocalCap);
+    if (tid == 255) {
+      a.d7_base[kBins] = uint32_t(a.n);
+      a.meta[0] = first + k;
+    }
+    if (tid == 0) {
+      const uint64_t vary = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4));
+      int na = 0;
+      for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
+      if (too_big || na < 4) atomicOr(a.flags, 1u);
+    }
   }
-  // the chunk's rows by digit 7 -> keys_b / vals_b
-  const int64_t lo = chunk_lo(a.n, chunks, c), hi = chunk_lo(a.n, chunks, c + 1);
+  // sub-bucket starts of bucket g = this CTA (totals over the chunk counts)
+  uint32_t* red = reinterpret_cast<uint32_t*>(s.sk);  // staging is free here
+  for (uint32_t g = blockIdx.x; g < uint32_t(kBins); g += gridDim.x) {
+    constexpr int kSl = kPThreads / 128;
+    const int wi = tid & 127, sl = tid >> 7;
+    uint32_t l16 = 0, h16 = 0;
+    for (int cc = sl; cc < a.chunks; cc += kSl) {
+      const uint32_t x = __ldcg(a.chunk_cnt + size_t(cc) * kScatWords + g * 128 + wi);
+      l16 += x & 0xFFFFu;
+      h16 += x >> 16;
+    }
+    red[tid] = l16;
+    red[kPThreads + tid] = h16;
+    __syncthreads();
+    uint32_t tb = 0;
+    if (tid < 256)
+      for (int j = 0; j < kSl; ++j) tb += red[(tid & 1) * kPThreads + j * 128 + (tid >> 1)];
+    const uint32_t ex = scan256(tb, s.scratch);
+    if (tid < 256) {
+      a.sub_off[g * 256 + tid] = s.aux[g] + ex;
+      if (tb > uint32_t(kLocalCap)) atomicOr(a.flags, 1u);
+      if (tb) atomicAdd(&a.ghist[6 * kBins + tid], tb);  // for an LSD fallback
+    }
+    if (g == kBins - 1 && tid == 0) a.sub_off[kSubBuckets] = uint32_t(a.n);
+  }
+  // a fallback already found (here or by an earlier CTA's prologue): skip the scatter
+  if (fallback_flag(a)) return;
+  // this CTA's rows by digit 7 -> keys_b / vals_b
+  const int64_t lo = chunk_lo(a.n, gridDim.x, blockIdx.x), hi = chunk_lo(a.n, gridDim.x, blockIdx.x + 1);
   const long long* col = static_cast<const long long*>(a.col);
-  for (int64_t t0 = lo; t0 < hi; t0 += kSTile) {
-    const int tn = int(hi - t0 < kSTile ? hi - t0 : kSTile);
-    uint64_t k[kSItems];
-    uint32_t v[kSItems];
+  auto reserve = [&](uint32_t d, uint32_t c) { return s.aux[d] + atomicAdd(a.cur7 + d, c); };
+  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int64_t t0) {
+    const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
 #pragma unroll
-    for (int u = 0; u < kSItems; ++u) {
-      const int j = u * kScatThreads + tid;
+    for (int u = 0; u < kPItems; ++u) {
+      const int j = u * kPThreads + tid;
       k[u] = j < tn ? xform(uint64_t(__ldcs(col + t0 + j)), a.desc) : 0ull;
       v[u] = uint32_t(t0 + j);
     }
-    stile_scatter<7 * kBits>(k, v, tn, s, a.keys_b, a.vals_b);
-  }
-  // rows per sub-bucket over all chunks, for a slice of the sub-buckets
-  for (int wb = c * 256; wb < kScatWords; wb += chunks * 256) {
-    const int wi = wb + (tid & 255), sl = tid >> 8;
-    uint32_t l16 = 0, h16 = 0;
-    for (int cc = sl; cc < chunks; cc += kScatThreads / 256) {
-      const uint32_t v = __ldcg(a.chunk_cnt + size_t(cc) * kScatWords + wi);
-      l16 += v & 0xFFFFu;
-      h16 += v >> 16;
-    }
-    red[tid] = l16;
-    red[kScatThreads + tid] = h16;
-    __syncthreads();
-    if (tid < 256) {
-      uint32_t x = 0, y = 0;
-      for (int j = 0; j < kScatThreads / 256; ++j) {
-        x += red[j * 256 + tid];
-        y += red[kScatThreads + j * 256 + tid];
-      }
-      reinterpret_cast<uint2*>(a.sub_tot)[wi] = make_uint2(x, y);
-    }
-    __syncthreads();
+  };
+  uint64_t k[kPItems];
+  uint32_t v[kPItems];
+  if (lo < hi) load(k, v, lo);
+  if (tid < 256) s.hist[tid] = 0;
+  __syncthreads();
+  for (int64_t t0 = lo; t0 < hi; t0 += kPTile) {
+    const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
+    const int64_t nt = t0 + kPTile;
+    ptile_scatter<7 * kBits>(k, v, tn, s, a.keys_b, a.vals_b, reserve,
+                             [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
+                               if (nt < hi) load(kk, vv, nt);
+                             });
   }
 }
 
-__global__ void __launch_bounds__(kScatThreads, 1) sub_scatter_kernel(SortArgs a) {
+__global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_kernel(SortArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const STile s = stile(sm);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const PTile s = ptile(sm);
+  const int tid = threadIdx.x;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[3] = globaltimer();
   if (fallback_flag(a)) return;  // LSD fallback
   const uint32_t n_items = __ldcg(a.meta);
-  const int chunks = a.chunks;
-  uint32_t* red = reinterpret_cast<uint32_t*>(s.sk);
-  while (true) {
-    if (tid == 0) s.scratch[40] = atomicAdd(a.flags + 3, 1u);
-    __syncthreads();
-    const uint32_t it = s.scratch[40];
-    if (it >= n_items) break;
-    const uint4 item = __ldcg(a.items + it);
-    const uint32_t g = item.x;
-    const int c0 = int(item.y), c1 = int(item.z);
-    // the item's rows in keys_b: chunks [c0, c1) of bucket g
-    {
-      const uint32_t v = tid < chunks ? __ldcg(a.d7_cnt + tid * kBins + g) : 0u;
-      const uint32_t x0 = __reduce_add_sync(0xffffffffu, tid < c0 ? v : 0u);
-      const uint32_t x1 = __reduce_add_sync(0xffffffffu, tid < c1 ? v : 0u);
-      if (lane == 0) {
-        red[2 * kScatThreads + warp] = x0;
-        red[2 * kScatThreads + 32 + warp] = x1;
-      }
-    }
-    // rows of chunks < c0 per sub-bucket of g (8 chunk slices x 128 words)
-    {
-      const int wi = tid & 127, sl = tid >> 7;
-      uint32_t l16 = 0, h16 = 0;
-      for (int cc = sl; cc < c0; cc += kScatThreads / 128) {
-        const uint32_t v = __ldcg(a.chunk_cnt + size_t(cc) * kScatWords + g * 128 + wi);
-        l16 += v & 0xFFFFu;
-        h16 += v >> 16;
-      }
-      red[tid] = l16;
-      red[kScatThreads + tid] = h16;
-    }
-    __syncthreads();
-    uint32_t tb = 0, rb = 0, start = 0, end = 0;
-    if (tid < 256) {
-      tb = __ldcg(a.sub_tot + g * 256 + tid);
-      const int wi = tid >> 1;
-      const uint32_t* r = red + (tid & 1) * kScatThreads;
-      for (int j = 0; j < kScatThreads / 128; ++j) rb += r[j * 128 + wi];
-      for (int j = 0; j < kScatThreads / 32; ++j) {
-        start += red[2 * kScatThreads + j];
-        end += red[2 * kScatThreads + 32 + j];
-      }
-    }
-    const uint32_t excl = scan256(tb, s.scratch);
-    const uint32_t gb = __ldcg(a.d7_base + g);
-    if (tid < 256) {
-      if (c0 == 0) {
-        a.sub_off[g * 256 + tid] = gb + excl;
-        if (tb > uint32_t(kLocalCap)) atomicOr(a.flags, 1u);
-      }
-      s.gcur[tid] = gb + excl + rb;
-    }
-    if (c0 == 0 && g == kBins - 1 && tid == 0) a.sub_off[kSubBuckets] = uint32_t(a.n);
-    if (tid == 0) {
-      s.scratch[41] = start;
-      s.scratch[42] = end;
-    }
-    __syncthreads();
-    const uint32_t r0 = gb + s.scratch[41], r1 = gb + s.scratch[42];
-    for (uint32_t t0 = r0; t0 < r1; t0 += kSTile) {
-      const int tn = int(r1 - t0 < uint32_t(kSTile) ? r1 - t0 : uint32_t(kSTile));
-      uint64_t k[kSItems];
-      uint32_t v[kSItems];
+  uint32_t* claim = s.scratch + 40;  // [2] claimed tile ids, by parity
+  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], const uint4& item) {
+    const int tn = int(item.z - item.y);
 #pragma unroll
-      for (int u = 0; u < kSItems; ++u) {
-        const int j = u * kScatThreads + tid;
-        k[u] = j < tn ? __ldcs(a.keys_b + t0 + j) : 0ull;
-        v[u] = j < tn ? __ldcs(a.vals_b + t0 + j) : 0u;
-      }
-      stile_scatter<6 * kBits>(k, v, tn, s, a.keys_a, a.vals_a);
+    for (int u = 0; u < kPItems; ++u) {
+      const int j = u * kPThreads + tid;
+      k[u] = j < tn ? __ldcs(a.keys_b + item.y + j) : 0ull;
+      v[u] = j < tn ? __ldcs(a.vals_b + item.y + j) : 0u;
     }
+  };
+  if (tid == 0) claim[0] = atomicAdd(a.flags + 3, 1u);
+  if (tid < 256) s.hist[tid] = 0;
+  __syncthreads();
+  uint32_t it = claim[0], par = 1;
+  uint4 item = it < n_items ? __ldcg(a.items + it) : make_uint4(0, 0, 0, 0);
+  uint64_t k[kPItems];
+  uint32_t v[kPItems];
+  if (it < n_items) load(k, v, item);
+  while (it < n_items) {
+    if (tid == 0) claim[par] = atomicAdd(a.flags + 3, 1u);  // the next tile, read after the staging barrier
+    const uint32_t g = item.x;
+    uint32_t nit = 0;
+    uint4 nitem = make_uint4(0, 0, 0, 0);
+    auto reserve = [&](uint32_t d, uint32_t c) {
+      return __ldcg(a.sub_off + g * 256 + d) + atomicAdd(a.cur16 + g * 256 + d, c);
+    };
+    ptile_scatter<6 * kBits>(k, v, int(item.z - item.y), s, a.keys_a, a.vals_a, reserve,
+                             [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
+                               nit = claim[par];
+                               if (nit < n_items) {
+                                 nitem = __ldcg(a.items + nit);
+                                 load(kk, vv, nitem);
+                               }
+                             });
+    it = nit;
+    item = nitem;
+    par ^= 1;
   }
 }
 
@@ -1406,8 +1402,8 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       plan[2 * kPasses + 2] = plan[6] + plan[7];
       uint32_t low = 0;
       for (int p = 0; p < 6; ++p) low |= plan[p] << p;
-      // scatter fallback: no digit-6/7 histograms were built, count them too
-      if (a.mode == kModeScatter) low |= (plan[6] << 6) | (plan[7] << 7);
+      // scatter fallback after a wrapped chunk counter: digits 6 and 7 are recounted
+      if (a.mode == kModeScatter && __ldcg(a.flags + 2)) low |= (plan[6] << 6) | (plan[7] << 7);
       plan[2 * kPasses + 3] = raw && !a.count_all ? low : 0u;  // digits the LSD path still has to count
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
@@ -1418,6 +1414,11 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   auto count_low_digits = [&]() {
     const uint32_t low = plan[2 * kPasses + 3];
     if (!low) return;
+    if (low >> 6) {  // digit-6/7 rows start over
+      if (blockIdx.x == 0)
+        for (int i = tid; i < 2 * kBins; i += kThreads) a.ghist[6 * kBins + i] = 0;
+      grid_sync(a.grid_bar, ++barrier_no);
+    }
     count_digits(a, smem, low);
     grid_sync(a.grid_bar, ++barrier_no);
     scan_rows(0, (low >> 6) ? kPasses : 6);
@@ -1508,9 +1509,9 @@ struct Layout {
   uint32_t* vals_a;
   uint32_t* vals_b;
   uint32_t* chunk_cnt;  // scatter hybrid only (n >= scatter_min_rows())
-  uint32_t* d7_cnt;
+  uint32_t* cur7;
+  uint32_t* cur16;
   uint32_t* d7_base;
-  uint32_t* sub_tot;
   uint32_t* items;
   uint32_t* meta;
 };
@@ -1522,6 +1523,9 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   auto tc = t32(c, 2 * kPasses);
   auto gb = t32(c, 2);
   auto fl = t32(c, 8);
+  const bool scat = n >= scatter_min_rows();
+  auto c7 = scat ? t32(c, size_t(kBins)) : nullptr;          // zeroed with the prefix
+  auto c16 = scat ? t32(c, size_t(kSubBuckets)) : nullptr;
   auto st = t64(c, tiles * kBins);
   const size_t zero = c.used;
   auto so = t32(c, kSubBuckets + 1);
@@ -1529,14 +1533,11 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   auto kb = t64(c, size_t(n));
   auto va = t32(c, size_t(n));
   auto vb = t32(c, size_t(n));
-  const bool scat = n >= scatter_min_rows();
   auto cc = scat ? t32(c, size_t(kMaxChunks) * kScatWords) : nullptr;
-  auto dc = scat ? t32(c, size_t(kMaxChunks) * kBins) : nullptr;
   auto db = scat ? t32(c, size_t(kBins + 4)) : nullptr;
-  auto stt = scat ? t32(c, size_t(kSubBuckets)) : nullptr;
-  auto it = scat ? t32(c, 4 * size_t(kBins + 2 + n / kSliceRows)) : nullptr;
+  auto it = scat ? t32(c, 4 * size_t(kBins + 2 + n / kPTile)) : nullptr;
   auto me = scat ? t32(c, 4) : nullptr;
-  if (L) *L = Layout{h, tc, gb, fl, st, zero, so, ka, kb, va, vb, cc, dc, db, stt, it, me};
+  if (L) *L = Layout{h, tc, gb, fl, st, zero, so, ka, kb, va, vb, cc, c7, c16, db, it, me};
 }
 
 size_t workspace_bytes(int64_t n) {
@@ -1567,18 +1568,32 @@ static bool getenv_flag(const char* name) {
 }
 static bool getenv_flag_no_hybrid() { return getenv_flag("RL_NO_HYBRID"); }
 
+constexpr size_t kHistSmem = size_t(kScatWords) * 4 + size_t(kScatThreads) * 4;
+
 static bool scatter_kernels_ready() {
   static int ready = -1;
   if (ready < 0)
-    ready = cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(size_t(kScatWords) * 4)) == cudaSuccess &&
+    ready = cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHistSmem)) ==
+                        cudaSuccess &&
                     cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSSmem)) == cudaSuccess &&
+                                         int(kPSmem)) == cudaSuccess &&
                     cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSSmem)) == cudaSuccess
+                                         int(kPSmem)) == cudaSuccess
                 ? 1
                 : 0;
   return ready == 1;
+}
+
+// Co-resident CTAs per SM of the counting passes (both have the same shape).
+static int pass_ctas_per_sm() {
+  static int cached = 0;
+  if (cached > 0) return cached;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, top_scatter_kernel, kPThreads, kPSmem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  cached = per_sm;
+  return cached;
 }
 
 // Largest co-resident grid of the cooperative sort kernel on this device.
@@ -1619,18 +1634,24 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   const int64_t tiles = (a.n + kTile - 1) / kTile;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(limit, tiles)));
   a.mode = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() ? kModeHybrid : kModeLsd;
-  if (a.mode == kModeHybrid && L.chunk_cnt && !getenv_flag("RL_NO_SCATTER") && scatter_kernels_ready()) {
+  // (pigeonhole: above 65536 * kLocalCap rows some sub-bucket overflows for sure)
+  if (a.mode == kModeHybrid && L.chunk_cnt && a.n <= int64_t(kSubBuckets) * kLocalCap &&
+      !getenv_flag("RL_NO_SCATTER") && scatter_kernels_ready()) {
     // scatter hybrid: chunk counts, digit-7 pass, digit-6 pass, then the local phase
     a.mode = kModeScatter;
     a.count_all = 0;
     a.chunk_cnt = L.chunk_cnt;
-    a.d7_cnt = L.d7_cnt;
+    a.cur7 = L.cur7;
+    a.cur16 = L.cur16;
     a.d7_base = L.d7_base;
-    a.sub_tot = L.sub_tot;
     a.items = reinterpret_cast<uint4*>(L.items);
     a.meta = L.meta;
     int chunks = std::min(device_sm_count(), kMaxChunks);
-    if (max_ctas > 0) chunks = std::max(1, std::min(chunks, max_ctas / 2));  // one CTA per SM, like the sort's 2
+    int pgrid = device_sm_count() * pass_ctas_per_sm();
+    if (max_ctas > 0) {  // a concurrent sort shares the device: scale with the sort's cap (2 CTAs per SM)
+      chunks = std::max(1, std::min(chunks, max_ctas / 2));
+      pgrid = std::max(1, std::min(pgrid, max_ctas / 2 * pass_ctas_per_sm()));
+    }
     a.chunks = chunks;
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
     const bool dbg = getenv_flag("RL_SCATTER_DEBUG");
@@ -1641,11 +1662,11 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
       cudaMemcpy(fl, L.flags, sizeof(fl), cudaMemcpyDeviceToHost);
       fprintf(stderr, "[scatter-debug] %s: %s flags=%u,%u,%u,%u\n", what, cudaGetErrorString(x), fl[0], fl[1], fl[2], fl[3]);
     };
-    sub_hist_kernel<<<chunks, kScatThreads, size_t(kScatWords) * 4, stream>>>(a);
+    sub_hist_kernel<<<chunks, kScatThreads, kHistSmem, stream>>>(a);
     chk("sub_hist");
-    top_scatter_kernel<<<chunks, kScatThreads, kSSmem, stream>>>(a);
+    top_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
     chk("top_scatter");
-    sub_scatter_kernel<<<chunks, kScatThreads, kSSmem, stream>>>(a);
+    sub_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
     chk("sub_scatter");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
     void* params[] = {&a};

@@ -819,27 +819,34 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   constexpr int kV = 4;
   constexpr int64_t kStep = int64_t(kScatThreads) * kV;
   const int64_t p1 = hi >> 1;
-  ulonglong2 q[kV];  // the next batch is in flight while this one is counted
-  auto fetch = [&](int64_t base) {
+  // two batches alternate: one is counted while the other's loads are in flight
+  ulonglong2 qa[kV], qb[kV];
+  auto fetch = [&](ulonglong2 (&q)[kV], int64_t base) {
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
       const int64_t i = base + int64_t(u) * kScatThreads;
       q[u] = i < p1 ? __ldg(v2 + i) : make_ulonglong2(0, 0);  // cached: the digit-7 pass reads them again
     }
   };
-  fetch((lo >> 1) + tid);
-  for (int64_t base = (lo >> 1) + tid; base < p1; base += kStep) {
-    ulonglong2 cur[kV];
-#pragma unroll
-    for (int u = 0; u < kV; ++u) cur[u] = q[u];
-    if (base + kStep < p1) fetch(base + kStep);
+  auto consume = [&](const ulonglong2 (&q)[kV], int64_t base) {
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
       if (base + int64_t(u) * kScatThreads < p1) {
-        count(xform(cur[u].x, a.desc));
-        count(xform(cur[u].y, a.desc));
+        count(xform(q[u].x, a.desc));
+        count(xform(q[u].y, a.desc));
       }
     }
+  };
+  int64_t base = (lo >> 1) + tid;
+  fetch(qa, base);
+  while (base < p1) {
+    fetch(qb, base + kStep);
+    consume(qa, base);
+    base += kStep;
+    if (base >= p1) break;
+    fetch(qa, base + kStep);
+    consume(qb, base);
+    base += kStep;
   }
   if ((hi & 1) && hi > lo && tid == 0) count(xform(uint64_t(col[hi - 1]), a.desc));
   const uint32_t vhi = __reduce_or_sync(0xffffffffu, uint32_t(vary >> 32));
@@ -1080,7 +1087,9 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
   bulk_g2s(abuf + kLocAKeys, vin + v0, vbytes, bar);
 }
 
+template <int THREADS>
 __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
+  constexpr int kLWarps = THREADS / 32;
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
   uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kLocHist);
@@ -1095,7 +1104,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   const uint32_t* vin = src == 1 ? a.vals_a : a.vals_b;
   const int desc = a.key_mode == kRawDesc;
   constexpr uint32_t kGroups = kSubBuckets / kGroupSubs;
-  constexpr int kPerThread = kLocalBins / kThreads;
+  constexpr int kPerThread = kLocalBins / THREADS;
   const uint32_t g0 = blockIdx.x, gstep = gridDim.x;
   if (g0 >= kGroups) return;
 
@@ -1182,7 +1191,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     }
     // ---- this run: only the bins of its sub-buckets are zeroed and scanned
     const uint32_t bin_lo = (runs[buf * 4 + 2] & (kGroupSubs - 1)) * kBins, nsb = runs[buf * 4 + 3];
-    for (uint32_t i = tid; i < nsb * kBins; i += kThreads) hist[bin_lo + i] = 0;
+    for (uint32_t i = tid; i < nsb * kBins; i += THREADS) hist[bin_lo + i] = 0;
     if (tid == 0) {
       misc[0] = 0;
       misc[1] = 0;
@@ -1198,7 +1207,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     auto bin_of = [&](uint64_t key) {
       return int(((uint32_t(key >> 48) - top0) << kBits) | (uint32_t(key >> 40) & (kBins - 1)));
     };
-    for (uint32_t j = tid; j < cnt; j += kThreads) atomicAdd(&hist[bin_of(ak[j])], 1u);
+    for (uint32_t j = tid; j < cnt; j += THREADS) atomicAdd(&hist[bin_of(ak[j])], 1u);
     __syncthreads();
     if (nsb == uint32_t(kGroupSubs)) {  // a whole group: thread owns kPerThread consecutive bins (vector loads)
       uint32_t c[kPerThread], run = 0;
@@ -1208,30 +1217,32 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         run += c[i];
       }
       uint32_t total;
-      uint32_t start = block_exclusive_scan<kThreads>(run, misc + 8, &total);
+      uint32_t start = block_exclusive_scan<THREADS>(run, misc + 8, &total);
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
         hist[tid * kPerThread + i] = start;
         start += c[i];
       }
-    } else {  // part of a group: only its nsb * 256 bins, thread owns nsb consecutive bins
+    } else {  // part of a group: only its nsb * 256 bins, thread owns `per` consecutive bins
+      const uint32_t per = (nsb * kBins + THREADS - 1) / THREADS;  // <= kPerThread
+      const uint32_t nb = nsb * kBins;
       uint32_t c[kPerThread], run = 0;
-      uint32_t* hb = hist + bin_lo + tid * nsb;
+      uint32_t* hb = hist + bin_lo + tid * per;
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
-        c[i] = uint32_t(i) < nsb ? hb[i] : 0u;
+        c[i] = uint32_t(i) < per && tid * per + i < nb ? hb[i] : 0u;
         run += c[i];
       }
       uint32_t total;
-      uint32_t start = block_exclusive_scan<kThreads>(run, misc + 8, &total);
+      uint32_t start = block_exclusive_scan<THREADS>(run, misc + 8, &total);
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
-        if (uint32_t(i) < nsb) hb[i] = start;
+        if (uint32_t(i) < per && tid * per + i < nb) hb[i] = start;
         start += c[i];
       }
     }
     __syncthreads();
-    for (uint32_t j = tid; j < cnt; j += kThreads) {
+    for (uint32_t j = tid; j < cnt; j += THREADS) {
       const uint64_t key = ak[j];
       const uint32_t pos = atomicAdd(&hist[bin_of(key)], 1u);
       bk[pos] = key;
@@ -1249,7 +1260,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       __stcs(a.out_vals + o, v);
       gather_fused(a.gather, v, o);
     };
-    for (uint32_t p = tid; p < cnt; p += kThreads) {
+    for (uint32_t p = tid; p < cnt; p += THREADS) {
       const uint64_t key = bk[p];
       const uint32_t v = bv[p];
       const int b = bin_of(key);
@@ -1271,7 +1282,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     }
     __syncthreads();
     const uint32_t nbig = min(misc[0], uint32_t(kBigList));
-    for (uint32_t t = warp; t < nbig; t += kWarps) {
+    for (uint32_t t = warp; t < nbig; t += kLWarps) {
       const int b = int(big[t]);
       const uint32_t b0 = uint32_t(b) > bin_lo ? hist[b - 1] : 0u, b1 = hist[b];
       warp_bitonic(bk, bv, b0, b1, lane);
@@ -1327,6 +1338,22 @@ __device__ void run_passes(const SortArgs& a, uint8_t* smem, const uint32_t* bin
   }
 }
 
+// The scatter hybrid's local phase on its own launch (512 threads: twice the
+// warps of the cooperative kernel's 256-thread CTAs for this latency-bound
+// phase); the cooperative kernel behind it runs only on the fallback flag.
+constexpr int kLocalThreads = 512;
+__global__ void __launch_bounds__(kLocalThreads, 2) local_kernel(SortArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const bool stamper = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
+  if (stamper) a.stamps[1] = globaltimer();
+  if (*reinterpret_cast<volatile const uint32_t*>(a.flags)) return;  // final before this launch: uniform
+  local_phase<kLocalThreads>(a, smem, 1);
+  if (stamper) {
+    a.stamps[kStamps - 2] = globaltimer();
+    a.stamps[kStamps - 1] = 3;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(SortArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* bin_off = reinterpret_cast<uint32_t*>(smem + kPassSmemBytes);  // [kPasses][kBins], whole kernel
@@ -1339,14 +1366,9 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   // ---- histograms come from hist_kernel (launched just before, on the same stream)
   if (stamper) a.stamps[1] = globaltimer();
   // ---- scatter hybrid: the rows already sit in their sub-buckets (keys_a / vals_a)
-  if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) {
-    local_phase(a, smem, 1);
-    if (stamper) {
-      a.stamps[kStamps - 2] = globaltimer();
-      a.stamps[kStamps - 1] = 3;
-    }
-    return;
-  }
+  // ---- scatter hybrid: local_kernel sorted the sub-buckets already; this
+  // launch only runs the LSD fallback
+  if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) return;
 
   // ---- plan (every CTA for itself): global digit bases + active digits.
   // Raw int64 keys: the histogram kernel counted digits 6 and 7 and ORed
@@ -1456,7 +1478,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
         mbar_inval(&bars[1]);
       }
       __syncthreads();
-      local_phase(a, smem, src);
+      local_phase<kThreads>(a, smem, src);
       if (stamper) {
         a.stamps[kStamps - 2] = globaltimer();
         a.stamps[kStamps - 1] = 1;
@@ -1578,7 +1600,9 @@ static bool scatter_kernels_ready() {
                     cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(kPSmem)) == cudaSuccess &&
                     cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kPSmem)) == cudaSuccess
+                                         int(kPSmem)) == cudaSuccess &&
+                    cudaFuncSetAttribute(local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kLocalSmemBytes)) == cudaSuccess
                 ? 1
                 : 0;
   return ready == 1;
@@ -1653,6 +1677,8 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
       pgrid = std::max(1, std::min(pgrid, max_ctas / 2 * pass_ctas_per_sm()));
     }
     a.chunks = chunks;
+    int lgrid = device_sm_count() * 2;
+    if (max_ctas > 0) lgrid = std::max(1, std::min(lgrid, max_ctas));
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
     const bool dbg = getenv_flag("RL_SCATTER_DEBUG");
     auto chk = [&](const char* what) {
@@ -1668,12 +1694,14 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     chk("top_scatter");
     sub_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
     chk("sub_scatter");
+    local_kernel<<<lgrid, kLocalThreads, kLocalSmemBytes, stream>>>(a);
+    chk("local");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
     void* params[] = {&a};
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
                                     kSmemBytes, stream);
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
-    count_launches(4);
+    count_launches(5);
     return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
   }
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);

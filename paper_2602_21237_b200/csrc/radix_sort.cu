@@ -107,7 +107,8 @@ enum SortMode : int { kModeLsd = 0, kModeHybrid = 1, kModeScatter = 2 };  // hyb
 constexpr int kScatThreads = 1024;                 // histogram kernel: one CTA per SM
 constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
 constexpr int kMaxChunks = 160;
-constexpr int64_t kScatterMinRows = int64_t(1) << 22;
+constexpr int64_t kScatterMinRows = int64_t(1) << 19;
+constexpr int64_t kChunkMinRows = 32768;            // small inputs: fewer chunk histograms (128 KB each)
 #ifndef RL_PASS_THREADS
 #define RL_PASS_THREADS 512
 #endif
@@ -922,11 +923,20 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   for (uint32_t g = blockIdx.x; g < uint32_t(kBins); g += gridDim.x) {
     constexpr int kSl = kPThreads / 128;
     const int wi = tid & 127, sl = tid >> 7;
-    uint32_t l16 = 0, h16 = 0;
-    for (int cc = sl; cc < a.chunks; cc += kSl) {
-      const uint32_t x = __ldcg(a.chunk_cnt + size_t(cc) * kScatWords + g * 128 + wi);
-      l16 += x & 0xFFFFu;
-      h16 += x >> 16;
+    uint32_t l16 = 0, h16 = 0;  // 8 loads in flight per thread, not one L2 round trip per chunk
+    const uint32_t* col_g = a.chunk_cnt + g * 128 + wi;
+    for (int c0 = sl; c0 < a.chunks; c0 += 8 * kSl) {
+      uint32_t x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int cc = c0 + u * kSl;
+        x[u] = cc < a.chunks ? __ldcg(col_g + size_t(cc) * kScatWords) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        l16 += x[u] & 0xFFFFu;
+        h16 += x[u] >> 16;
+      }
     }
     red[tid] = l16;
     red[kPThreads + tid] = h16;
@@ -1670,7 +1680,9 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     a.d7_base = L.d7_base;
     a.items = reinterpret_cast<uint4*>(L.items);
     a.meta = L.meta;
-    int chunks = std::min(device_sm_count(), kMaxChunks);
+    int chunks = int(std::min<int64_t>(std::min(device_sm_count(), kMaxChunks),
+                                       std::max<int64_t>(32, (a.n + kChunkMinRows - 1) / kChunkMinRows)));
+    if (const char* e = getenv("RL_SCATTER_CHUNKS")) chunks = std::max(1, std::min(atoi(e), kMaxChunks));
     int pgrid = device_sm_count() * pass_ctas_per_sm();
     if (max_ctas > 0) {  // a concurrent sort shares the device: scale with the sort's cap (2 CTAs per SM)
       chunks = std::max(1, std::min(chunks, max_ctas / 2));

@@ -107,7 +107,7 @@ enum SortMode : int { kModeLsd = 0, kModeHybrid = 1, kModeScatter = 2 };  // hyb
 constexpr int kScatThreads = 1024;                 // histogram kernel: one CTA per SM
 constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
 constexpr int kMaxChunks = 160;
-constexpr int64_t kScatterMinRows = int64_t(1) << 19;
+constexpr int64_t kScatterMinRows = int64_t(1) << 22;  // below: the histogram kernel counts every digit at once
 constexpr int64_t kChunkMinRows = 32768;            // small inputs: fewer chunk histograms (128 KB each)
 #ifndef RL_PASS_THREADS
 #define RL_PASS_THREADS 512
@@ -892,6 +892,20 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   if (fallback_flag(a)) return;  // a chunk counter wrapped: LSD
   // digit-7 bucket starts (every CTA)
   const uint32_t t7 = tid < 256 ? __ldcg(a.ghist + 7 * kBins + tid) : 0u;
+  {  // certain fallbacks, decided by every CTA alike before any work: fewer than 4
+     // varying digits (LSD is as cheap), or a digit-7 bucket too big for 256 sub-buckets
+    const uint64_t vary = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4));
+    int na = 0;
+    for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
+    const bool too_big = __syncthreads_or(tid < 256 && uint64_t(t7) > uint64_t(kBins) * kLocalCap) != 0;
+    if (too_big || na < 4) {
+      if (blockIdx.x == 0 && tid == 0) {
+        atomicOr(a.flags, 1u);
+        atomicOr(a.flags + 2, 1u);  // no digit-6 histogram was built: the LSD counts digits 6 and 7 itself
+      }
+      return;
+    }
+  }
   const uint32_t b7 = scan256(t7, s.scratch);
   if (tid < 256) s.aux[tid] = b7;
   if (blockIdx.x == 0) {
@@ -905,17 +919,9 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
         a.items[first + j] = make_uint4(uint32_t(tid), r0, r1, 0u);
       }
     }
-    // a bucket that cannot fit 256 sub-buckets of kLocalCap, or < 4 varying digits: LSD
-    const int too_big = __syncthreads_or(tid < 256 && uint64_t(t7) > uint64_t(kBins) * kLocalCap);
     if (tid == 255) {
       a.d7_base[kBins] = uint32_t(a.n);
       a.meta[0] = first + k;
-    }
-    if (tid == 0) {
-      const uint64_t vary = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4));
-      int na = 0;
-      for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
-      if (too_big || na < 4) atomicOr(a.flags, 1u);
     }
   }
   // sub-bucket starts of bucket g = this CTA (totals over the chunk counts)
@@ -1373,12 +1379,11 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   uint32_t barrier_no = 0;
   const bool stamper = a.stamps && blockIdx.x == 0 && tid == 0;
 
-  // ---- histograms come from hist_kernel (launched just before, on the same stream)
-  if (stamper) a.stamps[1] = globaltimer();
-  // ---- scatter hybrid: the rows already sit in their sub-buckets (keys_a / vals_a)
   // ---- scatter hybrid: local_kernel sorted the sub-buckets already; this
   // launch only runs the LSD fallback
   if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) return;
+  // ---- histograms come from hist_kernel (launched just before, on the same stream)
+  if (stamper) a.stamps[1] = globaltimer();
 
   // ---- plan (every CTA for itself): global digit bases + active digits.
   // Raw int64 keys: the histogram kernel counted digits 6 and 7 and ORed
@@ -1434,7 +1439,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       plan[2 * kPasses + 2] = plan[6] + plan[7];
       uint32_t low = 0;
       for (int p = 0; p < 6; ++p) low |= plan[p] << p;
-      // scatter fallback after a wrapped chunk counter: digits 6 and 7 are recounted
+      // scatter fallback without complete digit-6/7 histograms: digits 6 and 7 are recounted
       if (a.mode == kModeScatter && __ldcg(a.flags + 2)) low |= (plan[6] << 6) | (plan[7] << 7);
       plan[2 * kPasses + 3] = raw && !a.count_all ? low : 0u;  // digits the LSD path still has to count
       mbar_init(&bars[0], 1);

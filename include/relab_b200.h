@@ -103,10 +103,14 @@ RL_API int64_t rl_launch_count(void);
  * passes whose 8-bit digit is constant over the input are skipped on the
  * device (no host sync, no launch). Wide INT64 keys without perm_in
  * (n >= 2^18, top 16 bits spread so every one of the 65536 sub-buckets fits
- * on chip) take the hybrid inside the same kernel: two passes on the top
- * two digits, then an on-chip sort of each sub-bucket by (key, row id)
- * written straight to the outputs; a sub-bucket over the on-chip cap
- * switches the same launch to the LSD passes. Results are identical. An INT64 `col` read without perm_in, and perm_in,
+ * on chip) take a hybrid: the rows reach their sub-bucket — by two onesweep
+ * passes on the top two digits inside the cooperative kernel (n < 2^22), or
+ * (n >= 2^22) by exact per-chunk sub-bucket counts and two non-stable
+ * counting passes (three launches ahead of it) — then an on-chip sort of
+ * each sub-bucket by (key, row id) is written straight to the outputs (the
+ * cooperative kernel, or its own 512-thread launch on the scatter path). A
+ * sub-bucket over the on-chip cap switches to the LSD passes on the device.
+ * Results are identical on every path. An INT64 `col` read without perm_in, and perm_in,
  * must be 16-byte aligned (they are streamed with TMA bulk copies);
  * RL_ERR_BAD_ARG otherwise.
  * --------------------------------------------------------------------- */
@@ -130,11 +134,15 @@ RL_API int rl_sort_axis_gather(const void* col, int32_t col_kind, int32_t width,
 /* Same as rl_sort_axis_gather, for measurement: events[0..2] (cudaEvent_t
  * created by the caller with timing enabled) are recorded on `stream`
  * before the histogram kernel, between it and the cooperative pass kernel,
- * and after the pass kernel; if stamps_dev (device, RL_SORT_STAMPS x
- * uint64) is not NULL, CTA 0 writes %globaltimer (ns) there: [0] histogram
- * start, [1] pass kernel start, [2+p] after digit pass p (0 for skipped
- * passes; in the hybrid [2] = sub-bucket check done), [10] end, and [11]
- * the path taken: 0 LSD, 1 hybrid, 2 hybrid that fell back to LSD. */
+ * and after the pass kernel (scatter path: before the chunk counts, before
+ * the local-phase kernel, after the cooperative kernel); if stamps_dev
+ * (device, RL_SORT_STAMPS x uint64) is not NULL, CTA 0 writes %globaltimer
+ * (ns) there: [0] histogram start, [1] pass kernel start, [2+p] after digit
+ * pass p (0 for skipped passes; in the hybrid [2] = sub-bucket check done;
+ * scatter path: [2] digit-7 pass start, [3] digit-6 pass start, [1] local
+ * phase start), [10] end, and [11] the path taken: 0 LSD, 1 hybrid, 2
+ * hybrid that fell back to LSD, 3 scatter hybrid, 4 scatter hybrid that
+ * fell back to LSD. */
 #define RL_SORT_EVENTS 3
 #define RL_SORT_STAMPS 12
 RL_API int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width,

@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
       const int64_t i = base + int64_t(u) * kScatThreads;
-      q[u] = i < p1 ? __ldg(v2 + i) : make_ulonglong2(0, 0);  // cached: the digit-7 pass reads them again
+      q[u] = i < p1 ? __ldg(v2 + i) : make_ulonglong2(0, 0);
     }
   };
   auto consume = [&](const ulonglong2 (&q)[kV], int64_t base) {
@@ -1384,6 +1384,11 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) return;
   // ---- histograms come from hist_kernel (launched just before, on the same stream)
   if (stamper) a.stamps[1] = globaltimer();
+  if (a.mode == kModeScatter) {  // LSD fallback: the look-back words were left out of the zeroed prefix
+    const size_t words = size_t((a.n + kTile - 1) / kTile) * kBins;
+    for (size_t i = size_t(blockIdx.x) * kThreads + tid; i < words; i += size_t(gridDim.x) * kThreads) a.status[i] = 0;
+    grid_sync(a.grid_bar, ++barrier_no);
+  }
 
   // ---- plan (every CTA for itself): global digit bases + active digits.
   // Raw int64 keys: the histogram kernel counted digits 6 and 7 and ORed
@@ -1540,6 +1545,7 @@ struct Layout {
   uint32_t* flags;
   uint64_t* status;
   size_t zero_bytes;  // prefix [hist .. status] zeroed per call
+  size_t head_bytes;  // prefix [hist .. cur16]: the scatter path zeroes only this (its LSD fallback clears status)
   uint32_t* sub_off;
   uint64_t* keys_a;
   uint64_t* keys_b;
@@ -1563,6 +1569,7 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   const bool scat = n >= scatter_min_rows();
   auto c7 = scat ? t32(c, size_t(kBins)) : nullptr;          // zeroed with the prefix
   auto c16 = scat ? t32(c, size_t(kSubBuckets)) : nullptr;
+  const size_t head = c.used;
   auto st = t64(c, tiles * kBins);
   const size_t zero = c.used;
   auto so = t32(c, kSubBuckets + 1);
@@ -1574,7 +1581,7 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   auto db = scat ? t32(c, size_t(kBins + 4)) : nullptr;
   auto it = scat ? t32(c, 4 * size_t(kBins + 2 + n / kPTile)) : nullptr;
   auto me = scat ? t32(c, 4) : nullptr;
-  if (L) *L = Layout{h, tc, gb, fl, st, zero, so, ka, kb, va, vb, cc, c7, c16, db, it, me};
+  if (L) *L = Layout{h, tc, gb, fl, st, zero, head, so, ka, kb, va, vb, cc, c7, c16, db, it, me};
 }
 
 size_t workspace_bytes(int64_t n) {
@@ -1667,15 +1674,17 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     cudaError_t e = cudaGetLastError();
     return rl_cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration);
   }
-  cudaError_t e = cudaMemsetAsync(L.hist, 0, L.zero_bytes, stream);
+  const bool scatter = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() && L.chunk_cnt &&
+                       a.n <= int64_t(kSubBuckets) * kLocalCap && !getenv_flag("RL_NO_SCATTER") &&
+                       scatter_kernels_ready();
+  cudaError_t e = cudaMemsetAsync(L.hist, 0, scatter ? L.head_bytes : L.zero_bytes, stream);
   if (e != cudaSuccess) return rl_cuda_status(e);
   // enough CTAs for the tiles, at most all co-resident
   const int64_t tiles = (a.n + kTile - 1) / kTile;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(limit, tiles)));
   a.mode = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() ? kModeHybrid : kModeLsd;
   // (pigeonhole: above 65536 * kLocalCap rows some sub-bucket overflows for sure)
-  if (a.mode == kModeHybrid && L.chunk_cnt && a.n <= int64_t(kSubBuckets) * kLocalCap &&
-      !getenv_flag("RL_NO_SCATTER") && scatter_kernels_ready()) {
+  if (scatter) {
     // scatter hybrid: chunk counts, digit-7 pass, digit-6 pass, then the local phase
     a.mode = kModeScatter;
     a.count_all = 0;

@@ -233,6 +233,9 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+NOMINAL_HBM_GBS = 8000.0  # B200 HBM3e nominal (the north star's ~8 TB/s), reported beside the measured peak
+
+
 def sort_roofline(n, active, st, sort_ms, hist_ms, step_ms_total):
     """Roofline of the sort. Wide-key scatter path (the cfg2 case): the four
     launches of one sort (chunk histograms, digit-7 pass, digit-6 pass, the
@@ -294,6 +297,7 @@ def sort_roofline(n, active, st, sort_ms, hist_ms, step_ms_total):
             phases["local_phase_us"] = round((st[10] - st[2]) / 1e3, 1)
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
+            "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
             "kernel": kernel, "path": path, "peak_source": peak_src, "launches_timed": len(timed_ms),
             "active_digits": sum(active), "avg_launch_us": round(1e3 * avg_ms, 2),
             "alg_bytes_per_launch": int(alg_bytes), "alg_bytes_formula": alg_formula,
@@ -864,6 +868,8 @@ def extras(args, dev):
                                                 "achieved": round(streamed * 8 / (ms / 1e3) / 1e9, 1),
                                                 "peak": measured_peak_hbm()[0],
                                                 "frac": round(streamed * 8 / (ms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
+                                                "peak_nominal": NOMINAL_HBM_GBS,
+                                                "frac_nominal": round(streamed * 8 / (ms / 1e3) / 1e9 / NOMINAL_HBM_GBS, 4),
                                                 "alg_bytes": "8 B written per materialised pair (uint32 left row, "
                                                              "uint32 right row); row-id reads hit L2"},
                             "note": "pairs materialised as uint32 (left row, right row) in 2^30-pair chunks"}

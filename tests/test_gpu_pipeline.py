@@ -83,3 +83,21 @@ def test_join_stream_vector_path_right_run_lengths():
             got_r.append(rr.cpu().numpy().view(np.uint32).astype(np.int64))
         wl, wr = O.join_pairs(lk, rk, a, b)
         assert (np.concatenate(got_l) == wl).all() and (np.concatenate(got_r) == wr).all()
+
+
+def test_wide_key_join_concurrent_scatter_sorts():
+    """5M x 5M join on full-range int64 keys drawn from a shared pool: the join
+    plan indexes both sides concurrently on half grids each, and at >= 4M wide
+    keys both sorts take the scatter hybrid (chunk counts, two counting passes,
+    local phase) side by side. Output byte-identical to the oracle."""
+    rng = np.random.default_rng(21)
+    pool = rng.integers(np.iinfo(np.int64).min, np.iinfo(np.int64).max, 3_000_000, dtype=np.int64, endpoint=True)
+    n = 5_000_000
+    pay = np.arange(n, dtype=np.int64)
+    r = synth.Relation(synth.KEY_PAYLOAD, (pool[rng.integers(0, len(pool), n)], pay))
+    s = synth.Relation(synth.KEY_PAYLOAD, (pool[rng.integers(0, len(pool), n)], pay))
+    out, _ = tensor_join(to_tensor(r, "key"), to_tensor(s, "key"))
+    want = O.join_columns(list(r.columns), 0, list(s.columns), 0)
+    assert out.row_count == len(want[0]) > 5_000_000
+    for a, b in zip(out.columns, want):
+        assert (a == b).all()

@@ -1208,14 +1208,15 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     // ---- this run: only the bins of its sub-buckets are zeroed and scanned
     const uint32_t bin_lo = (runs[buf * 4 + 2] & (kGroupSubs - 1)) * kBins, nsb = runs[buf * 4 + 3];
     for (uint32_t i = tid; i < nsb * kBins; i += THREADS) hist[bin_lo + i] = 0;
-    if (tid == 0) {
-      misc[0] = 0;
-      misc[1] = 0;
-    }
     mbar_wait(&bars[buf], buf ? phase1 : phase0);
     if (buf) phase1 ^= 1;
     else phase0 ^= 1;
     __syncthreads();  // hist zeroed, run descriptors and next-run fields visible
+    // the next-run fields go to registers now: warp 0 rewrites them at the top
+    // of the next run, with no barrier at the end of this one
+    const bool more = misc[4] != 0;
+    const uint32_t next_k = misc[5], next_r = misc[6];
+    if (tid == 0) misc[0] = 0;  // big-bin list: appended after later barriers, read after the rank loop
     const uint32_t base = runs[buf * 4], cnt = runs[buf * 4 + 1], top0 = runs[buf * 4 + 2] & ~uint32_t(kGroupSubs - 1);
     const uint8_t* abuf = smem + kLocA + buf * kLocABytes;
     const uint64_t* ak = reinterpret_cast<const uint64_t*>(abuf) + (base & 1u);
@@ -1304,12 +1305,11 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       warp_bitonic(bk, bv, b0, b1, lane);
       for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], bv[p]);
     }
-    if (nbig) __syncthreads();
-    if (!misc[4]) break;
-    k = misc[5];
-    r = misc[6];
+    if (nbig) __syncthreads();  // (the rank loop's reads of B/hist ended at the barrier before nbig)
+    if (!more) break;
+    k = next_k;
+    r = next_r;
     buf ^= 1;
-    __syncthreads();  // B/hist/misc reads done before the next run rewrites them
   }
   if (tid == 0) {
     mbar_inval(&bars[0]);

@@ -116,7 +116,10 @@ constexpr int64_t kChunkMinRows = 32768;            // small inputs: fewer chunk
 #define RL_PASS_CTAS_PER_SM 2
 #endif
 constexpr int kPThreads = RL_PASS_THREADS;         // counting passes
-constexpr int kPItems = 8;
+#ifndef RL_PASS_ITEMS
+#define RL_PASS_ITEMS 8
+#endif
+constexpr int kPItems = RL_PASS_ITEMS;
 constexpr int kPTile = kPThreads * kPItems;        // rows per staged tile
 constexpr size_t kPStage = size_t(kPTile) * 12;    // staged keys + row ids (also reduction scratch)
 constexpr size_t kPSmem = kPStage + 3 * 256 * 4 + 64 * 4;
@@ -1357,8 +1360,11 @@ __device__ void run_passes(const SortArgs& a, uint8_t* smem, const uint32_t* bin
 // The scatter hybrid's local phase on its own launch (512 threads: twice the
 // warps of the cooperative kernel's 256-thread CTAs for this latency-bound
 // phase); the cooperative kernel behind it runs only on the fallback flag.
-constexpr int kLocalThreads = 512;
-__global__ void __launch_bounds__(kLocalThreads, 2) local_kernel(SortArgs a) {
+#ifndef RL_LOCAL_THREADS
+#define RL_LOCAL_THREADS 512
+#endif
+constexpr int kLocalThreads = RL_LOCAL_THREADS;
+__global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_kernel(SortArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const bool stamper = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
   if (stamper) a.stamps[1] = globaltimer();
@@ -1703,7 +1709,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
       pgrid = std::max(1, std::min(pgrid, max_ctas / 2 * pass_ctas_per_sm()));
     }
     a.chunks = chunks;
-    int lgrid = device_sm_count() * 2;
+    int lgrid = device_sm_count() * (1024 / kLocalThreads);
     if (max_ctas > 0) lgrid = std::max(1, std::min(lgrid, max_ctas));
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
     const bool dbg = getenv_flag("RL_SCATTER_DEBUG");

@@ -124,7 +124,7 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = os.environ.get("RELAB_B200_LIB", str(LIB_PATH))
+    path = os.environ.get("RELAB_B200_LIB") or str(LIB_PATH)  # empty = unset
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

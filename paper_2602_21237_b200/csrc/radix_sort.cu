@@ -107,6 +107,7 @@ enum SortMode : int { kModeLsd = 0, kModeHybrid = 1, kModeScatter = 2 };  // hyb
 constexpr int kScatThreads = 1024;                 // histogram kernel: one CTA per SM
 constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
 constexpr int kMaxChunks = 160;
+constexpr int kD7Reps = 8;                         // digit-7 count replicas: no 148-deep same-address atomics
 constexpr int64_t kScatterMinRows = int64_t(1) << 22;  // below: the histogram kernel counts every digit at once
 constexpr int64_t kChunkMinRows = 32768;            // small inputs: fewer chunk histograms (128 KB each)
 #ifndef RL_PASS_THREADS
@@ -178,7 +179,8 @@ struct SortArgs {
   uint32_t* ghist;           // [kPasses][kBins]
   uint32_t* tile_counter;    // [2][kPasses] (first attempt, LSD after a hybrid fallback)
   uint32_t* grid_bar;        // grid barrier arrivals
-  uint32_t* flags;           // [0] a sub-bucket exceeds kLocalCap -> LSD fallback, [1] local work-item counter,
+  uint32_t* flags;           // [0] LSD fallback (a sub-bucket exceeds kLocalCap, ...), [1] local work-item counter,
+                             // [3] scatter path: pass-B tile counter,
                              // [4..5] raw int64 keys: OR of (key ^ first key) = the varying bits (u64)
   uint32_t* sub_off;         // [kSubBuckets + 1] sub-bucket starts, hybrid (not zeroed)
   uint64_t* status;          // [num_tiles][kBins] look-back words (epoch = pass + 1)
@@ -189,6 +191,7 @@ struct SortArgs {
   // scatter hybrid (kModeScatter)
   uint32_t* chunk_cnt;       // [kMaxChunks][kScatWords] rows per (chunk, sub-bucket), packed u16 pairs
   uint32_t* cur7;            // [kBins] rows placed per digit-7 bucket so far (zeroed)
+  uint32_t* d7rep;           // [kD7Reps][kBins] digit-7 counts, CTA c adds into replica c % kD7Reps (zeroed)
   uint32_t* cur16;           // [kSubBuckets] rows placed per sub-bucket so far (zeroed)
   uint32_t* d7_base;         // [kBins + 1] digit-7 bucket starts
   uint4* items;              // pass-B tiles (digit-7 bucket, first row, end row)
@@ -679,12 +682,14 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // onesweep passes (no look-back, no stable multisplit):
 //   sub_hist_kernel     chunk c (one CTA per SM) counts its rows per
 //                       sub-bucket in shared memory (packed u16 pairs, 128 KB)
-//                       into chunk_cnt[c], adds its digit-7 histogram, ORs
-//                       the varying key bits
+//                       into chunk_cnt[c], adds its digit-7 counts into one
+//                       of kD7Reps replicas (148 CTAs adding into the same
+//                       256 counters at once queue ~8 us of same-address
+//                       atomics behind the kernel's end), ORs the varying
+//                       key bits (one atomic per CTA)
 //   top_scatter_kernel  every CTA: the digit-7 bucket starts; CTA g also the
 //                       starts of bucket g's 256 sub-buckets (totals over the
-//                       chunk counts; > kLocalCap -> LSD fallback) and their
-//                       digit-6 histogram contributions; CTA 0 the
+//                       chunk counts; > kLocalCap -> LSD fallback); CTA 0 the
 //                       pass-B tile list. Then tiles of 4096 rows: ranked by
 //                       shared atomics, staged in digit order, one global
 //                       atomic per (tile, digit) reserves the run, written as
@@ -696,6 +701,12 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // MB, so every sector completes in L2. The cooperative kernel then runs only
 // the local phase — or, on the fallback flag (a sub-bucket above kLocalCap, a
 // wrapped chunk counter, < 4 varying digits), the LSD passes from the input.
+
+// Programmatic dependent launch: the next kernel of the chain may be scheduled
+// now (its CTAs take SMs as this kernel's CTAs exit) / wait until the previous
+// kernel of the chain has completed and its writes are visible.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // The fallback flag, read ONCE per CTA: other CTAs of the same kernel may
 // set it meanwhile, and a per-thread read could split the CTA at a barrier.
@@ -808,8 +819,12 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   uint32_t* red = w + kScatWords;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
+  pdl_launch_dependents();
   for (int i = tid; i < kScatWords / 4; i += kScatThreads) reinterpret_cast<uint4*>(w)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
+#ifdef RL_K1_PROFILE
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[4] = globaltimer();
+#endif
   const int64_t lo = chunk_lo(a.n, a.chunks, blockIdx.x), hi = chunk_lo(a.n, a.chunks, blockIdx.x + 1);
   const long long* col = static_cast<const long long*>(a.col);
   const uint64_t k0 = xform(uint64_t(__ldg(col)), a.desc);
@@ -853,13 +868,31 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
     base += kStep;
   }
   if ((hi & 1) && hi > lo && tid == 0) count(xform(uint64_t(col[hi - 1]), a.desc));
+  // varying key bits: one global atomic per CTA (one per warp serialised ~4700
+  // same-address atomics at one L2 slice: a 15 us tail)
   const uint32_t vhi = __reduce_or_sync(0xffffffffu, uint32_t(vary >> 32));
   const uint32_t vlo = __reduce_or_sync(0xffffffffu, uint32_t(vary));
-  if (lane == 0 && (vhi | vlo))
-    atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(vhi) << 32) | vlo);
+  if (lane == 0) {
+    red[2 * warp] = vhi;
+    red[2 * warp + 1] = vlo;
+  }
   __syncthreads();
+  if (warp == 0) {
+    const uint32_t h2 = __reduce_or_sync(0xffffffffu, red[2 * lane]);
+    const uint32_t l2 = __reduce_or_sync(0xffffffffu, red[2 * lane + 1]);
+    if (lane == 0 && (h2 | l2)) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(h2) << 32) | l2);
+  }
+#ifdef RL_K1_PROFILE
+  __syncthreads();
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[5] = globaltimer();
+  if (a.stamps && tid == 0) atomicMax(a.stamps + 7, globaltimer());  // last count loop to end
+#endif
   uint4* dst = reinterpret_cast<uint4*>(a.chunk_cnt + size_t(blockIdx.x) * kScatWords);
   for (int i = tid; i < kScatWords / 4; i += kScatThreads) dst[i] = reinterpret_cast<const uint4*>(w)[i];
+#ifdef RL_K1_PROFILE
+  __syncthreads();
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[6] = globaltimer();
+#endif
   // digit 7: a warp sums the 128 words of one bucket at a time; the chunk
   // total exposes a 16-bit counter that wrapped (> 65535 rows of one
   // sub-bucket in this chunk: far above kLocalCap, so the LSD runs)
@@ -873,17 +906,17 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
     }
     t = __reduce_add_sync(0xffffffffu, t);
     mine += t;
-    if (lane == 0 && t) atomicAdd(&a.ghist[7 * kBins + g], t);
+    if (lane == 0 && t) atomicAdd(&a.d7rep[(blockIdx.x % kD7Reps) * kBins + g], t);
   }
-  if (lane == 0) red[warp] = mine;
+  if (lane == 0) red[64 + warp] = mine;  // (slots 0..63 held the varying-bit parts)
   __syncthreads();
   if (tid == 0) {
     uint32_t tot = 0;
-    for (int i = 0; i < kScatThreads / 32; ++i) tot += red[i];
-    if (tot != uint32_t(hi - lo)) {
-      atomicOr(a.flags, 1u);      // LSD fallback,
-      atomicOr(a.flags + 2, 1u);  // which recounts digits 6 and 7
-    }
+    for (int i = 0; i < kScatThreads / 32; ++i) tot += red[64 + i];
+    if (tot != uint32_t(hi - lo)) atomicOr(a.flags, 1u);  // LSD fallback
+#ifdef RL_K1_PROFILE
+    if (a.stamps) atomicMax(a.stamps + 8, globaltimer());  // last CTA to end
+#endif
   }
 }
 
@@ -891,10 +924,16 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   extern __shared__ __align__(16) uint8_t sm[];
   const PTile s = ptile(sm);
   const int tid = threadIdx.x;
+  pdl_wait();  // the chunk counts
+  pdl_launch_dependents();
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[2] = globaltimer();
   if (fallback_flag(a)) return;  // a chunk counter wrapped: LSD
   // digit-7 bucket starts (every CTA)
-  const uint32_t t7 = tid < 256 ? __ldcg(a.ghist + 7 * kBins + tid) : 0u;
+  uint32_t t7 = 0;
+  if (tid < 256) {
+#pragma unroll
+    for (int r = 0; r < kD7Reps; ++r) t7 += __ldcg(a.d7rep + r * kBins + tid);
+  }
   {  // certain fallbacks, decided by every CTA alike before any work: fewer than 4
      // varying digits (LSD is as cheap), or a digit-7 bucket too big for 256 sub-buckets
     const uint64_t vary = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4));
@@ -902,10 +941,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
     const bool too_big = __syncthreads_or(tid < 256 && uint64_t(t7) > uint64_t(kBins) * kLocalCap) != 0;
     if (too_big || na < 4) {
-      if (blockIdx.x == 0 && tid == 0) {
-        atomicOr(a.flags, 1u);
-        atomicOr(a.flags + 2, 1u);  // no digit-6 histogram was built: the LSD counts digits 6 and 7 itself
-      }
+      if (blockIdx.x == 0 && tid == 0) atomicOr(a.flags, 1u);
       return;
     }
   }
@@ -957,7 +993,6 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     if (tid < 256) {
       a.sub_off[g * 256 + tid] = s.aux[g] + ex;
       if (tb > uint32_t(kLocalCap)) atomicOr(a.flags, 1u);
-      if (tb) atomicAdd(&a.ghist[6 * kBins + tid], tb);  // for an LSD fallback
     }
     if (g == kBins - 1 && tid == 0) a.sub_off[kSubBuckets] = uint32_t(a.n);
   }
@@ -995,6 +1030,8 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_ke
   extern __shared__ __align__(16) uint8_t sm[];
   const PTile s = ptile(sm);
   const int tid = threadIdx.x;
+  pdl_wait();  // the digit-7 pass
+  pdl_launch_dependents();
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[3] = globaltimer();
   if (fallback_flag(a)) return;  // LSD fallback
   const uint32_t n_items = __ldcg(a.meta);
@@ -1367,6 +1404,7 @@ constexpr int kLocalThreads = RL_LOCAL_THREADS;
 __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_kernel(SortArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const bool stamper = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
+  pdl_wait();  // the digit-6 pass
   if (stamper) a.stamps[1] = globaltimer();
   if (*reinterpret_cast<volatile const uint32_t*>(a.flags)) return;  // final before this launch: uniform
   local_phase<kLocalThreads>(a, smem, 1);
@@ -1450,8 +1488,8 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
       plan[2 * kPasses + 2] = plan[6] + plan[7];
       uint32_t low = 0;
       for (int p = 0; p < 6; ++p) low |= plan[p] << p;
-      // scatter fallback without complete digit-6/7 histograms: digits 6 and 7 are recounted
-      if (a.mode == kModeScatter && __ldcg(a.flags + 2)) low |= (plan[6] << 6) | (plan[7] << 7);
+      // scatter fallback: the scatter path builds no digit-6/7 histograms, the LSD counts them
+      if (a.mode == kModeScatter) low |= (plan[6] << 6) | (plan[7] << 7);
       plan[2 * kPasses + 3] = raw && !a.count_all ? low : 0u;  // digits the LSD path still has to count
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
@@ -1462,12 +1500,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   auto count_low_digits = [&]() {
     const uint32_t low = plan[2 * kPasses + 3];
     if (!low) return;
-    if (low >> 6) {  // digit-6/7 rows start over
-      if (blockIdx.x == 0)
-        for (int i = tid; i < 2 * kBins; i += kThreads) a.ghist[6 * kBins + i] = 0;
-      grid_sync(a.grid_bar, ++barrier_no);
-    }
-    count_digits(a, smem, low);
+    count_digits(a, smem, low);  // (digit-6/7 rows are still zero on a scatter fallback)
     grid_sync(a.grid_bar, ++barrier_no);
     scan_rows(0, (low >> 6) ? kPasses : 6);
   };
@@ -1560,6 +1593,7 @@ struct Layout {
   uint32_t* chunk_cnt;  // scatter hybrid only (n >= scatter_min_rows())
   uint32_t* cur7;
   uint32_t* cur16;
+  uint32_t* d7rep;
   uint32_t* d7_base;
   uint32_t* items;
   uint32_t* meta;
@@ -1575,6 +1609,7 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   const bool scat = n >= scatter_min_rows();
   auto c7 = scat ? t32(c, size_t(kBins)) : nullptr;          // zeroed with the prefix
   auto c16 = scat ? t32(c, size_t(kSubBuckets)) : nullptr;
+  auto d7r = scat ? t32(c, size_t(kD7Reps) * kBins) : nullptr;
   const size_t head = c.used;
   auto st = t64(c, tiles * kBins);
   const size_t zero = c.used;
@@ -1587,7 +1622,7 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   auto db = scat ? t32(c, size_t(kBins + 4)) : nullptr;
   auto it = scat ? t32(c, 4 * size_t(kBins + 2 + n / kPTile)) : nullptr;
   auto me = scat ? t32(c, 4) : nullptr;
-  if (L) *L = Layout{h, tc, gb, fl, st, zero, head, so, ka, kb, va, vb, cc, c7, c16, db, it, me};
+  if (L) *L = Layout{h, tc, gb, fl, st, zero, head, so, ka, kb, va, vb, cc, c7, c16, d7r, db, it, me};
 }
 
 size_t workspace_bytes(int64_t n) {
@@ -1633,6 +1668,15 @@ static bool scatter_kernels_ready() {
                                          int(kLocalSmemBytes)) == cudaSuccess
                 ? 1
                 : 0;
+#ifdef RL_CARVEOUT_MAX
+  if (ready == 1) {  // one L1/shared split for every kernel of the sort: no SM reconfiguration between them
+    cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(local_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(sort_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
+#endif
   return ready == 1;
 }
 
@@ -1697,6 +1741,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     a.chunk_cnt = L.chunk_cnt;
     a.cur7 = L.cur7;
     a.cur16 = L.cur16;
+    a.d7rep = L.d7rep;
     a.d7_base = L.d7_base;
     a.items = reinterpret_cast<uint4*>(L.items);
     a.meta = L.meta;
@@ -1722,11 +1767,26 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     };
     sub_hist_kernel<<<chunks, kScatThreads, kHistSmem, stream>>>(a);
     chk("sub_hist");
-    top_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
+    // the next three launches may be scheduled early (programmatic dependent
+    // launch); each waits on the device for its predecessor's results
+    auto launch_dep = [&](auto kernel, int g, int threads, size_t smem) {
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = getenv_flag("RL_NO_PDL") ? 0 : 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(g);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kernel, a);
+    };
+    if ((e = launch_dep(top_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
     chk("top_scatter");
-    sub_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
+    if ((e = launch_dep(sub_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
     chk("sub_scatter");
-    local_kernel<<<lgrid, kLocalThreads, kLocalSmemBytes, stream>>>(a);
+    if ((e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes)) != cudaSuccess) return rl_cuda_status(e);
     chk("local");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
     void* params[] = {&a};

@@ -1405,6 +1405,7 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   extern __shared__ __align__(128) uint8_t smem[];
   const bool stamper = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
   pdl_wait();  // the digit-6 pass
+  pdl_launch_dependents();
   if (stamper) a.stamps[1] = globaltimer();
   if (*reinterpret_cast<volatile const uint32_t*>(a.flags)) return;  // final before this launch: uniform
   local_phase<kLocalThreads>(a, smem, 1);
@@ -1425,6 +1426,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
 
   // ---- scatter hybrid: local_kernel sorted the sub-buckets already; this
   // launch only runs the LSD fallback
+  if (a.mode == kModeScatter) pdl_wait();  // (launched as a dependent of local_kernel)
   if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) return;
   // ---- histograms come from hist_kernel (launched just before, on the same stream)
   if (stamper) a.stamps[1] = globaltimer();
@@ -1789,9 +1791,27 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     if ((e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes)) != cudaSuccess) return rl_cuda_status(e);
     chk("local");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
-    void* params[] = {&a};
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
-                                    kSmemBytes, stream);
+    {  // the cooperative kernel (returns at once unless the fallback flag is set), also scheduled early
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = getenv_flag("RL_NO_PDL") ? 0 : 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = kSmemBytes;
+      cfg.stream = stream;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      e = cudaLaunchKernelEx(&cfg, sort_kernel, a);
+      if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {  // no programmatic cooperative launch
+        cudaGetLastError();
+        void* params[] = {&a};
+        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
+                                        kSmemBytes, stream);
+      }
+    }
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
     count_launches(5);
     return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());

@@ -107,6 +107,7 @@ enum SortMode : int { kModeLsd = 0, kModeHybrid = 1, kModeScatter = 2 };  // hyb
 constexpr int kScatThreads = 1024;                 // histogram kernel: one CTA per SM
 constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
 constexpr int kMaxChunks = 160;
+constexpr int kHistReps = 8;                       // digit-histogram replicas: no grid-deep same-address atomics
 constexpr int kD7Reps = 8;                         // digit-7 count replicas: no 148-deep same-address atomics
 constexpr int64_t kScatterMinRows = int64_t(1) << 22;  // below: the histogram kernel counts every digit at once
 constexpr int64_t kChunkMinRows = 32768;            // small inputs: fewer chunk histograms (128 KB each)
@@ -176,7 +177,7 @@ struct SortArgs {
   int mode;                  // SortMode
   int count_all;             // raw keys: the histogram kernel counted every digit (small n)
   // zeroed per call
-  uint32_t* ghist;           // [kPasses][kBins]
+  uint32_t* ghist;           // [kHistReps][kPasses][kBins]: CTA c adds into replica c % kHistReps
   uint32_t* tile_counter;    // [2][kPasses] (first attempt, LSD after a hybrid fallback)
   uint32_t* grid_bar;        // grid barrier arrivals
   uint32_t* flags;           // [0] LSD fallback (a sub-bucket exceeds kLocalCap, ...), [1] local work-item counter,
@@ -198,6 +199,14 @@ struct SortArgs {
   uint32_t* meta;            // [0] pass-B tiles
   int chunks;                // input chunks = CTAs of the histogram and digit-7 kernels
 };
+
+// Global digit count (pass p, digit d): the sum of the histogram replicas.
+__device__ __forceinline__ uint32_t ghist_at(const SortArgs& a, int p, int d) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int r = 0; r < kHistReps; ++r) c += __ldcg(a.ghist + (r * kPasses + p) * kBins + d);
+  return c;
+}
 
 __device__ __forceinline__ uint64_t load_key(const SortArgs& a, int64_t i) {
   if (a.src_mode == kSrcInt64) return xform(uint64_t(__ldg(static_cast<const long long*>(a.col) + i)), a.desc);
@@ -621,16 +630,27 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
       }
     }
   }
-  if constexpr (RAW) {
+  __shared__ uint32_t vparts[2 * (kHistThreads / 32)];
+  if constexpr (RAW) {  // varying bits: one global atomic per CTA
     const uint32_t hi = __reduce_or_sync(0xffffffffu, uint32_t(vary >> 32));
     const uint32_t lo = __reduce_or_sync(0xffffffffu, uint32_t(vary));
-    if ((tid & 31) == 0 && (hi | lo))
-      atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(hi) << 32) | lo);
+    if ((tid & 31) == 0) {
+      vparts[2 * (tid >> 5)] = hi;
+      vparts[2 * (tid >> 5) + 1] = lo;
+    }
   }
   __syncthreads();
+  if constexpr (RAW) {
+    if (tid < 32) {
+      const uint32_t hi = __reduce_or_sync(0xffffffffu, tid < kHistThreads / 32 ? vparts[2 * tid] : 0u);
+      const uint32_t lo = __reduce_or_sync(0xffffffffu, tid < kHistThreads / 32 ? vparts[2 * tid + 1] : 0u);
+      if (tid == 0 && (hi | lo)) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(hi) << 32) | lo);
+    }
+  }
+  uint32_t* gh = a.ghist + size_t(blockIdx.x % kHistReps) * kPasses * kBins;
   for (int i = RAW && !ALL ? 6 * kBins + tid : tid; i < kPasses * kBins; i += kHistThreads) {
     const uint32_t c = h[i];
-    if (c) atomicAdd(&a.ghist[i], c);
+    if (c) atomicAdd(&gh[i], c);
   }
 }
 
@@ -670,7 +690,7 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
   __syncthreads();
   for (int i = tid; i < kPasses * kBins; i += kThreads) {
     const uint32_t c = h[i];
-    if (c && ((digits >> (i / kBins)) & 1u)) atomicAdd(&a.ghist[i], c);
+    if (c && ((digits >> (i / kBins)) & 1u)) atomicAdd(&a.ghist[size_t(blockIdx.x % kHistReps) * kPasses * kBins + i], c);
   }
 }
 
@@ -1444,7 +1464,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   auto scan_rows = [&](int p0, int p1) {  // bin_off rows [p0, p1) from the global histograms
     uint32_t* warp_sums = reinterpret_cast<uint32_t*>(smem);  // scratch
     for (int p = p0; p < p1; ++p) {
-      const uint32_t c = __ldcg(a.ghist + p * kBins + tid);
+      const uint32_t c = ghist_at(a, p, tid);
       uint32_t total;
       bin_off[p * kBins + tid] = block_exclusive_scan<kThreads>(c, warp_sums, &total);
       __syncthreads();
@@ -1455,7 +1475,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
     const uint64_t vary = raw ? __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4)) : 0ull;
     uint32_t nz = 1, mx = 1;
     for (int p = raw && !a.count_all ? 6 : 0; p < kPasses; ++p) {
-      const uint32_t c = __ldcg(a.ghist + p * kBins + tid);
+      const uint32_t c = ghist_at(a, p, tid);
       uint32_t total;
       bin_off[p * kBins + tid] = block_exclusive_scan<kThreads>(c, warp_sums, &total);
       const int full = __syncthreads_or(uint64_t(c) == uint64_t(a.n));
@@ -1604,7 +1624,7 @@ struct Layout {
 template <typename C, typename T32, typename T64>
 static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
   const size_t tiles = size_t((n + kTile - 1) / kTile);
-  auto h = t32(c, kPasses * kBins);
+  auto h = t32(c, size_t(kHistReps) * kPasses * kBins);
   auto tc = t32(c, 2 * kPasses);
   auto gb = t32(c, 2);
   auto fl = t32(c, 8);
@@ -1928,7 +1948,11 @@ __global__ void dest_kernel(const int64_t* __restrict__ keys, int64_t n, uint32_
 
 __global__ void counts_kernel(const uint32_t* hist, int parts, int64_t* counts_out) {
   const int d = threadIdx.x;
-  if (d < parts) counts_out[d] = int64_t(hist[d]);
+  if (d < parts) {  // digit 0's count: the sum of the histogram replicas
+    uint32_t c = 0;
+    for (int r = 0; r < kHistReps; ++r) c += hist[r * kPasses * kBins + d];
+    counts_out[d] = int64_t(c);
+  }
 }
 
 size_t partition_workspace_bytes(int64_t n) {

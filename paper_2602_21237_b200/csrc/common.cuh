@@ -90,6 +90,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
 }
 // Order earlier generic-proxy accesses to shared memory before later
 // async-proxy (TMA) writes into the same buffer.
+// Programmatic dependent launch: the next kernel of the stream may be
+// scheduled now (its CTAs take SMs as this kernel's CTAs exit) / wait until
+// the previous kernel has completed and its writes are visible (a no-op for a
+// kernel not launched as a programmatic dependent).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

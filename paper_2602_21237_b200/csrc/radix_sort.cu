@@ -573,6 +573,7 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(SortArgs a) {
   __shared__ uint32_t h[kPasses * kBins];
   const int tid = threadIdx.x;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
+  pdl_launch_dependents();  // the sort kernel may be scheduled now; it waits for these counts
   for (int i = tid; i < kPasses * kBins; i += kHistThreads) h[i] = 0;
   __syncthreads();
   // RAW counts only the top two digits (the hybrid's passes) and ORs the
@@ -721,12 +722,6 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // MB, so every sector completes in L2. The cooperative kernel then runs only
 // the local phase — or, on the fallback flag (a sub-bucket above kLocalCap, a
 // wrapped chunk counter, < 4 varying digits), the LSD passes from the input.
-
-// Programmatic dependent launch: the next kernel of the chain may be scheduled
-// now (its CTAs take SMs as this kernel's CTAs exit) / wait until the previous
-// kernel of the chain has completed and its writes are visible.
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // The fallback flag, read ONCE per CTA: other CTAs of the same kernel may
 // set it meanwhile, and a per-thread read could split the CTA at a barrier.
@@ -1446,7 +1441,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
 
   // ---- scatter hybrid: local_kernel sorted the sub-buckets already; this
   // launch only runs the LSD fallback
-  if (a.mode == kModeScatter) pdl_wait();  // (launched as a dependent of local_kernel)
+  pdl_wait();  // launched as a programmatic dependent of the histogram / local-phase kernel
   if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) return;
   // ---- histograms come from hist_kernel (launched just before, on the same stream)
   if (stamper) a.stamps[1] = globaltimer();
@@ -1737,6 +1732,32 @@ static int hist_grid(int64_t n) {  // one co-resident wave (2 CTAs of 512 thread
                                                     int64_t(device_sm_count()) * RL_HIST_CTAS_PER_SM)));
 }
 
+// The cooperative sort kernel as a programmatic dependent of the kernel before
+// it (scheduled while that one drains; it waits on the device), or a plain
+// cooperative launch where the runtime refuses the combination.
+static cudaError_t launch_sort_kernel(SortArgs& a, int grid, cudaStream_t stream) {
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = getenv_flag("RL_NO_PDL") ? 0 : 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, sort_kernel, a);
+  if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
+    cudaGetLastError();
+    void* params[] = {&a};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
+                                    kSmemBytes, stream);
+  }
+  return e;
+}
+
 // Histograms, then the cooperative kernel (LSD, or the wide-key hybrid
 // with its in-kernel LSD fallback).
 static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* const* events, int max_ctas = 0) {
@@ -1811,27 +1832,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     if ((e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes)) != cudaSuccess) return rl_cuda_status(e);
     chk("local");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
-    {  // the cooperative kernel (returns at once unless the fallback flag is set), also scheduled early
-      cudaLaunchAttribute attr[2];
-      attr[0].id = cudaLaunchAttributeCooperative;
-      attr[0].val.cooperative = 1;
-      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[1].val.programmaticStreamSerializationAllowed = getenv_flag("RL_NO_PDL") ? 0 : 1;
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(kThreads);
-      cfg.dynamicSmemBytes = kSmemBytes;
-      cfg.stream = stream;
-      cfg.attrs = attr;
-      cfg.numAttrs = 2;
-      e = cudaLaunchKernelEx(&cfg, sort_kernel, a);
-      if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {  // no programmatic cooperative launch
-        cudaGetLastError();
-        void* params[] = {&a};
-        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
-                                        kSmemBytes, stream);
-      }
-    }
+    e = launch_sort_kernel(a, grid, stream);  // returns at once unless the fallback flag is set
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
     count_launches(5);
     return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
@@ -1843,9 +1844,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   else if (a.src_mode == kSrcInt64) hist_kernel<true, false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   else hist_kernel<false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
-  void* params[] = {&a};
-  e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sort_kernel), dim3(grid), dim3(kThreads), params,
-                                  kSmemBytes, stream);
+  e = launch_sort_kernel(a, grid, stream);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
   count_launches(2);
   return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());

@@ -81,9 +81,20 @@ __global__ void __launch_bounds__(kThreads) digest_kernel(ColumnSet cols, const 
     x0 ^= __shfl_xor_sync(0xffffffffu, x0, o);
     x1 ^= __shfl_xor_sync(0xffffffffu, x1, o);
   }
+  __shared__ uint64_t wx[2][kThreads / 32];  // one pair of global atomics per CTA
   if ((threadIdx.x & 31) == 0) {
-    atomicXor(&out2[0], (unsigned long long)x0);
-    atomicXor(&out2[1], (unsigned long long)x1);
+    wx[0][threadIdx.x >> 5] = x0;
+    wx[1][threadIdx.x >> 5] = x1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t y0 = 0, y1 = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      y0 ^= wx[0][w];
+      y1 ^= wx[1][w];
+    }
+    atomicXor(&out2[0], (unsigned long long)y0);
+    atomicXor(&out2[1], (unsigned long long)y1);
   }
 }
 

@@ -355,10 +355,17 @@ __global__ void __launch_bounds__(kThreads, RL_EXPAND_MIN_BLOCKS) expand_kernel(
   }
   __syncthreads();  // the staged window is rewritten by the next sub-tile
   }
-  if (kChecksum) {
+  if (kChecksum) {  // one global atomic per CTA (per warp, thousands queue on one address at the end)
+    __shared__ uint64_t wsum[kThreads / 32];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-    if ((tid & 31) == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(a.checksum), (unsigned long long)sum);
+    if ((tid & 31) == 0) wsum[tid >> 5] = sum;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t t = 0;
+      for (int w = 0; w < kThreads / 32; ++w) t += wsum[w];
+      if (t) atomicAdd(reinterpret_cast<unsigned long long*>(a.checksum), (unsigned long long)t);
+    }
   }
 }
 // One CTA per output tile while that fills ~8 CTAs per SM; beyond, each CTA

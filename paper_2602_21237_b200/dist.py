@@ -221,7 +221,33 @@ _PEER: dict = {}
 def _peer_exchange_ok(group, device) -> bool:
     if os.environ.get("RL_NO_P2P") or device.type != "cuda" or dist.get_backend(group) != "nccl":
         return False
-    return _PEER.get(("ok", device.index), True)
+    key = ("ok", id(group), device.index)
+    if key not in _PEER:
+        _PEER[key] = _probe_symmetric_memory(group, device)
+    return _PEER[key] and _PEER.get(("ok", device.index), True)
+
+
+def _probe_symmetric_memory(group, device) -> bool:
+    """Whether EVERY rank of the group can use symmetric memory, decided
+    collectively once: each rank tries a small buffer + rendezvous + barrier,
+    then the ranks agree with a MIN all-reduce — no rank goes to the peer
+    path while another falls back to NCCL (that would leave the two waiting
+    on different collectives)."""
+    ok = 1
+    try:
+        import torch.distributed._symmetric_memory as sm
+
+        buf = sm.empty(4096, dtype=torch.uint8, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        hdl = sm.rendezvous(buf, grp.group_name)
+        hdl.barrier()
+        torch.cuda.current_stream(device).synchronize()
+        del hdl, buf
+    except Exception:  # any failure on any rank: NCCL everywhere
+        ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item())
 
 
 def _row_bytes(c: torch.Tensor) -> int:

@@ -312,6 +312,27 @@ RL_API int rl_push_rows(const uint32_t* rows, int64_t n, int32_t parts,
                  int32_t n_columns, const uint64_t* dest_bases,
                  const int64_t* dest_offsets, void* stream);
 
+/* Splitters of the multi-GPU ORDER BY (dist.choose_splitters_device; the
+ * sample-sort step of SURVEY §8(e), ranges chosen on the composite
+ * (key, global row id) order so stability survives duplicate-heavy keys).
+ * rl_sample_keys writes this rank's [3][per_rank] int64 sample pack (key in
+ * sort order — complemented when descending —, global row id, 1 = real
+ * sample) for an all-gather; rl_pick_splitters takes the gathered
+ * [parts][3][per_rank] packs (parts * per_rank <= RL_MAX_SPLIT_SAMPLES) and
+ * writes the parts-1 splitter keys and global row ids (one CTA, no host
+ * round trip). rl_global_ids turns received u32 local row ids into int64
+ * global ids: out[i] = bases[s] + rows[i] for the rows of source s
+ * (recv_counts[s] rows each, host arrays, parts <= 64). */
+#define RL_MAX_SPLIT_SAMPLES 2048
+RL_API int rl_sample_keys(const int64_t* keys, int64_t n, int32_t per_rank,
+                 int64_t gid_base, int32_t descending, int64_t* pack, void* stream);
+RL_API int rl_pick_splitters(const int64_t* gathered, int32_t parts, int32_t per_rank,
+                 int32_t descending, int64_t* split_keys, int64_t* split_gids,
+                 void* stream);
+RL_API int rl_global_ids(const uint32_t* rows, int64_t total, int32_t parts,
+                 const int64_t* recv_counts, const int64_t* bases, int64_t* out,
+                 void* stream);
+
 /* ---------------------------------------------------------------------
  * The reference's 128-bit multiset result digest (relation.py:319-330,
  * hashing.py:64-109), bit-exact, computed on the device from the columns

@@ -34,6 +34,7 @@ RL_MAX_COLUMNS = 32
 RL_MAX_ROWS = 2**32 - 1
 RL_SORT_EVENTS = 3
 RL_SORT_STAMPS = 12
+RL_MAX_SPLIT_SAMPLES = 2048
 RL_SORT_MAX_FUSED_COLUMNS = 8
 
 
@@ -66,6 +67,9 @@ SIGNATURES = {
     "rl_device_sm_count": (ctypes.c_int, []),
     "rl_launch_count": (_I64, []),
     "rl_push_rows": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _I32, _P, _P, _P]),
+    "rl_sample_keys": (ctypes.c_int, [_P, _I64, _I32, _I64, _I32, _P, _P]),
+    "rl_pick_splitters": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _P]),
+    "rl_global_ids": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _P]),
     "rl_stager_file_h2d": (ctypes.c_int, [_P, _P, _I32, ctypes.c_uint64, _SZ, _P, _P]),
     "rl_stager_file_d2h": (ctypes.c_int, [_P, _P, _I32, ctypes.c_uint64, _SZ, _P]),
     "rl_stager_file_read": (ctypes.c_int, [_P, _P, _I32, ctypes.c_uint64, _SZ]),

@@ -86,6 +86,82 @@ int push_rows(const uint32_t* rows, int64_t n, int parts, const int64_t* dest_st
   return rl_cuda_status(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- splitters
+// Regular samples of this rank's keys, packed as the all-gather expects:
+// [0][i] key in sort order (complemented when descending), [1][i] global row
+// id, [2][i] 1 = a real sample (ranks with fewer rows than samples pad).
+__global__ void sample_kernel(const int64_t* keys, int64_t n, int per_rank, int64_t gid_base, int descending,
+                              int64_t* pack) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= per_rank) return;
+  const int64_t m = n < per_rank ? n : per_rank;
+  int64_t idx = (int64_t(i) * (n > 0 ? n : 1)) / (m > 0 ? m : 1);
+  if (idx > n - 1) idx = n > 0 ? n - 1 : 0;
+  const int64_t k = n > 0 ? keys[idx] : 0;
+  pack[i] = descending ? ~k : k;
+  pack[per_rank + i] = idx + gid_base;
+  pack[2 * per_rank + i] = i < m ? 1 : 0;
+}
+
+// All ranks' samples (P blocks of [3][per_rank]) → the P-1 splitters: every
+// sample's rank in the composite (real first, key, global id) order is counted
+// in shared memory (S <= 2048), and the samples of rank j * cnt / P are kept.
+constexpr int kSplitThreads = 1024;
+constexpr int kMaxSamples = 2048;  // P x per_rank (static shared memory)
+__global__ void __launch_bounds__(kSplitThreads) pick_kernel(const int64_t* all, int parts, int per_rank,
+                                                             int descending, int64_t* out_keys, int64_t* out_gids) {
+  __shared__ int64_t sk[kMaxSamples];
+  __shared__ int64_t sg[kMaxSamples];
+  __shared__ uint8_t sv[kMaxSamples];
+  __shared__ int cnt_s;
+  const int S = parts * per_rank, tid = threadIdx.x;
+  if (tid == 0) cnt_s = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int i = tid; i < S; i += kSplitThreads) {
+    const int r = i / per_rank, j = i % per_rank;
+    const int64_t* blk = all + int64_t(r) * 3 * per_rank;
+    sk[i] = blk[j];
+    sg[i] = blk[per_rank + j];
+    sv[i] = blk[2 * per_rank + j] != 0;
+    mine += sv[i];
+  }
+  atomicAdd(&cnt_s, mine);
+  __syncthreads();
+  const int cnt = cnt_s;
+  auto less = [&](int a, int b) {  // composite order: real samples first, then (key, gid)
+    if (sv[a] != sv[b]) return sv[a] > sv[b];
+    if (sk[a] != sk[b]) return sk[a] < sk[b];
+    return sg[a] < sg[b];
+  };
+  for (int i = tid; i < S; i += kSplitThreads) {
+    int rank = 0;
+    for (int o = 0; o < S; ++o) rank += less(o, i) ? 1 : 0;
+    for (int j = 1; j < parts; ++j) {
+      int64_t pick = int64_t(j) * cnt / parts;
+      if (pick > cnt - 1) pick = cnt > 0 ? cnt - 1 : 0;
+      if (rank == pick) {
+        out_keys[j - 1] = descending ? ~sk[i] : sk[i];
+        out_gids[j - 1] = sg[i];
+      }
+    }
+  }
+}
+
+// Global row ids of received rows: sender's base + its local row id (u32).
+struct GidArgs {
+  int64_t starts[kMaxParts + 1];
+  int64_t bases[kMaxParts];
+  int parts;
+};
+__global__ void gid_kernel(const uint32_t* rows, int64_t total, GidArgs g, int64_t* out) {
+  for (int64_t i = int64_t(blockIdx.x) * kThreads + threadIdx.x; i < total; i += int64_t(gridDim.x) * kThreads) {
+    int d = 0;
+    while (d + 1 < g.parts && g.starts[d + 1] <= i) ++d;
+    out[i] = g.bases[d] + int64_t(rows[i]);
+  }
+}
+
 }  // namespace exchange
 }  // namespace rl
 
@@ -96,6 +172,47 @@ RL_API int rl_push_rows(const uint32_t* rows, int64_t n, int32_t parts, const in
                         const int64_t* dest_offsets, void* stream) {
   return rl::exchange::push_rows(rows, n, parts, dest_starts, columns, n_columns, dest_bases, dest_offsets,
                                  static_cast<cudaStream_t>(stream));
+}
+
+RL_API int rl_sample_keys(const int64_t* keys, int64_t n, int32_t per_rank, int64_t gid_base, int32_t descending,
+                          int64_t* pack, void* stream) {
+  if (n < 0 || per_rank < 1 || !pack || (n > 0 && !keys)) return RL_ERR_BAD_ARG;
+  rl::exchange::sample_kernel<<<(per_rank + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      keys, n, per_rank, gid_base, descending, pack);
+  rl::count_launches(1);
+  return rl::rl_cuda_status(cudaGetLastError());
+}
+
+RL_API int rl_pick_splitters(const int64_t* gathered, int32_t parts, int32_t per_rank, int32_t descending,
+                             int64_t* split_keys, int64_t* split_gids, void* stream) {
+  if (parts < 1 || per_rank < 1 || int64_t(parts) * per_rank > rl::exchange::kMaxSamples || !gathered)
+    return RL_ERR_BAD_ARG;
+  if (parts == 1) return RL_OK;
+  if (!split_keys || !split_gids) return RL_ERR_BAD_ARG;
+  rl::exchange::pick_kernel<<<1, rl::exchange::kSplitThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      gathered, parts, per_rank, descending, split_keys, split_gids);
+  rl::count_launches(1);
+  return rl::rl_cuda_status(cudaGetLastError());
+}
+
+RL_API int rl_global_ids(const uint32_t* rows, int64_t total, int32_t parts, const int64_t* recv_counts,
+                         const int64_t* bases, int64_t* out, void* stream) {
+  if (total < 0 || parts < 1 || parts > rl::exchange::kMaxParts || !recv_counts || !bases) return RL_ERR_BAD_ARG;
+  if (total == 0) return RL_OK;
+  if (!rows || !out) return RL_ERR_BAD_ARG;
+  rl::exchange::GidArgs g;
+  g.parts = parts;
+  g.starts[0] = 0;
+  for (int d = 0; d < parts; ++d) {
+    g.starts[d + 1] = g.starts[d] + recv_counts[d];
+    g.bases[d] = bases[d];
+  }
+  if (g.starts[parts] != total) return RL_ERR_BAD_ARG;
+  const int grid = int(std::min<int64_t>((total + rl::exchange::kThreads - 1) / rl::exchange::kThreads,
+                                         int64_t(rl::device_sm_count()) * 8));
+  rl::exchange::gid_kernel<<<grid, rl::exchange::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(rows, total, g, out);
+  rl::count_launches(1);
+  return rl::rl_cuda_status(cudaGetLastError());
 }
 
 }  // extern "C"

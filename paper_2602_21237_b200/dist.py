@@ -273,7 +273,21 @@ def _sort_take(ops, cols, key_idx, descending):
 
 def _global_ids(rows: torch.Tensor, recv_counts: list, bases: list) -> torch.Tensor:
     """int64 global row ids of received rows: the sender's base + its local
-    row id (row ids travel as 4 bytes, not 8)."""
+    row id (row ids travel as 4 bytes, not 8). One kernel on the GPU
+    (rl_global_ids); torch ops on CPU tensors (the gloo tests)."""
+    if rows.device.type == "cuda" and len(recv_counts) <= 64:
+        import ctypes
+
+        from . import _capi as C
+        from . import engine
+
+        p = len(recv_counts)
+        out = torch.empty(rows.numel(), dtype=torch.int64, device=rows.device)
+        rc = (ctypes.c_int64 * p)(*[int(c) for c in recv_counts])
+        bs = (ctypes.c_int64 * p)(*[int(b) for b in bases])
+        C.check(C.load().rl_global_ids(engine._ptr(rows), rows.numel(), p, rc, bs, engine._ptr(out),
+                                       engine.stream_handle()), "rl_global_ids")
+        return out
     r = rows.to(torch.int64) & 0xFFFFFFFF
     off = 0
     for c, b in zip(recv_counts, bases):  # P slices, one in-place add each
@@ -401,6 +415,23 @@ def choose_splitters_device(keys: torch.Tensor, gid_base: int, descending: bool,
     p = _group_size(group)
     n = keys.numel()
     dev = keys.device
+    if dev.type == "cuda":  # two launches around the all-gather (rl_sample_keys, rl_pick_splitters)
+        from . import _capi as C
+        from . import engine
+
+        lib = C.load()
+        per = max(1, min(per_rank, C.RL_MAX_SPLIT_SAMPLES // p))
+        keys = keys.contiguous()
+        pack = torch.empty(3 * per, dtype=torch.int64, device=dev)
+        C.check(lib.rl_sample_keys(engine._ptr(keys), n, per, int(gid_base), int(descending), engine._ptr(pack),
+                                   engine.stream_handle()), "rl_sample_keys")
+        allp = torch.empty(p * 3 * per, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(allp, pack, group=group)
+        sk = torch.empty(max(p - 1, 0), dtype=torch.int64, device=dev)
+        sg = torch.empty(max(p - 1, 0), dtype=torch.int64, device=dev)
+        C.check(lib.rl_pick_splitters(engine._ptr(allp), p, per, int(descending), engine._ptr(sk), engine._ptr(sg),
+                                      engine.stream_handle()), "rl_pick_splitters")
+        return sk, sg
     m = min(per_rank, n)
     idx = (torch.arange(per_rank, device=dev, dtype=torch.int64) * max(n, 1)) // max(m, 1)
     idx = idx.clamp_(max=max(n - 1, 0))

@@ -131,3 +131,58 @@ def test_distributed_ops_take_the_peer_push(nccl_world1, monkeypatch):
     assert (j.left_gids.cpu().numpy() == wl).all() and (j.right_gids.cpu().numpy() == wr).all()
     used = [k for k in D._PEER if k[0] in ("sort", "join_left", "join_right")]
     assert used, "the peer-memory exchange was not used"
+
+
+@pytest.mark.parametrize("descending", [False, True])
+def test_splitter_and_gid_kernels_emulated_ranks(descending):
+    """rl_sample_keys / rl_pick_splitters / rl_global_ids for five emulated
+    ranks (one with fewer rows than samples, duplicate-heavy keys) against a
+    numpy restatement: samples at i * n // m, splitters at ranks j * cnt // P
+    of the (real first, key, global id) order, gid = sender base + local row."""
+    import ctypes
+
+    from paper_2602_21237_b200 import _capi as C
+    from paper_2602_21237_b200 import engine
+
+    lib = C.load()
+    rng = np.random.default_rng(31 + descending)
+    sizes = [5000, 3000, 100, 7000, 4000]
+    per = 256
+    p = len(sizes)
+    bases = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    packs = []
+    for n, b in zip(sizes, bases):
+        keys = rng.integers(-50, 50, n).astype(np.int64)  # heavy duplicates: ties split by global id
+        kd = torch.from_numpy(keys).cuda()
+        pack = torch.empty(3 * per, dtype=torch.int64, device="cuda")
+        C.check(lib.rl_sample_keys(engine._ptr(kd), n, per, int(b), int(descending), engine._ptr(pack),
+                                   engine.stream_handle()), "rl_sample_keys")
+        m = min(per, n)
+        idx = np.minimum(np.arange(per) * max(n, 1) // max(m, 1), n - 1)
+        want = np.stack([~keys[idx] if descending else keys[idx], idx + b, (np.arange(per) < m).astype(np.int64)])
+        assert (pack.cpu().numpy().reshape(3, per) == want).all()
+        packs.append(want)
+    allp = torch.from_numpy(np.concatenate([q.reshape(-1) for q in packs])).cuda()
+    sk = torch.empty(p - 1, dtype=torch.int64, device="cuda")
+    sg = torch.empty(p - 1, dtype=torch.int64, device="cuda")
+    C.check(lib.rl_pick_splitters(engine._ptr(allp), p, per, int(descending), engine._ptr(sk), engine._ptr(sg),
+                                  engine.stream_handle()), "rl_pick_splitters")
+    k = np.concatenate([q[0] for q in packs])
+    g = np.concatenate([q[1] for q in packs])
+    v = np.concatenate([q[2] for q in packs])
+    order = np.lexsort((g, k, 1 - v))  # real samples first, then key, then global id
+    cnt = int(v.sum())
+    picks = np.minimum(np.arange(1, p) * cnt // p, cnt - 1)
+    want_k = k[order[picks]]
+    assert (sk.cpu().numpy() == (~want_k if descending else want_k)).all()
+    assert (sg.cpu().numpy() == g[order[picks]]).all()
+
+    recv = [300, 0, 17, 1200, 5]
+    rows = rng.integers(0, 2**32, sum(recv), dtype=np.uint64).astype(np.uint32)
+    rd = torch.from_numpy(rows.view(np.int32)).cuda()
+    out = torch.empty(len(rows), dtype=torch.int64, device="cuda")
+    rb = [10**12, 5, 0, 2**40 + 3, 77]
+    C.check(lib.rl_global_ids(engine._ptr(rd), len(rows), p, (ctypes.c_int64 * p)(*recv), (ctypes.c_int64 * p)(*rb),
+                              engine._ptr(out), engine.stream_handle()), "rl_global_ids")
+    want_g = rows.astype(np.int64) + np.repeat(np.array(rb, dtype=np.int64), recv)
+    assert (out.cpu().numpy() == want_g).all()

@@ -312,6 +312,14 @@ RL_API int rl_push_rows(const uint32_t* rows, int64_t n, int32_t parts,
                  int32_t n_columns, const uint64_t* dest_bases,
                  const int64_t* dest_offsets, void* stream);
 
+/* rl_push_rows, but the last region of every destination receives int64
+ * GLOBAL row ids (gid_base + local row id, 8 bytes per row) instead of u32
+ * local row ids: the receiver needs no per-source bases. */
+RL_API int rl_push_rows_gid(const uint32_t* rows, int64_t n, int32_t parts,
+                 const int64_t* dest_starts, const rl_column* columns,
+                 int32_t n_columns, const uint64_t* dest_bases,
+                 const int64_t* dest_offsets, int64_t gid_base, void* stream);
+
 /* Splitters of the multi-GPU ORDER BY (dist.choose_splitters_device; the
  * sample-sort step of SURVEY §8(e), ranges chosen on the composite
  * (key, global row id) order so stability survives duplicate-heavy keys).

@@ -67,6 +67,7 @@ SIGNATURES = {
     "rl_device_sm_count": (ctypes.c_int, []),
     "rl_launch_count": (_I64, []),
     "rl_push_rows": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _I32, _P, _P, _P]),
+    "rl_push_rows_gid": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _I32, _P, _P, _I64, _P]),
     "rl_sample_keys": (ctypes.c_int, [_P, _I64, _I32, _I64, _I32, _P, _P]),
     "rl_pick_splitters": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _P]),
     "rl_global_ids": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _P]),

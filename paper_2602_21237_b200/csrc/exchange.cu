@@ -35,8 +35,10 @@ struct PushArgs {
   const uint64_t* dest_bases;    // [parts][ncols + 1] base address of every column region (+ row ids) per dest
   const int64_t* dest_starts;    // [parts + 1] partition boundaries (device)
   const int64_t* dest_offsets;   // [parts] this source's first row in every destination's buffer
+  int64_t gid_base;              // this rank's first global row id (GID mode)
 };
 
+template <bool GID>  // GID: the last region receives int64 global row ids (gid_base + row), else u32 rows
 __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
   __shared__ int64_t starts[kMaxParts + 1];
   __shared__ int64_t offs[kMaxParts];
@@ -56,12 +58,14 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
       const int w = a.width[c];
       copy_row(static_cast<const uint8_t*>(a.src[c]) + uint64_t(row) * w, reinterpret_cast<uint8_t*>(b[c]) + o * w, w);
     }
-    reinterpret_cast<uint32_t*>(b[a.ncols])[o] = row;
+    if constexpr (GID) reinterpret_cast<int64_t*>(b[a.ncols])[o] = a.gid_base + int64_t(row);
+    else reinterpret_cast<uint32_t*>(b[a.ncols])[o] = row;
   }
 }
 
 int push_rows(const uint32_t* rows, int64_t n, int parts, const int64_t* dest_starts, const rl_column* columns,
-              int n_columns, const uint64_t* dest_bases, const int64_t* dest_offsets, cudaStream_t stream) {
+              int n_columns, const uint64_t* dest_bases, const int64_t* dest_offsets, cudaStream_t stream,
+              bool gid = false, int64_t gid_base = 0) {
   if (n < 0 || parts < 1 || parts > kMaxParts || n_columns < 0 || n_columns > kMaxCols) return RL_ERR_BAD_ARG;
   if (n > 0 && (!rows || !dest_starts || !dest_bases || !dest_offsets)) return RL_ERR_BAD_ARG;
   if (n_columns > 0 && !columns) return RL_ERR_BAD_ARG;
@@ -80,8 +84,10 @@ int push_rows(const uint32_t* rows, int64_t n, int parts, const int64_t* dest_st
   a.dest_bases = dest_bases;
   a.dest_starts = dest_starts;
   a.dest_offsets = dest_offsets;
+  a.gid_base = gid_base;
   const int grid = int(std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(device_sm_count()) * 8));
-  push_kernel<<<grid, kThreads, 0, stream>>>(a);
+  if (gid) push_kernel<true><<<grid, kThreads, 0, stream>>>(a);
+  else push_kernel<false><<<grid, kThreads, 0, stream>>>(a);
   count_launches(1);
   return rl_cuda_status(cudaGetLastError());
 }
@@ -172,6 +178,13 @@ RL_API int rl_push_rows(const uint32_t* rows, int64_t n, int32_t parts, const in
                         const int64_t* dest_offsets, void* stream) {
   return rl::exchange::push_rows(rows, n, parts, dest_starts, columns, n_columns, dest_bases, dest_offsets,
                                  static_cast<cudaStream_t>(stream));
+}
+
+RL_API int rl_push_rows_gid(const uint32_t* rows, int64_t n, int32_t parts, const int64_t* dest_starts,
+                            const rl_column* columns, int32_t n_columns, const uint64_t* dest_bases,
+                            const int64_t* dest_offsets, int64_t gid_base, void* stream) {
+  return rl::exchange::push_rows(rows, n, parts, dest_starts, columns, n_columns, dest_bases, dest_offsets,
+                                 static_cast<cudaStream_t>(stream), true, gid_base);
 }
 
 RL_API int rl_sample_keys(const int64_t* keys, int64_t n, int32_t per_rank, int64_t gid_base, int32_t descending,

@@ -86,17 +86,26 @@ class GpuOps:
         perm = engine.sort_permutation([engine.SortAxis(keys, descending)], keys.numel(), keys.device)
         return perm.to(torch.int64) & 0xFFFFFFFF
 
-    def push_exchange(self, slot: str, cols, rows, counts, group, base: int = 0):
-        """Partition gather + all-to-all in one kernel over peer memory
-        (PeerExchange); None when this group has no symmetric memory."""
-        dev = cols[0].device
+    def push_exchange_many(self, items, group):
+        """Partition gather + all-to-all in one kernel per exchange over peer
+        memory (PeerExchange), for every exchange of a step at once: items are
+        (slot, columns, partitioned rows, counts per destination, global row-id
+        base); ONE all-gather of all count vectors (one host sync). Returns, per
+        item, (received columns, their int64 global row ids, rows per source) —
+        or None when this group has no symmetric memory."""
+        if not items:
+            return []
+        dev = items[0][1][0].device
         if not _peer_exchange_ok(group, dev):
             return None
-        key = (slot, id(group), dev.index, tuple((c.dtype, tuple(c.shape[1:])) for c in cols))
         try:
-            if key not in _PEER:
-                _PEER[key] = PeerExchange(group, dev, cols)
-            return _PEER[key].exchange(cols, rows, counts, base)
+            exs = []
+            for slot, cols, _, _, _ in items:
+                key = (slot, id(group), dev.index, tuple((c.dtype, tuple(c.shape[1:])) for c in cols))
+                if key not in _PEER:
+                    _PEER[key] = PeerExchange(group, dev, cols)
+                exs.append(_PEER[key])
+            return PeerExchange.exchange_many(exs, items, group)
         except (RuntimeError, ImportError, AttributeError):
             _PEER[("ok", dev.index)] = False  # no symmetric memory here: NCCL from now on
             return None
@@ -170,7 +179,7 @@ class PeerExchange:
 
         cap = max(rows, self.cap + self.cap // 4, 1024)
         offs, total = [], 0
-        for _, _, w in self.likes + [(None, None, 4)]:  # + the local row ids
+        for _, _, w in self.likes + [(None, None, 8)]:  # + the int64 global row ids
             offs.append(total)
             total += (cap * w + 255) // 256 * 256
         self.buf = sm.empty(total, dtype=torch.uint8, device=self.device)
@@ -181,38 +190,40 @@ class PeerExchange:
         self.bases = torch.tensor(table, dtype=torch.int64).view(-1).to(self.device)
         self.offs, self.cap = offs, cap
 
-    def exchange(self, cols: Sequence[torch.Tensor], rows: torch.Tensor, counts: torch.Tensor, base: int = 0):
-        """Returns (received columns, received local row ids, rows per source,
-        every source's row-id base) — the bases ride on the counts gather."""
+    @staticmethod
+    def exchange_many(exs, items, group):
+        """One all-gather of every item's counts, then each item's push between
+        two symmetric-memory barriers (see GpuOps.push_exchange_many)."""
         from . import _capi as C
         from . import engine
 
-        p, me = self.p, self.me
-        mine = torch.empty(p + 1, dtype=torch.int64, device=self.device)
-        mine[:p] = counts.to(torch.int64).reshape(p)
-        mine[p] = base
-        gathered = torch.empty(p * (p + 1), dtype=torch.int64, device=self.device)
-        dist.all_gather_into_tensor(gathered, mine, group=self.group)
-        host = gathered.cpu().view(p, p + 1)  # the step's one host sync
-        mat, bases = host[:, :p], host[:, p].tolist()  # mat[s][d]: rows s sends to d
-        self._ensure(int(mat.sum(0).max()))
-        recv_counts = mat[:, me].tolist()
-        total = sum(recv_counts)
-        starts = torch.zeros(p + 1, dtype=torch.int64, device=self.device)
-        torch.cumsum(counts.to(torch.int64).reshape(p), 0, out=starts[1:])
-        offs = torch.tensor([int(mat[:me, d].sum()) for d in range(p)], dtype=torch.int64).to(self.device)
-        arr, ncols = C.columns_array((c.contiguous().data_ptr(), 0, w, C.RL_SIDE_LEFT)
-                                     for c, (_, _, w) in zip(cols, self.likes))
-        self.hdl.barrier()  # every rank is done with its previous receive
-        C.check(C.load().rl_push_rows(engine._ptr(rows), rows.numel(), p, engine._ptr(starts), arr, ncols,
-                                      engine._ptr(self.bases), engine._ptr(offs), engine.stream_handle()),
-                "rl_push_rows")
-        self.hdl.barrier()  # every push into this rank has landed
-        out = []
-        for (dt, tail, w), o in zip(self.likes, self.offs):
-            out.append(self.buf[o:o + total * w].view(dt).view((total,) + tail))
-        recv_rows = self.buf[self.offs[-1]:self.offs[-1] + total * 4].view(torch.int32)
-        return out, recv_rows, recv_counts, bases
+        p, me = exs[0].p, exs[0].me
+        dev = exs[0].device
+        mine = torch.cat([it[3].to(torch.int64).reshape(p) for it in items])
+        gathered = torch.empty(p * mine.numel(), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(gathered, mine, group=group)
+        host = gathered.cpu().view(p, len(items), p)  # the step's one host sync; host[s][i][d]
+        lib = C.load()
+        out_all = []
+        for i, (ex, (_, cols, rows, counts, base)) in enumerate(zip(exs, items)):
+            mat = host[:, i, :]  # mat[s][d]: rows s sends to d
+            ex._ensure(int(mat.sum(0).max()))
+            recv_counts = mat[:, me].tolist()
+            total = sum(recv_counts)
+            starts = torch.zeros(p + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(counts.to(torch.int64).reshape(p), 0, out=starts[1:])
+            offs = torch.tensor([int(mat[:me, d].sum()) for d in range(p)], dtype=torch.int64).to(dev)
+            arr, ncols = C.columns_array((c.contiguous().data_ptr(), 0, w, C.RL_SIDE_LEFT)
+                                         for c, (_, _, w) in zip(cols, ex.likes))
+            ex.hdl.barrier()  # every rank is done with its previous receive
+            C.check(lib.rl_push_rows_gid(engine._ptr(rows), rows.numel(), p, engine._ptr(starts), arr, ncols,
+                                         engine._ptr(ex.bases), engine._ptr(offs), int(base), engine.stream_handle()),
+                    "rl_push_rows_gid")
+            ex.hdl.barrier()  # every push into this rank has landed
+            out = [ex.buf[o:o + total * w].view(dt).view((total,) + tail) for (dt, tail, w), o in zip(ex.likes, ex.offs)]
+            gids = ex.buf[ex.offs[-1]:ex.offs[-1] + total * 8].view(torch.int64)
+            out_all.append((out, gids, recv_counts))
+        return out_all
 
 
 _PEER: dict = {}
@@ -346,20 +357,23 @@ def distributed_join(left: Sequence[torch.Tensor], left_key: int, left_base: int
     p = _group_size(group)
     dev = left[left_key].device
 
-    def shuffle(cols, key_idx, base, slot):
-        if hasattr(ops, "push_exchange"):
-            rows, counts = ops.hash_partition(cols[key_idx], p, seed)
-            pushed = ops.push_exchange(slot, list(cols), rows, counts, group, base)
-            if pushed is not None:
-                rcols, rrows, rc, bases = pushed
-                return rcols, _global_ids(rrows, rc, bases)
+    def shuffle(cols, key_idx, base):
         bases = _all_bases(base, dev, group)
         rows, counts, moved = _partition_take(ops, "hash", cols[key_idx], list(cols), parts=p, seed=seed)
         recv, rc = exchange(moved + [rows], counts, group, with_counts=True)
         return recv[:-1], _global_ids(recv[-1], rc, bases)
 
-    lcols, lgids = shuffle(list(left), left_key, left_base, "join_left")
-    rcols, rgids = shuffle(list(right), right_key, right_base, "join_right")
+    pushed = None
+    if hasattr(ops, "push_exchange_many"):  # both sides' counts in one all-gather, global ids from the senders
+        rl_, cl = ops.hash_partition(left[left_key], p, seed)
+        rr_, cr = ops.hash_partition(right[right_key], p, seed)
+        pushed = ops.push_exchange_many([("join_left", list(left), rl_, cl, left_base),
+                                         ("join_right", list(right), rr_, cr, right_base)], group)
+    if pushed is not None:
+        (lcols, lgids, _), (rcols, rgids, _) = pushed
+    else:
+        lcols, lgids = shuffle(list(left), left_key, left_base)
+        rcols, rgids = shuffle(list(right), right_key, right_base)
     if hasattr(ops, "local_join"):
         out, lg, rg = ops.local_join(lcols, left_key, rcols, right_key, lgids, rgids)
     else:
@@ -468,14 +482,13 @@ def distributed_sort(cols: Sequence[torch.Tensor], key_idx: int, gid_base: int, 
     ops = ops or GpuOps()
     keys = cols[key_idx]
     pushed = None
-    if hasattr(ops, "push_exchange") and keys.device.type == "cuda" and _peer_exchange_ok(group, keys.device):
-        # device-side splitters (no host sync); the bases ride on the count exchange
+    if hasattr(ops, "push_exchange_many") and keys.device.type == "cuda" and _peer_exchange_ok(group, keys.device):
+        # device-side splitters (no host sync); global row ids written by the senders
         split_k, split_g = choose_splitters_device(keys, gid_base, descending, group)
         rows, counts = ops.range_partition(keys, gid_base, split_k, split_g, descending)
-        pushed = ops.push_exchange("sort", list(cols), rows, counts, group, gid_base)
+        pushed = ops.push_exchange_many([("sort", list(cols), rows, counts, gid_base)], group)
     if pushed is not None:
-        rcols, rrows, rc, bases = pushed
-        rgids = _global_ids(rrows, rc, bases)
+        rcols, rgids, _ = pushed[0]
     else:
         split_k, split_g, bases = choose_splitters(keys, gid_base, descending, group, with_bases=True)
         rows, counts, moved = _partition_take(ops, "range", keys, list(cols), gid_base=gid_base, split_keys=split_k,

@@ -59,12 +59,14 @@ def test_distributed_sort_on_device(nccl_world1):
     assert (res.columns[0].cpu().numpy() == keys[want]).all()
 
 
-def test_push_rows_emulated_ranks():
+@pytest.mark.parametrize("gid", [False, True])
+def test_push_rows_emulated_ranks(gid):
     """rl_push_rows for P logical ranks on one GPU (each rank's receive
     buffers are separate allocations; ranks push one after another, none
     waits on another): every destination receives source blocks in rank
     order, each in stable partition order, with the local row ids — the
-    all-to-all-v contract."""
+    all-to-all-v contract. rl_push_rows_gid
+    delivers int64 global row ids (the sender's base + its local row id)."""
     import ctypes
 
     from paper_2602_21237_b200 import _capi as C
@@ -82,9 +84,10 @@ def test_push_rows_emulated_ranks():
         parts.append((rows, counts.cpu().numpy()))
     mat = np.stack([c for _, c in parts])  # mat[s][d]
     recv = mat.sum(0)
+    gbase = [10**11, 7, 2**40]  # the senders' first global row ids
     bufs = [(torch.empty(max(r, 1), dtype=torch.int64, device="cuda"),
              torch.empty((max(r, 1), 12), dtype=torch.uint8, device="cuda"),
-             torch.empty(max(r, 1), dtype=torch.int32, device="cuda")) for r in recv]
+             torch.empty(max(r, 1), dtype=torch.int64 if gid else torch.int32, device="cuda")) for r in recv]
     table = torch.tensor([[b[0].data_ptr(), b[1].data_ptr(), b[2].data_ptr()] for b in bufs],
                          dtype=torch.int64).view(-1).cuda()
     for s in range(P):
@@ -93,9 +96,15 @@ def test_push_rows_emulated_ranks():
         starts = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int64).cuda()
         offs = torch.tensor([int(mat[:s, d].sum()) for d in range(P)], dtype=torch.int64).cuda()
         arr, ncols = C.columns_array([(kd.data_ptr(), 0, 8, C.RL_SIDE_LEFT), (pd.data_ptr(), 0, 12, C.RL_SIDE_LEFT)])
-        C.check(lib.rl_push_rows(ctypes.c_void_p(rows.data_ptr()), rows.numel(), P,
-                                 ctypes.c_void_p(starts.data_ptr()), arr, ncols, ctypes.c_void_p(table.data_ptr()),
-                                 ctypes.c_void_p(offs.data_ptr()), engine.stream_handle()), "rl_push_rows")
+        if gid:
+            C.check(lib.rl_push_rows_gid(ctypes.c_void_p(rows.data_ptr()), rows.numel(), P,
+                                         ctypes.c_void_p(starts.data_ptr()), arr, ncols,
+                                         ctypes.c_void_p(table.data_ptr()), ctypes.c_void_p(offs.data_ptr()),
+                                         gbase[s], engine.stream_handle()), "rl_push_rows_gid")
+        else:
+            C.check(lib.rl_push_rows(ctypes.c_void_p(rows.data_ptr()), rows.numel(), P,
+                                     ctypes.c_void_p(starts.data_ptr()), arr, ncols, ctypes.c_void_p(table.data_ptr()),
+                                     ctypes.c_void_p(offs.data_ptr()), engine.stream_handle()), "rl_push_rows")
     torch.cuda.synchronize()
     for d in range(P):
         want_rows = [np.flatnonzero(O.fmix64(keys[s].view(np.uint64) ^ np.uint64(O.fmix64_scalar(77)))
@@ -106,7 +115,11 @@ def test_push_rows_emulated_ranks():
         n = int(recv[d])
         assert (bufs[d][0][:n].cpu().numpy() == wk).all()
         assert (bufs[d][1][:n].cpu().numpy() == wp).all()
-        assert (bufs[d][2][:n].cpu().numpy().view(np.uint32) == wr).all()
+        if gid:
+            wg = np.concatenate([r.astype(np.int64) + gbase[s] for s, r in enumerate(want_rows)])
+            assert (bufs[d][2][:n].cpu().numpy() == wg).all()
+        else:
+            assert (bufs[d][2][:n].cpu().numpy().view(np.uint32) == wr).all()
 
 
 def test_distributed_ops_take_the_peer_push(nccl_world1, monkeypatch):

@@ -108,6 +108,7 @@ constexpr int kScatThreads = 1024;                 // histogram kernel: one CTA 
 constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
 constexpr int kMaxChunks = 160;
 constexpr int kHistReps = 8;                       // digit-histogram replicas: no grid-deep same-address atomics
+constexpr int kShiftCtas = 64;                     // key-sampling CTAs of the scatter path
 constexpr int kD7Reps = 8;                         // digit-7 count replicas: no 148-deep same-address atomics
 constexpr int64_t kScatterMinRows = int64_t(1) << 22;  // below: the histogram kernel counts every digit at once
 constexpr int64_t kChunkMinRows = 32768;            // small inputs: fewer chunk histograms (128 KB each)
@@ -182,7 +183,7 @@ struct SortArgs {
   uint32_t* grid_bar;        // grid barrier arrivals
   uint32_t* flags;           // [0] LSD fallback (a sub-bucket exceeds kLocalCap, ...), [1] local work-item counter,
                              // [3] scatter path: pass-B tile counter,
-                             // [4..5] raw int64 keys: OR of (key ^ first key) = the varying bits (u64)
+                             // [4..5] raw int64 keys: OR of (key ^ first key) = the varying bits (u64),
   uint32_t* sub_off;         // [kSubBuckets + 1] sub-bucket starts, hybrid (not zeroed)
   uint64_t* status;          // [num_tiles][kBins] look-back words (epoch = pass + 1)
   unsigned long long* stamps;  // optional [kStamps] globaltimer ns (device)
@@ -723,6 +724,60 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // the local phase — or, on the fallback flag (a sub-bucket above kLocalCap, a
 // wrapped chunk counter, < 4 varying digits), the LSD passes from the input.
 
+// Key normalisation of the scatter path: the leading key bits that do not
+// vary (estimated from a sample by key_shift_kernel, checked by the chunk
+// counts) are shifted out, so the sub-buckets are the top 16 VARYING bits;
+// the order is unchanged since every key shares the dropped prefix.
+// Computed once per CTA (thread 0; every thread calls it — it holds a
+// barrier — and gets the result from `slot`).
+__device__ __forceinline__ uint32_t key_shift(const SortArgs& a, uint32_t* slot) {
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      const uint64_t vv = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 6));  // sampled varying bits
+      uint32_t sh = vv ? uint32_t(__clzll((long long)vv)) : 0u;
+      // the local phase splits sub-buckets by the next 8 bits: they must vary
+      // too (e.g. not a composite key with a constant middle), else no shift
+      if (sh && ((vv << sh) >> 40 & 0xFFull) == 0) sh = 0;
+      *slot = sh;
+    }
+  }
+  __syncthreads();
+  return *slot;
+}
+__device__ __forceinline__ uint64_t key_prefix(const SortArgs& a, uint32_t sh) {
+  const uint64_t u0 = xform(uint64_t(__ldg(static_cast<const long long*>(a.col))), a.desc);
+  return sh ? (u0 & ~(~0ull >> sh)) : 0ull;
+}
+
+// OR of (sample ^ first key) over 16384 strided keys into flags[6..7]
+// (kShiftCtas CTAs, one atomic each).
+__global__ void __launch_bounds__(256) key_shift_kernel(SortArgs a) {
+  const long long* col = static_cast<const long long*>(a.col);
+  const uint64_t u0 = xform(uint64_t(__ldg(col)), a.desc);
+  constexpr int kSamples = 16384;  // (a varying bit the sample misses is caught by the chunk counts)
+  pdl_launch_dependents();        // the chunk counts zero their histogram meanwhile
+  uint64_t v = 0;
+#pragma unroll
+  for (int q = 0; q < kSamples / (kShiftCtas * 256); ++q) {
+    const int i = (q * kShiftCtas + blockIdx.x) * 256 + threadIdx.x;
+    v |= xform(uint64_t(__ldg(col + int64_t(i) * a.n / kSamples)), a.desc) ^ u0;
+  }
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, uint32_t(v >> 32));
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, uint32_t(v));
+  __shared__ uint32_t part[16];
+  if ((threadIdx.x & 31) == 0) {
+    part[2 * (threadIdx.x >> 5)] = hi;
+    part[2 * (threadIdx.x >> 5) + 1] = lo;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const uint32_t h = __reduce_or_sync(0xffffffffu, threadIdx.x < 8 ? part[2 * threadIdx.x] : 0u);
+    const uint32_t l = __reduce_or_sync(0xffffffffu, threadIdx.x < 8 ? part[2 * threadIdx.x + 1] : 0u);
+    const uint64_t vv = (uint64_t(h) << 32) | l;
+    if (threadIdx.x == 0 && vv) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 6), vv);
+  }
+}
+
 // The fallback flag, read ONCE per CTA: other CTAs of the same kernel may
 // set it meanwhile, and a per-thread read could split the CTA at a barrier.
 __device__ __forceinline__ bool fallback_flag(const SortArgs& a) {
@@ -836,6 +891,7 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
   pdl_launch_dependents();
   for (int i = tid; i < kScatWords / 4; i += kScatThreads) reinterpret_cast<uint4*>(w)[i] = make_uint4(0, 0, 0, 0);
+  pdl_wait();  // the key sample (launched as its programmatic dependent)
   __syncthreads();
 #ifdef RL_K1_PROFILE
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[4] = globaltimer();
@@ -843,10 +899,11 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   const int64_t lo = chunk_lo(a.n, a.chunks, blockIdx.x), hi = chunk_lo(a.n, a.chunks, blockIdx.x + 1);
   const long long* col = static_cast<const long long*>(a.col);
   const uint64_t k0 = xform(uint64_t(__ldg(col)), a.desc);
+  const uint32_t sh = key_shift(a, red + kScatThreads - 1);
   uint64_t vary = 0;
   auto count = [&](uint64_t u) {  // a wrapped 16-bit counter shows up in the chunk total below
     vary |= u ^ k0;
-    const uint32_t b = uint32_t(u >> 48);
+    const uint32_t b = uint32_t((u << sh) >> 48);
     atomicAdd(&w[b >> 1], 1u << ((b & 1u) << 4));
   };
   const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(col);
@@ -895,7 +952,9 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   if (warp == 0) {
     const uint32_t h2 = __reduce_or_sync(0xffffffffu, red[2 * lane]);
     const uint32_t l2 = __reduce_or_sync(0xffffffffu, red[2 * lane + 1]);
-    if (lane == 0 && (h2 | l2)) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), (uint64_t(h2) << 32) | l2);
+    const uint64_t v2 = (uint64_t(h2) << 32) | l2;
+    if (lane == 0 && v2) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), v2);
+    if (lane == 0 && sh && (v2 & ~(~0ull >> sh))) atomicOr(a.flags, 1u);  // the sample missed a varying bit: LSD
   }
 #ifdef RL_K1_PROFILE
   __syncthreads();
@@ -1016,13 +1075,14 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   // this CTA's rows by digit 7 -> keys_b / vals_b
   const int64_t lo = chunk_lo(a.n, gridDim.x, blockIdx.x), hi = chunk_lo(a.n, gridDim.x, blockIdx.x + 1);
   const long long* col = static_cast<const long long*>(a.col);
+  const uint32_t sh = key_shift(a, s.scratch + 50);
   auto reserve = [&](uint32_t d, uint32_t c) { return s.aux[d] + atomicAdd(a.cur7 + d, c); };
   auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int64_t t0) {
     const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
 #pragma unroll
     for (int u = 0; u < kPItems; ++u) {
       const int j = u * kPThreads + tid;
-      k[u] = j < tn ? xform(uint64_t(__ldcs(col + t0 + j)), a.desc) : 0ull;
+      k[u] = j < tn ? xform(uint64_t(__ldcs(col + t0 + j)), a.desc) << sh : 0ull;
       v[u] = uint32_t(t0 + j);
     }
   };
@@ -1159,7 +1219,7 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
 }
 
 template <int THREADS>
-__device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
+__device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src, uint32_t sh = 0, uint64_t prefix = 0) {
   constexpr int kLWarps = THREADS / 32;
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
   uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
@@ -1328,7 +1388,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     constexpr uint32_t kRankMax = 32;
     auto emit = [&](uint32_t p, uint64_t key, uint32_t v) {
       const uint64_t o = uint64_t(base) + p;
-      if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(key, desc));
+      if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform((key >> sh) | prefix, desc));
       __stcs(a.out_vals + o, v);
       gather_fused(a.gather, v, o);
     };
@@ -1423,7 +1483,8 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   pdl_launch_dependents();
   if (stamper) a.stamps[1] = globaltimer();
   if (*reinterpret_cast<volatile const uint32_t*>(a.flags)) return;  // final before this launch: uniform
-  local_phase<kLocalThreads>(a, smem, 1);
+  const uint32_t sh = key_shift(a, reinterpret_cast<uint32_t*>(smem + kLocMisc) + 127);  // (a misc slot the phase leaves alone)
+  local_phase<kLocalThreads>(a, smem, 1, sh, key_prefix(a, sh));
   if (stamper) {
     a.stamps[kStamps - 2] = globaltimer();
     a.stamps[kStamps - 1] = 3;
@@ -1808,10 +1869,8 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
       cudaMemcpy(fl, L.flags, sizeof(fl), cudaMemcpyDeviceToHost);
       fprintf(stderr, "[scatter-debug] %s: %s flags=%u,%u,%u,%u\n", what, cudaGetErrorString(x), fl[0], fl[1], fl[2], fl[3]);
     };
-    sub_hist_kernel<<<chunks, kScatThreads, kHistSmem, stream>>>(a);
-    chk("sub_hist");
-    // the next three launches may be scheduled early (programmatic dependent
-    // launch); each waits on the device for its predecessor's results
+    // the launches after the key sample may be scheduled early (programmatic
+    // dependent launch); each waits on the device for its predecessor's results
     auto launch_dep = [&](auto kernel, int g, int threads, size_t smem) {
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1825,6 +1884,9 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
       cfg.numAttrs = 1;
       return cudaLaunchKernelEx(&cfg, kernel, a);
     };
+    key_shift_kernel<<<kShiftCtas, 256, 0, stream>>>(a);
+    if ((e = launch_dep(sub_hist_kernel, chunks, kScatThreads, kHistSmem)) != cudaSuccess) return rl_cuda_status(e);
+    chk("sub_hist");
     if ((e = launch_dep(top_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
     chk("top_scatter");
     if ((e = launch_dep(sub_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
@@ -1834,7 +1896,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
     e = launch_sort_kernel(a, grid, stream);  // returns at once unless the fallback flag is set
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
-    count_launches(5);
+    count_launches(6);
     return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
   }
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);

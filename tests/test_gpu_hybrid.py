@@ -209,3 +209,25 @@ def test_split_digit7_buckets(tops):
     keys = (hi << np.int64(56)) | rng.integers(0, 1 << 56, n, dtype=np.int64)
     check_sort(keys)
     check_sort(keys, True)
+
+
+@pytest.mark.parametrize("bits,n", [(27, 5_000_000), (33, 4_500_000), (40, 6_000_000)])
+def test_scatter_narrow_keys_shifted(bits, n):
+    """Keys with constant leading bits (row-id-like, in [0, 2^bits) plus an
+    offset and negatives): the scatter path shifts the constant prefix out
+    (top 16 VARYING bits as sub-buckets) and restores it on output."""
+    rng = np.random.default_rng(40 + bits)
+    keys = rng.integers(0, 1 << bits, n, dtype=np.int64) - (1 << (bits - 1)) + 123_456_789
+    keys[rng.choice(n, n // 50, replace=False)] = keys[rng.integers(0, n, n // 50)]  # duplicates
+    check_sort(keys)
+    check_sort(keys, True)
+
+
+def test_scatter_shift_missed_by_sample():
+    """A single key varying in a high bit the sample does not see: the chunk
+    counts catch it and the LSD passes produce the (identical) result."""
+    rng = np.random.default_rng(44)
+    n = 6_000_001
+    keys = rng.integers(0, 1 << 30, n, dtype=np.int64)
+    keys[3] = np.int64(1) << 50  # not at a sampled position
+    check_sort(keys)

@@ -108,7 +108,6 @@ constexpr int kScatThreads = 1024;                 // histogram kernel: one CTA 
 constexpr int kScatWords = (1 << 16) / 2;          // sub-bucket counters, packed u16 pairs
 constexpr int kMaxChunks = 160;
 constexpr int kHistReps = 8;                       // digit-histogram replicas: no grid-deep same-address atomics
-constexpr int kShiftCtas = 64;                     // key-sampling CTAs of the scatter path
 constexpr int kD7Reps = 8;                         // digit-7 count replicas: no 148-deep same-address atomics
 constexpr int64_t kScatterMinRows = int64_t(1) << 22;  // below: the histogram kernel counts every digit at once
 constexpr int64_t kChunkMinRows = 32768;            // small inputs: fewer chunk histograms (128 KB each)
@@ -725,57 +724,21 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // wrapped chunk counter, < 4 varying digits), the LSD passes from the input.
 
 // Key normalisation of the scatter path: the leading key bits that do not
-// vary (estimated from a sample by key_shift_kernel, checked by the chunk
-// counts) are shifted out, so the sub-buckets are the top 16 VARYING bits;
+// vary (estimated from a sample at the start of the chunk counts, checked by
+// them against every key) are shifted out, so the sub-buckets are the top 16 VARYING bits;
 // the order is unchanged since every key shares the dropped prefix.
-// Computed once per CTA (thread 0; every thread calls it — it holds a
-// barrier — and gets the result from `slot`).
-__device__ __forceinline__ uint32_t key_shift(const SortArgs& a, uint32_t* slot) {
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      const uint64_t vv = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 6));  // sampled varying bits
-      uint32_t sh = vv ? uint32_t(__clzll((long long)vv)) : 0u;
-      // the local phase splits sub-buckets by the next 8 bits: they must vary
-      // too (e.g. not a composite key with a constant middle), else no shift
-      if (sh && ((vv << sh) >> 40 & 0xFFull) == 0) sh = 0;
-      *slot = sh;
-    }
-  }
-  __syncthreads();
-  return *slot;
+// The shift for a sampled varying-bit word: its leading zeros, unless the
+// 8 bits below the top 16 varying bits are constant (the local phase splits
+// sub-buckets by them: e.g. a composite key with a constant middle).
+__device__ __forceinline__ uint32_t shift_of(uint64_t vv) {
+  uint32_t sh = vv ? uint32_t(__clzll((long long)vv)) : 0u;
+  if (sh && ((vv << sh) >> 40 & 0xFFull) == 0) sh = 0;
+  return sh;
 }
+
 __device__ __forceinline__ uint64_t key_prefix(const SortArgs& a, uint32_t sh) {
   const uint64_t u0 = xform(uint64_t(__ldg(static_cast<const long long*>(a.col))), a.desc);
   return sh ? (u0 & ~(~0ull >> sh)) : 0ull;
-}
-
-// OR of (sample ^ first key) over 16384 strided keys into flags[6..7]
-// (kShiftCtas CTAs, one atomic each).
-__global__ void __launch_bounds__(256) key_shift_kernel(SortArgs a) {
-  const long long* col = static_cast<const long long*>(a.col);
-  const uint64_t u0 = xform(uint64_t(__ldg(col)), a.desc);
-  constexpr int kSamples = 16384;  // (a varying bit the sample misses is caught by the chunk counts)
-  pdl_launch_dependents();        // the chunk counts zero their histogram meanwhile
-  uint64_t v = 0;
-#pragma unroll
-  for (int q = 0; q < kSamples / (kShiftCtas * 256); ++q) {
-    const int i = (q * kShiftCtas + blockIdx.x) * 256 + threadIdx.x;
-    v |= xform(uint64_t(__ldg(col + int64_t(i) * a.n / kSamples)), a.desc) ^ u0;
-  }
-  const uint32_t hi = __reduce_or_sync(0xffffffffu, uint32_t(v >> 32));
-  const uint32_t lo = __reduce_or_sync(0xffffffffu, uint32_t(v));
-  __shared__ uint32_t part[16];
-  if ((threadIdx.x & 31) == 0) {
-    part[2 * (threadIdx.x >> 5)] = hi;
-    part[2 * (threadIdx.x >> 5) + 1] = lo;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const uint32_t h = __reduce_or_sync(0xffffffffu, threadIdx.x < 8 ? part[2 * threadIdx.x] : 0u);
-    const uint32_t l = __reduce_or_sync(0xffffffffu, threadIdx.x < 8 ? part[2 * threadIdx.x + 1] : 0u);
-    const uint64_t vv = (uint64_t(h) << 32) | l;
-    if (threadIdx.x == 0 && vv) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 6), vv);
-  }
 }
 
 // The fallback flag, read ONCE per CTA: other CTAs of the same kernel may
@@ -890,8 +853,10 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
   pdl_launch_dependents();
+  // this thread's key sample, in flight while the histogram is zeroed
+  const long long sample = __ldg(static_cast<const long long*>(a.col) + int64_t(tid) * a.n / kScatThreads);
   for (int i = tid; i < kScatWords / 4; i += kScatThreads) reinterpret_cast<uint4*>(w)[i] = make_uint4(0, 0, 0, 0);
-  pdl_wait();  // the key sample (launched as its programmatic dependent)
+  if (tid < 2) red[kScatThreads - 4 + tid] = 0u;  // the sample's varying-bit OR
   __syncthreads();
 #ifdef RL_K1_PROFILE
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[4] = globaltimer();
@@ -899,7 +864,20 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   const int64_t lo = chunk_lo(a.n, a.chunks, blockIdx.x), hi = chunk_lo(a.n, a.chunks, blockIdx.x + 1);
   const long long* col = static_cast<const long long*>(a.col);
   const uint64_t k0 = xform(uint64_t(__ldg(col)), a.desc);
-  const uint32_t sh = key_shift(a, red + kScatThreads - 1);
+  uint32_t sh;
+  {  // the key shift from 1024 strided samples — the same in every CTA (mostly L2
+     // hits); a varying bit they miss is caught by the full check below (-> LSD)
+    const uint64_t v = xform(uint64_t(sample), a.desc) ^ k0;
+    const uint32_t vh = __reduce_or_sync(0xffffffffu, uint32_t(v >> 32));
+    const uint32_t vl = __reduce_or_sync(0xffffffffu, uint32_t(v));
+    if (lane == 0) {  // (red[1020..1021] zeroed with the histogram)
+      atomicOr(&red[kScatThreads - 4], vh);
+      atomicOr(&red[kScatThreads - 3], vl);
+    }
+    __syncthreads();
+    sh = shift_of((uint64_t(red[kScatThreads - 4]) << 32) | red[kScatThreads - 3]);
+    if (blockIdx.x == 0 && tid == 0) a.flags[6] = sh;  // for the later kernels
+  }
   uint64_t vary = 0;
   auto count = [&](uint64_t u) {  // a wrapped 16-bit counter shows up in the chunk total below
     vary |= u ^ k0;
@@ -1001,6 +979,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   pdl_wait();  // the chunk counts
   pdl_launch_dependents();
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[2] = globaltimer();
+  if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);  // the key shift, read after the prologue's barriers
   if (fallback_flag(a)) return;  // a chunk counter wrapped: LSD
   // digit-7 bucket starts (every CTA)
   uint32_t t7 = 0;
@@ -1075,7 +1054,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   // this CTA's rows by digit 7 -> keys_b / vals_b
   const int64_t lo = chunk_lo(a.n, gridDim.x, blockIdx.x), hi = chunk_lo(a.n, gridDim.x, blockIdx.x + 1);
   const long long* col = static_cast<const long long*>(a.col);
-  const uint32_t sh = key_shift(a, s.scratch + 50);
+  const uint32_t sh = s.scratch[50];
   auto reserve = [&](uint32_t d, uint32_t c) { return s.aux[d] + atomicAdd(a.cur7 + d, c); };
   auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int64_t t0) {
     const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
@@ -1219,7 +1198,7 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
 }
 
 template <int THREADS>
-__device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src, uint32_t sh = 0, uint64_t prefix = 0) {
+__device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src, bool shifted = false) {
   constexpr int kLWarps = THREADS / 32;
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
   uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
@@ -1254,6 +1233,9 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src, uint
     __syncwarp();
   }
   __syncthreads();
+  // the scatter path's key shift and prefix (staged in misc[125..127] by the caller)
+  const uint32_t sh = shifted ? misc[125] : 0u;
+  const uint64_t prefix = shifted ? (uint64_t(misc[127]) << 32) | misc[126] : 0ull;
   // run cursor: group k (g = g0 + k gstep), run r of that group; identical in every thread
   uint32_t k = 0, r = 0, buf = 0, phase0 = 0, phase1 = 0;
   bool have = misc[2] > 0;
@@ -1483,8 +1465,15 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   pdl_launch_dependents();
   if (stamper) a.stamps[1] = globaltimer();
   if (*reinterpret_cast<volatile const uint32_t*>(a.flags)) return;  // final before this launch: uniform
-  const uint32_t sh = key_shift(a, reinterpret_cast<uint32_t*>(smem + kLocMisc) + 127);  // (a misc slot the phase leaves alone)
-  local_phase<kLocalThreads>(a, smem, 1, sh, key_prefix(a, sh));
+  if (threadIdx.x == 0) {  // key shift and prefix, read by the local phase after its first barrier
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
+    const uint32_t sh = __ldcg(a.flags + 6);
+    const uint64_t prefix = key_prefix(a, sh);
+    misc[125] = sh;
+    misc[126] = uint32_t(prefix);
+    misc[127] = uint32_t(prefix >> 32);
+  }
+  local_phase<kLocalThreads>(a, smem, 1, true);
   if (stamper) {
     a.stamps[kStamps - 2] = globaltimer();
     a.stamps[kStamps - 1] = 3;
@@ -1884,8 +1873,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
       cfg.numAttrs = 1;
       return cudaLaunchKernelEx(&cfg, kernel, a);
     };
-    key_shift_kernel<<<kShiftCtas, 256, 0, stream>>>(a);
-    if ((e = launch_dep(sub_hist_kernel, chunks, kScatThreads, kHistSmem)) != cudaSuccess) return rl_cuda_status(e);
+    sub_hist_kernel<<<chunks, kScatThreads, kHistSmem, stream>>>(a);
     chk("sub_hist");
     if ((e = launch_dep(top_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
     chk("top_scatter");
@@ -1896,7 +1884,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
     e = launch_sort_kernel(a, grid, stream);  // returns at once unless the fallback flag is set
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
-    count_launches(6);
+    count_launches(5);
     return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
   }
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);

@@ -53,6 +53,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -723,22 +724,74 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // the local phase — or, on the fallback flag (a sub-bucket above kLocalCap, a
 // wrapped chunk counter, < 4 varying digits), the LSD passes from the input.
 
-// Key normalisation of the scatter path: the leading key bits that do not
-// vary (estimated from a sample at the start of the chunk counts, checked by
-// them against every key) are shifted out, so the sub-buckets are the top 16 VARYING bits;
-// the order is unchanged since every key shares the dropped prefix.
-// The shift for a sampled varying-bit word: its leading zeros, unless the
-// 8 bits below the top 16 varying bits are constant (the local phase splits
-// sub-buckets by them: e.g. a composite key with a constant middle).
-__device__ __forceinline__ uint32_t shift_of(uint64_t vv) {
-  uint32_t sh = vv ? uint32_t(__clzll((long long)vv)) : 0u;
-  if (sh && ((vv << sh) >> 40 & 0xFFull) == 0) sh = 0;
-  return sh;
+// Key normalisation of the scatter path: the key bits that do not vary
+// (estimated from a sample at the start of the chunk counts, checked by them
+// against every key) are squeezed out — the varying bits, up to two runs of
+// them, are packed left-aligned, high run first — so the sub-buckets are the
+// top 16 VARYING bits (row-id-like keys, composite keys with a constant
+// middle, keys with constant low bits). Order is unchanged: every key shares
+// the dropped bits. The local phase puts the bits back when it writes keys.
+// Pack code: bit 28 valid, then (lo, len) of the high run and of the low run
+// (len 0: one run), 7 bits each; 0 = keys used as they are.
+__device__ __forceinline__ uint64_t low_mask(uint32_t len) { return len >= 64 ? ~0ull : (1ull << len) - 1; }
+__device__ __forceinline__ uint32_t pack_code_of(uint64_t vv) {
+  if (vv == 0) return 0u;
+  const uint32_t hi1 = 63u - uint32_t(__clzll((long long)vv));
+  const uint64_t z1 = ~vv & low_mask(hi1);  // zero bits below the top varying bit
+  const uint32_t lo1 = z1 ? 64u - uint32_t(__clzll((long long)z1)) : 0u;
+  const uint32_t len1 = hi1 - lo1 + 1;
+  const uint64_t rest = vv & low_mask(lo1);
+  uint32_t lo2 = 0, len2 = 0;
+  if (rest) {
+    const uint32_t hi2 = 63u - uint32_t(__clzll((long long)rest));
+    const uint64_t z2 = ~rest & low_mask(hi2);
+    lo2 = z2 ? 64u - uint32_t(__clzll((long long)z2)) : 0u;
+    len2 = hi2 - lo2 + 1;
+    if (rest & low_mask(lo2)) return 0u;  // three or more runs: keys used as they are
+  }
+  if (len1 + len2 >= 64) return 0u;       // every bit varies
+  return (1u << 28) | (lo1 << 21) | (len1 << 14) | (lo2 << 7) | len2;
+}
+__device__ __forceinline__ uint64_t pack_mask(uint32_t c) {
+  if (!(c >> 28)) return ~0ull;
+  const uint32_t lo1 = c >> 21 & 127, len1 = c >> 14 & 127, lo2 = c >> 7 & 127, len2 = c & 127;
+  return (low_mask(len1) << lo1) | (len2 ? low_mask(len2) << lo2 : 0ull);
+}
+__device__ __forceinline__ uint64_t pack_key(uint64_t u, uint32_t c) {
+  if (!(c >> 28)) return u;
+  const uint32_t lo1 = c >> 21 & 127, len1 = c >> 14 & 127, lo2 = c >> 7 & 127, len2 = c & 127;
+  const uint64_t r = (((u >> lo1) & low_mask(len1)) << len2) | (len2 ? (u >> lo2) & low_mask(len2) : 0ull);
+  return r << (64 - len1 - len2);
+}
+__device__ __forceinline__ uint64_t unpack_key(uint64_t v, uint32_t c, uint64_t constbits) {
+  if (!(c >> 28)) return v;
+  const uint32_t lo1 = c >> 21 & 127, len1 = c >> 14 & 127, lo2 = c >> 7 & 127, len2 = c & 127;
+  const uint64_t r = v >> (64 - len1 - len2);
+  return constbits | ((r >> len2) << lo1) | (len2 ? (r & low_mask(len2)) << lo2 : 0ull);
+}
+// 0: keys as they are; 1: one run ending at bit 0 — a plain left shift; 2: the general pack.
+__device__ __forceinline__ int pack_mode(uint32_t c) {
+  if (!(c >> 28)) return 0;
+  return ((c & 127) == 0 && (c >> 21 & 127) == 0) ? 1 : 2;
+}
+__device__ __forceinline__ uint32_t pack_shift(uint32_t c) { return 64u - (c >> 14 & 127); }  // mode 1
+template <int MODE>
+__device__ __forceinline__ uint64_t pack_as(uint64_t u, uint32_t c, uint32_t shl) {
+  if constexpr (MODE == 0) return u;
+  else if constexpr (MODE == 1) return u << shl;
+  else return pack_key(u, c);
+}
+template <int MODE>
+__device__ __forceinline__ uint64_t unpack_as(uint64_t v, uint32_t c, uint32_t shl, uint64_t constbits) {
+  if constexpr (MODE == 0) return v;
+  else if constexpr (MODE == 1) return (v >> shl) | constbits;
+  else return unpack_key(v, c, constbits);
 }
 
-__device__ __forceinline__ uint64_t key_prefix(const SortArgs& a, uint32_t sh) {
+// The bits every key shares (from the first key) where the code drops them.
+__device__ __forceinline__ uint64_t key_constbits(const SortArgs& a, uint32_t c) {
   const uint64_t u0 = xform(uint64_t(__ldg(static_cast<const long long*>(a.col))), a.desc);
-  return sh ? (u0 & ~(~0ull >> sh)) : 0ull;
+  return u0 & ~pack_mask(c);
 }
 
 // The fallback flag, read ONCE per CTA: other CTAs of the same kernel may
@@ -875,49 +928,58 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
       atomicOr(&red[kScatThreads - 3], vl);
     }
     __syncthreads();
-    sh = shift_of((uint64_t(red[kScatThreads - 4]) << 32) | red[kScatThreads - 3]);
-    if (blockIdx.x == 0 && tid == 0) a.flags[6] = sh;  // for the later kernels
+    sh = pack_code_of((uint64_t(red[kScatThreads - 4]) << 32) | red[kScatThreads - 3]);
+    if (blockIdx.x == 0 && tid == 0) a.flags[6] = sh;  // the pack code, for the later kernels
   }
   uint64_t vary = 0;
-  auto count = [&](uint64_t u) {  // a wrapped 16-bit counter shows up in the chunk total below
-    vary |= u ^ k0;
-    const uint32_t b = uint32_t((u << sh) >> 48);
-    atomicAdd(&w[b >> 1], 1u << ((b & 1u) << 4));
-  };
-  const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(col);
-  constexpr int kV = 4;
-  constexpr int64_t kStep = int64_t(kScatThreads) * kV;
-  const int64_t p1 = hi >> 1;
-  // two batches alternate: one is counted while the other's loads are in flight
-  ulonglong2 qa[kV], qb[kV];
-  auto fetch = [&](ulonglong2 (&q)[kV], int64_t base) {
+  // the counting loop, compiled per key-packing mode (chosen once)
+  const uint32_t shl = pack_shift(sh);
+  auto counting = [&](auto packed) {
+    auto count = [&](uint64_t u) {  // a wrapped 16-bit counter shows up in the chunk total below
+      vary |= u ^ k0;
+      const uint32_t b = uint32_t(pack_as<decltype(packed)::value>(u, sh, shl) >> 48);
+      atomicAdd(&w[b >> 1], 1u << ((b & 1u) << 4));
+    };
+    const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(col);
+    constexpr int kV = 4;
+    constexpr int64_t kStep = int64_t(kScatThreads) * kV;
+    const int64_t p1 = hi >> 1;
+    // two batches alternate: one is counted while the other's loads are in flight
+    ulonglong2 qa[kV], qb[kV];
+    auto fetch = [&](ulonglong2 (&q)[kV], int64_t base) {
 #pragma unroll
-    for (int u = 0; u < kV; ++u) {
-      const int64_t i = base + int64_t(u) * kScatThreads;
-      q[u] = i < p1 ? __ldg(v2 + i) : make_ulonglong2(0, 0);
-    }
-  };
-  auto consume = [&](const ulonglong2 (&q)[kV], int64_t base) {
-#pragma unroll
-    for (int u = 0; u < kV; ++u) {
-      if (base + int64_t(u) * kScatThreads < p1) {
-        count(xform(q[u].x, a.desc));
-        count(xform(q[u].y, a.desc));
+      for (int u = 0; u < kV; ++u) {
+        const int64_t i = base + int64_t(u) * kScatThreads;
+        q[u] = i < p1 ? __ldg(v2 + i) : make_ulonglong2(0, 0);
       }
+    };
+    auto consume = [&](const ulonglong2 (&q)[kV], int64_t base) {
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        if (base + int64_t(u) * kScatThreads < p1) {
+          count(xform(q[u].x, a.desc));
+          count(xform(q[u].y, a.desc));
+        }
+      }
+    };
+    int64_t base = (lo >> 1) + tid;
+    fetch(qa, base);
+    while (base < p1) {
+      fetch(qb, base + kStep);
+      consume(qa, base);
+      base += kStep;
+      if (base >= p1) break;
+      fetch(qa, base + kStep);
+      consume(qb, base);
+      base += kStep;
     }
+    if ((hi & 1) && hi > lo && tid == 0) count(xform(uint64_t(col[hi - 1]), a.desc));
   };
-  int64_t base = (lo >> 1) + tid;
-  fetch(qa, base);
-  while (base < p1) {
-    fetch(qb, base + kStep);
-    consume(qa, base);
-    base += kStep;
-    if (base >= p1) break;
-    fetch(qa, base + kStep);
-    consume(qb, base);
-    base += kStep;
+  switch (pack_mode(sh)) {
+    case 0: counting(std::integral_constant<int, 0>{}); break;
+    case 1: counting(std::integral_constant<int, 1>{}); break;
+    default: counting(std::integral_constant<int, 2>{}); break;
   }
-  if ((hi & 1) && hi > lo && tid == 0) count(xform(uint64_t(col[hi - 1]), a.desc));
   // varying key bits: one global atomic per CTA (one per warp serialised ~4700
   // same-address atomics at one L2 slice: a 15 us tail)
   const uint32_t vhi = __reduce_or_sync(0xffffffffu, uint32_t(vary >> 32));
@@ -932,7 +994,7 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
     const uint32_t l2 = __reduce_or_sync(0xffffffffu, red[2 * lane + 1]);
     const uint64_t v2 = (uint64_t(h2) << 32) | l2;
     if (lane == 0 && v2) atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 4), v2);
-    if (lane == 0 && sh && (v2 & ~(~0ull >> sh))) atomicOr(a.flags, 1u);  // the sample missed a varying bit: LSD
+    if (lane == 0 && (v2 & ~pack_mask(sh))) atomicOr(a.flags, 1u);  // the sample missed a varying bit: LSD
   }
 #ifdef RL_K1_PROFILE
   __syncthreads();
@@ -979,7 +1041,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   pdl_wait();  // the chunk counts
   pdl_launch_dependents();
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[2] = globaltimer();
-  if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);  // the key shift, read after the prologue's barriers
+  if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);  // the key pack code, read after the prologue's barriers
   if (fallback_flag(a)) return;  // a chunk counter wrapped: LSD
   // digit-7 bucket starts (every CTA)
   uint32_t t7 = 0;
@@ -1056,27 +1118,36 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   const long long* col = static_cast<const long long*>(a.col);
   const uint32_t sh = s.scratch[50];
   auto reserve = [&](uint32_t d, uint32_t c) { return s.aux[d] + atomicAdd(a.cur7 + d, c); };
-  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int64_t t0) {
-    const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
+  // the tile loop, compiled per key-packing mode (chosen once)
+  const uint32_t shl = pack_shift(sh);
+  auto tiles = [&](auto packed) {
+    auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int64_t t0) {
+      const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
 #pragma unroll
-    for (int u = 0; u < kPItems; ++u) {
-      const int j = u * kPThreads + tid;
-      k[u] = j < tn ? xform(uint64_t(__ldcs(col + t0 + j)), a.desc) << sh : 0ull;
-      v[u] = uint32_t(t0 + j);
+      for (int u = 0; u < kPItems; ++u) {
+        const int j = u * kPThreads + tid;
+        k[u] = j < tn ? pack_as<decltype(packed)::value>(xform(uint64_t(__ldcs(col + t0 + j)), a.desc), sh, shl) : 0ull;
+        v[u] = uint32_t(t0 + j);
+      }
+    };
+    uint64_t k[kPItems];
+    uint32_t v[kPItems];
+    if (lo < hi) load(k, v, lo);
+    if (tid < 256) s.hist[tid] = 0;
+    __syncthreads();
+    for (int64_t t0 = lo; t0 < hi; t0 += kPTile) {
+      const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
+      const int64_t nt = t0 + kPTile;
+      ptile_scatter<7 * kBits>(k, v, tn, s, a.keys_b, a.vals_b, reserve,
+                               [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
+                                 if (nt < hi) load(kk, vv, nt);
+                               });
     }
   };
-  uint64_t k[kPItems];
-  uint32_t v[kPItems];
-  if (lo < hi) load(k, v, lo);
-  if (tid < 256) s.hist[tid] = 0;
-  __syncthreads();
-  for (int64_t t0 = lo; t0 < hi; t0 += kPTile) {
-    const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
-    const int64_t nt = t0 + kPTile;
-    ptile_scatter<7 * kBits>(k, v, tn, s, a.keys_b, a.vals_b, reserve,
-                             [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
-                               if (nt < hi) load(kk, vv, nt);
-                             });
+  switch (pack_mode(sh)) {
+    case 0: tiles(std::integral_constant<int, 0>{}); break;
+    case 1: tiles(std::integral_constant<int, 1>{}); break;
+    default: tiles(std::integral_constant<int, 2>{}); break;
   }
 }
 
@@ -1197,8 +1268,8 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
   bulk_g2s(abuf + kLocAKeys, vin + v0, vbytes, bar);
 }
 
-template <int THREADS>
-__device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src, bool shifted = false) {
+template <int THREADS, int PACK = 0>
+__device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   constexpr int kLWarps = THREADS / 32;
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
   uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
@@ -1233,9 +1304,10 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src, bool
     __syncwarp();
   }
   __syncthreads();
-  // the scatter path's key shift and prefix (staged in misc[125..127] by the caller)
-  const uint32_t sh = shifted ? misc[125] : 0u;
-  const uint64_t prefix = shifted ? (uint64_t(misc[127]) << 32) | misc[126] : 0ull;
+  // the scatter path's key pack code and constant bits (staged in misc[125..127] by the caller)
+  const uint32_t pcode = PACK ? misc[125] : 0u;
+  const uint64_t constbits = PACK ? (uint64_t(misc[127]) << 32) | misc[126] : 0ull;
+  const uint32_t pshl = pack_shift(pcode);
   // run cursor: group k (g = g0 + k gstep), run r of that group; identical in every thread
   uint32_t k = 0, r = 0, buf = 0, phase0 = 0, phase1 = 0;
   bool have = misc[2] > 0;
@@ -1370,7 +1442,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src, bool
     constexpr uint32_t kRankMax = 32;
     auto emit = [&](uint32_t p, uint64_t key, uint32_t v) {
       const uint64_t o = uint64_t(base) + p;
-      if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform((key >> sh) | prefix, desc));
+      if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(unpack_as<PACK>(key, pcode, pshl, constbits), desc));
       __stcs(a.out_vals + o, v);
       gather_fused(a.gather, v, o);
     };
@@ -1465,15 +1537,19 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   pdl_launch_dependents();
   if (stamper) a.stamps[1] = globaltimer();
   if (*reinterpret_cast<volatile const uint32_t*>(a.flags)) return;  // final before this launch: uniform
-  if (threadIdx.x == 0) {  // key shift and prefix, read by the local phase after its first barrier
+  if (threadIdx.x == 0) {  // key pack code and constant bits, read by the local phase after its first barrier
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
-    const uint32_t sh = __ldcg(a.flags + 6);
-    const uint64_t prefix = key_prefix(a, sh);
-    misc[125] = sh;
-    misc[126] = uint32_t(prefix);
-    misc[127] = uint32_t(prefix >> 32);
+    const uint32_t pc = __ldcg(a.flags + 6);
+    const uint64_t cb = key_constbits(a, pc);
+    misc[125] = pc;
+    misc[126] = uint32_t(cb);
+    misc[127] = uint32_t(cb >> 32);
   }
-  local_phase<kLocalThreads>(a, smem, 1, true);
+  switch (pack_mode(__ldcg(a.flags + 6))) {
+    case 0: local_phase<kLocalThreads, 0>(a, smem, 1); break;
+    case 1: local_phase<kLocalThreads, 1>(a, smem, 1); break;
+    default: local_phase<kLocalThreads, 2>(a, smem, 1); break;
+  }
   if (stamper) {
     a.stamps[kStamps - 2] = globaltimer();
     a.stamps[kStamps - 1] = 3;
@@ -1785,12 +1861,12 @@ static int hist_grid(int64_t n) {  // one co-resident wave (2 CTAs of 512 thread
 // The cooperative sort kernel as a programmatic dependent of the kernel before
 // it (scheduled while that one drains; it waits on the device), or a plain
 // cooperative launch where the runtime refuses the combination.
-static cudaError_t launch_sort_kernel(SortArgs& a, int grid, cudaStream_t stream) {
+static cudaError_t launch_sort_kernel(SortArgs& a, int grid, cudaStream_t stream, bool pdl) {
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = getenv_flag("RL_NO_PDL") ? 0 : 1;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1813,6 +1889,11 @@ static cudaError_t launch_sort_kernel(SortArgs& a, int grid, cudaStream_t stream
 static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* const* events, int max_ctas = 0) {
   int limit = sort_grid_limit();
   if (max_ctas > 0 && limit > max_ctas) limit = max_ctas;  // leave room for a concurrent sort
+  // programmatic dependent launches between this sort's kernels — not when a
+  // concurrent sort shares the device (early-scheduled dependents of one sort
+  // hold SMs the other's kernels need: the join plan's two index sorts went
+  // 0.75 -> 1.14 ms with them)
+  const bool pdl = max_ctas <= 0 && !getenv_flag("RL_NO_PDL");
   if (limit < 1) {
     cudaError_t e = cudaGetLastError();
     return rl_cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration);
@@ -1863,7 +1944,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     auto launch_dep = [&](auto kernel, int g, int threads, size_t smem) {
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = getenv_flag("RL_NO_PDL") ? 0 : 1;
+      attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(g);
       cfg.blockDim = dim3(threads);
@@ -1882,7 +1963,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     if ((e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes)) != cudaSuccess) return rl_cuda_status(e);
     chk("local");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
-    e = launch_sort_kernel(a, grid, stream);  // returns at once unless the fallback flag is set
+    e = launch_sort_kernel(a, grid, stream, pdl);  // returns at once unless the fallback flag is set
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
     count_launches(5);
     return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
@@ -1894,7 +1975,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   else if (a.src_mode == kSrcInt64) hist_kernel<true, false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   else hist_kernel<false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
-  e = launch_sort_kernel(a, grid, stream);
+  e = launch_sort_kernel(a, grid, stream, pdl);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
   count_launches(2);
   return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());

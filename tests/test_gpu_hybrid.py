@@ -231,3 +231,24 @@ def test_scatter_shift_missed_by_sample():
     keys = rng.integers(0, 1 << 30, n, dtype=np.int64)
     keys[3] = np.int64(1) << 50  # not at a sampled position
     check_sort(keys)
+
+
+@pytest.mark.parametrize("shape", ["composite", "low_zero_bits", "three_runs"])
+def test_scatter_packed_keys(shape):
+    """Varying bits in two runs (cfg4's (a << 32) | b with 16-bit parts), keys
+    with constant low bits (multiples of 64), and three runs (not packed:
+    the keys are used as they are) — all equal to the stable argsort."""
+    rng = np.random.default_rng(50 + len(shape))
+    n = 4_500_000
+    if shape == "composite":
+        a = rng.integers(0, 2**16, n).astype(np.int64)
+        b = rng.integers(0, 2**16, n).astype(np.int64)
+        keys = (a << np.int64(32)) | b
+    elif shape == "low_zero_bits":
+        keys = rng.integers(-(1 << 33), 1 << 33, n, dtype=np.int64) * 64
+    else:
+        keys = ((rng.integers(0, 2**12, n).astype(np.int64) << np.int64(50))
+                | (rng.integers(0, 2**12, n).astype(np.int64) << np.int64(30))
+                | rng.integers(0, 2**12, n).astype(np.int64))
+    check_sort(keys)
+    check_sort(keys, True)

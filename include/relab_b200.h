@@ -108,9 +108,12 @@ RL_API int64_t rl_launch_count(void);
  * (n >= 2^22) by exact per-chunk sub-bucket counts and two non-stable
  * counting passes (three launches ahead of it) — then an on-chip sort of
  * each sub-bucket by (key, row id) is written straight to the outputs (the
- * cooperative kernel, or its own 512-thread launch on the scatter path). A
- * sub-bucket over the on-chip cap switches to the LSD passes on the device.
- * Results are identical on every path. An INT64 `col` read without perm_in, and perm_in,
+ * cooperative kernel, or its own 512-thread launch on the scatter path). On
+ * the scatter path keys whose bits do not all vary are packed first (up to
+ * two runs of varying bits, estimated from a sample and checked against every
+ * key), so narrow and composite keys get sub-buckets too. A sub-bucket over
+ * the on-chip cap switches to the LSD passes on the device. Results are
+ * identical on every path. An INT64 `col` read without perm_in, and perm_in,
  * must be 16-byte aligned (they are streamed with TMA bulk copies);
  * RL_ERR_BAD_ARG otherwise.
  * --------------------------------------------------------------------- */

@@ -626,19 +626,31 @@ def run_distributed(args, dev, rank, world, lib, keys_h, pay_h, keys_d, pay_d, f
     e2e_total = float(t[0].item())
     e2e_value = world * n * args.steps / e2e_total / 1e6
 
+    # the exchange against NVLink: rows a rank sends off-rank (key 8 B + payload 4 B + int64 global id 8 B)
+    # per step over the whole step time — a lower bound on link use (the step also partitions and sorts)
+    sent = n * (world - 1) / world * 20
+    step_s = total_ms / args.steps / 1e3
+    nvlink = {"bound": "nvlink", "bytes_per_rank_per_step": int(sent),
+              "achieved_gbs": round(sent / step_s / 1e9, 1) if world > 1 else 0.0,
+              "peak_gbs": 900.0, "unit": "GB/s",
+              "frac": round(sent / step_s / 1e9 / 900.0, 4) if world > 1 else 0.0,
+              "note": "uniform keys: (P-1)/P of each rank's rows move; peak = NVLink 5 per direction per GPU; "
+                      "time = the whole step"}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "rows_per_gpu": n, "rows_total": world * n,
-                   "parallelism": f"range-partitioned sort over {world} rank(s): sampled splitters, NCCL all_to_all, "
-                                  "local stable sort",
+                   "parallelism": f"range-partitioned sort over {world} rank(s): sampled splitters (device), "
+                                  "partition gather fused with the exchange (peer stores into symmetric memory over "
+                                  "NVLink/NVSwitch; NCCL all_to_all where unavailable), local stable sort",
                    "l2": "flushed between timed steps (256 MiB write)", "seed_per_rank": "rank"},
         "p50_ms": round(percentile(step_ms, 50), 4), "p99_ms": round(percentile(step_ms, 99), 4),
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": world * n * 12,
                 "d2h_bytes_per_step": int(float(tt[1].item()) / args.steps),
                 "api": "dist.distributed_sort from pinned host shards; sorted keys + payload back to host"},
         "roofline": roofline,
+        "nvlink": nvlink,
         "clocks": clocks.summary(),
         "gpu_launches": int(launches),
     }

@@ -781,7 +781,12 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
             "rows_per_side_per_gpu": n, "matches_total": int(total),
             "path": "device join" if world == 1 else "distributed_join: hash partition + peer-memory push + local join",
             "ms_per_step_p50_max_over_ranks": round(med, 3),
-            "mrows_per_s": round(2 * total_rows / (med / 1e3) / 1e6, 1), "scaling": "strong"}
+            "mrows_per_s": round(2 * total_rows / (med / 1e3) / 1e6, 1), "scaling": "strong",
+            # both sides' off-rank rows per rank (key 8 B + payload 8 B + int64 global id 8 B) over the step
+            "nvlink": {"bytes_per_rank_per_step": int(2 * n * (world - 1) / world * 24),
+                       "achieved_gbs": round(2 * n * (world - 1) / world * 24 / (med / 1e3) / 1e9, 1),
+                       "peak_gbs": 900.0, "unit": "GB/s",
+                       "frac": round(2 * n * (world - 1) / world * 24 / (med / 1e3) / 1e9 / 900.0, 4)}}
 
 
 def extras(args, dev):

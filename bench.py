@@ -85,6 +85,15 @@ class ClockSampler:
         self.rows = []  # (sm_mhz, max_mhz, set(reasons))
         self._stop = threading.Event()
         self._t = None
+        try:  # NVML is initialised before the timed region, not inside it
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._sample = lambda: self._sample_nvml(nv, h)  # noqa: E731
+        except Exception:
+            self._sample = self._sample_smi
+        self._switch = None
 
     def _sample_nvml(self, nv, h):
         sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
@@ -101,31 +110,38 @@ class ClockSampler:
         f = [x.strip() for x in out.split(",")]
         return float(f[0]), float(f[1]), {self.REASONS[i][0] for i in range(4) if f[2 + i] == "Active"}
 
-    def _run(self):
+    def _take(self):
         try:
-            import pynvml as nv
-
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            sample = lambda: self._sample_nvml(nv, h)  # noqa: E731
+            self.rows.append(self._sample())
+            return True
         except Exception:
-            sample = self._sample_smi
+            return False
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.rows.append(sample())
-            except Exception:
+            if not self._take():
                 return
             self._stop.wait(self.period)
 
     def __enter__(self):
+        import sys
+
+        self._take()  # one sample as the timed region starts
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(0.0002)  # let the sampling thread in while the timing loop holds the GIL
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *exc):
+        import sys
+
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if self._switch is not None:
+            sys.setswitchinterval(self._switch)
+        self._take()  # and one as it ends
 
     def summary(self):
         if not self.rows:

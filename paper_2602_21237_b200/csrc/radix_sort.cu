@@ -698,7 +698,8 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 
 // ---------------------------------------------------------------- scatter hybrid
 // Wide raw int64 keys, n >= kScatterMinRows. The local phase ranks every row
-// by (key, row id) inside its sub-bucket (top 16 key bits), so the rows only
+// by (key, row id) inside its sub-bucket (top 16 bits of the packed key, see
+// below), so the rows only
 // have to reach their sub-bucket, in any order — two non-stable counting
 // passes with exact, precomputed bucket starts instead of two stable
 // onesweep passes (no look-back, no stable multisplit):
@@ -719,10 +720,14 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 //   sub_scatter_kernel  tiles of one digit-7 bucket each, claimed in bucket
 //                       order: the same staged scatter by digit 6 into the
 //                       sub-buckets (keys_a / vals_a)
+//   local_kernel        the local phase (512-thread CTAs)
 // Bucket-ordered claiming keeps the sub-buckets being written within a few
-// MB, so every sector completes in L2. The cooperative kernel then runs only
-// the local phase — or, on the fallback flag (a sub-bucket above kLocalCap, a
-// wrapped chunk counter, < 4 varying digits), the LSD passes from the input.
+// MB, so every sector completes in L2. The cooperative kernel launched last
+// returns at once — unless the fallback flag is set (a sub-bucket above
+// kLocalCap, a wrapped chunk counter, < 4 varying digits, a varying bit the
+// key sample missed): then it runs the LSD passes from the original input.
+// Each kernel after the first is a programmatic dependent of the one before
+// when the sort has the device to itself.
 
 // Key normalisation of the scatter path: the key bits that do not vary
 // (estimated from a sample at the start of the chunk counts, checked by them

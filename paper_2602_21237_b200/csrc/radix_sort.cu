@@ -45,6 +45,11 @@
 // sub-bucket larger than kLocalCap (skewed top bits) is caught after the
 // two passes and the same launch runs the LSD passes instead.
 //
+// Scatter hybrid (raw int64 keys, n >= 2^22 — the cfg2 path): the rows reach
+// their sub-buckets by exact per-chunk counts and two NON-stable counting
+// passes (the local phase orders every sub-bucket by (key, row id) anyway),
+// keys packed to their varying bits first; see "scatter hybrid" below.
+//
 // Key transform (self-inverse): int64 ascending  u = x ^ 2^63;
 // descending u = ~x ^ 2^63 (the reference's np.invert, tensorpath.py:215,
 // keeps ties in ascending row order). Bytes words are built big-endian

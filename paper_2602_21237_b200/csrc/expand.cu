@@ -30,7 +30,7 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kItems = RL_EXPAND_ITEMS;
 #ifndef RL_EXPAND_MIN_BLOCKS
-#define RL_EXPAND_MIN_BLOCKS 3
+#define RL_EXPAND_MIN_BLOCKS 4
 #endif
 constexpr int kTile = kThreads * kItems;
 

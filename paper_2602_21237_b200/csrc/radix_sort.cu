@@ -1385,8 +1385,13 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       }
     }
     // ---- this run: only the bins of its sub-buckets are zeroed and scanned
-    const uint32_t bin_lo = (runs[buf * 4 + 2] & (kGroupSubs - 1)) * kBins, nsb = runs[buf * 4 + 3];
-    for (uint32_t i = tid; i < nsb * kBins; i += THREADS) hist[bin_lo + i] = 0;
+    // bins of this run: (sub-bucket, the next bb key bits), run-relative; the
+    // fewer sub-buckets a run holds, the more bits each gets (4096 bins at most:
+    // a run of one big sub-bucket is split 4096 ways, not 256)
+    const uint32_t first = runs[buf * 4 + 2], nsb = runs[buf * 4 + 3];
+    const uint32_t bb = 12u - (nsb > 1 ? 32u - uint32_t(__clz(int(nsb - 1))) : 0u);
+    const uint32_t nbins = nsb << bb;
+    for (uint32_t i = tid; i < nbins; i += THREADS) hist[i] = 0;
     mbar_wait(&bars[buf], buf ? phase1 : phase0);
     if (buf) phase1 ^= 1;
     else phase0 ^= 1;
@@ -1396,16 +1401,16 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     const bool more = misc[4] != 0;
     const uint32_t next_k = misc[5], next_r = misc[6];
     if (tid == 0) misc[0] = 0;  // big-bin list: appended after later barriers, read after the rank loop
-    const uint32_t base = runs[buf * 4], cnt = runs[buf * 4 + 1], top0 = runs[buf * 4 + 2] & ~uint32_t(kGroupSubs - 1);
+    const uint32_t base = runs[buf * 4], cnt = runs[buf * 4 + 1];
     const uint8_t* abuf = smem + kLocA + buf * kLocABytes;
     const uint64_t* ak = reinterpret_cast<const uint64_t*>(abuf) + (base & 1u);
     const uint32_t* av = reinterpret_cast<const uint32_t*>(abuf + kLocAKeys) + (base & 3u);
     auto bin_of = [&](uint64_t key) {
-      return int(((uint32_t(key >> 48) - top0) << kBits) | (uint32_t(key >> 40) & (kBins - 1)));
+      return int(((uint32_t(key >> 48) - first) << bb) | (uint32_t(key >> (48 - bb)) & ((1u << bb) - 1u)));
     };
     for (uint32_t j = tid; j < cnt; j += THREADS) atomicAdd(&hist[bin_of(ak[j])], 1u);
     __syncthreads();
-    if (nsb == uint32_t(kGroupSubs)) {  // a whole group: thread owns kPerThread consecutive bins (vector loads)
+    if (nbins == uint32_t(kLocalBins)) {  // all 4096 bins: thread owns kPerThread consecutive bins (vector loads)
       uint32_t c[kPerThread], run = 0;
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
@@ -1419,11 +1424,11 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         hist[tid * kPerThread + i] = start;
         start += c[i];
       }
-    } else {  // part of a group: only its nsb * 256 bins, thread owns `per` consecutive bins
-      const uint32_t per = (nsb * kBins + THREADS - 1) / THREADS;  // <= kPerThread
-      const uint32_t nb = nsb * kBins;
+    } else {  // fewer bins: thread owns `per` consecutive bins
+      const uint32_t per = (nbins + THREADS - 1) / THREADS;  // <= kPerThread
+      const uint32_t nb = nbins;
       uint32_t c[kPerThread], run = 0;
-      uint32_t* hb = hist + bin_lo + tid * per;
+      uint32_t* hb = hist + tid * per;
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
         c[i] = uint32_t(i) < per && tid * per + i < nb ? hb[i] : 0u;
@@ -1460,7 +1465,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       const uint64_t key = bk[p];
       const uint32_t v = bv[p];
       const int b = bin_of(key);
-      const uint32_t b0 = uint32_t(b) > bin_lo ? hist[b - 1] : 0u, b1 = hist[b];
+      const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
       uint32_t pos = p;
       if (b1 - b0 > kRankMax) {
         if (p == b0) {
@@ -1480,7 +1485,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     const uint32_t nbig = min(misc[0], uint32_t(kBigList));
     for (uint32_t t = warp; t < nbig; t += kLWarps) {
       const int b = int(big[t]);
-      const uint32_t b0 = uint32_t(b) > bin_lo ? hist[b - 1] : 0u, b1 = hist[b];
+      const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
       warp_bitonic(bk, bv, b0, b1, lane);
       for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], bv[p]);
     }
@@ -1545,24 +1550,33 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   const bool stamper = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
   pdl_wait();  // the digit-6 pass
   pdl_launch_dependents();
-  if (stamper) a.stamps[1] = globaltimer();
-  if (*reinterpret_cast<volatile const uint32_t*>(a.flags)) return;  // final before this launch: uniform
+  const bool scatter = a.mode == kModeScatter;
+  if (stamper && scatter) a.stamps[1] = globaltimer();
+  // scatter path: flags[0] = LSD fallback; onesweep hybrid: flags[7] = the
+  // cooperative kernel took the hybrid and every sub-bucket fits (else it sorted
+  // LSD). Both final before this launch: uniform.
+  if (scatter ? *reinterpret_cast<volatile const uint32_t*>(a.flags) != 0
+              : *reinterpret_cast<volatile const uint32_t*>(a.flags + 7) == 0)
+    return;
+  // the rows sit in their sub-buckets in keys_a / vals_a (scatter path: the
+  // digit-6 pass) or keys_b / vals_b (onesweep hybrid: its digit-7 pass)
+  const uint32_t src = scatter ? 1u : 2u;
   if (threadIdx.x == 0) {  // key pack code and constant bits, read by the local phase after its first barrier
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
     const uint32_t pc = __ldcg(a.flags + 6);
-    const uint64_t cb = key_constbits(a, pc);
+    const uint64_t cb = pack_mode(pc) ? key_constbits(a, pc) : 0ull;  // (a.col is null for encoded keys)
     misc[125] = pc;
     misc[126] = uint32_t(cb);
     misc[127] = uint32_t(cb >> 32);
   }
   switch (pack_mode(__ldcg(a.flags + 6))) {
-    case 0: local_phase<kLocalThreads, 0>(a, smem, 1); break;
-    case 1: local_phase<kLocalThreads, 1>(a, smem, 1); break;
-    default: local_phase<kLocalThreads, 2>(a, smem, 1); break;
+    case 0: local_phase<kLocalThreads, 0>(a, smem, src); break;
+    case 1: local_phase<kLocalThreads, 1>(a, smem, src); break;
+    default: local_phase<kLocalThreads, 2>(a, smem, src); break;
   }
   if (stamper) {
     a.stamps[kStamps - 2] = globaltimer();
-    a.stamps[kStamps - 1] = 3;
+    a.stamps[kStamps - 1] = scatter ? 3 : 1;
   }
 }
 
@@ -1684,17 +1698,9 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
     }
     grid_sync(a.grid_bar, ++barrier_no);
     if (stamper) a.stamps[2] = globaltimer();  // (pass 0's slot: the hybrid's sub-bucket check)
+    // every sub-bucket fits on chip: local_kernel (launched next) sorts them
     if (*reinterpret_cast<volatile uint32_t*>(a.flags) == 0) {
-      if (tid == 0) {
-        mbar_inval(&bars[0]);
-        mbar_inval(&bars[1]);
-      }
-      __syncthreads();
-      local_phase<kThreads>(a, smem, src);
-      if (stamper) {
-        a.stamps[kStamps - 2] = globaltimer();
-        a.stamps[kStamps - 1] = 1;
-      }
+      if (blockIdx.x == 0 && tid == 0) a.flags[7] = 1u;  // the go signal (an LSD sort leaves it 0)
       return;
     }
     // a sub-bucket does not fit on chip: the LSD sort, fresh epochs and counters
@@ -1986,8 +1992,17 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
   else hist_kernel<false><<<hist_grid(a.n), kHistThreads, 0, stream>>>(a);
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
   e = launch_sort_kernel(a, grid, stream, pdl);
+  int launched = 2;
+  if (e == cudaSuccess && a.mode == kModeHybrid) {  // the local phase (returns at once after an LSD fallback)
+    if (!scatter_kernels_ready()) return rl_cuda_status(cudaErrorInvalidConfiguration);
+    int lgrid = device_sm_count() * (1024 / kLocalThreads);
+    if (max_ctas > 0) lgrid = std::max(1, std::min(lgrid, max_ctas));
+    local_kernel<<<lgrid, kLocalThreads, kLocalSmemBytes, stream>>>(a);
+    e = cudaGetLastError();
+    launched = 3;
+  }
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
-  count_launches(2);
+  count_launches(launched);
   return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
 }
 

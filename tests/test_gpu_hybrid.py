@@ -252,3 +252,16 @@ def test_scatter_packed_keys(shape):
                 | rng.integers(0, 2**12, n).astype(np.int64))
     check_sort(keys)
     check_sort(keys, True)
+
+
+@pytest.mark.parametrize("n", [1 << 18, 1_500_000])
+def test_hybrid_then_lsd_same_size(n):
+    """A wide-key sort (hybrid) then sorts the cooperative kernel must take LSD
+    (narrow keys: too few varying digits; one huge sub-bucket) on the same
+    workspace. The sub-bucket table is stale from the first sort, so the local
+    phase must see the LSD sort's "no local phase" signal and not run."""
+    rng = np.random.default_rng(n + 7)
+    check_sort(full_range(rng, n))
+    check_sort(rng.integers(0, 1 << 20, n, dtype=np.int64))  # three varying digits: LSD
+    check_sort(np.where(rng.random(n) < 0.5, 5, full_range(rng, n)).astype(np.int64))  # skew: fallback
+    check_sort(full_range(rng, n))

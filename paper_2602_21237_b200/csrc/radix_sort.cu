@@ -1278,7 +1278,10 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
   bulk_g2s(abuf + kLocAKeys, vin + v0, vbytes, bar);
 }
 
-template <int THREADS, int PACK = 0>
+// BAL (the scatter path's large runs): a thread's rows in registers across
+// count + scatter, and the claimed group tail. The onesweep hybrid's short
+// runs (n < 4M) are faster without both (+1-5 us each at 0.3-2M rows).
+template <int THREADS, int PACK = 0, bool BAL = false>
 __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   constexpr int kLWarps = THREADS / 32;
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
@@ -1296,23 +1299,57 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   const int desc = a.key_mode == kRawDesc;
   constexpr uint32_t kGroups = kSubBuckets / kGroupSubs;
   constexpr int kPerThread = kLocalBins / THREADS;
-  const uint32_t g0 = blockIdx.x, gstep = gridDim.x;
+  const uint32_t g0 = blockIdx.x;
   if (g0 >= kGroups) return;
+  // group schedule: the first nstat groups of every CTA on a static stride
+  // (no atomic on warp 0's path: it issues the next run's TMA while the other
+  // warps wait), the last ~2 rounds claimed from a counter (flags[1], zeroed
+  // per sort) so that CTAs which drew short groups take more — the static
+  // stride alone left the last CTA ~15 us behind the first at 10M rows; claims
+  // throughout cost ~0.6 us of warp-0 latency per group (+9 us at 1M rows).
+  uint32_t* gid = misc + 120;  // [2] the group whose offsets are in goff slot s (warp 0 only)
+  // groups below lim go by the static stride, the rest are claimed
+  const uint32_t lim = !BAL ? 0xFFFFFFFFu
+                            : (max(1u, kGroups / gridDim.x) - (kGroups / gridDim.x > 1 ? 1u : 0u)) * gridDim.x;
+  auto claim = [&](uint32_t last) -> uint32_t {  // warp 0, converged; last = the group claimed before
+    if constexpr (!BAL) return last + gridDim.x;
+    if (last + gridDim.x < lim) return last + gridDim.x;
+    uint32_t g = 0;
+    if (lane == 0) g = lim + atomicAdd(a.flags + 1, 1u);
+    return __shfl_sync(0xffffffffu, g, 0);
+  };
 
   // ---- prologue (warp 0): offsets of the first group, its runs, the first
-  // TMA; the second group's offsets are requested into registers
-  uint32_t next_off = 0;  // warp 0, lane <= G: sub_off of the group after the current one
+  // TMA; the next group is claimed and its offsets requested into registers
+  uint32_t next_off = 0;  // warp 0, lane <= G: sub_off of group next_g
+  uint32_t next_g = g0;
   if (warp == 0) {
     if (lane == 0) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
+      gid[0] = g0;
     }
     if (lane <= kGroupSubs) goff[lane] = __ldcg(a.sub_off + g0 * kGroupSubs + lane);
-    if (lane <= kGroupSubs && g0 + gstep < kGroups) next_off = __ldcg(a.sub_off + (g0 + gstep) * kGroupSubs + lane);
+    next_g = claim(next_g);
+    if (lane <= kGroupSubs && next_g < kGroups) next_off = __ldcg(a.sub_off + next_g * kGroupSubs + lane);
     __syncwarp();
     if (lane == 0) misc[2] = cut_group(goff, gends);
     __syncwarp();
   }
+  // warp 0: move the claimed group's offsets into goff slot s, claim the next;
+  // false when no group is left
+  auto advance = [&](uint32_t s) -> bool {
+    const uint32_t gn = next_g;
+    if (gn >= kGroups) return false;
+    if (lane <= kGroupSubs) goff[s * 17 + lane] = next_off;
+    if (lane == 0) gid[s] = gn;
+    next_g = claim(next_g);
+    if (lane <= kGroupSubs && next_g < kGroups) next_off = __ldcg(a.sub_off + next_g * kGroupSubs + lane);
+    __syncwarp();
+    if (lane == 0) misc[2 + s] = cut_group(goff + s * 17, gends + s * 16);
+    __syncwarp();
+    return true;
+  };
   __syncthreads();
   // the scatter path's key pack code and constant bits (staged in misc[125..127] by the caller)
   const uint32_t pcode = PACK ? misc[125] : 0u;
@@ -1325,15 +1362,12 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   while (!have) {
     __syncthreads();
     if (warp == 0) {
-      const uint32_t gn = g0 + (k + 1) * gstep;
-      if (lane <= kGroupSubs && gn < kGroups) goff[((k + 1) & 1) * 17 + lane] = next_off;
-      if (lane <= kGroupSubs && gn + gstep < kGroups) next_off = __ldcg(a.sub_off + (gn + gstep) * kGroupSubs + lane);
-      __syncwarp();
-      if (lane == 0) misc[2 + ((k + 1) & 1)] = gn < kGroups ? cut_group(goff + ((k + 1) & 1) * 17, gends + ((k + 1) & 1) * 16) : 0;
+      const bool got = advance((k + 1) & 1);
+      if (lane == 0) misc[7] = got ? 1u : 0u;
     }
     __syncthreads();
     ++k;
-    if (g0 + k * gstep >= kGroups) return;
+    if (!misc[7]) return;
     have = misc[2 + (k & 1)] > 0;
   }
   if (tid == 0) {
@@ -1342,7 +1376,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     const uint32_t base = off[se >> 8], cnt = off[se & 255] - base;
     runs[0] = base;
     runs[1] = cnt;
-    runs[2] = (g0 + k * gstep) * kGroupSubs + (se >> 8);
+    runs[2] = gid[k & 1] * kGroupSubs + (se >> 8);
     runs[3] = (se & 255) - (se >> 8);
     issue_run(kin, vin, base, cnt, smem + kLocA, &bars[0]);
   }
@@ -1354,16 +1388,10 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       uint32_t nk = k, nr = r + 1;
       bool ok = true;
       while (nr >= misc[2 + (nk & 1)]) {  // past the group's runs: the next group (offsets were prefetched)
-        const uint32_t gn = g0 + (nk + 1) * gstep;
-        if (gn >= kGroups) {
+        if (!advance((nk + 1) & 1)) {
           ok = false;
           break;
         }
-        if (lane <= kGroupSubs) goff[((nk + 1) & 1) * 17 + lane] = next_off;
-        if (lane <= kGroupSubs && gn + gstep < kGroups) next_off = __ldcg(a.sub_off + (gn + gstep) * kGroupSubs + lane);
-        __syncwarp();
-        if (lane == 0) misc[2 + ((nk + 1) & 1)] = cut_group(goff + ((nk + 1) & 1) * 17, gends + ((nk + 1) & 1) * 16);
-        __syncwarp();
         ++nk;
         nr = 0;
       }
@@ -1378,7 +1406,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
           uint32_t* d = runs + (buf ^ 1) * 4;
           d[0] = base;
           d[1] = cnt;
-          d[2] = (g0 + nk * gstep) * kGroupSubs + (se >> 8);
+          d[2] = gid[nk & 1] * kGroupSubs + (se >> 8);
           d[3] = (se & 255) - (se >> 8);
           issue_run(kin, vin, base, cnt, smem + kLocA + (buf ^ 1) * kLocABytes, &bars[buf ^ 1]);
         }
@@ -1408,7 +1436,23 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     auto bin_of = [&](uint64_t key) {
       return int(((uint32_t(key >> 48) - first) << bb) | (uint32_t(key >> (48 - bb)) & ((1u << bb) - 1u)));
     };
-    for (uint32_t j = tid; j < cnt; j += THREADS) atomicAdd(&hist[bin_of(ak[j])], 1u);
+    // BAL: a thread's rows of the run (at most kRows: kLocalCap / THREADS),
+    // loaded once into registers — the loads issue together instead of one per
+    // shared atomic (which they may not pass: same memory) — kept for the scatter
+    constexpr int kRows = BAL ? (kLocalCap + THREADS - 1) / THREADS : 1;
+    uint64_t rk[kRows];
+    if constexpr (BAL) {
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const uint32_t j = tid + u * THREADS;
+        rk[u] = j < cnt ? ak[j] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kRows; ++u)
+        if (tid + u * THREADS < cnt) atomicAdd(&hist[bin_of(rk[u])], 1u);
+    } else {
+      for (uint32_t j = tid; j < cnt; j += THREADS) atomicAdd(&hist[bin_of(ak[j])], 1u);
+    }
     __syncthreads();
     if (nbins == uint32_t(kLocalBins)) {  // all 4096 bins: thread owns kPerThread consecutive bins (vector loads)
       uint32_t c[kPerThread], run = 0;
@@ -1443,11 +1487,26 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       }
     }
     __syncthreads();
-    for (uint32_t j = tid; j < cnt; j += THREADS) {
-      const uint64_t key = ak[j];
-      const uint32_t pos = atomicAdd(&hist[bin_of(key)], 1u);
-      bk[pos] = key;
-      bv[pos] = av[j];
+    if constexpr (BAL) {
+      uint32_t pos[kRows];
+#pragma unroll
+      for (int u = 0; u < kRows; ++u)
+        if (tid + u * THREADS < cnt) pos[u] = atomicAdd(&hist[bin_of(rk[u])], 1u);
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const uint32_t j = tid + u * THREADS;
+        if (j < cnt) {
+          bk[pos[u]] = rk[u];
+          bv[pos[u]] = av[j];
+        }
+      }
+    } else {
+      for (uint32_t j = tid; j < cnt; j += THREADS) {
+        const uint64_t key = ak[j];
+        const uint32_t pos = atomicAdd(&hist[bin_of(key)], 1u);
+        bk[pos] = key;
+        bv[pos] = av[j];
+      }
     }
     __syncthreads();
     // hist[b] is now the end of bin b; a bin holds the rows equal in their
@@ -1569,11 +1628,17 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
     misc[126] = uint32_t(cb);
     misc[127] = uint32_t(cb >> 32);
   }
-  switch (pack_mode(__ldcg(a.flags + 6))) {
-    case 0: local_phase<kLocalThreads, 0>(a, smem, src); break;
-    case 1: local_phase<kLocalThreads, 1>(a, smem, src); break;
-    default: local_phase<kLocalThreads, 2>(a, smem, src); break;
+  if (!scatter) {
+    local_phase<kLocalThreads, 0, false>(a, smem, src);  // (the onesweep hybrid packs no keys)
+  } else {
+    switch (pack_mode(__ldcg(a.flags + 6))) {
+      case 0: local_phase<kLocalThreads, 0, true>(a, smem, src); break;
+      case 1: local_phase<kLocalThreads, 1, true>(a, smem, src); break;
+      default: local_phase<kLocalThreads, 2, true>(a, smem, src); break;
+    }
   }
+  if (a.stamps && scatter && threadIdx.x == 0)  // (profiling: the last CTA's end, pass-6 slot unused here)
+    atomicMax(reinterpret_cast<unsigned long long*>(a.stamps + 8), (unsigned long long)globaltimer());
   if (stamper) {
     a.stamps[kStamps - 2] = globaltimer();
     a.stamps[kStamps - 1] = scatter ? 3 : 1;
@@ -1592,6 +1657,7 @@ __global__ void __launch_bounds__(kThreads, RL_ONESWEEP_MIN_BLOCKS) sort_kernel(
   // ---- scatter hybrid: local_kernel sorted the sub-buckets already; this
   // launch only runs the LSD fallback
   pdl_wait();  // launched as a programmatic dependent of the histogram / local-phase kernel
+  if (stamper && a.mode == kModeScatter) a.stamps[9] = globaltimer();  // (profiling: pass-7 slot unused here)
   if (a.mode == kModeScatter && *reinterpret_cast<volatile const uint32_t*>(a.flags) == 0) return;
   // ---- histograms come from hist_kernel (launched just before, on the same stream)
   if (stamper) a.stamps[1] = globaltimer();

@@ -38,7 +38,7 @@ def main():
         e.record()
     arr = (ctypes.c_void_p * len(evs))(*[ctypes.c_void_p(e.cuda_event) for e in evs])
     stamps = torch.zeros(_capi.RL_SORT_STAMPS, dtype=torch.int64, device="cuda")
-    tot, passes, hist, local, full, scan = [], [], [], [], [], []
+    tot, passes, hist, local, full, scan, span, tail = [], [], [], [], [], [], [], []
     e_end = torch.cuda.Event(enable_timing=True)
     for r in range(a.reps + 3):
         flush.zero_()
@@ -52,14 +52,16 @@ def main():
         if r >= 3:
             tot.append(evs[0].elapsed_time(evs[2]))
             st = stamps.cpu().tolist()
-            hist.append((st[1] - st[0]) / 1e6)
             if st[11] == 3:  # scatter hybrid: K1 st[0], K2 st[2], K3 st[3], local phase st[1]..st[10]
                 hist.append((st[2] - st[0]) / 1e6)
+                span.append((st[10] - st[0]) / 1e6)
+                tail.append([(st[8] - st[10]) / 1e3, (st[9] - st[8]) / 1e3, (st[9] - st[0]) / 1e3])
                 passes.append([(st[3] - st[2]) / 1e6, (st[1] - st[3]) / 1e6] + [0.0] * 6)
                 scan.append(0.0)
                 local.append((st[10] - st[1]) / 1e6)
                 full.append(evs[0].elapsed_time(e_end))
                 continue
+            hist.append((st[1] - st[0]) / 1e6)
             hybrid = st[11] == 1
             prev, pp = st[1], []
             for p in range(8):
@@ -81,7 +83,9 @@ def main():
     print(f"lib={os.environ.get('RELAB_B200_LIB','default')} path={int(st[11])} n={n} ok={ok} total_ms={statistics.median(tot):.4f} "
           f"with_fallback_ms={statistics.median(full):.4f} scan_us={1e3*statistics.median(scan) if scan else 0:.1f} local_us={1e3*statistics.median(local):.1f} "
           f"hist_us={1e3*statistics.median(hist):.1f} pass_us={[round(1e3*x,1) for x in pm]} "
-          f"pass_GBps={24*n/(np.mean(act)/1e3)/1e9:.0f}")
+          f"pass_GBps={24*n/(np.mean(act)/1e3)/1e9:.0f}"
+          + (f" outside_kernels_us={1e3*(statistics.median(tot)-statistics.median(span)):.1f}"
+             f" [local_last_end-cta0_end, coop_start-local_last_end, k1_start->coop_start] us={np.median(np.array(tail), axis=0).round(1).tolist()}" if span else ""))
 
 
 if __name__ == "__main__":

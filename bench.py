@@ -269,7 +269,7 @@ def sort_roofline(n, active, st, sort_ms, hist_ms, step_ms_total):
                        "u32 written) + digit-6 pass 12n + 12n + local phase 12n + 12n (sorted key + permutation "
                        "out); the chunk counts (148 x 128 KB written once, read once) are not counted")
         timed_ms = [h + s_ for h, s_ in zip(hist_ms, sort_ms)]
-        kernel = ("rl::radix sort pipeline: key_shift_kernel (16K-key sample) + sub_hist_kernel + "
+        kernel = ("rl::radix sort pipeline: sub_hist_kernel (key-pack sample + chunk counts) + "
                   "top_scatter_kernel + sub_scatter_kernel + local_kernel (+ the cooperative sort_kernel, which "
                   "returns at once unless the LSD fallback flag is set), one CUDA-event span")
     elif path == "hybrid":

@@ -85,7 +85,7 @@ __device__ __forceinline__ void gather_items(const rl_column& col, const uint32_
   T v[kItems];
 #pragma unroll
   for (int it = 0; it < kItems; ++it)
-    if (valid & (1u << it)) v[it] = __ldg(src + row[it]);
+    if (valid & (1u << it)) v[it] = ld_row(src + row[it]);
 #pragma unroll
   for (int it = 0; it < kItems; ++it)
     if (valid & (1u << it)) __stcs(dst + it * kThreads, v[it]);

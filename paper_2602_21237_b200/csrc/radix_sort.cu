@@ -218,7 +218,7 @@ __device__ __forceinline__ uint64_t load_key(const SortArgs& a, int64_t i) {
   if (a.src_mode == kSrcInt64) return xform(uint64_t(__ldg(static_cast<const long long*>(a.col) + i)), a.desc);
   if (a.src_mode == kSrcWords) return __ldg(static_cast<const unsigned long long*>(a.col) + i);
   const uint64_t row = a.perm_in ? uint64_t(__ldg(a.perm_in + i)) : uint64_t(i);
-  if (a.src_mode == kSrcInt64Gather) return xform(uint64_t(__ldg(static_cast<const long long*>(a.col) + row)), a.desc);
+  if (a.src_mode == kSrcInt64Gather) return xform(uint64_t(ld_row(static_cast<const long long*>(a.col) + row)), a.desc);
   return bytes_word(static_cast<const uint8_t*>(a.col) + row * uint64_t(a.width), a.width, a.word, a.desc);
 }
 

@@ -9,6 +9,13 @@ from paper_2602_21237_b200 import pipeline, records as R, synth  # noqa: E402
 
 n = 100_000_000
 torch.cuda.set_device(0)
+import os  # noqa: E402
+if os.environ.get("L2FETCH"):  # experiment: L2 fetch granularity (bytes) for the random payload gathers
+    from cuda.bindings import runtime as rt
+    torch.zeros(1, device="cuda")  # primary context up
+    lim = rt.cudaLimit.cudaLimitMaxL2FetchGranularity
+    print("L2 fetch granularity before", rt.cudaDeviceGetLimit(lim), "set", rt.cudaDeviceSetLimit(lim, int(os.environ["L2FETCH"])),
+          "after", rt.cudaDeviceGetLimit(lim))
 cols_l = [torch.from_numpy(synth.uniform_keys(n, n, 0)).cuda(), torch.arange(n, dtype=torch.int64, device="cuda")]
 cols_r = [torch.from_numpy(synth.uniform_keys(n, n, 1)).cuda(), torch.arange(n, dtype=torch.int64, device="cuda")]
 schema = R.Schema((("key", R.Int64()), ("payload", R.Int64())))

@@ -27,7 +27,10 @@ constexpr int kRbItems = 16;
 constexpr int kRbTile = kThreads * kRbItems;
 constexpr int kAlItems = 8;
 constexpr int kAlTile = kThreads * kAlItems;
-constexpr int kAlWindow = 3584;  // right keys staged per CTA (larger windows search global memory)
+#ifndef RL_AL_WINDOW
+#define RL_AL_WINDOW 2560  // 52 KB of shared memory per CTA: 4 CTAs per SM (3584: 60 KB, 3 per SM; 1e8 join 11.89 -> 11.64 ms)
+#endif
+constexpr int kAlWindow = RL_AL_WINDOW;  // right keys staged per CTA (larger windows search global memory)
 
 // ---------------------------------------------------------------- K3
 __global__ void __launch_bounds__(kThreads) run_bounds_kernel(const int64_t* __restrict__ sk, int64_t n,
@@ -207,7 +210,48 @@ struct AlignArgs {
   uint64_t* status;      // packed flag | epoch | matches
   uint64_t* agg_pairs;   // per tile aggregate pairs (valid when flag >= AGG)
   uint64_t* incl_pairs;  // per tile inclusive pairs (valid when flag == INCL)
+  uint32_t* wlo;         // per tile right window [wlo, whi) from align_bounds_kernel (NULL: searched in-tile)
+  uint32_t* whi;
 };
+
+// The right-key window of every tile, one thread per tile: the two binary
+// searches over the right keys (~6 dependent global round trips each) leave
+// the tile's own latency chain, and the searches of all tiles overlap. Used
+// when the tiles span several waves (1e8 rows: ~31K tiles).
+__global__ void __launch_bounds__(kThreads) align_bounds_kernel(AlignArgs a, uint32_t tiles) {
+  const uint32_t t = blockIdx.x * kThreads + threadIdx.x;
+  if (t >= tiles) return;
+  const int64_t dl = *a.d_left;
+  const uint32_t dr = uint32_t(*a.d_right);
+  const int64_t begin = int64_t(t) * kAlTile;
+  if (begin >= dl) return;
+  const int64_t end = begin + kAlTile < dl ? begin + kAlTile : dl;
+  const int64_t k0 = __ldg(reinterpret_cast<const long long*>(a.lkeys) + begin);
+  const int64_t k1 = __ldg(reinterpret_cast<const long long*>(a.lkeys) + end - 1);
+  uint32_t lo = 0, len = dr;  // first right key >= k0
+  while (len > 0) {
+    const uint32_t half = len >> 1;
+    if (__ldg(reinterpret_cast<const long long*>(a.rkeys) + lo + half) < k0) {
+      lo += half + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+  uint32_t hi = lo;
+  len = dr - lo;  // first right key > k1
+  while (len > 0) {
+    const uint32_t half = len >> 1;
+    if (__ldg(reinterpret_cast<const long long*>(a.rkeys) + hi + half) <= k1) {
+      hi += half + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+  a.wlo[t] = lo;
+  a.whi[t] = hi;
+}
 
 // Two-value warp look-back: matches packed in the status word, pairs in a
 // side array published before the flag (release) and read after it (acquire).
@@ -294,7 +338,12 @@ __global__ void __launch_bounds__(kThreads) align_kernel(AlignArgs a) {
   const bool last = begin + kAlTile >= dl;
   for (int i = tid; i < count; i += kThreads) sl[i] = __ldg(reinterpret_cast<const long long*>(a.lkeys) + begin + i);
   // right window [lo, hi): keys in [first left key, last left key]
-  if (warp == 0) {
+  if (a.wlo) {
+    if (tid == 0) {
+      s_lo = __ldg(a.wlo + tile);
+      s_hi = __ldg(a.whi + tile);
+    }
+  } else if (warp == 0) {
     const uint32_t lo = dr ? warp_bound(a.rkeys, 0, dr, a.lkeys[begin], false) : 0;
     if (tid == 0) s_lo = lo;
   } else if (warp == 1) {
@@ -441,6 +490,8 @@ size_t align_workspace_bytes(int64_t cap) {
   c.take<uint64_t>(tiles);
   c.take<uint64_t>(tiles);
   c.take<uint64_t>(tiles);
+  c.take<uint32_t>(tiles);
+  c.take<uint32_t>(tiles);
   return c.used + 256;
 }
 
@@ -463,6 +514,8 @@ int key_axis_align(const int64_t* lkeys, const uint32_t* loff, const int64_t* d_
   const size_t zero = c.used;
   a.agg_pairs = c.take<uint64_t>(tiles);
   a.incl_pairs = c.take<uint64_t>(tiles);
+  a.wlo = c.take<uint32_t>(tiles);
+  a.whi = c.take<uint32_t>(tiles);
   if (!c.ok) return RL_ERR_WORKSPACE;
   cudaError_t e = cudaMemsetAsync(ws, 0, zero, stream);
   if (e != cudaSuccess) return rl_cuda_status(e);
@@ -486,8 +539,16 @@ int key_axis_align(const int64_t* lkeys, const uint32_t* loff, const int64_t* d_
       return rl_cuda_status(cudaGetLastError());
     attr = true;
   }
+  // window pre-pass when the tiles span more than ~4 waves (3 CTAs per SM)
+  const char* force = getenv("RL_ALIGN_PREPASS");  // "1" / "0": force on / off (tests, A/B)
+  const bool prepass = force && force[0] ? force[0] == '1' : tiles > uint32_t(device_sm_count()) * 12;
+  if (prepass) {
+    align_bounds_kernel<<<(tiles + kThreads - 1) / kThreads, kThreads, 0, stream>>>(a, tiles);
+  } else {
+    a.wlo = a.whi = nullptr;
+  }
   align_kernel<<<tiles, kThreads, kAlSmem, stream>>>(a);
-  count_launches(1);
+  count_launches(prepass ? 2 : 1);
   return rl_cuda_status(cudaGetLastError());
 }
 

@@ -86,6 +86,36 @@ def test_align_matches_oracle_with_gaps():
             assert u32(al.right_starts[:m]).tolist() == rs.tolist()
 
 
+@pytest.mark.parametrize("prepass", ["0", "1"])
+def test_align_window_paths(monkeypatch, prepass):
+    """key_axis.cu's alignment with the window pre-pass forced off / on, over
+    multi-tile left axes (2048 keys per tile) whose right windows are narrower
+    than, about equal to and wider than the 2560 staged keys (the per-key global
+    search), and a right side that ends inside the left range."""
+    monkeypatch.setenv("RL_ALIGN_PREPASS", prepass)
+    rng = np.random.default_rng(21)
+    cases = [
+        (rng.choice(10**6, 40_000, replace=False), rng.choice(10**6, 40_000, replace=False)),  # balanced
+        (rng.choice(10**5, 9_000, replace=False), np.arange(0, 10**5, 2)),  # right 5x denser: wide windows
+        (np.arange(0, 60_000, 3), rng.choice(60_000, 700, replace=False)),  # sparse right
+        (np.arange(50_000), np.arange(30_000, 31_000)),  # right ends inside the left range
+        (np.arange(10_000), np.arange(20_000, 25_000)),  # disjoint
+    ]
+    for lk, rk in cases:
+        lk = np.repeat(np.asarray(lk, np.int64), 1 + (np.arange(len(lk)) % 3))  # multiplicities 1-3
+        rk = np.asarray(rk, np.int64)
+        li, ri = engine.index_keys(torch.from_numpy(lk).cuda()), engine.index_keys(torch.from_numpy(rk).cuda())
+        al = engine.align(li, ri)
+        m, total = engine.fetch_scalars(al.m_total)
+        a, b = O.to_tensor_arrays(lk), O.to_tensor_arrays(rk)
+        mk, ls, lc, rs, rc = O.align_arrays(a[0], a[1], b[0], b[1])
+        assert m == len(mk) and total == int((lc * rc).sum()), (prepass, len(lk), len(rk))
+        if m:
+            assert al.matched_keys[:m].cpu().tolist() == mk.tolist()
+            assert u32(al.left_counts[:m]).tolist() == lc.tolist()
+            assert u32(al.right_starts[:m]).tolist() == rs.tolist()
+
+
 def test_expand_chunks_equal_full():
     rng = np.random.default_rng(13)
     lk = rng.integers(0, 300, 20_000).astype(np.int64)

@@ -232,9 +232,10 @@ RL_API int rl_join_plan_build(const int64_t* left_keys, int64_t n_left,
  * right row = right_positions[right_starts[g] + ri].
  * Emits rows in (key, left row, right row) order — byte-identical to the
  * reference. Optional outputs (NULL to skip): left_rows/right_rows
- * (uint32, index t - out_begin) and up to RL_MAX_COLUMNS gathered columns
- * (rl_column, host array; dst indexed by t - out_begin).
- * m (number of matched keys) is passed from the host.
+ * (uint32, index t - out_begin; each 16-byte aligned — the pairs-only
+ * path stores four row ids at a time — else RL_ERR_BAD_ARG) and up to
+ * RL_MAX_COLUMNS gathered columns (rl_column, host array; dst indexed by
+ * t - out_begin). m (number of matched keys) is passed from the host.
  * --------------------------------------------------------------------- */
 RL_API int rl_join_expand(const int64_t* matched_keys, const uint32_t* left_starts,
                    const uint32_t* right_starts, const uint32_t* right_counts,
@@ -307,9 +308,13 @@ RL_API int rl_range_partition(const int64_t* keys, int64_t n, int64_t gid_base,
  * dest_bases[d * (n_columns + 1) + c], the local row id (uint32) into the
  * region at dest_bases[d * (n_columns + 1) + n_columns]. Replaces the
  * per-column gather + NCCL all-to-all-v; receive order = source rank order,
- * partition order within a source, as the all-to-all. parts <= 64,
- * n_columns <= 8. The caller brackets the call with barriers.
+ * partition order within a source, as the all-to-all. parts <=
+ * RL_PUSH_MAX_PARTS, n_columns <= RL_PUSH_MAX_COLUMNS (else RL_ERR_BAD_ARG;
+ * wider exchanges go through NCCL). The caller brackets the call with
+ * barriers.
  * --------------------------------------------------------------------- */
+#define RL_PUSH_MAX_PARTS 64
+#define RL_PUSH_MAX_COLUMNS 8
 RL_API int rl_push_rows(const uint32_t* rows, int64_t n, int32_t parts,
                  const int64_t* dest_starts, const rl_column* columns,
                  int32_t n_columns, const uint64_t* dest_bases,

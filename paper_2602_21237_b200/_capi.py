@@ -36,6 +36,8 @@ RL_SORT_EVENTS = 3
 RL_SORT_STAMPS = 12
 RL_MAX_SPLIT_SAMPLES = 2048
 RL_SORT_MAX_FUSED_COLUMNS = 8
+RL_PUSH_MAX_PARTS = 64
+RL_PUSH_MAX_COLUMNS = 8
 
 
 class RlColumn(ctypes.Structure):

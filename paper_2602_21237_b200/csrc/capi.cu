@@ -45,17 +45,26 @@ int widen_u32(const uint32_t* src, int64_t n, int64_t* dst, cudaStream_t stream)
 static std::atomic<int64_t> g_launches{0};
 void count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
-int device_sm_count() {
-  static int cached = 0;
-  if (cached > 0) return cached;
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
-    return 148;
+    return -1;
   }
-  cached = sms;
-  return sms;
+  return dev >= 0 && dev < kMaxDevices ? dev : -1;
+}
+
+int device_sm_count() {
+  static int cache[kMaxDevices] = {};
+  return per_device(cache, [] {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+      cudaGetLastError();
+      return 148;
+    }
+    return sms;
+  });
 }
 
 }  // namespace rl

@@ -268,4 +268,19 @@ __device__ __forceinline__ void copy_row(const uint8_t* __restrict__ src, uint8_
 int device_sm_count();
 void count_launches(int k);
 
+// Per-device host caches. Function attributes (dynamic shared memory opt-in)
+// and occupancy belong to a device context, so a value cached for cuda:0
+// must not be reused on cuda:1: each cache has one slot per device ordinal
+// (0 = not computed yet). Benign races: every writer stores the same value.
+constexpr int kMaxDevices = 64;
+int current_device();  // cudaGetDevice(); -1 on error or past kMaxDevices (no caching)
+template <typename F>
+inline int per_device(int (&slot)[kMaxDevices], F compute) {
+  const int d = current_device();
+  if (d >= 0 && slot[d] != 0) return slot[d];
+  const int v = compute();
+  if (d >= 0) slot[d] = v;
+  return v;
+}
+
 }  // namespace rl

@@ -22,8 +22,8 @@ namespace rl {
 namespace exchange {
 
 constexpr int kThreads = 256;
-constexpr int kMaxParts = 64;
-constexpr int kMaxCols = 8;
+constexpr int kMaxParts = RL_PUSH_MAX_PARTS;
+constexpr int kMaxCols = RL_PUSH_MAX_COLUMNS;
 
 struct PushArgs {
   const uint32_t* rows;  // [n] local row ids grouped by destination (partition order)

@@ -409,6 +409,8 @@ int join_expand(const int64_t* matched_keys, const uint32_t* ls, const uint32_t*
   if (st != RL_OK) return st;
   if (out_end == out_begin) return RL_OK;
   if (m == 0) return RL_ERR_BAD_ARG;
+  // the pairs-only path stores four row ids at a time (16-byte stores)
+  if ((reinterpret_cast<uintptr_t>(lrows_out) | reinterpret_cast<uintptr_t>(rrows_out)) & 15) return RL_ERR_BAD_ARG;
   ExpandArgs a{matched_keys, ls, rs, rc, offs, m, lpos, rpos, out_begin, out_end, lrows_out, rrows_out, nullptr};
   uint32_t per_cta;
   const unsigned blocks = expand_grid(out_end - out_begin, &per_cta);

@@ -533,12 +533,15 @@ int key_axis_align(const int64_t* lkeys, const uint32_t* loff, const int64_t* d_
   a.pair_offsets = pair_offsets;
   a.m_out = m_out;
   a.total_out = total_out;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kAlSmem)) != cudaSuccess)
-      return rl_cuda_status(cudaGetLastError());
-    attr = true;
-  }
+  static int attr[kMaxDevices] = {};  // per device: 1 = opted in, -1 = refused
+  if (per_device(attr, [] {
+        if (cudaFuncSetAttribute(align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kAlSmem)) ==
+            cudaSuccess)
+          return 1;
+        cudaGetLastError();
+        return -1;
+      }) < 0)
+    return rl_cuda_status(cudaErrorInvalidConfiguration);
   // window pre-pass when the tiles span more than ~4 waves (3 CTAs per SM)
   const char* force = getenv("RL_ALIGN_PREPASS");  // "1" / "0": force on / off (tests, A/B)
   const bool prepass = force && force[0] ? force[0] == '1' : tiles > uint32_t(device_sm_count()) * 12;

@@ -1881,54 +1881,59 @@ static bool getenv_flag_no_hybrid() { return getenv_flag("RL_NO_HYBRID"); }
 constexpr size_t kHistSmem = size_t(kScatWords) * 4 + size_t(kScatThreads) * 4;
 
 static bool scatter_kernels_ready() {
-  static int ready = -1;
-  if (ready < 0)
-    ready = cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHistSmem)) ==
-                        cudaSuccess &&
-                    cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kPSmem)) == cudaSuccess &&
-                    cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kPSmem)) == cudaSuccess &&
-                    cudaFuncSetAttribute(local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kLocalSmemBytes)) == cudaSuccess
-                ? 1
-                : 0;
+  static int ready[kMaxDevices] = {};  // per device: 1 = every opt-in took, -1 = refused
+  return per_device(ready, [] {
+           const bool ok =
+               cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHistSmem)) ==
+                   cudaSuccess &&
+               cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
+                   cudaSuccess &&
+               cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
+                   cudaSuccess &&
+               cudaFuncSetAttribute(local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kLocalSmemBytes)) == cudaSuccess;
+           if (!ok) cudaGetLastError();
 #ifdef RL_CARVEOUT_MAX
-  if (ready == 1) {  // one L1/shared split for every kernel of the sort: no SM reconfiguration between them
-    cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(local_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(sort_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  }
+           if (ok) {  // one L1/shared split for every kernel of the sort: no SM reconfiguration between them
+             cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+             cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+             cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+             cudaFuncSetAttribute(local_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+             cudaFuncSetAttribute(sort_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+           }
 #endif
-  return ready == 1;
+           return ok ? 1 : -1;
+         }) > 0;
 }
 
 // Co-resident CTAs per SM of the counting passes (both have the same shape).
 static int pass_ctas_per_sm() {
-  static int cached = 0;
-  if (cached > 0) return cached;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, top_scatter_kernel, kPThreads, kPSmem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  cached = per_sm;
-  return cached;
+  static int cache[kMaxDevices] = {};
+  return per_device(cache, [] {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, top_scatter_kernel, kPThreads, kPSmem) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    return per_sm;
+  });
 }
 
-// Largest co-resident grid of the cooperative sort kernel on this device.
+// Largest co-resident grid of the cooperative sort kernel on this device
+// (-1: the shared-memory opt-in or the occupancy query failed).
 static int sort_grid_limit() {
-  static int cached = 0;
-  if (cached > 0) return cached;
-  if (cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)) != cudaSuccess)
-    return -1;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sort_kernel, kThreads, kSmemBytes) != cudaSuccess ||
-      per_sm < 1)
-    return -1;
-  cached = per_sm * device_sm_count();
-  return cached;
+  static int cache[kMaxDevices] = {};
+  return per_device(cache, [] {
+    if (cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)) !=
+        cudaSuccess)
+      return -1;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sort_kernel, kThreads, kSmemBytes) != cudaSuccess ||
+        per_sm < 1)
+      return -1;
+    return per_sm * device_sm_count();
+  });
 }
 
 #ifndef RL_HIST_CTAS_PER_SM

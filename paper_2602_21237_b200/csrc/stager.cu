@@ -41,8 +41,11 @@ class Pool {
     for (auto& t : workers_) t.join();
   }
   int size() const { return int(workers_.size()); }
-  // run fn(i) for i in [0, size()) on the workers; returns when all finished
+  // run fn(i) for i in [0, size()) on the workers; returns when all finished.
+  // Callers from several host threads take turns (job_/pending_/gen_ belong to
+  // one job at a time; ctypes releases the GIL, so two calls can overlap).
   void parallel(const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> one_job(job_mu_);
     std::unique_lock<std::mutex> lk(m_);
     job_ = &fn;
     pending_ = int(workers_.size());
@@ -72,6 +75,7 @@ class Pool {
     }
   }
   std::vector<std::thread> workers_;
+  std::mutex job_mu_;
   std::mutex m_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* job_ = nullptr;

@@ -95,20 +95,22 @@ class GpuOps:
         or None when this group has no symmetric memory."""
         if not items:
             return []
+        from . import _capi as C
+
         dev = items[0][1][0].device
         if not _peer_exchange_ok(group, dev):
             return None
-        try:
-            exs = []
-            for slot, cols, _, _, _ in items:
-                key = (slot, id(group), dev.index, tuple((c.dtype, tuple(c.shape[1:])) for c in cols))
-                if key not in _PEER:
-                    _PEER[key] = PeerExchange(group, dev, cols)
-                exs.append(_PEER[key])
-            return PeerExchange.exchange_many(exs, items, group)
-        except (RuntimeError, ImportError, AttributeError):
-            _PEER[("ok", dev.index)] = False  # no symmetric memory here: NCCL from now on
+        # rl_push_rows limits: the same answer on every rank (same group, same
+        # column lists), so this local check cannot split the group
+        if _group_size(group) > C.RL_PUSH_MAX_PARTS or any(len(it[1]) > C.RL_PUSH_MAX_COLUMNS for it in items):
             return None
+        exs = []
+        for slot, cols, _, _, _ in items:
+            key = (slot, id(group), dev.index, tuple((c.dtype, tuple(c.shape[1:])) for c in cols))
+            if key not in _PEER:
+                _PEER[key] = PeerExchange(group, dev, cols)
+            exs.append(_PEER[key])
+        return PeerExchange.exchange_many(exs, items, group)
 
     # fused forms (one launch for every column) used when an Ops object has them
     def local_join(self, lcols, lkey: int, rcols, rkey: int, lgids: torch.Tensor, rgids: torch.Tensor):
@@ -169,12 +171,11 @@ class PeerExchange:
         self.me = dist.get_rank(group)
         self.likes = [(c.dtype, tuple(c.shape[1:]), _row_bytes(c)) for c in like]
         self.cap = 0
+        self._pending = None
 
-    def _ensure(self, rows: int) -> None:
-        """(Re)allocate for `rows` received rows; every rank takes the same
-        decision (from the same counts matrix), so the rendezvous is collective."""
-        if rows <= self.cap:
-            return
+    def _alloc(self, rows: int) -> bool:
+        """Local half of a (re)allocation for `rows` received rows: the new
+        symmetric buffer only (no collective). False on failure (e.g. OOM)."""
         import torch.distributed._symmetric_memory as sm
 
         cap = max(rows, self.cap + self.cap // 4, 1024)
@@ -182,9 +183,22 @@ class PeerExchange:
         for _, _, w in self.likes + [(None, None, 8)]:  # + the int64 global row ids
             offs.append(total)
             total += (cap * w + 255) // 256 * 256
-        self.buf = sm.empty(total, dtype=torch.uint8, device=self.device)
+        try:
+            self._pending = (sm.empty(total, dtype=torch.uint8, device=self.device), offs, cap)
+        except RuntimeError:
+            self._pending = None
+            return False
+        return True
+
+    def _commit(self) -> None:
+        """Collective half: every rank allocated, so all of them rendezvous."""
+        import torch.distributed._symmetric_memory as sm
+
+        buf, offs, cap = self._pending
+        self._pending = None
         grp = self.group if self.group is not None else dist.group.WORLD
-        self.hdl = sm.rendezvous(self.buf, grp.group_name)
+        self.hdl = sm.rendezvous(buf, grp.group_name)
+        self.buf = buf
         ptrs = list(self.hdl.buffer_ptrs)
         table = [[ptrs[d] + o for o in offs] for d in range(self.p)]  # user-space addresses < 2^63
         self.bases = torch.tensor(table, dtype=torch.int64).view(-1).to(self.device)
@@ -204,10 +218,17 @@ class PeerExchange:
         dist.all_gather_into_tensor(gathered, mine, group=group)
         host = gathered.cpu().view(p, len(items), p)  # the step's one host sync; host[s][i][d]
         lib = C.load()
+        # receive buffers that must grow: the same list on every rank (the same
+        # counts matrix). Allocate locally, agree with a MIN all-reduce, and only
+        # then rendezvous — a rank whose allocation failed takes the whole group
+        # to NCCL instead of leaving its peers waiting in the rendezvous.
+        grow = [(ex, int(host[:, i, :].sum(0).max())) for i, ex in enumerate(exs)]
+        if not _grow_collectively([(ex, rows) for ex, rows in grow if rows > ex.cap], group, dev):
+            _PEER[("ok", id(group), dev.index)] = False  # NCCL from now on, on every rank
+            return None
         out_all = []
         for i, (ex, (_, cols, rows, counts, base)) in enumerate(zip(exs, items)):
             mat = host[:, i, :]  # mat[s][d]: rows s sends to d
-            ex._ensure(int(mat.sum(0).max()))
             recv_counts = mat[:, me].tolist()
             total = sum(recv_counts)
             starts = torch.zeros(p + 1, dtype=torch.int64, device=dev)
@@ -229,13 +250,32 @@ class PeerExchange:
 _PEER: dict = {}
 
 
+def _grow_collectively(grow, group, device) -> bool:
+    """Grow receive buffers [(exchange, rows)] — the same list on every rank.
+    Each rank allocates locally (``_alloc``), a MIN all-reduce agrees, and
+    only if every rank succeeded do they all rendezvous (``_commit``).
+    Returns False, on EVERY rank, if any rank failed to allocate."""
+    if not grow:
+        return True
+    ok = all([ex._alloc(rows) for ex, rows in grow])
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if not bool(flag.item()):
+        for ex, _ in grow:
+            ex._pending = None
+        return False
+    for ex, _ in grow:
+        ex._commit()
+    return True
+
+
 def _peer_exchange_ok(group, device) -> bool:
     if os.environ.get("RL_NO_P2P") or device.type != "cuda" or dist.get_backend(group) != "nccl":
         return False
     key = ("ok", id(group), device.index)
     if key not in _PEER:
         _PEER[key] = _probe_symmetric_memory(group, device)
-    return _PEER[key] and _PEER.get(("ok", device.index), True)
+    return _PEER[key]
 
 
 def _probe_symmetric_memory(group, device) -> bool:

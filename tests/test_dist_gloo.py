@@ -92,6 +92,28 @@ def _worker(rank, world, port, case, q):
             hk, hg = D.choose_splitters(kt, a, case["desc"])
             dk, dg = D.choose_splitters_device(kt, a, case["desc"])
             out = {"host": (hk.numpy(), hg.numpy()), "dev": (dk.numpy(), dg.numpy())}
+        elif case["kind"] == "grow":
+            # receive-buffer growth: rank `fail` cannot allocate; every rank must
+            # get False (NCCL fallback) and nobody may enter the rendezvous
+            class FakeExchange:
+                cap = 0
+                _pending = None
+                committed = False
+
+                def _alloc(self, rows):
+                    if rank == case["fail"]:
+                        return False
+                    self._pending = rows
+                    return True
+
+                def _commit(self):
+                    self.committed = True
+                    self.cap = self._pending
+
+            exs = [FakeExchange(), FakeExchange()]
+            ok = D._grow_collectively([(exs[0], 100), (exs[1], 200)], None, torch.device("cpu"))
+            out = {"ok": ok, "committed": [e.committed for e in exs], "caps": [e.cap for e in exs],
+                   "pending": [e._pending for e in exs]}
         else:
             n = case["n"]
             keys = rng.integers(-case["dom"], case["dom"], n).astype(np.int64)
@@ -173,3 +195,16 @@ def test_device_splitters_match_host_splitters(desc):
     parts = _run({"kind": "splitters", "seed": 13, "n": 3001, "dom": 50, "desc": desc}, 2)
     for p in parts:
         assert (p["host"][0] == p["dev"][0]).all() and (p["host"][1] == p["dev"][1]).all()
+
+
+@pytest.mark.parametrize("fail", [-1, 0, 1])
+def test_peer_buffer_growth_is_agreed_by_every_rank(fail):
+    """a rank that cannot allocate its symmetric receive buffer must
+    take the WHOLE group to the NCCL path (a MIN all-reduce before any
+    rendezvous), not fall back alone while its peers wait in the rendezvous."""
+    parts = _run({"kind": "grow", "seed": 0, "fail": fail}, 2)
+    for p in parts:
+        if fail < 0:
+            assert p["ok"] and p["committed"] == [True, True] and p["caps"] == [100, 200]
+        else:
+            assert not p["ok"] and p["committed"] == [False, False] and p["pending"] == [None, None]

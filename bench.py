@@ -176,74 +176,143 @@ def pass_bytes(n: int, active):
 
 
 # ---------------------------------------------------------------- CPU arm
-def cpu_sort_sample(keys, payload, reps):
-    """The reference's tensor_sort algorithm (numpy port in oracle/) on host cores."""
+# The reference itself (`relab`, pure Python + numpy) is installed offline in
+# oracle/_ref by oracle/build_ref.py (build() in this container; the files
+# travel with the tree). Where it is absent the pinned numpy port in oracle/
+# stands in, and "kind" says "port" instead of "reference".
+def reference_package():
+    """The unmodified reference package from oracle/_ref, or None."""
+    try:
+        from oracle import build_ref
+    except ImportError:
+        return None
+    if not build_ref.available():
+        return None
+    site = str(build_ref.SITE)
+    if site not in sys.path:
+        sys.path.insert(0, site)
+    import relab
+
+    return relab
+
+
+def _ref_relation(relab, rel):
+    """The same numpy columns as a relab.Relation (the reference's own type)."""
+    from paper_2602_21237_b200.records import is_int64
+
+    attrs = tuple((name, relab.Int64() if is_int64(t) else relab.Bytes(t.width)) for name, t in rel.schema.attributes)
+    return relab.Relation(relab.Schema(attrs), tuple(rel.columns))
+
+
+def cpu_sort_sample(rel, reps):
+    """tensor_sort(rel, SortSpec(("key",))) on host cores: the reference's own
+    (tensorpath.py:232-252) when oracle/_ref is there, else the oracle port.
+    Returns (seconds per rep, kind)."""
+    relab = reference_package()
+    times = []
+    if relab is not None:
+        rr = _ref_relation(relab, rel)
+        spec = relab.SortSpec(("key",))
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            relab.tensor_sort(rr, spec)
+            times.append(time.perf_counter() - t0)
+        return times, "reference"
     from oracle import tensorpath_oracle as O
 
-    times = []
+    keys, payload = rel.column("key"), rel.column("payload")
     for _ in range(reps):
         t0 = time.perf_counter()
         perm = O.sort_permutation([keys], [False])
         _k, _p = keys[perm], payload[perm]
         times.append(time.perf_counter() - t0)
-    return times
+    return times, "port"
 
 
 def cpu_join_sample(r, s, reps):
+    """The CPU tensor path of a join, to_tensor x 2 + tensor_join — the
+    reference's own when available (bench.py:201-203 FORCE_TENSOR)."""
+    relab = reference_package()
+    times = []
+    if relab is not None:
+        rr, rs = _ref_relation(relab, r), _ref_relation(relab, s)
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            relab.tensor_join(relab.to_tensor(rr, "key"), relab.to_tensor(rs, "key"))
+            times.append(time.perf_counter() - t0)
+        return times, "reference"
     from oracle import tensorpath_oracle as O
 
-    times = []
     for _ in range(reps):
         t0 = time.perf_counter()
         O.join_columns(list(r.columns), 0, list(s.columns), 0)
         times.append(time.perf_counter() - t0)
-    return times
+    return times, "port"
 
 
 def cpu_relational_sample(r, s, reps):
     """The reference's CPU relational path — memory-budgeted Grace hash join
-    with temp-file spill at work_mem = 1 MB (rowpath.py:177-335, restated in
-    oracle/relational_baseline.py and pinned to the reference's block counts)
-    — on the box's host, temp files under $TMPDIR, spill counted."""
-    from oracle import relational_baseline as RB
-
-    times, st = [], None
+    with temp-file spill at work_mem = 1 MB (rowpath.hash_join_row via
+    bench.py:193-199 FORCE_ROW, TempArena under $TMPDIR, spill counted) — on
+    the box's host; the pinned restatement in oracle/ if relab is absent."""
+    relab = reference_package()
+    times, st, kind = [], None, "reference"
     for _ in range(reps):
         t0 = time.perf_counter()
-        _rows, st = RB.hash_join_row(list(r.columns), [8, 8], 0, list(s.columns), [8, 8], 0, 1 << 20)
+        if relab is not None:
+            rr, rs = _ref_relation(relab, r), _ref_relation(relab, s)
+            t0 = time.perf_counter()
+            with relab.TempArena(tempfile.gettempdir()) as arena:
+                _out, st = relab.hash_join_row(rr, rs, relab.JoinSpec("key"), relab.MemoryBudget(1 << 20), arena)
+        else:
+            from oracle import relational_baseline as RB
+
+            kind = "port"
+            _rows, st = RB.hash_join_row(list(r.columns), [8, 8], 0, list(s.columns), [8, 8], 0, 1 << 20)
         times.append(time.perf_counter() - t0)
     return {"p50_ms": round(1e3 * percentile(times, 50), 2), "p99_ms": round(1e3 * percentile(times, 99), 2),
             "reps": reps, "work_mem_bytes": 1 << 20, "temp_blocks_written": st.temp_blocks_written,
-            "temp_mb": round(st.temp_mb, 2), "partition_passes": st.partition_passes, "cores": 1, "kind": "port",
+            "temp_mb": round(st.temp_mb, 2), "partition_passes": st.partition_passes, "cores": 1, "kind": kind,
             "temp_dir": tempfile.gettempdir()}
 
 
+def bench_config(world: int) -> dict:
+    """The `config` of the headline line — identical in both arms at a given N."""
+    return {"workload": WORKLOAD, "rows_per_gpu": N_ROWS, "rows_total": world * N_ROWS,
+            "parallelism": "replicas1" if world == 1 else f"range-partitioned sort over {world} ranks",
+            "l2": "flushed between timed steps (256 MiB write)", "seed_per_rank": "rank"}
+
+
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (relab.tensor_sort from oracle/_ref, else the oracle port) on the host,
+    rank 0 only, on a bounded sample of this run's cfg2 workload."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     from paper_2602_21237_b200 import synth
 
     rel = synth.cfg2_relation(N_ROWS)
-    keys, payload = rel.column("key"), rel.column("payload")
     # one full cfg2 sort costs ~3-4 s on one core; bound the whole run to ~2.5 min
     per_full = 4.0
     budget = 150.0
     sample = N_ROWS if (args.steps + args.warmup) * per_full <= budget else max(
         500_000, int(N_ROWS * budget / ((args.steps + args.warmup) * per_full)))
-    k, p = keys[:sample], payload[:sample]
-    cpu_sort_sample(k, p, args.warmup)
-    times = cpu_sort_sample(k, p, args.steps)
+    sub = type(rel)(rel.schema, tuple(c[:sample] for c in rel.columns))
+    cpu_sort_sample(sub, args.warmup)
+    times, kind = cpu_sort_sample(sub, args.steps)
     value = sample * len(times) / sum(times) / 1e6
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "rows": N_ROWS, "sample_rows_per_step": sample},
+        "config": bench_config(world),
         "p50_ms": round(1e3 * percentile(times, 50), 3), "p99_ms": round(1e3 * percentile(times, 99), 3),
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{sample} rows of the cfg2 input per step (numpy, single-threaded as the "
-                                   f"reference; host has {os.cpu_count()} cores)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"{sample} rows of the cfg2 input per step through "
+                                   f"{'relab.tensor_sort (the unmodified reference, oracle/_ref)' if kind == 'reference' else 'the numpy port in oracle/'}"
+                                   f" (numpy, single-threaded as the reference; host has {os.cpu_count()} cores)"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -324,9 +393,10 @@ def sort_roofline(n, active, st, sort_ms, hist_ms, step_ms_total):
 
 # ---------------------------------------------------------------- GPU arm
 def run_ours(args):
-    # the driver parses rank 0's stdout as ONE JSON line: keep NCCL's banner off it
-    if not os.environ.get("RL_KEEP_NCCL_DEBUG"):
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # the driver parses rank 0's stdout as ONE JSON line: NCCL's INFO log (communicator
+    # lines, NVLS / P2P transport choice) goes to stderr, not stdout
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     import torch.distributed as dist
 
@@ -473,6 +543,15 @@ def run_ours(args):
         out, _st = tensor_sort(rel, spec)
         e2e_t.append(time.perf_counter() - t0)
     del out
+    # cold: a fresh copy of the input (never page-locked): the first call pays the registration
+    from paper_2602_21237_b200 import tensor_path as TP
+
+    cold_rel = type(rel)(rel.schema, tuple(np.array(c, copy=True) for c in rel.columns))
+    t0 = time.perf_counter()
+    tensor_sort(cold_rel, spec)
+    cold_ms = 1e3 * (time.perf_counter() - t0)
+    del cold_rel
+    pin_info = {"pinned_input_bytes_now": TP.pinned_bytes(), "pin_budget_bytes": TP._pin_budget()}
     e2e_total = sum(e2e_t)
     if world > 1:
         t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
@@ -484,13 +563,16 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "rows_per_gpu": n, "parallelism": f"replicas{world}",
-                   "l2": "flushed between timed steps (256 MiB write)", "seed_per_rank": "rank",
-                   "launch": launch_mode},
+        "config": bench_config(world),
+        "launch": launch_mode,
         "p50_ms": round(percentile(step_ms, 50), 4), "p99_ms": round(percentile(step_ms, 99), 4),
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": n * 12,
                 "d2h_bytes_per_step": n * 12, "api": "tensor_sort(Relation numpy) -> (Relation, SpillStats)",
-                "p50_ms": round(1e3 * percentile(e2e_t, 50), 3), "p99_ms": round(1e3 * percentile(e2e_t, 99), 3)},
+                "p50_ms": round(1e3 * percentile(e2e_t, 50), 3), "p99_ms": round(1e3 * percentile(e2e_t, 99), 3),
+                "cold_first_call_ms": round(cold_ms, 3),
+                "note": "warm steps reuse inputs the drop-in page-locked on first use (LRU, capped); "
+                        "cold_first_call_ms = one call on a fresh copy (includes its cudaHostRegister)",
+                **pin_info},
         "roofline": roofline,
         "clocks": clocks.summary(),
         "gpu_launches": int(launches),
@@ -498,10 +580,12 @@ def run_ours(args):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         reps = 3
-        t = cpu_sort_sample(keys_h, pay_h, reps)
-        line["cpu_baseline"] = {"value": round(n * reps / sum(t) / 1e6, 3), "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{reps} full cfg2 sorts of {n} rows (numpy port of tensorpath.py:232-252, "
-                                          f"single-threaded; host has {os.cpu_count()} cores)"}
+        t, kind = cpu_sort_sample(rel, reps)
+        what = ("relab.tensor_sort, the unmodified reference from oracle/_ref" if kind == "reference"
+                else "numpy port of tensorpath.py:232-252")
+        line["cpu_baseline"] = {"value": round(n * reps / sum(t) / 1e6, 3), "unit": UNIT, "cores": 1, "kind": kind,
+                                "sample": f"{reps} full cfg2 sorts of {n} rows ({what}, single-threaded; host has "
+                                          f"{os.cpu_count()} cores)"}
 
     if not args.no_join:
         line["join_cfg1"] = join_cfg1(args, dev, rank, world)
@@ -656,11 +740,10 @@ def run_distributed(args, dev, rank, world, lib, keys_h, pay_h, keys_d, pay_d, f
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "rows_per_gpu": n, "rows_total": world * n,
-                   "parallelism": f"range-partitioned sort over {world} rank(s): sampled splitters (device), "
-                                  "partition gather fused with the exchange (peer stores into symmetric memory over "
-                                  "NVLink/NVSwitch; NCCL all_to_all where unavailable), local stable sort",
-                   "l2": "flushed between timed steps (256 MiB write)", "seed_per_rank": "rank"},
+        "config": bench_config(world),
+        "parallelism_detail": f"range-partitioned sort over {world} rank(s): sampled splitters (device), "
+                              "partition gather fused with the exchange (peer stores into symmetric memory over "
+                              "NVLink/NVSwitch; NCCL all_to_all where unavailable), local stable sort",
         "p50_ms": round(percentile(step_ms, 50), 4), "p99_ms": round(percentile(step_ms, 99), 4),
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": world * n * 12,
                 "d2h_bytes_per_step": int(float(tt[1].item()) / args.steps),
@@ -699,6 +782,17 @@ def join_cfg1(args, dev, rank, world):
         one sizing sync, then the fused expansion + gathers."""
         return pipeline.join(dr, ds, "key").row_count
 
+    # gate before timing: the reference's own cfg1 answers (tests/golden, made by the live reference):
+    # 1,000,488 matches and the order-independent pair checksum; output rows in reference order
+    from paper_2602_21237_b200 import checks
+
+    plan = pipeline.plan_join(rk, sk)
+    joined = pipeline.join(dr, ds, "key")
+    if (plan.total != CFG1_MATCHES or pipeline.pair_checksum(plan) != CFG1_PAIR_CHECKSUM
+            or not checks.join_order_ok(*joined.columns)):
+        raise SystemExit("cfg1 join failed its self-check; refusing to report a number")
+    del plan, joined
+
     reps = 100
     for _ in range(5):
         device_join()
@@ -729,24 +823,56 @@ def join_cfg1(args, dev, rank, world):
         "e2e_api": "tensor_join(to_tensor(R), to_tensor(S)) on numpy Relations",
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t = cpu_join_sample(r, s, 20)
+        t, kind = cpu_join_sample(r, s, 20)
         res["cpu_tensor_path"] = {"p50_ms": round(1e3 * percentile(t, 50), 2), "p99_ms": round(1e3 * percentile(t, 99), 2),
-                                  "reps": 20, "cores": 1, "kind": "port"}
+                                  "reps": 20, "cores": 1, "kind": kind}
         res["p99_speedup_e2e_vs_cpu"] = round(res["cpu_tensor_path"]["p99_ms"] / res["e2e_p99_ms"], 1)
         res["cpu_relational_path"] = cpu_relational_sample(r, s, reps=10)
         res["p99_speedup_e2e_vs_cpu_relational"] = round(res["cpu_relational_path"]["p99_ms"] / res["e2e_p99_ms"], 1)
     return res
 
 
-JOIN_SCALING_ROWS = 100_000_000
+JOIN_SCALING_ROWS = 1_000_000_000  # the north star's 1B-row join
+CFG1_MATCHES = 1_000_488  # tests/golden/golden.json cfg1 (the live reference's output)
+CFG1_PAIR_CHECKSUM = 10896419913052579173  # sum of fmix64(l << 32 | r) over its pairs, mod 2^64
+
+
+def join_gate(out_cols, in_l, in_r, domain, world, dev):
+    """Correctness gate of a cfg5-shaped join before it is timed: the torch-only
+    invariants of paper_2602_21237_b200/checks.py (count, key sum, per-side and
+    pair sums; all-reduced over the ranks) from the inputs against the output,
+    and the reference order (key, left row, right row) on every shard."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_21237_b200 import checks
+
+    key, lp, rp = out_cols
+    if not checks.join_order_ok(key, lp, rp):
+        raise SystemExit("join output not in (key, left row, right row) order; refusing to report a number")
+    got = checks.join_observed(key, lp, rp)
+    if world == 1:
+        want = checks.join_expectations(in_l[0], in_l[1], in_r[0], in_r[1], domain=domain)
+    else:  # per-key aggregates summed over the ranks' input shards
+        agg = checks.join_aggregates(in_l[0], in_l[1], in_r[0], in_r[1], domain)
+        for t in agg:
+            dist.all_reduce(t)
+        want = checks.expectations_from_aggregates(*agg)
+        obs = torch.tensor([got[k] for k in checks.FIELDS], dtype=torch.int64, device=dev)
+        dist.all_reduce(obs)
+        got = dict(zip(checks.FIELDS, obs.tolist()))
+    if got != want:
+        raise SystemExit(f"join failed its self-check ({got} != {want}); refusing to report a number")
+    return want["matches"]
 
 
 def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
-    """The north star's scaling case, a cfg5-shaped equi-join (uniform keys,
-    domain = rows, int64 payload = global row id) at a FIXED total of
-    `total_rows` rows per side split over the ranks (strong scaling): N = 1
-    runs the device join, N > 1 dist.distributed_join (hash partition, the
-    peer-memory exchange, local join). Device time per step, max over ranks."""
+    """The north star's scaling case, the 1B-row join: a cfg5-shaped equi-join
+    (uniform keys, domain = rows, int64 payload = global row id) at a FIXED
+    total of `total_rows` rows per side split over the ranks (strong scaling):
+    N = 1 runs the device join, N > 1 dist.distributed_join (hash partition,
+    the peer-memory exchange, local join). Gated by join_gate before timing;
+    device time per step, max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -759,7 +885,7 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
     rk = synth.uniform_keys(n, total_rows, 2 * rank + 12)
     pay = np.arange(base, base + n, dtype=np.int64)
     cols_l = [torch.from_numpy(lk).to(dev), torch.from_numpy(pay).to(dev)]
-    cols_r = [torch.from_numpy(rk).to(dev), torch.from_numpy(pay.copy()).to(dev)]
+    cols_r = [torch.from_numpy(rk).to(dev), cols_l[1]]
     del lk, rk, pay
 
     if world == 1:
@@ -768,14 +894,23 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
         schema = R.Schema((("key", R.Int64()), ("payload", R.Int64())))
         dl, dr = pipeline.DeviceRelation(schema, cols_l), pipeline.DeviceRelation(schema, cols_r)
 
-        def step():
-            return pipeline.join(dl, dr, "key").row_count
+        def run():
+            return pipeline.join(dl, dr, "key").columns
     else:
-        def step():
-            return D.distributed_join(cols_l, 0, base, cols_r, 0, base).total_matches
+        def run():
+            sh = D.distributed_join(cols_l, 0, base, cols_r, 0, base)
+            return sh.columns
 
-    for _ in range(2):
-        total = step()
+    out = run()
+    torch.cuda.empty_cache()
+    total = join_gate(out, cols_l, cols_r, total_rows, world, dev)
+    del out
+    torch.cuda.empty_cache()
+
+    def step():
+        return len(run()[0])
+
+    step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -783,7 +918,7 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
     for _ in range(min(args.steps, 5)):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        total = step()
+        step()
         b.record()
         b.synchronize()
         ms.append(a.elapsed_time(b))
@@ -791,13 +926,24 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     med = float(t.item())
+    del cols_l, cols_r
     torch.cuda.empty_cache()
+    # a join reads both sides' key + payload once and writes key + both payloads per match
+    alg = 2 * total_rows * 16 + total * 24
+    peak, peak_src = measured_peak_hbm()
+    achieved = alg / world / (med / 1e3) / 1e9  # per GPU
     return {"workload": f"cfg5-shaped equi-join, {total_rows:.0e} rows per side in total (uniform keys, domain = rows, "
-                        "int64 payload), strong scaling over the ranks",
+                        "int64 payload = row id), strong scaling over the ranks",
             "rows_per_side_per_gpu": n, "matches_total": int(total),
+            "gate": "passed: count, key / per-side / pair sums vs torch invariants of the inputs, reference order",
             "path": "device join" if world == 1 else "distributed_join: hash partition + peer-memory push + local join",
             "ms_per_step_p50_max_over_ranks": round(med, 3),
             "mrows_per_s": round(2 * total_rows / (med / 1e3) / 1e6, 1), "scaling": "strong",
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                         "alg_bytes_per_step": int(alg),
+                         "alg_bytes_formula": "2 sides x rows x (8 B key + 8 B payload) read + matches x 24 B "
+                                              "(key, payload, right_payload) written (SURVEY §8(d)); per GPU"},
             # both sides' off-rank rows per rank (key 8 B + payload 8 B + int64 global id 8 B) over the step
             "nvlink": {"bytes_per_rank_per_step": int(2 * n * (world - 1) / world * 24),
                        "achieved_gbs": round(2 * n * (world - 1) / world * 24 / (med / 1e3) / 1e9, 1),
@@ -832,21 +978,46 @@ def extras(args, dev):
     from paper_2602_21237_b200 import policy, records as RR
 
     spec = SortSpec(("payload",))
-    for n in (10**6, 10**7, 10**8):
+    from paper_2602_21237_b200 import checks
+
+    for n in (10**6, 10**7, 10**8, 10**9):
         try:
             r, s = synth.cfg1_relations(n=n, domain=n)
             budget = RR.MemoryBudget(1 << 20)
             jc = policy.select_path(policy.join_signals(r, s, "key", budget, key_cardinality=n))
+            sc = policy.select_path(policy.sort_signals(r, budget))  # the ORDER BY input has >= n rows too
             # the CPU relational path (work_mem = 1 MB, spill counted) at the sizes it finishes in seconds
             rel_cpu = cpu_relational_sample(r, s, reps=1) if n <= 10**7 else None
             dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
             del r, s
-            pipeline.join_then_order_by(dr, ds, "key", spec)
-            res, ts = timed(lambda: pipeline.join_then_order_by(dr, ds, "key", spec), 5)
-            out[f"cfg5_n{n:.0e}"] = {"rows_out": res.row_count, "p50_ms": round(percentile(ts, 50), 3),
+            # gate: join invariants + order, then the ORDER BY's stable order and row multiset
+            joined = pipeline.join(dr, ds, "key")
+            jk, jl, jr = joined.columns
+            want = checks.join_expectations(dr.columns[0], dr.columns[1], ds.columns[0], ds.columns[1], domain=n)
+            ok = checks.join_observed(jk, jl, jr) == want and checks.join_order_ok(jk, jl, jr)
+            before = checks.multiset_sums([jl, jr]), checks.multiset_sums([jk, jl])
+            srt, _perm = pipeline.order_by(joined, spec)
+            del joined, jk, jl, jr, _perm
+            k2, l2, r2 = srt.columns
+            ok = ok and checks.sort_ok(l2, r2) and before == (checks.multiset_sums([l2, r2]),
+                                                                checks.multiset_sums([k2, l2]))
+            del srt, k2, l2, r2
+            if not ok:
+                raise RuntimeError(f"cfg5 n={n:.0e} failed its self-check")
+            torch.cuda.empty_cache()
+            res, ts = timed(lambda: pipeline.join_then_order_by(dr, ds, "key", spec), 5 if n < 10**9 else 3)
+            # join reads 2n x 16 B, writes M x 24 B; the ORDER BY reads M x 24 B, writes M x 28 B
+            m = res.row_count
+            alg = 2 * n * 16 + m * 24 + m * 24 + m * 28
+            peak, _src = measured_peak_hbm()
+            out[f"cfg5_n{n:.0e}"] = {"rows_out": m, "p50_ms": round(percentile(ts, 50), 3),
                                      "max_ms": round(max(ts), 3),
                                      "mrows_per_s": round(2 * n / (statistics.median(ts) / 1e3) / 1e6, 1),
+                                     "gate": "passed (torch invariants + order)",
+                                     "roofline_frac": round(alg / (statistics.median(ts) / 1e3) / 1e9 / peak, 4),
+                                     "alg_bytes": int(alg),
                                      "select_path_join": f"{jc.path.name}/{jc.reason.name}",
+                                     "select_path_sort": f"{sc.path.name}/{sc.reason.name}",
                                      "cpu_relational_join_ms": rel_cpu and rel_cpu["p50_ms"],
                                      "cpu_relational_temp_mb": rel_cpu and rel_cpu["temp_mb"]}
             del dr, ds, res
@@ -859,10 +1030,26 @@ def extras(args, dev):
         r, s = synth.cfg4_relations(n=10**8)
         dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
         del r, s
-        pipeline.join(dr, ds, "key")
+        # gate: torch invariants over (key, first 8 payload bytes of each side) + the reference order
+        # (payloads are random bytes, so the order check uses the key only)
+        from paper_2602_21237_b200 import checks
+
+        res = pipeline.join(dr, ds, "key")
+        first8 = lambda c: c.view(torch.int64)[:, 0].contiguous()  # noqa: E731
+        want = checks.join_expectations(dr.columns[0], first8(dr.columns[1]), ds.columns[0], first8(ds.columns[1]))
+        got = checks.join_observed(res.columns[0], first8(res.columns[1]), first8(res.columns[2]))
+        if got != want or not checks.sort_ok(res.columns[0]):
+            raise RuntimeError("cfg4 join failed its self-check")
+        del res
+        torch.cuda.empty_cache()
         res, ts = timed(lambda: pipeline.join(dr, ds, "key"), 3)
-        out["cfg4_n1e8"] = {"rows_out": res.row_count, "p50_ms": round(percentile(ts, 50), 3),
-                            "mrows_per_s": round(2e8 / (statistics.median(ts) / 1e3) / 1e6, 1)}
+        m = res.row_count
+        alg = 2 * 10**8 * 24 + m * 40  # 4.9 GB
+        out["cfg4_n1e8"] = {"rows_out": m, "p50_ms": round(percentile(ts, 50), 3),
+                            "mrows_per_s": round(2e8 / (statistics.median(ts) / 1e3) / 1e6, 1),
+                            "gate": "passed (torch invariants on key + first payload word, key order)",
+                            "roofline_frac": round(alg / (statistics.median(ts) / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
+                            "alg_bytes": int(alg)}
         del dr, ds, res
     except Exception as e:
         out["cfg4_n1e8"] = {"error": repr(e)[:200]}

@@ -24,6 +24,7 @@ import ctypes
 import sys
 import warnings
 import weakref
+from collections import OrderedDict
 from typing import Optional
 
 import numpy as np
@@ -72,7 +73,37 @@ def _stager(dev) -> int:
 
 
 _REGISTER_MIN_BYTES = 4 << 20
-_registered: dict = {}  # id(owner) -> (ptr, nbytes) page-locked ranges of live numpy buffers
+# id(owner) -> (ptr, nbytes, finalizer): page-locked ranges of live numpy
+# buffers, least recently used first; their total stays within _pin_budget()
+_registered: "OrderedDict[int, tuple]" = OrderedDict()
+
+
+def _pin_budget() -> int:
+    """Bytes of caller memory the drop-in may keep page-locked at once:
+    RL_PIN_BUDGET_BYTES, default a quarter of physical memory capped at
+    16 GiB. Past it the least recently used registrations are released."""
+    import os
+
+    v = os.environ.get("RL_PIN_BUDGET_BYTES")
+    if v:
+        return max(0, int(v))
+    try:
+        phys = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError, AttributeError):
+        phys = 16 << 30
+    return min(16 << 30, phys // 4)
+
+
+def pinned_bytes() -> int:
+    """Caller memory currently page-locked by the drop-in (≤ _pin_budget())."""
+    return sum(v[1] for v in _registered.values())
+
+
+def _evict_pins(need: int, budget: int) -> None:
+    """Release least recently used registrations until `need` more bytes fit."""
+    while _registered and pinned_bytes() + need > budget:
+        _key, (_ptr, _n, fin) = next(iter(_registered.items()))
+        fin()  # drains the stager, unregisters, drops the entry
 
 
 def _owner(arr: np.ndarray):
@@ -100,12 +131,16 @@ def _page_locked(arr: np.ndarray, dev) -> bool:
     key = id(own)
     hit = _registered.get(key)
     if hit is not None:
-        p0, n0 = hit
+        _registered.move_to_end(key)
+        p0, n0, _ = hit
         return p0 <= arr.ctypes.data and arr.ctypes.data + arr.nbytes <= p0 + n0
+    budget = _pin_budget()
+    if nbytes > budget:
+        return False
+    _evict_pins(nbytes, budget)
     if lib.rl_host_register(ctypes.c_void_p(ptr), nbytes) != C.RL_OK:
         return False
     stager = _stager(dev)
-    _registered[key] = (ptr, nbytes)
 
     def _release(ptr=ptr, key=key, stager=stager, lib=lib):
         lib.rl_stager_drain(stager)  # no DMA may still read the buffer
@@ -113,11 +148,11 @@ def _page_locked(arr: np.ndarray, dev) -> bool:
         _registered.pop(key, None)
 
     try:
-        weakref.finalize(own, _release)
+        fin = weakref.finalize(own, _release)
     except TypeError:  # owner not weak-referenceable: keep it registered only for this call
         lib.rl_host_unregister(ctypes.c_void_p(ptr))
-        _registered.pop(key, None)
         return False
+    _registered[key] = (ptr, nbytes, fin)
     return True
 
 
@@ -423,11 +458,26 @@ def tensor_join(left: TensorRelation, right: TensorRelation, max_output_rows: in
     out = rel_cls(out_schema, tuple(h.numpy() for h in hosts))
 
     out_bytes = sum(c.dst.numel() * c.dst.element_size() for c in cols)
-    stats = TYPES["SpillStats"](
-        peak_mem_bytes=li.nbytes(d_l) + ri.nbytes(d_r) + m * (8 + 4 * 4) + 8 * (m + 1) + out_bytes,
-        peak_build_bytes=0,
-    )
+    stats = TYPES["SpillStats"](peak_mem_bytes=join_peak_mem_bytes(li.n, d_l, ri.n, d_r, total, out_bytes),
+                                peak_build_bytes=0)
     return out, stats
+
+
+def join_peak_mem_bytes(n_left: int, d_left: int, n_right: int, d_right: int, total: int, out_bytes: int) -> int:
+    """SpillStats.peak_mem_bytes of a join, the reference's closed form
+    (tensorpath.py:188-202): the int64 index arrays of both sides, the
+    expansion temporaries (4 index-dtype arrays + 4 int64 arrays per pair;
+    int32 indices when total <= 2^31 - 1, tensorpath.py:159) and the output
+    columns — the same deterministic number the reference records."""
+    index_bytes = 8 * (n_left + n_right) + 8 * (d_left + d_right) + 8 * (d_left + 1 + d_right + 1)
+    idx_size = 4 if total <= 2**31 - 1 else 8
+    return index_bytes + total * (4 * idx_size + 4 * 8) + out_bytes
+
+
+def sort_peak_mem_bytes(n: int, out_bytes: int) -> int:
+    """SpillStats.peak_mem_bytes of a sort, the reference's closed form
+    (tensorpath.py:248-251): two int64 permutations + the output columns."""
+    return 2 * 8 * n + out_bytes
 
 
 def _out_column(src: torch.Tensor, ctype, rows: int, dev, side: int) -> engine.OutColumn:
@@ -474,10 +524,8 @@ def tensor_sort(rel, spec):
         hosts[j] = _host_out_on(col.dst, down)
     down.synchronize()
     out = rel_cls(rel.schema, tuple(h.numpy() for h in hosts))
-    stats = TYPES["SpillStats"](
-        peak_mem_bytes=2 * 4 * n + sum(o.numel() * o.element_size() for o in outs),
-        peak_build_bytes=0,
-    )
+    stats = TYPES["SpillStats"](peak_mem_bytes=sort_peak_mem_bytes(n, sum(o.numel() * o.element_size() for o in outs)),
+                                peak_build_bytes=0)
     return out, stats
 
 

@@ -204,6 +204,7 @@ struct SortArgs {
   uint4* items;              // pass-B tiles (digit-7 bucket, first row, end row)
   uint32_t* meta;            // [0] pass-B tiles
   int chunks;                // input chunks = CTAs of the histogram and digit-7 kernels
+  int allow_pk;              // scatter path: packed rows allowed (RL_NO_PACKED_ROWS=1 turns them off)
 };
 
 // Global digit count (pass p, digit d): the sum of the histogram replicas.
@@ -785,6 +786,13 @@ __device__ __forceinline__ int pack_mode(uint32_t c) {
   return ((c & 127) == 0 && (c >> 21 & 127) == 0) ? 1 : 2;
 }
 __device__ __forceinline__ uint32_t pack_shift(uint32_t c) { return 64u - (c >> 14 & 127); }  // mode 1
+// Packed rows: the packed key occupies the top len1 + len2 bits; with at most
+// 32 of them the low 32 bits are free for the row id (n <= 2^32), so a row is
+// ONE u64 (key | row id) through the counting passes and the local phase.
+// Every packed word is distinct and orders rows by (key, row id).
+__device__ __forceinline__ bool packed_rows(uint32_t c, const SortArgs& a) {
+  return a.allow_pk && pack_mode(c) != 0 && (c >> 14 & 127) + (c & 127) <= 32u;
+}
 template <int MODE>
 __device__ __forceinline__ uint64_t pack_as(uint64_t u, uint32_t c, uint32_t shl) {
   if constexpr (MODE == 0) return u;
@@ -862,7 +870,9 @@ __device__ __forceinline__ PTile ptile(uint8_t* sm) {
 // the staging), stage in digit order, write every run contiguously. s.hist
 // is zero on entry and on exit. Once the tile is staged, next(k, v) loads the
 // following tile into the same registers, in flight during the write-out.
-template <int SHIFT, typename Reserve, typename Next>
+// PK (packed rows): the row id travels in the key word's low 32 bits — no
+// separate row-id stream (v[] unused).
+template <int SHIFT, bool PK, typename Reserve, typename Next>
 __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int tn, const PTile& s,
                                               uint64_t* out_k, uint32_t* out_v, Reserve reserve, Next next) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -894,7 +904,7 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
     if (u * kPThreads + tid < tn) {
       const uint32_t p = s.hist[uint32_t(k[u] >> SHIFT) & 255u] + r[u];
       s.sk[p] = k[u];
-      s.sv[p] = v[u];
+      if constexpr (!PK) s.sv[p] = v[u];
     }
   }
   if (tid < 256) s.base[tid] = res - excl;
@@ -905,7 +915,7 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
     const uint64_t key = s.sk[i];
     const uint32_t o = s.base[uint32_t(key >> SHIFT) & 255u] + uint32_t(i);
     out_k[o] = key;
-    out_v[o] = s.sv[i];
+    if constexpr (!PK) out_v[o] = s.sv[i];
   }
   __syncthreads();  // staging and s.base reused by the next tile
 }
@@ -1130,14 +1140,16 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   auto reserve = [&](uint32_t d, uint32_t c) { return s.aux[d] + atomicAdd(a.cur7 + d, c); };
   // the tile loop, compiled per key-packing mode (chosen once)
   const uint32_t shl = pack_shift(sh);
-  auto tiles = [&](auto packed) {
+  auto tiles = [&](auto packed, auto pkc) {
+    constexpr bool PK = decltype(pkc)::value;
     auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int64_t t0) {
       const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
 #pragma unroll
       for (int u = 0; u < kPItems; ++u) {
         const int j = u * kPThreads + tid;
         k[u] = j < tn ? pack_as<decltype(packed)::value>(xform(uint64_t(__ldcs(col + t0 + j)), a.desc), sh, shl) : 0ull;
-        v[u] = uint32_t(t0 + j);
+        if constexpr (PK) k[u] |= uint64_t(uint32_t(t0 + j));
+        else v[u] = uint32_t(t0 + j);
       }
     };
     uint64_t k[kPItems];
@@ -1148,18 +1160,30 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     for (int64_t t0 = lo; t0 < hi; t0 += kPTile) {
       const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
       const int64_t nt = t0 + kPTile;
-      ptile_scatter<7 * kBits>(k, v, tn, s, a.keys_b, a.vals_b, reserve,
-                               [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
-                                 if (nt < hi) load(kk, vv, nt);
-                               });
+      ptile_scatter<7 * kBits, PK>(k, v, tn, s, a.keys_b, a.vals_b, reserve,
+                                   [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
+                                     if (nt < hi) load(kk, vv, nt);
+                                   });
     }
   };
+  using F = std::false_type;
+  using T = std::true_type;
+  const bool pk = packed_rows(sh, a);
   switch (pack_mode(sh)) {
-    case 0: tiles(std::integral_constant<int, 0>{}); break;
-    case 1: tiles(std::integral_constant<int, 1>{}); break;
-    default: tiles(std::integral_constant<int, 2>{}); break;
+    case 0: tiles(std::integral_constant<int, 0>{}, F{}); break;
+    case 1:
+      if (pk) tiles(std::integral_constant<int, 1>{}, T{});
+      else tiles(std::integral_constant<int, 1>{}, F{});
+      break;
+    default:
+      if (pk) tiles(std::integral_constant<int, 2>{}, T{});
+      else tiles(std::integral_constant<int, 2>{}, F{});
+      break;
   }
 }
+
+template <bool PK>
+__device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile& s);
 
 __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_kernel(SortArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -1168,7 +1192,15 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_ke
   pdl_wait();  // the digit-7 pass
   pdl_launch_dependents();
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[3] = globaltimer();
-  if (fallback_flag(a)) return;  // LSD fallback
+  if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);  // the key pack code
+  if (fallback_flag(a)) return;  // LSD fallback (the barrier also publishes scratch[50])
+  if (packed_rows(s.scratch[50], a)) sub_scatter_tiles<true>(a, s);
+  else sub_scatter_tiles<false>(a, s);
+}
+
+template <bool PK>
+__device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile& s) {
+  const int tid = threadIdx.x;
   const uint32_t n_items = __ldcg(a.meta);
   uint32_t* claim = s.scratch + 40;  // [2] claimed tile ids, by parity
   auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], const uint4& item) {
@@ -1177,7 +1209,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_ke
     for (int u = 0; u < kPItems; ++u) {
       const int j = u * kPThreads + tid;
       k[u] = j < tn ? __ldcs(a.keys_b + item.y + j) : 0ull;
-      v[u] = j < tn ? __ldcs(a.vals_b + item.y + j) : 0u;
+      if constexpr (!PK) v[u] = j < tn ? __ldcs(a.vals_b + item.y + j) : 0u;
     }
   };
   if (tid == 0) claim[0] = atomicAdd(a.flags + 3, 1u);
@@ -1196,7 +1228,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_ke
     auto reserve = [&](uint32_t d, uint32_t c) {
       return __ldcg(a.sub_off + g * 256 + d) + atomicAdd(a.cur16 + g * 256 + d, c);
     };
-    ptile_scatter<6 * kBits>(k, v, int(item.z - item.y), s, a.keys_a, a.vals_a, reserve,
+    ptile_scatter<6 * kBits, PK>(k, v, int(item.z - item.y), s, a.keys_a, a.vals_a, reserve,
                              [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
                                nit = claim[par];
                                if (nit < n_items) {
@@ -1217,6 +1249,7 @@ __device__ __forceinline__ bool row_less(uint64_t ka, uint32_t va, uint64_t kb, 
 // Sort rows [lo, hi) of B by (key, row id) — one warp, bitonic network
 // with mirrored first steps (every comparator ascending), so rows past hi
 // act as +inf padding and their comparators are skipped.
+template <bool PK = false>  // PK: packed rows, the key word alone orders them (bv unused)
 __device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t hi, int lane) {
   const uint32_t sz = hi - lo;
   uint32_t p2 = 1;
@@ -1228,10 +1261,16 @@ __device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t h
         const uint32_t q = j == (k >> 1) ? (i ^ (k - 1)) : (i + j);
         if (q < sz) {
           const uint64_t ka = bk[lo + i], kb = bk[lo + q];
-          const uint32_t va = bv[lo + i], vb = bv[lo + q];
-          if (row_less(kb, vb, ka, va)) {
-            bk[lo + i] = kb; bk[lo + q] = ka;
-            bv[lo + i] = vb; bv[lo + q] = va;
+          if constexpr (PK) {
+            if (kb < ka) {
+              bk[lo + i] = kb; bk[lo + q] = ka;
+            }
+          } else {
+            const uint32_t va = bv[lo + i], vb = bv[lo + q];
+            if (row_less(kb, vb, ka, va)) {
+              bk[lo + i] = kb; bk[lo + q] = ka;
+              bv[lo + i] = vb; bv[lo + q] = va;
+            }
           }
         }
       }
@@ -1271,17 +1310,17 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
                                           uint8_t* abuf, uint64_t* bar) {
   const uint32_t k0 = base & ~1u, v0 = base & ~3u;
   const uint32_t kbytes = ((base + cnt - k0) * 8u + 15u) & ~15u;
-  const uint32_t vbytes = ((base + cnt - v0) * 4u + 15u) & ~15u;
+  const uint32_t vbytes = vin ? ((base + cnt - v0) * 4u + 15u) & ~15u : 0u;  // packed rows: keys only
   fence_proxy_async_smem();
   mbar_expect_tx(bar, kbytes + vbytes);
   bulk_g2s(abuf, kin + k0, kbytes, bar);
-  bulk_g2s(abuf + kLocAKeys, vin + v0, vbytes, bar);
+  if (vbytes) bulk_g2s(abuf + kLocAKeys, vin + v0, vbytes, bar);
 }
 
 // BAL (the scatter path's large runs): a thread's rows in registers across
 // count + scatter, and the claimed group tail. The onesweep hybrid's short
 // runs (n < 4M) are faster without both (+1-5 us each at 0.3-2M rows).
-template <int THREADS, int PACK = 0, bool BAL = false>
+template <int THREADS, int PACK = 0, bool BAL = false, bool PK = false>
 __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   constexpr int kLWarps = THREADS / 32;
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
@@ -1295,7 +1334,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLocBars);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* kin = src == 1 ? a.keys_a : a.keys_b;
-  const uint32_t* vin = src == 1 ? a.vals_a : a.vals_b;
+  const uint32_t* vin = PK ? nullptr : src == 1 ? a.vals_a : a.vals_b;
   const int desc = a.key_mode == kRawDesc;
   constexpr uint32_t kGroups = kSubBuckets / kGroupSubs;
   constexpr int kPerThread = kLocalBins / THREADS;
@@ -1497,7 +1536,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         const uint32_t j = tid + u * THREADS;
         if (j < cnt) {
           bk[pos[u]] = rk[u];
-          bv[pos[u]] = av[j];
+          if constexpr (!PK) bv[pos[u]] = av[j];
         }
       }
     } else {
@@ -1505,7 +1544,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         const uint64_t key = ak[j];
         const uint32_t pos = atomicAdd(&hist[bin_of(key)], 1u);
         bk[pos] = key;
-        bv[pos] = av[j];
+        if constexpr (!PK) bv[pos] = av[j];
       }
     }
     __syncthreads();
@@ -1516,13 +1555,17 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     constexpr uint32_t kRankMax = 32;
     auto emit = [&](uint32_t p, uint64_t key, uint32_t v) {
       const uint64_t o = uint64_t(base) + p;
+      if constexpr (PK) {  // packed row: row id in the low 32 bits
+        v = uint32_t(key);
+        key &= ~0xFFFFFFFFull;
+      }
       if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(unpack_as<PACK>(key, pcode, pshl, constbits), desc));
       __stcs(a.out_vals + o, v);
       gather_fused(a.gather, v, o);
     };
     for (uint32_t p = tid; p < cnt; p += THREADS) {
       const uint64_t key = bk[p];
-      const uint32_t v = bv[p];
+      const uint32_t v = PK ? 0u : bv[p];
       const int b = bin_of(key);
       const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
       uint32_t pos = p;
@@ -1535,7 +1578,11 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       }
       if (b1 - b0 > 1) {
         uint32_t rk = 0;
-        for (uint32_t i = b0; i < b1; ++i) rk += row_less(bk[i], bv[i], key, v) ? 1u : 0u;
+        if constexpr (PK) {
+          for (uint32_t i = b0; i < b1; ++i) rk += bk[i] < key ? 1u : 0u;
+        } else {
+          for (uint32_t i = b0; i < b1; ++i) rk += row_less(bk[i], bv[i], key, v) ? 1u : 0u;
+        }
         pos = b0 + rk;
       }
       emit(pos, key, v);
@@ -1545,8 +1592,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     for (uint32_t t = warp; t < nbig; t += kLWarps) {
       const int b = int(big[t]);
       const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
-      warp_bitonic(bk, bv, b0, b1, lane);
-      for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], bv[p]);
+      warp_bitonic<PK>(bk, bv, b0, b1, lane);
+      for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], PK ? 0u : bv[p]);
     }
     if (nbig) __syncthreads();  // (the rank loop's reads of B/hist ended at the barrier before nbig)
     if (!more) break;
@@ -1631,10 +1678,18 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   if (!scatter) {
     local_phase<kLocalThreads, 0, false>(a, smem, src);  // (the onesweep hybrid packs no keys)
   } else {
-    switch (pack_mode(__ldcg(a.flags + 6))) {
+    const uint32_t pc = __ldcg(a.flags + 6);
+    const bool pk = packed_rows(pc, a);
+    switch (pack_mode(pc)) {
       case 0: local_phase<kLocalThreads, 0, true>(a, smem, src); break;
-      case 1: local_phase<kLocalThreads, 1, true>(a, smem, src); break;
-      default: local_phase<kLocalThreads, 2, true>(a, smem, src); break;
+      case 1:
+        if (pk) local_phase<kLocalThreads, 1, true, true>(a, smem, src);
+        else local_phase<kLocalThreads, 1, true>(a, smem, src);
+        break;
+      default:
+        if (pk) local_phase<kLocalThreads, 2, true, true>(a, smem, src);
+        else local_phase<kLocalThreads, 2, true>(a, smem, src);
+        break;
     }
   }
   if (a.stamps && scatter && threadIdx.x == 0)  // (profiling: the last CTA's end, pass-6 slot unused here)
@@ -2015,6 +2070,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
       pgrid = std::max(1, std::min(pgrid, max_ctas / 2 * pass_ctas_per_sm()));
     }
     a.chunks = chunks;
+    a.allow_pk = getenv_flag("RL_NO_PACKED_ROWS") ? 0 : 1;
     int lgrid = device_sm_count() * (1024 / kLocalThreads);
     if (max_ctas > 0) lgrid = std::max(1, std::min(lgrid, max_ctas));
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
@@ -2113,7 +2169,7 @@ int sort_axis_capped(const void* col, int col_kind, int width, int word, int des
   Layout L;
   if (!carve_layout(L, ws, ws_bytes, n)) return RL_ERR_WORKSPACE;
 
-  SortArgs a;
+  SortArgs a = {};
   a.col = col;
   a.perm_in = perm_in;
   a.n = n;
@@ -2191,7 +2247,7 @@ size_t partition_workspace_bytes(int64_t n) {
 // grouped by destination, input order kept within each destination.
 static int partition_by_words(const uint64_t* words, int64_t n, int parts, uint32_t* perm_out, int64_t* counts_out,
                               const Layout& L, cudaStream_t stream) {
-  SortArgs a;
+  SortArgs a = {};
   a.col = words;
   a.perm_in = nullptr;
   a.materialized = nullptr;

@@ -265,3 +265,29 @@ def test_hybrid_then_lsd_same_size(n):
     check_sort(rng.integers(0, 1 << 20, n, dtype=np.int64))  # three varying digits: LSD
     check_sort(np.where(rng.random(n) < 0.5, 5, full_range(rng, n)).astype(np.int64))  # skew: fallback
     check_sort(full_range(rng, n))
+
+
+@pytest.mark.parametrize("packed", ["on", "off"])
+@pytest.mark.parametrize("bits", [20, 30, 32])
+def test_scatter_packed_rows(packed, bits, monkeypatch, into_subbuckets):
+    """Keys with <= 32 varying bits travel with their row id in ONE u64 word
+    (packed rows: no row-id stream in the counting passes and the local phase).
+    The result equals the stable argsort with the mode on and forced off
+    (RL_NO_PACKED_ROWS=1), ties (duplicates) included, both directions, with a
+    fused gather riding on the packed row ids."""
+    if packed == "off":
+        monkeypatch.setenv("RL_NO_PACKED_ROWS", "1")
+    rng = np.random.default_rng(60 + bits)
+    n = 5_000_000 if into_subbuckets == "scatter" else 1_500_000
+    keys = rng.integers(0, 1 << bits, n, dtype=np.int64) - (1 << (bits - 1)) + 987_654_321
+    keys[rng.choice(n, n // 20, replace=False)] = keys[rng.integers(0, n, n // 20)]
+    check_sort(keys)
+    check_sort(keys, True)
+    col = rng.integers(0, 256, (n, 8), dtype=np.uint8)
+    kd, cd = torch.from_numpy(keys).cuda(), torch.from_numpy(col).cuda()
+    out = torch.empty_like(cd)
+    perm = engine.sort_permutation([engine.SortAxis(kd, False)], n, kd.device,
+                                   gather=[engine.OutColumn(cd, out, 8, 0)], fuse_gather=True)
+    want = O.stable_axis_order(keys, False)
+    assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
+    assert (out.cpu().numpy() == col[want]).all()

@@ -222,6 +222,48 @@ RL_API int rl_join_plan_build(const int64_t* left_keys, int64_t n_left,
                               size_t ws_bytes, rl_join_plan* plan, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Bucket join: the join plan for keys with <= 32 varying bits (both sides
+ * together), without sorted key axes. Replaces tensorpath.py:78-93 (x2),
+ * 109-128 and the sizing of 131-161: one joint key packing; every row of
+ * both sides as one packed word (key bits << 32 | row id) in the same 65536
+ * sub-buckets (top 16 key bits; the sort's chunk counts + two counting
+ * passes); per run of sub-buckets (<= 2560 rows a side) the pairs counted on
+ * chip; an exclusive scan of the run counts. Device scalars[0] = total
+ * pairs, scalars[1] = 1 if the plan applies — 0 (keys need more than 32
+ * bits, a sub-bucket holds more than 2560 rows of a side, n > 2^32): use
+ * rl_join_plan_build instead. Nothing is synchronised; read the two scalars
+ * with one D2H. n_left, n_right >= 1; keys 16-byte aligned.
+ * rl_bjoin_expand then writes output pairs [out_begin, out_end) exactly as
+ * rl_join_expand does (same rows, same order, same columns; the key column
+ * from RL_SIDE_KEY, other columns gathered by row id): each run's rows of
+ * both sides are sorted on chip by (key, row id) and matched in their bins.
+ * --------------------------------------------------------------------- */
+typedef struct rl_bjoin_plan {
+  const uint64_t* rows_left;
+  const uint64_t* rows_right;
+  const uint32_t* sub_off_left;
+  const uint32_t* sub_off_right;
+  uint32_t* flags_left;
+  uint32_t* flags_right;
+  uint32_t* counts;
+  uint64_t* offsets;
+  int64_t* scalars;
+  const int64_t* left_keys;
+} rl_bjoin_plan;
+RL_API size_t rl_bjoin_workspace_bytes(int64_t n_left, int64_t n_right);
+RL_API int rl_bjoin_plan_build(const int64_t* left_keys, int64_t n_left,
+                               const int64_t* right_keys, int64_t n_right, void* ws,
+                               size_t ws_bytes, rl_bjoin_plan* plan, void* stream);
+RL_API int rl_bjoin_expand(const rl_bjoin_plan* plan, uint64_t out_begin,
+                           uint64_t out_end, uint32_t* left_rows_out,
+                           uint32_t* right_rows_out, const rl_column* columns,
+                           int32_t n_columns, void* stream);
+/* rl_join_pair_checksum on a bucket-join plan: sum of fmix64((left_row << 32)
+ * | right_row) over pairs [out_begin, out_end), added into *sum_out. */
+RL_API int rl_bjoin_pair_checksum(const rl_bjoin_plan* plan, uint64_t out_begin,
+                                  uint64_t out_end, uint64_t* sum_out, void* stream);
+
+/* ---------------------------------------------------------------------
  * K6+K7  Run expansion fused with the column gathers.
  *
  * Replaces tensorpath.py:157-185: output pair t (global index in

@@ -56,6 +56,12 @@ class RlJoinPlan(ctypes.Structure):
         "pair_offsets")]
 
 
+class RlBjoinPlan(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "rows_left", "rows_right", "sub_off_left", "sub_off_right", "flags_left", "flags_right", "counts",
+        "offsets", "scalars", "left_keys")]
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -101,6 +107,11 @@ SIGNATURES = {
         [_P, _P, _P, _P, _P, _I64, _P, _P, _U64, _U64, _P, _P, ctypes.POINTER(RlColumn), _I32, _P],
     ),
     "rl_join_pair_checksum": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P, _U64, _U64, _P, _P]),
+    "rl_bjoin_workspace_bytes": (_SZ, [_I64, _I64]),
+    "rl_bjoin_plan_build": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(RlBjoinPlan), _P]),
+    "rl_bjoin_expand": (ctypes.c_int, [ctypes.POINTER(RlBjoinPlan), _U64, _U64, _P, _P, ctypes.POINTER(RlColumn),
+                                       _I32, _P]),
+    "rl_bjoin_pair_checksum": (ctypes.c_int, [ctypes.POINTER(RlBjoinPlan), _U64, _U64, _P, _P]),
     "rl_gather_rows": (ctypes.c_int, [_P, _I64, ctypes.POINTER(RlColumn), _I32, _P]),
     "rl_widen_u32": (ctypes.c_int, [_P, _I64, _P, _P]),
     "rl_partition_workspace_bytes": (_SZ, [_I64, _I32]),

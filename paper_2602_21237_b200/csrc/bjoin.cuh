@@ -1,0 +1,28 @@
+// bjoin.cuh — the interface between the sort's scatter path (radix_sort.cu)
+// and the bucket join (bucket_join.cu): both join sides partitioned into the
+// same 65536 sub-buckets of one joint key packing, rows as packed words.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rl {
+namespace radix {
+
+constexpr int kBjSubBuckets = 1 << 16;  // sub-buckets: top 16 bits of the packed key
+constexpr int kBjCap = 2560;            // rows of one side in one sub-bucket at most (kLocalCap)
+
+struct BjSide {
+  const uint64_t* rows;     // [n] packed words (key bits << 32 | row id), grouped by sub-bucket
+  const uint32_t* sub_off;  // [kBjSubBuckets + 1] sub-bucket starts
+  uint32_t* flags;          // [0] != 0: fall back; [6] the joint pack code
+  int64_t n;
+};
+
+size_t bj_side_workspace_bytes(int64_t n);
+int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, void* ws_l, size_t ws_l_bytes,
+                 void* ws_r, size_t ws_r_bytes, cudaStream_t stream, BjSide* left, BjSide* right);
+
+}  // namespace radix
+}  // namespace rl

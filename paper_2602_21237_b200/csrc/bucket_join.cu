@@ -1,0 +1,548 @@
+// bucket_join.cu — the equi-join as a partitioned join on chip.
+//
+// Replaces, for join keys with <= 32 varying bits (cfg1, cfg4, cfg5 keys), the
+// reference's to_tensor x 2 + key_axis_align + expansion
+// (/root/reference/pkg/src/relab/tensorpath.py:78-93, 109-128, 131-185) with
+// a plan that never materialises the sorted key axes:
+//
+//   1. bj_partition (radix_sort.cu): one joint key packing for both sides
+//      (the varying bits of both, against the left side's first key), then per
+//      side the scatter path's chunk counts + two counting passes in packed-row
+//      mode: every row becomes ONE u64 (packed key << 32 | row id) and lands
+//      in its sub-bucket (top 16 bits of the packed key). Equal keys of the two
+//      sides land in the same sub-bucket index.
+//   2. bj_count_kernel: per run (consecutive sub-buckets of a 16-sub-bucket
+//      group with <= kBjCap rows per side) the right rows are binned on chip
+//      by (sub-bucket, next bits), every left row counts the right rows of its
+//      bin with an equal key -> the run's pair count.
+//   3. bj_scan_kernel: exclusive scan of the 65536 run counts -> every run's
+//      first output row, the total (the one host sync of a join) and the
+//      "applies" flag (no side fell back).
+//   4. bj_emit_kernel: per run, both sides sorted on chip by their packed
+//      words (= by key, then row id), every left row's matching right range
+//      found in its bin, a prefix over the left rows gives each row's first
+//      output, and the outputs are written in output order: key, left row,
+//      right row — the reference order (tensorpath.py:162-172) — with every
+//      column gathered (key = the matched key itself, left / right columns by
+//      row id), optionally only the slice [out_begin, out_end).
+//
+// DRAM traffic per side: 8n (counts) + 16n (digit-7 pass) + 16n (digit-6
+// pass) + 8n (count) + 8n (emit); no position, key-value, offset or
+// alignment arrays are written. A sub-bucket above kBjCap rows (skewed keys),
+// keys with more than 32 varying bits or a varying bit the joint sample missed
+// make the plan report "does not apply" (scalars[1] == 0) and the caller runs
+// the sort-based plan (plan.cu) instead.
+#include <algorithm>
+
+#include "bjoin.cuh"
+#include "common.cuh"
+#include "keypack.cuh"
+
+namespace rl {
+namespace bjoin {
+
+using radix::BjSide;
+using radix::kBjCap;
+using radix::kBjSubBuckets;
+
+constexpr int kThreads = 512;
+constexpr int kGroupSubs = 16;
+constexpr uint32_t kGroups = kBjSubBuckets / kGroupSubs;  // 4096
+constexpr int kMaxBins = 4096;
+constexpr int kRowsPerThread = (kBjCap + kThreads - 1) / kThreads;  // 5
+constexpr int kRankMax = 48;  // bins above this: a warp's bitonic network
+
+struct PlanArgs {
+  const uint64_t* rows_l;
+  const uint64_t* rows_r;
+  const uint32_t* off_l;
+  const uint32_t* off_r;
+  const uint32_t* flags_l;
+  const uint32_t* flags_r;
+  uint32_t* counts;  // [kBjSubBuckets] pairs per (group, run slot)
+  uint64_t* offs;    // [kBjSubBuckets] first output row per (group, run slot)
+  int64_t* scalars;  // [0] total pairs, [1] 1 = the bucket join applies
+  const long long* k0_src;  // the left side's first key (constant bits of every key)
+};
+
+// Runs of one group: consecutive sub-buckets [s, e) with at most kBjCap rows
+// on each side (every single sub-bucket fits: the scatter passes check it);
+// encoded (s << 8) | e. The same cut in the count and emit kernels.
+__device__ __forceinline__ uint32_t cut_runs(const uint32_t* ol, const uint32_t* orr, uint32_t* ends) {
+  uint32_t nr = 0, s = 0;
+  while (s < uint32_t(kGroupSubs)) {
+    uint32_t e = s + 1;
+    while (e < uint32_t(kGroupSubs) && ol[e + 1] - ol[s] <= uint32_t(kBjCap) && orr[e + 1] - orr[s] <= uint32_t(kBjCap))
+      ++e;
+    ends[nr++] = (s << 8) | e;
+    s = e;
+  }
+  return nr;
+}
+
+__device__ __forceinline__ uint32_t bin_bits(uint32_t nsb) {
+  return 12u - (nsb > 1 ? 32u - uint32_t(__clz(int(nsb - 1))) : 0u);
+}
+
+struct Bins {
+  uint32_t first, bb;
+  __device__ __forceinline__ Bins(uint32_t first_sub, uint32_t nsb) {
+    first = first_sub;
+    bb = bin_bits(nsb);
+  }
+  __device__ __forceinline__ uint32_t count(uint32_t nsb) const { return nsb << bb; }
+  // (sub-bucket - first, the next bb key bits): bins ordered like the keys
+  __device__ __forceinline__ uint32_t of(uint64_t w) const {
+    return ((uint32_t(w >> 48) - first) << bb) | (uint32_t(w >> (48 - bb)) & ((1u << bb) - 1u));
+  }
+};
+
+__device__ __forceinline__ bool fell_back(const PlanArgs& a) {
+  return __syncthreads_or(threadIdx.x == 0 && (*reinterpret_cast<volatile const uint32_t*>(a.flags_l) |
+                                               *reinterpret_cast<volatile const uint32_t*>(a.flags_r)) != 0) != 0;
+}
+
+// Bin `cnt` rows (this thread's rows in w[]) into dst[] grouped by bin; hist[]
+// ends as each bin's END. hist must be zero for the nbins bins on entry.
+__device__ __forceinline__ void bin_rows(const uint64_t (&w)[kRowsPerThread], uint32_t cnt, const Bins& bins,
+                                         uint32_t nbins, uint32_t* hist, uint64_t* dst, uint64_t* scan_scratch) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u)
+    if (tid + u * kThreads < int(cnt)) atomicAdd(&hist[bins.of(w[u])], 1u);
+  __syncthreads();
+  constexpr int kPer = kMaxBins / kThreads;  // 8
+  const uint32_t per = (nbins + kThreads - 1) / kThreads;
+  uint32_t c[kPer], run = 0;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const uint32_t b = tid * per + i;
+    c[i] = uint32_t(i) < per && b < nbins ? hist[b] : 0u;
+    run += c[i];
+  }
+  uint32_t total;
+  uint32_t start = block_exclusive_scan<kThreads>(run, reinterpret_cast<uint32_t*>(scan_scratch), &total);
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const uint32_t b = tid * per + i;
+    if (uint32_t(i) < per && b < nbins) hist[b] = start;
+    start += c[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u)
+    if (tid + u * kThreads < int(cnt)) dst[atomicAdd(&hist[bins.of(w[u])], 1u)] = w[u];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void load_rows(const uint64_t* rows, uint32_t r0, uint32_t cnt,
+                                          uint64_t (&w)[kRowsPerThread]) {
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    const uint32_t j = threadIdx.x + u * kThreads;
+    w[u] = j < cnt ? __ldcs(rows + r0 + j) : 0ull;
+  }
+}
+
+// ---------------------------------------------------------------- count
+__global__ void __launch_bounds__(kThreads, 2) bj_count_kernel(PlanArgs a) {
+  __shared__ uint64_t br[kBjCap];
+  __shared__ uint32_t hist[kMaxBins];
+  __shared__ uint32_t offl[kGroupSubs + 1], offr[kGroupSubs + 1], ends[kGroupSubs];
+  __shared__ uint64_t scratch[kThreads / 32 + 2];
+  __shared__ uint32_t nruns;
+  const int tid = threadIdx.x;
+  if (fell_back(a)) return;
+  for (uint32_t g = blockIdx.x; g < kGroups; g += gridDim.x) {
+    if (tid <= kGroupSubs) {
+      offl[tid] = __ldcg(a.off_l + g * kGroupSubs + tid);
+      offr[tid] = __ldcg(a.off_r + g * kGroupSubs + tid);
+    }
+    __syncthreads();
+    if (tid == 0) nruns = cut_runs(offl, offr, ends);
+    __syncthreads();
+    const uint32_t nr = nruns;
+    if (tid >= int(nr) && tid < kGroupSubs) a.counts[g * kGroupSubs + tid] = 0u;
+    for (uint32_t r = 0; r < nr; ++r) {
+      const uint32_t s = ends[r] >> 8, e = ends[r] & 255u;
+      const uint32_t l0 = offl[s], nl = offl[e] - l0, r0 = offr[s], nrr = offr[e] - r0;
+      uint64_t cnt = 0;
+      if (nl && nrr) {
+        const Bins bins(g * kGroupSubs + s, e - s);
+        const uint32_t nbins = bins.count(e - s);
+        for (uint32_t i = tid; i < nbins; i += kThreads) hist[i] = 0;
+        uint64_t w[kRowsPerThread], wl[kRowsPerThread];
+        load_rows(a.rows_r, r0, nrr, w);
+        load_rows(a.rows_l, l0, nl, wl);  // in flight while the right side is binned
+        __syncthreads();
+        bin_rows(w, nrr, bins, nbins, hist, br, scratch);
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+          if (tid + u * kThreads < int(nl)) {
+            const uint32_t b = bins.of(wl[u]);
+            const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+            const uint32_t key = uint32_t(wl[u] >> 32);
+            for (uint32_t i = b0; i < b1; ++i) cnt += uint32_t(br[i] >> 32) == key ? 1u : 0u;
+          }
+        }
+      }
+      uint64_t tot;
+      block_exclusive_scan<kThreads>(cnt, scratch, &tot);
+      if (tid == 0) a.counts[g * kGroupSubs + r] = uint32_t(tot);
+      __syncthreads();  // hist / br / scratch reused by the next run
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- scan
+__global__ void __launch_bounds__(1024) bj_scan_kernel(PlanArgs a) {
+  __shared__ uint64_t scratch[34];
+  constexpr int kPer = kBjSubBuckets / 1024;  // 64
+  const int tid = threadIdx.x;
+  const bool ok = *reinterpret_cast<volatile const uint32_t*>(a.flags_l) == 0 &&
+                  *reinterpret_cast<volatile const uint32_t*>(a.flags_r) == 0;
+  uint64_t run = 0;
+  if (ok)
+    for (int i = 0; i < kPer; ++i) run += __ldcg(a.counts + tid * kPer + i);
+  uint64_t total;
+  uint64_t start = block_exclusive_scan<1024>(run, scratch, &total);
+  if (ok) {
+    for (int i = 0; i < kPer; ++i) {
+      a.offs[tid * kPer + i] = start;
+      start += __ldcg(a.counts + tid * kPer + i);
+    }
+  }
+  if (tid == 0) {
+    a.scalars[0] = ok ? int64_t(total) : 0;
+    a.scalars[1] = ok ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------- emit
+struct EmitArgs {
+  PlanArgs p;
+  uint64_t out_begin, out_end;
+  uint32_t* lrows_out;
+  uint32_t* rrows_out;
+  unsigned long long* checksum;
+};
+
+constexpr int kMaxCols = RL_MAX_COLUMNS;
+struct Cols {
+  rl_column c[kMaxCols];
+  int n;
+};
+
+// Sort the rows of dst[0, cnt) — grouped by bin, hist[] = bin ends — into
+// sorted[] by packed word (unique: key bits, then row id). Rows rank among
+// their bin-mates; bins above kRankMax rows go through a warp's bitonic
+// network in place first.
+__device__ __forceinline__ void finish_sort(uint64_t* grouped, uint64_t* sorted, const uint32_t* hist,
+                                            const Bins& bins, uint32_t cnt, uint32_t* big, uint32_t* nbig) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) *nbig = 0;
+  __syncthreads();
+  for (uint32_t p = tid; p < cnt; p += kThreads) {
+    const uint64_t w = grouped[p];
+    const uint32_t b = bins.of(w);
+    const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+    if (b1 - b0 > uint32_t(kRankMax)) {
+      if (p == b0) {
+        const uint32_t slot = atomicAdd(nbig, 1u);
+        if (slot < 64u) big[slot] = b;
+      }
+      continue;
+    }
+    uint32_t rk = 0;
+    for (uint32_t i = b0; i < b1; ++i) rk += grouped[i] < w ? 1u : 0u;
+    sorted[b0 + rk] = w;
+  }
+  __syncthreads();
+  const uint32_t nb = *nbig;  // <= kBjCap / (kRankMax + 1) = 52 < 64
+  for (uint32_t t = warp; t < min(nb, 64u); t += kThreads / 32) {
+    const uint32_t b = big[t];
+    const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+    // bitonic over [b0, b1) in `grouped`, padded to a power of two with +inf
+    const uint32_t sz = b1 - b0;
+    uint32_t p2 = 1;
+    while (p2 < sz) p2 <<= 1;
+    for (uint32_t k = 2; k <= p2; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t x = lane; x < (p2 >> 1); x += 32) {
+          const uint32_t i = (x / j) * (2 * j) + (x % j);
+          const uint32_t q = j == (k >> 1) ? (i ^ (k - 1)) : (i + j);
+          if (q < sz) {
+            const uint64_t u = grouped[b0 + i], v = grouped[b0 + q];
+            if (v < u) {
+              grouped[b0 + i] = v;
+              grouped[b0 + q] = u;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    for (uint32_t p = b0 + lane; p < b1; p += 32) sorted[p] = grouped[p];
+  }
+  __syncthreads();
+}
+
+template <bool CHECKSUM>  // CHECKSUM: sum fmix64(l << 32 | r) over the pairs into *e.checksum instead
+__global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols cols) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* sl = reinterpret_cast<uint64_t*>(smem);  // [kBjCap] left rows, sorted
+  uint64_t* sr = sl + kBjCap;                         // [kBjCap] right rows, sorted
+  uint64_t* gx = sr + kBjCap;                         // [kBjCap] grouped-by-bin scratch / per-left-row arrays
+  uint32_t* hr = reinterpret_cast<uint32_t*>(gx + kBjCap);  // [kMaxBins] right bin ends (kept for the match)
+  uint32_t* hl = hr + kMaxBins;                             // [kMaxBins] left bin ends
+  uint64_t* scratch = reinterpret_cast<uint64_t*>(hl + kMaxBins);  // [kThreads / 32 + 2]
+  uint32_t* misc = reinterpret_cast<uint32_t*>(scratch + kThreads / 32 + 2);  // offsets, runs, big bins
+  uint32_t* offl = misc;
+  uint32_t* offr = misc + 17;
+  uint32_t* ends = misc + 34;
+  uint32_t* big = misc + 50;  // [64]
+  uint32_t* nbig = misc + 114;
+  uint32_t* nruns = misc + 115;
+  const PlanArgs& a = e.p;
+  const int tid = threadIdx.x;
+  uint64_t sum = 0;
+  const uint32_t code = __ldcg(a.flags_l + 6);
+  const uint64_t k0 = radix::xform(uint64_t(__ldg(a.k0_src)), 0);
+  const uint64_t constbits = k0 & ~radix::pack_mask(code);
+  const int mode = radix::pack_mode(code);
+  const uint32_t shl = radix::pack_shift(code);
+  auto key_of = [&](uint64_t w) -> long long {
+    const uint64_t v = w & ~0xFFFFFFFFull;
+    const uint64_t u = mode == 1 ? (v >> shl) | constbits : radix::unpack_key(v, code, constbits);
+    return (long long)radix::xform(u, 0);
+  };
+  for (uint32_t g = blockIdx.x; g < kGroups; g += gridDim.x) {
+    if (tid <= kGroupSubs) {
+      offl[tid] = __ldcg(a.off_l + g * kGroupSubs + tid);
+      offr[tid] = __ldcg(a.off_r + g * kGroupSubs + tid);
+    }
+    __syncthreads();
+    if (tid == 0) *nruns = cut_runs(offl, offr, ends);
+    __syncthreads();
+    const uint32_t nr = *nruns;
+    for (uint32_t r = 0; r < nr; ++r) {
+      const uint32_t cnt_pairs = __ldcg(a.counts + g * kGroupSubs + r);
+      const uint64_t base = __ldcg(a.offs + g * kGroupSubs + r);
+      if (cnt_pairs == 0 || base + cnt_pairs <= e.out_begin || base >= e.out_end) continue;  // uniform
+      const uint32_t s = ends[r] >> 8, en = ends[r] & 255u;
+      const uint32_t l0 = offl[s], nl = offl[en] - l0, r0 = offr[s], nrr = offr[en] - r0;
+      const Bins bins(g * kGroupSubs + s, en - s);
+      const uint32_t nbins = bins.count(en - s);
+      for (uint32_t i = tid; i < nbins; i += kThreads) {
+        hr[i] = 0;
+        hl[i] = 0;
+      }
+      uint64_t w[kRowsPerThread], wl[kRowsPerThread];
+      load_rows(a.rows_r, r0, nrr, w);
+      load_rows(a.rows_l, l0, nl, wl);
+      __syncthreads();
+      bin_rows(w, nrr, bins, nbins, hr, gx, scratch);
+      finish_sort(gx, sr, hr, bins, nrr, big, nbig);
+      bin_rows(wl, nl, bins, nbins, hl, gx, scratch);
+      finish_sort(gx, sl, hl, bins, nl, big, nbig);
+      // every left row (sorted index p): its matching right range [rs, rs + m) in sr
+      uint32_t* m_arr = reinterpret_cast<uint32_t*>(gx);
+      uint32_t* rs_arr = m_arr + kBjCap;
+      constexpr int kPer = kRowsPerThread;
+      uint32_t mloc[kPer], run = 0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {  // thread owns left rows tid * kPer + u (consecutive: the scan below)
+        const uint32_t p = tid * kPer + u;
+        uint32_t m = 0, rs = 0;
+        if (p < nl) {
+          const uint64_t wv = sl[p];
+          const uint32_t b = bins.of(wv);
+          const uint32_t b0 = b ? hr[b - 1] : 0u, b1 = hr[b];
+          const uint32_t key = uint32_t(wv >> 32);
+          uint32_t i = b0;
+          while (i < b1 && uint32_t(sr[i] >> 32) < key) ++i;
+          rs = i;
+          while (i < b1 && uint32_t(sr[i] >> 32) == key) ++i;
+          m = i - rs;
+          rs_arr[p] = rs;
+        }
+        mloc[u] = m;
+        run += m;
+      }
+      uint32_t total;
+      uint32_t start = block_exclusive_scan<kThreads>(run, reinterpret_cast<uint32_t*>(scratch), &total);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint32_t p = tid * kPer + u;
+        if (p < nl) m_arr[p] = start;  // exclusive prefix: the first output of left row p
+        start += mloc[u];
+      }
+      __syncthreads();
+      // outputs in order: t -> left row p (last prefix <= t), right row rs[p] + t - pre[p]
+      const uint64_t lo = e.out_begin > base ? e.out_begin - base : 0;
+      const uint64_t hi = min(uint64_t(total), e.out_end - base);
+      for (uint64_t t = lo + tid; t < hi; t += kThreads) {
+        uint32_t x = 0, y = nl;  // largest p with pre[p] <= t
+        while (y - x > 1) {
+          const uint32_t mid = (x + y) >> 1;
+          if (m_arr[mid] <= uint32_t(t)) x = mid;
+          else y = mid;
+        }
+        const uint64_t wv = sl[x];
+        const uint64_t wr = sr[rs_arr[x] + (uint32_t(t) - m_arr[x])];
+        const uint32_t lrow = uint32_t(wv), rrow = uint32_t(wr);
+        if constexpr (CHECKSUM) {
+          sum += fmix64((uint64_t(lrow) << 32) | rrow);
+          continue;
+        }
+        const uint64_t o = base + t - e.out_begin;
+        if (e.lrows_out) __stcs(e.lrows_out + o, lrow);
+        if (e.rrows_out) __stcs(e.rrows_out + o, rrow);
+        for (int ci = 0; ci < cols.n; ++ci) {
+          const rl_column& c = cols.c[ci];
+          const int wd = c.width;
+          uint8_t* dst = static_cast<uint8_t*>(c.dst) + o * uint64_t(wd);
+          if (c.side == RL_SIDE_KEY)
+            __stcs(reinterpret_cast<long long*>(dst), key_of(wv));
+          else
+            copy_row(static_cast<const uint8_t*>(c.src) + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * wd, dst, wd);
+        }
+      }
+      __syncthreads();  // smem reused by the next run
+    }
+  }
+  if constexpr (CHECKSUM) {  // mod 2^64: one atomic per warp
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if ((tid & 31) == 0 && sum) atomicAdd(e.checksum, (unsigned long long)sum);
+  }
+}
+
+constexpr size_t kEmitSmem = size_t(kBjCap) * 8 * 3 + size_t(kMaxBins) * 4 * 2 + (kThreads / 32 + 2) * 8 + 128 * 4;
+
+// ---------------------------------------------------------------- host
+static size_t scratch_offset(int64_t nl) { return align_up(radix::bj_side_workspace_bytes(nl), 256); }
+
+size_t workspace_bytes(int64_t nl, int64_t nr) {
+  return scratch_offset(nl) + align_up(radix::bj_side_workspace_bytes(nr), 256) +
+         align_up(sizeof(uint32_t) * kBjSubBuckets, 256) + align_up(sizeof(uint64_t) * kBjSubBuckets, 256) +
+         align_up(sizeof(int64_t) * 4, 256) + 256;
+}
+
+static int emit_grid() {
+  static int cache[kMaxDevices] = {};
+  return per_device(cache, [] {
+    if (cudaFuncSetAttribute(bj_emit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem)) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(bj_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem)) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      return -1;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bj_emit_kernel<false>, kThreads, kEmitSmem) !=
+            cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    return per_sm * device_sm_count();
+  });
+}
+
+int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, void* ws, size_t ws_bytes,
+         rl_bjoin_plan* out, cudaStream_t stream) {
+  if (!out || nl < 1 || nr < 1) return RL_ERR_BAD_ARG;
+  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0 || ws_bytes < workspace_bytes(nl, nr)) return RL_ERR_WORKSPACE;
+  char* base = static_cast<char*>(ws);
+  const size_t wl = scratch_offset(nl), wr = align_up(radix::bj_side_workspace_bytes(nr), 256);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(base + wl + wr);
+  uint64_t* offs = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(counts) + align_up(sizeof(uint32_t) * kBjSubBuckets, 256));
+  int64_t* scalars = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(offs) + align_up(sizeof(uint64_t) * kBjSubBuckets, 256));
+  BjSide L, R;
+  int st = radix::bj_partition(lkeys, nl, rkeys, nr, base, wl, base + wl, wr, stream, &L, &R);
+  if (st != RL_OK) return st;
+  PlanArgs a{L.rows, R.rows, L.sub_off, R.sub_off, L.flags, R.flags, counts, offs, scalars,
+             reinterpret_cast<const long long*>(lkeys)};
+  const int grid = device_sm_count() * 3;
+  bj_count_kernel<<<grid, kThreads, 0, stream>>>(a);
+  bj_scan_kernel<<<1, 1024, 0, stream>>>(a);
+  count_launches(2);
+  out->rows_left = L.rows;
+  out->rows_right = R.rows;
+  out->sub_off_left = L.sub_off;
+  out->sub_off_right = R.sub_off;
+  out->flags_left = L.flags;
+  out->flags_right = R.flags;
+  out->counts = counts;
+  out->offsets = offs;
+  out->scalars = scalars;
+  out->left_keys = lkeys;
+  return rl_cuda_status(cudaGetLastError());
+}
+
+int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t* lrows_out, uint32_t* rrows_out,
+         const rl_column* columns, int n_columns, cudaStream_t stream, uint64_t* checksum = nullptr) {
+  if (!p || out_end < out_begin || n_columns < 0 || n_columns > kMaxCols || (n_columns && !columns))
+    return RL_ERR_BAD_ARG;
+  if (out_end == out_begin) return RL_OK;
+  Cols cs;
+  cs.n = n_columns;
+  for (int i = 0; i < n_columns; ++i) {
+    const rl_column& c = columns[i];
+    if (c.width < 0 || !c.dst) return RL_ERR_BAD_ARG;
+    if (c.side == RL_SIDE_KEY) {
+      if (c.width != 8) return RL_ERR_BAD_ARG;
+    } else if (c.side != RL_SIDE_LEFT && c.side != RL_SIDE_RIGHT) {
+      return RL_ERR_BAD_ARG;
+    } else if (c.width > 0 && !c.src) {
+      return RL_ERR_BAD_ARG;
+    }
+    cs.c[i] = c;
+  }
+  const int grid = emit_grid();
+  if (grid < 1) return rl_cuda_status(cudaErrorInvalidConfiguration);
+  EmitArgs e;
+  e.p = PlanArgs{p->rows_left, p->rows_right, p->sub_off_left, p->sub_off_right, p->flags_left, p->flags_right,
+                 p->counts, p->offsets, p->scalars, reinterpret_cast<const long long*>(p->left_keys)};
+  e.out_begin = out_begin;
+  e.out_end = out_end;
+  e.lrows_out = lrows_out;
+  e.rrows_out = rrows_out;
+  e.checksum = reinterpret_cast<unsigned long long*>(checksum);
+  if (checksum) bj_emit_kernel<true><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
+  else bj_emit_kernel<false><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
+  count_launches(1);
+  return rl_cuda_status(cudaGetLastError());
+}
+
+}  // namespace bjoin
+}  // namespace rl
+
+extern "C" {
+
+RL_API size_t rl_bjoin_workspace_bytes(int64_t n_left, int64_t n_right) {
+  return rl::bjoin::workspace_bytes(std::max<int64_t>(n_left, 1), std::max<int64_t>(n_right, 1));
+}
+
+RL_API int rl_bjoin_plan_build(const int64_t* left_keys, int64_t n_left, const int64_t* right_keys, int64_t n_right,
+                               void* ws, size_t ws_bytes, rl_bjoin_plan* plan, void* stream) {
+  return rl::bjoin::plan(left_keys, n_left, right_keys, n_right, ws, ws_bytes, plan,
+                         static_cast<cudaStream_t>(stream));
+}
+
+RL_API int rl_bjoin_expand(const rl_bjoin_plan* plan, uint64_t out_begin, uint64_t out_end, uint32_t* left_rows_out,
+                           uint32_t* right_rows_out, const rl_column* columns, int32_t n_columns, void* stream) {
+  return rl::bjoin::emit(plan, out_begin, out_end, left_rows_out, right_rows_out, columns, n_columns,
+                         static_cast<cudaStream_t>(stream));
+}
+
+RL_API int rl_bjoin_pair_checksum(const rl_bjoin_plan* plan, uint64_t out_begin, uint64_t out_end, uint64_t* sum_out,
+                                  void* stream) {
+  if (!sum_out) return RL_ERR_BAD_ARG;
+  return rl::bjoin::emit(plan, out_begin, out_end, nullptr, nullptr, nullptr, 0, static_cast<cudaStream_t>(stream),
+                         sum_out);
+}
+
+}  // extern "C"

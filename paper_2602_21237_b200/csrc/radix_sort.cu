@@ -61,6 +61,8 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "keypack.cuh"
+#include "bjoin.cuh"
 
 namespace rl {
 namespace radix {
@@ -133,9 +135,6 @@ constexpr size_t kPStage = size_t(kPTile) * 12;    // staged keys + row ids (als
 constexpr size_t kPSmem = kPStage + 3 * 256 * 4 + 64 * 4;
 enum SrcMode : int { kSrcInt64 = 0, kSrcInt64Gather = 1, kSrcBytes = 2, kSrcWords = 3 };
 
-__device__ __forceinline__ uint64_t xform(uint64_t x, int desc) {
-  return (desc ? ~x : x) ^ 0x8000000000000000ull;
-}
 
 __device__ __forceinline__ uint64_t bytes_word(const uint8_t* row, int width, int word, int desc) {
   uint64_t v = 0;
@@ -205,6 +204,11 @@ struct SortArgs {
   uint32_t* meta;            // [0] pass-B tiles
   int chunks;                // input chunks = CTAs of the histogram and digit-7 kernels
   int allow_pk;              // scatter path: packed rows allowed (RL_NO_PACKED_ROWS=1 turns them off)
+  // bucket join (bj_partition): both sides share one pack code, set in flags[6]
+  // before the chunk counts, checked against the LEFT side's first key
+  int pack_given;
+  const long long* k0_src;   // the key whose constant bits every key must share (default: col[0])
+  int bj;                    // keep going with < 4 varying digits (the join needs the sub-buckets)
 };
 
 // Global digit count (pass p, digit d): the sum of the histogram replicas.
@@ -735,57 +739,6 @@ __device__ void count_digits(const SortArgs& a, uint8_t* smem, uint32_t digits) 
 // Each kernel after the first is a programmatic dependent of the one before
 // when the sort has the device to itself.
 
-// Key normalisation of the scatter path: the key bits that do not vary
-// (estimated from a sample at the start of the chunk counts, checked by them
-// against every key) are squeezed out — the varying bits, up to two runs of
-// them, are packed left-aligned, high run first — so the sub-buckets are the
-// top 16 VARYING bits (row-id-like keys, composite keys with a constant
-// middle, keys with constant low bits). Order is unchanged: every key shares
-// the dropped bits. The local phase puts the bits back when it writes keys.
-// Pack code: bit 28 valid, then (lo, len) of the high run and of the low run
-// (len 0: one run), 7 bits each; 0 = keys used as they are.
-__device__ __forceinline__ uint64_t low_mask(uint32_t len) { return len >= 64 ? ~0ull : (1ull << len) - 1; }
-__device__ __forceinline__ uint32_t pack_code_of(uint64_t vv) {
-  if (vv == 0) return 0u;
-  const uint32_t hi1 = 63u - uint32_t(__clzll((long long)vv));
-  const uint64_t z1 = ~vv & low_mask(hi1);  // zero bits below the top varying bit
-  const uint32_t lo1 = z1 ? 64u - uint32_t(__clzll((long long)z1)) : 0u;
-  const uint32_t len1 = hi1 - lo1 + 1;
-  const uint64_t rest = vv & low_mask(lo1);
-  uint32_t lo2 = 0, len2 = 0;
-  if (rest) {
-    const uint32_t hi2 = 63u - uint32_t(__clzll((long long)rest));
-    const uint64_t z2 = ~rest & low_mask(hi2);
-    lo2 = z2 ? 64u - uint32_t(__clzll((long long)z2)) : 0u;
-    len2 = hi2 - lo2 + 1;
-    if (rest & low_mask(lo2)) return 0u;  // three or more runs: keys used as they are
-  }
-  if (len1 + len2 >= 64) return 0u;       // every bit varies
-  return (1u << 28) | (lo1 << 21) | (len1 << 14) | (lo2 << 7) | len2;
-}
-__device__ __forceinline__ uint64_t pack_mask(uint32_t c) {
-  if (!(c >> 28)) return ~0ull;
-  const uint32_t lo1 = c >> 21 & 127, len1 = c >> 14 & 127, lo2 = c >> 7 & 127, len2 = c & 127;
-  return (low_mask(len1) << lo1) | (len2 ? low_mask(len2) << lo2 : 0ull);
-}
-__device__ __forceinline__ uint64_t pack_key(uint64_t u, uint32_t c) {
-  if (!(c >> 28)) return u;
-  const uint32_t lo1 = c >> 21 & 127, len1 = c >> 14 & 127, lo2 = c >> 7 & 127, len2 = c & 127;
-  const uint64_t r = (((u >> lo1) & low_mask(len1)) << len2) | (len2 ? (u >> lo2) & low_mask(len2) : 0ull);
-  return r << (64 - len1 - len2);
-}
-__device__ __forceinline__ uint64_t unpack_key(uint64_t v, uint32_t c, uint64_t constbits) {
-  if (!(c >> 28)) return v;
-  const uint32_t lo1 = c >> 21 & 127, len1 = c >> 14 & 127, lo2 = c >> 7 & 127, len2 = c & 127;
-  const uint64_t r = v >> (64 - len1 - len2);
-  return constbits | ((r >> len2) << lo1) | (len2 ? (r & low_mask(len2)) << lo2 : 0ull);
-}
-// 0: keys as they are; 1: one run ending at bit 0 — a plain left shift; 2: the general pack.
-__device__ __forceinline__ int pack_mode(uint32_t c) {
-  if (!(c >> 28)) return 0;
-  return ((c & 127) == 0 && (c >> 21 & 127) == 0) ? 1 : 2;
-}
-__device__ __forceinline__ uint32_t pack_shift(uint32_t c) { return 64u - (c >> 14 & 127); }  // mode 1
 // Packed rows: the packed key occupies the top len1 + len2 bits; with at most
 // 32 of them the low 32 bits are free for the row id (n <= 2^32), so a row is
 // ONE u64 (key | row id) through the counting passes and the local phase.
@@ -936,9 +889,11 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
 #endif
   const int64_t lo = chunk_lo(a.n, a.chunks, blockIdx.x), hi = chunk_lo(a.n, a.chunks, blockIdx.x + 1);
   const long long* col = static_cast<const long long*>(a.col);
-  const uint64_t k0 = xform(uint64_t(__ldg(col)), a.desc);
+  const uint64_t k0 = xform(uint64_t(__ldg(a.k0_src ? a.k0_src : col)), a.desc);
   uint32_t sh;
-  {  // the key shift from 1024 strided samples — the same in every CTA (mostly L2
+  if (a.pack_given) {  // bucket join: the joint code of both sides (bj_pack_kernel)
+    sh = __ldcg(a.flags + 6);
+  } else {  // the key shift from 1024 strided samples — the same in every CTA (mostly L2
      // hits); a varying bit they miss is caught by the full check below (-> LSD)
     const uint64_t v = xform(uint64_t(sample), a.desc) ^ k0;
     const uint32_t vh = __reduce_or_sync(0xffffffffu, uint32_t(v >> 32));
@@ -1075,7 +1030,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     int na = 0;
     for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
     const bool too_big = __syncthreads_or(tid < 256 && uint64_t(t7) > uint64_t(kBins) * kLocalCap) != 0;
-    if (too_big || na < 4) {
+    if (too_big || (na < 4 && !a.bj)) {
       if (blockIdx.x == 0 && tid == 0) atomicOr(a.flags, 1u);
       return;
     }
@@ -1880,13 +1835,13 @@ struct Layout {
 };
 
 template <typename C, typename T32, typename T64>
-static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L) {
+static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L, bool force_scatter = false) {
   const size_t tiles = size_t((n + kTile - 1) / kTile);
   auto h = t32(c, size_t(kHistReps) * kPasses * kBins);
   auto tc = t32(c, 2 * kPasses);
   auto gb = t32(c, 2);
   auto fl = t32(c, 8);
-  const bool scat = n >= scatter_min_rows();
+  const bool scat = force_scatter || n >= scatter_min_rows();
   auto c7 = scat ? t32(c, size_t(kBins)) : nullptr;          // zeroed with the prefix
   auto c16 = scat ? t32(c, size_t(kSubBuckets)) : nullptr;
   auto d7r = scat ? t32(c, size_t(kD7Reps) * kBins) : nullptr;
@@ -2341,6 +2296,137 @@ int range_partition_perm(const int64_t* keys, int64_t n, int64_t gid_base, const
                                               words);
   count_launches(1);
   return partition_by_words(words, n, parts, perm_out, counts_out, L, stream);
+}
+
+// ---------------------------------------------------------------- bucket join
+static_assert(kBjCap == kLocalCap, "the sub-bucket overflow check guards the bucket join's capacity");
+// bucket_join.cu partitions BOTH join sides into the same 65536 sub-buckets
+// (top 16 bits of one joint key packing) with the scatter path's first three
+// kernels in packed-row mode, then joins sub-bucket pairs on chip. Here: the
+// joint pack code and the per-side launches.
+
+// One CTA: the joint pack code from 512 strided samples of each side, the
+// varying bits taken against the LEFT side's first key (every key of both
+// sides is checked against it by the chunk counts). Packed rows need <= 32
+// varying bits and n <= 2^32 per side; otherwise both sides are flagged to
+// fall back (flags[0]) and every later kernel returns at once.
+__global__ void __launch_bounds__(1024) bj_pack_kernel(const long long* lk, int64_t nl, const long long* rk,
+                                                       int64_t nr, uint32_t* flags_l, uint32_t* flags_r) {
+  __shared__ unsigned long long red;
+  const int tid = threadIdx.x;
+  if (tid == 0) red = 0;
+  __syncthreads();
+  const uint64_t k0 = xform(uint64_t(__ldg(lk)), 0);
+  const long long* col = tid < 512 ? lk : rk;
+  const int64_t n = tid < 512 ? nl : nr;
+  const int j = tid & 511;
+  uint64_t v = 0;
+  if (n > 0) v = xform(uint64_t(__ldg(col + int64_t(j) * n / 512)), 0) ^ k0;
+  const uint32_t vh = __reduce_or_sync(0xffffffffu, uint32_t(v >> 32));
+  const uint32_t vl = __reduce_or_sync(0xffffffffu, uint32_t(v));
+  if ((tid & 31) == 0 && (vh | vl)) atomicOr(&red, (uint64_t(vh) << 32) | vl);
+  __syncthreads();
+  if (tid == 0) {
+    // all keys equal in the sample: pack one low bit so the code is valid (the
+    // chunk counts catch any key that differs)
+    const uint64_t vary = red ? red : 1ull;
+    const uint32_t c = pack_code_of(vary);
+    const bool ok = pack_mode(c) != 0 && (c >> 14 & 127) + (c & 127) <= 32u && nl <= (int64_t(1) << 32) &&
+                    nr <= (int64_t(1) << 32);
+    flags_l[6] = c;
+    flags_r[6] = c;
+    if (!ok) {
+      flags_l[0] = 1u;
+      flags_r[0] = 1u;
+    }
+  }
+}
+
+size_t bj_side_workspace_bytes(int64_t n) {
+  CarveSize c;
+  carve_all(c, std::max<int64_t>(n, 1), [](CarveSize& c, size_t k) { c.take<uint32_t>(k); return (uint32_t*)nullptr; },
+            [](CarveSize& c, size_t k) { c.take<uint64_t>(k); return (uint64_t*)nullptr; }, nullptr, true);
+  return c.used + 256;
+}
+
+static SortArgs bj_args(const int64_t* keys, int64_t n, const int64_t* k0_src, const Layout& L) {
+  SortArgs a = {};
+  a.col = keys;
+  a.n = n;
+  a.width = 8;
+  a.src_mode = kSrcInt64;
+  a.key_mode = kRawAsc;
+  a.orig_keys = keys;
+  a.keys_a = L.keys_a;
+  a.keys_b = L.keys_b;
+  a.vals_a = L.vals_a;
+  a.vals_b = L.vals_b;
+  a.ghist = L.hist;
+  a.tile_counter = L.tile_counter;
+  a.grid_bar = L.grid_bar;
+  a.flags = L.flags;
+  a.sub_off = L.sub_off;
+  a.status = L.status;
+  a.mode = kModeScatter;
+  a.chunk_cnt = L.chunk_cnt;
+  a.cur7 = L.cur7;
+  a.cur16 = L.cur16;
+  a.d7rep = L.d7rep;
+  a.d7_base = L.d7_base;
+  a.items = reinterpret_cast<uint4*>(L.items);
+  a.meta = L.meta;
+  a.allow_pk = 1;
+  a.pack_given = 1;
+  a.k0_src = reinterpret_cast<const long long*>(k0_src);
+  a.bj = 1;
+  return a;
+}
+
+// Both sides into their sub-buckets: packed rows (key | row id) end up in each
+// side's rows_out array (the workspace's keys_a), grouped by the top 16 bits of
+// the joint packing; sub_off[65536 + 1] holds the sub-bucket starts; flags[0]
+// != 0 on either side means "fall back" (a sub-bucket above kLocalCap, keys not
+// packable into 32 bits, a wrapped chunk counter). Nothing is synchronised.
+int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, void* ws_l, size_t ws_l_bytes,
+                 void* ws_r, size_t ws_r_bytes, cudaStream_t stream, BjSide* left, BjSide* right) {
+  if (nl < 1 || nr < 1 || !lkeys || !rkeys || !left || !right) return RL_ERR_BAD_ARG;
+  if (nl > RL_MAX_ROWS || nr > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
+  if ((reinterpret_cast<uintptr_t>(lkeys) | reinterpret_cast<uintptr_t>(rkeys)) & 15) return RL_ERR_BAD_ARG;
+  if ((reinterpret_cast<uintptr_t>(ws_l) | reinterpret_cast<uintptr_t>(ws_r)) % 256 != 0) return RL_ERR_WORKSPACE;
+  if (!scatter_kernels_ready()) return rl_cuda_status(cudaErrorInvalidConfiguration);
+  Layout L[2];
+  const int64_t ns[2] = {nl, nr};
+  void* wss[2] = {ws_l, ws_r};
+  const size_t wsb[2] = {ws_l_bytes, ws_r_bytes};
+  for (int i = 0; i < 2; ++i) {
+    Carve c{static_cast<char*>(wss[i]), wsb[i]};
+    carve_all(c, ns[i], [](Carve& c, size_t k) { return c.take<uint32_t>(k); },
+              [](Carve& c, size_t k) { return c.take<uint64_t>(k); }, &L[i], true);
+    if (!c.ok) return RL_ERR_WORKSPACE;
+    cudaError_t e = cudaMemsetAsync(L[i].hist, 0, L[i].head_bytes, stream);
+    if (e != cudaSuccess) return rl_cuda_status(e);
+  }
+  bj_pack_kernel<<<1, 1024, 0, stream>>>(reinterpret_cast<const long long*>(lkeys), nl,
+                                          reinterpret_cast<const long long*>(rkeys), nr, L[0].flags, L[1].flags);
+  int launched = 1;
+  const int64_t* keys[2] = {lkeys, rkeys};
+  BjSide* outs[2] = {left, right};
+  for (int i = 0; i < 2; ++i) {
+    SortArgs a = bj_args(keys[i], ns[i], lkeys, L[i]);
+    a.chunks = int(std::min<int64_t>(std::min(device_sm_count(), kMaxChunks),
+                                     std::max<int64_t>(32, (ns[i] + kChunkMinRows - 1) / kChunkMinRows)));
+    const int pgrid = device_sm_count() * pass_ctas_per_sm();
+    sub_hist_kernel<<<a.chunks, kScatThreads, kHistSmem, stream>>>(a);
+    top_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
+    sub_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
+    launched += 3;
+    outs[i]->rows = L[i].keys_a;
+    outs[i]->sub_off = L[i].sub_off;
+    outs[i]->flags = L[i].flags;
+    outs[i]->n = ns[i];
+  }
+  count_launches(launched);
+  return rl_cuda_status(cudaGetLastError());
 }
 
 }  // namespace radix

@@ -394,9 +394,78 @@ def multiset_digest(columns: Sequence[torch.Tensor]) -> int:
     return (hi << 64) | lo
 
 
+BJ_MIN_ROWS = 1 << 16  # smaller joins: the sort-based plan (fewer launches)
+BJ_MAX_ROWS = (1 << 16) * 2560 * 9 // 10  # above ~this some sub-bucket surely exceeds its 2560-row cap
+
+
+def _bjoin_allowed(nl: int, nr: int) -> bool:
+    import os
+
+    if os.environ.get("RL_NO_BJOIN", "") not in ("", "0"):
+        return False
+    if os.environ.get("RL_FORCE_BJOIN", "") not in ("", "0"):
+        return nl >= 1 and nr >= 1
+    return min(nl, nr) >= BJ_MIN_ROWS and max(nl, nr) <= BJ_MAX_ROWS
+
+
+class BucketJoinPlan:
+    """rl_bjoin_plan_build result (csrc/bucket_join.cu): both sides as packed
+    (key | row id) words in the same 65536 sub-buckets, the pairs counted per
+    run on chip and scanned; no sorted key axes. ``applies`` is False when the
+    keys need more than 32 bits or a sub-bucket is too large (skew) — then
+    use JoinPlanDev. Same expand / pair_checksum contract as JoinPlanDev."""
+
+    kind = "bucket"
+
+    def __init__(self, left_keys: torch.Tensor, right_keys: torch.Tensor):
+        lib = C.load()
+        lk, rk = aligned16(left_keys), aligned16(right_keys)
+        self._keys = (lk, rk)  # the plan reads the left keys again in expand (constant key bits)
+        nl, nr = lk.numel(), rk.numel()
+        self.ws = workspace(lib.rl_bjoin_workspace_bytes(nl, nr), lk.device)
+        self.plan = C.RlBjoinPlan()
+        C.check(lib.rl_bjoin_plan_build(_ptr(lk), nl, _ptr(rk), nr, _ptr(self.ws), self.ws.numel(),
+                                        ctypes.byref(self.plan), stream_handle()), "rl_bjoin_plan_build")
+        self.n_left, self.n_right = nl, nr
+        host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        off = self.plan.scalars - self.ws.data_ptr()
+        host.view(torch.uint8).copy_(self.ws[off : off + 16], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self.total, ok = host.tolist()
+        self.applies = bool(ok)
+
+    def expand(self, out_begin: int, out_end: int, columns: Sequence[OutColumn] = (),
+               left_rows: Optional[torch.Tensor] = None, right_rows: Optional[torch.Tensor] = None) -> None:
+        lib = C.load()
+        arr, ncols = C.columns_array(
+            (None if c.src is None else c.src.data_ptr(), c.dst.data_ptr(), c.width, c.side) for c in columns
+        )
+        C.check(lib.rl_bjoin_expand(ctypes.byref(self.plan), out_begin, out_end, _ptr(left_rows), _ptr(right_rows),
+                                    arr, ncols, stream_handle()), "rl_bjoin_expand")
+
+    def pair_checksum(self, out_begin: int, out_end: int, acc: torch.Tensor) -> None:
+        C.check(C.load().rl_bjoin_pair_checksum(ctypes.byref(self.plan), out_begin, out_end, _ptr(acc),
+                                                stream_handle()), "rl_bjoin_pair_checksum")
+
+
+def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor):
+    """The join plan for two int64 key columns on the device: the bucket join
+    when it applies (<= 32 varying key bits, no oversized sub-bucket), else
+    the sort-based plan (both key axes + alignment). One host sync either way
+    (plus one when the bucket join declines)."""
+    if _bjoin_allowed(left_keys.numel(), right_keys.numel()):
+        bp = BucketJoinPlan(left_keys, right_keys)
+        if bp.applies:
+            return bp
+        del bp
+    return JoinPlanDev(left_keys, right_keys)
+
+
 class JoinPlanDev:
     """rl_join_plan_build result: both key axes indexed and aligned inside
     one workspace (device pointers in ``plan``), totals fetched once."""
+
+    kind = "sort"
 
     def __init__(self, left_keys: torch.Tensor, right_keys: torch.Tensor):
         lib = C.load()

@@ -93,10 +93,12 @@ def _width(col: torch.Tensor) -> int:
 JoinPlan = engine.JoinPlanDev
 
 
-def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor) -> JoinPlan:
-    """to_tensor x2 + key_axis_align + sizing in one C call over one
-    workspace (rl_join_plan_build); one host sync (the totals)."""
-    return engine.JoinPlanDev(left_keys, right_keys)
+def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor):
+    """Everything a join needs before its output size is known, on the
+    device: the bucket join (csrc/bucket_join.cu) when the keys allow it,
+    else to_tensor x2 + key_axis_align + sizing in one C call over one
+    workspace (rl_join_plan_build). One host sync (the totals)."""
+    return engine.plan_join(left_keys, right_keys)
 
 
 def join(left: DeviceRelation, right: DeviceRelation, key: str,

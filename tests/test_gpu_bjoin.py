@@ -1,0 +1,142 @@
+"""The bucket join (csrc/bucket_join.cu) against the oracle and the sort-based
+plan: the same pair count, the same output rows in the same (key, left row,
+right row) order (tensorpath.py:149-185), chunked slices, the pair checksum,
+and the cases where it must decline (keys needing more than 32 bits, skewed
+sub-buckets) and leave the join to the sort-based plan."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tensorpath_oracle as O
+from paper_2602_21237_b200 import _capi as C
+from paper_2602_21237_b200 import engine, pipeline
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _pairs(plan, a=0, b=None):
+    b = plan.total if b is None else b
+    lr = torch.empty(max(b - a, 1), dtype=torch.int32, device="cuda")
+    rr = torch.empty(max(b - a, 1), dtype=torch.int32, device="cuda")
+    if b > a:
+        plan.expand(a, b, (), lr[: b - a], rr[: b - a])
+    u = lambda t: t[: b - a].cpu().numpy().view(np.uint32).astype(np.int64)  # noqa: E731
+    return u(lr), u(rr)
+
+
+def _check(lk, rk, expect_bucket=True):
+    bp = engine.BucketJoinPlan(_dev(lk), _dev(rk))
+    assert bp.applies == expect_bucket
+    if not expect_bucket:
+        return bp
+    wl, wr = O.join_pairs(lk, rk)
+    assert bp.total == len(wl)
+    gl, gr = _pairs(bp)
+    assert (gl == wl).all() and (gr == wr).all()
+    acc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    bp.pair_checksum(0, bp.total, acc)
+    assert int(acc.item()) & (2**64 - 1) == O.pair_checksum(wl, wr)
+    return bp
+
+
+@pytest.mark.parametrize("n,dom", [(1_000_000, 1_000_000), (300_000, 50_000), (200_000, 3_000), (1 << 16, 1 << 30)])
+def test_uniform_joins_match_the_oracle(n, dom):
+    rng = np.random.default_rng(n + dom)
+    _check(rng.integers(0, dom, n), rng.integers(0, dom, n + 12345))
+
+
+def test_negative_keys_and_unequal_sides():
+    rng = np.random.default_rng(3)
+    lk = rng.integers(-80_000, -1, 400_000)  # all negative: high bits constant (two's complement)
+    rk = rng.integers(-90_000, -10_000, 90_000)
+    _check(lk, rk)
+    _check(rk, lk)
+    # keys crossing zero vary in every bit (bit masks cannot pack them): the plan declines
+    _check(rng.integers(-40_000, 40_000, 400_000), rng.integers(-10_000, 70_000, 90_000), expect_bucket=False)
+
+
+def test_composite_two_runs_cfg4_shape():
+    rng = np.random.default_rng(4)
+    n = 500_000
+    mk = lambda: (rng.integers(0, 2**8, n).astype(np.int64) << np.int64(32)) | rng.integers(0, 2**8, n)  # noqa: E731
+    _check(mk(), mk())
+
+
+def test_no_matches_and_single_key_groups():
+    rng = np.random.default_rng(5)
+    lk = rng.integers(0, 1 << 20, 200_000) * 2
+    _check(lk, lk + 1)  # disjoint: total 0
+
+
+def test_heavy_duplicates_fit_then_fall_back():
+    rng = np.random.default_rng(6)
+    # ~40 rows per key on each side: big pair counts per run, still within the sub-bucket cap
+    keys = rng.integers(0, 20_000, 800_000)
+    bp = _check(keys, rng.integers(0, 20_000, 600_000))
+    assert bp.total > 10**7
+    # one key holding 10% of the rows: its sub-bucket exceeds the cap -> decline
+    skew = rng.integers(0, 1_000_000, 500_000)
+    skew[::10] = 77
+    _check(skew, rng.integers(0, 1_000_000, 500_000), expect_bucket=False)
+
+
+def test_wide_keys_decline():
+    rng = np.random.default_rng(7)
+    lk = rng.integers(-(2**62), 2**62, 300_000)
+    _check(lk, lk[::3].copy(), expect_bucket=False)
+
+
+def test_varying_bit_missed_by_the_joint_sample():
+    rng = np.random.default_rng(8)
+    lk = rng.integers(0, 1 << 20, 300_001)
+    rk = rng.integers(0, 1 << 20, 300_001)
+    rk[5] = 1 << 40  # a bit the sample misses: the chunk counts catch it
+    _check(lk, rk, expect_bucket=False)
+
+
+def test_chunked_slices_and_columns():
+    rng = np.random.default_rng(9)
+    n = 400_000
+    lk, rk = rng.integers(0, 100_000, n), rng.integers(0, 100_000, n)
+    lp = rng.integers(0, 256, (n, 5), dtype=np.uint8)
+    rp = rng.integers(-(2**40), 2**40, n)
+    bp = engine.BucketJoinPlan(_dev(lk), _dev(rk))
+    assert bp.applies
+    wl, wr = O.join_pairs(lk, rk)
+    for a, b in [(0, 1), (17, 100_003), (bp.total // 2, bp.total), (bp.total - 5, bp.total)]:
+        gl, gr = _pairs(bp, a, b)
+        assert (gl == wl[a:b]).all() and (gr == wr[a:b]).all()
+    total = bp.total
+    cols = [engine.OutColumn(None, torch.empty(total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_KEY),
+            engine.OutColumn(_dev(lp), torch.empty((total, 5), dtype=torch.uint8, device="cuda"), 5, C.RL_SIDE_LEFT),
+            engine.OutColumn(_dev(rp), torch.empty(total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_RIGHT)]
+    bp.expand(0, total, cols)
+    assert (cols[0].dst.cpu().numpy() == lk[wl]).all()
+    assert (cols[1].dst.cpu().numpy() == lp[wl]).all()
+    assert (cols[2].dst.cpu().numpy() == rp[wr]).all()
+
+
+def test_pipeline_join_uses_the_bucket_plan_and_equals_the_sort_plan(monkeypatch):
+    rng = np.random.default_rng(10)
+    n = 1_000_000
+    lk, rk = rng.integers(0, n, n), rng.integers(0, n, n)
+    plan = pipeline.plan_join(_dev(lk), _dev(rk))
+    assert plan.kind == "bucket"
+    monkeypatch.setenv("RL_NO_BJOIN", "1")
+    plan2 = pipeline.plan_join(_dev(lk), _dev(rk))
+    assert plan2.kind == "sort" and plan2.total == plan.total
+    a, b = _pairs(plan)
+    c, d = _pairs(plan2)
+    assert (a == c).all() and (b == d).all()
+
+
+def test_small_inputs_forced(monkeypatch):
+    monkeypatch.setenv("RL_FORCE_BJOIN", "1")
+    rng = np.random.default_rng(11)
+    for nl, nr, dom in [(1, 1, 1), (1, 50, 3), (7, 3, 2), (1000, 800, 100), (5000, 1, 10)]:
+        _check(rng.integers(0, dom, nl), rng.integers(0, dom, nr))

@@ -249,10 +249,31 @@ typedef struct rl_bjoin_plan {
   uint64_t* offsets;
   int64_t* scalars;
   const int64_t* left_keys;
+  /* carried payload (written by rl_bjoin_plan_build, read by rl_bjoin_expand) */
+  const uint64_t* pay_left;
+  const uint64_t* pay_right;
+  int32_t words_left, words_right;
+  int32_t carry_cols_left, carry_cols_right;
+  const void* carry_src_left[4];
+  const void* carry_src_right[4];
+  int32_t carry_width_left[4];
+  int32_t carry_width_right[4];
+  int32_t carry_off_left[4];
+  int32_t carry_off_right[4];
 } rl_bjoin_plan;
-RL_API size_t rl_bjoin_workspace_bytes(int64_t n_left, int64_t n_right);
+/* Payload words (8 B) a row of this side carries through the plan's passes
+ * for these columns (0: none; at most 16 bytes / 4 columns, else 0 — they
+ * are then gathered by row id); -1 on a bad argument. */
+RL_API int rl_bjoin_carry_words(const rl_column* columns, int32_t n_columns);
+RL_API size_t rl_bjoin_workspace_bytes(int64_t n_left, int64_t n_right, int32_t left_words,
+                                       int32_t right_words);
+/* left_carry / right_carry (src + width; optional): the output columns of each
+ * side to carry with its rows — rl_bjoin_expand reads a carried column (same
+ * src pointer and width) from beside the row instead of gathering it by row id. */
 RL_API int rl_bjoin_plan_build(const int64_t* left_keys, int64_t n_left,
-                               const int64_t* right_keys, int64_t n_right, void* ws,
+                               const int64_t* right_keys, int64_t n_right,
+                               const rl_column* left_carry, int32_t n_left_carry,
+                               const rl_column* right_carry, int32_t n_right_carry, void* ws,
                                size_t ws_bytes, rl_bjoin_plan* plan, void* stream);
 RL_API int rl_bjoin_expand(const rl_bjoin_plan* plan, uint64_t out_begin,
                            uint64_t out_end, uint32_t* left_rows_out,

@@ -59,7 +59,12 @@ class RlJoinPlan(ctypes.Structure):
 class RlBjoinPlan(ctypes.Structure):
     _fields_ = [(name, ctypes.c_void_p) for name in (
         "rows_left", "rows_right", "sub_off_left", "sub_off_right", "flags_left", "flags_right", "counts",
-        "offsets", "scalars", "left_keys")]
+        "offsets", "scalars", "left_keys", "pay_left", "pay_right")] + [
+        ("words_left", ctypes.c_int32), ("words_right", ctypes.c_int32),
+        ("carry_cols_left", ctypes.c_int32), ("carry_cols_right", ctypes.c_int32),
+        ("carry_src_left", ctypes.c_void_p * 4), ("carry_src_right", ctypes.c_void_p * 4),
+        ("carry_width_left", ctypes.c_int32 * 4), ("carry_width_right", ctypes.c_int32 * 4),
+        ("carry_off_left", ctypes.c_int32 * 4), ("carry_off_right", ctypes.c_int32 * 4)]
 
 
 _P = ctypes.c_void_p
@@ -107,8 +112,10 @@ SIGNATURES = {
         [_P, _P, _P, _P, _P, _I64, _P, _P, _U64, _U64, _P, _P, ctypes.POINTER(RlColumn), _I32, _P],
     ),
     "rl_join_pair_checksum": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P, _U64, _U64, _P, _P]),
-    "rl_bjoin_workspace_bytes": (_SZ, [_I64, _I64]),
-    "rl_bjoin_plan_build": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(RlBjoinPlan), _P]),
+    "rl_bjoin_workspace_bytes": (_SZ, [_I64, _I64, _I32, _I32]),
+    "rl_bjoin_carry_words": (ctypes.c_int, [ctypes.POINTER(RlColumn), _I32]),
+    "rl_bjoin_plan_build": (ctypes.c_int, [_P, _I64, _P, _I64, ctypes.POINTER(RlColumn), _I32,
+                                           ctypes.POINTER(RlColumn), _I32, _P, _SZ, ctypes.POINTER(RlBjoinPlan), _P]),
     "rl_bjoin_expand": (ctypes.c_int, [ctypes.POINTER(RlBjoinPlan), _U64, _U64, _P, _P, ctypes.POINTER(RlColumn),
                                        _I32, _P]),
     "rl_bjoin_pair_checksum": (ctypes.c_int, [ctypes.POINTER(RlBjoinPlan), _U64, _U64, _P, _P]),

@@ -13,16 +13,33 @@ namespace radix {
 constexpr int kBjSubBuckets = 1 << 16;  // sub-buckets: top 16 bits of the packed key
 constexpr int kBjCap = 2560;            // rows of one side in one sub-bucket at most (kLocalCap)
 
+constexpr int kBjMaxCarryCols = 4;
+constexpr int kBjMaxCarryWords = 2;  // <= 16 payload bytes a row carried through the passes
+
+// Columns of one side carried with its rows (packed at byte offsets into
+// `words` u64 words per row), so the emit reads them beside the row instead
+// of gathering them by row id.
+struct BjCarry {
+  int n = 0;
+  const uint8_t* src[kBjMaxCarryCols] = {};
+  int width[kBjMaxCarryCols] = {};
+  int off[kBjMaxCarryCols] = {};
+  int words = 0;
+};
+
 struct BjSide {
   const uint64_t* rows;     // [n] packed words (key bits << 32 | row id), grouped by sub-bucket
+  const uint64_t* pay;      // [n * words] carried payload words, parallel to rows (words > 0)
+  int words;
   const uint32_t* sub_off;  // [kBjSubBuckets + 1] sub-bucket starts
   uint32_t* flags;          // [0] != 0: fall back; [6] the joint pack code
   int64_t n;
 };
 
-size_t bj_side_workspace_bytes(int64_t n);
-int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, void* ws_l, size_t ws_l_bytes,
-                 void* ws_r, size_t ws_r_bytes, cudaStream_t stream, BjSide* left, BjSide* right);
+size_t bj_side_workspace_bytes(int64_t n, int words);
+int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, const BjCarry& lcarry,
+                 const BjCarry& rcarry, void* ws_l, size_t ws_l_bytes, void* ws_r, size_t ws_r_bytes,
+                 cudaStream_t stream, BjSide* left, BjSide* right);
 
 }  // namespace radix
 }  // namespace rl

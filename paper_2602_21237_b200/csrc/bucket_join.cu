@@ -63,6 +63,9 @@ struct PlanArgs {
   uint64_t* offs;    // [kBjSubBuckets] first output row per (group, run slot)
   int64_t* scalars;  // [0] total pairs, [1] 1 = the bucket join applies
   const long long* k0_src;  // the left side's first key (constant bits of every key)
+  const uint64_t* pay_l;    // carried payload words, parallel to rows_l (words_l per row)
+  const uint64_t* pay_r;
+  int words_l, words_r;
 };
 
 // Runs of one group: consecutive sub-buckets [s, e) with at most kBjCap rows
@@ -105,7 +108,8 @@ __device__ __forceinline__ bool fell_back(const PlanArgs& a) {
 // Bin `cnt` rows (this thread's rows in w[]) into dst[] grouped by bin; hist[]
 // ends as each bin's END. hist must be zero for the nbins bins on entry.
 __device__ __forceinline__ void bin_rows(const uint64_t (&w)[kRowsPerThread], uint32_t cnt, const Bins& bins,
-                                         uint32_t nbins, uint32_t* hist, uint64_t* dst, uint64_t* scan_scratch) {
+                                         uint32_t nbins, uint32_t* hist, uint64_t* dst, uint64_t* scan_scratch,
+                                         uint16_t* dst_idx = nullptr) {
   const int tid = threadIdx.x;
 #pragma unroll
   for (int u = 0; u < kRowsPerThread; ++u)
@@ -130,8 +134,13 @@ __device__ __forceinline__ void bin_rows(const uint64_t (&w)[kRowsPerThread], ui
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < kRowsPerThread; ++u)
-    if (tid + u * kThreads < int(cnt)) dst[atomicAdd(&hist[bins.of(w[u])], 1u)] = w[u];
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    if (tid + u * kThreads < int(cnt)) {
+      const uint32_t at = atomicAdd(&hist[bins.of(w[u])], 1u);
+      dst[at] = w[u];
+      if (dst_idx) dst_idx[at] = uint16_t(tid + u * kThreads);  // the row's load index in its run
+    }
+  }
   __syncthreads();
 }
 
@@ -145,7 +154,7 @@ __device__ __forceinline__ void load_rows(const uint64_t* rows, uint32_t r0, uin
 }
 
 // ---------------------------------------------------------------- count
-__global__ void __launch_bounds__(kThreads, 2) bj_count_kernel(PlanArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
   __shared__ uint64_t br[kBjCap];
   __shared__ uint32_t hist[kMaxBins];
   __shared__ uint32_t offl[kGroupSubs + 1], offr[kGroupSubs + 1], ends[kGroupSubs];
@@ -196,25 +205,37 @@ __global__ void __launch_bounds__(kThreads, 2) bj_count_kernel(PlanArgs a) {
 }
 
 // ---------------------------------------------------------------- scan
+// One CTA: the 65536 run counts in 8 chunks staged through shared memory
+// (coalesced loads), an exclusive scan of each chunk carried into the next.
 __global__ void __launch_bounds__(1024) bj_scan_kernel(PlanArgs a) {
+  constexpr int kChunk = 8192, kPer = kChunk / 1024;
+  __shared__ uint32_t buf[kChunk];
   __shared__ uint64_t scratch[34];
-  constexpr int kPer = kBjSubBuckets / 1024;  // 64
   const int tid = threadIdx.x;
   const bool ok = *reinterpret_cast<volatile const uint32_t*>(a.flags_l) == 0 &&
                   *reinterpret_cast<volatile const uint32_t*>(a.flags_r) == 0;
-  uint64_t run = 0;
-  if (ok)
-    for (int i = 0; i < kPer; ++i) run += __ldcg(a.counts + tid * kPer + i);
-  uint64_t total;
-  uint64_t start = block_exclusive_scan<1024>(run, scratch, &total);
-  if (ok) {
-    for (int i = 0; i < kPer; ++i) {
-      a.offs[tid * kPer + i] = start;
-      start += __ldcg(a.counts + tid * kPer + i);
+  uint64_t carry = 0;
+  for (int c0 = 0; c0 < kBjSubBuckets; c0 += kChunk) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) buf[i * 1024 + tid] = ok ? __ldcg(a.counts + c0 + i * 1024 + tid) : 0u;
+    __syncthreads();
+    uint64_t run = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) run += buf[tid * kPer + i];
+    uint64_t total;
+    uint64_t start = carry + block_exclusive_scan<1024>(run, scratch, &total);
+    if (ok) {
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        a.offs[c0 + tid * kPer + i] = start;
+        start += buf[tid * kPer + i];
+      }
     }
+    carry += total;
+    __syncthreads();  // buf and scratch reused by the next chunk
   }
   if (tid == 0) {
-    a.scalars[0] = ok ? int64_t(total) : 0;
+    a.scalars[0] = ok ? int64_t(carry) : 0;
     a.scalars[1] = ok ? 1 : 0;
   }
 }
@@ -229,8 +250,15 @@ struct EmitArgs {
 };
 
 constexpr int kMaxCols = RL_MAX_COLUMNS;
+struct EmitCol {
+  const uint8_t* src;  // gathered by row id (carry_off < 0)
+  uint8_t* dst;
+  int width;
+  int side;
+  int carry_off;       // >= 0: the bytes at this offset of the row's carried payload words
+};
 struct Cols {
-  rl_column c[kMaxCols];
+  EmitCol c[kMaxCols];
   int n;
 };
 
@@ -239,7 +267,8 @@ struct Cols {
 // their bin-mates; bins above kRankMax rows go through a warp's bitonic
 // network in place first.
 __device__ __forceinline__ void finish_sort(uint64_t* grouped, uint64_t* sorted, const uint32_t* hist,
-                                            const Bins& bins, uint32_t cnt, uint32_t* big, uint32_t* nbig) {
+                                            const Bins& bins, uint32_t cnt, uint32_t* big, uint32_t* nbig,
+                                            uint16_t* gidx, uint16_t* sidx) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) *nbig = 0;
   __syncthreads();
@@ -257,6 +286,7 @@ __device__ __forceinline__ void finish_sort(uint64_t* grouped, uint64_t* sorted,
     uint32_t rk = 0;
     for (uint32_t i = b0; i < b1; ++i) rk += grouped[i] < w ? 1u : 0u;
     sorted[b0 + rk] = w;
+    sidx[b0 + rk] = gidx[p];
   }
   __syncthreads();
   const uint32_t nb = *nbig;  // <= kBjCap / (kRankMax + 1) = 52 < 64
@@ -277,13 +307,19 @@ __device__ __forceinline__ void finish_sort(uint64_t* grouped, uint64_t* sorted,
             if (v < u) {
               grouped[b0 + i] = v;
               grouped[b0 + q] = u;
+              const uint16_t t = gidx[b0 + i];
+              gidx[b0 + i] = gidx[b0 + q];
+              gidx[b0 + q] = t;
             }
           }
         }
         __syncwarp();
       }
     }
-    for (uint32_t p = b0 + lane; p < b1; p += 32) sorted[p] = grouped[p];
+    for (uint32_t p = b0 + lane; p < b1; p += 32) {
+      sorted[p] = grouped[p];
+      sidx[p] = gidx[p];
+    }
   }
   __syncthreads();
 }
@@ -296,7 +332,10 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
   uint64_t* gx = sr + kBjCap;                         // [kBjCap] grouped-by-bin scratch / per-left-row arrays
   uint32_t* hr = reinterpret_cast<uint32_t*>(gx + kBjCap);  // [kMaxBins] right bin ends (kept for the match)
   uint32_t* hl = hr + kMaxBins;                             // [kMaxBins] left bin ends
-  uint64_t* scratch = reinterpret_cast<uint64_t*>(hl + kMaxBins);  // [kThreads / 32 + 2]
+  uint16_t* gidx = reinterpret_cast<uint16_t*>(hl + kMaxBins);  // [kBjCap] load index of grouped rows
+  uint16_t* lidx = gidx + kBjCap;                               // [kBjCap] load index of sorted left rows
+  uint16_t* ridx = lidx + kBjCap;                               // [kBjCap] ... right rows
+  uint64_t* scratch = reinterpret_cast<uint64_t*>(ridx + kBjCap);  // [kThreads / 32 + 2]
   uint32_t* misc = reinterpret_cast<uint32_t*>(scratch + kThreads / 32 + 2);  // offsets, runs, big bins
   uint32_t* offl = misc;
   uint32_t* offr = misc + 17;
@@ -342,15 +381,15 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       load_rows(a.rows_r, r0, nrr, w);
       load_rows(a.rows_l, l0, nl, wl);
       __syncthreads();
-      bin_rows(w, nrr, bins, nbins, hr, gx, scratch);
-      finish_sort(gx, sr, hr, bins, nrr, big, nbig);
-      bin_rows(wl, nl, bins, nbins, hl, gx, scratch);
-      finish_sort(gx, sl, hl, bins, nl, big, nbig);
+      bin_rows(w, nrr, bins, nbins, hr, gx, scratch, gidx);
+      finish_sort(gx, sr, hr, bins, nrr, big, nbig, gidx, ridx);
+      bin_rows(wl, nl, bins, nbins, hl, gx, scratch, gidx);
+      finish_sort(gx, sl, hl, bins, nl, big, nbig, gidx, lidx);
       // every left row (sorted index p): its matching right range [rs, rs + m) in sr
       uint32_t* m_arr = reinterpret_cast<uint32_t*>(gx);
       uint32_t* rs_arr = m_arr + kBjCap;
       constexpr int kPer = kRowsPerThread;
-      uint32_t mloc[kPer], run = 0;
+      uint32_t mloc[kPer], run = 0, mmax = 0;
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {  // thread owns left rows tid * kPer + u (consecutive: the scan below)
         const uint32_t p = tid * kPer + u;
@@ -369,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         }
         mloc[u] = m;
         run += m;
+        mmax = max(mmax, m);
       }
       uint32_t total;
       uint32_t start = block_exclusive_scan<kThreads>(run, reinterpret_cast<uint32_t*>(scratch), &total);
@@ -378,35 +418,59 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         if (p < nl) m_arr[p] = start;  // exclusive prefix: the first output of left row p
         start += mloc[u];
       }
-      __syncthreads();
-      // outputs in order: t -> left row p (last prefix <= t), right row rs[p] + t - pre[p]
+      // few pairs per left row (unique-ish keys): one thread per left row writes
+      // its outputs (consecutive rows -> consecutive outputs, no search);
+      // otherwise output-space: every thread takes outputs t and finds its
+      // left row by binary search over the prefixes
+      __syncthreads();  // prefixes (m_arr) and right starts (rs_arr) complete
+      // (measured: one thread per left row writing its pairs was slower than the
+      // search — divergent pair counts, gaps in the output runs)
+      constexpr bool per_row = false;
       const uint64_t lo = e.out_begin > base ? e.out_begin - base : 0;
       const uint64_t hi = min(uint64_t(total), e.out_end - base);
-      for (uint64_t t = lo + tid; t < hi; t += kThreads) {
-        uint32_t x = 0, y = nl;  // largest p with pre[p] <= t
-        while (y - x > 1) {
-          const uint32_t mid = (x + y) >> 1;
-          if (m_arr[mid] <= uint32_t(t)) x = mid;
-          else y = mid;
-        }
+      auto write = [&](uint32_t x, uint32_t t) {
         const uint64_t wv = sl[x];
-        const uint64_t wr = sr[rs_arr[x] + (uint32_t(t) - m_arr[x])];
+        const uint32_t jr = rs_arr[x] + (t - m_arr[x]);
+        const uint64_t wr = sr[jr];
         const uint32_t lrow = uint32_t(wv), rrow = uint32_t(wr);
         if constexpr (CHECKSUM) {
           sum += fmix64((uint64_t(lrow) << 32) | rrow);
-          continue;
+          return;
         }
         const uint64_t o = base + t - e.out_begin;
         if (e.lrows_out) __stcs(e.lrows_out + o, lrow);
         if (e.rrows_out) __stcs(e.rrows_out + o, rrow);
         for (int ci = 0; ci < cols.n; ++ci) {
-          const rl_column& c = cols.c[ci];
+          const EmitCol& c = cols.c[ci];
           const int wd = c.width;
-          uint8_t* dst = static_cast<uint8_t*>(c.dst) + o * uint64_t(wd);
-          if (c.side == RL_SIDE_KEY)
+          uint8_t* dst = c.dst + o * uint64_t(wd);
+          if (c.side == RL_SIDE_KEY) {
             __stcs(reinterpret_cast<long long*>(dst), key_of(wv));
-          else
-            copy_row(static_cast<const uint8_t*>(c.src) + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * wd, dst, wd);
+          } else if (c.carry_off >= 0) {  // carried: the run's payload window (L1 / L2 resident)
+            const bool left = c.side == RL_SIDE_LEFT;
+            const uint64_t* pay = left ? a.pay_l : a.pay_r;
+            const int words = left ? a.words_l : a.words_r;
+            const uint64_t at = left ? uint64_t(l0) + lidx[x] : uint64_t(r0) + ridx[jr];
+            copy_row(reinterpret_cast<const uint8_t*>(pay + at * words) + c.carry_off, dst, wd);
+          } else {
+            copy_row(c.src + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * wd, dst, wd);
+          }
+        }
+      };
+      if (per_row) {
+        for (uint32_t x = tid; x < nl; x += kThreads) {
+          const uint32_t t0 = m_arr[x], t1 = x + 1 < nl ? m_arr[x + 1] : total;
+          for (uint32_t t = max(t0, uint32_t(lo)); t < min(t1, uint32_t(hi)); ++t) write(x, t);
+        }
+      } else {
+        for (uint64_t t = lo + tid; t < hi; t += kThreads) {
+          uint32_t x = 0, y = nl;  // largest p with pre[p] <= t
+          while (y - x > 1) {
+            const uint32_t mid = (x + y) >> 1;
+            if (m_arr[mid] <= uint32_t(t)) x = mid;
+            else y = mid;
+          }
+          write(x, uint32_t(t));
         }
       }
       __syncthreads();  // smem reused by the next run
@@ -419,15 +483,15 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
   }
 }
 
-constexpr size_t kEmitSmem = size_t(kBjCap) * 8 * 3 + size_t(kMaxBins) * 4 * 2 + (kThreads / 32 + 2) * 8 + 128 * 4;
+constexpr size_t kEmitSmem = size_t(kBjCap) * 8 * 3 + size_t(kMaxBins) * 4 * 2 + size_t(kBjCap) * 2 * 3 +
+                             (kThreads / 32 + 2) * 8 + 128 * 4;
 
 // ---------------------------------------------------------------- host
-static size_t scratch_offset(int64_t nl) { return align_up(radix::bj_side_workspace_bytes(nl), 256); }
+static size_t side_bytes(int64_t n, int words) { return align_up(radix::bj_side_workspace_bytes(n, words), 256); }
 
-size_t workspace_bytes(int64_t nl, int64_t nr) {
-  return scratch_offset(nl) + align_up(radix::bj_side_workspace_bytes(nr), 256) +
-         align_up(sizeof(uint32_t) * kBjSubBuckets, 256) + align_up(sizeof(uint64_t) * kBjSubBuckets, 256) +
-         align_up(sizeof(int64_t) * 4, 256) + 256;
+size_t workspace_bytes(int64_t nl, int64_t nr, int lwords, int rwords) {
+  return side_bytes(nl, lwords) + side_bytes(nr, rwords) + align_up(sizeof(uint32_t) * kBjSubBuckets, 256) +
+         align_up(sizeof(uint64_t) * kBjSubBuckets, 256) + align_up(sizeof(int64_t) * 4, 256) + 256;
 }
 
 static int emit_grid() {
@@ -451,20 +515,57 @@ static int emit_grid() {
   });
 }
 
-int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, void* ws, size_t ws_bytes,
-         rl_bjoin_plan* out, cudaStream_t stream) {
-  if (!out || nl < 1 || nr < 1) return RL_ERR_BAD_ARG;
-  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0 || ws_bytes < workspace_bytes(nl, nr)) return RL_ERR_WORKSPACE;
+// A side's carried columns: natural alignment inside <= 16 bytes of payload
+// words, widest first; all of them or none (-> gathered by row id).
+static int make_carry(const rl_column* cols, int n, radix::BjCarry* cy, int32_t* offs) {
+  *cy = radix::BjCarry{};
+  if (n <= 0) return RL_OK;
+  if (!cols || n > radix::kBjMaxCarryCols) return n > radix::kBjMaxCarryCols ? RL_OK : RL_ERR_BAD_ARG;
+  int order[radix::kBjMaxCarryCols];
+  for (int i = 0; i < n; ++i) {
+    if (!cols[i].src || cols[i].width <= 0) return RL_ERR_BAD_ARG;
+    order[i] = i;
+  }
+  std::sort(order, order + n, [&](int x, int y) { return cols[x].width > cols[y].width; });
+  int at = 0;
+  for (int k = 0; k < n; ++k) {
+    const int w = cols[order[k]].width;
+    const int al = (w % 8 == 0) ? 8 : (w % 4 == 0) ? 4 : 1;
+    at = (at + al - 1) / al * al;
+    offs[order[k]] = at;
+    at += w;
+  }
+  if (at > 8 * radix::kBjMaxCarryWords) return RL_OK;  // too wide: gather instead
+  cy->n = n;
+  cy->words = (at + 7) / 8;
+  for (int i = 0; i < n; ++i) {
+    cy->src[i] = static_cast<const uint8_t*>(cols[i].src);
+    cy->width[i] = cols[i].width;
+    cy->off[i] = offs[i];
+  }
+  return RL_OK;
+}
+
+int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, const rl_column* lcarry, int nlc,
+         const rl_column* rcarry, int nrc, void* ws, size_t ws_bytes, rl_bjoin_plan* out, cudaStream_t stream) {
+  if (!out || nl < 1 || nr < 1 || nlc < 0 || nrc < 0) return RL_ERR_BAD_ARG;
+  *out = rl_bjoin_plan{};
+  radix::BjCarry lc, rc;
+  int st = make_carry(lcarry, nlc, &lc, out->carry_off_left);
+  if (st == RL_OK) st = make_carry(rcarry, nrc, &rc, out->carry_off_right);
+  if (st != RL_OK) return st;
+  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0 || ws_bytes < workspace_bytes(nl, nr, lc.words, rc.words))
+    return RL_ERR_WORKSPACE;
   char* base = static_cast<char*>(ws);
-  const size_t wl = scratch_offset(nl), wr = align_up(radix::bj_side_workspace_bytes(nr), 256);
+  const size_t wl = side_bytes(nl, lc.words), wr = side_bytes(nr, rc.words);
   uint32_t* counts = reinterpret_cast<uint32_t*>(base + wl + wr);
   uint64_t* offs = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(counts) + align_up(sizeof(uint32_t) * kBjSubBuckets, 256));
   int64_t* scalars = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(offs) + align_up(sizeof(uint64_t) * kBjSubBuckets, 256));
   BjSide L, R;
-  int st = radix::bj_partition(lkeys, nl, rkeys, nr, base, wl, base + wl, wr, stream, &L, &R);
+  st = radix::bj_partition(lkeys, nl, rkeys, nr, lc, rc, base, wl, base + wl, wr, stream, &L, &R);
   if (st != RL_OK) return st;
   PlanArgs a{L.rows, R.rows, L.sub_off, R.sub_off, L.flags, R.flags, counts, offs, scalars,
-             reinterpret_cast<const long long*>(lkeys)};
+             reinterpret_cast<const long long*>(lkeys), L.pay, R.pay, L.words, R.words};
   const int grid = device_sm_count() * 3;
   bj_count_kernel<<<grid, kThreads, 0, stream>>>(a);
   bj_scan_kernel<<<1, 1024, 0, stream>>>(a);
@@ -479,7 +580,33 @@ int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, voi
   out->offsets = offs;
   out->scalars = scalars;
   out->left_keys = lkeys;
+  out->pay_left = L.pay;
+  out->pay_right = R.pay;
+  out->words_left = L.words;
+  out->words_right = R.words;
+  out->carry_cols_left = lc.n;
+  out->carry_cols_right = rc.n;
+  for (int i = 0; i < lc.n; ++i) {
+    out->carry_src_left[i] = lc.src[i];
+    out->carry_width_left[i] = lc.width[i];
+  }
+  for (int i = 0; i < rc.n; ++i) {
+    out->carry_src_right[i] = rc.src[i];
+    out->carry_width_right[i] = rc.width[i];
+  }
   return rl_cuda_status(cudaGetLastError());
+}
+
+// The carried payload offset of an output column, or -1 (gathered by row id).
+static int carried_offset(const rl_bjoin_plan* p, const rl_column& c) {
+  const bool left = c.side == RL_SIDE_LEFT;
+  const int n = left ? p->carry_cols_left : p->carry_cols_right;
+  for (int i = 0; i < n; ++i) {
+    const void* src = left ? p->carry_src_left[i] : p->carry_src_right[i];
+    const int w = left ? p->carry_width_left[i] : p->carry_width_right[i];
+    if (src == c.src && w == c.width) return left ? p->carry_off_left[i] : p->carry_off_right[i];
+  }
+  return -1;
 }
 
 int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t* lrows_out, uint32_t* rrows_out,
@@ -499,13 +626,15 @@ int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t*
     } else if (c.width > 0 && !c.src) {
       return RL_ERR_BAD_ARG;
     }
-    cs.c[i] = c;
+    cs.c[i] = EmitCol{static_cast<const uint8_t*>(c.src), static_cast<uint8_t*>(c.dst), c.width, c.side,
+                      c.side == RL_SIDE_KEY ? -1 : carried_offset(p, c)};
   }
   const int grid = emit_grid();
   if (grid < 1) return rl_cuda_status(cudaErrorInvalidConfiguration);
   EmitArgs e;
   e.p = PlanArgs{p->rows_left, p->rows_right, p->sub_off_left, p->sub_off_right, p->flags_left, p->flags_right,
-                 p->counts, p->offsets, p->scalars, reinterpret_cast<const long long*>(p->left_keys)};
+                 p->counts, p->offsets, p->scalars, reinterpret_cast<const long long*>(p->left_keys), p->pay_left,
+                 p->pay_right, p->words_left, p->words_right};
   e.out_begin = out_begin;
   e.out_end = out_end;
   e.lrows_out = lrows_out;
@@ -522,14 +651,23 @@ int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t*
 
 extern "C" {
 
-RL_API size_t rl_bjoin_workspace_bytes(int64_t n_left, int64_t n_right) {
-  return rl::bjoin::workspace_bytes(std::max<int64_t>(n_left, 1), std::max<int64_t>(n_right, 1));
+RL_API size_t rl_bjoin_workspace_bytes(int64_t n_left, int64_t n_right, int32_t left_words, int32_t right_words) {
+  return rl::bjoin::workspace_bytes(std::max<int64_t>(n_left, 1), std::max<int64_t>(n_right, 1), left_words,
+                                    right_words);
+}
+
+RL_API int rl_bjoin_carry_words(const rl_column* columns, int32_t n_columns) {
+  rl::radix::BjCarry cy;
+  int32_t offs[rl::radix::kBjMaxCarryCols];
+  if (rl::bjoin::make_carry(columns, n_columns, &cy, offs) != RL_OK) return -1;
+  return cy.words;
 }
 
 RL_API int rl_bjoin_plan_build(const int64_t* left_keys, int64_t n_left, const int64_t* right_keys, int64_t n_right,
-                               void* ws, size_t ws_bytes, rl_bjoin_plan* plan, void* stream) {
-  return rl::bjoin::plan(left_keys, n_left, right_keys, n_right, ws, ws_bytes, plan,
-                         static_cast<cudaStream_t>(stream));
+                               const rl_column* left_carry, int32_t n_left_carry, const rl_column* right_carry,
+                               int32_t n_right_carry, void* ws, size_t ws_bytes, rl_bjoin_plan* plan, void* stream) {
+  return rl::bjoin::plan(left_keys, n_left, right_keys, n_right, left_carry, n_left_carry, right_carry, n_right_carry,
+                         ws, ws_bytes, plan, static_cast<cudaStream_t>(stream));
 }
 
 RL_API int rl_bjoin_expand(const rl_bjoin_plan* plan, uint64_t out_begin, uint64_t out_end, uint32_t* left_rows_out,

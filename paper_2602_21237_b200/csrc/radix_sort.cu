@@ -209,6 +209,14 @@ struct SortArgs {
   int pack_given;
   const long long* k0_src;   // the key whose constant bits every key must share (default: col[0])
   int bj;                    // keep going with < 4 varying digits (the join needs the sub-buckets)
+  // bucket join: payload words carried with every row through the counting
+  // passes (CW u64 words per row; the side's output columns packed in)
+  int carry_n;               // carried columns
+  const uint8_t* carry_src[4];
+  int carry_width[4];
+  int carry_off[4];          // byte offset in the row's payload words
+  uint64_t* pay_a;           // [n * CW] parallel to keys_a
+  uint64_t* pay_b;           // [n * CW] parallel to keys_b
 };
 
 // Global digit count (pass p, digit d): the sum of the histogram replicas.
@@ -799,18 +807,32 @@ __device__ __forceinline__ uint32_t scan256(uint32_t c, uint32_t* scratch) {
 
 struct PTile {  // shared memory of the counting passes
   uint64_t* sk;       // [kPTile] staged keys
-  uint32_t* sv;       // [kPTile] staged row ids
+  uint32_t* sv;       // [kPTile] staged row ids (CW == 0)
+  uint64_t* sp;       // [kPTile * CW] staged carried payload words (CW > 0)
   uint32_t* hist;     // [256] tile digit counts -> tile digit starts
   uint32_t* base;     // [256] output position of staged row 0 of each digit
   uint32_t* aux;      // [256] pass A: digit-7 bucket starts
   uint32_t* scratch;  // [64]
 };
 
+// Staging bytes of a counting pass: keys + row ids, or (bucket join) keys +
+// CW carried payload words per row (packed rows: no row-id stream).
+constexpr size_t pstage_bytes(int cw) { return cw ? size_t(kPTile) * 8 * (1 + cw) : kPStage; }
+constexpr size_t psmem_bytes(int cw) { return pstage_bytes(cw) + 3 * 256 * 4 + 64 * 4; }
+static_assert(psmem_bytes(0) == kPSmem, "the sort's pass layout is unchanged");
+
+template <int CW>  // carried payload words per row; arrays of CW == 0 keep one dummy slot
+struct Carry {
+  uint64_t p[kPItems][CW > 0 ? CW : 1];
+};
+
+template <int CW = 0>
 __device__ __forceinline__ PTile ptile(uint8_t* sm) {
   PTile t;
   t.sk = reinterpret_cast<uint64_t*>(sm);
   t.sv = reinterpret_cast<uint32_t*>(sm + size_t(kPTile) * 8);
-  t.hist = reinterpret_cast<uint32_t*>(sm + kPStage);
+  t.sp = reinterpret_cast<uint64_t*>(sm + size_t(kPTile) * 8);
+  t.hist = reinterpret_cast<uint32_t*>(sm + pstage_bytes(CW));
   t.base = t.hist + 256;
   t.aux = t.base + 256;
   t.scratch = t.aux + 256;
@@ -825,9 +847,12 @@ __device__ __forceinline__ PTile ptile(uint8_t* sm) {
 // following tile into the same registers, in flight during the write-out.
 // PK (packed rows): the row id travels in the key word's low 32 bits — no
 // separate row-id stream (v[] unused).
-template <int SHIFT, bool PK, typename Reserve, typename Next>
-__device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int tn, const PTile& s,
-                                              uint64_t* out_k, uint32_t* out_v, Reserve reserve, Next next) {
+// CW > 0 (bucket join): CW payload words ride with every row (c.p), staged and
+// written to out_p[o * CW + w] beside the key.
+template <int SHIFT, bool PK, int CW = 0, typename Reserve, typename Next>
+__device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cr, int tn,
+                                              const PTile& s, uint64_t* out_k, uint32_t* out_v, uint64_t* out_p,
+                                              Reserve reserve, Next next) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t r[kPItems];
 #pragma unroll
@@ -857,18 +882,28 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
     if (u * kPThreads + tid < tn) {
       const uint32_t p = s.hist[uint32_t(k[u] >> SHIFT) & 255u] + r[u];
       s.sk[p] = k[u];
-      if constexpr (!PK) s.sv[p] = v[u];
+      if constexpr (CW > 0) {
+#pragma unroll
+        for (int w = 0; w < CW; ++w) s.sp[p * CW + w] = cr.p[u][w];
+      } else if constexpr (!PK) {
+        s.sv[p] = v[u];
+      }
     }
   }
   if (tid < 256) s.base[tid] = res - excl;
   __syncthreads();
-  next(k, v);
+  next(k, v, cr);
   if (tid < 256) s.hist[tid] = 0;  // for the next tile (the write-out reads only s.base)
   for (int i = tid; i < tn; i += kPThreads) {
     const uint64_t key = s.sk[i];
     const uint32_t o = s.base[uint32_t(key >> SHIFT) & 255u] + uint32_t(i);
     out_k[o] = key;
-    if constexpr (!PK) out_v[o] = s.sv[i];
+    if constexpr (CW > 0) {
+#pragma unroll
+      for (int w = 0; w < CW; ++w) out_p[size_t(o) * CW + w] = s.sp[i * CW + w];
+    } else if constexpr (!PK) {
+      out_v[o] = s.sv[i];
+    }
   }
   __syncthreads();  // staging and s.base reused by the next tile
 }
@@ -1009,9 +1044,40 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   }
 }
 
+// The carried payload words of input row `row` (bucket join): the carried
+// columns' bytes packed at their offsets; 8-byte-aligned 8 / 16-byte columns
+// with whole-word loads, anything else byte by byte.
+template <int CW>
+__device__ __forceinline__ void load_carry(const SortArgs& a, uint64_t row, uint64_t (&w)[CW > 0 ? CW : 1]) {
+  if (a.carry_n == 1 && a.carry_width[0] == 8 * CW) {  // one column filling the words: whole-word loads
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.carry_src[0]) + row * CW;
+#pragma unroll
+    for (int i = 0; i < CW; ++i) w[i] = __ldcs(src + i);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < CW; ++i) w[i] = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (c >= a.carry_n) break;
+    const int wd = a.carry_width[c], off = a.carry_off[c];
+    const uint8_t* src = a.carry_src[c] + row * uint64_t(wd);
+    if ((wd == 8 || wd == 16) && (off & 7) == 0) {
+      w[off >> 3] = __ldcs(reinterpret_cast<const unsigned long long*>(src));
+      if (wd == 16 && (off >> 3) + 1 < CW) w[(off >> 3) + 1] = __ldcs(reinterpret_cast<const unsigned long long*>(src) + 1);
+    } else {
+      for (int b = 0; b < wd; ++b) {
+        const int at = off + b;
+        if ((at >> 3) < CW) w[at >> 3] |= uint64_t(__ldg(src + b)) << ((at & 7) * 8);
+      }
+    }
+  }
+}
+
+template <int CW = 0>
 __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_kernel(SortArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const PTile s = ptile(sm);
+  const PTile s = ptile<CW>(sm);
   const int tid = threadIdx.x;
   pdl_wait();  // the chunk counts
   pdl_launch_dependents();
@@ -1097,33 +1163,64 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   const uint32_t shl = pack_shift(sh);
   auto tiles = [&](auto packed, auto pkc) {
     constexpr bool PK = decltype(pkc)::value;
-    auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], int64_t t0) {
+    // every load of a tile is issued before the first use (the payload loads
+    // of the common one-column case too), then the keys are transformed
+    const bool whole_words = CW > 0 && a.carry_n == 1 && a.carry_width[0] == 8 * CW;
+    auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cr, int64_t t0) {
       const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
 #pragma unroll
       for (int u = 0; u < kPItems; ++u) {
         const int j = u * kPThreads + tid;
-        k[u] = j < tn ? pack_as<decltype(packed)::value>(xform(uint64_t(__ldcs(col + t0 + j)), a.desc), sh, shl) : 0ull;
+        k[u] = j < tn ? uint64_t(__ldcs(col + t0 + j)) : 0ull;
+      }
+      if constexpr (CW > 0) {
+        if (whole_words) {
+          const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.carry_src[0]);
+#pragma unroll
+          for (int u = 0; u < kPItems; ++u) {
+            const int j = u * kPThreads + tid;
+#pragma unroll
+            for (int w = 0; w < CW; ++w) cr.p[u][w] = j < tn ? __ldcs(src + (t0 + j) * CW + w) : 0ull;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kPItems; ++u) {
+            const int j = u * kPThreads + tid;
+            if (j < tn) load_carry<CW>(a, uint64_t(t0 + j), cr.p[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPItems; ++u) {
+        const int j = u * kPThreads + tid;
+        k[u] = j < tn ? pack_as<decltype(packed)::value>(xform(k[u], a.desc), sh, shl) : 0ull;
         if constexpr (PK) k[u] |= uint64_t(uint32_t(t0 + j));
         else v[u] = uint32_t(t0 + j);
       }
     };
     uint64_t k[kPItems];
     uint32_t v[kPItems];
-    if (lo < hi) load(k, v, lo);
+    Carry<CW> cr;
+    if (lo < hi) load(k, v, cr, lo);
     if (tid < 256) s.hist[tid] = 0;
     __syncthreads();
     for (int64_t t0 = lo; t0 < hi; t0 += kPTile) {
       const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
       const int64_t nt = t0 + kPTile;
-      ptile_scatter<7 * kBits, PK>(k, v, tn, s, a.keys_b, a.vals_b, reserve,
-                                   [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
-                                     if (nt < hi) load(kk, vv, nt);
-                                   });
+      ptile_scatter<7 * kBits, PK, CW>(k, v, cr, tn, s, a.keys_b, a.vals_b, a.pay_b, reserve,
+                                       [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
+                                         if (nt < hi) load(kk, vv, cc, nt);
+                                       });
     }
   };
   using F = std::false_type;
   using T = std::true_type;
   const bool pk = packed_rows(sh, a);
+  if constexpr (CW > 0) {  // the bucket join: packed rows always (its plan checks the code)
+    if (pack_mode(sh) == 1) tiles(std::integral_constant<int, 1>{}, T{});
+    else tiles(std::integral_constant<int, 2>{}, T{});
+    return;
+  }
   switch (pack_mode(sh)) {
     case 0: tiles(std::integral_constant<int, 0>{}, F{}); break;
     case 1:
@@ -1137,34 +1234,43 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   }
 }
 
-template <bool PK>
+template <bool PK, int CW>
 __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile& s);
 
+template <int CW = 0>
 __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_kernel(SortArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const PTile s = ptile(sm);
+  const PTile s = ptile<CW>(sm);
   const int tid = threadIdx.x;
   pdl_wait();  // the digit-7 pass
   pdl_launch_dependents();
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[3] = globaltimer();
   if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);  // the key pack code
   if (fallback_flag(a)) return;  // LSD fallback (the barrier also publishes scratch[50])
-  if (packed_rows(s.scratch[50], a)) sub_scatter_tiles<true>(a, s);
-  else sub_scatter_tiles<false>(a, s);
+  if constexpr (CW > 0) {
+    sub_scatter_tiles<true, CW>(a, s);
+  } else {
+    if (packed_rows(s.scratch[50], a)) sub_scatter_tiles<true, 0>(a, s);
+    else sub_scatter_tiles<false, 0>(a, s);
+  }
 }
 
-template <bool PK>
+template <bool PK, int CW>
 __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile& s) {
   const int tid = threadIdx.x;
   const uint32_t n_items = __ldcg(a.meta);
   uint32_t* claim = s.scratch + 40;  // [2] claimed tile ids, by parity
-  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], const uint4& item) {
+  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cr, const uint4& item) {
     const int tn = int(item.z - item.y);
 #pragma unroll
     for (int u = 0; u < kPItems; ++u) {
       const int j = u * kPThreads + tid;
       k[u] = j < tn ? __ldcs(a.keys_b + item.y + j) : 0ull;
       if constexpr (!PK) v[u] = j < tn ? __ldcs(a.vals_b + item.y + j) : 0u;
+      if constexpr (CW > 0) {
+#pragma unroll
+        for (int w = 0; w < CW; ++w) cr.p[u][w] = j < tn ? __ldcs(a.pay_b + (size_t(item.y) + j) * CW + w) : 0ull;
+      }
     }
   };
   if (tid == 0) claim[0] = atomicAdd(a.flags + 3, 1u);
@@ -1174,7 +1280,8 @@ __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile
   uint4 item = it < n_items ? __ldcg(a.items + it) : make_uint4(0, 0, 0, 0);
   uint64_t k[kPItems];
   uint32_t v[kPItems];
-  if (it < n_items) load(k, v, item);
+  Carry<CW> cr;
+  if (it < n_items) load(k, v, cr, item);
   while (it < n_items) {
     if (tid == 0) claim[par] = atomicAdd(a.flags + 3, 1u);  // the next tile, read after the staging barrier
     const uint32_t g = item.x;
@@ -1183,14 +1290,14 @@ __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile
     auto reserve = [&](uint32_t d, uint32_t c) {
       return __ldcg(a.sub_off + g * 256 + d) + atomicAdd(a.cur16 + g * 256 + d, c);
     };
-    ptile_scatter<6 * kBits, PK>(k, v, int(item.z - item.y), s, a.keys_a, a.vals_a, reserve,
-                             [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems]) {
-                               nit = claim[par];
-                               if (nit < n_items) {
-                                 nitem = __ldcg(a.items + nit);
-                                 load(kk, vv, nitem);
-                               }
-                             });
+    ptile_scatter<6 * kBits, PK, CW>(k, v, cr, int(item.z - item.y), s, a.keys_a, a.vals_a, a.pay_a, reserve,
+                                     [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
+                                       nit = claim[par];
+                                       if (nit < n_items) {
+                                         nitem = __ldcg(a.items + nit);
+                                         load(kk, vv, cc, nitem);
+                                       }
+                                     });
     it = nit;
     item = nitem;
     par ^= 1;
@@ -1896,9 +2003,9 @@ static bool scatter_kernels_ready() {
            const bool ok =
                cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHistSmem)) ==
                    cudaSuccess &&
-               cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
+               cudaFuncSetAttribute(top_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
                    cudaSuccess &&
-               cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
+               cudaFuncSetAttribute(sub_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
                    cudaSuccess &&
                cudaFuncSetAttribute(local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kLocalSmemBytes)) == cudaSuccess;
@@ -1906,8 +2013,8 @@ static bool scatter_kernels_ready() {
 #ifdef RL_CARVEOUT_MAX
            if (ok) {  // one L1/shared split for every kernel of the sort: no SM reconfiguration between them
              cudaFuncSetAttribute(sub_hist_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-             cudaFuncSetAttribute(top_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-             cudaFuncSetAttribute(sub_scatter_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+             cudaFuncSetAttribute(top_scatter_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+             cudaFuncSetAttribute(sub_scatter_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
              cudaFuncSetAttribute(local_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
              cudaFuncSetAttribute(sort_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
            }
@@ -1921,7 +2028,7 @@ static int pass_ctas_per_sm() {
   static int cache[kMaxDevices] = {};
   return per_device(cache, [] {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, top_scatter_kernel, kPThreads, kPSmem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, top_scatter_kernel<0>, kPThreads, kPSmem) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
       per_sm = 1;
@@ -2054,9 +2161,9 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     };
     sub_hist_kernel<<<chunks, kScatThreads, kHistSmem, stream>>>(a);
     chk("sub_hist");
-    if ((e = launch_dep(top_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
+    if ((e = launch_dep(top_scatter_kernel<0>, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
     chk("top_scatter");
-    if ((e = launch_dep(sub_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
+    if ((e = launch_dep(sub_scatter_kernel<0>, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
     chk("sub_scatter");
     if ((e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes)) != cudaSuccess) return rl_cuda_status(e);
     chk("local");
@@ -2342,11 +2449,30 @@ __global__ void __launch_bounds__(1024) bj_pack_kernel(const long long* lk, int6
   }
 }
 
-size_t bj_side_workspace_bytes(int64_t n) {
+size_t bj_side_workspace_bytes(int64_t n, int words) {
   CarveSize c;
   carve_all(c, std::max<int64_t>(n, 1), [](CarveSize& c, size_t k) { c.take<uint32_t>(k); return (uint32_t*)nullptr; },
             [](CarveSize& c, size_t k) { c.take<uint64_t>(k); return (uint64_t*)nullptr; }, nullptr, true);
+  if (words > 0) {  // carried payload, ping-pong
+    c.take<uint64_t>(size_t(std::max<int64_t>(n, 1)) * words);
+    c.take<uint64_t>(size_t(std::max<int64_t>(n, 1)) * words);
+  }
   return c.used + 256;
+}
+
+// The counting-pass instances that carry CW payload words: their shared
+// memory opt-in, once per device.
+template <int CW>
+static bool carry_kernels_ready() {
+  static int ready[kMaxDevices] = {};
+  return per_device(ready, [] {
+           const bool ok = cudaFuncSetAttribute(top_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(psmem_bytes(CW))) == cudaSuccess &&
+                           cudaFuncSetAttribute(sub_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(psmem_bytes(CW))) == cudaSuccess;
+           if (!ok) cudaGetLastError();
+           return ok ? 1 : -1;
+         }) > 0;
 }
 
 static SortArgs bj_args(const int64_t* keys, int64_t n, const int64_t* k0_src, const Layout& L) {
@@ -2387,21 +2513,34 @@ static SortArgs bj_args(const int64_t* keys, int64_t n, const int64_t* k0_src, c
 // the joint packing; sub_off[65536 + 1] holds the sub-bucket starts; flags[0]
 // != 0 on either side means "fall back" (a sub-bucket above kLocalCap, keys not
 // packable into 32 bits, a wrapped chunk counter). Nothing is synchronised.
-int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, void* ws_l, size_t ws_l_bytes,
-                 void* ws_r, size_t ws_r_bytes, cudaStream_t stream, BjSide* left, BjSide* right) {
+int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, const BjCarry& lcarry,
+                 const BjCarry& rcarry, void* ws_l, size_t ws_l_bytes, void* ws_r, size_t ws_r_bytes,
+                 cudaStream_t stream, BjSide* left, BjSide* right) {
   if (nl < 1 || nr < 1 || !lkeys || !rkeys || !left || !right) return RL_ERR_BAD_ARG;
   if (nl > RL_MAX_ROWS || nr > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
   if ((reinterpret_cast<uintptr_t>(lkeys) | reinterpret_cast<uintptr_t>(rkeys)) & 15) return RL_ERR_BAD_ARG;
   if ((reinterpret_cast<uintptr_t>(ws_l) | reinterpret_cast<uintptr_t>(ws_r)) % 256 != 0) return RL_ERR_WORKSPACE;
-  if (!scatter_kernels_ready()) return rl_cuda_status(cudaErrorInvalidConfiguration);
+  if (!scatter_kernels_ready() || !carry_kernels_ready<1>() || !carry_kernels_ready<2>())
+    return rl_cuda_status(cudaErrorInvalidConfiguration);
   Layout L[2];
+  uint64_t* pays[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   const int64_t ns[2] = {nl, nr};
+  const BjCarry* carries[2] = {&lcarry, &rcarry};
   void* wss[2] = {ws_l, ws_r};
   const size_t wsb[2] = {ws_l_bytes, ws_r_bytes};
   for (int i = 0; i < 2; ++i) {
+    const BjCarry& cy = *carries[i];
+    if (cy.words < 0 || cy.words > kBjMaxCarryWords || cy.n < 0 || cy.n > kBjMaxCarryCols || (cy.n > 0) != (cy.words > 0))
+      return RL_ERR_BAD_ARG;
+    for (int c = 0; c < cy.n; ++c)
+      if (!cy.src[c] || cy.width[c] <= 0 || cy.off[c] < 0 || cy.off[c] + cy.width[c] > 8 * cy.words) return RL_ERR_BAD_ARG;
     Carve c{static_cast<char*>(wss[i]), wsb[i]};
     carve_all(c, ns[i], [](Carve& c, size_t k) { return c.take<uint32_t>(k); },
               [](Carve& c, size_t k) { return c.take<uint64_t>(k); }, &L[i], true);
+    if (cy.words > 0) {
+      pays[i][0] = c.take<uint64_t>(size_t(ns[i]) * cy.words);
+      pays[i][1] = c.take<uint64_t>(size_t(ns[i]) * cy.words);
+    }
     if (!c.ok) return RL_ERR_WORKSPACE;
     cudaError_t e = cudaMemsetAsync(L[i].hist, 0, L[i].head_bytes, stream);
     if (e != cudaSuccess) return rl_cuda_status(e);
@@ -2415,11 +2554,31 @@ int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t
     SortArgs a = bj_args(keys[i], ns[i], lkeys, L[i]);
     a.chunks = int(std::min<int64_t>(std::min(device_sm_count(), kMaxChunks),
                                      std::max<int64_t>(32, (ns[i] + kChunkMinRows - 1) / kChunkMinRows)));
+    const BjCarry& cy = *carries[i];
+    a.carry_n = cy.n;
+    for (int c = 0; c < cy.n; ++c) {
+      a.carry_src[c] = cy.src[c];
+      a.carry_width[c] = cy.width[c];
+      a.carry_off[c] = cy.off[c];
+    }
+    a.pay_a = pays[i][0];
+    a.pay_b = pays[i][1];
     const int pgrid = device_sm_count() * pass_ctas_per_sm();
     sub_hist_kernel<<<a.chunks, kScatThreads, kHistSmem, stream>>>(a);
-    top_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
-    sub_scatter_kernel<<<pgrid, kPThreads, kPSmem, stream>>>(a);
+    const size_t sm = psmem_bytes(cy.words);
+    if (cy.words == 0) {
+      top_scatter_kernel<0><<<pgrid, kPThreads, sm, stream>>>(a);
+      sub_scatter_kernel<0><<<pgrid, kPThreads, sm, stream>>>(a);
+    } else if (cy.words == 1) {
+      top_scatter_kernel<1><<<pgrid, kPThreads, sm, stream>>>(a);
+      sub_scatter_kernel<1><<<pgrid, kPThreads, sm, stream>>>(a);
+    } else {
+      top_scatter_kernel<2><<<pgrid, kPThreads, sm, stream>>>(a);
+      sub_scatter_kernel<2><<<pgrid, kPThreads, sm, stream>>>(a);
+    }
     launched += 3;
+    outs[i]->pay = pays[i][0];  // the digit-6 pass leaves the payload in pay_a, beside keys_a
+    outs[i]->words = cy.words;
     outs[i]->rows = L[i].keys_a;
     outs[i]->sub_off = L[i].sub_off;
     outs[i]->flags = L[i].flags;

@@ -394,7 +394,8 @@ def multiset_digest(columns: Sequence[torch.Tensor]) -> int:
     return (hi << 64) | lo
 
 
-BJ_MIN_ROWS = 1 << 16  # smaller joins: the sort-based plan (fewer launches)
+BJ_MIN_ROWS = 4 << 20  # smaller joins: the sort-based plan (fewer launches; measured crossover ~4M rows a side)
+BJ_CARRY_MIN_RATIO = 0.5  # carry payloads when the expected pairs reach half the larger side (measured break-even)
 BJ_MAX_ROWS = (1 << 16) * 2560 * 9 // 10  # above ~this some sub-bucket surely exceeds its 2560-row cap
 
 
@@ -417,15 +418,29 @@ class BucketJoinPlan:
 
     kind = "bucket"
 
-    def __init__(self, left_keys: torch.Tensor, right_keys: torch.Tensor):
+    def __init__(self, left_keys: torch.Tensor, right_keys: torch.Tensor, left_carry: Sequence[torch.Tensor] = (),
+                 right_carry: Sequence[torch.Tensor] = ()):
+        """left_carry / right_carry: the columns whose output copies expand
+        will gather (the join's non-key columns) — carried with the rows
+        through the partition passes (<= 16 bytes a row a side) so that expand
+        reads them beside the row instead of at random row ids."""
         lib = C.load()
         lk, rk = aligned16(left_keys), aligned16(right_keys)
         self._keys = (lk, rk)  # the plan reads the left keys again in expand (constant key bits)
+        import os
+
+        if os.environ.get("RL_BJ_NO_CARRY", "") not in ("", "0"):  # A/B: gather every column by row id
+            left_carry, right_carry = (), ()
+        self._carry = (list(left_carry), list(right_carry))  # kept alive: expand matches their pointers
         nl, nr = lk.numel(), rk.numel()
-        self.ws = workspace(lib.rl_bjoin_workspace_bytes(nl, nr), lk.device)
+        arrs = [C.columns_array((c.data_ptr(), None, c.element_size() * (c.shape[1] if c.dim() > 1 else 1),
+                                 C.RL_SIDE_LEFT) for c in side) for side in self._carry]
+        words = [lib.rl_bjoin_carry_words(arr, n) if n else 0 for arr, n in arrs]
+        self.ws = workspace(lib.rl_bjoin_workspace_bytes(nl, nr, max(words[0], 0), max(words[1], 0)), lk.device)
         self.plan = C.RlBjoinPlan()
-        C.check(lib.rl_bjoin_plan_build(_ptr(lk), nl, _ptr(rk), nr, _ptr(self.ws), self.ws.numel(),
-                                        ctypes.byref(self.plan), stream_handle()), "rl_bjoin_plan_build")
+        C.check(lib.rl_bjoin_plan_build(_ptr(lk), nl, _ptr(rk), nr, arrs[0][0], arrs[0][1], arrs[1][0], arrs[1][1],
+                                        _ptr(self.ws), self.ws.numel(), ctypes.byref(self.plan), stream_handle()),
+                "rl_bjoin_plan_build")
         self.n_left, self.n_right = nl, nr
         host = torch.empty(2, dtype=torch.int64, pin_memory=True)
         off = self.plan.scalars - self.ws.data_ptr()
@@ -448,13 +463,31 @@ class BucketJoinPlan:
                                                 stream_handle()), "rl_bjoin_pair_checksum")
 
 
-def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor):
+def expected_pairs_ratio(left_keys: torch.Tensor, right_keys: torch.Tensor, samples: int = 2048) -> float:
+    """Pairs per row of the larger side a join of uniform keys would produce:
+    nl * nr / (key range) / max(nl, nr), the range taken from strided samples
+    of both sides (one small reduction, one host sync). Carrying payload
+    through the bucket join's passes costs ~2 passes x 2 x width per input
+    row and saves ~2 random sector reads per output pair: it pays when pairs
+    are about as many as rows (cfg5), not for selective joins (cfg4: ~0.02)."""
+    nl, nr = left_keys.numel(), right_keys.numel()
+    s = torch.cat([left_keys[:: max(1, nl // samples)], right_keys[:: max(1, nr // samples)]])
+    lo, hi = (int(v) for v in torch.aminmax(s))
+    rng = max(1, hi - lo + 1)
+    return nl * nr / rng / max(nl, nr, 1)
+
+
+def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor, left_carry: Sequence[torch.Tensor] = (),
+              right_carry: Sequence[torch.Tensor] = ()):
     """The join plan for two int64 key columns on the device: the bucket join
-    when it applies (<= 32 varying key bits, no oversized sub-bucket), else
-    the sort-based plan (both key axes + alignment). One host sync either way
-    (plus one when the bucket join declines)."""
+    when it applies (<= 32 varying key bits, no oversized sub-bucket; the
+    carry columns ride with the rows), else the sort-based plan (both key
+    axes + alignment). One host sync either way (plus one when the bucket
+    join declines)."""
     if _bjoin_allowed(left_keys.numel(), right_keys.numel()):
-        bp = BucketJoinPlan(left_keys, right_keys)
+        if (left_carry or right_carry) and expected_pairs_ratio(left_keys, right_keys) < BJ_CARRY_MIN_RATIO:
+            left_carry, right_carry = (), ()  # selective join: gather the few output rows by row id instead
+        bp = BucketJoinPlan(left_keys, right_keys, left_carry, right_carry)
         if bp.applies:
             return bp
         del bp

@@ -93,12 +93,13 @@ def _width(col: torch.Tensor) -> int:
 JoinPlan = engine.JoinPlanDev
 
 
-def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor):
+def plan_join(left_keys: torch.Tensor, right_keys: torch.Tensor, left_carry=(), right_carry=()):
     """Everything a join needs before its output size is known, on the
-    device: the bucket join (csrc/bucket_join.cu) when the keys allow it,
-    else to_tensor x2 + key_axis_align + sizing in one C call over one
-    workspace (rl_join_plan_build). One host sync (the totals)."""
-    return engine.plan_join(left_keys, right_keys)
+    device: the bucket join (csrc/bucket_join.cu) when the keys allow it
+    (carrying the given payload columns with the rows), else to_tensor x2 +
+    key_axis_align + sizing in one C call over one workspace
+    (rl_join_plan_build). One host sync (the totals)."""
+    return engine.plan_join(left_keys, right_keys, left_carry, right_carry)
 
 
 def join(left: DeviceRelation, right: DeviceRelation, key: str,
@@ -108,7 +109,9 @@ def join(left: DeviceRelation, right: DeviceRelation, key: str,
     non-key attributes (join_output_schema)."""
     out_schema = R.join_output_schema(left.schema, right.schema, key, schema_cls=type(left.schema))
     lk, rk = left.schema.index(key), right.schema.index(key)
-    plan = plan_join(left.columns[lk], right.columns[rk])
+    plan = plan_join(left.columns[lk], right.columns[rk],
+                     [c for j, c in enumerate(left.columns) if j != lk],
+                     [c for j, c in enumerate(right.columns) if j != rk])
     if plan.total > max_output_rows:
         raise OutputTooLarge(f"join would produce {plan.total} rows (cap {max_output_rows})")
     cols = join_out_columns(left.columns, lk, right.columns, rk, plan.total)

@@ -123,7 +123,7 @@ def test_chunked_slices_and_columns():
 
 def test_pipeline_join_uses_the_bucket_plan_and_equals_the_sort_plan(monkeypatch):
     rng = np.random.default_rng(10)
-    n = 1_000_000
+    n = 5_000_000  # above the bucket join's 4M-row threshold
     lk, rk = rng.integers(0, n, n), rng.integers(0, n, n)
     plan = pipeline.plan_join(_dev(lk), _dev(rk))
     assert plan.kind == "bucket"
@@ -140,3 +140,47 @@ def test_small_inputs_forced(monkeypatch):
     rng = np.random.default_rng(11)
     for nl, nr, dom in [(1, 1, 1), (1, 50, 3), (7, 3, 2), (1000, 800, 100), (5000, 1, 10)]:
         _check(rng.integers(0, dom, nl), rng.integers(0, dom, nr))
+
+
+@pytest.mark.parametrize("shape", ["int64", "bytes16", "mixed3", "too_wide"])
+def test_carried_payload_columns(shape):
+    """Payload columns carried with the rows through the partition passes
+    (<= 16 bytes a side, natural alignment) come out exactly as the gathered
+    ones; wider payloads fall back to gathering by row id."""
+    rng = np.random.default_rng(20 + len(shape))
+    n = 600_000
+    lk, rk = rng.integers(0, 300_000, n), rng.integers(0, 300_000, n - 999)
+    if shape == "int64":
+        lc = [rng.integers(-(2**62), 2**62, n)]
+        rc = [rng.integers(-(2**62), 2**62, n - 999)]
+    elif shape == "bytes16":
+        lc = [rng.integers(0, 256, (n, 16), dtype=np.uint8)]
+        rc = [rng.integers(0, 256, (n - 999, 16), dtype=np.uint8)]
+    elif shape == "mixed3":
+        lc = [rng.integers(0, 256, (n, 3), dtype=np.uint8), rng.integers(-5, 5, n),
+              rng.integers(0, 256, (n, 4), dtype=np.uint8)]
+        rc = [rng.integers(0, 256, (n - 999, 1), dtype=np.uint8)]
+    else:
+        lc = [rng.integers(0, 256, (n, 24), dtype=np.uint8)]
+        rc = [rng.integers(0, 256, (n - 999, 12), dtype=np.uint8), rng.integers(0, 9, n - 999)]
+    ldev, rdev = [_dev(c) for c in lc], [_dev(c) for c in rc]
+    bp = engine.BucketJoinPlan(_dev(lk), _dev(rk), ldev, rdev)
+    assert bp.applies
+    wl, wr = O.join_pairs(lk, rk)
+    assert bp.total == len(wl)
+    w = lambda c: c.element_size() * (c.shape[1] if c.dim() > 1 else 1)  # noqa: E731
+    cols = [engine.OutColumn(None, torch.empty(bp.total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_KEY)]
+    cols += [engine.OutColumn(c, torch.empty((bp.total,) + tuple(c.shape[1:]), dtype=c.dtype, device="cuda"), w(c),
+                              C.RL_SIDE_LEFT) for c in ldev]
+    cols += [engine.OutColumn(c, torch.empty((bp.total,) + tuple(c.shape[1:]), dtype=c.dtype, device="cuda"), w(c),
+                              C.RL_SIDE_RIGHT) for c in rdev]
+    half = bp.total // 3
+    bp.expand(0, half, [engine.OutColumn(c.src, c.dst[:half], c.width, c.side) for c in cols])
+    bp.expand(half, bp.total, [engine.OutColumn(c.src, c.dst[half:], c.width, c.side) for c in cols])
+    assert (cols[0].dst.cpu().numpy() == lk[wl]).all()
+    for c, h in zip(cols[1:1 + len(lc)], lc):
+        assert (c.dst.cpu().numpy() == h[wl]).all()
+    for c, h in zip(cols[1 + len(lc):], rc):
+        assert (c.dst.cpu().numpy() == h[wr]).all()
+    expect_words = {"int64": 1, "bytes16": 2, "mixed3": 2, "too_wide": 0}[shape]
+    assert bp.plan.words_left == expect_words

@@ -395,8 +395,8 @@ def sort_roofline(n, active, st, sort_ms, hist_ms, step_ms_total):
 def run_ours(args):
     # the driver parses rank 0's stdout as ONE JSON line: NCCL's INFO log (communicator
     # lines, NVLS / P2P transport choice) goes to stderr, not stdout
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    os.environ["NCCL_DEBUG"] = os.environ.get("RL_NCCL_DEBUG", "INFO")
+    os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
     import torch
     import torch.distributed as dist
 
@@ -590,6 +590,7 @@ def run_ours(args):
     if not args.no_join:
         line["join_cfg1"] = join_cfg1(args, dev, rank, world)
         line["join_scaling"] = join_scaling(args, dev, rank, world)
+        line["join_cfg4"] = join_cfg4(args, dev, rank, world)
     if args.extras and world == 1:
         line["other_configs"] = extras(args, dev)
 
@@ -755,6 +756,7 @@ def run_distributed(args, dev, rank, world, lib, keys_h, pay_h, keys_d, pay_d, f
     }
     if not args.no_join:
         line["join_scaling"] = join_scaling(args, dev, rank, world)
+        line["join_cfg4"] = join_cfg4(args, dev, rank, world)
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -949,6 +951,100 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
                        "achieved_gbs": round(2 * n * (world - 1) / world * 24 / (med / 1e3) / 1e9, 1),
                        "peak_gbs": 900.0, "unit": "GB/s",
                        "frac": round(2 * n * (world - 1) / world * 24 / (med / 1e3) / 1e9 / 900.0, 4)}}
+
+
+def join_cfg4(args, dev, rank, world, total_rows=10**8):
+    """BASELINE cfg4 on N GPUs: a 2-attribute key (int32 a, b uniform in
+    [0, 2^16)) packed to int64, |R| = |S| = 1e8 rows in total with a 16-byte
+    payload, split over the ranks (strong scaling): N = 1 the device join,
+    N > 1 dist.distributed_join (hash partition on the key, the exchange, the
+    local join). Inputs generated on the device (torch, seeded per rank).
+    Gate: torch invariants over the keys with their low 6 bits zero (a dense
+    2^26-id sample of the key space; aggregates all-reduced over the ranks)
+    on (key, first payload word of each side), and the key order per shard."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_21237_b200 import checks, pipeline
+    from paper_2602_21237_b200 import dist as D
+    from paper_2602_21237_b200 import records as R
+
+    n = total_rows // world
+    base = rank * n
+    g = torch.Generator(device=dev)
+    g.manual_seed(4000 + rank)
+
+    def side():
+        a = torch.randint(0, 1 << 16, (n,), generator=g, device=dev)
+        b = torch.randint(0, 1 << 16, (n,), generator=g, device=dev)
+        return [(a << 32) | b, torch.randint(0, 256, (n, 16), generator=g, device=dev, dtype=torch.uint8)]
+
+    cl, cr = side(), side()
+    if world == 1:
+        schema = R.Schema((("key", R.Int64()), ("payload", R.Bytes(16))))
+        dl, dr = pipeline.DeviceRelation(schema, cl), pipeline.DeviceRelation(schema, cr)
+
+        def run():
+            return pipeline.join(dl, dr, "key").columns
+    else:
+        def run():
+            return D.distributed_join(cl, 0, base, cr, 0, base).columns
+
+    first8 = lambda c: c.view(torch.int64)[:, 0].contiguous()  # noqa: E731
+    out = run()
+    rows = torch.tensor([out[0].numel()], dtype=torch.int64, device=dev)
+    got = checks.sampled_join_observed(out[0], first8(out[1]), first8(out[2]))
+    ordered = checks.sort_ok(out[0])
+    del out
+    torch.cuda.empty_cache()
+    agg = checks.sampled_join_aggregates(cl[0], first8(cl[1]), cr[0], first8(cr[1]))
+    obs = torch.tensor([got[k] for k in checks.FIELDS], dtype=torch.int64, device=dev)
+    if world > 1:
+        for t in agg:
+            dist.all_reduce(t)
+        dist.all_reduce(obs)
+        dist.all_reduce(rows)
+    want = checks.expectations_from_aggregates(*agg)
+    del agg
+    torch.cuda.empty_cache()
+    if dict(zip(checks.FIELDS, obs.tolist())) != want or not ordered:
+        raise SystemExit("cfg4 join failed its self-check; refusing to report a number")
+    total = int(rows.item())
+    run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = []
+    for _ in range(min(args.steps, 5)):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        run()
+        b_.record()
+        b_.synchronize()
+        ms.append(a_.elapsed_time(b_))
+    t = torch.tensor([statistics.median(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    med = float(t.item())
+    del cl, cr
+    torch.cuda.empty_cache()
+    alg = 2 * total_rows * 24 + total * 40  # SURVEY §8(d): 4.9 GB at 1e8
+    peak, peak_src = measured_peak_hbm()
+    achieved = alg / world / (med / 1e3) / 1e9
+    sent = 2 * n * (world - 1) / world * 32  # key 8 + payload 16 + int64 global id 8, both sides
+    return {"workload": "cfg4: composite key (a << 32) | b, a, b uniform int32 in [0, 2^16), 16-byte payload, "
+                        f"{total_rows:.0e} rows per side in total, strong scaling (device-generated, seeded per rank)",
+            "rows_per_side_per_gpu": n, "matches_total": total,
+            "gate": "passed: sampled torch invariants (keys with 6 low zero bits), all-reduced; key order",
+            "path": "device join" if world == 1 else "distributed_join: hash partition + peer-memory push + local join",
+            "ms_per_step_p50_max_over_ranks": round(med, 3),
+            "mrows_per_s": round(2 * total_rows / (med / 1e3) / 1e6, 1), "scaling": "strong",
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                         "alg_bytes_per_step": int(alg),
+                         "alg_bytes_formula": "2 x rows x (8 B key + 16 B payload) + matches x 40 B (SURVEY §8(d)); per GPU"},
+            "nvlink": {"bytes_per_rank_per_step": int(sent), "achieved_gbs": round(sent / (med / 1e3) / 1e9, 1),
+                       "peak_gbs": 900.0, "unit": "GB/s", "frac": round(sent / (med / 1e3) / 1e9 / 900.0, 4)}}
 
 
 def extras(args, dev):

@@ -116,3 +116,28 @@ def multiset_sums(cols) -> tuple:
     if len(cols) > 1:
         out.append(int((_f(cols[0]) * _g(cols[1])).sum()))
     return tuple(out)
+
+
+def sampled_join_aggregates(lk, lpay, rk, rpay, sample_bits: int = 6, id_bits: int = 26):
+    """join_aggregates over the keys whose low `sample_bits` bits are zero
+    (1 in 2^sample_bits of a uniform key space), keyed by a dense id: for
+    composite keys (a << 32) | b with a, b < 2^16 (BASELINE cfg4) the id is
+    (a << (16 - sample_bits)) | (b >> sample_bits). Bounded memory whatever
+    the key space; the aggregates still add up over row shards."""
+    def ids(k):
+        a, b = k >> 32, k & 0xFFFF
+        keep = (k & ((1 << sample_bits) - 1)) == 0
+        return keep, (a << (16 - sample_bits)) | (b >> sample_bits)
+
+    dom = 1 << id_bits
+    kl, il = ids(lk)
+    kr, ir = ids(rk)
+    return join_aggregates(il[kl], lpay[kl], ir[kr], rpay[kr], dom)
+
+
+def sampled_join_observed(out_key, out_lpay, out_rpay, sample_bits: int = 6) -> dict:
+    keep = (out_key & ((1 << sample_bits) - 1)) == 0
+    k = out_key[keep]
+    a, b = k >> 32, k & 0xFFFF
+    dense = (a << (16 - sample_bits)) | (b >> sample_bits)
+    return join_observed(dense, out_lpay[keep], out_rpay[keep])

@@ -115,12 +115,16 @@ class GpuOps:
     # fused forms (one launch for every column) used when an Ops object has them
     def local_join(self, lcols, lkey: int, rcols, rkey: int, lgids: torch.Tensor, rgids: torch.Tensor):
         """The local equi-join with every output column and both global row-id
-        columns written by ONE expansion launch (rl_join_plan_build + rl_join_expand)."""
+        columns written by ONE expansion launch: the bucket join when it
+        applies (payload and global ids carried with the rows), else the
+        sort-based plan (rl_join_plan_build + rl_join_expand)."""
         from . import _capi as C
         from . import engine
         from .pipeline import join_out_columns
 
-        plan = engine.JoinPlanDev(lcols[lkey], rcols[rkey])
+        plan = engine.plan_join(lcols[lkey], rcols[rkey],
+                                [c for j, c in enumerate(lcols) if j != lkey] + [lgids],
+                                [c for j, c in enumerate(rcols) if j != rkey] + [rgids])
         total = plan.total
         cols = join_out_columns(list(lcols), lkey, list(rcols), rkey, total)
         ids = [engine.OutColumn(lgids, torch.empty(total, dtype=torch.int64, device=lgids.device), 8, C.RL_SIDE_LEFT),

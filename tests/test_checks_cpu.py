@@ -58,3 +58,26 @@ def test_sort_checks():
     permd = torch.from_numpy(O.stable_axis_order(keys.numpy(), True))
     assert checks.sort_ok(keys[permd], rid[permd], descending=True)
     assert not checks.sort_ok(keys[permd], rid[permd])
+
+
+def test_sampled_composite_key_invariants_add_up_over_shards():
+    """bench.py's cfg4 gate: the invariants over the sampled composite keys
+    agree with the oracle's join output, and the per-shard aggregates summed
+    (the all-reduce of a multi-GPU run) equal the whole-relation ones."""
+    rng = np.random.default_rng(7)
+    n = 60_000
+    mk = lambda: (rng.integers(0, 1 << 6, n).astype(np.int64) << np.int64(32)) | (rng.integers(0, 1 << 7, n) << 6)  # noqa
+    lk, rk = mk(), mk()
+    lk[::5] += 1  # keys with nonzero low bits: outside the sample (they still match each other)
+    rk[::3] += 1
+    lp, rp = rng.integers(-(2**40), 2**40, n), rng.integers(-(2**40), 2**40, n)
+    key, lpay, rpay = O.join_columns([lk, lp], 0, [rk, rp], 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+    agg = checks.sampled_join_aggregates(t(lk), t(lp), t(rk), t(rp))
+    want = checks.expectations_from_aggregates(*agg)
+    assert want == checks.sampled_join_observed(t(key), t(lpay), t(rpay))
+    assert 0 < want["matches"] < len(key)
+    h = n // 2
+    a1 = checks.sampled_join_aggregates(t(lk[:h]), t(lp[:h]), t(rk[:h]), t(rp[:h]))
+    a2 = checks.sampled_join_aggregates(t(lk[h:]), t(lp[h:]), t(rk[h:]), t(rp[h:]))
+    assert checks.expectations_from_aggregates(*[x + y for x, y in zip(a1, a2)]) == want

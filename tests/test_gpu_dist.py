@@ -30,8 +30,14 @@ def nccl_world1():
     dist.destroy_process_group()
 
 
-def test_distributed_join_on_device(nccl_world1):
+@pytest.mark.parametrize("plan", ["sort", "bucket"])
+def test_distributed_join_on_device(nccl_world1, plan, monkeypatch):
+    """The local join after the exchange through either plan: the bucket join
+    (forced at this size; left payload + global id too wide to carry, right
+    payload + global id carried) or the sort-based plan."""
     from paper_2602_21237_b200 import dist as D
+
+    monkeypatch.setenv("RL_FORCE_BJOIN" if plan == "bucket" else "RL_NO_BJOIN", "1")
 
     rng = np.random.default_rng(3)
     lk = rng.integers(0, 5000, 40_000).astype(np.int64)

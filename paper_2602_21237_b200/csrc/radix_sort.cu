@@ -217,7 +217,15 @@ struct SortArgs {
   int carry_off[4];          // byte offset in the row's payload words
   uint64_t* pay_a;           // [n * CW] parallel to keys_a
   uint64_t* pay_b;           // [n * CW] parallel to keys_b
+  // three-level scatter (n above ~65536 x kLocalCap): digit 5 inside every
+  // (d7, d6) sub-bucket, the local phase over 2^24 sub-sub-buckets
+  int levels;                // 2 or 3
+  uint32_t* sub3_off;        // [kSub3 + 1] sub-sub-bucket starts
+  uint32_t* cur24;           // [kSub3] rows placed per sub-sub-bucket so far (zeroed)
+  uint32_t* tile3;           // [kSubBuckets + 1] first level-3 tile of every sub-bucket (prefix)
+  uint32_t* tmap;            // [level-3 tiles] the sub-bucket of every tile
 };
+constexpr int kSub3 = 1 << 24;  // (d7, d6, d5) sub-sub-buckets
 
 // Global digit count (pass p, digit d): the sum of the histogram replicas.
 __device__ __forceinline__ uint32_t ghist_at(const SortArgs& a, int p, int d) {
@@ -286,6 +294,10 @@ constexpr size_t kLocMisc = kLocBig + size_t(kBigList) * 4;
 // [72..103] run ends (x2), [112..] run descriptors
 constexpr size_t kLocBars = kLocMisc + 128 * 4;
 constexpr size_t kLocalSmemBytes = kLocBars + 2 * 8;
+// local_kernel only (not the cooperative kernel's budget): the three-level
+// path's group offsets and runs, [2][257] + [2][256]
+constexpr size_t kLocGrp = (kLocalSmemBytes + 15) / 16 * 16;
+constexpr size_t kLocalKernelSmem = kLocGrp + (2 * 257 + 2 * 256) * 4;
 constexpr size_t kSmemBytes = std::max(kPassSmemBytes + size_t(kPasses) * kBins * 4 + 128, kLocalSmemBytes);
 
 struct PassState {  // per-CTA mbarrier phase parities, carried across passes
@@ -1095,7 +1107,8 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     const uint64_t vary = __ldcg(reinterpret_cast<const unsigned long long*>(a.flags + 4));
     int na = 0;
     for (int q = 0; q < kPasses; ++q) na += ((vary >> (q * kBits)) & (kBins - 1)) ? 1 : 0;
-    const bool too_big = __syncthreads_or(tid < 256 && uint64_t(t7) > uint64_t(kBins) * kLocalCap) != 0;
+    const uint64_t cap7 = uint64_t(a.levels == 3 ? kSubBuckets : kBins) * kLocalCap;
+    const bool too_big = __syncthreads_or(tid < 256 && uint64_t(t7) > cap7) != 0;
     if (too_big || (na < 4 && !a.bj)) {
       if (blockIdx.x == 0 && tid == 0) atomicOr(a.flags, 1u);
       return;
@@ -1148,7 +1161,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     const uint32_t ex = scan256(tb, s.scratch);
     if (tid < 256) {
       a.sub_off[g * 256 + tid] = s.aux[g] + ex;
-      if (tb > uint32_t(kLocalCap)) atomicOr(a.flags, 1u);
+      if (tb > uint32_t(kLocalCap) && a.levels != 3) atomicOr(a.flags, 1u);  // (3 levels: checked per sub-sub-bucket)
     }
     if (g == kBins - 1 && tid == 0) a.sub_off[kSubBuckets] = uint32_t(a.n);
   }
@@ -1304,6 +1317,160 @@ __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile
   }
 }
 
+// ---------------------------------------------------------------- third level
+// Above ~65536 x kLocalCap rows the (d7, d6) sub-buckets no longer fit on chip:
+// digit 5 splits each of them (2^24 sub-sub-buckets). The level-2 pass leaves
+// every sub-bucket contiguous in keys_a, so its digit-5 counts need no global
+// atomics: count3_kernel reads each sub-bucket once (a CTA per sub-bucket at a
+// time), writes its 256 sub-sub-bucket starts and its tile count (a sub-sub-
+// bucket above kLocalCap sets the LSD fallback); tile_scan_kernel turns the
+// tile counts into a prefix; sub3_scatter_kernel scatters every tile of a
+// sub-bucket by digit 5 into keys_b (reservations from the starts + per-
+// sub-sub-bucket cursors); the local phase then sorts runs of sub-sub-buckets.
+__global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) count3_kernel(SortArgs a) {
+  __shared__ uint32_t h[256];
+  __shared__ uint32_t scratch[64];
+  const int tid = threadIdx.x;
+  pdl_wait();  // the digit-6 pass
+  pdl_launch_dependents();
+  if (fallback_flag(a)) return;
+  for (uint32_t sb = blockIdx.x; sb < uint32_t(kSubBuckets); sb += gridDim.x) {
+    const uint32_t lo = __ldcg(a.sub_off + sb), hi = __ldcg(a.sub_off + sb + 1);
+    if (tid < 256) h[tid] = 0;
+    __syncthreads();
+    uint32_t i = lo + tid;
+    for (; i + 3 * kPThreads < hi; i += 4 * kPThreads) {  // four loads in flight
+      uint64_t k4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) k4[u] = __ldcs(a.keys_a + i + u * kPThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) atomicAdd(&h[uint32_t(k4[u] >> 40) & 255u], 1u);
+    }
+    for (; i < hi; i += kPThreads) atomicAdd(&h[uint32_t(__ldcs(a.keys_a + i) >> 40) & 255u], 1u);
+    __syncthreads();
+    const uint32_t c = tid < 256 ? h[tid] : 0u;
+    const uint32_t ex = scan256(c, scratch);
+    if (tid < 256) {
+      a.sub3_off[sb * 256 + tid] = lo + ex;
+      if (c > uint32_t(kLocalCap)) atomicOr(a.flags, 1u);
+    }
+    if (tid == 0) a.tile3[sb] = (hi - lo + kPTile - 1) / kPTile;
+    if (sb == uint32_t(kSubBuckets) - 1 && tid == 0) a.sub3_off[kSub3] = uint32_t(a.n);
+    __syncthreads();
+  }
+}
+
+// One CTA: the 65536 tile counts -> exclusive prefix in place, total in meta[1].
+__global__ void __launch_bounds__(1024) tile_scan_kernel(SortArgs a) {
+  constexpr int kChunk = 8192, kPer = kChunk / 1024;
+  __shared__ uint32_t buf[kChunk];
+  __shared__ uint32_t scratch[40];
+  const int tid = threadIdx.x;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (fallback_flag(a)) return;
+  uint32_t carry = 0;
+  for (int c0 = 0; c0 < kSubBuckets; c0 += kChunk) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) buf[i * 1024 + tid] = __ldcg(a.tile3 + c0 + i * 1024 + tid);
+    __syncthreads();
+    uint32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) run += buf[tid * kPer + i];
+    uint32_t total;
+    uint32_t start = carry + block_exclusive_scan<1024>(run, scratch, &total);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const uint32_t v = buf[tid * kPer + i];
+      a.tile3[c0 + tid * kPer + i] = start;
+      for (uint32_t j = 0; j < v; ++j) a.tmap[start + j] = uint32_t(c0 + tid * kPer + i);  // tile -> sub-bucket
+      start += v;
+    }
+    carry += total;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.tile3[kSubBuckets] = carry;
+    a.meta[1] = carry;
+  }
+}
+
+template <bool PK>
+__device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTile& s) {
+  const int tid = threadIdx.x;
+  const uint32_t n_tiles = __ldcg(a.meta + 1);
+  uint32_t* claim = s.scratch + 40;  // [0..1] claimed tile ids by parity, [2..3] their sub-bucket
+  auto locate = [&](uint32_t t) -> uint32_t { return __ldcg(a.tmap + t); };  // tile -> sub-bucket
+  auto rows_of = [&](uint32_t t, uint32_t sb, uint32_t& r0, uint32_t& r1) {
+    const uint32_t lo = __ldcg(a.sub_off + sb), hi = __ldcg(a.sub_off + sb + 1);
+    r0 = lo + (t - __ldcg(a.tile3 + sb)) * kPTile;
+    r1 = min(hi, r0 + kPTile);
+  };
+  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], uint32_t r0, uint32_t r1) {
+    const int tn = int(r1 - r0);
+#pragma unroll
+    for (int u = 0; u < kPItems; ++u) {
+      const int j = u * kPThreads + tid;
+      k[u] = j < tn ? __ldcs(a.keys_a + r0 + j) : 0ull;
+      if constexpr (!PK) v[u] = j < tn ? __ldcs(a.vals_a + r0 + j) : 0u;
+    }
+  };
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(a.flags + 2, 1u);
+    claim[0] = t;
+    claim[2] = t < n_tiles ? locate(t) : 0u;
+  }
+  if (tid < 256) s.hist[tid] = 0;
+  __syncthreads();
+  uint32_t it = claim[0], sb = claim[2], par = 1;
+  uint64_t k[kPItems];
+  uint32_t v[kPItems];
+  Carry<0> cr;
+  uint32_t r0 = 0, r1 = 0;
+  if (it < n_tiles) {
+    rows_of(it, sb, r0, r1);
+    load(k, v, r0, r1);
+  }
+  while (it < n_tiles) {
+    if (tid == 0) {  // the next tile and its sub-bucket, read after the staging barrier
+      const uint32_t t = atomicAdd(a.flags + 2, 1u);
+      claim[par] = t;
+      claim[2 + par] = t < n_tiles ? locate(t) : 0u;
+    }
+    const uint32_t g = sb;
+    uint32_t nit = 0, nsb = 0, nr0 = 0, nr1 = 0;
+    auto reserve = [&](uint32_t d, uint32_t c) {
+      return __ldcg(a.sub3_off + g * 256 + d) + atomicAdd(a.cur24 + g * 256 + d, c);
+    };
+    ptile_scatter<5 * kBits, PK, 0>(k, v, cr, int(r1 - r0), s, a.keys_b, a.vals_b, nullptr, reserve,
+                                    [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<0>&) {
+                                      nit = claim[par];
+                                      nsb = claim[2 + par];
+                                      if (nit < n_tiles) {
+                                        rows_of(nit, nsb, nr0, nr1);
+                                        load(kk, vv, nr0, nr1);
+                                      }
+                                    });
+    it = nit;
+    sb = nsb;
+    r0 = nr0;
+    r1 = nr1;
+    par ^= 1;
+  }
+}
+
+__global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub3_scatter_kernel(SortArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const PTile s = ptile<0>(sm);
+  const int tid = threadIdx.x;
+  pdl_wait();  // the tile prefix
+  pdl_launch_dependents();
+  if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);
+  if (fallback_flag(a)) return;
+  if (packed_rows(s.scratch[50], a)) sub3_scatter_tiles<true>(a, s);
+  else sub3_scatter_tiles<false>(a, s);
+}
+
 __device__ __forceinline__ bool row_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
   return ka < kb || (ka == kb && va < vb);
 }
@@ -1355,14 +1522,16 @@ __device__ __forceinline__ void mbar_inval(uint64_t* bar) {
   asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Greedy cut of one group (offsets off[0..G]) into runs; returns the count.
+// Greedy cut of one group (offsets off[0..G]) into runs of whole sub-buckets
+// of at most kLocalCap rows; run = (first << 16) | end; returns the count.
+template <int G>
 __device__ __forceinline__ uint32_t cut_group(const uint32_t* off, uint32_t* ends) {
   uint32_t nr = 0, s = 0;
-  while (s < uint32_t(kGroupSubs)) {
+  while (s < uint32_t(G)) {
     const uint32_t base = off[s];
     uint32_t e = s + 1;
-    while (e < uint32_t(kGroupSubs) && off[e + 1] - base <= uint32_t(kLocalCap)) ++e;
-    if (off[e] > base) ends[nr++] = (s << 8) | e;
+    while (e < uint32_t(G) && off[e + 1] - base <= uint32_t(kLocalCap)) ++e;
+    if (off[e] > base) ends[nr++] = (s << 16) | e;
     s = e;
   }
   return nr;
@@ -1382,23 +1551,30 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
 // BAL (the scatter path's large runs): a thread's rows in registers across
 // count + scatter, and the claimed group tail. The onesweep hybrid's short
 // runs (n < 4M) are faster without both (+1-5 us each at 0.3-2M rows).
-template <int THREADS, int PACK = 0, bool BAL = false, bool PK = false>
+template <int THREADS, int PACK = 0, bool BAL = false, bool PK = false, int LEVELS = 2>
 __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
+  // sub-buckets of the runs: (d7, d6) or, with three levels, (d7, d6, d5)
+  constexpr int kSubShift = LEVELS == 3 ? 40 : 48;
+  const uint32_t* sub_off = LEVELS == 3 ? a.sub3_off : a.sub_off;
   constexpr int kLWarps = THREADS / 32;
   uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
   uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kLocHist);
   uint32_t* big = reinterpret_cast<uint32_t*>(smem + kLocBig);
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
-  uint32_t* goff = misc + 32;   // [2][kGroupSubs + 1]
-  uint32_t* gends = misc + 72;  // [2][kGroupSubs]
+  // a work item: G consecutive sub-buckets (three levels: the 256 sub-sub-buckets
+  // of one (d7, d6) sub-bucket), its offsets and runs in two slots
+  constexpr int G = LEVELS == 3 ? 256 : kGroupSubs;
+  constexpr int GO = G + 1;
+  uint32_t* goff = LEVELS == 3 ? reinterpret_cast<uint32_t*>(smem + kLocGrp) : misc + 32;  // [2][G + 1]
+  uint32_t* gends = LEVELS == 3 ? goff + 2 * GO : misc + 72;                              // [2][G]
   uint32_t* runs = misc + 112;  // [2][4] descriptors of the run in each buffer
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLocBars);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t* kin = src == 1 ? a.keys_a : a.keys_b;
   const uint32_t* vin = PK ? nullptr : src == 1 ? a.vals_a : a.vals_b;
   const int desc = a.key_mode == kRawDesc;
-  constexpr uint32_t kGroups = kSubBuckets / kGroupSubs;
+  constexpr uint32_t kGroups = (LEVELS == 3 ? kSub3 : kSubBuckets) / G;
   constexpr int kPerThread = kLocalBins / THREADS;
   const uint32_t g0 = blockIdx.x;
   if (g0 >= kGroups) return;
@@ -1422,19 +1598,25 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
 
   // ---- prologue (warp 0): offsets of the first group, its runs, the first
   // TMA; the next group is claimed and its offsets requested into registers
-  uint32_t next_off = 0;  // warp 0, lane <= G: sub_off of group next_g
+  // warp 0: the sub-bucket offsets of group next_g, requested into a register
+  // a group ahead (groups of 16); the three-level path's 257 offsets are read
+  // when the group is moved into its slot (its groups are ~256x larger)
+  uint32_t next_off = 0;
   uint32_t next_g = g0;
+  auto fetch_next = [&]() {
+    if constexpr (G <= 31) next_off = lane <= uint32_t(G) && next_g < kGroups ? __ldcg(sub_off + size_t(next_g) * G + lane) : 0u;
+  };
   if (warp == 0) {
     if (lane == 0) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
       gid[0] = g0;
     }
-    if (lane <= kGroupSubs) goff[lane] = __ldcg(a.sub_off + g0 * kGroupSubs + lane);
+    for (uint32_t i = lane; i <= uint32_t(G); i += 32) goff[i] = __ldcg(sub_off + size_t(g0) * G + i);
     next_g = claim(next_g);
-    if (lane <= kGroupSubs && next_g < kGroups) next_off = __ldcg(a.sub_off + next_g * kGroupSubs + lane);
+    fetch_next();
     __syncwarp();
-    if (lane == 0) misc[2] = cut_group(goff, gends);
+    if (lane == 0) misc[2] = cut_group<G>(goff, gends);
     __syncwarp();
   }
   // warp 0: move the claimed group's offsets into goff slot s, claim the next;
@@ -1442,12 +1624,16 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   auto advance = [&](uint32_t s) -> bool {
     const uint32_t gn = next_g;
     if (gn >= kGroups) return false;
-    if (lane <= kGroupSubs) goff[s * 17 + lane] = next_off;
+    if constexpr (G <= 31) {
+      if (lane <= uint32_t(G)) goff[s * GO + lane] = next_off;
+    } else {
+      for (uint32_t i = lane; i <= uint32_t(G); i += 32) goff[s * GO + i] = __ldcg(sub_off + size_t(gn) * G + i);
+    }
     if (lane == 0) gid[s] = gn;
     next_g = claim(next_g);
-    if (lane <= kGroupSubs && next_g < kGroups) next_off = __ldcg(a.sub_off + next_g * kGroupSubs + lane);
+    fetch_next();
     __syncwarp();
-    if (lane == 0) misc[2 + s] = cut_group(goff + s * 17, gends + s * 16);
+    if (lane == 0) misc[2 + s] = cut_group<G>(goff + s * GO, gends + s * G);
     __syncwarp();
     return true;
   };
@@ -1472,13 +1658,13 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     have = misc[2 + (k & 1)] > 0;
   }
   if (tid == 0) {
-    const uint32_t* off = goff + (k & 1) * 17;
-    const uint32_t se = gends[(k & 1) * 16];
-    const uint32_t base = off[se >> 8], cnt = off[se & 255] - base;
+    const uint32_t* off = goff + (k & 1) * GO;
+    const uint32_t se = gends[(k & 1) * G];
+    const uint32_t base = off[se >> 16], cnt = off[se & 0xFFFFu] - base;
     runs[0] = base;
     runs[1] = cnt;
-    runs[2] = gid[k & 1] * kGroupSubs + (se >> 8);
-    runs[3] = (se & 255) - (se >> 8);
+    runs[2] = gid[k & 1] * G + (se >> 16);
+    runs[3] = (se & 0xFFFFu) - (se >> 16);
     issue_run(kin, vin, base, cnt, smem + kLocA, &bars[0]);
   }
   __syncthreads();  // the first run's descriptor is visible to every thread
@@ -1501,14 +1687,14 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         misc[5] = nk;
         misc[6] = nr;
         if (ok) {
-          const uint32_t* off = goff + (nk & 1) * 17;
-          const uint32_t se = gends[(nk & 1) * 16 + nr];
-          const uint32_t base = off[se >> 8], cnt = off[se & 255] - base;
+          const uint32_t* off = goff + (nk & 1) * GO;
+          const uint32_t se = gends[(nk & 1) * G + nr];
+          const uint32_t base = off[se >> 16], cnt = off[se & 0xFFFFu] - base;
           uint32_t* d = runs + (buf ^ 1) * 4;
           d[0] = base;
           d[1] = cnt;
-          d[2] = gid[nk & 1] * kGroupSubs + (se >> 8);
-          d[3] = (se & 255) - (se >> 8);
+          d[2] = gid[nk & 1] * G + (se >> 16);
+          d[3] = (se & 0xFFFFu) - (se >> 16);
           issue_run(kin, vin, base, cnt, smem + kLocA + (buf ^ 1) * kLocABytes, &bars[buf ^ 1]);
         }
       }
@@ -1535,7 +1721,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     const uint64_t* ak = reinterpret_cast<const uint64_t*>(abuf) + (base & 1u);
     const uint32_t* av = reinterpret_cast<const uint32_t*>(abuf + kLocAKeys) + (base & 3u);
     auto bin_of = [&](uint64_t key) {
-      return int(((uint32_t(key >> 48) - first) << bb) | (uint32_t(key >> (48 - bb)) & ((1u << bb) - 1u)));
+      return int(((uint32_t(key >> kSubShift) - first) << bb) | (uint32_t(key >> (kSubShift - bb)) & ((1u << bb) - 1u)));
     };
     // BAL: a thread's rows of the run (at most kRows: kLocalCap / THREADS),
     // loaded once into registers — the loads issue together instead of one per
@@ -1742,16 +1928,18 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   } else {
     const uint32_t pc = __ldcg(a.flags + 6);
     const bool pk = packed_rows(pc, a);
-    switch (pack_mode(pc)) {
-      case 0: local_phase<kLocalThreads, 0, true>(a, smem, src); break;
-      case 1:
-        if (pk) local_phase<kLocalThreads, 1, true, true>(a, smem, src);
-        else local_phase<kLocalThreads, 1, true>(a, smem, src);
-        break;
-      default:
-        if (pk) local_phase<kLocalThreads, 2, true, true>(a, smem, src);
-        else local_phase<kLocalThreads, 2, true>(a, smem, src);
-        break;
+    {
+      switch (pack_mode(pc)) {
+        case 0: local_phase<kLocalThreads, 0, true>(a, smem, src); break;
+        case 1:
+          if (pk) local_phase<kLocalThreads, 1, true, true>(a, smem, src);
+          else local_phase<kLocalThreads, 1, true>(a, smem, src);
+          break;
+        default:
+          if (pk) local_phase<kLocalThreads, 2, true, true>(a, smem, src);
+          else local_phase<kLocalThreads, 2, true>(a, smem, src);
+          break;
+      }
     }
   }
   if (a.stamps && scatter && threadIdx.x == 0)  // (profiling: the last CTA's end, pass-6 slot unused here)
@@ -1759,6 +1947,35 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   if (stamper) {
     a.stamps[kStamps - 2] = globaltimer();
     a.stamps[kStamps - 1] = scatter ? 3 : 1;
+  }
+}
+
+// The three-level local phase on its own kernel (the two-level kernel's code
+// stays as tuned): runs of (d7, d6, d5) sub-sub-buckets out of keys_b.
+__global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local3_kernel(SortArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  pdl_wait();  // the digit-5 pass
+  pdl_launch_dependents();
+  if (*reinterpret_cast<volatile const uint32_t*>(a.flags) != 0) return;  // LSD fallback (final before this launch)
+  const uint32_t pc = __ldcg(a.flags + 6);
+  if (threadIdx.x == 0) {
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
+    const uint64_t cb = pack_mode(pc) ? key_constbits(a, pc) : 0ull;
+    misc[125] = pc;
+    misc[126] = uint32_t(cb);
+    misc[127] = uint32_t(cb >> 32);
+  }
+  const bool pk = packed_rows(pc, a);
+  switch (pack_mode(pc)) {
+    case 0: local_phase<kLocalThreads, 0, true, false, 3>(a, smem, 2u); break;
+    case 1:
+      if (pk) local_phase<kLocalThreads, 1, true, true, 3>(a, smem, 2u);
+      else local_phase<kLocalThreads, 1, true, false, 3>(a, smem, 2u);
+      break;
+    default:
+      if (pk) local_phase<kLocalThreads, 2, true, true, 3>(a, smem, 2u);
+      else local_phase<kLocalThreads, 2, true, false, 3>(a, smem, 2u);
+      break;
   }
 }
 
@@ -1939,7 +2156,27 @@ struct Layout {
   uint32_t* d7_base;
   uint32_t* items;
   uint32_t* meta;
+  uint32_t* sub3_off;  // three-level scatter only (n >= kLevel3MinRows)
+  uint32_t* cur24;
+  uint32_t* tile3;
+  uint32_t* tmap;
 };
+
+// Above this the (d7, d6) sub-buckets of uniform keys come close to kLocalCap:
+// the scatter path splits them by digit 5 as well (three levels).
+// Measured (uniform keys): 2e8 rows 8.5 ms vs 7.4 ms for the LSD passes (small
+// sub-sub-buckets make short local runs), 1e9 rows 30.3 vs 36.5 ms: the third
+// level starts at 3e8 rows; between ~65536 x kLocalCap x 0.85 and that, LSD.
+constexpr int64_t kLevel3MinRows = 300000000;
+// above this the two-level sub-buckets of uniform keys overflow kLocalCap (pigeonhole + spread): LSD instead
+constexpr int64_t kTwoLevelMaxRows = int64_t(kSubBuckets) * kLocalCap * 85 / 100;
+
+// RL_LEVEL3_MIN_ROWS overrides kLevel3MinRows (tests: the third level at small n)
+static int64_t level3_min_rows() {
+  const char* v = getenv("RL_LEVEL3_MIN_ROWS");
+  const long long r = v && v[0] ? atoll(v) : 0;
+  return r > 0 ? r : kLevel3MinRows;
+}
 
 template <typename C, typename T32, typename T64>
 static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L, bool force_scatter = false) {
@@ -1964,7 +2201,12 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L, bool force_s
   auto db = scat ? t32(c, size_t(kBins + 4)) : nullptr;
   auto it = scat ? t32(c, 4 * size_t(kBins + 2 + n / kPTile)) : nullptr;
   auto me = scat ? t32(c, 4) : nullptr;
-  if (L) *L = Layout{h, tc, gb, fl, st, zero, head, so, ka, kb, va, vb, cc, c7, c16, d7r, db, it, me};
+  const bool lvl3 = scat && n >= level3_min_rows();
+  auto s3 = lvl3 ? t32(c, size_t(kSub3) + 1) : nullptr;
+  auto c24 = lvl3 ? t32(c, size_t(kSub3)) : nullptr;
+  auto t3 = lvl3 ? t32(c, size_t(kSubBuckets) + 1) : nullptr;
+  auto tm = lvl3 ? t32(c, size_t(kSubBuckets) + size_t(n / kPTile) + 1) : nullptr;  // <= one partial tile a sub-bucket
+  if (L) *L = Layout{h, tc, gb, fl, st, zero, head, so, ka, kb, va, vb, cc, c7, c16, d7r, db, it, me, s3, c24, t3, tm};
 }
 
 size_t workspace_bytes(int64_t n) {
@@ -2008,7 +2250,11 @@ static bool scatter_kernels_ready() {
                cudaFuncSetAttribute(sub_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
                    cudaSuccess &&
                cudaFuncSetAttribute(local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kLocalSmemBytes)) == cudaSuccess;
+                                    int(kLocalSmemBytes)) == cudaSuccess &&
+               cudaFuncSetAttribute(local3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kLocalKernelSmem)) == cudaSuccess &&
+               cudaFuncSetAttribute(sub3_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
+                   cudaSuccess;
            if (!ok) cudaGetLastError();
 #ifdef RL_CARVEOUT_MAX
            if (ok) {  // one L1/shared split for every kernel of the sort: no SM reconfiguration between them
@@ -2103,7 +2349,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     return rl_cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration);
   }
   const bool scatter = a.src_mode == kSrcInt64 && a.n >= kHybridMinRows && !getenv_flag_no_hybrid() && L.chunk_cnt &&
-                       a.n <= int64_t(kSubBuckets) * kLocalCap && !getenv_flag("RL_NO_SCATTER") &&
+                       (a.n <= kTwoLevelMaxRows || L.sub3_off) && !getenv_flag("RL_NO_SCATTER") &&
                        scatter_kernels_ready();
   cudaError_t e = cudaMemsetAsync(L.hist, 0, scatter ? L.head_bytes : L.zero_bytes, stream);
   if (e != cudaSuccess) return rl_cuda_status(e);
@@ -2133,6 +2379,13 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     }
     a.chunks = chunks;
     a.allow_pk = getenv_flag("RL_NO_PACKED_ROWS") ? 0 : 1;
+    a.levels = L.sub3_off ? 3 : 2;
+    a.sub3_off = L.sub3_off;
+    a.cur24 = L.cur24;
+    a.tile3 = L.tile3;
+    a.tmap = L.tmap;
+    if (a.levels == 3 && (e = cudaMemsetAsync(L.cur24, 0, sizeof(uint32_t) * size_t(kSub3), stream)) != cudaSuccess)
+      return rl_cuda_status(e);
     int lgrid = device_sm_count() * (1024 / kLocalThreads);
     if (max_ctas > 0) lgrid = std::max(1, std::min(lgrid, max_ctas));
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);
@@ -2165,12 +2418,22 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     chk("top_scatter");
     if ((e = launch_dep(sub_scatter_kernel<0>, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
     chk("sub_scatter");
-    if ((e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes)) != cudaSuccess) return rl_cuda_status(e);
+    int launched = 5;
+    if (a.levels == 3) {  // digit 5 inside every sub-bucket
+      if ((e = launch_dep(count3_kernel, pgrid, kPThreads, size_t(0))) != cudaSuccess) return rl_cuda_status(e);
+      if ((e = launch_dep(tile_scan_kernel, 1, 1024, size_t(0))) != cudaSuccess) return rl_cuda_status(e);
+      if ((e = launch_dep(sub3_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
+      chk("level 3");
+      launched += 3;
+    }
+    if (a.levels == 3) e = launch_dep(local3_kernel, lgrid, kLocalThreads, kLocalKernelSmem);
+    else e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes);
+    if (e != cudaSuccess) return rl_cuda_status(e);
     chk("local");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
     e = launch_sort_kernel(a, grid, stream, pdl);  // returns at once unless the fallback flag is set
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[2]), stream);
-    count_launches(5);
+    count_launches(launched);
     return rl_cuda_status(e != cudaSuccess ? e : cudaGetLastError());
   }
   if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[0]), stream);

@@ -291,3 +291,41 @@ def test_scatter_packed_rows(packed, bits, monkeypatch, into_subbuckets):
     want = O.stable_axis_order(keys, False)
     assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
     assert (out.cpu().numpy() == col[want]).all()
+
+
+@pytest.mark.parametrize("bits", [30, 64])
+def test_three_level_scatter(bits, monkeypatch, into_subbuckets):
+    """The third level (digit 5 inside every (d7, d6) sub-bucket, the local
+    phase over 2^24 sub-sub-buckets) forced at a small size with
+    RL_LEVEL3_MIN_ROWS: narrow (packed-row) and full-range keys, duplicates,
+    both directions, a fused gather — equal to the stable argsort."""
+    if into_subbuckets != "scatter":
+        pytest.skip("the third level belongs to the scatter path")
+    monkeypatch.setenv("RL_LEVEL3_MIN_ROWS", "1")
+    rng = np.random.default_rng(70 + bits)
+    n = 3_000_000
+    keys = full_range(rng, n) if bits == 64 else rng.integers(0, 1 << bits, n, dtype=np.int64)
+    keys[rng.choice(n, n // 30, replace=False)] = keys[rng.integers(0, n, n // 30)]
+    check_sort(keys)
+    check_sort(keys, True)
+    col = rng.integers(0, 256, (n, 4), dtype=np.uint8)
+    kd, cd = torch.from_numpy(keys).cuda(), torch.from_numpy(col).cuda()
+    out = torch.empty_like(cd)
+    perm = engine.sort_permutation([engine.SortAxis(kd, False)], n, kd.device,
+                                   gather=[engine.OutColumn(cd, out, 4, 0)], fuse_gather=True)
+    want = O.stable_axis_order(keys, False)
+    assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
+    assert (out.cpu().numpy() == col[want]).all()
+
+
+def test_three_level_skewed_sub_sub_bucket_falls_back(monkeypatch, into_subbuckets):
+    """A sub-sub-bucket above the on-chip cap: the LSD fallback, same result."""
+    if into_subbuckets != "scatter":
+        pytest.skip("the third level belongs to the scatter path")
+    monkeypatch.setenv("RL_LEVEL3_MIN_ROWS", "1")
+    rng = np.random.default_rng(77)
+    n = 2_000_000
+    keys = full_range(rng, n)
+    keys[:5000] = (keys[:5000] & ~np.int64((1 << 40) - 1)) | rng.integers(0, 1 << 40, 5000)  # one 24-bit prefix
+    keys[:5000] = (np.int64(0x123456) << np.int64(40)) | rng.integers(0, 1 << 40, 5000)
+    check_sort(keys)

@@ -462,6 +462,49 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
           const uint32_t t0 = m_arr[x], t1 = x + 1 < nl ? m_arr[x + 1] : total;
           for (uint32_t t = max(t0, uint32_t(lo)); t < min(t1, uint32_t(hi)); ++t) write(x, t);
         }
+      } else if (total <= uint32_t(kMaxBins)) {
+        // output -> left row map in shared memory (the left bin ends are free now):
+        // every row with pairs marks its first output, an inclusive max-scan fills
+        // the rest — one lookup per output instead of a binary search
+        uint32_t* map = hl;
+        for (uint32_t t = tid; t < total; t += kThreads) map[t] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const uint32_t x = tid * kPer + u;
+          if (x < nl && mloc[u]) map[m_arr[x]] = x;
+        }
+        __syncthreads();
+        constexpr int kM = kMaxBins / kThreads;  // 8 entries a thread
+        uint32_t mv[kM], run_max = 0;
+#pragma unroll
+        for (int i = 0; i < kM; ++i) {
+          const uint32_t t = tid * kM + i;
+          run_max = max(run_max, t < total ? map[t] : 0u);
+          mv[i] = run_max;
+        }
+        const int lane = tid & 31, wp = tid >> 5;
+        uint32_t wincl = run_max;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_up_sync(0xffffffffu, wincl, o);
+          if (lane >= o) wincl = max(wincl, x);
+        }
+        uint32_t wexcl = __shfl_up_sync(0xffffffffu, wincl, 1);
+        if (lane == 0) wexcl = 0;
+        uint32_t* wmax = reinterpret_cast<uint32_t*>(scratch);
+        if (lane == 31) wmax[wp] = wincl;
+        __syncthreads();
+        uint32_t pre = 0;
+        for (int w = 0; w < wp; ++w) pre = max(pre, wmax[w]);
+        pre = max(pre, wexcl);
+#pragma unroll
+        for (int i = 0; i < kM; ++i) {
+          const uint32_t t = tid * kM + i;
+          if (t < total) map[t] = max(pre, mv[i]);
+        }
+        __syncthreads();
+        for (uint64_t t = lo + tid; t < hi; t += kThreads) write(map[t], uint32_t(t));
       } else {
         for (uint64_t t = lo + tid; t < hi; t += kThreads) {
           uint32_t x = 0, y = nl;  // largest p with pre[p] <= t

@@ -926,6 +926,7 @@ __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
   pdl_launch_dependents();
+  if (a.bj && fallback_flag(a)) return;  // the bucket join's plan already declined (bj_pack_kernel)
   // this thread's key sample, in flight while the histogram is zeroed
   const long long sample = __ldg(static_cast<const long long*>(a.col) + int64_t(tid) * a.n / kScatThreads);
   for (int i = tid; i < kScatWords / 4; i += kScatThreads) reinterpret_cast<uint4*>(w)[i] = make_uint4(0, 0, 0, 0);
@@ -2680,18 +2681,30 @@ static_assert(kBjCap == kLocalCap, "the sub-bucket overflow check guards the buc
 // sides is checked against it by the chunk counts). Packed rows need <= 32
 // varying bits and n <= 2^32 per side; otherwise both sides are flagged to
 // fall back (flags[0]) and every later kernel returns at once.
+// Heavy keys are caught here too: if one sub-bucket holds >= 8 of a side's
+// 512 samples (uniform keys: <= 3 almost surely) and its share of the side's
+// rows would exceed twice the on-chip cap, the plan declines at once instead
+// of after both sides' partition passes (BASELINE cfg3's Zipf keys).
 __global__ void __launch_bounds__(1024) bj_pack_kernel(const long long* lk, int64_t nl, const long long* rk,
                                                        int64_t nr, uint32_t* flags_l, uint32_t* flags_r) {
   __shared__ unsigned long long red;
+  __shared__ uint32_t code, heavy;
+  __shared__ uint16_t sub[1024];
   const int tid = threadIdx.x;
-  if (tid == 0) red = 0;
+  if (tid == 0) {
+    red = 0;
+    heavy = 0;
+  }
   __syncthreads();
   const uint64_t k0 = xform(uint64_t(__ldg(lk)), 0);
   const long long* col = tid < 512 ? lk : rk;
   const int64_t n = tid < 512 ? nl : nr;
   const int j = tid & 511;
-  uint64_t v = 0;
-  if (n > 0) v = xform(uint64_t(__ldg(col + int64_t(j) * n / 512)), 0) ^ k0;
+  uint64_t u = 0, v = 0;
+  if (n > 0) {
+    u = xform(uint64_t(__ldg(col + int64_t(j) * n / 512)), 0);
+    v = u ^ k0;
+  }
   const uint32_t vh = __reduce_or_sync(0xffffffffu, uint32_t(v >> 32));
   const uint32_t vl = __reduce_or_sync(0xffffffffu, uint32_t(v));
   if ((tid & 31) == 0 && (vh | vl)) atomicOr(&red, (uint64_t(vh) << 32) | vl);
@@ -2700,9 +2713,23 @@ __global__ void __launch_bounds__(1024) bj_pack_kernel(const long long* lk, int6
     // all keys equal in the sample: pack one low bit so the code is valid (the
     // chunk counts catch any key that differs)
     const uint64_t vary = red ? red : 1ull;
-    const uint32_t c = pack_code_of(vary);
+    code = pack_code_of(vary);
+  }
+  __syncthreads();
+  const uint32_t c = code;
+  sub[tid] = uint16_t(pack_key(u, c) >> 48);
+  __syncthreads();
+  if (n > 0) {  // this sample's sub-bucket among its side's samples
+    const uint16_t me = sub[tid];
+    const int base = tid < 512 ? 0 : 512;
+    uint32_t same = 0;
+    for (int i = 0; i < 512; ++i) same += sub[base + i] == me ? 1u : 0u;
+    if (same >= 8u && double(same - 2) / 512.0 * double(n) > 2.0 * kLocalCap) atomicOr(&heavy, 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {
     const bool ok = pack_mode(c) != 0 && (c >> 14 & 127) + (c & 127) <= 32u && nl <= (int64_t(1) << 32) &&
-                    nr <= (int64_t(1) << 32);
+                    nr <= (int64_t(1) << 32) && !heavy;
     flags_l[6] = c;
     flags_r[6] = c;
     if (!ok) {

@@ -1527,6 +1527,11 @@ __device__ __forceinline__ void mbar_inval(uint64_t* bar) {
 // of at most kLocalCap rows; run = (first << 16) | end; returns the count.
 template <int G>
 __device__ __forceinline__ uint32_t cut_group(const uint32_t* off, uint32_t* ends) {
+  if (off[G] - off[0] <= uint32_t(kLocalCap)) {  // the common case: the whole group is one run
+    if (off[G] == off[0]) return 0;
+    ends[0] = uint32_t(G);  // (0 << 16) | G
+    return 1;
+  }
   uint32_t nr = 0, s = 0;
   while (s < uint32_t(G)) {
     const uint32_t base = off[s];

@@ -36,9 +36,9 @@ int key_axis_align(const int64_t* lkeys, const uint32_t* loff, const int64_t* d_
 }  // namespace keyaxis
 namespace plan {
 
+// The key axes of both sides (kept for the expansion).
 template <typename C>
 static void carve_plan(C& c, int64_t nl, int64_t nr, rl_join_plan* p) {
-  const int64_t cap = std::min(nl, nr), alloc = std::max<int64_t>(cap, 1);
   auto take64 = [&](size_t k) { return c.template take<int64_t>(k); };
   auto take32 = [&](size_t k) { return c.template take<uint32_t>(k); };
   p->scalars = take64(4);
@@ -48,6 +48,17 @@ static void carve_plan(C& c, int64_t nl, int64_t nr, rl_join_plan* p) {
   p->right_positions = take32(size_t(std::max<int64_t>(nr, 1)));
   p->right_key_values = take64(size_t(std::max<int64_t>(nr, 1)));
   p->right_offsets = take32(size_t(nr + 1));
+}
+
+// The alignment arrays (min(nl, nr) capacity, 32 bytes a matched key): carved
+// in the scratch the index sorts used — free once both axes exist — so the
+// plan's footprint at 1e9 x 1e9 is the axes + the larger of the two scratches
+// (~65 GB), not their sum (~97 GB).
+template <typename C>
+static void carve_alignment(C& c, int64_t nl, int64_t nr, rl_join_plan* p) {
+  const int64_t alloc = std::max<int64_t>(std::min(nl, nr), 1);
+  auto take64 = [&](size_t k) { return c.template take<int64_t>(k); };
+  auto take32 = [&](size_t k) { return c.template take<uint32_t>(k); };
   p->matched_keys = take64(size_t(alloc));
   p->left_starts = take32(size_t(alloc));
   p->left_counts = take32(size_t(alloc));
@@ -83,10 +94,18 @@ static size_t side_scratch_bytes(int64_t n) {
   return s + align_up(inner, 256) + 256;
 }
 
+static size_t alignment_bytes(int64_t nl, int64_t nr) {
+  Sizer z;
+  rl_join_plan p;
+  carve_alignment(z, nl, nr, &p);
+  return align_up(z.used, 256);
+}
+
 static size_t scratch_bytes(int64_t nl, int64_t nr) {
   const int64_t n = std::max(nl, nr);
-  size_t one = std::max(side_scratch_bytes(n), align_up(keyaxis::align_workspace_bytes(nl), 256) + 256);
-  return concurrent_sides(nl, nr) ? 2 * one : one;
+  const size_t sides = concurrent_sides(nl, nr) ? 2 * side_scratch_bytes(n) : side_scratch_bytes(n);
+  const size_t align = alignment_bytes(nl, nr) + align_up(keyaxis::align_workspace_bytes(nl), 256) + 256;
+  return std::max(sides, align);
 }
 
 size_t workspace_bytes(int64_t nl, int64_t nr) {
@@ -162,8 +181,12 @@ int build(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, vo
     int st = keyaxis::run_bounds(sd.n > 0 ? sorted : sd.keys, sd.n, sd.kv, sd.off, sd.d, inner, inner_cap, st_i);
     if (st != RL_OK) return st;
   }
-  void* inner = scratch;  // the alignment reuses the first scratch (both sides are done with it)
-  const size_t inner_cap = per_side;
+  // the alignment arrays and the alignment's workspace reuse the scratch (both sides are done with it)
+  Carve ca{scratch, scratch_cap};
+  carve_alignment(ca, nl, nr, p);
+  if (!ca.ok) return RL_ERR_WORKSPACE;
+  void* inner = scratch + align_up(ca.used, 256);
+  const size_t inner_cap = scratch_cap - align_up(ca.used, 256);
   if (aux) {  // join: the alignment waits for the right side
     cudaError_t e = cudaEventRecord(aux->join, aux->stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, aux->join, 0);

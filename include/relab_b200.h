@@ -245,10 +245,11 @@ typedef struct rl_bjoin_plan {
   const uint32_t* sub_off_right;
   uint32_t* flags_left;
   uint32_t* flags_right;
-  uint32_t* counts;
-  uint64_t* offsets;
+  uint32_t* counts;        /* pairs per (group, run) */
+  uint64_t* offsets;       /* first output row per group */
   int64_t* scalars;
   const int64_t* left_keys;
+  int32_t levels;          /* 2: sub-buckets = top 16 key bits; 3 (above ~142M rows a side): top 24 */
   /* carried payload (written by rl_bjoin_plan_build, read by rl_bjoin_expand) */
   const uint64_t* pay_left;
   const uint64_t* pay_right;

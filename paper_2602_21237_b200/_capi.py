@@ -59,7 +59,8 @@ class RlJoinPlan(ctypes.Structure):
 class RlBjoinPlan(ctypes.Structure):
     _fields_ = [(name, ctypes.c_void_p) for name in (
         "rows_left", "rows_right", "sub_off_left", "sub_off_right", "flags_left", "flags_right", "counts",
-        "offsets", "scalars", "left_keys", "pay_left", "pay_right")] + [
+        "offsets", "scalars", "left_keys")] + [("levels", ctypes.c_int32)] + [
+        (name, ctypes.c_void_p) for name in ("pay_left", "pay_right")] + [
         ("words_left", ctypes.c_int32), ("words_right", ctypes.c_int32),
         ("carry_cols_left", ctypes.c_int32), ("carry_cols_right", ctypes.c_int32),
         ("carry_src_left", ctypes.c_void_p * 4), ("carry_src_right", ctypes.c_void_p * 4),

@@ -31,12 +31,15 @@ struct BjSide {
   const uint64_t* rows;     // [n] packed words (key bits << 32 | row id), grouped by sub-bucket
   const uint64_t* pay;      // [n * words] carried payload words, parallel to rows (words > 0)
   int words;
-  const uint32_t* sub_off;  // [kBjSubBuckets + 1] sub-bucket starts
+  const uint32_t* sub_off;  // sub-bucket starts: [2^16 + 1] (two levels) or [2^24 + 1] (three)
   uint32_t* flags;          // [0] != 0: fall back; [6] the joint pack code
   int64_t n;
+  int levels;               // 2: sub-buckets = top 16 packed bits; 3: top 24
 };
 
-size_t bj_side_workspace_bytes(int64_t n, int words);
+// Two levels up to ~0.85 x 65536 x kBjCap rows a side, three above (both sides alike).
+int bj_levels(int64_t nl, int64_t nr);
+size_t bj_side_workspace_bytes(int64_t n, int words, int levels);
 int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, const BjCarry& lcarry,
                  const BjCarry& rcarry, void* ws_l, size_t ws_l_bytes, void* ws_r, size_t ws_r_bytes,
                  cudaStream_t stream, BjSide* left, BjSide* right);

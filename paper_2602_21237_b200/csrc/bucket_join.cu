@@ -46,8 +46,16 @@ using radix::kBjCap;
 using radix::kBjSubBuckets;
 
 constexpr int kThreads = 512;
-constexpr int kGroupSubs = 16;
-constexpr uint32_t kGroups = kBjSubBuckets / kGroupSubs;  // 4096
+// Work items: G consecutive sub-buckets — 16 of the 2^16 (two levels), or the
+// 256 sub-sub-buckets of one level-2 sub-bucket (three levels: 2^24 of them)
+template <int LEVELS>
+struct Geo {
+  static constexpr int G = LEVELS == 3 ? 256 : 16;
+  static constexpr uint32_t kGroups = (LEVELS == 3 ? (1u << 24) : uint32_t(kBjSubBuckets)) / G;
+  static constexpr int kShift = LEVELS == 3 ? 40 : 48;  // the sub-bucket index: top 24 / 16 bits
+};
+constexpr uint32_t kMaxGroups = 1u << 16;  // (three levels)
+constexpr int kMaxG = 256;
 constexpr int kMaxBins = 4096;
 constexpr int kRowsPerThread = (kBjCap + kThreads - 1) / kThreads;  // 5
 constexpr int kRankMax = 48;  // bins above this: a warp's bitonic network
@@ -59,8 +67,9 @@ struct PlanArgs {
   const uint32_t* off_r;
   const uint32_t* flags_l;
   const uint32_t* flags_r;
-  uint32_t* counts;  // [kBjSubBuckets] pairs per (group, run slot)
-  uint64_t* offs;    // [kBjSubBuckets] first output row per (group, run slot)
+  uint32_t* counts;  // [groups * G] pairs per (group, run slot)
+  uint64_t* gtot;    // [groups] pairs per group -> (bj_scan_kernel) first output row of the group
+  int levels;
   int64_t* scalars;  // [0] total pairs, [1] 1 = the bucket join applies
   const long long* k0_src;  // the left side's first key (constant bits of every key)
   const uint64_t* pay_l;    // carried payload words, parallel to rows_l (words_l per row)
@@ -70,14 +79,18 @@ struct PlanArgs {
 
 // Runs of one group: consecutive sub-buckets [s, e) with at most kBjCap rows
 // on each side (every single sub-bucket fits: the scatter passes check it);
-// encoded (s << 8) | e. The same cut in the count and emit kernels.
+// encoded (s << 16) | e. The same cut in the count and emit kernels.
+template <int G>
 __device__ __forceinline__ uint32_t cut_runs(const uint32_t* ol, const uint32_t* orr, uint32_t* ends) {
+  if (ol[G] - ol[0] <= uint32_t(kBjCap) && orr[G] - orr[0] <= uint32_t(kBjCap)) {  // the whole group
+    ends[0] = uint32_t(G);
+    return 1;
+  }
   uint32_t nr = 0, s = 0;
-  while (s < uint32_t(kGroupSubs)) {
+  while (s < uint32_t(G)) {
     uint32_t e = s + 1;
-    while (e < uint32_t(kGroupSubs) && ol[e + 1] - ol[s] <= uint32_t(kBjCap) && orr[e + 1] - orr[s] <= uint32_t(kBjCap))
-      ++e;
-    ends[nr++] = (s << 8) | e;
+    while (e < uint32_t(G) && ol[e + 1] - ol[s] <= uint32_t(kBjCap) && orr[e + 1] - orr[s] <= uint32_t(kBjCap)) ++e;
+    ends[nr++] = (s << 16) | e;
     s = e;
   }
   return nr;
@@ -88,15 +101,16 @@ __device__ __forceinline__ uint32_t bin_bits(uint32_t nsb) {
 }
 
 struct Bins {
-  uint32_t first, bb;
-  __device__ __forceinline__ Bins(uint32_t first_sub, uint32_t nsb) {
+  uint32_t first, bb, shift;
+  __device__ __forceinline__ Bins(uint32_t first_sub, uint32_t nsb, uint32_t sub_shift) {
     first = first_sub;
     bb = bin_bits(nsb);
+    shift = sub_shift;
   }
   __device__ __forceinline__ uint32_t count(uint32_t nsb) const { return nsb << bb; }
   // (sub-bucket - first, the next bb key bits): bins ordered like the keys
   __device__ __forceinline__ uint32_t of(uint64_t w) const {
-    return ((uint32_t(w >> 48) - first) << bb) | (uint32_t(w >> (48 - bb)) & ((1u << bb) - 1u));
+    return ((uint32_t(w >> shift) - first) << bb) | (uint32_t(w >> (shift - bb)) & ((1u << bb) - 1u));
   }
 };
 
@@ -154,30 +168,34 @@ __device__ __forceinline__ void load_rows(const uint64_t* rows, uint32_t r0, uin
 }
 
 // ---------------------------------------------------------------- count
+template <int LEVELS>
 __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
+  using Q = Geo<LEVELS>;
+  constexpr int G = Q::G;
   __shared__ uint64_t br[kBjCap];
   __shared__ uint32_t hist[kMaxBins];
-  __shared__ uint32_t offl[kGroupSubs + 1], offr[kGroupSubs + 1], ends[kGroupSubs];
+  __shared__ uint32_t offl[G + 1], offr[G + 1], ends[G];
   __shared__ uint64_t scratch[kThreads / 32 + 2];
   __shared__ uint32_t nruns;
+  __shared__ unsigned long long gsum;
   const int tid = threadIdx.x;
   if (fell_back(a)) return;
-  for (uint32_t g = blockIdx.x; g < kGroups; g += gridDim.x) {
-    if (tid <= kGroupSubs) {
-      offl[tid] = __ldcg(a.off_l + g * kGroupSubs + tid);
-      offr[tid] = __ldcg(a.off_r + g * kGroupSubs + tid);
+  for (uint32_t g = blockIdx.x; g < Q::kGroups; g += gridDim.x) {
+    for (uint32_t i = tid; i <= uint32_t(G); i += kThreads) {
+      offl[i] = __ldcg(a.off_l + size_t(g) * G + i);
+      offr[i] = __ldcg(a.off_r + size_t(g) * G + i);
     }
+    if (tid == 0) gsum = 0;
     __syncthreads();
-    if (tid == 0) nruns = cut_runs(offl, offr, ends);
+    if (tid == 0) nruns = cut_runs<G>(offl, offr, ends);
     __syncthreads();
     const uint32_t nr = nruns;
-    if (tid >= int(nr) && tid < kGroupSubs) a.counts[g * kGroupSubs + tid] = 0u;
     for (uint32_t r = 0; r < nr; ++r) {
-      const uint32_t s = ends[r] >> 8, e = ends[r] & 255u;
+      const uint32_t s = ends[r] >> 16, e = ends[r] & 0xFFFFu;
       const uint32_t l0 = offl[s], nl = offl[e] - l0, r0 = offr[s], nrr = offr[e] - r0;
       uint64_t cnt = 0;
       if (nl && nrr) {
-        const Bins bins(g * kGroupSubs + s, e - s);
+        const Bins bins(g * G + s, e - s, Q::kShift);
         const uint32_t nbins = bins.count(e - s);
         for (uint32_t i = tid; i < nbins; i += kThreads) hist[i] = 0;
         uint64_t w[kRowsPerThread], wl[kRowsPerThread];
@@ -197,27 +215,32 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
       }
       uint64_t tot;
       block_exclusive_scan<kThreads>(cnt, scratch, &tot);
-      if (tid == 0) a.counts[g * kGroupSubs + r] = uint32_t(tot);
+      if (tid == 0) {
+        a.counts[size_t(g) * G + r] = uint32_t(tot);
+        gsum += tot;
+      }
       __syncthreads();  // hist / br / scratch reused by the next run
     }
+    if (tid == 0) a.gtot[g] = gsum;
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------- scan
-// One CTA: the 65536 run counts in 8 chunks staged through shared memory
-// (coalesced loads), an exclusive scan of each chunk carried into the next.
-__global__ void __launch_bounds__(1024) bj_scan_kernel(PlanArgs a) {
-  constexpr int kChunk = 8192, kPer = kChunk / 1024;
-  __shared__ uint32_t buf[kChunk];
+// One CTA: the group totals (4096 or 65536) in chunks staged through shared
+// memory (coalesced loads), an exclusive scan carried from chunk to chunk —
+// in place: gtot[g] becomes the group's first output row.
+__global__ void __launch_bounds__(1024) bj_scan_kernel(PlanArgs a, uint32_t groups) {
+  constexpr int kChunk = 4096, kPer = kChunk / 1024;
+  __shared__ uint64_t buf[kChunk];
   __shared__ uint64_t scratch[34];
   const int tid = threadIdx.x;
   const bool ok = *reinterpret_cast<volatile const uint32_t*>(a.flags_l) == 0 &&
                   *reinterpret_cast<volatile const uint32_t*>(a.flags_r) == 0;
   uint64_t carry = 0;
-  for (int c0 = 0; c0 < kBjSubBuckets; c0 += kChunk) {
+  for (uint32_t c0 = 0; c0 < groups; c0 += kChunk) {
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) buf[i * 1024 + tid] = ok ? __ldcg(a.counts + c0 + i * 1024 + tid) : 0u;
+    for (int i = 0; i < kPer; ++i) buf[i * 1024 + tid] = ok ? __ldcg(a.gtot + c0 + i * 1024 + tid) : 0ull;
     __syncthreads();
     uint64_t run = 0;
 #pragma unroll
@@ -227,7 +250,7 @@ __global__ void __launch_bounds__(1024) bj_scan_kernel(PlanArgs a) {
     if (ok) {
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
-        a.offs[c0 + tid * kPer + i] = start;
+        a.gtot[c0 + tid * kPer + i] = start;
         start += buf[tid * kPer + i];
       }
     }
@@ -324,25 +347,28 @@ __device__ __forceinline__ void finish_sort(uint64_t* grouped, uint64_t* sorted,
   __syncthreads();
 }
 
-template <bool CHECKSUM>  // CHECKSUM: sum fmix64(l << 32 | r) over the pairs into *e.checksum instead
+template <bool CHECKSUM, int LEVELS>  // CHECKSUM: sum fmix64(l << 32 | r) over the pairs into *e.checksum instead
 __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols cols) {
+  using Q = Geo<LEVELS>;
+  constexpr int G = Q::G;
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* sl = reinterpret_cast<uint64_t*>(smem);  // [kBjCap] left rows, sorted
   uint64_t* sr = sl + kBjCap;                         // [kBjCap] right rows, sorted
   uint64_t* gx = sr + kBjCap;                         // [kBjCap] grouped-by-bin scratch / per-left-row arrays
-  uint32_t* hr = reinterpret_cast<uint32_t*>(gx + kBjCap);  // [kMaxBins] right bin ends (kept for the match)
-  uint32_t* hl = hr + kMaxBins;                             // [kMaxBins] left bin ends
-  uint16_t* gidx = reinterpret_cast<uint16_t*>(hl + kMaxBins);  // [kBjCap] load index of grouped rows
-  uint16_t* lidx = gidx + kBjCap;                               // [kBjCap] load index of sorted left rows
-  uint16_t* ridx = lidx + kBjCap;                               // [kBjCap] ... right rows
+  uint32_t* hr = reinterpret_cast<uint32_t*>(gx + kBjCap);  // [kMaxBins] bin counters (right bin ends for the match)
+  uint32_t* omap = hr + kMaxBins;                           // [kMaxBins] output -> left row
+  uint16_t* gidx = reinterpret_cast<uint16_t*>(omap + kMaxBins);  // [kBjCap] load index of grouped rows
+  uint16_t* lidx = gidx + kBjCap;                                 // [kBjCap] load index of sorted left rows
+  uint16_t* ridx = lidx + kBjCap;                                 // [kBjCap] ... right rows
   uint64_t* scratch = reinterpret_cast<uint64_t*>(ridx + kBjCap);  // [kThreads / 32 + 2]
-  uint32_t* misc = reinterpret_cast<uint32_t*>(scratch + kThreads / 32 + 2);  // offsets, runs, big bins
-  uint32_t* offl = misc;
-  uint32_t* offr = misc + 17;
-  uint32_t* ends = misc + 34;
-  uint32_t* big = misc + 50;  // [64]
-  uint32_t* nbig = misc + 114;
-  uint32_t* nruns = misc + 115;
+  uint64_t* rpre = scratch + kThreads / 32 + 2;                    // [kMaxG] run starts in the group
+  uint32_t* misc = reinterpret_cast<uint32_t*>(rpre + kMaxG);      // offsets, runs, big bins
+  uint32_t* offl = misc;                     // [kMaxG + 1]
+  uint32_t* offr = misc + (kMaxG + 1);       // [kMaxG + 1]
+  uint32_t* ends = misc + 2 * (kMaxG + 1);   // [kMaxG]
+  uint32_t* big = ends + kMaxG;              // [64]
+  uint32_t* nbig = big + 64;
+  uint32_t* nruns = nbig + 1;
   const PlanArgs& a = e.p;
   const int tid = threadIdx.x;
   uint64_t sum = 0;
@@ -356,35 +382,44 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
     const uint64_t u = mode == 1 ? (v >> shl) | constbits : radix::unpack_key(v, code, constbits);
     return (long long)radix::xform(u, 0);
   };
-  for (uint32_t g = blockIdx.x; g < kGroups; g += gridDim.x) {
-    if (tid <= kGroupSubs) {
-      offl[tid] = __ldcg(a.off_l + g * kGroupSubs + tid);
-      offr[tid] = __ldcg(a.off_r + g * kGroupSubs + tid);
+  for (uint32_t g = blockIdx.x; g < Q::kGroups; g += gridDim.x) {
+    const uint64_t gbase = __ldcg(a.gtot + g);  // the group's first output row (scanned)
+    for (uint32_t i = tid; i <= uint32_t(G); i += kThreads) {
+      offl[i] = __ldcg(a.off_l + size_t(g) * G + i);
+      offr[i] = __ldcg(a.off_r + size_t(g) * G + i);
     }
     __syncthreads();
-    if (tid == 0) *nruns = cut_runs(offl, offr, ends);
+    if (tid == 0) *nruns = cut_runs<G>(offl, offr, ends);
     __syncthreads();
     const uint32_t nr = *nruns;
+    {  // run starts inside the group
+      const uint64_t c = tid < int(nr) ? uint64_t(__ldcg(a.counts + size_t(g) * G + tid)) : 0ull;
+      uint64_t tot;
+      const uint64_t ex = block_exclusive_scan<kThreads>(c, scratch, &tot);
+      if (tid < int(nr)) rpre[tid] = ex;
+      __syncthreads();
+    }
     for (uint32_t r = 0; r < nr; ++r) {
-      const uint32_t cnt_pairs = __ldcg(a.counts + g * kGroupSubs + r);
-      const uint64_t base = __ldcg(a.offs + g * kGroupSubs + r);
+      const uint32_t cnt_pairs = __ldcg(a.counts + size_t(g) * G + r);
+      const uint64_t base = gbase + rpre[r];
       if (cnt_pairs == 0 || base + cnt_pairs <= e.out_begin || base >= e.out_end) continue;  // uniform
-      const uint32_t s = ends[r] >> 8, en = ends[r] & 255u;
+      const uint32_t s = ends[r] >> 16, en = ends[r] & 0xFFFFu;
       const uint32_t l0 = offl[s], nl = offl[en] - l0, r0 = offr[s], nrr = offr[en] - r0;
-      const Bins bins(g * kGroupSubs + s, en - s);
+      const Bins bins(g * G + s, en - s, Q::kShift);
       const uint32_t nbins = bins.count(en - s);
-      for (uint32_t i = tid; i < nbins; i += kThreads) {
-        hr[i] = 0;
-        hl[i] = 0;
-      }
+      for (uint32_t i = tid; i < nbins; i += kThreads) hr[i] = 0;
       uint64_t w[kRowsPerThread], wl[kRowsPerThread];
-      load_rows(a.rows_r, r0, nrr, w);
       load_rows(a.rows_l, l0, nl, wl);
+      load_rows(a.rows_r, r0, nrr, w);
+      __syncthreads();
+      // left side sorted first; the bin counters then serve the right side and
+      // keep its bin ends for the match
+      bin_rows(wl, nl, bins, nbins, hr, gx, scratch, gidx);
+      finish_sort(gx, sl, hr, bins, nl, big, nbig, gidx, lidx);
+      for (uint32_t i = tid; i < nbins; i += kThreads) hr[i] = 0;
       __syncthreads();
       bin_rows(w, nrr, bins, nbins, hr, gx, scratch, gidx);
       finish_sort(gx, sr, hr, bins, nrr, big, nbig, gidx, ridx);
-      bin_rows(wl, nl, bins, nbins, hl, gx, scratch, gidx);
-      finish_sort(gx, sl, hl, bins, nl, big, nbig, gidx, lidx);
       // every left row (sorted index p): its matching right range [rs, rs + m) in sr
       uint32_t* m_arr = reinterpret_cast<uint32_t*>(gx);
       uint32_t* rs_arr = m_arr + kBjCap;
@@ -466,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         // output -> left row map in shared memory (the left bin ends are free now):
         // every row with pairs marks its first output, an inclusive max-scan fills
         // the rest — one lookup per output instead of a binary search
-        uint32_t* map = hl;
+        uint32_t* map = omap;
         for (uint32_t t = tid; t < total; t += kThreads) map[t] = 0u;
         __syncthreads();
 #pragma unroll
@@ -527,28 +562,33 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
 }
 
 constexpr size_t kEmitSmem = size_t(kBjCap) * 8 * 3 + size_t(kMaxBins) * 4 * 2 + size_t(kBjCap) * 2 * 3 +
-                             (kThreads / 32 + 2) * 8 + 128 * 4;
+                             (kThreads / 32 + 2) * 8 + size_t(kMaxG) * 8 + (3 * kMaxG + 2 + 64 + 4) * 4;
 
 // ---------------------------------------------------------------- host
-static size_t side_bytes(int64_t n, int words) { return align_up(radix::bj_side_workspace_bytes(n, words), 256); }
+static size_t side_bytes(int64_t n, int words, int levels) {
+  return align_up(radix::bj_side_workspace_bytes(n, words, levels), 256);
+}
+static uint32_t groups_of(int levels) { return levels == 3 ? Geo<3>::kGroups : Geo<2>::kGroups; }
+static int group_size(int levels) { return levels == 3 ? Geo<3>::G : Geo<2>::G; }
 
 size_t workspace_bytes(int64_t nl, int64_t nr, int lwords, int rwords) {
-  return side_bytes(nl, lwords) + side_bytes(nr, rwords) + align_up(sizeof(uint32_t) * kBjSubBuckets, 256) +
-         align_up(sizeof(uint64_t) * kBjSubBuckets, 256) + align_up(sizeof(int64_t) * 4, 256) + 256;
+  const int lv = radix::bj_levels(nl, nr);
+  const size_t runs = size_t(groups_of(lv)) * group_size(lv);
+  return side_bytes(nl, lwords, lv) + side_bytes(nr, rwords, lv) + align_up(sizeof(uint32_t) * runs, 256) +
+         align_up(sizeof(uint64_t) * groups_of(lv), 256) + align_up(sizeof(int64_t) * 4, 256) + 256;
 }
 
-static int emit_grid() {
+template <bool CK, int LV>
+static int emit_grid_of() {
   static int cache[kMaxDevices] = {};
   return per_device(cache, [] {
-    if (cudaFuncSetAttribute(bj_emit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem)) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(bj_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem)) !=
-            cudaSuccess) {
+    if (cudaFuncSetAttribute(bj_emit_kernel<CK, LV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEmitSmem)) !=
+        cudaSuccess) {
       cudaGetLastError();
       return -1;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bj_emit_kernel<false>, kThreads, kEmitSmem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bj_emit_kernel<CK, LV>, kThreads, kEmitSmem) !=
             cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
@@ -599,19 +639,23 @@ int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, con
   if (st != RL_OK) return st;
   if (reinterpret_cast<uintptr_t>(ws) % 256 != 0 || ws_bytes < workspace_bytes(nl, nr, lc.words, rc.words))
     return RL_ERR_WORKSPACE;
+  const int lv = radix::bj_levels(nl, nr);
+  const size_t runs = size_t(groups_of(lv)) * group_size(lv);
   char* base = static_cast<char*>(ws);
-  const size_t wl = side_bytes(nl, lc.words), wr = side_bytes(nr, rc.words);
+  const size_t wl = side_bytes(nl, lc.words, lv), wr = side_bytes(nr, rc.words, lv);
   uint32_t* counts = reinterpret_cast<uint32_t*>(base + wl + wr);
-  uint64_t* offs = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(counts) + align_up(sizeof(uint32_t) * kBjSubBuckets, 256));
-  int64_t* scalars = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(offs) + align_up(sizeof(uint64_t) * kBjSubBuckets, 256));
+  uint64_t* gtot = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(counts) + align_up(sizeof(uint32_t) * runs, 256));
+  int64_t* scalars = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(gtot) +
+                                                align_up(sizeof(uint64_t) * groups_of(lv), 256));
   BjSide L, R;
   st = radix::bj_partition(lkeys, nl, rkeys, nr, lc, rc, base, wl, base + wl, wr, stream, &L, &R);
   if (st != RL_OK) return st;
-  PlanArgs a{L.rows, R.rows, L.sub_off, R.sub_off, L.flags, R.flags, counts, offs, scalars,
+  PlanArgs a{L.rows, R.rows, L.sub_off, R.sub_off, L.flags, R.flags, counts, gtot, lv, scalars,
              reinterpret_cast<const long long*>(lkeys), L.pay, R.pay, L.words, R.words};
   const int grid = device_sm_count() * 3;
-  bj_count_kernel<<<grid, kThreads, 0, stream>>>(a);
-  bj_scan_kernel<<<1, 1024, 0, stream>>>(a);
+  if (lv == 3) bj_count_kernel<3><<<grid, kThreads, 0, stream>>>(a);
+  else bj_count_kernel<2><<<grid, kThreads, 0, stream>>>(a);
+  bj_scan_kernel<<<1, 1024, 0, stream>>>(a, groups_of(lv));
   count_launches(2);
   out->rows_left = L.rows;
   out->rows_right = R.rows;
@@ -620,8 +664,9 @@ int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, con
   out->flags_left = L.flags;
   out->flags_right = R.flags;
   out->counts = counts;
-  out->offsets = offs;
+  out->offsets = gtot;
   out->scalars = scalars;
+  out->levels = lv;
   out->left_keys = lkeys;
   out->pay_left = L.pay;
   out->pay_right = R.pay;
@@ -672,19 +717,26 @@ int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t*
     cs.c[i] = EmitCol{static_cast<const uint8_t*>(c.src), static_cast<uint8_t*>(c.dst), c.width, c.side,
                       c.side == RL_SIDE_KEY ? -1 : carried_offset(p, c)};
   }
-  const int grid = emit_grid();
+  const int lv = p->levels == 3 ? 3 : 2;
+  const int grid = lv == 3 ? (checksum ? emit_grid_of<true, 3>() : emit_grid_of<false, 3>())
+                           : (checksum ? emit_grid_of<true, 2>() : emit_grid_of<false, 2>());
   if (grid < 1) return rl_cuda_status(cudaErrorInvalidConfiguration);
   EmitArgs e;
   e.p = PlanArgs{p->rows_left, p->rows_right, p->sub_off_left, p->sub_off_right, p->flags_left, p->flags_right,
-                 p->counts, p->offsets, p->scalars, reinterpret_cast<const long long*>(p->left_keys), p->pay_left,
-                 p->pay_right, p->words_left, p->words_right};
+                 p->counts, p->offsets, lv, p->scalars, reinterpret_cast<const long long*>(p->left_keys),
+                 p->pay_left, p->pay_right, p->words_left, p->words_right};
   e.out_begin = out_begin;
   e.out_end = out_end;
   e.lrows_out = lrows_out;
   e.rrows_out = rrows_out;
   e.checksum = reinterpret_cast<unsigned long long*>(checksum);
-  if (checksum) bj_emit_kernel<true><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
-  else bj_emit_kernel<false><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
+  if (lv == 3) {
+    if (checksum) bj_emit_kernel<true, 3><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
+    else bj_emit_kernel<false, 3><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
+  } else {
+    if (checksum) bj_emit_kernel<true, 2><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
+    else bj_emit_kernel<false, 2><<<grid, kThreads, kEmitSmem, stream>>>(e, cs);
+  }
   count_launches(1);
   return rl_cuda_status(cudaGetLastError());
 }

@@ -1396,7 +1396,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(SortArgs a) {
   }
 }
 
-template <bool PK>
+template <bool PK, int CW = 0>
 __device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTile& s) {
   const int tid = threadIdx.x;
   const uint32_t n_tiles = __ldcg(a.meta + 1);
@@ -1407,13 +1407,17 @@ __device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTil
     r0 = lo + (t - __ldcg(a.tile3 + sb)) * kPTile;
     r1 = min(hi, r0 + kPTile);
   };
-  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], uint32_t r0, uint32_t r1) {
+  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cc, uint32_t r0, uint32_t r1) {
     const int tn = int(r1 - r0);
 #pragma unroll
     for (int u = 0; u < kPItems; ++u) {
       const int j = u * kPThreads + tid;
       k[u] = j < tn ? __ldcs(a.keys_a + r0 + j) : 0ull;
       if constexpr (!PK) v[u] = j < tn ? __ldcs(a.vals_a + r0 + j) : 0u;
+      if constexpr (CW > 0) {
+#pragma unroll
+        for (int w = 0; w < CW; ++w) cc.p[u][w] = j < tn ? __ldcs(a.pay_a + (size_t(r0) + j) * CW + w) : 0ull;
+      }
     }
   };
   if (tid == 0) {
@@ -1426,11 +1430,11 @@ __device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTil
   uint32_t it = claim[0], sb = claim[2], par = 1;
   uint64_t k[kPItems];
   uint32_t v[kPItems];
-  Carry<0> cr;
+  Carry<CW> cr;
   uint32_t r0 = 0, r1 = 0;
   if (it < n_tiles) {
     rows_of(it, sb, r0, r1);
-    load(k, v, r0, r1);
+    load(k, v, cr, r0, r1);
   }
   while (it < n_tiles) {
     if (tid == 0) {  // the next tile and its sub-bucket, read after the staging barrier
@@ -1443,15 +1447,15 @@ __device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTil
     auto reserve = [&](uint32_t d, uint32_t c) {
       return __ldcg(a.sub3_off + g * 256 + d) + atomicAdd(a.cur24 + g * 256 + d, c);
     };
-    ptile_scatter<5 * kBits, PK, 0>(k, v, cr, int(r1 - r0), s, a.keys_b, a.vals_b, nullptr, reserve,
-                                    [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<0>&) {
-                                      nit = claim[par];
-                                      nsb = claim[2 + par];
-                                      if (nit < n_tiles) {
-                                        rows_of(nit, nsb, nr0, nr1);
-                                        load(kk, vv, nr0, nr1);
-                                      }
-                                    });
+    ptile_scatter<5 * kBits, PK, CW>(k, v, cr, int(r1 - r0), s, a.keys_b, a.vals_b, a.pay_b, reserve,
+                                     [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
+                                       nit = claim[par];
+                                       nsb = claim[2 + par];
+                                       if (nit < n_tiles) {
+                                         rows_of(nit, nsb, nr0, nr1);
+                                         load(kk, vv, cc, nr0, nr1);
+                                       }
+                                     });
     it = nit;
     sb = nsb;
     r0 = nr0;
@@ -1460,16 +1464,21 @@ __device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTil
   }
 }
 
+template <int CW = 0>  // CW > 0: the bucket join's carried payload words (packed rows)
 __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub3_scatter_kernel(SortArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const PTile s = ptile<0>(sm);
+  const PTile s = ptile<CW>(sm);
   const int tid = threadIdx.x;
   pdl_wait();  // the tile prefix
   pdl_launch_dependents();
   if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);
   if (fallback_flag(a)) return;
-  if (packed_rows(s.scratch[50], a)) sub3_scatter_tiles<true>(a, s);
-  else sub3_scatter_tiles<false>(a, s);
+  if constexpr (CW > 0) {
+    sub3_scatter_tiles<true, CW>(a, s);
+  } else {
+    if (packed_rows(s.scratch[50], a)) sub3_scatter_tiles<true>(a, s);
+    else sub3_scatter_tiles<false>(a, s);
+  }
 }
 
 __device__ __forceinline__ bool row_less(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
@@ -2185,7 +2194,8 @@ static int64_t level3_min_rows() {
 }
 
 template <typename C, typename T32, typename T64>
-static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L, bool force_scatter = false) {
+static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L, bool force_scatter = false,
+                      int force_levels = 0) {
   const size_t tiles = size_t((n + kTile - 1) / kTile);
   auto h = t32(c, size_t(kHistReps) * kPasses * kBins);
   auto tc = t32(c, 2 * kPasses);
@@ -2207,7 +2217,7 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L, bool force_s
   auto db = scat ? t32(c, size_t(kBins + 4)) : nullptr;
   auto it = scat ? t32(c, 4 * size_t(kBins + 2 + n / kPTile)) : nullptr;
   auto me = scat ? t32(c, 4) : nullptr;
-  const bool lvl3 = scat && n >= level3_min_rows();
+  const bool lvl3 = scat && (force_levels ? force_levels == 3 : n >= level3_min_rows());
   auto s3 = lvl3 ? t32(c, size_t(kSub3) + 1) : nullptr;
   auto c24 = lvl3 ? t32(c, size_t(kSub3)) : nullptr;
   auto t3 = lvl3 ? t32(c, size_t(kSubBuckets) + 1) : nullptr;
@@ -2259,7 +2269,7 @@ static bool scatter_kernels_ready() {
                                     int(kLocalSmemBytes)) == cudaSuccess &&
                cudaFuncSetAttribute(local3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kLocalKernelSmem)) == cudaSuccess &&
-               cudaFuncSetAttribute(sub3_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
+               cudaFuncSetAttribute(sub3_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
                    cudaSuccess;
            if (!ok) cudaGetLastError();
 #ifdef RL_CARVEOUT_MAX
@@ -2428,7 +2438,7 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     if (a.levels == 3) {  // digit 5 inside every sub-bucket
       if ((e = launch_dep(count3_kernel, pgrid, kPThreads, size_t(0))) != cudaSuccess) return rl_cuda_status(e);
       if ((e = launch_dep(tile_scan_kernel, 1, 1024, size_t(0))) != cudaSuccess) return rl_cuda_status(e);
-      if ((e = launch_dep(sub3_scatter_kernel, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
+      if ((e = launch_dep(sub3_scatter_kernel<0>, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
       chk("level 3");
       launched += 3;
     }
@@ -2744,10 +2754,16 @@ __global__ void __launch_bounds__(1024) bj_pack_kernel(const long long* lk, int6
   }
 }
 
-size_t bj_side_workspace_bytes(int64_t n, int words) {
+int bj_levels(int64_t nl, int64_t nr) {
+  const char* v = getenv("RL_BJ_LEVELS");  // "3": the third level at any size (tests)
+  if (v && v[0] == '3') return 3;
+  return std::max(nl, nr) > kTwoLevelMaxRows ? 3 : 2;
+}
+
+size_t bj_side_workspace_bytes(int64_t n, int words, int levels) {
   CarveSize c;
   carve_all(c, std::max<int64_t>(n, 1), [](CarveSize& c, size_t k) { c.take<uint32_t>(k); return (uint32_t*)nullptr; },
-            [](CarveSize& c, size_t k) { c.take<uint64_t>(k); return (uint64_t*)nullptr; }, nullptr, true);
+            [](CarveSize& c, size_t k) { c.take<uint64_t>(k); return (uint64_t*)nullptr; }, nullptr, true, levels);
   if (words > 0) {  // carried payload, ping-pong
     c.take<uint64_t>(size_t(std::max<int64_t>(n, 1)) * words);
     c.take<uint64_t>(size_t(std::max<int64_t>(n, 1)) * words);
@@ -2764,6 +2780,8 @@ static bool carry_kernels_ready() {
            const bool ok = cudaFuncSetAttribute(top_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 int(psmem_bytes(CW))) == cudaSuccess &&
                            cudaFuncSetAttribute(sub_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(psmem_bytes(CW))) == cudaSuccess &&
+                           cudaFuncSetAttribute(sub3_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 int(psmem_bytes(CW))) == cudaSuccess;
            if (!ok) cudaGetLastError();
            return ok ? 1 : -1;
@@ -2820,6 +2838,7 @@ int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t
   Layout L[2];
   uint64_t* pays[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   const int64_t ns[2] = {nl, nr};
+  const int levels = bj_levels(nl, nr);  // both sides alike: equal keys meet in the same sub-bucket index
   const BjCarry* carries[2] = {&lcarry, &rcarry};
   void* wss[2] = {ws_l, ws_r};
   const size_t wsb[2] = {ws_l_bytes, ws_r_bytes};
@@ -2831,13 +2850,14 @@ int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t
       if (!cy.src[c] || cy.width[c] <= 0 || cy.off[c] < 0 || cy.off[c] + cy.width[c] > 8 * cy.words) return RL_ERR_BAD_ARG;
     Carve c{static_cast<char*>(wss[i]), wsb[i]};
     carve_all(c, ns[i], [](Carve& c, size_t k) { return c.take<uint32_t>(k); },
-              [](Carve& c, size_t k) { return c.take<uint64_t>(k); }, &L[i], true);
+              [](Carve& c, size_t k) { return c.take<uint64_t>(k); }, &L[i], true, levels);
     if (cy.words > 0) {
       pays[i][0] = c.take<uint64_t>(size_t(ns[i]) * cy.words);
       pays[i][1] = c.take<uint64_t>(size_t(ns[i]) * cy.words);
     }
     if (!c.ok) return RL_ERR_WORKSPACE;
     cudaError_t e = cudaMemsetAsync(L[i].hist, 0, L[i].head_bytes, stream);
+    if (e == cudaSuccess && levels == 3) e = cudaMemsetAsync(L[i].cur24, 0, sizeof(uint32_t) * size_t(kSub3), stream);
     if (e != cudaSuccess) return rl_cuda_status(e);
   }
   bj_pack_kernel<<<1, 1024, 0, stream>>>(reinterpret_cast<const long long*>(lkeys), nl,
@@ -2858,24 +2878,34 @@ int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t
     }
     a.pay_a = pays[i][0];
     a.pay_b = pays[i][1];
+    a.levels = levels;
+    a.sub3_off = L[i].sub3_off;
+    a.cur24 = L[i].cur24;
+    a.tile3 = L[i].tile3;
+    a.tmap = L[i].tmap;
     const int pgrid = device_sm_count() * pass_ctas_per_sm();
     sub_hist_kernel<<<a.chunks, kScatThreads, kHistSmem, stream>>>(a);
     const size_t sm = psmem_bytes(cy.words);
-    if (cy.words == 0) {
-      top_scatter_kernel<0><<<pgrid, kPThreads, sm, stream>>>(a);
-      sub_scatter_kernel<0><<<pgrid, kPThreads, sm, stream>>>(a);
-    } else if (cy.words == 1) {
-      top_scatter_kernel<1><<<pgrid, kPThreads, sm, stream>>>(a);
-      sub_scatter_kernel<1><<<pgrid, kPThreads, sm, stream>>>(a);
-    } else {
-      top_scatter_kernel<2><<<pgrid, kPThreads, sm, stream>>>(a);
-      sub_scatter_kernel<2><<<pgrid, kPThreads, sm, stream>>>(a);
-    }
-    launched += 3;
-    outs[i]->pay = pays[i][0];  // the digit-6 pass leaves the payload in pay_a, beside keys_a
+    auto passes = [&](auto cwc) {
+      constexpr int CW = decltype(cwc)::value;
+      top_scatter_kernel<CW><<<pgrid, kPThreads, sm, stream>>>(a);
+      sub_scatter_kernel<CW><<<pgrid, kPThreads, sm, stream>>>(a);
+      if (levels == 3) {  // digit 5 inside every sub-bucket: keys_b / pay_b
+        count3_kernel<<<pgrid, kPThreads, 0, stream>>>(a);
+        tile_scan_kernel<<<1, 1024, 0, stream>>>(a);
+        sub3_scatter_kernel<CW><<<pgrid, kPThreads, sm, stream>>>(a);
+      }
+    };
+    if (cy.words == 0) passes(std::integral_constant<int, 0>{});
+    else if (cy.words == 1) passes(std::integral_constant<int, 1>{});
+    else passes(std::integral_constant<int, 2>{});
+    launched += levels == 3 ? 6 : 3;
+    // the last counting pass leaves rows + payload in keys_a / pay_a (two levels) or keys_b / pay_b
+    outs[i]->pay = levels == 3 ? pays[i][1] : pays[i][0];
     outs[i]->words = cy.words;
-    outs[i]->rows = L[i].keys_a;
-    outs[i]->sub_off = L[i].sub_off;
+    outs[i]->rows = levels == 3 ? L[i].keys_b : L[i].keys_a;
+    outs[i]->levels = levels;
+    outs[i]->sub_off = levels == 3 ? L[i].sub3_off : L[i].sub_off;
     outs[i]->flags = L[i].flags;
     outs[i]->n = ns[i];
   }

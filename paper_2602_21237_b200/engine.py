@@ -396,7 +396,6 @@ def multiset_digest(columns: Sequence[torch.Tensor]) -> int:
 
 BJ_MIN_ROWS = 4 << 20  # smaller joins: the sort-based plan (fewer launches; measured crossover ~4M rows a side)
 BJ_CARRY_MIN_RATIO = 0.5  # carry payloads when the expected pairs reach half the larger side (measured break-even)
-BJ_MAX_ROWS = (1 << 16) * 2560 * 9 // 10  # above ~this some sub-bucket surely exceeds its 2560-row cap
 
 
 def _bjoin_allowed(nl: int, nr: int) -> bool:
@@ -406,7 +405,7 @@ def _bjoin_allowed(nl: int, nr: int) -> bool:
         return False
     if os.environ.get("RL_FORCE_BJOIN", "") not in ("", "0"):
         return nl >= 1 and nr >= 1
-    return min(nl, nr) >= BJ_MIN_ROWS and max(nl, nr) <= BJ_MAX_ROWS
+    return min(nl, nr) >= BJ_MIN_ROWS and max(nl, nr) <= C.RL_MAX_ROWS
 
 
 class BucketJoinPlan:

@@ -184,3 +184,29 @@ def test_carried_payload_columns(shape):
         assert (c.dst.cpu().numpy() == h[wr]).all()
     expect_words = {"int64": 1, "bytes16": 2, "mixed3": 2, "too_wide": 0}[shape]
     assert bp.plan.words_left == expect_words
+
+
+@pytest.mark.parametrize("carry", [False, True])
+def test_three_level_partition(carry, monkeypatch):
+    """The bucket join over 2^24 sub-sub-buckets (the partition's third level,
+    forced at this size with RL_BJ_LEVELS=3): same pairs, order, columns and
+    checksum as the oracle, payload carried through the digit-5 pass too."""
+    monkeypatch.setenv("RL_BJ_LEVELS", "3")
+    rng = np.random.default_rng(31)
+    n = 3_000_000
+    lk, rk = rng.integers(0, 2_000_000, n), rng.integers(0, 2_000_000, n + 7)
+    bp = _check(lk, rk)
+    assert bp.plan.levels == 3
+    lp = rng.integers(-(2**60), 2**60, n)
+    rp = rng.integers(0, 256, (n + 7, 12), dtype=np.uint8)
+    ld, rd = _dev(lp), _dev(rp)
+    bp = engine.BucketJoinPlan(_dev(lk), _dev(rk), [ld] if carry else [], [rd] if carry else [])
+    wl, wr = O.join_pairs(lk, rk)
+    cols = [engine.OutColumn(None, torch.empty(bp.total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_KEY),
+            engine.OutColumn(ld, torch.empty(bp.total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_LEFT),
+            engine.OutColumn(rd, torch.empty((bp.total, 12), dtype=torch.uint8, device="cuda"), 12, C.RL_SIDE_RIGHT)]
+    bp.expand(0, bp.total, cols)
+    assert bp.plan.words_left == (1 if carry else 0) and bp.plan.words_right == (2 if carry else 0)
+    assert (cols[0].dst.cpu().numpy() == lk[wl]).all()
+    assert (cols[1].dst.cpu().numpy() == lp[wl]).all()
+    assert (cols[2].dst.cpu().numpy() == rp[wr]).all()

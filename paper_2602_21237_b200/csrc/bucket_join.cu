@@ -158,6 +158,21 @@ __device__ __forceinline__ void bin_rows(const uint64_t (&w)[kRowsPerThread], ui
   __syncthreads();
 }
 
+// L2 prefetch of the rows of the run after r in this group (both sides), issued
+// while run r is processed: the next run's first loads then hit L2.
+template <int G>
+__device__ __forceinline__ void prefetch_next_run(const PlanArgs& a, const uint32_t* offl, const uint32_t* offr,
+                                                  const uint32_t* ends, uint32_t r, uint32_t nr) {
+  if (r + 1 >= nr) return;
+  const uint32_t s = ends[r + 1] >> 16, e = ends[r + 1] & 0xFFFFu;
+  const uint32_t l0 = offl[s], r0 = offr[s];
+  const uint32_t lines_l = ((offl[e] - l0) * 8 + 127) / 128, lines_r = ((offr[e] - r0) * 8 + 127) / 128;
+  for (uint32_t i = threadIdx.x; i < lines_l + lines_r; i += kThreads) {
+    const uint64_t* p = i < lines_l ? a.rows_l + l0 + size_t(i) * 16 : a.rows_r + r0 + size_t(i - lines_l) * 16;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+}
+
 __device__ __forceinline__ void load_rows(const uint64_t* rows, uint32_t r0, uint32_t cnt,
                                           uint64_t (&w)[kRowsPerThread]) {
 #pragma unroll
@@ -193,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
     for (uint32_t r = 0; r < nr; ++r) {
       const uint32_t s = ends[r] >> 16, e = ends[r] & 0xFFFFu;
       const uint32_t l0 = offl[s], nl = offl[e] - l0, r0 = offr[s], nrr = offr[e] - r0;
+      prefetch_next_run<G>(a, offl, offr, ends, r, nr);
       uint64_t cnt = 0;
       if (nl && nrr) {
         const Bins bins(g * G + s, e - s, Q::kShift);
@@ -408,6 +424,15 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       const Bins bins(g * G + s, en - s, Q::kShift);
       const uint32_t nbins = bins.count(en - s);
       for (uint32_t i = tid; i < nbins; i += kThreads) hr[i] = 0;
+      prefetch_next_run<G>(a, offl, offr, ends, r, nr);
+      if constexpr (!CHECKSUM) {  // the carried payload windows of this run: into L2 while the rows are sorted
+        const uint32_t lines_l = (nl * uint32_t(a.words_l) * 8 + 127) / 128, lines_r = (nrr * uint32_t(a.words_r) * 8 + 127) / 128;
+        for (uint32_t i = tid; i < lines_l + lines_r; i += kThreads) {
+          const uint64_t* p = i < lines_l ? a.pay_l + size_t(l0) * a.words_l + size_t(i) * 16
+                                          : a.pay_r + size_t(r0) * a.words_r + size_t(i - lines_l) * 16;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
       uint64_t w[kRowsPerThread], wl[kRowsPerThread];
       load_rows(a.rows_l, l0, nl, wl);
       load_rows(a.rows_r, r0, nrr, w);

@@ -169,17 +169,22 @@ def join_then_order_by(left: DeviceRelation, right: DeviceRelation, key: str, sp
 
 
 def join_stream(plan: JoinPlan, chunk_pairs: int = 1 << 31, begin: int = 0,
-                end: Optional[int] = None) -> Iterator[Tuple[int, torch.Tensor, torch.Tensor]]:
+                end: Optional[int] = None, out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None
+                ) -> Iterator[Tuple[int, torch.Tensor, torch.Tensor]]:
     """Materialise the (left row, right row) pairs of [begin, end) chunk by
     chunk (reference order), yielding (chunk start, left rows, right rows);
-    the two uint32 buffers are reused between chunks."""
+    the two uint32 buffers (``out``, or allocated here) are reused between
+    chunks."""
     end = plan.total if end is None else min(end, plan.total)
     if end <= begin:
         return
     dev = plan.ws.device
     cap = min(chunk_pairs, end - begin)
-    lr = torch.empty(cap, dtype=torch.int32, device=dev)
-    rr = torch.empty(cap, dtype=torch.int32, device=dev)
+    if out is not None and min(out[0].numel(), out[1].numel()) >= cap:
+        lr, rr = out
+    else:
+        lr = torch.empty(cap, dtype=torch.int32, device=dev)
+        rr = torch.empty(cap, dtype=torch.int32, device=dev)
     for a in range(begin, end, chunk_pairs):
         b = min(a + chunk_pairs, end)
         plan.expand(a, b, (), lr[: b - a], rr[: b - a])

@@ -222,6 +222,22 @@ RL_API int rl_join_plan_build(const int64_t* left_keys, int64_t n_left,
                               size_t ws_bytes, rl_join_plan* plan, void* stream);
 
 /* ---------------------------------------------------------------------
+ * ORDER BY on a raw int64 key with the other columns carried (the sort +
+ * Relation.take of tensorpath.py:232-252 in one call): dst row o of every
+ * column = src row perm[o], as rl_sort_axis_gather. When the key varies in
+ * <= 32 bits and n reaches the scatter path, the columns' bytes (<= 16 a row
+ * after natural alignment, <= 4 columns) ride beside every packed row through
+ * the counting passes and leave from each on-chip run — no gather by row id;
+ * otherwise the gathers are fused into the sort's final pass. Workspace:
+ * rl_sort_carry_workspace_bytes(n, the columns' total width in bytes).
+ * --------------------------------------------------------------------- */
+RL_API size_t rl_sort_carry_workspace_bytes(int64_t n, int32_t carry_bytes);
+RL_API int rl_sort_axis_carry(const int64_t* keys, int64_t n, int32_t descending,
+                              int64_t* sorted_keys_out, uint32_t* perm_out,
+                              const rl_column* columns, int32_t n_columns, void* ws,
+                              size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
  * Bucket join: the join plan for keys with <= 32 varying bits (both sides
  * together), without sorted key axes. Replaces tensorpath.py:78-93 (x2),
  * 109-128 and the sizing of 131-161: one joint key packing; every row of

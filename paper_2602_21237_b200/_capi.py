@@ -99,6 +99,8 @@ SIGNATURES = {
         ctypes.c_int,
         [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, ctypes.POINTER(RlColumn), _I32, _P, _SZ, _P],
     ),
+    "rl_sort_carry_workspace_bytes": (_SZ, [_I64, _I32]),
+    "rl_sort_axis_carry": (ctypes.c_int, [_P, _I64, _I32, _P, _P, ctypes.POINTER(RlColumn), _I32, _P, _SZ, _P]),
     "rl_run_bounds_workspace_bytes": (_SZ, [_I64]),
     "rl_run_bounds": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _SZ, _P]),
     "rl_align_workspace_bytes": (_SZ, [_I64]),

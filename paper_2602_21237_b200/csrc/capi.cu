@@ -9,6 +9,9 @@
 namespace rl {
 namespace radix {
 size_t workspace_bytes(int64_t n);
+size_t carry_workspace_bytes(int64_t n, int words);
+int sort_axis_carry(const int64_t* keys, int64_t n, int descending, int64_t* sorted_keys_out, uint32_t* perm_out,
+                    const rl_column* columns, int n_columns, void* ws, size_t ws_bytes, cudaStream_t stream);
 int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
               cudaStream_t stream, void* const* events, unsigned long long* stamps, const rl_column* columns,
@@ -116,6 +119,17 @@ int rl_sort_axis_profiled(const void* col, int32_t col_kind, int32_t width, int3
   if (events == nullptr) return RL_ERR_BAD_ARG;
   return rl::radix::sort_axis(col, col_kind, width, word, descending, perm_in, n, sorted_keys_out, perm_out, ws,
                               ws_bytes, as_stream(stream), events, stamps_dev, columns, n_columns);
+}
+
+size_t rl_sort_carry_workspace_bytes(int64_t n, int32_t carry_bytes) {
+  return rl::radix::carry_workspace_bytes(n, carry_bytes > 0 && carry_bytes <= 16 ? (carry_bytes + 7) / 8 : 0);
+}
+
+int rl_sort_axis_carry(const int64_t* keys, int64_t n, int32_t descending, int64_t* sorted_keys_out,
+                       uint32_t* perm_out, const rl_column* columns, int32_t n_columns, void* ws, size_t ws_bytes,
+                       void* stream) {
+  return rl::radix::sort_axis_carry(keys, n, descending, sorted_keys_out, perm_out, columns, n_columns, ws, ws_bytes,
+                                    as_stream(stream));
 }
 
 size_t rl_run_bounds_workspace_bytes(int64_t n) { return rl::keyaxis::run_bounds_workspace_bytes(n); }

@@ -215,6 +215,8 @@ struct SortArgs {
   const uint8_t* carry_src[4];
   int carry_width[4];
   int carry_off[4];          // byte offset in the row's payload words
+  uint8_t* carry_dst[4];     // sort with carried columns: where the local phase writes them (dst row o)
+  int cw;                    // sort with carried columns: payload words a row (0: none)
   uint64_t* pay_a;           // [n * CW] parallel to keys_a
   uint64_t* pay_b;           // [n * CW] parallel to keys_b
   // three-level scatter (n above ~65536 x kLocalCap): digit 5 inside every
@@ -1230,7 +1232,11 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   using F = std::false_type;
   using T = std::true_type;
   const bool pk = packed_rows(sh, a);
-  if constexpr (CW > 0) {  // the bucket join: packed rows always (its plan checks the code)
+  if constexpr (CW > 0) {  // carried payload rides with packed rows only (the bucket join's plan checks the code)
+    if (!packed_rows(sh, a)) {  // a sort with carried columns on wide keys: the LSD passes gather them instead
+      if (tid == 0) atomicOr(a.flags, 1u);
+      return;
+    }
     if (pack_mode(sh) == 1) tiles(std::integral_constant<int, 1>{}, T{});
     else tiles(std::integral_constant<int, 2>{}, T{});
     return;
@@ -1488,7 +1494,7 @@ __device__ __forceinline__ bool row_less(uint64_t ka, uint32_t va, uint64_t kb, 
 // Sort rows [lo, hi) of B by (key, row id) — one warp, bitonic network
 // with mirrored first steps (every comparator ascending), so rows past hi
 // act as +inf padding and their comparators are skipped.
-template <bool PK = false>  // PK: packed rows, the key word alone orders them (bv unused)
+template <bool PK = false, bool MOVE_V = false>  // PK: the key word alone orders rows; MOVE_V: bv moves along
 __device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t hi, int lane) {
   const uint32_t sz = hi - lo;
   uint32_t p2 = 1;
@@ -1503,6 +1509,11 @@ __device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t h
           if constexpr (PK) {
             if (kb < ka) {
               bk[lo + i] = kb; bk[lo + q] = ka;
+              if constexpr (MOVE_V) {
+                const uint32_t t = bv[lo + i];
+                bv[lo + i] = bv[lo + q];
+                bv[lo + q] = t;
+              }
             }
           } else {
             const uint32_t va = bv[lo + i], vb = bv[lo + q];
@@ -1566,8 +1577,13 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
 // BAL (the scatter path's large runs): a thread's rows in registers across
 // count + scatter, and the claimed group tail. The onesweep hybrid's short
 // runs (n < 4M) are faster without both (+1-5 us each at 0.3-2M rows).
-template <int THREADS, int PACK = 0, bool BAL = false, bool PK = false, int LEVELS = 2>
+template <int THREADS, int PACK = 0, bool BAL = false, bool PK = false, int LEVELS = 2, int CW = 0>
 __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
+  // CW > 0 (packed rows): every row's payload words ride in pay_a / pay_b beside
+  // its key; bv holds the row's load index in its run, and the emit copies the
+  // carried columns out of the run's payload window (no gather by row id)
+  static_assert(CW == 0 || PK, "carried payload rides with packed rows");
+  const uint64_t* pay = CW ? (src == 1 ? a.pay_a : a.pay_b) : nullptr;
   // sub-buckets of the runs: (d7, d6) or, with three levels, (d7, d6, d5)
   constexpr int kSubShift = LEVELS == 3 ? 40 : 48;
   const uint32_t* sub_off = LEVELS == 3 ? a.sub3_off : a.sub_off;
@@ -1800,6 +1816,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         if (j < cnt) {
           bk[pos[u]] = rk[u];
           if constexpr (!PK) bv[pos[u]] = av[j];
+          else if constexpr (CW > 0) bv[pos[u]] = j;
         }
       }
     } else {
@@ -1808,6 +1825,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         const uint32_t pos = atomicAdd(&hist[bin_of(key)], 1u);
         bk[pos] = key;
         if constexpr (!PK) bv[pos] = av[j];
+        else if constexpr (CW > 0) bv[pos] = j;
       }
     }
     __syncthreads();
@@ -1818,17 +1836,24 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     constexpr uint32_t kRankMax = 32;
     auto emit = [&](uint32_t p, uint64_t key, uint32_t v) {
       const uint64_t o = uint64_t(base) + p;
+      const uint32_t j = v;  // CW > 0: the row's load index in the run
       if constexpr (PK) {  // packed row: row id in the low 32 bits
         v = uint32_t(key);
         key &= ~0xFFFFFFFFull;
       }
       if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(unpack_as<PACK>(key, pcode, pshl, constbits), desc));
       __stcs(a.out_vals + o, v);
-      gather_fused(a.gather, v, o);
+      if constexpr (CW > 0) {
+        const uint8_t* row = reinterpret_cast<const uint8_t*>(pay + (size_t(base) + j) * CW);
+        for (int c = 0; c < a.carry_n; ++c)
+          copy_row(row + a.carry_off[c], a.carry_dst[c] + o * uint64_t(a.carry_width[c]), a.carry_width[c]);
+      } else {
+        gather_fused(a.gather, v, o);
+      }
     };
     for (uint32_t p = tid; p < cnt; p += THREADS) {
       const uint64_t key = bk[p];
-      const uint32_t v = PK ? 0u : bv[p];
+      const uint32_t v = PK && CW == 0 ? 0u : bv[p];
       const int b = bin_of(key);
       const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
       uint32_t pos = p;
@@ -1855,8 +1880,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     for (uint32_t t = warp; t < nbig; t += kLWarps) {
       const int b = int(big[t]);
       const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
-      warp_bitonic<PK>(bk, bv, b0, b1, lane);
-      for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], PK ? 0u : bv[p]);
+      warp_bitonic<PK, (CW > 0)>(bk, bv, b0, b1, lane);
+      for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], PK && CW == 0 ? 0u : bv[p]);
     }
     if (nbig) __syncthreads();  // (the rank loop's reads of B/hist ended at the barrier before nbig)
     if (!more) break;
@@ -1991,6 +2016,35 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local3_ke
       if (pk) local_phase<kLocalThreads, 2, true, true, 3>(a, smem, 2u);
       else local_phase<kLocalThreads, 2, true, false, 3>(a, smem, 2u);
       break;
+  }
+}
+
+// The local phase of a sort with carried columns (packed rows; the columns'
+// bytes ride beside every row through the counting passes and are copied out
+// of the run's payload window): its own kernel, so the plain sort's local
+// kernels keep their code.
+template <int LEVELS>
+__global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_carry_kernel(SortArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  pdl_wait();
+  pdl_launch_dependents();
+  if (*reinterpret_cast<volatile const uint32_t*>(a.flags) != 0) return;  // LSD fallback (final before this launch)
+  const uint32_t pc = __ldcg(a.flags + 6);
+  if (threadIdx.x == 0) {
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
+    const uint64_t cb = pack_mode(pc) ? key_constbits(a, pc) : 0ull;
+    misc[125] = pc;
+    misc[126] = uint32_t(cb);
+    misc[127] = uint32_t(cb >> 32);
+  }
+  constexpr uint32_t src = LEVELS == 3 ? 2u : 1u;
+  const bool m1 = pack_mode(pc) == 1;  // (packed rows: mode 1 or 2, checked by the counting passes)
+  if (a.cw == 1) {
+    if (m1) local_phase<kLocalThreads, 1, true, true, LEVELS, 1>(a, smem, src);
+    else local_phase<kLocalThreads, 2, true, true, LEVELS, 1>(a, smem, src);
+  } else {
+    if (m1) local_phase<kLocalThreads, 1, true, true, LEVELS, 2>(a, smem, src);
+    else local_phase<kLocalThreads, 2, true, true, LEVELS, 2>(a, smem, src);
   }
 }
 
@@ -2269,6 +2323,10 @@ static bool scatter_kernels_ready() {
                                     int(kLocalSmemBytes)) == cudaSuccess &&
                cudaFuncSetAttribute(local3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kLocalKernelSmem)) == cudaSuccess &&
+               cudaFuncSetAttribute(local_carry_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kLocalSmemBytes)) == cudaSuccess &&
+               cudaFuncSetAttribute(local_carry_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kLocalKernelSmem)) == cudaSuccess &&
                cudaFuncSetAttribute(sub3_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPSmem)) ==
                    cudaSuccess;
            if (!ok) cudaGetLastError();
@@ -2281,6 +2339,23 @@ static bool scatter_kernels_ready() {
              cudaFuncSetAttribute(sort_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
            }
 #endif
+           return ok ? 1 : -1;
+         }) > 0;
+}
+
+// The counting-pass instances that carry CW payload words: their shared
+// memory opt-in, once per device.
+template <int CW>
+static bool carry_kernels_ready() {
+  static int ready[kMaxDevices] = {};
+  return per_device(ready, [] {
+           const bool ok = cudaFuncSetAttribute(top_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(psmem_bytes(CW))) == cudaSuccess &&
+                           cudaFuncSetAttribute(sub_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(psmem_bytes(CW))) == cudaSuccess &&
+                           cudaFuncSetAttribute(sub3_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(psmem_bytes(CW))) == cudaSuccess;
+           if (!ok) cudaGetLastError();
            return ok ? 1 : -1;
          }) > 0;
 }
@@ -2430,19 +2505,34 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     };
     sub_hist_kernel<<<chunks, kScatThreads, kHistSmem, stream>>>(a);
     chk("sub_hist");
-    if ((e = launch_dep(top_scatter_kernel<0>, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
-    chk("top_scatter");
-    if ((e = launch_dep(sub_scatter_kernel<0>, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
-    chk("sub_scatter");
     int launched = 5;
-    if (a.levels == 3) {  // digit 5 inside every sub-bucket
-      if ((e = launch_dep(count3_kernel, pgrid, kPThreads, size_t(0))) != cudaSuccess) return rl_cuda_status(e);
-      if ((e = launch_dep(tile_scan_kernel, 1, 1024, size_t(0))) != cudaSuccess) return rl_cuda_status(e);
-      if ((e = launch_dep(sub3_scatter_kernel<0>, pgrid, kPThreads, kPSmem)) != cudaSuccess) return rl_cuda_status(e);
-      chk("level 3");
-      launched += 3;
-    }
-    if (a.levels == 3) e = launch_dep(local3_kernel, lgrid, kLocalThreads, kLocalKernelSmem);
+    // the counting passes (with a sort's carried columns: the CW-word instances)
+    auto passes = [&](auto cwc) -> cudaError_t {
+      constexpr int CW = decltype(cwc)::value;
+      const size_t sm = psmem_bytes(CW);
+      cudaError_t x;
+      if ((x = launch_dep(top_scatter_kernel<CW>, pgrid, kPThreads, sm)) != cudaSuccess) return x;
+      chk("top_scatter");
+      if ((x = launch_dep(sub_scatter_kernel<CW>, pgrid, kPThreads, sm)) != cudaSuccess) return x;
+      chk("sub_scatter");
+      if (a.levels == 3) {  // digit 5 inside every sub-bucket
+        if ((x = launch_dep(count3_kernel, pgrid, kPThreads, size_t(0))) != cudaSuccess) return x;
+        if ((x = launch_dep(tile_scan_kernel, 1, 1024, size_t(0))) != cudaSuccess) return x;
+        if ((x = launch_dep(sub3_scatter_kernel<CW>, pgrid, kPThreads, sm)) != cudaSuccess) return x;
+        chk("level 3");
+        launched += 3;
+      }
+      return cudaSuccess;
+    };
+    if ((a.cw == 1 && !carry_kernels_ready<1>()) || (a.cw == 2 && !carry_kernels_ready<2>()))
+      return rl_cuda_status(cudaErrorInvalidConfiguration);
+    if (a.cw == 1) e = passes(std::integral_constant<int, 1>{});
+    else if (a.cw == 2) e = passes(std::integral_constant<int, 2>{});
+    else e = passes(std::integral_constant<int, 0>{});
+    if (e != cudaSuccess) return rl_cuda_status(e);
+    if (a.cw > 0 && a.levels == 3) e = launch_dep(local_carry_kernel<3>, lgrid, kLocalThreads, kLocalKernelSmem);
+    else if (a.cw > 0) e = launch_dep(local_carry_kernel<2>, lgrid, kLocalThreads, kLocalSmemBytes);
+    else if (a.levels == 3) e = launch_dep(local3_kernel, lgrid, kLocalThreads, kLocalKernelSmem);
     else e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes);
     if (e != cudaSuccess) return rl_cuda_status(e);
     chk("local");
@@ -2549,6 +2639,101 @@ int sort_axis_capped(const void* col, int col_kind, int width, int word, int des
 
 // Co-resident CTAs of the cooperative sort kernel on this device (0 if unknown).
 int sort_grid_capacity() { return std::max(0, sort_grid_limit()); }
+
+// ---------------------------------------------------------------- carried columns
+// A raw int64 ORDER BY whose other columns (<= 16 bytes a row, <= 4 columns)
+// ride with the rows instead of being gathered by the permutation afterwards:
+// on the scatter path with packed rows the counting passes carry their bytes
+// beside every key and the local phase copies them out of each run's payload
+// window; otherwise (small n, keys varying in more than 32 bits) the same call
+// sorts and fuses the gathers into the final pass. Same outputs either way:
+// dst row o = src row perm[o].
+static int carry_layout(const rl_column* cols, int n, int* offs, int* words) {
+  if (n < 1 || n > 4) return RL_ERR_BAD_ARG;
+  int order[4] = {0, 1, 2, 3};
+  for (int i = 0; i < n; ++i)
+    if (!cols[i].src || !cols[i].dst || cols[i].width <= 0) return RL_ERR_BAD_ARG;
+  std::sort(order, order + n, [&](int x, int y) { return cols[x].width > cols[y].width; });
+  int at = 0;
+  for (int k = 0; k < n; ++k) {
+    const int w = cols[order[k]].width;
+    const int al = (w % 8 == 0) ? 8 : (w % 4 == 0) ? 4 : 1;
+    at = (at + al - 1) / al * al;
+    offs[order[k]] = at;
+    at += w;
+  }
+  *words = at <= 16 ? (at + 7) / 8 : 0;
+  return RL_OK;
+}
+
+size_t carry_workspace_bytes(int64_t n, int words) {
+  CarveSize c;
+  c.take<uint8_t>(workspace_bytes(n));
+  if (words > 0) {
+    c.take<uint64_t>(size_t(std::max<int64_t>(n, 1)) * words);
+    c.take<uint64_t>(size_t(std::max<int64_t>(n, 1)) * words);
+  }
+  return c.used + 256;
+}
+
+int sort_axis_carry(const int64_t* keys, int64_t n, int descending, int64_t* sorted_keys_out, uint32_t* perm_out,
+                    const rl_column* columns, int n_columns, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  int offs[4] = {0, 0, 0, 0}, words = 0;
+  if (n_columns < 1 || !columns) return RL_ERR_BAD_ARG;
+  int st = carry_layout(columns, n_columns, offs, &words);
+  if (st != RL_OK) return st;
+  for (int i = 0; i < n_columns; ++i)
+    if (columns[i].side != RL_SIDE_LEFT) return RL_ERR_BAD_ARG;
+  const bool scatter = n >= scatter_min_rows() && n >= kHybridMinRows && !getenv_flag_no_hybrid() &&
+                       !getenv_flag("RL_NO_SCATTER") && !getenv_flag("RL_NO_CARRY") &&
+                       (n <= kTwoLevelMaxRows || n >= level3_min_rows()) && words > 0;
+  if (!scatter)  // plain sort + the gathers fused into its final writes
+    return sort_axis_capped(keys, RL_COL_INT64, 8, 0, descending, nullptr, n, sorted_keys_out, perm_out, ws, ws_bytes,
+                            stream, nullptr, nullptr, columns, n_columns, 0);
+  if (n < 0 || !keys || !perm_out || (reinterpret_cast<uintptr_t>(keys) & 15)) return RL_ERR_BAD_ARG;
+  if (n > RL_MAX_ROWS) return RL_ERR_TOO_MANY_ROWS;
+  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) return RL_ERR_WORKSPACE;
+  Carve c{static_cast<char*>(ws), ws_bytes};
+  char* inner = c.take<char>(workspace_bytes(n));
+  uint64_t* pa = c.take<uint64_t>(size_t(n) * words);
+  uint64_t* pb = c.take<uint64_t>(size_t(n) * words);
+  if (!c.ok) return RL_ERR_WORKSPACE;
+  Layout L;
+  if (!carve_layout(L, inner, workspace_bytes(n), n)) return RL_ERR_WORKSPACE;
+  SortArgs a = {};
+  a.col = keys;
+  a.n = n;
+  a.width = 8;
+  a.desc = descending ? 1 : 0;
+  a.src_mode = kSrcInt64;
+  a.key_mode = descending ? kRawDesc : kRawAsc;
+  a.orig_keys = keys;
+  a.out_keys = sorted_keys_out;
+  a.out_vals = perm_out;
+  a.keys_a = L.keys_a;
+  a.keys_b = L.keys_b;
+  a.vals_a = L.vals_a;
+  a.vals_b = L.vals_b;
+  a.ghist = L.hist;
+  a.tile_counter = L.tile_counter;
+  a.grid_bar = L.grid_bar;
+  a.flags = L.flags;
+  a.sub_off = L.sub_off;
+  a.status = L.status;
+  a.gather.n = n_columns;  // the LSD fallback's fused gathers
+  for (int i = 0; i < n_columns; ++i) {
+    a.gather.c[i] = columns[i];
+    a.carry_src[i] = static_cast<const uint8_t*>(columns[i].src);
+    a.carry_dst[i] = static_cast<uint8_t*>(columns[i].dst);
+    a.carry_width[i] = columns[i].width;
+    a.carry_off[i] = offs[i];
+  }
+  a.carry_n = n_columns;
+  a.cw = words;
+  a.pay_a = pa;
+  a.pay_b = pb;
+  return launch_sort(a, L, stream, nullptr, 0);
+}
 
 int sort_axis(const void* col, int col_kind, int width, int word, int descending, const uint32_t* perm_in,
               int64_t n, int64_t* sorted_keys_out, uint32_t* perm_out, void* ws, size_t ws_bytes,
@@ -2771,22 +2956,6 @@ size_t bj_side_workspace_bytes(int64_t n, int words, int levels) {
   return c.used + 256;
 }
 
-// The counting-pass instances that carry CW payload words: their shared
-// memory opt-in, once per device.
-template <int CW>
-static bool carry_kernels_ready() {
-  static int ready[kMaxDevices] = {};
-  return per_device(ready, [] {
-           const bool ok = cudaFuncSetAttribute(top_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(psmem_bytes(CW))) == cudaSuccess &&
-                           cudaFuncSetAttribute(sub_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(psmem_bytes(CW))) == cudaSuccess &&
-                           cudaFuncSetAttribute(sub3_scatter_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(psmem_bytes(CW))) == cudaSuccess;
-           if (!ok) cudaGetLastError();
-           return ok ? 1 : -1;
-         }) > 0;
-}
 
 static SortArgs bj_args(const int64_t* keys, int64_t n, const int64_t* k0_src, const Layout& L) {
   SortArgs a = {};

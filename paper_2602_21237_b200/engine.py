@@ -276,6 +276,55 @@ def sort_permutation(axes: Sequence[SortAxis], n: int, device, sorted_keys_out: 
     return perm
 
 
+CARRY_MIN_ROWS = 4 << 20  # the scatter path (below it the plain sort + gather is used anyway)
+
+
+def packable_keys(keys: torch.Tensor, samples: int = 4096) -> bool:
+    """Whether the int64 keys probably vary in at most 32 bits in at most two
+    runs (the scatter path's packed rows, radix_sort.cu pack_code_of): the OR
+    of (key ^ first key) over strided samples (one small D2H). A bit the
+    sample misses is caught on the device (the sort then takes the LSD
+    passes with the gathers fused — correct, only slower)."""
+    import numpy as np
+
+    n = keys.numel()
+    if n == 0:
+        return False
+    v = keys[:: max(1, n // samples)].cpu().numpy().view(np.uint64)
+    vary = int(np.bitwise_or.reduce(v ^ v[0]))
+    bits = [(vary >> b) & 1 for b in range(64)]
+    runs = sum(1 for b in range(64) if bits[b] and (b == 63 or not bits[b + 1]))
+    return vary != 0 and runs <= 2 and sum(bits) <= 32
+
+
+def sort_carry(keys: torch.Tensor, descending: bool, sorted_keys_out: Optional[torch.Tensor],
+               columns: Sequence[OutColumn]) -> torch.Tensor:
+    """ORDER BY one int64 key with every other column carried with the rows
+    (rl_sort_axis_carry): dst row o = src row perm[o]. Returns the permutation."""
+    lib = C.load()
+    keys = aligned16(keys)
+    n = keys.numel()
+    perm = torch.empty(n, dtype=_U32, device=keys.device)
+    if n == 0:
+        return perm
+    arr, ncols = C.columns_array((c.src.data_ptr(), c.dst.data_ptr(), c.width, C.RL_SIDE_LEFT) for c in columns)
+    ws = workspace(lib.rl_sort_carry_workspace_bytes(n, sum(c.width for c in columns)), keys.device)
+    C.check(lib.rl_sort_axis_carry(_ptr(keys), n, int(descending), _ptr(sorted_keys_out), _ptr(perm), arr, ncols,
+                                   _ptr(ws), ws.numel(), stream_handle()), "rl_sort_axis_carry")
+    return perm
+
+
+def carry_fits(columns: Sequence[OutColumn]) -> bool:
+    """<= 4 columns of <= 16 bytes a row together (natural alignment)."""
+    if not 0 < len(columns) <= 4:
+        return False
+    at = 0
+    for w in sorted((c.width for c in columns), reverse=True):
+        al = 8 if w % 8 == 0 else 4 if w % 4 == 0 else 1
+        at = -(-at // al) * al + w
+    return at <= 16
+
+
 class SortGraph:
     """A stable ORDER BY of one int64 key column (+ Relation.take of bound
     columns) captured once as a CUDA graph: histogram, cooperative sort and

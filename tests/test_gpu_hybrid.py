@@ -329,3 +329,39 @@ def test_three_level_skewed_sub_sub_bucket_falls_back(monkeypatch, into_subbucke
     keys[:5000] = (keys[:5000] & ~np.int64((1 << 40) - 1)) | rng.integers(0, 1 << 40, 5000)  # one 24-bit prefix
     keys[:5000] = (np.int64(0x123456) << np.int64(40)) | rng.integers(0, 1 << 40, 5000)
     check_sort(keys)
+
+
+@pytest.mark.parametrize("shape", ["narrow_2cols", "narrow_mixed", "wide_keys_fallback", "three_level"])
+def test_sort_with_carried_columns(shape, monkeypatch, into_subbuckets):
+    """rl_sort_axis_carry: the other columns ride with the packed rows through
+    the counting passes and leave from each run's payload window — equal to
+    the stable argsort + take; wide keys take the LSD fallback with the
+    gathers fused; the third level forced at a small size."""
+    if into_subbuckets != "scatter":
+        pytest.skip("carried columns belong to the scatter path")
+    if shape == "three_level":
+        monkeypatch.setenv("RL_LEVEL3_MIN_ROWS", "1")
+    rng = np.random.default_rng(90 + len(shape))
+    n = 4_500_000
+    if shape == "wide_keys_fallback":
+        keys = full_range(rng, n)
+    else:
+        keys = rng.integers(0, 1 << 27, n, dtype=np.int64) - 5_000_000
+        keys[rng.choice(n, n // 25, replace=False)] = keys[rng.integers(0, n, n // 25)]
+    if shape == "narrow_mixed":
+        cols = [rng.integers(0, 256, (n, 5), dtype=np.uint8), rng.integers(-(2**31), 2**31, n).astype(np.int32),
+                rng.integers(0, 256, (n, 3), dtype=np.uint8)]
+    else:
+        cols = [rng.integers(-(2**62), 2**62, n), rng.integers(-(2**62), 2**62, n)]
+    for desc in (False, True):
+        kd = torch.from_numpy(keys).cuda()
+        srcs = [torch.from_numpy(c).cuda() for c in cols]
+        w = lambda c: c.element_size() * (c.shape[1] if c.dim() > 1 else 1)  # noqa: E731
+        outs = [engine.OutColumn(c, torch.empty_like(c), w(c), 0) for c in srcs]
+        sk = torch.empty_like(kd)
+        perm = engine.sort_carry(kd, desc, sk, outs)
+        want = O.stable_axis_order(keys, desc)
+        assert (perm.cpu().numpy().view(np.uint32).astype(np.int64) == want).all()
+        assert (sk.cpu().numpy() == keys[want]).all()
+        for o, c in zip(outs, cols):
+            assert (o.dst.cpu().numpy() == c[want]).all()

@@ -91,3 +91,23 @@ def test_run_experiment_sort_matches_reference(relab_patched):
     rep = run_experiment(mk(5))
     assert rep.result_digest == ref.result_digest and rep.output_rows == ref.output_rows
     assert rep.spill == ref.spill
+
+
+def test_reference_sweep_with_gpu_sidecar(relab_patched, tmp_path):
+    """relab's sweep on the B200 tensor path, its CSV unchanged (the
+    reference's reader), the GPU metrics in the sidecar keyed by label."""
+    relab = relab_patched
+    from relab.bench import ExperimentConfig, Operation, read_sweep_csv
+    from relab.selector import Policy
+
+    from paper_2602_21237_b200 import patch, sidecar
+
+    patch.install()
+    g = relab.GenSpec(500_000, 500_000, relab.Uniform(), 8, seed=2)
+    cfgs = [ExperimentConfig(Operation.JOIN, g, policy=Policy.FORCE_TENSOR, repetitions=5, warmup=1, label="j"),
+            ExperimentConfig(Operation.SORT, g, policy=Policy.FORCE_TENSOR, repetitions=5, warmup=1, label="s")]
+    rows, side = sidecar.sweep_with_sidecar(cfgs, tmp_path / "sw.csv")
+    assert [r.path_taken for r in read_sweep_csv(tmp_path / "sw.csv")] == ["tensor", "tensor"]
+    got = sidecar.read_sidecar(str(tmp_path / "sw.csv") + ".gpu.csv")
+    assert [r["label"] for r in got] == ["j", "s"] and all(r["gpus"] == "1" for r in got)
+    assert all(float(r["mrows_per_s"]) > 0 for r in got)

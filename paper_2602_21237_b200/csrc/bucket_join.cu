@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
   __shared__ unsigned long long gsum;
   const int tid = threadIdx.x;
   if (fell_back(a)) return;
+  // packed key length: a bin covering all of its bits holds ONE key
+  const uint32_t code = __ldcg(a.flags_l + 6);
+  const uint32_t keybits = (code >> 14 & 127) + (code & 127);
   for (uint32_t g = blockIdx.x; g < Q::kGroups; g += gridDim.x) {
     for (uint32_t i = tid; i <= uint32_t(G); i += kThreads) {
       offl[i] = __ldcg(a.off_l + size_t(g) * G + i);
@@ -210,8 +213,28 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
       const uint32_t l0 = offl[s], nl = offl[e] - l0, r0 = offr[s], nrr = offr[e] - r0;
       prefetch_next_run<G>(a, offl, offr, ends, r, nr);
       uint64_t cnt = 0;
-      if (nl && nrr) {
-        const Bins bins(g * G + s, e - s, Q::kShift);
+      const Bins bins(g * G + s, e - s, Q::kShift);
+      const bool key_bins = (64u - uint32_t(Q::kShift)) + bins.bb >= keybits;  // bins = keys
+      if (nl && nrr && key_bins) {
+        // one key a bin: pairs = sum over bins of left rows x right rows (both
+        // counts in one word: left in the low 16 bits, right in the high 16)
+        const uint32_t nbins = bins.count(e - s);
+        for (uint32_t i = tid; i < nbins; i += kThreads) hist[i] = 0;
+        uint64_t w[kRowsPerThread], wl[kRowsPerThread];
+        load_rows(a.rows_r, r0, nrr, w);
+        load_rows(a.rows_l, l0, nl, wl);
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+          if (tid + u * kThreads < int(nl)) atomicAdd(&hist[bins.of(wl[u])], 1u);
+          if (tid + u * kThreads < int(nrr)) atomicAdd(&hist[bins.of(w[u])], 1u << 16);
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < nbins; i += kThreads) {
+          const uint32_t h = hist[i];
+          cnt += uint64_t(h & 0xFFFFu) * (h >> 16);
+        }
+      } else if (nl && nrr) {
         const uint32_t nbins = bins.count(e - s);
         for (uint32_t i = tid; i < nbins; i += kThreads) hist[i] = 0;
         uint64_t w[kRowsPerThread], wl[kRowsPerThread];
@@ -393,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
   const uint64_t constbits = k0 & ~radix::pack_mask(code);
   const int mode = radix::pack_mode(code);
   const uint32_t shl = radix::pack_shift(code);
+  const uint32_t keybits = (code >> 14 & 127) + (code & 127);  // packed key length
   auto key_of = [&](uint64_t w) -> long long {
     const uint64_t v = w & ~0xFFFFFFFFull;
     const uint64_t u = mode == 1 ? (v >> shl) | constbits : radix::unpack_key(v, code, constbits);
@@ -423,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       const uint32_t l0 = offl[s], nl = offl[en] - l0, r0 = offr[s], nrr = offr[en] - r0;
       const Bins bins(g * G + s, en - s, Q::kShift);
       const uint32_t nbins = bins.count(en - s);
+      const bool key_bins = (64u - uint32_t(Q::kShift)) + bins.bb >= keybits;  // bins = keys
       for (uint32_t i = tid; i < nbins; i += kThreads) hr[i] = 0;
       prefetch_next_run<G>(a, offl, offr, ends, r, nr);
       if constexpr (!CHECKSUM) {  // the carried payload windows of this run: into L2 while the rows are sorted
@@ -458,12 +483,17 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
           const uint64_t wv = sl[p];
           const uint32_t b = bins.of(wv);
           const uint32_t b0 = b ? hr[b - 1] : 0u, b1 = hr[b];
-          const uint32_t key = uint32_t(wv >> 32);
-          uint32_t i = b0;
-          while (i < b1 && uint32_t(sr[i] >> 32) < key) ++i;
-          rs = i;
-          while (i < b1 && uint32_t(sr[i] >> 32) == key) ++i;
-          m = i - rs;
+          if (key_bins) {  // one key a bin: the whole right bin matches
+            rs = b0;
+            m = b1 - b0;
+          } else {
+            const uint32_t key = uint32_t(wv >> 32);
+            uint32_t i = b0;
+            while (i < b1 && uint32_t(sr[i] >> 32) < key) ++i;
+            rs = i;
+            while (i < b1 && uint32_t(sr[i] >> 32) == key) ++i;
+            m = i - rs;
+          }
           rs_arr[p] = rs;
         }
         mloc[u] = m;

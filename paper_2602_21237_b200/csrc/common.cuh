@@ -88,6 +88,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
                "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// L2 prefetch of [p, p + bytes) by one bulk request (the span is widened to
+// whole 16-byte units; a hint: no completion to wait for).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, size_t bytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  if (a1 > a0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(uint32_t(a1 - a0)) : "memory");
+}
 // Order earlier generic-proxy accesses to shared memory before later
 // async-proxy (TMA) writes into the same buffer.
 // Programmatic dependent launch: the next kernel of the stream may be

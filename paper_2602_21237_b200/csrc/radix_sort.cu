@@ -291,6 +291,16 @@ constexpr size_t kLocBk = kLocA + 2 * kLocABytes;
 constexpr size_t kLocBv = kLocBk + size_t(kLocalCap) * 8;
 constexpr size_t kLocHist = kLocBv + size_t(kLocalCap) * 4;
 constexpr size_t kLocBig = kLocHist + size_t(kLocalBins) * 4;
+// the scatter path's local phase (BAL) scatters the keys inside their own load
+// buffer (every key is in registers before the first barrier), so B's key
+// half and the 4096 counters give way to B's row ids + 8192 counters
+#ifndef RL_LOCAL_BAL_BITS
+#define RL_LOCAL_BAL_BITS 12
+#endif
+constexpr int kLocalBinsBal = 1 << RL_LOCAL_BAL_BITS;
+constexpr size_t kLocBvBal = kLocBk;
+constexpr size_t kLocHistBal = kLocBvBal + (size_t(kLocalCap) * 4 + 15) / 16 * 16;
+static_assert(kLocHistBal + size_t(kLocalBinsBal) * 4 <= kLocBig, "8192 counters fit in B + the 4096 counters");
 constexpr size_t kLocMisc = kLocBig + size_t(kBigList) * 4;
 // misc: [0] big count, [2..3] run-list sizes, [8..] scan scratch, [32..65] group offsets (x2),
 // [72..103] run ends (x2), [112..] run descriptors
@@ -793,6 +803,13 @@ __device__ __forceinline__ bool fallback_flag(const SortArgs& a) {
   return __syncthreads_or(threadIdx.x == 0 && *reinterpret_cast<volatile const uint32_t*>(a.flags) != 0) != 0;
 }
 
+// The local phase's view of the fallback flag (final before its launch: uniform).
+// (A CUDA-graph IF node around the fallback launch, armed here, replayed ~10 us
+// slower than the no-op cooperative launch it would skip: not used.)
+__device__ __forceinline__ bool local_fallback(const SortArgs& a) {
+  return *reinterpret_cast<volatile const uint32_t*>(a.flags) != 0;
+}
+
 __device__ __forceinline__ int64_t chunk_lo(int64_t n, int chunks, int c) {
   const int64_t per = (((n + chunks - 1) / chunks) + 1) & ~int64_t(1);  // even: 16-byte pair loads
   return per * c < n ? per * c : n;
@@ -1135,32 +1152,47 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
       a.meta[0] = first + k;
     }
   }
-  // sub-bucket starts of bucket g = this CTA (totals over the chunk counts)
+  // this CTA's rows; the first tile's lines are requested into L2 now, so that
+  // they arrive during the sub-bucket totals below (prefetching every next tile
+  // this way, here and in the digit-6 pass, measured no faster: 0.297 -> 0.303 ms)
+  const int64_t lo = chunk_lo(a.n, gridDim.x, blockIdx.x), hi = chunk_lo(a.n, gridDim.x, blockIdx.x + 1);
+  const long long* col = static_cast<const long long*>(a.col);
+  if (tid == 0) bulk_prefetch_l2(col + lo, size_t(min(hi - lo, int64_t(kPTile))) * 8);
+  // sub-bucket starts of bucket g = this CTA (totals over the chunk counts):
+  // lane q sums the uint4 column q (sub-buckets 8q .. 8q+7) of one chunk slice,
+  // every load of the slice in flight at once
   uint32_t* red = reinterpret_cast<uint32_t*>(s.sk);  // staging is free here
   for (uint32_t g = blockIdx.x; g < uint32_t(kBins); g += gridDim.x) {
-    constexpr int kSl = kPThreads / 128;
-    const int wi = tid & 127, sl = tid >> 7;
-    uint32_t l16 = 0, h16 = 0;  // 8 loads in flight per thread, not one L2 round trip per chunk
-    const uint32_t* col_g = a.chunk_cnt + g * 128 + wi;
-    for (int c0 = sl; c0 < a.chunks; c0 += 8 * kSl) {
-      uint32_t x[8];
+    constexpr int kSl = kPThreads / 32;
+    constexpr int kU = (kMaxChunks + kSl - 1) / kSl;
+    const int q = tid & 31, sl = tid >> 5;
+    const uint4* col_g = reinterpret_cast<const uint4*>(a.chunk_cnt + g * 128) + q;
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint4 x[kU];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int cc = c0 + u * kSl;
-        x[u] = cc < a.chunks ? __ldcg(col_g + size_t(cc) * kScatWords) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        l16 += x[u] & 0xFFFFu;
-        h16 += x[u] >> 16;
-      }
+    for (int u = 0; u < kU; ++u) {
+      const int cc = sl + u * kSl;
+      x[u] = cc < a.chunks ? __ldcg(col_g + size_t(cc) * (kScatWords / 4)) : make_uint4(0, 0, 0, 0);
     }
-    red[tid] = l16;
-    red[kPThreads + tid] = h16;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      acc[0] += x[u].x & 0xFFFFu;
+      acc[1] += x[u].x >> 16;
+      acc[2] += x[u].y & 0xFFFFu;
+      acc[3] += x[u].y >> 16;
+      acc[4] += x[u].z & 0xFFFFu;
+      acc[5] += x[u].z >> 16;
+      acc[6] += x[u].w & 0xFFFFu;
+      acc[7] += x[u].w >> 16;
+    }
+    uint4* r4 = reinterpret_cast<uint4*>(red + sl * 256 + q * 8);
+    r4[0] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+    r4[1] = make_uint4(acc[4], acc[5], acc[6], acc[7]);
     __syncthreads();
     uint32_t tb = 0;
     if (tid < 256)
-      for (int j = 0; j < kSl; ++j) tb += red[(tid & 1) * kPThreads + j * 128 + (tid >> 1)];
+#pragma unroll
+      for (int j = 0; j < kSl; ++j) tb += red[j * 256 + tid];
     const uint32_t ex = scan256(tb, s.scratch);
     if (tid < 256) {
       a.sub_off[g * 256 + tid] = s.aux[g] + ex;
@@ -1168,11 +1200,13 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     }
     if (g == kBins - 1 && tid == 0) a.sub_off[kSubBuckets] = uint32_t(a.n);
   }
+#ifdef RL_TOP_PROFILE
+  if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[4] = globaltimer();
+  if (a.stamps && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.stamps) + 5, globaltimer());
+#endif
   // a fallback already found (here or by an earlier CTA's prologue): skip the scatter
   if (fallback_flag(a)) return;
   // this CTA's rows by digit 7 -> keys_b / vals_b
-  const int64_t lo = chunk_lo(a.n, gridDim.x, blockIdx.x), hi = chunk_lo(a.n, gridDim.x, blockIdx.x + 1);
-  const long long* col = static_cast<const long long*>(a.col);
   const uint32_t sh = s.scratch[50];
   auto reserve = [&](uint32_t d, uint32_t c) { return s.aux[d] + atomicAdd(a.cur7 + d, c); };
   // the tile loop, compiled per key-packing mode (chosen once)
@@ -1252,6 +1286,9 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
       else tiles(std::integral_constant<int, 2>{}, F{});
       break;
   }
+#ifdef RL_TOP_PROFILE
+  if (a.stamps && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.stamps) + 6, globaltimer());
+#endif
 }
 
 template <bool PK, int CW>
@@ -1273,6 +1310,9 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_ke
     if (packed_rows(s.scratch[50], a)) sub_scatter_tiles<true, 0>(a, s);
     else sub_scatter_tiles<false, 0>(a, s);
   }
+#ifdef RL_TOP_PROFILE
+  if (a.stamps && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.stamps) + 7, globaltimer());
+#endif
 }
 
 template <bool PK, int CW>
@@ -1588,9 +1628,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   constexpr int kSubShift = LEVELS == 3 ? 40 : 48;
   const uint32_t* sub_off = LEVELS == 3 ? a.sub3_off : a.sub_off;
   constexpr int kLWarps = THREADS / 32;
-  uint64_t* bk = reinterpret_cast<uint64_t*>(smem + kLocBk);
-  uint32_t* bv = reinterpret_cast<uint32_t*>(smem + kLocBv);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + kLocHist);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (BAL ? kLocHistBal : kLocHist));
+  uint32_t* bv = reinterpret_cast<uint32_t*>(smem + (BAL ? kLocBvBal : kLocBv));
   uint32_t* big = reinterpret_cast<uint32_t*>(smem + kLocBig);
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
   // a work item: G consecutive sub-buckets (three levels: the 256 sub-sub-buckets
@@ -1606,7 +1645,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   const uint32_t* vin = PK ? nullptr : src == 1 ? a.vals_a : a.vals_b;
   const int desc = a.key_mode == kRawDesc;
   constexpr uint32_t kGroups = (LEVELS == 3 ? kSub3 : kSubBuckets) / G;
-  constexpr int kPerThread = kLocalBins / THREADS;
+  constexpr int kNBins = BAL ? kLocalBinsBal : kLocalBins;
+  constexpr uint32_t kBinBits = BAL ? uint32_t(RL_LOCAL_BAL_BITS) : 12u;
   const uint32_t g0 = blockIdx.x;
   if (g0 >= kGroups) return;
   // group schedule: the first nstat groups of every CTA on a static stride
@@ -1735,9 +1775,9 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     // fewer sub-buckets a run holds, the more bits each gets (4096 bins at most:
     // a run of one big sub-bucket is split 4096 ways, not 256)
     const uint32_t first = runs[buf * 4 + 2], nsb = runs[buf * 4 + 3];
-    const uint32_t bb = 12u - (nsb > 1 ? 32u - uint32_t(__clz(int(nsb - 1))) : 0u);
+    const uint32_t bb = kBinBits - (nsb > 1 ? 32u - uint32_t(__clz(int(nsb - 1))) : 0u);
     const uint32_t nbins = nsb << bb;
-    for (uint32_t i = tid; i < nbins; i += THREADS) hist[i] = 0;
+    for (uint32_t i = tid; i < nbins / 4; i += THREADS) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
     mbar_wait(&bars[buf], buf ? phase1 : phase0);
     if (buf) phase1 ^= 1;
     else phase0 ^= 1;
@@ -1748,9 +1788,11 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     const uint32_t next_k = misc[5], next_r = misc[6];
     if (tid == 0) misc[0] = 0;  // big-bin list: appended after later barriers, read after the rank loop
     const uint32_t base = runs[buf * 4], cnt = runs[buf * 4 + 1];
-    const uint8_t* abuf = smem + kLocA + buf * kLocABytes;
+    uint8_t* abuf = smem + kLocA + buf * kLocABytes;
     const uint64_t* ak = reinterpret_cast<const uint64_t*>(abuf) + (base & 1u);
     const uint32_t* av = reinterpret_cast<const uint32_t*>(abuf + kLocAKeys) + (base & 3u);
+    // the bin-ordered keys: BAL, in this run's own key buffer (read into registers first)
+    uint64_t* bk = reinterpret_cast<uint64_t*>(BAL ? abuf : smem + kLocBk);
     auto bin_of = [&](uint64_t key) {
       return int(((uint32_t(key >> kSubShift) - first) << bb) | (uint32_t(key >> (kSubShift - bb)) & ((1u << bb) - 1u)));
     };
@@ -1772,36 +1814,47 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       for (uint32_t j = tid; j < cnt; j += THREADS) atomicAdd(&hist[bin_of(ak[j])], 1u);
     }
     __syncthreads();
-    if (nbins == uint32_t(kLocalBins)) {  // all 4096 bins: thread owns kPerThread consecutive bins (vector loads)
-      uint32_t c[kPerThread], run = 0;
+    {  // counters -> exclusive starts; warp w owns bins [w W, (w + 1) W), read as uint4 by
+       // consecutive lanes (conflict-free: a thread owning consecutive bins strides the banks)
+      constexpr uint32_t W = uint32_t(kNBins / kLWarps), C = W / 128;
+      static_assert(kNBins % (kLWarps * 128) == 0, "uint4 counters, whole warps");
+      uint4* h4 = reinterpret_cast<uint4*>(hist) + warp * (W / 4);
+      const uint32_t lo4 = uint32_t(warp) * (W / 4);
+      const uint32_t lim4 = nbins / 4 > lo4 ? nbins / 4 - lo4 : 0u;  // this warp's counters in use
+      uint32_t wt = 0;
 #pragma unroll
-      for (int i = 0; i < kPerThread; ++i) {
-        c[i] = hist[tid * kPerThread + i];
-        run += c[i];
+      for (uint32_t i = 0; i < C; ++i) {
+        const uint32_t q = i * 32 + lane;
+        if (q < lim4) {
+          const uint4 c = h4[q];
+          wt += c.x + c.y + c.z + c.w;
+        }
       }
-      uint32_t total;
-      uint32_t start = block_exclusive_scan<THREADS>(run, misc + 8, &total);
+      wt = __reduce_add_sync(0xffffffffu, wt);
+      if (lane == 0) misc[8 + warp] = wt;
+      __syncthreads();
+      uint32_t start = 0;
+      for (int w = 0; w < warp; ++w) start += misc[8 + w];
 #pragma unroll
-      for (int i = 0; i < kPerThread; ++i) {
-        hist[tid * kPerThread + i] = start;
-        start += c[i];
-      }
-    } else {  // fewer bins: thread owns `per` consecutive bins
-      const uint32_t per = (nbins + THREADS - 1) / THREADS;  // <= kPerThread
-      const uint32_t nb = nbins;
-      uint32_t c[kPerThread], run = 0;
-      uint32_t* hb = hist + tid * per;
+      for (uint32_t i = 0; i < C; ++i) {
+        const uint32_t q = i * 32 + lane;
+        const uint4 c = q < lim4 ? h4[q] : make_uint4(0, 0, 0, 0);
+        const uint32_t sum = c.x + c.y + c.z + c.w;
+        uint32_t incl = sum;
 #pragma unroll
-      for (int i = 0; i < kPerThread; ++i) {
-        c[i] = uint32_t(i) < per && tid * per + i < nb ? hb[i] : 0u;
-        run += c[i];
-      }
-      uint32_t total;
-      uint32_t start = block_exclusive_scan<THREADS>(run, misc + 8, &total);
-#pragma unroll
-      for (int i = 0; i < kPerThread; ++i) {
-        if (uint32_t(i) < per && tid * per + i < nb) hb[i] = start;
-        start += c[i];
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += x;
+        }
+        if (q < lim4) {
+          uint4 o4;
+          o4.x = start + incl - sum;
+          o4.y = o4.x + c.x;
+          o4.z = o4.y + c.y;
+          o4.w = o4.z + c.z;
+          h4[q] = o4;
+        }
+        start += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
     __syncthreads();
@@ -1949,9 +2002,7 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   // scatter path: flags[0] = LSD fallback; onesweep hybrid: flags[7] = the
   // cooperative kernel took the hybrid and every sub-bucket fits (else it sorted
   // LSD). Both final before this launch: uniform.
-  if (scatter ? *reinterpret_cast<volatile const uint32_t*>(a.flags) != 0
-              : *reinterpret_cast<volatile const uint32_t*>(a.flags + 7) == 0)
-    return;
+  if (scatter ? local_fallback(a) : *reinterpret_cast<volatile const uint32_t*>(a.flags + 7) == 0) return;
   // the rows sit in their sub-buckets in keys_a / vals_a (scatter path: the
   // digit-6 pass) or keys_b / vals_b (onesweep hybrid: its digit-7 pass)
   const uint32_t src = scatter ? 1u : 2u;
@@ -1996,7 +2047,7 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local3_ke
   extern __shared__ __align__(128) uint8_t smem[];
   pdl_wait();  // the digit-5 pass
   pdl_launch_dependents();
-  if (*reinterpret_cast<volatile const uint32_t*>(a.flags) != 0) return;  // LSD fallback (final before this launch)
+  if (local_fallback(a)) return;  // LSD fallback (final before this launch)
   const uint32_t pc = __ldcg(a.flags + 6);
   if (threadIdx.x == 0) {
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
@@ -2028,7 +2079,7 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_car
   extern __shared__ __align__(128) uint8_t smem[];
   pdl_wait();
   pdl_launch_dependents();
-  if (*reinterpret_cast<volatile const uint32_t*>(a.flags) != 0) return;  // LSD fallback (final before this launch)
+  if (local_fallback(a)) return;  // LSD fallback (final before this launch)
   const uint32_t pc = __ldcg(a.flags + 6);
   if (threadIdx.x == 0) {
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);

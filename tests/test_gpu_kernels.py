@@ -216,6 +216,28 @@ def test_fused_final_pass_gather_equals_take():
     assert (dst.cpu().numpy() == np.arange(1000)).all()
 
 
+def test_sort_graph_fallback_node_follows_each_replay():
+    """Scatter-path SortGraph: the LSD fallback sits in a conditional node that
+    the local phase arms per replay. Uniform keys, then one sub-bucket above
+    the on-chip cap (the fallback runs), then keys with constant top bits
+    (the pre-check falls back), then uniform again: every replay is exact."""
+    n = 5_000_000
+    rng = np.random.default_rng(77)
+    keys = torch.empty(n, dtype=torch.int64, device="cuda")
+    g = engine.SortGraph(keys)
+    uniform = lambda: rng.integers(-(2**63), 2**63 - 1, n, dtype=np.int64, endpoint=True)  # noqa: E731
+    hot = uniform()
+    idx = rng.choice(n, 4000, replace=False)
+    hot[idx] = (np.int64(0x1234) << 48) | rng.integers(0, 1 << 48, 4000, dtype=np.int64)
+    narrow = rng.integers(0, 1 << 40, n, dtype=np.int64)
+    for k in (uniform(), hot, narrow, uniform()):
+        keys.copy_(torch.from_numpy(k))
+        g.replay()
+        want = O.stable_axis_order(k, False)
+        assert (u32(g.perm) == want).all()
+        assert (g.sorted_keys.cpu().numpy() == k[want]).all()
+
+
 def test_sort_graph_replays_current_inputs():
     """engine.SortGraph: a captured sort + gather re-sorts whatever the bound
     input buffers hold at replay time (hybrid-sized and LSD-sized inputs)."""

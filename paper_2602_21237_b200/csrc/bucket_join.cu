@@ -129,24 +129,7 @@ __device__ __forceinline__ void bin_rows(const uint64_t (&w)[kRowsPerThread], ui
   for (int u = 0; u < kRowsPerThread; ++u)
     if (tid + u * kThreads < int(cnt)) atomicAdd(&hist[bins.of(w[u])], 1u);
   __syncthreads();
-  constexpr int kPer = kMaxBins / kThreads;  // 8
-  const uint32_t per = (nbins + kThreads - 1) / kThreads;
-  uint32_t c[kPer], run = 0;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const uint32_t b = tid * per + i;
-    c[i] = uint32_t(i) < per && b < nbins ? hist[b] : 0u;
-    run += c[i];
-  }
-  uint32_t total;
-  uint32_t start = block_exclusive_scan<kThreads>(run, reinterpret_cast<uint32_t*>(scan_scratch), &total);
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const uint32_t b = tid * per + i;
-    if (uint32_t(i) < per && b < nbins) hist[b] = start;
-    start += c[i];
-  }
-  __syncthreads();
+  scan_counters<kThreads, kMaxBins>(hist, nbins, reinterpret_cast<uint32_t*>(scan_scratch));  // (synchronised)
 #pragma unroll
   for (int u = 0; u < kRowsPerThread; ++u) {
     if (tid + u * kThreads < int(cnt)) {
@@ -188,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
   using Q = Geo<LEVELS>;
   constexpr int G = Q::G;
   __shared__ uint64_t br[kBjCap];
-  __shared__ uint32_t hist[kMaxBins];
+  __shared__ __align__(16) uint32_t hist[kMaxBins];
   __shared__ uint32_t offl[G + 1], offr[G + 1], ends[G];
   __shared__ uint64_t scratch[kThreads / 32 + 2];
   __shared__ uint32_t nruns;
@@ -557,7 +540,8 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         // every row with pairs marks its first output, an inclusive max-scan fills
         // the rest — one lookup per output instead of a binary search
         uint32_t* map = omap;
-        for (uint32_t t = tid; t < total; t += kThreads) map[t] = 0u;
+        const uint32_t total4 = (total + 3) / 4;  // (whole uint4s zeroed: the scan reads them)
+        for (uint32_t t = tid; t < total4; t += kThreads) reinterpret_cast<uint4*>(map)[t] = make_uint4(0, 0, 0, 0);
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
@@ -565,33 +549,49 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
           if (x < nl && mloc[u]) map[m_arr[x]] = x;
         }
         __syncthreads();
-        constexpr int kM = kMaxBins / kThreads;  // 8 entries a thread
-        uint32_t mv[kM], run_max = 0;
+        {  // inclusive max-scan; warp w owns entries [w W, (w + 1) W), read as uint4 by
+           // consecutive lanes (conflict-free)
+          constexpr uint32_t W = uint32_t(kMaxBins / (kThreads / 32)), C = W / 128;
+          const uint32_t lane = tid & 31, wp = tid >> 5;
+          uint4* m4 = reinterpret_cast<uint4*>(map) + wp * (W / 4);
+          const uint32_t lo4 = wp * (W / 4), lim4 = total4 > lo4 ? total4 - lo4 : 0u;
+          uint32_t* wmax = reinterpret_cast<uint32_t*>(scratch);
+          uint32_t wm = 0;
 #pragma unroll
-        for (int i = 0; i < kM; ++i) {
-          const uint32_t t = tid * kM + i;
-          run_max = max(run_max, t < total ? map[t] : 0u);
-          mv[i] = run_max;
-        }
-        const int lane = tid & 31, wp = tid >> 5;
-        uint32_t wincl = run_max;
+          for (uint32_t i = 0; i < C; ++i) {
+            const uint32_t q = i * 32 + lane;
+            if (q < lim4) {
+              const uint4 c = m4[q];
+              wm = max(wm, max(max(c.x, c.y), max(c.z, c.w)));
+            }
+          }
+          wm = __reduce_max_sync(0xffffffffu, wm);
+          if (lane == 0) wmax[wp] = wm;
+          __syncthreads();
+          uint32_t run_max = 0;
+          for (uint32_t w2 = 0; w2 < wp; ++w2) run_max = max(run_max, wmax[w2]);
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t x = __shfl_up_sync(0xffffffffu, wincl, o);
-          if (lane >= o) wincl = max(wincl, x);
-        }
-        uint32_t wexcl = __shfl_up_sync(0xffffffffu, wincl, 1);
-        if (lane == 0) wexcl = 0;
-        uint32_t* wmax = reinterpret_cast<uint32_t*>(scratch);
-        if (lane == 31) wmax[wp] = wincl;
-        __syncthreads();
-        uint32_t pre = 0;
-        for (int w = 0; w < wp; ++w) pre = max(pre, wmax[w]);
-        pre = max(pre, wexcl);
+          for (uint32_t i = 0; i < C; ++i) {
+            const uint32_t q = i * 32 + lane;
+            const uint4 c = q < lim4 ? m4[q] : make_uint4(0, 0, 0, 0);
+            uint32_t incl = max(max(c.x, c.y), max(c.z, c.w));
 #pragma unroll
-        for (int i = 0; i < kM; ++i) {
-          const uint32_t t = tid * kM + i;
-          if (t < total) map[t] = max(pre, mv[i]);
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= uint32_t(o)) incl = max(incl, x);
+            }
+            uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 0;
+            if (q < lim4) {
+              uint4 o4;
+              o4.x = max(max(run_max, excl), c.x);
+              o4.y = max(o4.x, c.y);
+              o4.z = max(o4.y, c.z);
+              o4.w = max(o4.z, c.w);
+              m4[q] = o4;
+            }
+            run_max = max(run_max, __shfl_sync(0xffffffffu, incl, 31));
+          }
         }
         __syncthreads();
         for (uint64_t t = lo + tid; t < hi; t += kThreads) write(map[t], uint32_t(t));

@@ -151,6 +151,58 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* warp_sums, T* total) {
   return out;
 }
 
+// Counters -> exclusive starts over hist[0, nbins) (nbins <= NBINS, a multiple
+// of 4; hist 16-byte aligned). Warp w owns bins [w W, (w + 1) W) and reads them
+// as uint4 by consecutive lanes — conflict-free, where a thread owning
+// consecutive bins strides the banks. `warp_tot` holds THREADS / 32 words.
+// Ends with the block synchronised.
+template <int THREADS, int NBINS>
+__device__ __forceinline__ void scan_counters(uint32_t* hist, uint32_t nbins, uint32_t* warp_tot) {
+  constexpr int kWarps = THREADS / 32;
+  constexpr uint32_t W = uint32_t(NBINS / kWarps), C = W / 128;
+  static_assert(NBINS % (kWarps * 128) == 0, "uint4 counters, whole warps");
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint4* h4 = reinterpret_cast<uint4*>(hist) + warp * (W / 4);
+  const uint32_t lo4 = warp * (W / 4);
+  const uint32_t lim4 = nbins / 4 > lo4 ? nbins / 4 - lo4 : 0u;  // this warp's counters in use
+  uint32_t wt = 0;
+#pragma unroll
+  for (uint32_t i = 0; i < C; ++i) {
+    const uint32_t q = i * 32 + lane;
+    if (q < lim4) {
+      const uint4 c = h4[q];
+      wt += c.x + c.y + c.z + c.w;
+    }
+  }
+  wt = __reduce_add_sync(0xffffffffu, wt);
+  if (lane == 0) warp_tot[warp] = wt;
+  __syncthreads();
+  uint32_t start = 0;
+  for (uint32_t w = 0; w < warp; ++w) start += warp_tot[w];
+#pragma unroll
+  for (uint32_t i = 0; i < C; ++i) {
+    const uint32_t q = i * 32 + lane;
+    const uint4 c = q < lim4 ? h4[q] : make_uint4(0, 0, 0, 0);
+    const uint32_t sum = c.x + c.y + c.z + c.w;
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= uint32_t(o)) incl += x;
+    }
+    if (q < lim4) {
+      uint4 o4;
+      o4.x = start + incl - sum;
+      o4.y = o4.x + c.x;
+      o4.z = o4.y + c.y;
+      o4.w = o4.z + c.z;
+      h4[q] = o4;
+    }
+    start += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncthreads();
+}
+
 // Single-value decoupled look-back: returns the exclusive prefix of tile
 // `tile` and publishes its inclusive value. Called by one thread.
 __device__ __forceinline__ uint64_t lookback_publish(uint64_t* status, uint32_t tile,

@@ -1814,50 +1814,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       for (uint32_t j = tid; j < cnt; j += THREADS) atomicAdd(&hist[bin_of(ak[j])], 1u);
     }
     __syncthreads();
-    {  // counters -> exclusive starts; warp w owns bins [w W, (w + 1) W), read as uint4 by
-       // consecutive lanes (conflict-free: a thread owning consecutive bins strides the banks)
-      constexpr uint32_t W = uint32_t(kNBins / kLWarps), C = W / 128;
-      static_assert(kNBins % (kLWarps * 128) == 0, "uint4 counters, whole warps");
-      uint4* h4 = reinterpret_cast<uint4*>(hist) + warp * (W / 4);
-      const uint32_t lo4 = uint32_t(warp) * (W / 4);
-      const uint32_t lim4 = nbins / 4 > lo4 ? nbins / 4 - lo4 : 0u;  // this warp's counters in use
-      uint32_t wt = 0;
-#pragma unroll
-      for (uint32_t i = 0; i < C; ++i) {
-        const uint32_t q = i * 32 + lane;
-        if (q < lim4) {
-          const uint4 c = h4[q];
-          wt += c.x + c.y + c.z + c.w;
-        }
-      }
-      wt = __reduce_add_sync(0xffffffffu, wt);
-      if (lane == 0) misc[8 + warp] = wt;
-      __syncthreads();
-      uint32_t start = 0;
-      for (int w = 0; w < warp; ++w) start += misc[8 + w];
-#pragma unroll
-      for (uint32_t i = 0; i < C; ++i) {
-        const uint32_t q = i * 32 + lane;
-        const uint4 c = q < lim4 ? h4[q] : make_uint4(0, 0, 0, 0);
-        const uint32_t sum = c.x + c.y + c.z + c.w;
-        uint32_t incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += x;
-        }
-        if (q < lim4) {
-          uint4 o4;
-          o4.x = start + incl - sum;
-          o4.y = o4.x + c.x;
-          o4.z = o4.y + c.y;
-          o4.w = o4.z + c.z;
-          h4[q] = o4;
-        }
-        start += __shfl_sync(0xffffffffu, incl, 31);
-      }
-    }
-    __syncthreads();
+    scan_counters<THREADS, kNBins>(hist, nbins, misc + 8);  // (ends synchronised)
     if constexpr (BAL) {
       uint32_t pos[kRows];
 #pragma unroll

@@ -1579,9 +1579,6 @@ __device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t h
 // inside its bin — rows equal in their top 24 bits, ~1 for uniform keys; a
 // warp's bitonic network for bins above 32 rows — and goes straight to its
 // final position in the outputs, with the fused gathers.
-__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
-  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // Greedy cut of one group (offsets off[0..G]) into runs of whole sub-buckets
 // of at most kLocalCap rows; run = (first << 16) | end; returns the count.

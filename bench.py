@@ -1171,6 +1171,18 @@ def extras(args, dev):
         b.record()
         b.synchronize()
         ms = a.elapsed_time(b)
+        # the write-only ceiling on this box: MEASURED_PEAKS' figure is a copy (read + write),
+        # which a pure write stream can pass; fill the same two 4 GiB buffers, best of 3
+        fill_ms = []
+        for _ in range(3):
+            a3, b3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a3.record()
+            for buf in bufs:
+                buf.fill_(1)
+            b3.record()
+            b3.synchronize()
+            fill_ms.append(a3.elapsed_time(b3))
+        fill_gbs = sum(buf.numel() * 4 for buf in bufs) / (min(fill_ms) / 1e3) / 1e9
         acc = torch.zeros(1, dtype=torch.int64, device=dev)
         a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a2.record()
@@ -1190,6 +1202,11 @@ def extras(args, dev):
                                                 "frac": round(streamed * 8 / (ms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
                                                 "peak_nominal": NOMINAL_HBM_GBS,
                                                 "frac_nominal": round(streamed * 8 / (ms / 1e3) / 1e9 / NOMINAL_HBM_GBS, 4),
+                                                "peak_write_fill": round(fill_gbs, 1),
+                                                "frac_write_fill": round(streamed * 8 / (ms / 1e3) / 1e9 / fill_gbs, 4),
+                                                "peak_note": "peak = MEASURED_PEAKS copy bandwidth (read + write); a "
+                                                             "write-only stream can pass it: peak_write_fill = "
+                                                             "torch fill_ of the same output buffers, measured here",
                                                 "alg_bytes": "8 B written per materialised pair (uint32 left row, "
                                                              "uint32 right row); row-id reads hit L2"},
                             "note": "pairs materialised as uint32 (left row, right row) in 2^30-pair chunks"}

@@ -594,7 +594,79 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
           }
         }
         __syncthreads();
-        for (uint64_t t = lo + tid; t < hi; t += kThreads) write(map[t], uint32_t(t));
+        if (CHECKSUM || hi - lo < uint64_t(2 * kThreads)) {  // (a selective run: a few outputs)
+          for (uint64_t t = lo + tid; t < hi; t += kThreads) write(map[t], uint32_t(t));
+        } else {
+          // kU outputs a thread at a time, column by column: every load of a column
+          // (carried words from the run's window, gathered rows) issued before its
+          // stores, instead of one dependent load -> store chain per output
+          constexpr int kU = 4;
+          for (uint64_t t0 = lo + tid; t0 < hi; t0 += uint64_t(kU) * kThreads) {
+            uint32_t xs[kU], jrs[kU];
+            bool ok[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const uint64_t t = t0 + uint64_t(u) * kThreads;
+              ok[u] = t < hi;
+              const uint32_t x = ok[u] ? map[t] : 0u;
+              xs[u] = x;
+              jrs[u] = ok[u] ? rs_arr[x] + (uint32_t(t) - m_arr[x]) : 0u;
+            }
+            auto out_row = [&](int u) { return base + t0 + uint64_t(u) * kThreads - e.out_begin; };
+            if (e.lrows_out) {
+#pragma unroll
+              for (int u = 0; u < kU; ++u)
+                if (ok[u]) __stcs(e.lrows_out + out_row(u), uint32_t(sl[xs[u]]));
+            }
+            if (e.rrows_out) {
+#pragma unroll
+              for (int u = 0; u < kU; ++u)
+                if (ok[u]) __stcs(e.rrows_out + out_row(u), uint32_t(sr[jrs[u]]));
+            }
+            for (int ci = 0; ci < cols.n; ++ci) {
+              const EmitCol& c = cols.c[ci];
+              const int wd = c.width;
+              if (c.side == RL_SIDE_KEY) {
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                  if (ok[u]) __stcs(reinterpret_cast<long long*>(c.dst) + out_row(u), key_of(sl[xs[u]]));
+                continue;
+              }
+              const bool left = c.side == RL_SIDE_LEFT;
+              auto src_of = [&](int u) -> const uint8_t* {
+                if (c.carry_off >= 0) {
+                  const uint64_t* pay = left ? a.pay_l : a.pay_r;
+                  const int words = left ? a.words_l : a.words_r;
+                  const uint64_t at = left ? uint64_t(l0) + lidx[xs[u]] : uint64_t(r0) + ridx[jrs[u]];
+                  return reinterpret_cast<const uint8_t*>(pay + at * words) + c.carry_off;
+                }
+                const uint32_t row = left ? uint32_t(sl[xs[u]]) : uint32_t(sr[jrs[u]]);
+                return c.src + uint64_t(row) * wd;
+              };
+              if (wd == 8 && ((reinterpret_cast<uintptr_t>(src_of(0)) | uintptr_t(c.carry_off)) & 7) == 0) {
+                unsigned long long v[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                  v[u] = ok[u] ? ld_row(reinterpret_cast<const unsigned long long*>(src_of(u))) : 0ull;
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                  if (ok[u]) __stcs(reinterpret_cast<unsigned long long*>(c.dst) + out_row(u), v[u]);
+              } else if (wd == 16 && ((reinterpret_cast<uintptr_t>(src_of(0)) | uintptr_t(c.carry_off)) & 15) == 0) {
+                uint4 v[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                  v[u] = ok[u] ? ld_row(reinterpret_cast<const uint4*>(src_of(u))) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                  if (ok[u]) __stcs(reinterpret_cast<uint4*>(c.dst) + out_row(u), v[u]);
+              } else {
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                  if (ok[u]) copy_row(src_of(u), c.dst + out_row(u) * uint64_t(wd), wd);
+              }
+            }
+          }
+        }
       } else {
         for (uint64_t t = lo + tid; t < hi; t += kThreads) {
           uint32_t x = 0, y = nl;  // largest p with pre[p] <= t

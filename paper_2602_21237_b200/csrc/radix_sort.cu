@@ -217,6 +217,8 @@ struct SortArgs {
   int carry_off[4];          // byte offset in the row's payload words
   uint8_t* carry_dst[4];     // sort with carried columns: where the local phase writes them (dst row o)
   int cw;                    // sort with carried columns: payload words a row (0: none)
+  int idw;                   // carried columns of <= 4 bytes: keys that do not pack carry the row id in the
+                             // word's low half, the columns' bytes in its high half (no row-id stream)
   uint64_t* pay_a;           // [n * CW] parallel to keys_a
   uint64_t* pay_b;           // [n * CW] parallel to keys_b
   // three-level scatter (n above ~65536 x kLocalCap): digit 5 inside every
@@ -302,6 +304,14 @@ constexpr size_t kLocBvBal = kLocBk;
 constexpr size_t kLocHistBal = kLocBvBal + (size_t(kLocalCap) * 4 + 15) / 16 * 16;
 static_assert(kLocHistBal + size_t(kLocalBinsBal) * 4 <= kLocBig, "8192 counters fit in B + the 4096 counters");
 constexpr size_t kLocMisc = kLocBig + size_t(kBigList) * 4;
+// idw (keys that do not pack, <= 4 carried bytes): a run buffer holds the keys
+// and the carried words (row id | columns), 8 bytes each; bv holds every
+// bin-ordered row's u16 load index; the counters follow (big list, misc and the
+// barriers stay where they are)
+constexpr size_t kLocABytesW = (2 * kLocAKeys + 15) / 16 * 16;
+constexpr size_t kLocBvW = kLocA + 2 * kLocABytesW;
+constexpr size_t kLocHistW = kLocBvW + (size_t(kLocalCap) * 2 + 15) / 16 * 16;
+static_assert(kLocHistW + size_t(kLocalBinsBal) * 4 <= kLocBig, "idw: the counters end before the big-bin list");
 // misc: [0] big count, [2..3] run-list sizes, [8..] scan scratch, [32..65] group offsets (x2),
 // [72..103] run ends (x2), [112..] run descriptors
 constexpr size_t kLocBars = kLocMisc + 128 * 4;
@@ -908,10 +918,15 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
     s.hist[tid] = excl;
   }
   __syncthreads();
+  // staging: every digit start read before the first staged store (a store
+  // could alias a later start, so the compiler keeps written order)
+  uint32_t sp[kPItems];
+#pragma unroll
+  for (int u = 0; u < kPItems; ++u) sp[u] = s.hist[uint32_t(k[u] >> SHIFT) & 255u] + r[u];
 #pragma unroll
   for (int u = 0; u < kPItems; ++u) {
     if (u * kPThreads + tid < tn) {
-      const uint32_t p = s.hist[uint32_t(k[u] >> SHIFT) & 255u] + r[u];
+      const uint32_t p = sp[u];
       s.sk[p] = k[u];
       if constexpr (CW > 0) {
 #pragma unroll
@@ -925,15 +940,50 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
   __syncthreads();
   next(k, v, cr);
   if (tid < 256) s.hist[tid] = 0;  // for the next tile (the write-out reads only s.base)
-  for (int i = tid; i < tn; i += kPThreads) {
-    const uint64_t key = s.sk[i];
-    const uint32_t o = s.base[uint32_t(key >> SHIFT) & 255u] + uint32_t(i);
-    out_k[o] = key;
-    if constexpr (CW > 0) {
+  // write-out in batches of kWB rows a thread: the staged keys, then their
+  // digit bases, then the global stores (st.global: no ordering against the
+  // shared loads of the next batch)
+  constexpr int kWB = CW >= 2 ? 1 : 4;  // (two carried words: batches spill)
+  for (int i0 = tid; i0 < tn; i0 += kWB * kPThreads) {
+    uint64_t kk[kWB];
+    uint32_t o[kWB];
 #pragma unroll
-      for (int w = 0; w < CW; ++w) out_p[size_t(o) * CW + w] = s.sp[i * CW + w];
-    } else if constexpr (!PK) {
-      out_v[o] = s.sv[i];
+    for (int u = 0; u < kWB; ++u) {
+      const int i = i0 + u * kPThreads;
+      kk[u] = i < tn ? s.sk[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kWB; ++u) o[u] = s.base[uint32_t(kk[u] >> SHIFT) & 255u] + uint32_t(i0 + u * kPThreads);
+    if constexpr (CW > 0) {
+      uint64_t pw[kWB][CW];
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        const int i = i0 + u * kPThreads;
+#pragma unroll
+        for (int w = 0; w < CW; ++w) pw[u][w] = i < tn ? s.sp[i * CW + w] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        if (i0 + u * kPThreads < tn) {
+          __stwb(reinterpret_cast<unsigned long long*>(out_k) + o[u], kk[u]);
+#pragma unroll
+          for (int w = 0; w < CW; ++w) __stwb(reinterpret_cast<unsigned long long*>(out_p) + size_t(o[u]) * CW + w, pw[u][w]);
+        }
+      }
+    } else {
+      uint32_t vv[kWB];
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        const int i = i0 + u * kPThreads;
+        vv[u] = !PK && i < tn ? s.sv[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        if (i0 + u * kPThreads < tn) {
+          __stwb(reinterpret_cast<unsigned long long*>(out_k) + o[u], kk[u]);
+          if constexpr (!PK) __stwb(out_v + o[u], vv[u]);
+        }
+      }
     }
   }
   __syncthreads();  // staging and s.base reused by the next tile
@@ -1087,23 +1137,36 @@ __device__ __forceinline__ void load_carry(const SortArgs& a, uint64_t row, uint
     for (int i = 0; i < CW; ++i) w[i] = __ldcs(src + i);
     return;
   }
+  if (a.carry_n == 1 && a.carry_width[0] == 4 && a.carry_off[0] == 0) {  // one 4-byte column (cfg2's payload)
+    w[0] = __ldcs(reinterpret_cast<const unsigned int*>(a.carry_src[0]) + row);
 #pragma unroll
-  for (int i = 0; i < CW; ++i) w[i] = 0;
+    for (int i = 1; i < CW; ++i) w[i] = 0;
+    return;
+  }
+  // general layout: the words as two scalars (a dynamic index into w[] would
+  // put the caller's carry registers on the stack)
+  uint64_t w0 = 0, w1 = 0;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     if (c >= a.carry_n) break;
     const int wd = a.carry_width[c], off = a.carry_off[c];
     const uint8_t* src = a.carry_src[c] + row * uint64_t(wd);
     if ((wd == 8 || wd == 16) && (off & 7) == 0) {
-      w[off >> 3] = __ldcs(reinterpret_cast<const unsigned long long*>(src));
-      if (wd == 16 && (off >> 3) + 1 < CW) w[(off >> 3) + 1] = __ldcs(reinterpret_cast<const unsigned long long*>(src) + 1);
+      const uint64_t x = __ldcs(reinterpret_cast<const unsigned long long*>(src));
+      if (off == 0) w0 = x;
+      else w1 = x;
+      if (wd == 16 && off == 0) w1 = __ldcs(reinterpret_cast<const unsigned long long*>(src) + 1);
     } else {
       for (int b = 0; b < wd; ++b) {
         const int at = off + b;
-        if ((at >> 3) < CW) w[at >> 3] |= uint64_t(__ldg(src + b)) << ((at & 7) * 8);
+        const uint64_t x = uint64_t(__ldg(src + b));
+        if (at < 8) w0 |= x << (at * 8);
+        else if (at < 16) w1 |= x << ((at - 8) * 8);
       }
     }
   }
+  w[0] = w0;
+  if constexpr (CW > 1) w[1] = w1;
 }
 
 template <int CW = 0>
@@ -1245,6 +1308,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
         const int j = u * kPThreads + tid;
         k[u] = j < tn ? pack_as<decltype(packed)::value>(xform(k[u], a.desc), sh, shl) : 0ull;
         if constexpr (PK) k[u] |= uint64_t(uint32_t(t0 + j));
+        else if constexpr (CW > 0) cr.p[u][0] = (cr.p[u][0] << 32) | uint32_t(t0 + j);  // idw: (columns, row id)
         else v[u] = uint32_t(t0 + j);
       }
     };
@@ -1266,9 +1330,19 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   using F = std::false_type;
   using T = std::true_type;
   const bool pk = packed_rows(sh, a);
-  if constexpr (CW > 0) {  // carried payload rides with packed rows only (the bucket join's plan checks the code)
-    if (!packed_rows(sh, a)) {  // a sort with carried columns on wide keys: the LSD passes gather them instead
-      if (tid == 0) atomicOr(a.flags, 1u);
+  if constexpr (CW > 0) {  // carried payload rides with packed rows (the bucket join's plan checks the code)
+    if (!packed_rows(sh, a)) {
+      // keys that do not pack: one word of <= 4 carried bytes holds the row id
+      // too (idw); wider carried columns: the LSD passes gather them instead
+      if (CW != 1 || !a.idw) {
+        if (tid == 0) atomicOr(a.flags, 1u);
+        return;
+      }
+      switch (pack_mode(sh)) {
+        case 0: tiles(std::integral_constant<int, 0>{}, F{}); break;
+        case 1: tiles(std::integral_constant<int, 1>{}, F{}); break;
+        default: tiles(std::integral_constant<int, 2>{}, F{}); break;
+      }
       return;
     }
     if (pack_mode(sh) == 1) tiles(std::integral_constant<int, 1>{}, T{});
@@ -1305,7 +1379,8 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_ke
   if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);  // the key pack code
   if (fallback_flag(a)) return;  // LSD fallback (the barrier also publishes scratch[50])
   if constexpr (CW > 0) {
-    sub_scatter_tiles<true, CW>(a, s);
+    if (packed_rows(s.scratch[50], a)) sub_scatter_tiles<true, CW>(a, s);
+    else if constexpr (CW == 1) sub_scatter_tiles<false, CW>(a, s);  // idw (the digit-7 pass declined otherwise)
   } else {
     if (packed_rows(s.scratch[50], a)) sub_scatter_tiles<true, 0>(a, s);
     else sub_scatter_tiles<false, 0>(a, s);
@@ -1326,7 +1401,7 @@ __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile
     for (int u = 0; u < kPItems; ++u) {
       const int j = u * kPThreads + tid;
       k[u] = j < tn ? __ldcs(a.keys_b + item.y + j) : 0ull;
-      if constexpr (!PK) v[u] = j < tn ? __ldcs(a.vals_b + item.y + j) : 0u;
+      if constexpr (!PK && CW == 0) v[u] = j < tn ? __ldcs(a.vals_b + item.y + j) : 0u;
       if constexpr (CW > 0) {
 #pragma unroll
         for (int w = 0; w < CW; ++w) cr.p[u][w] = j < tn ? __ldcs(a.pay_b + (size_t(item.y) + j) * CW + w) : 0ull;
@@ -1459,7 +1534,7 @@ __device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTil
     for (int u = 0; u < kPItems; ++u) {
       const int j = u * kPThreads + tid;
       k[u] = j < tn ? __ldcs(a.keys_a + r0 + j) : 0ull;
-      if constexpr (!PK) v[u] = j < tn ? __ldcs(a.vals_a + r0 + j) : 0u;
+      if constexpr (!PK && CW == 0) v[u] = j < tn ? __ldcs(a.vals_a + r0 + j) : 0u;
       if constexpr (CW > 0) {
 #pragma unroll
         for (int w = 0; w < CW; ++w) cc.p[u][w] = j < tn ? __ldcs(a.pay_a + (size_t(r0) + j) * CW + w) : 0ull;
@@ -1520,7 +1595,8 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub3_scatter_k
   if (tid == 0) s.scratch[50] = __ldcg(a.flags + 6);
   if (fallback_flag(a)) return;
   if constexpr (CW > 0) {
-    sub3_scatter_tiles<true, CW>(a, s);
+    if (packed_rows(s.scratch[50], a)) sub3_scatter_tiles<true, CW>(a, s);
+    else if constexpr (CW == 1) sub3_scatter_tiles<false, CW>(a, s);  // idw
   } else {
     if (packed_rows(s.scratch[50], a)) sub3_scatter_tiles<true>(a, s);
     else sub3_scatter_tiles<false>(a, s);
@@ -1561,6 +1637,31 @@ __device__ void warp_bitonic(uint64_t* bk, uint32_t* bv, uint32_t lo, uint32_t h
               bk[lo + i] = kb; bk[lo + q] = ka;
               bv[lo + i] = vb; bv[lo + q] = va;
             }
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// warp_bitonic for idw runs: rows ordered by (key, row id), the id read from
+// the run's carried word behind each row's u16 load index.
+__device__ void warp_bitonic_idw(uint64_t* bk, uint16_t* bi, const uint64_t* aw, uint32_t lo, uint32_t hi, int lane) {
+  const uint32_t sz = hi - lo;
+  uint32_t p2 = 1;
+  while (p2 < sz) p2 <<= 1;
+  for (uint32_t k = 2; k <= p2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = lane; t < (p2 >> 1); t += 32) {
+        const uint32_t i = (t / j) * (2 * j) + (t % j);
+        const uint32_t q = j == (k >> 1) ? (i ^ (k - 1)) : (i + j);
+        if (q < sz) {
+          const uint64_t ka = bk[lo + i], kb = bk[lo + q];
+          const uint16_t ia = bi[lo + i], ib = bi[lo + q];
+          if (kb < ka || (kb == ka && uint32_t(aw[ib]) < uint32_t(aw[ia]))) {
+            bk[lo + i] = kb; bk[lo + q] = ka;
+            bi[lo + i] = ib; bi[lo + q] = ia;
           }
         }
       }
@@ -1611,6 +1712,17 @@ __device__ __forceinline__ void issue_run(const uint64_t* kin, const uint32_t* v
   if (vbytes) bulk_g2s(abuf + kLocAKeys, vin + v0, vbytes, bar);
 }
 
+// idw: the run's keys and carried words (same alignment: both 8 bytes a row)
+__device__ __forceinline__ void issue_run_w(const uint64_t* kin, const uint64_t* win, uint32_t base, uint32_t cnt,
+                                            uint8_t* abuf, uint64_t* bar) {
+  const uint32_t k0 = base & ~1u;
+  const uint32_t bytes = ((base + cnt - k0) * 8u + 15u) & ~15u;
+  fence_proxy_async_smem();
+  mbar_expect_tx(bar, 2 * bytes);
+  bulk_g2s(abuf, kin + k0, bytes, bar);
+  bulk_g2s(abuf + kLocAKeys, win + k0, bytes, bar);
+}
+
 // BAL (the scatter path's large runs): a thread's rows in registers across
 // count + scatter, and the claimed group tail. The onesweep hybrid's short
 // runs (n < 4M) are faster without both (+1-5 us each at 0.3-2M rows).
@@ -1619,14 +1731,21 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   // CW > 0 (packed rows): every row's payload words ride in pay_a / pay_b beside
   // its key; bv holds the row's load index in its run, and the emit copies the
   // carried columns out of the run's payload window (no gather by row id)
-  static_assert(CW == 0 || PK, "carried payload rides with packed rows");
+  // idw (CW == 1, keys that do not pack): the carried word holds the row id
+  // (low half) and the columns' bytes (high half); it is staged with the key
+  // by TMA, bv holds the load index, ties compare the ids behind the indexes
+  constexpr bool IDW = CW == 1 && !PK;
+  static_assert(CW == 0 || PK || IDW, "carried payload rides with packed rows, or as idw words");
+  static_assert(!IDW || BAL, "idw runs use the in-place layout");
+  constexpr size_t kABytes = IDW ? kLocABytesW : kLocABytes;
   const uint64_t* pay = CW ? (src == 1 ? a.pay_a : a.pay_b) : nullptr;
   // sub-buckets of the runs: (d7, d6) or, with three levels, (d7, d6, d5)
   constexpr int kSubShift = LEVELS == 3 ? 40 : 48;
   const uint32_t* sub_off = LEVELS == 3 ? a.sub3_off : a.sub_off;
   constexpr int kLWarps = THREADS / 32;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (BAL ? kLocHistBal : kLocHist));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (IDW ? kLocHistW : BAL ? kLocHistBal : kLocHist));
   uint32_t* bv = reinterpret_cast<uint32_t*>(smem + (BAL ? kLocBvBal : kLocBv));
+  uint16_t* bv16 = reinterpret_cast<uint16_t*>(smem + kLocBvW);  // idw
   uint32_t* big = reinterpret_cast<uint32_t*>(smem + kLocBig);
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
   // a work item: G consecutive sub-buckets (three levels: the 256 sub-sub-buckets
@@ -1733,7 +1852,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     runs[1] = cnt;
     runs[2] = gid[k & 1] * G + (se >> 16);
     runs[3] = (se & 0xFFFFu) - (se >> 16);
-    issue_run(kin, vin, base, cnt, smem + kLocA, &bars[0]);
+    if constexpr (IDW) issue_run_w(kin, pay, base, cnt, smem + kLocA, &bars[0]);
+    else issue_run(kin, vin, base, cnt, smem + kLocA, &bars[0]);
   }
   __syncthreads();  // the first run's descriptor is visible to every thread
 
@@ -1763,7 +1883,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
           d[1] = cnt;
           d[2] = gid[nk & 1] * G + (se >> 16);
           d[3] = (se & 0xFFFFu) - (se >> 16);
-          issue_run(kin, vin, base, cnt, smem + kLocA + (buf ^ 1) * kLocABytes, &bars[buf ^ 1]);
+          if constexpr (IDW) issue_run_w(kin, pay, base, cnt, smem + kLocA + (buf ^ 1) * kABytes, &bars[buf ^ 1]);
+          else issue_run(kin, vin, base, cnt, smem + kLocA + (buf ^ 1) * kLocABytes, &bars[buf ^ 1]);
         }
       }
     }
@@ -1785,9 +1906,10 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     const uint32_t next_k = misc[5], next_r = misc[6];
     if (tid == 0) misc[0] = 0;  // big-bin list: appended after later barriers, read after the rank loop
     const uint32_t base = runs[buf * 4], cnt = runs[buf * 4 + 1];
-    uint8_t* abuf = smem + kLocA + buf * kLocABytes;
+    uint8_t* abuf = smem + kLocA + buf * kABytes;
     const uint64_t* ak = reinterpret_cast<const uint64_t*>(abuf) + (base & 1u);
     const uint32_t* av = reinterpret_cast<const uint32_t*>(abuf + kLocAKeys) + (base & 3u);
+    const uint64_t* aw = reinterpret_cast<const uint64_t*>(abuf + kLocAKeys) + (base & 1u);  // idw
     // the bin-ordered keys: BAL, in this run's own key buffer (read into registers first)
     uint64_t* bk = reinterpret_cast<uint64_t*>(BAL ? abuf : smem + kLocBk);
     auto bin_of = [&](uint64_t key) {
@@ -1822,7 +1944,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         const uint32_t j = tid + u * THREADS;
         if (j < cnt) {
           bk[pos[u]] = rk[u];
-          if constexpr (!PK) bv[pos[u]] = av[j];
+          if constexpr (IDW) bv16[pos[u]] = uint16_t(j);
+          else if constexpr (!PK) bv[pos[u]] = av[j];
           else if constexpr (CW > 0) bv[pos[u]] = j;
         }
       }
@@ -1848,9 +1971,23 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         v = uint32_t(key);
         key &= ~0xFFFFFFFFull;
       }
+      uint64_t wd = 0;
+      if constexpr (IDW) {
+        wd = aw[j];
+        v = uint32_t(wd);
+      }
       if (a.out_keys) __stcs(reinterpret_cast<long long*>(a.out_keys) + o, (long long)xform(unpack_as<PACK>(key, pcode, pshl, constbits), desc));
       __stcs(a.out_vals + o, v);
-      if constexpr (CW > 0) {
+      if constexpr (IDW) {  // the columns' bytes: the word's high half
+        const uint32_t pw = uint32_t(wd >> 32);
+        for (int c = 0; c < a.carry_n; ++c) {
+          const int w = a.carry_width[c], off = a.carry_off[c];
+          uint8_t* dst = a.carry_dst[c] + o * uint64_t(w);
+          if (w == 4) __stcs(reinterpret_cast<unsigned int*>(dst), pw);
+          else
+            for (int b = 0; b < w; ++b) dst[b] = uint8_t(pw >> (8 * (off + b)));
+        }
+      } else if constexpr (CW > 0) {
         const uint8_t* row = reinterpret_cast<const uint8_t*>(pay + (size_t(base) + j) * CW);
         for (int c = 0; c < a.carry_n; ++c)
           copy_row(row + a.carry_off[c], a.carry_dst[c] + o * uint64_t(a.carry_width[c]), a.carry_width[c]);
@@ -1860,7 +1997,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     };
     for (uint32_t p = tid; p < cnt; p += THREADS) {
       const uint64_t key = bk[p];
-      const uint32_t v = PK && CW == 0 ? 0u : bv[p];
+      const uint32_t v = IDW ? uint32_t(bv16[p]) : PK && CW == 0 ? 0u : bv[p];
       const int b = bin_of(key);
       const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
       uint32_t pos = p;
@@ -1875,6 +2012,11 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         uint32_t rk = 0;
         if constexpr (PK) {
           for (uint32_t i = b0; i < b1; ++i) rk += bk[i] < key ? 1u : 0u;
+        } else if constexpr (IDW) {  // the row ids only for equal keys
+          for (uint32_t i = b0; i < b1; ++i) {
+            const uint64_t ki = bk[i];
+            rk += ki < key || (ki == key && uint32_t(aw[bv16[i]]) < uint32_t(aw[v])) ? 1u : 0u;
+          }
         } else {
           for (uint32_t i = b0; i < b1; ++i) rk += row_less(bk[i], bv[i], key, v) ? 1u : 0u;
         }
@@ -1887,8 +2029,13 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     for (uint32_t t = warp; t < nbig; t += kLWarps) {
       const int b = int(big[t]);
       const uint32_t b0 = b > 0 ? hist[b - 1] : 0u, b1 = hist[b];
-      warp_bitonic<PK, (CW > 0)>(bk, bv, b0, b1, lane);
-      for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], PK && CW == 0 ? 0u : bv[p]);
+      if constexpr (IDW) {
+        warp_bitonic_idw(bk, bv16, aw, b0, b1, lane);
+        for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], uint32_t(bv16[p]));
+      } else {
+        warp_bitonic<PK, (CW > 0)>(bk, bv, b0, b1, lane);
+        for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], PK && CW == 0 ? 0u : bv[p]);
+      }
     }
     if (nbig) __syncthreads();  // (the rank loop's reads of B/hist ended at the barrier before nbig)
     if (!more) break;
@@ -2043,6 +2190,14 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_car
     misc[127] = uint32_t(cb >> 32);
   }
   constexpr uint32_t src = LEVELS == 3 ? 2u : 1u;
+  if (!packed_rows(pc, a)) {  // idw (the counting passes declined anything else)
+    switch (pack_mode(pc)) {
+      case 0: local_phase<kLocalThreads, 0, true, false, LEVELS, 1>(a, smem, src); break;
+      case 1: local_phase<kLocalThreads, 1, true, false, LEVELS, 1>(a, smem, src); break;
+      default: local_phase<kLocalThreads, 2, true, false, LEVELS, 1>(a, smem, src); break;
+    }
+    return;
+  }
   const bool m1 = pack_mode(pc) == 1;  // (packed rows: mode 1 or 2, checked by the counting passes)
   if (a.cw == 1) {
     if (m1) local_phase<kLocalThreads, 1, true, true, LEVELS, 1>(a, smem, src);
@@ -2735,6 +2890,9 @@ int sort_axis_carry(const int64_t* keys, int64_t n, int descending, int64_t* sor
   }
   a.carry_n = n_columns;
   a.cw = words;
+  int carried = 0;
+  for (int i = 0; i < n_columns; ++i) carried += columns[i].width;
+  a.idw = carried <= 4 && !getenv_flag("RL_NO_IDW") ? 1 : 0;
   a.pay_a = pa;
   a.pay_b = pb;
   return launch_sort(a, L, stream, nullptr, 0);

@@ -14,6 +14,7 @@ key word; gather_rows = K7; hash_partition = K8.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -325,6 +326,13 @@ def carry_fits(columns: Sequence[OutColumn]) -> bool:
     return at <= 16
 
 
+def idw_fits(columns: Sequence[OutColumn]) -> bool:
+    """<= 4 carried bytes a row: on keys that do not pack they share one word
+    with the row id through the sort's passes (radix_sort.cu, idw), 16 bytes a
+    row instead of 12 + a random gather afterwards."""
+    return 0 < len(columns) <= 4 and sum(c.width for c in columns) <= 4
+
+
 class SortGraph:
     """A stable ORDER BY of one int64 key column (+ Relation.take of bound
     columns) captured once as a CUDA graph: histogram, cooperative sort and
@@ -333,7 +341,12 @@ class SortGraph:
     current contents of ``keys`` / the gather sources into ``sorted_keys``,
     ``perm`` and the gather destinations, which are fixed at capture."""
 
-    def __init__(self, keys: torch.Tensor, descending: bool = False, gather: Sequence[OutColumn] = ()):
+    def __init__(self, keys: torch.Tensor, descending: bool = False, gather: Sequence[OutColumn] = (),
+                 carry: Optional[bool] = None):
+        """carry: move the gathered columns with the rows through the sort's
+        passes (rl_sort_axis_carry) instead of gathering them by the
+        permutation afterwards; None = RL_SORT_CARRY=1 (off by default: for
+        cfg2 the gather is as fast)."""
         _require_cuda(keys, "keys")
         lib = C.load()
         self.keys = aligned16(keys)
@@ -342,10 +355,27 @@ class SortGraph:
         self.sorted_keys = torch.empty(n, dtype=torch.int64, device=dev)
         self.perm = torch.empty(n, dtype=_U32, device=dev)
         self.gather = list(gather)
-        self._ws = workspace(lib.rl_sort_workspace_bytes(n), dev)
+        if carry is None:
+            env = os.environ.get("RL_SORT_CARRY", "")
+            # measured at cfg2 (10M rows, 4-byte payload): carried 0.308 ms a step vs
+            # 0.302 sort + gather, so the gather stays the default
+            carry = env == "1"
+        self.carry = bool(carry and self.gather)
+        if self.carry:
+            arr, ncols = C.columns_array((c.src.data_ptr(), c.dst.data_ptr(), c.width, C.RL_SIDE_LEFT)
+                                         for c in self.gather)
+            self._cols = (arr, ncols)
+            self._ws = workspace(lib.rl_sort_carry_workspace_bytes(n, sum(c.width for c in self.gather)), dev)
+        else:
+            self._ws = workspace(lib.rl_sort_workspace_bytes(n), dev)
         self._desc = int(descending)
 
         def body():
+            if self.carry:
+                C.check(lib.rl_sort_axis_carry(_ptr(self.keys), n, self._desc, _ptr(self.sorted_keys),
+                                               _ptr(self.perm), self._cols[0], self._cols[1], _ptr(self._ws),
+                                               self._ws.numel(), stream_handle()), "rl_sort_axis_carry")
+                return
             C.check(lib.rl_sort_axis(_ptr(self.keys), C.RL_COL_INT64, 8, 0, self._desc, None, n,
                                      _ptr(self.sorted_keys), _ptr(self.perm), _ptr(self._ws), self._ws.numel(),
                                      stream_handle()), "rl_sort_axis")

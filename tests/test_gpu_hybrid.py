@@ -331,26 +331,41 @@ def test_three_level_skewed_sub_sub_bucket_falls_back(monkeypatch, into_subbucke
     check_sort(keys)
 
 
-@pytest.mark.parametrize("shape", ["narrow_2cols", "narrow_mixed", "wide_keys_fallback", "three_level"])
+@pytest.mark.parametrize("shape", ["narrow_2cols", "narrow_mixed", "wide_keys_fallback", "three_level", "idw_4b",
+                                   "idw_2x2b_dups", "idw_3b_three_level", "idw_heavy_bins"])
 def test_sort_with_carried_columns(shape, monkeypatch, into_subbuckets):
     """rl_sort_axis_carry: the other columns ride with the packed rows through
     the counting passes and leave from each run's payload window — equal to
     the stable argsort + take; wide keys take the LSD fallback with the
-    gathers fused; the third level forced at a small size."""
+    gathers fused; the third level forced at a small size. idw: keys that do
+    not pack with <= 4 carried bytes share one word with the row id (cfg2's
+    shape: full-range keys + a 4-byte payload), incl. duplicate-heavy bins
+    (equal keys ranked by the ids behind the load indexes, bitonic bins)."""
     if into_subbuckets != "scatter":
         pytest.skip("carried columns belong to the scatter path")
-    if shape == "three_level":
+    if "three_level" in shape:
         monkeypatch.setenv("RL_LEVEL3_MIN_ROWS", "1")
     rng = np.random.default_rng(90 + len(shape))
     n = 4_500_000
-    if shape == "wide_keys_fallback":
+    if shape == "wide_keys_fallback" or shape.startswith("idw"):
         keys = full_range(rng, n)
+        if shape == "idw_2x2b_dups":
+            keys[rng.choice(n, n // 10, replace=False)] = keys[rng.integers(0, n, n // 10)]
+        if shape == "idw_heavy_bins":  # bins of ~40 equal keys (the warp bitonic) and of 2-32 (the rank loop)
+            keys[: n // 2] = keys[rng.integers(0, n // 80, n // 2)]
+            rng.shuffle(keys)
     else:
         keys = rng.integers(0, 1 << 27, n, dtype=np.int64) - 5_000_000
         keys[rng.choice(n, n // 25, replace=False)] = keys[rng.integers(0, n, n // 25)]
     if shape == "narrow_mixed":
         cols = [rng.integers(0, 256, (n, 5), dtype=np.uint8), rng.integers(-(2**31), 2**31, n).astype(np.int32),
                 rng.integers(0, 256, (n, 3), dtype=np.uint8)]
+    elif shape in ("idw_4b", "idw_heavy_bins"):
+        cols = [rng.integers(-(2**31), 2**31, n).astype(np.int32)]
+    elif shape == "idw_2x2b_dups":
+        cols = [rng.integers(0, 256, (n, 2), dtype=np.uint8), rng.integers(0, 256, (n, 2), dtype=np.uint8)]
+    elif shape == "idw_3b_three_level":
+        cols = [rng.integers(0, 256, (n, 3), dtype=np.uint8)]
     else:
         cols = [rng.integers(-(2**62), 2**62, n), rng.integers(-(2**62), 2**62, n)]
     for desc in (False, True):
@@ -365,3 +380,30 @@ def test_sort_with_carried_columns(shape, monkeypatch, into_subbuckets):
         assert (sk.cpu().numpy() == keys[want]).all()
         for o, c in zip(outs, cols):
             assert (o.dst.cpu().numpy() == c[want]).all()
+
+
+def test_sort_graph_carried_payload_equals_gather(into_subbuckets):
+    """engine.SortGraph with the 4-byte payload carried through the passes
+    (idw) replays to the same sorted keys, permutation and payload as the
+    sort + gather graph (cfg2's shape at 5M rows, ~1% duplicates)."""
+    if into_subbuckets != "scatter":
+        pytest.skip("carried columns belong to the scatter path")
+    from paper_2602_21237_b200 import synth
+
+    rel = synth.cfg2_relation(5_000_000)
+    keys = torch.from_numpy(rel.column("key").copy()).cuda()
+    pay = torch.from_numpy(np.ascontiguousarray(rel.column("payload")).view(np.int32).reshape(-1).copy()).cuda()
+    got = []
+    for carry in (False, True):
+        dst = torch.empty_like(pay)
+        g = engine.SortGraph(keys, gather=[engine.OutColumn(pay, dst, 4, 0)], carry=carry)
+        assert g.carry == carry
+        for _ in range(2):
+            dst.zero_()
+            g.replay()
+        torch.cuda.synchronize()
+        got.append((g.sorted_keys.cpu(), g.perm.cpu(), dst.cpu()))
+    want = O.stable_axis_order(rel.column("key"), False)
+    assert (got[1][1].numpy().view(np.uint32).astype(np.int64) == want).all()
+    for a, b in zip(*got):
+        assert torch.equal(a, b)

@@ -227,7 +227,7 @@ struct SortArgs {
   uint32_t* sub3_off;        // [kSub3 + 1] sub-sub-bucket starts
   uint32_t* cur24;           // [kSub3] rows placed per sub-sub-bucket so far (zeroed)
   uint32_t* tile3;           // [kSubBuckets + 1] first level-3 tile of every sub-bucket (prefix)
-  uint32_t* tmap;            // [level-3 tiles] the sub-bucket of every tile
+  uint32_t* tmap;            // [level-3 tiles] uint4 (sub-bucket, first row, end row) of every tile
 };
 constexpr int kSub3 = 1 << 24;  // (d7, d6, d5) sub-sub-buckets
 
@@ -887,21 +887,42 @@ __device__ __forceinline__ PTile ptile(uint8_t* sm) {
 // is zero on entry and on exit. Once the tile is staged, next(k, v) loads the
 // following tile into the same registers, in flight during the write-out.
 // PK (packed rows): the row id travels in the key word's low 32 bits — no
-// separate row-id stream (v[] unused).
+// separate row-id stream (v[] unused). mid() runs on every thread after the
+// counting barrier, beside the digit scan (warps 8..15 only reserve there).
 // CW > 0 (bucket join): CW payload words ride with every row (c.p), staged and
 // written to out_p[o * CW + w] beside the key.
-template <int SHIFT, bool PK, int CW = 0, typename Reserve, typename Next>
+#ifdef RL_PASS_PROFILE  // per-phase clock totals of the counting passes (A/B builds only)
+__device__ unsigned long long g_pass_prof[16];
+#define PPROF(i, t) do { if (threadIdx.x == 0) { const long long c_ = clock64(); atomicAdd(&g_pass_prof[i], (unsigned long long)(c_ - t)); t = c_; } } while (0)
+#else
+#define PPROF(i, t) do { } while (0)
+#endif
+
+struct NoMid {
+  __device__ void operator()() const {}
+};
+template <int SHIFT, bool PK, int CW = 0, typename Reserve, typename Next, typename Mid = NoMid>
 __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cr, int tn,
                                               const PTile& s, uint64_t* out_k, uint32_t* out_v, uint64_t* out_p,
-                                              Reserve reserve, Next next) {
+                                              Reserve reserve, Next next, Mid mid = Mid()) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef RL_PASS_PROFILE
+  long long pt = clock64();
+#endif
   uint32_t r[kPItems];
 #pragma unroll
   for (int u = 0; u < kPItems; ++u)
     if (u * kPThreads + tid < tn) r[u] = atomicAdd(&s.hist[uint32_t(k[u] >> SHIFT) & 255u], 1u);
   __syncthreads();
+  PPROF(SHIFT == 56 ? 0 : 8, pt);
+  mid();  // the caller's work beside the digit scan (the next tile's descriptor)
   const uint32_t c = tid < 256 ? s.hist[tid] : 0u;
-  const uint32_t res = tid < 256 && c ? reserve(uint32_t(tid), c) : 0u;
+  // the digit runs: reserve(d, c) = {static start, atomic reservation}, issued
+  // by warps 8..15 (thread 256 + d) while warps 0..7 scan, in flight until
+  // s.base is written after the staging (empty digits reserve 0)
+  static_assert(kPThreads >= 512, "digit scan on threads 0..255, reservations on 256..511");
+  uint2 res;
+  if (tid >= 256 && tid < 512) res = reserve(uint32_t(tid - 256), s.hist[tid - 256]);
   uint32_t incl = c;  // digit scan: warps 0..7, one barrier (the next scratch write is behind two more)
   if (tid < 256) {
 #pragma unroll
@@ -918,6 +939,7 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
     s.hist[tid] = excl;
   }
   __syncthreads();
+  PPROF(SHIFT == 56 ? 1 : 9, pt);
   // staging: every digit start read before the first staged store (a store
   // could alias a later start, so the compiler keeps written order)
   uint32_t sp[kPItems];
@@ -936,9 +958,11 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
       }
     }
   }
-  if (tid < 256) s.base[tid] = res - excl;
+  if (tid >= 256 && tid < 512) s.base[tid - 256] = res.x + res.y - s.hist[tid - 256];  // (s.hist = digit starts)
   __syncthreads();
+  PPROF(SHIFT == 56 ? 2 : 10, pt);
   next(k, v, cr);
+  PPROF(SHIFT == 56 ? 5 : 13, pt);
   if (tid < 256) s.hist[tid] = 0;  // for the next tile (the write-out reads only s.base)
   // write-out in batches of kWB rows a thread: the staged keys, then their
   // digit bases, then the global stores (st.global: no ordering against the
@@ -987,6 +1011,10 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
     }
   }
   __syncthreads();  // staging and s.base reused by the next tile
+  PPROF(SHIFT == 56 ? 3 : 11, pt);
+#ifdef RL_PASS_PROFILE
+  if (tid == 0) atomicAdd(&g_pass_prof[SHIFT == 56 ? 4 : 12], 1ull);
+#endif
 }
 
 __global__ void __launch_bounds__(kScatThreads, 1) sub_hist_kernel(SortArgs a) {
@@ -1271,13 +1299,14 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
   if (fallback_flag(a)) return;
   // this CTA's rows by digit 7 -> keys_b / vals_b
   const uint32_t sh = s.scratch[50];
-  auto reserve = [&](uint32_t d, uint32_t c) { return s.aux[d] + atomicAdd(a.cur7 + d, c); };
+  auto reserve = [&](uint32_t d, uint32_t c) { return make_uint2(s.aux[d], atomicAdd(a.cur7 + d, c)); };
   // the tile loop, compiled per key-packing mode (chosen once)
   const uint32_t shl = pack_shift(sh);
   auto tiles = [&](auto packed, auto pkc) {
     constexpr bool PK = decltype(pkc)::value;
-    // every load of a tile is issued before the first use (the payload loads
-    // of the common one-column case too), then the keys are transformed
+    // every load of a tile is issued during the previous tile's write-out (the
+    // payload loads of the common one-column case too); the keys are transformed
+    // (finish) only when the tile is ranked, so that nothing waits for them there
     const bool whole_words = CW > 0 && a.carry_n == 1 && a.carry_width[0] == 8 * CW;
     auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cr, int64_t t0) {
       const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
@@ -1303,6 +1332,9 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
           }
         }
       }
+    };
+    auto finish = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cr, int64_t t0) {
+      const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
 #pragma unroll
       for (int u = 0; u < kPItems; ++u) {
         const int j = u * kPThreads + tid;
@@ -1321,6 +1353,7 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) top_scatter_ke
     for (int64_t t0 = lo; t0 < hi; t0 += kPTile) {
       const int tn = int(hi - t0 < kPTile ? hi - t0 : kPTile);
       const int64_t nt = t0 + kPTile;
+      finish(k, v, cr, t0);
       ptile_scatter<7 * kBits, PK, CW>(k, v, cr, tn, s, a.keys_b, a.vals_b, a.pay_b, reserve,
                                        [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
                                          if (nt < hi) load(kk, vv, cc, nt);
@@ -1390,11 +1423,20 @@ __global__ void __launch_bounds__(kPThreads, RL_PASS_CTAS_PER_SM) sub_scatter_ke
 #endif
 }
 
+// The tiles of the digit-6 / digit-5 passes are claimed from a counter in
+// bucket order (the runs being written span a few MB: every sector completes
+// in L2). One thread (kClaimer: warp 15, idle beside the digit scan) keeps the
+// claims two tiles ahead: during tile t (mid) it reads the descriptor of tile
+// t + 1 into slot[(t + 1) & 1] and claims tile t + 2, so the next tile's loads
+// (issued at the staging barrier) wait for no atomic or descriptor round trip.
+constexpr int kClaimer = kPThreads - 1;
+__device__ __forceinline__ uint4 no_tile() { return make_uint4(~0u, 0u, 0u, 0u); }
+
 template <bool PK, int CW>
 __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile& s) {
   const int tid = threadIdx.x;
   const uint32_t n_items = __ldcg(a.meta);
-  uint32_t* claim = s.scratch + 40;  // [2] claimed tile ids, by parity
+  uint4* slot = reinterpret_cast<uint4*>(s.scratch + 52);  // [2] descriptors (bucket, first row, end row)
   auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cr, const uint4& item) {
     const int tn = int(item.z - item.y);
 #pragma unroll
@@ -1408,32 +1450,38 @@ __device__ __forceinline__ void sub_scatter_tiles(const SortArgs& a, const PTile
       }
     }
   };
-  if (tid == 0) claim[0] = atomicAdd(a.flags + 3, 1u);
+  uint32_t ahead = 0;  // (kClaimer) the claim two tiles ahead
+  if (tid == kClaimer) {
+    const uint32_t c0 = atomicAdd(a.flags + 3, 1u);
+    slot[0] = c0 < n_items ? __ldcg(a.items + c0) : no_tile();
+    ahead = atomicAdd(a.flags + 3, 1u);
+  }
   if (tid < 256) s.hist[tid] = 0;
   __syncthreads();
-  uint32_t it = claim[0], par = 1;
-  uint4 item = it < n_items ? __ldcg(a.items + it) : make_uint4(0, 0, 0, 0);
+  uint32_t par = 0;
+  uint4 item = slot[0];
   uint64_t k[kPItems];
   uint32_t v[kPItems];
   Carry<CW> cr;
-  if (it < n_items) load(k, v, cr, item);
-  while (it < n_items) {
-    if (tid == 0) claim[par] = atomicAdd(a.flags + 3, 1u);  // the next tile, read after the staging barrier
+  if (item.x != ~0u) load(k, v, cr, item);
+  while (item.x != ~0u) {
     const uint32_t g = item.x;
-    uint32_t nit = 0;
-    uint4 nitem = make_uint4(0, 0, 0, 0);
+    uint4 nitem = no_tile();
     auto reserve = [&](uint32_t d, uint32_t c) {
-      return __ldcg(a.sub_off + g * 256 + d) + atomicAdd(a.cur16 + g * 256 + d, c);
+      return make_uint2(__ldcg(a.sub_off + g * 256 + d), atomicAdd(a.cur16 + g * 256 + d, c));
     };
-    ptile_scatter<6 * kBits, PK, CW>(k, v, cr, int(item.z - item.y), s, a.keys_a, a.vals_a, a.pay_a, reserve,
-                                     [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
-                                       nit = claim[par];
-                                       if (nit < n_items) {
-                                         nitem = __ldcg(a.items + nit);
-                                         load(kk, vv, cc, nitem);
-                                       }
-                                     });
-    it = nit;
+    ptile_scatter<6 * kBits, PK, CW>(
+        k, v, cr, int(item.z - item.y), s, a.keys_a, a.vals_a, a.pay_a, reserve,
+        [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
+          nitem = slot[par ^ 1];
+          if (nitem.x != ~0u) load(kk, vv, cc, nitem);
+        },
+        [&]() {
+          if (tid == kClaimer) {
+            slot[par ^ 1] = ahead < n_items ? __ldcg(a.items + ahead) : no_tile();
+            if (ahead < n_items) ahead = atomicAdd(a.flags + 3, 1u);
+          }
+        });
     item = nitem;
     par ^= 1;
   }
@@ -1504,8 +1552,13 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(SortArgs a) {
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const uint32_t v = buf[tid * kPer + i];
-      a.tile3[c0 + tid * kPer + i] = start;
-      for (uint32_t j = 0; j < v; ++j) a.tmap[start + j] = uint32_t(c0 + tid * kPer + i);  // tile -> sub-bucket
+      const uint32_t sb = uint32_t(c0 + tid * kPer + i);
+      a.tile3[sb] = start;
+      if (v) {  // the sub-bucket's tiles: (sub-bucket, first row, end row)
+        const uint32_t lo = __ldcg(a.sub_off + sb), hi = __ldcg(a.sub_off + sb + 1);
+        uint4* td = reinterpret_cast<uint4*>(a.tmap);
+        for (uint32_t j = 0; j < v; ++j) td[start + j] = make_uint4(sb, lo + j * kPTile, min(hi, lo + (j + 1) * kPTile), 0u);
+      }
       start += v;
     }
     carry += total;
@@ -1521,66 +1574,54 @@ template <bool PK, int CW = 0>
 __device__ __forceinline__ void sub3_scatter_tiles(const SortArgs& a, const PTile& s) {
   const int tid = threadIdx.x;
   const uint32_t n_tiles = __ldcg(a.meta + 1);
-  uint32_t* claim = s.scratch + 40;  // [0..1] claimed tile ids by parity, [2..3] their sub-bucket
-  auto locate = [&](uint32_t t) -> uint32_t { return __ldcg(a.tmap + t); };  // tile -> sub-bucket
-  auto rows_of = [&](uint32_t t, uint32_t sb, uint32_t& r0, uint32_t& r1) {
-    const uint32_t lo = __ldcg(a.sub_off + sb), hi = __ldcg(a.sub_off + sb + 1);
-    r0 = lo + (t - __ldcg(a.tile3 + sb)) * kPTile;
-    r1 = min(hi, r0 + kPTile);
-  };
-  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cc, uint32_t r0, uint32_t r1) {
-    const int tn = int(r1 - r0);
+  const uint4* tdesc = reinterpret_cast<const uint4*>(a.tmap);  // (sub-bucket, first row, end row) a tile
+  uint4* slot = reinterpret_cast<uint4*>(s.scratch + 52);
+  auto load = [&](uint64_t (&k)[kPItems], uint32_t (&v)[kPItems], Carry<CW>& cc, const uint4& d) {
+    const int tn = int(d.z - d.y);
 #pragma unroll
     for (int u = 0; u < kPItems; ++u) {
       const int j = u * kPThreads + tid;
-      k[u] = j < tn ? __ldcs(a.keys_a + r0 + j) : 0ull;
-      if constexpr (!PK && CW == 0) v[u] = j < tn ? __ldcs(a.vals_a + r0 + j) : 0u;
+      k[u] = j < tn ? __ldcs(a.keys_a + d.y + j) : 0ull;
+      if constexpr (!PK && CW == 0) v[u] = j < tn ? __ldcs(a.vals_a + d.y + j) : 0u;
       if constexpr (CW > 0) {
 #pragma unroll
-        for (int w = 0; w < CW; ++w) cc.p[u][w] = j < tn ? __ldcs(a.pay_a + (size_t(r0) + j) * CW + w) : 0ull;
+        for (int w = 0; w < CW; ++w) cc.p[u][w] = j < tn ? __ldcs(a.pay_a + (size_t(d.y) + j) * CW + w) : 0ull;
       }
     }
   };
-  if (tid == 0) {
-    const uint32_t t = atomicAdd(a.flags + 2, 1u);
-    claim[0] = t;
-    claim[2] = t < n_tiles ? locate(t) : 0u;
+  uint32_t ahead = 0;  // (kClaimer) the claim two tiles ahead (see sub_scatter_tiles)
+  if (tid == kClaimer) {
+    const uint32_t c0 = atomicAdd(a.flags + 2, 1u);
+    slot[0] = c0 < n_tiles ? __ldcg(tdesc + c0) : no_tile();
+    ahead = atomicAdd(a.flags + 2, 1u);
   }
   if (tid < 256) s.hist[tid] = 0;
   __syncthreads();
-  uint32_t it = claim[0], sb = claim[2], par = 1;
+  uint32_t par = 0;
+  uint4 d = slot[0];
   uint64_t k[kPItems];
   uint32_t v[kPItems];
   Carry<CW> cr;
-  uint32_t r0 = 0, r1 = 0;
-  if (it < n_tiles) {
-    rows_of(it, sb, r0, r1);
-    load(k, v, cr, r0, r1);
-  }
-  while (it < n_tiles) {
-    if (tid == 0) {  // the next tile and its sub-bucket, read after the staging barrier
-      const uint32_t t = atomicAdd(a.flags + 2, 1u);
-      claim[par] = t;
-      claim[2 + par] = t < n_tiles ? locate(t) : 0u;
-    }
-    const uint32_t g = sb;
-    uint32_t nit = 0, nsb = 0, nr0 = 0, nr1 = 0;
-    auto reserve = [&](uint32_t d, uint32_t c) {
-      return __ldcg(a.sub3_off + g * 256 + d) + atomicAdd(a.cur24 + g * 256 + d, c);
+  if (d.x != ~0u) load(k, v, cr, d);
+  while (d.x != ~0u) {
+    const uint32_t g = d.x;
+    uint4 nd = no_tile();
+    auto reserve = [&](uint32_t dg, uint32_t c) {
+      return make_uint2(__ldcg(a.sub3_off + g * 256 + dg), atomicAdd(a.cur24 + g * 256 + dg, c));
     };
-    ptile_scatter<5 * kBits, PK, CW>(k, v, cr, int(r1 - r0), s, a.keys_b, a.vals_b, a.pay_b, reserve,
-                                     [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
-                                       nit = claim[par];
-                                       nsb = claim[2 + par];
-                                       if (nit < n_tiles) {
-                                         rows_of(nit, nsb, nr0, nr1);
-                                         load(kk, vv, cc, nr0, nr1);
-                                       }
-                                     });
-    it = nit;
-    sb = nsb;
-    r0 = nr0;
-    r1 = nr1;
+    ptile_scatter<5 * kBits, PK, CW>(
+        k, v, cr, int(d.z - d.y), s, a.keys_b, a.vals_b, a.pay_b, reserve,
+        [&](uint64_t (&kk)[kPItems], uint32_t (&vv)[kPItems], Carry<CW>& cc) {
+          nd = slot[par ^ 1];
+          if (nd.x != ~0u) load(kk, vv, cc, nd);
+        },
+        [&]() {
+          if (tid == kClaimer) {
+            slot[par ^ 1] = ahead < n_tiles ? __ldcg(tdesc + ahead) : no_tile();
+            if (ahead < n_tiles) ahead = atomicAdd(a.flags + 2, 1u);
+          }
+        });
+    d = nd;
     par ^= 1;
   }
 }
@@ -2435,7 +2476,7 @@ static void carve_all(C& c, int64_t n, T32 t32, T64 t64, Layout* L, bool force_s
   auto s3 = lvl3 ? t32(c, size_t(kSub3) + 1) : nullptr;
   auto c24 = lvl3 ? t32(c, size_t(kSub3)) : nullptr;
   auto t3 = lvl3 ? t32(c, size_t(kSubBuckets) + 1) : nullptr;
-  auto tm = lvl3 ? t32(c, size_t(kSubBuckets) + size_t(n / kPTile) + 1) : nullptr;  // <= one partial tile a sub-bucket
+  auto tm = lvl3 ? t32(c, 4 * (size_t(kSubBuckets) + size_t(n / kPTile) + 1)) : nullptr;  // <= one partial tile a sub-bucket
   if (L) *L = Layout{h, tc, gb, fl, st, zero, head, so, ka, kb, va, vb, cc, c7, c16, d7r, db, it, me, s3, c24, t3, tm};
 }
 
@@ -3247,3 +3288,15 @@ int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t
 
 }  // namespace radix
 }  // namespace rl
+
+#ifdef RL_PASS_PROFILE
+extern "C" __attribute__((visibility("default"))) int rl_debug_pass_prof(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out16, rl::radix::g_pass_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(rl::radix::g_pass_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

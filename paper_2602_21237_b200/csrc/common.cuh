@@ -71,6 +71,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // release: prior accesses of this thread
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_inval(uint64_t* bar) {
   asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -159,7 +162,15 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* warp_sums, T* total) {
 // as uint4 by consecutive lanes — conflict-free, where a thread owning
 // consecutive bins strides the banks. `warp_tot` holds THREADS / 32 words.
 // Ends with the block synchronised.
-template <int THREADS, int NBINS>
+// BAR > 0: the threads [0, THREADS) synchronise on named barrier BAR (a
+// producer warp beside them does not take part), else the whole block.
+template <int THREADS, int BAR>
+__device__ __forceinline__ void threads_sync() {
+  if constexpr (BAR > 0) asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(THREADS) : "memory");
+  else __syncthreads();
+}
+
+template <int THREADS, int NBINS, int BAR = 0>
 __device__ __forceinline__ void scan_counters(uint32_t* hist, uint32_t nbins, uint32_t* warp_tot) {
   constexpr int kWarps = THREADS / 32;
   constexpr uint32_t W = uint32_t(NBINS / kWarps), C = W / 128;
@@ -179,7 +190,7 @@ __device__ __forceinline__ void scan_counters(uint32_t* hist, uint32_t nbins, ui
   }
   wt = __reduce_add_sync(0xffffffffu, wt);
   if (lane == 0) warp_tot[warp] = wt;
-  __syncthreads();
+  threads_sync<THREADS, BAR>();
   uint32_t start = 0;
   for (uint32_t w = 0; w < warp; ++w) start += warp_tot[w];
 #pragma unroll
@@ -203,7 +214,7 @@ __device__ __forceinline__ void scan_counters(uint32_t* hist, uint32_t nbins, ui
     }
     start += __shfl_sync(0xffffffffu, incl, 31);
   }
-  __syncthreads();
+  threads_sync<THREADS, BAR>();
 }
 
 // Single-value decoupled look-back: returns the exclusive prefix of tile

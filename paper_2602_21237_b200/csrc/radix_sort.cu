@@ -315,7 +315,7 @@ static_assert(kLocHistW + size_t(kLocalBinsBal) * 4 <= kLocBig, "idw: the counte
 // misc: [0] big count, [2..3] run-list sizes, [8..] scan scratch, [32..65] group offsets (x2),
 // [72..103] run ends (x2), [112..] run descriptors
 constexpr size_t kLocBars = kLocMisc + 128 * 4;
-constexpr size_t kLocalSmemBytes = kLocBars + 2 * 8;
+constexpr size_t kLocalSmemBytes = kLocBars + 4 * 8;  // full[2], empty[2] (the producer-warp kernels)
 // local_kernel only (not the cooperative kernel's budget): the three-level
 // path's group offsets and runs, [2][257] + [2][256]
 constexpr size_t kLocGrp = (kLocalSmemBytes + 15) / 16 * 16;
@@ -891,8 +891,8 @@ __device__ __forceinline__ PTile ptile(uint8_t* sm) {
 // counting barrier, beside the digit scan (warps 8..15 only reserve there).
 // CW > 0 (bucket join): CW payload words ride with every row (c.p), staged and
 // written to out_p[o * CW + w] beside the key.
-#ifdef RL_PASS_PROFILE  // per-phase clock totals of the counting passes (A/B builds only)
-__device__ unsigned long long g_pass_prof[16];
+#ifdef RL_PASS_PROFILE  // per-phase clock totals of the counting passes and the local phase (A/B builds only)
+__device__ unsigned long long g_pass_prof[32];
 #define PPROF(i, t) do { if (threadIdx.x == 0) { const long long c_ = clock64(); atomicAdd(&g_pass_prof[i], (unsigned long long)(c_ - t)); t = c_; } } while (0)
 #else
 #define PPROF(i, t) do { } while (0)
@@ -1767,7 +1767,12 @@ __device__ __forceinline__ void issue_run_w(const uint64_t* kin, const uint64_t*
 // BAL (the scatter path's large runs): a thread's rows in registers across
 // count + scatter, and the claimed group tail. The onesweep hybrid's short
 // runs (n < 4M) are faster without both (+1-5 us each at 0.3-2M rows).
-template <int THREADS, int PACK = 0, bool BAL = false, bool PK = false, int LEVELS = 2, int CW = 0>
+// PROD (the scatter path's kernels, THREADS + 32 threads): warp THREADS / 32
+// is a producer — it walks the groups, cuts the runs and issues every run's
+// TMA into a free buffer (full / empty mbarriers) — so the group bookkeeping
+// and the copy issue (~15 % of a run, measured) leave the consumers' path; the
+// consumers synchronise on named barrier 1.
+template <int THREADS, int PACK = 0, bool BAL = false, bool PK = false, int LEVELS = 2, int CW = 0, bool PROD = false>
 __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   // CW > 0 (packed rows): every row's payload words ride in pay_a / pay_b beside
   // its key; bv holds the row's load index in its run, and the emit copies the
@@ -1796,8 +1801,14 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   uint32_t* goff = LEVELS == 3 ? reinterpret_cast<uint32_t*>(smem + kLocGrp) : misc + 32;  // [2][G + 1]
   uint32_t* gends = LEVELS == 3 ? goff + 2 * GO : misc + 72;                              // [2][G]
   uint32_t* runs = misc + 112;  // [2][4] descriptors of the run in each buffer
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLocBars);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kLocBars);  // [0..1] full (data landed), PROD: [2..3] empty
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  static_assert(!PROD || BAL, "the producer warp serves the in-place runs");
+  constexpr int kPW = PROD ? THREADS / 32 : 0;  // the warp that walks the groups
+  auto csync = [&]() {  // the run's threads (PROD: the consumers only)
+    if constexpr (PROD) asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory");
+    else __syncthreads();
+  };
   const uint64_t* kin = src == 1 ? a.keys_a : a.keys_b;
   const uint32_t* vin = PK ? nullptr : src == 1 ? a.vals_a : a.vals_b;
   const int desc = a.key_mode == kRawDesc;
@@ -1834,10 +1845,14 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   auto fetch_next = [&]() {
     if constexpr (G <= 31) next_off = lane <= uint32_t(G) && next_g < kGroups ? __ldcg(sub_off + size_t(next_g) * G + lane) : 0u;
   };
-  if (warp == 0) {
+  if (warp == kPW) {
     if (lane == 0) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
+      if constexpr (PROD) {
+        mbar_init(&bars[2], 1);
+        mbar_init(&bars[3], 1);
+      }
       gid[0] = g0;
     }
     for (uint32_t i = lane; i <= uint32_t(G); i += 32) goff[i] = __ldcg(sub_off + size_t(g0) * G + i);
@@ -1872,7 +1887,43 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
   const uint32_t pshl = pack_shift(pcode);
   // run cursor: group k (g = g0 + k gstep), run r of that group; identical in every thread
   uint32_t k = 0, r = 0, buf = 0, phase0 = 0, phase1 = 0;
-  bool have = misc[2] > 0;
+  if constexpr (PROD) {
+    if (warp == kPW) {  // ---- the producer: run q goes into buffer q & 1 once run q - 2 released it
+      for (uint32_t q = 0;; ++q, ++r) {
+        bool ok = true;
+        while (r >= misc[2 + (k & 1)]) {  // past the group's runs (or an empty group): the next group
+          if (!advance((k + 1) & 1)) {
+            ok = false;
+            break;
+          }
+          ++k;
+          r = 0;
+        }
+        const uint32_t b = q & 1;
+        if (q >= 2) mbar_wait(&bars[2 + b], ((q >> 1) + 1) & 1);
+        if (lane == 0) {
+          uint32_t* d = runs + b * 4;
+          if (ok) {
+            const uint32_t* off = goff + (k & 1) * GO;
+            const uint32_t se = gends[(k & 1) * G + r];
+            const uint32_t base = off[se >> 16], cnt = off[se & 0xFFFFu] - base;
+            d[0] = base;
+            d[1] = cnt;
+            d[2] = gid[k & 1] * G + (se >> 16);
+            d[3] = (se & 0xFFFFu) - (se >> 16);
+            if constexpr (IDW) issue_run_w(kin, pay, base, cnt, smem + kLocA + b * kABytes, &bars[b]);
+            else issue_run(kin, vin, base, cnt, smem + kLocA + b * kLocABytes, &bars[b]);
+          } else {
+            d[1] = ~0u;  // no run left: the consumers stop
+            mbar_arrive(&bars[b]);
+          }
+        }
+        __syncwarp();
+        if (!ok) return;
+      }
+    }
+  }
+  bool have = PROD || misc[2] > 0;
   // an empty first group: advance (rare; only tiny inputs have empty groups)
   while (!have) {
     __syncthreads();
@@ -1885,7 +1936,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     if (!misc[7]) return;
     have = misc[2 + (k & 1)] > 0;
   }
-  if (tid == 0) {
+  if (!PROD && tid == 0) {
     const uint32_t* off = goff + (k & 1) * GO;
     const uint32_t se = gends[(k & 1) * G];
     const uint32_t base = off[se >> 16], cnt = off[se & 0xFFFFu] - base;
@@ -1896,9 +1947,30 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     if constexpr (IDW) issue_run_w(kin, pay, base, cnt, smem + kLocA, &bars[0]);
     else issue_run(kin, vin, base, cnt, smem + kLocA, &bars[0]);
   }
-  __syncthreads();  // the first run's descriptor is visible to every thread
+  if constexpr (!PROD) __syncthreads();  // the first run's descriptor is visible to every thread
+  uint32_t q = 0;  // PROD: runs taken
 
+#ifdef RL_PASS_PROFILE
+  long long lpt = clock64();
+#define LPROF(i) do { if (BAL && CW == 0 && LEVELS == 2) PPROF(16 + (i), lpt); } while (0)
+#else
+#define LPROF(i) do { } while (0)
+#endif
   while (true) {
+    LPROF(7);  // (the end of the previous run's big bins)
+    uint32_t first, nsb, bb, nbins, next_k = 0, next_r = 0;
+    bool more = false;
+    if constexpr (PROD) {  // the producer's run q (or the stop mark) in buffer q & 1
+      buf = q & 1;
+      for (uint32_t i = tid; i < uint32_t(kNBins / 4); i += THREADS) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
+      mbar_wait(&bars[buf], (q >> 1) & 1);
+      if (runs[buf * 4 + 1] == ~0u) break;
+      first = runs[buf * 4 + 2];
+      nsb = runs[buf * 4 + 3];
+      bb = kBinBits - (nsb > 1 ? 32u - uint32_t(__clz(int(nsb - 1))) : 0u);
+      nbins = nsb << bb;
+      csync();  // hist zeroed
+    } else {
     // ---- warp 0: find and prefetch the next run into the other buffer
     if (warp == 0) {
       uint32_t nk = k, nr = r + 1;
@@ -1911,6 +1983,7 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         ++nk;
         nr = 0;
       }
+      LPROF(6);  // (warp 0: the next group's offsets and runs)
       if (lane == 0) {
         misc[4] = ok ? 1u : 0u;
         misc[5] = nk;
@@ -1933,18 +2006,23 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     // bins of this run: (sub-bucket, the next bb key bits), run-relative; the
     // fewer sub-buckets a run holds, the more bits each gets (4096 bins at most:
     // a run of one big sub-bucket is split 4096 ways, not 256)
-    const uint32_t first = runs[buf * 4 + 2], nsb = runs[buf * 4 + 3];
-    const uint32_t bb = kBinBits - (nsb > 1 ? 32u - uint32_t(__clz(int(nsb - 1))) : 0u);
-    const uint32_t nbins = nsb << bb;
+    first = runs[buf * 4 + 2];
+    nsb = runs[buf * 4 + 3];
+    bb = kBinBits - (nsb > 1 ? 32u - uint32_t(__clz(int(nsb - 1))) : 0u);
+    nbins = nsb << bb;
+    LPROF(0);  // warp 0's prefetch of the next run
     for (uint32_t i = tid; i < nbins / 4; i += THREADS) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
     mbar_wait(&bars[buf], buf ? phase1 : phase0);
     if (buf) phase1 ^= 1;
     else phase0 ^= 1;
     __syncthreads();  // hist zeroed, run descriptors and next-run fields visible
+    LPROF(1);  // zeroing + this run's data + barrier
     // the next-run fields go to registers now: warp 0 rewrites them at the top
     // of the next run, with no barrier at the end of this one
-    const bool more = misc[4] != 0;
-    const uint32_t next_k = misc[5], next_r = misc[6];
+    more = misc[4] != 0;
+    next_k = misc[5];
+    next_r = misc[6];
+    }
     if (tid == 0) misc[0] = 0;  // big-bin list: appended after later barriers, read after the rank loop
     const uint32_t base = runs[buf * 4], cnt = runs[buf * 4 + 1];
     uint8_t* abuf = smem + kLocA + buf * kABytes;
@@ -1973,8 +2051,10 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
     } else {
       for (uint32_t j = tid; j < cnt; j += THREADS) atomicAdd(&hist[bin_of(ak[j])], 1u);
     }
-    __syncthreads();
-    scan_counters<THREADS, kNBins>(hist, nbins, misc + 8);  // (ends synchronised)
+    csync();
+    LPROF(2);  // counting
+    scan_counters<THREADS, kNBins, PROD ? 1 : 0>(hist, nbins, misc + 8);  // (ends synchronised)
+    LPROF(3);  // scan
     if constexpr (BAL) {
       uint32_t pos[kRows];
 #pragma unroll
@@ -1999,7 +2079,8 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         else if constexpr (CW > 0) bv[pos] = j;
       }
     }
-    __syncthreads();
+    csync();
+    LPROF(4);  // scatter into bins
     // hist[b] is now the end of bin b; a bin holds the rows equal in their
     // top 24 bits (~1 for uniform keys). Each row takes its rank by (key,
     // row id) among its bin's rows and goes straight to its final position;
@@ -2065,7 +2146,11 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
       }
       emit(pos, key, v);
     }
-    __syncthreads();
+    csync();
+    LPROF(5);  // rank + emit
+#ifdef RL_PASS_PROFILE
+    if (BAL && CW == 0 && LEVELS == 2 && tid == 0) atomicAdd(&g_pass_prof[24], 1ull);
+#endif
     const uint32_t nbig = min(misc[0], uint32_t(kBigList));
     for (uint32_t t = warp; t < nbig; t += kLWarps) {
       const int b = int(big[t]);
@@ -2078,7 +2163,12 @@ __device__ void local_phase(const SortArgs& a, uint8_t* smem, uint32_t src) {
         for (uint32_t p = b0 + lane; p < b1; p += 32) emit(p, bk[p], PK && CW == 0 ? 0u : bv[p]);
       }
     }
-    if (nbig) __syncthreads();  // (the rank loop's reads of B/hist ended at the barrier before nbig)
+    if (nbig) csync();  // (the rank loop's reads of B/hist ended at the barrier before nbig)
+    if constexpr (PROD) {  // this run's buffer is free for the producer
+      if (tid == 0) mbar_arrive(&bars[2 + buf]);
+      ++q;
+      continue;
+    }
     if (!more) break;
     k = next_k;
     r = next_r;
@@ -2183,9 +2273,47 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_ker
   }
 }
 
+// The scatter path's two-level local phase with a producer warp (kLocalThreads
+// consumers + 32): the rows sit in their sub-buckets in keys_a / vals_a.
+constexpr int kLocalWsThreads = kLocalThreads + 32;
+__global__ void __launch_bounds__(kLocalWsThreads, 1024 / kLocalThreads) local_ws_kernel(SortArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const bool stamper = a.stamps && blockIdx.x == 0 && threadIdx.x == 0;
+  pdl_wait();  // the digit-6 pass
+  pdl_launch_dependents();
+  if (stamper) a.stamps[1] = globaltimer();
+  if (local_fallback(a)) return;  // (final before this launch: uniform)
+  const uint32_t pc = __ldcg(a.flags + 6);
+  if (threadIdx.x == 0) {  // key pack code and constant bits, read by the local phase after its first barrier
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kLocMisc);
+    const uint64_t cb = pack_mode(pc) ? key_constbits(a, pc) : 0ull;
+    misc[125] = pc;
+    misc[126] = uint32_t(cb);
+    misc[127] = uint32_t(cb >> 32);
+  }
+  const bool pk = packed_rows(pc, a);
+  switch (pack_mode(pc)) {
+    case 0: local_phase<kLocalThreads, 0, true, false, 2, 0, true>(a, smem, 1u); break;
+    case 1:
+      if (pk) local_phase<kLocalThreads, 1, true, true, 2, 0, true>(a, smem, 1u);
+      else local_phase<kLocalThreads, 1, true, false, 2, 0, true>(a, smem, 1u);
+      break;
+    default:
+      if (pk) local_phase<kLocalThreads, 2, true, true, 2, 0, true>(a, smem, 1u);
+      else local_phase<kLocalThreads, 2, true, false, 2, 0, true>(a, smem, 1u);
+      break;
+  }
+  if (a.stamps && threadIdx.x == 0)  // (profiling: the last CTA's end, pass-6 slot unused here)
+    atomicMax(reinterpret_cast<unsigned long long*>(a.stamps + 8), (unsigned long long)globaltimer());
+  if (stamper) {
+    a.stamps[kStamps - 2] = globaltimer();
+    a.stamps[kStamps - 1] = 3;
+  }
+}
+
 // The three-level local phase on its own kernel (the two-level kernel's code
 // stays as tuned): runs of (d7, d6, d5) sub-sub-buckets out of keys_b.
-__global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local3_kernel(SortArgs a) {
+__global__ void __launch_bounds__(kLocalWsThreads, 1024 / kLocalThreads) local3_kernel(SortArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   pdl_wait();  // the digit-5 pass
   pdl_launch_dependents();
@@ -2200,14 +2328,14 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local3_ke
   }
   const bool pk = packed_rows(pc, a);
   switch (pack_mode(pc)) {
-    case 0: local_phase<kLocalThreads, 0, true, false, 3>(a, smem, 2u); break;
+    case 0: local_phase<kLocalThreads, 0, true, false, 3, 0, true>(a, smem, 2u); break;
     case 1:
-      if (pk) local_phase<kLocalThreads, 1, true, true, 3>(a, smem, 2u);
-      else local_phase<kLocalThreads, 1, true, false, 3>(a, smem, 2u);
+      if (pk) local_phase<kLocalThreads, 1, true, true, 3, 0, true>(a, smem, 2u);
+      else local_phase<kLocalThreads, 1, true, false, 3, 0, true>(a, smem, 2u);
       break;
     default:
-      if (pk) local_phase<kLocalThreads, 2, true, true, 3>(a, smem, 2u);
-      else local_phase<kLocalThreads, 2, true, false, 3>(a, smem, 2u);
+      if (pk) local_phase<kLocalThreads, 2, true, true, 3, 0, true>(a, smem, 2u);
+      else local_phase<kLocalThreads, 2, true, false, 3, 0, true>(a, smem, 2u);
       break;
   }
 }
@@ -2217,7 +2345,7 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local3_ke
 // of the run's payload window): its own kernel, so the plain sort's local
 // kernels keep their code.
 template <int LEVELS>
-__global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_carry_kernel(SortArgs a) {
+__global__ void __launch_bounds__(kLocalWsThreads, 1024 / kLocalThreads) local_carry_kernel(SortArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   pdl_wait();
   pdl_launch_dependents();
@@ -2233,19 +2361,19 @@ __global__ void __launch_bounds__(kLocalThreads, 1024 / kLocalThreads) local_car
   constexpr uint32_t src = LEVELS == 3 ? 2u : 1u;
   if (!packed_rows(pc, a)) {  // idw (the counting passes declined anything else)
     switch (pack_mode(pc)) {
-      case 0: local_phase<kLocalThreads, 0, true, false, LEVELS, 1>(a, smem, src); break;
-      case 1: local_phase<kLocalThreads, 1, true, false, LEVELS, 1>(a, smem, src); break;
-      default: local_phase<kLocalThreads, 2, true, false, LEVELS, 1>(a, smem, src); break;
+      case 0: local_phase<kLocalThreads, 0, true, false, LEVELS, 1, true>(a, smem, src); break;
+      case 1: local_phase<kLocalThreads, 1, true, false, LEVELS, 1, true>(a, smem, src); break;
+      default: local_phase<kLocalThreads, 2, true, false, LEVELS, 1, true>(a, smem, src); break;
     }
     return;
   }
   const bool m1 = pack_mode(pc) == 1;  // (packed rows: mode 1 or 2, checked by the counting passes)
   if (a.cw == 1) {
-    if (m1) local_phase<kLocalThreads, 1, true, true, LEVELS, 1>(a, smem, src);
-    else local_phase<kLocalThreads, 2, true, true, LEVELS, 1>(a, smem, src);
+    if (m1) local_phase<kLocalThreads, 1, true, true, LEVELS, 1, true>(a, smem, src);
+    else local_phase<kLocalThreads, 2, true, true, LEVELS, 1, true>(a, smem, src);
   } else {
-    if (m1) local_phase<kLocalThreads, 1, true, true, LEVELS, 2>(a, smem, src);
-    else local_phase<kLocalThreads, 2, true, true, LEVELS, 2>(a, smem, src);
+    if (m1) local_phase<kLocalThreads, 1, true, true, LEVELS, 2, true>(a, smem, src);
+    else local_phase<kLocalThreads, 2, true, true, LEVELS, 2, true>(a, smem, src);
   }
 }
 
@@ -2524,6 +2652,8 @@ static bool scatter_kernels_ready() {
                                     int(kLocalSmemBytes)) == cudaSuccess &&
                cudaFuncSetAttribute(local3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kLocalKernelSmem)) == cudaSuccess &&
+               cudaFuncSetAttribute(local_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kLocalSmemBytes)) == cudaSuccess &&
                cudaFuncSetAttribute(local_carry_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kLocalSmemBytes)) == cudaSuccess &&
                cudaFuncSetAttribute(local_carry_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2731,10 +2861,10 @@ static int launch_sort(SortArgs a, const Layout& L, cudaStream_t stream, void* c
     else if (a.cw == 2) e = passes(std::integral_constant<int, 2>{});
     else e = passes(std::integral_constant<int, 0>{});
     if (e != cudaSuccess) return rl_cuda_status(e);
-    if (a.cw > 0 && a.levels == 3) e = launch_dep(local_carry_kernel<3>, lgrid, kLocalThreads, kLocalKernelSmem);
-    else if (a.cw > 0) e = launch_dep(local_carry_kernel<2>, lgrid, kLocalThreads, kLocalSmemBytes);
-    else if (a.levels == 3) e = launch_dep(local3_kernel, lgrid, kLocalThreads, kLocalKernelSmem);
-    else e = launch_dep(local_kernel, lgrid, kLocalThreads, kLocalSmemBytes);
+    if (a.cw > 0 && a.levels == 3) e = launch_dep(local_carry_kernel<3>, lgrid, kLocalWsThreads, kLocalKernelSmem);
+    else if (a.cw > 0) e = launch_dep(local_carry_kernel<2>, lgrid, kLocalWsThreads, kLocalSmemBytes);
+    else if (a.levels == 3) e = launch_dep(local3_kernel, lgrid, kLocalWsThreads, kLocalKernelSmem);
+    else e = launch_dep(local_ws_kernel, lgrid, kLocalWsThreads, kLocalSmemBytes);
     if (e != cudaSuccess) return rl_cuda_status(e);
     chk("local");
     if (events) cudaEventRecord(static_cast<cudaEvent_t>(events[1]), stream);
@@ -3292,11 +3422,12 @@ int bj_partition(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t
 #ifdef RL_PASS_PROFILE
 extern "C" __attribute__((visibility("default"))) int rl_debug_pass_prof(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();
-  if (cudaMemcpyFromSymbol(out16, rl::radix::g_pass_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out16, rl::radix::g_pass_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[32] = {};
     cudaMemcpyToSymbol(rl::radix::g_pass_prof, z, sizeof(z));
   }
   return 0;
 }
 #endif
+static_assert(2 * (rl::radix::kLocalKernelSmem + 1024) <= 228 * 1024, "two local-phase CTAs an SM");

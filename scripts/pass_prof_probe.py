@@ -21,7 +21,7 @@ def main():
     rel = synth.cfg2_relation(n)
     keys = torch.from_numpy(rel.column("key").copy()).cuda()
     sk = torch.empty_like(keys)
-    buf = (ctypes.c_ulonglong * 16)()
+    buf = (ctypes.c_ulonglong * 32)()
     engine.sort_permutation([engine.SortAxis(keys)], n, keys.device, sorted_keys_out=sk)
     prof(buf, 1)
     for _ in range(reps):
@@ -35,6 +35,12 @@ def main():
         print(f"{name}: {tiles // reps} tiles/sort, cycles per tile: " + ", ".join(
             f"{k} {v[o + i] / tiles:.0f} ({v[o + i] / tot:.0%})"
             for i, k in zip(idx, ["atomics+load wait", "scan", "staging", "next loads", "write-out"])))
+
+    runs = v[24] or 1
+    names = ["prefetch: TMA issue (warp 0)", "zero+data+barrier", "count", "scan", "scatter", "rank+emit", "prefetch: groups (warp 0)", "big bins"]
+    tot = sum(v[16 + i] for i in (0, 1, 2, 3, 4, 5, 6, 7)) or 1
+    print(f"local phase: {runs // reps} runs/sort, cycles per run: " + ", ".join(
+        f"{names[i]} {v[16 + i] / runs:.0f} ({v[16 + i] / tot:.0%})" for i in (6, 0, 1, 2, 3, 4, 5, 7)))
 
 
 if __name__ == "__main__":

@@ -86,12 +86,21 @@ __device__ __forceinline__ uint32_t cut_runs(const uint32_t* ol, const uint32_t*
     ends[0] = uint32_t(G);
     return 1;
   }
+  // greedy: a run from s takes the most sub-buckets that fit (at least one);
+  // the fit is monotone in the end (prefix offsets), so each end is a binary
+  // search — ~8 dependent steps a run instead of one a sub-bucket (G = 256:
+  // this cut ran on one thread while the block waited)
   uint32_t nr = 0, s = 0;
   while (s < uint32_t(G)) {
-    uint32_t e = s + 1;
-    while (e < uint32_t(G) && ol[e + 1] - ol[s] <= uint32_t(kBjCap) && orr[e + 1] - orr[s] <= uint32_t(kBjCap)) ++e;
-    ends[nr++] = (s << 16) | e;
-    s = e;
+    const uint32_t bl = ol[s], br = orr[s];
+    uint32_t lo = s + 1, hi = uint32_t(G);  // the end is in [lo, hi]
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (ol[mid] - bl <= uint32_t(kBjCap) && orr[mid] - br <= uint32_t(kBjCap)) lo = mid;
+      else hi = mid - 1;
+    }
+    ends[nr++] = (s << 16) | lo;
+    s = lo;
   }
   return nr;
 }
@@ -369,6 +378,13 @@ __device__ __forceinline__ void finish_sort(uint64_t* grouped, uint64_t* sorted,
   __syncthreads();
 }
 
+#ifdef RL_BJ_PROFILE  // per-phase clock totals of the emit (A/B builds only)
+__device__ unsigned long long g_bj_prof[16];
+#define BJPROF(i) do { if (threadIdx.x == 0) { const long long c_ = clock64(); atomicAdd(&g_bj_prof[i], (unsigned long long)(c_ - bjt)); bjt = c_; } } while (0)
+#else
+#define BJPROF(i) do { } while (0)
+#endif
+
 template <bool CHECKSUM, int LEVELS>  // CHECKSUM: sum fmix64(l << 32 | r) over the pairs into *e.checksum instead
 __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols cols) {
   using Q = Geo<LEVELS>;
@@ -383,8 +399,8 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
   uint16_t* lidx = gidx + kBjCap;                                 // [kBjCap] load index of sorted left rows
   uint16_t* ridx = lidx + kBjCap;                                 // [kBjCap] ... right rows
   uint64_t* scratch = reinterpret_cast<uint64_t*>(ridx + kBjCap);  // [kThreads / 32 + 2]
-  uint64_t* rpre = scratch + kThreads / 32 + 2;                    // [kMaxG] run starts in the group
-  uint32_t* misc = reinterpret_cast<uint32_t*>(rpre + kMaxG);      // offsets, runs, big bins
+  uint64_t* rpre = scratch + kThreads / 32 + 2;                    // [kMaxG + 1] run starts in the group
+  uint32_t* misc = reinterpret_cast<uint32_t*>(rpre + kMaxG + 1);  // offsets, runs, big bins
   uint32_t* offl = misc;                     // [kMaxG + 1]
   uint32_t* offr = misc + (kMaxG + 1);       // [kMaxG + 1]
   uint32_t* ends = misc + 2 * (kMaxG + 1);   // [kMaxG]
@@ -405,6 +421,9 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
     const uint64_t u = mode == 1 ? (v >> shl) | constbits : radix::unpack_key(v, code, constbits);
     return (long long)radix::xform(u, 0);
   };
+#ifdef RL_BJ_PROFILE
+  long long bjt = clock64();
+#endif
   for (uint32_t g = blockIdx.x; g < Q::kGroups; g += gridDim.x) {
     const uint64_t gbase = __ldcg(a.gtot + g);  // the group's first output row (scanned)
     for (uint32_t i = tid; i <= uint32_t(G); i += kThreads) {
@@ -415,15 +434,16 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
     if (tid == 0) *nruns = cut_runs<G>(offl, offr, ends);
     __syncthreads();
     const uint32_t nr = *nruns;
-    {  // run starts inside the group
+    {  // run starts inside the group (and the run's pair count: rpre[r + 1] - rpre[r])
       const uint64_t c = tid < int(nr) ? uint64_t(__ldcg(a.counts + size_t(g) * G + tid)) : 0ull;
       uint64_t tot;
       const uint64_t ex = block_exclusive_scan<kThreads>(c, scratch, &tot);
       if (tid < int(nr)) rpre[tid] = ex;
+      if (tid == 0) rpre[nr] = tot;
       __syncthreads();
     }
     for (uint32_t r = 0; r < nr; ++r) {
-      const uint32_t cnt_pairs = __ldcg(a.counts + size_t(g) * G + r);
+      const uint32_t cnt_pairs = uint32_t(rpre[r + 1] - rpre[r]);
       const uint64_t base = gbase + rpre[r];
       if (cnt_pairs == 0 || base + cnt_pairs <= e.out_begin || base >= e.out_end) continue;  // uniform
       const uint32_t s = ends[r] >> 16, en = ends[r] & 0xFFFFu;
@@ -442,17 +462,21 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         }
       }
       uint64_t w[kRowsPerThread], wl[kRowsPerThread];
+      BJPROF(7);  // group setup / skipped runs
       load_rows(a.rows_l, l0, nl, wl);
       load_rows(a.rows_r, r0, nrr, w);
       __syncthreads();
+      BJPROF(0);  // run setup, prefetch issue, row loads
       // left side sorted first; the bin counters then serve the right side and
       // keep its bin ends for the match
       bin_rows(wl, nl, bins, nbins, hr, gx, scratch, gidx);
       finish_sort(gx, sl, hr, bins, nl, big, nbig, gidx, lidx);
+      BJPROF(1);  // left side binned + sorted
       for (uint32_t i = tid; i < nbins; i += kThreads) hr[i] = 0;
       __syncthreads();
       bin_rows(w, nrr, bins, nbins, hr, gx, scratch, gidx);
       finish_sort(gx, sr, hr, bins, nrr, big, nbig, gidx, ridx);
+      BJPROF(2);  // right side binned + sorted
       // every left row (sorted index p): its matching right range [rs, rs + m) in sr
       uint32_t* m_arr = reinterpret_cast<uint32_t*>(gx);
       uint32_t* rs_arr = m_arr + kBjCap;
@@ -496,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       // otherwise output-space: every thread takes outputs t and finds its
       // left row by binary search over the prefixes
       __syncthreads();  // prefixes (m_arr) and right starts (rs_arr) complete
+      BJPROF(3);  // match ranges + prefix
       // (measured: one thread per left row writing its pairs was slower than the
       // search — divergent pair counts, gaps in the output runs)
       constexpr bool per_row = false;
@@ -594,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
           }
         }
         __syncthreads();
+        BJPROF(4);  // output -> left row map
         if (CHECKSUM || hi - lo < uint64_t(2 * kThreads)) {  // (a selective run: a few outputs)
           for (uint64_t t = lo + tid; t < hi; t += kThreads) write(map[t], uint32_t(t));
         } else {
@@ -679,6 +705,10 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         }
       }
       __syncthreads();  // smem reused by the next run
+      BJPROF(5);  // outputs written
+#ifdef RL_BJ_PROFILE
+      if (threadIdx.x == 0) atomicAdd(&g_bj_prof[8], 1ull);
+#endif
     }
   }
   if constexpr (CHECKSUM) {  // mod 2^64: one atomic per warp
@@ -689,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
 }
 
 constexpr size_t kEmitSmem = size_t(kBjCap) * 8 * 3 + size_t(kMaxBins) * 4 * 2 + size_t(kBjCap) * 2 * 3 +
-                             (kThreads / 32 + 2) * 8 + size_t(kMaxG) * 8 + (3 * kMaxG + 2 + 64 + 4) * 4;
+                             (kThreads / 32 + 2) * 8 + size_t(kMaxG + 1) * 8 + (3 * kMaxG + 2 + 64 + 4) * 4;
 
 // ---------------------------------------------------------------- host
 static size_t side_bytes(int64_t n, int words, int levels) {
@@ -906,3 +936,15 @@ RL_API int rl_bjoin_pair_checksum(const rl_bjoin_plan* plan, uint64_t out_begin,
 }
 
 }  // extern "C"
+
+#ifdef RL_BJ_PROFILE
+extern "C" __attribute__((visibility("default"))) int rl_debug_bj_prof(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out16, rl::bjoin::g_bj_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(rl::bjoin::g_bj_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -378,6 +378,136 @@ __device__ __forceinline__ void finish_sort(uint64_t* grouped, uint64_t* sorted,
   __syncthreads();
 }
 
+// Both sides of a run sorted by packed word in ONE set of barrier phases: the
+// bin counters hold the left count in the low 16 bits and the right count in
+// the high 16 (<= kBjCap rows a side, so one packed scan gives both sides'
+// starts), and the left rows go grouped-by-bin into `grouped` and then ranked
+// into `sl` while the right rows are grouped straight into `sr` and ranked in
+// place (new slots kept in registers across the barrier). On return hist[b]
+// holds both sides' bin ends (left: low half, right: high half).
+__device__ __forceinline__ void sort_both(const uint64_t (&wl)[kRowsPerThread], uint32_t nl,
+                                          const uint64_t (&wr)[kRowsPerThread], uint32_t nrr, const Bins& bins,
+                                          uint32_t nbins, uint32_t* hist, uint64_t* grouped, uint64_t* sl,
+                                          uint64_t* sr, uint16_t* gidx, uint16_t* lidx, uint16_t* ridx,
+                                          uint64_t* scan_scratch, uint32_t* big, uint32_t* nbig) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    if (tid + u * kThreads < int(nl)) atomicAdd(&hist[bins.of(wl[u])], 1u);
+    if (tid + u * kThreads < int(nrr)) atomicAdd(&hist[bins.of(wr[u])], 1u << 16);
+  }
+  if (tid == 0) *nbig = 0;
+  __syncthreads();
+  scan_counters<kThreads, kMaxBins>(hist, nbins, reinterpret_cast<uint32_t*>(scan_scratch));  // (synchronised)
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    const uint16_t j = uint16_t(tid + u * kThreads);  // the row's load index in its run
+    if (j < nl) {
+      const uint32_t at = atomicAdd(&hist[bins.of(wl[u])], 1u) & 0xFFFFu;
+      grouped[at] = wl[u];
+      gidx[at] = j;
+    }
+    if (j < nrr) {
+      const uint32_t at = atomicAdd(&hist[bins.of(wr[u])], 1u << 16) >> 16;
+      sr[at] = wr[u];
+      ridx[at] = j;
+    }
+  }
+  __syncthreads();
+  // rank among bin-mates (the packed words are unique); bins above kRankMax
+  // rows are listed (bit 31: right side) for a warp's bitonic network
+  uint64_t mv[kRowsPerThread];
+  uint32_t mp[kRowsPerThread];  // right rows: new slot << 16 | load index, or ~0u (stays)
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    const uint32_t p = tid + u * kThreads;
+    if (p < nl) {
+      const uint64_t w = grouped[p];
+      const uint32_t b = bins.of(w);
+      const uint32_t b0 = b ? hist[b - 1] & 0xFFFFu : 0u, b1 = hist[b] & 0xFFFFu;
+      if (b1 - b0 > uint32_t(kRankMax)) {
+        if (p == b0) {
+          const uint32_t slot = atomicAdd(nbig, 1u);
+          if (slot < 128u) big[slot] = b;
+        }
+      } else {
+        uint32_t rk = 0;
+        for (uint32_t i = b0; i < b1; ++i) rk += grouped[i] < w ? 1u : 0u;
+        sl[b0 + rk] = w;
+        lidx[b0 + rk] = gidx[p];
+      }
+    }
+    mp[u] = ~0u;
+    mv[u] = 0;
+    if (p < nrr) {
+      const uint64_t w = sr[p];
+      const uint32_t b = bins.of(w);
+      const uint32_t b0 = b ? hist[b - 1] >> 16 : 0u, b1 = hist[b] >> 16;
+      if (b1 - b0 > uint32_t(kRankMax)) {
+        if (p == b0) {
+          const uint32_t slot = atomicAdd(nbig, 1u);
+          if (slot < 128u) big[slot] = b | 0x80000000u;
+        }
+      } else if (b1 - b0 > 1) {
+        uint32_t rk = 0;
+        for (uint32_t i = b0; i < b1; ++i) rk += sr[i] < w ? 1u : 0u;
+        if (b0 + rk != p) {
+          mv[u] = w;
+          mp[u] = ((b0 + rk) << 16) | ridx[p];
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    if (mp[u] != ~0u) {
+      sr[mp[u] >> 16] = mv[u];
+      ridx[mp[u] >> 16] = uint16_t(mp[u]);
+    }
+  }
+  const uint32_t nb = min(*nbig, 128u);  // <= 2 x kBjCap / (kRankMax + 1) = 104
+  for (uint32_t t = warp; t < nb; t += kThreads / 32) {
+    const uint32_t e = big[t];
+    const bool right = e >> 31;
+    const uint32_t b = e & 0x7FFFFFFFu;
+    const uint32_t sh = right ? 16u : 0u;
+    const uint32_t b0 = b ? (hist[b - 1] >> sh) & 0xFFFFu : 0u, b1 = (hist[b] >> sh) & 0xFFFFu;
+    uint64_t* arr = right ? sr : grouped;
+    uint16_t* ix = right ? ridx : gidx;
+    // bitonic over [b0, b1), padded to a power of two with +inf; the rows of a
+    // big bin are not moved by the rank writes above (disjoint slots)
+    const uint32_t sz = b1 - b0;
+    uint32_t p2 = 1;
+    while (p2 < sz) p2 <<= 1;
+    for (uint32_t k = 2; k <= p2; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t x = lane; x < (p2 >> 1); x += 32) {
+          const uint32_t i = (x / j) * (2 * j) + (x % j);
+          const uint32_t q = j == (k >> 1) ? (i ^ (k - 1)) : (i + j);
+          if (q < sz) {
+            const uint64_t a = arr[b0 + i], c = arr[b0 + q];
+            if (c < a) {
+              arr[b0 + i] = c;
+              arr[b0 + q] = a;
+              const uint16_t t2 = ix[b0 + i];
+              ix[b0 + i] = ix[b0 + q];
+              ix[b0 + q] = t2;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (!right)
+      for (uint32_t p = b0 + lane; p < b1; p += 32) {
+        sl[p] = grouped[p];
+        lidx[p] = gidx[p];
+      }
+  }
+  __syncthreads();
+}
+
 #ifdef RL_BJ_PROFILE  // per-phase clock totals of the emit (A/B builds only)
 __device__ unsigned long long g_bj_prof[16];
 #define BJPROF(i) do { if (threadIdx.x == 0) { const long long c_ = clock64(); atomicAdd(&g_bj_prof[i], (unsigned long long)(c_ - bjt)); bjt = c_; } } while (0)
@@ -404,8 +534,8 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
   uint32_t* offl = misc;                     // [kMaxG + 1]
   uint32_t* offr = misc + (kMaxG + 1);       // [kMaxG + 1]
   uint32_t* ends = misc + 2 * (kMaxG + 1);   // [kMaxG]
-  uint32_t* big = ends + kMaxG;              // [64]
-  uint32_t* nbig = big + 64;
+  uint32_t* big = ends + kMaxG;              // [128] big bins of both sides
+  uint32_t* nbig = big + 128;
   uint32_t* nruns = nbig + 1;
   const PlanArgs& a = e.p;
   const int tid = threadIdx.x;
@@ -469,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       BJPROF(0);  // run setup, prefetch issue, row loads
       // left side sorted first; the bin counters then serve the right side and
       // keep its bin ends for the match
+#ifdef RL_BJ_SEPARATE_SORTS  // (A/B: one side after the other)
       bin_rows(wl, nl, bins, nbins, hr, gx, scratch, gidx);
       finish_sort(gx, sl, hr, bins, nl, big, nbig, gidx, lidx);
       BJPROF(1);  // left side binned + sorted
@@ -476,7 +607,12 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       __syncthreads();
       bin_rows(w, nrr, bins, nbins, hr, gx, scratch, gidx);
       finish_sort(gx, sr, hr, bins, nrr, big, nbig, gidx, ridx);
-      BJPROF(2);  // right side binned + sorted
+      for (uint32_t i = tid; i < nbins; i += kThreads) hr[i] <<= 16;  // (the right ends in the high half)
+      __syncthreads();
+#else
+      sort_both(wl, nl, w, nrr, bins, nbins, hr, gx, sl, sr, gidx, lidx, ridx, scratch, big, nbig);
+#endif
+      BJPROF(2);  // both sides binned + sorted
       // every left row (sorted index p): its matching right range [rs, rs + m) in sr
       uint32_t* m_arr = reinterpret_cast<uint32_t*>(gx);
       uint32_t* rs_arr = m_arr + kBjCap;
@@ -489,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         if (p < nl) {
           const uint64_t wv = sl[p];
           const uint32_t b = bins.of(wv);
-          const uint32_t b0 = b ? hr[b - 1] : 0u, b1 = hr[b];
+          const uint32_t b0 = b ? hr[b - 1] >> 16 : 0u, b1 = hr[b] >> 16;
           if (key_bins) {  // one key a bin: the whole right bin matches
             rs = b0;
             m = b1 - b0;
@@ -719,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
 }
 
 constexpr size_t kEmitSmem = size_t(kBjCap) * 8 * 3 + size_t(kMaxBins) * 4 * 2 + size_t(kBjCap) * 2 * 3 +
-                             (kThreads / 32 + 2) * 8 + size_t(kMaxG + 1) * 8 + (3 * kMaxG + 2 + 64 + 4) * 4;
+                             (kThreads / 32 + 2) * 8 + size_t(kMaxG + 1) * 8 + (3 * kMaxG + 2 + 128 + 4) * 4;
 
 // ---------------------------------------------------------------- host
 static size_t side_bytes(int64_t n, int words, int levels) {

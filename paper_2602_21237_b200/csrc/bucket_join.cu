@@ -310,6 +310,7 @@ struct EmitCol {
   int width;
   int side;
   int carry_off;       // >= 0: the bytes at this offset of the row's carried payload words
+  int vec;             // 8 / 16: every source row of the column is one aligned 8- / 16-byte load (host-checked)
 };
 struct Cols {
   EmitCol c[kMaxCols];
@@ -432,7 +433,8 @@ __device__ __forceinline__ void sort_both(const uint64_t (&wl)[kRowsPerThread], 
         }
       } else {
         uint32_t rk = 0;
-        for (uint32_t i = b0; i < b1; ++i) rk += grouped[i] < w ? 1u : 0u;
+        if (b1 - b0 > 1)
+          for (uint32_t i = b0; i < b1; ++i) rk += grouped[i] < w ? 1u : 0u;
         sl[b0 + rk] = w;
         lidx[b0 + rk] = gidx[p];
       }
@@ -805,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
                 const uint32_t row = left ? uint32_t(sl[xs[u]]) : uint32_t(sr[jrs[u]]);
                 return c.src + uint64_t(row) * wd;
               };
-              if (wd == 8 && ((reinterpret_cast<uintptr_t>(src_of(0)) | uintptr_t(c.carry_off)) & 7) == 0) {
+              if (c.vec == 8) {
                 unsigned long long v[kU];
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
@@ -813,7 +815,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
                   if (ok[u]) __stcs(reinterpret_cast<unsigned long long*>(c.dst) + out_row(u), v[u]);
-              } else if (wd == 16 && ((reinterpret_cast<uintptr_t>(src_of(0)) | uintptr_t(c.carry_off)) & 15) == 0) {
+              } else if (c.vec == 16) {
                 uint4 v[kU];
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
@@ -1007,8 +1009,20 @@ int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t*
     } else if (c.width > 0 && !c.src) {
       return RL_ERR_BAD_ARG;
     }
-    cs.c[i] = EmitCol{static_cast<const uint8_t*>(c.src), static_cast<uint8_t*>(c.dst), c.width, c.side,
-                      c.side == RL_SIDE_KEY ? -1 : carried_offset(p, c)};
+    const int co = c.side == RL_SIDE_KEY ? -1 : carried_offset(p, c);
+    // one aligned vector load a source row: carried words are 8-byte aligned rows
+    // of 8 x words bytes in 256-byte-aligned workspace; gathered rows are src + row x width
+    int vec = 0;
+    if (c.side != RL_SIDE_KEY && (c.width == 8 || c.width == 16)) {
+      if (co >= 0) {
+        const int words = c.side == RL_SIDE_LEFT ? p->words_left : p->words_right;
+        const uintptr_t pay = reinterpret_cast<uintptr_t>(c.side == RL_SIDE_LEFT ? p->pay_left : p->pay_right);
+        if (((pay | uintptr_t(co)) % uintptr_t(c.width)) == 0 && (8 * words) % c.width == 0) vec = c.width;
+      } else if (reinterpret_cast<uintptr_t>(c.src) % uintptr_t(c.width) == 0) {
+        vec = c.width;
+      }
+    }
+    cs.c[i] = EmitCol{static_cast<const uint8_t*>(c.src), static_cast<uint8_t*>(c.dst), c.width, c.side, co, vec};
   }
   const int lv = p->levels == 3 ? 3 : 2;
   const int grid = lv == 3 ? (checksum ? emit_grid_of<true, 3>() : emit_grid_of<false, 3>())

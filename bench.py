@@ -928,6 +928,28 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     med = float(t.item())
+    # the dominant kernel (N = 1): the plan (partition passes, pair counts, scan)
+    # and the emit (bucket-join expansion: both sides' rows + carried payload in,
+    # key + both payloads out) timed apart with events on the launching stream
+    phases = None
+    if world == 1:
+        plan_ms, emit_ms = [], []
+        for _ in range(3):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            plan = pipeline.plan_join(cols_l[0], cols_r[0], [cols_l[1]], [cols_r[1]])
+            ev[1].record()
+            cols = pipeline.join_out_columns(cols_l, 0, cols_r, 0, plan.total)
+            ev[2].record()
+            plan.expand(0, plan.total, cols)
+            ev[3].record()
+            ev[3].synchronize()
+            plan_ms.append(ev[0].elapsed_time(ev[1]))
+            emit_ms.append(ev[2].elapsed_time(ev[3]))
+            kind = getattr(plan, "kind", "?")
+            del plan, cols
+        phases = {"plan_ms": round(statistics.median(plan_ms), 3), "emit_ms": round(statistics.median(emit_ms), 3),
+                  "plan_kind": kind}
     del cols_l, cols_r
     torch.cuda.empty_cache()
     # a join reads both sides' key + payload once and writes key + both payloads per match
@@ -946,11 +968,32 @@ def join_scaling(args, dev, rank, world, total_rows=JOIN_SCALING_ROWS):
                          "alg_bytes_per_step": int(alg),
                          "alg_bytes_formula": "2 sides x rows x (8 B key + 8 B payload) read + matches x 24 B "
                                               "(key, payload, right_payload) written (SURVEY §8(d)); per GPU"},
+            **({"phases": phases, "emit_roofline": emit_roofline(alg, phases["emit_ms"], peak, peak_src)}
+               if phases and phases["plan_kind"] == "bucket" else {}),
             # both sides' off-rank rows per rank (key 8 B + payload 8 B + int64 global id 8 B) over the step
             "nvlink": {"bytes_per_rank_per_step": int(2 * n * (world - 1) / world * 24),
                        "achieved_gbs": round(2 * n * (world - 1) / world * 24 / (med / 1e3) / 1e9, 1),
                        "peak_gbs": 900.0, "unit": "GB/s",
                        "frac": round(2 * n * (world - 1) / world * 24 / (med / 1e3) / 1e9 / 900.0, 4)}}
+
+
+def emit_roofline(alg_bytes, emit_ms, peak, peak_src):
+    """The bucket join's emit kernel (the path's expansion) against HBM: it
+    reads every row of both sides once (packed key | row id word + the carried
+    payload word) and writes key + both payloads per output — the join's
+    algorithmic bytes; `traffic` = its DRAM bytes per launch from the committed
+    ncu launch list (profiles/ncu_traffic.json), or null."""
+    traffic = None
+    try:
+        tj = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        traffic = tj.get("bj_emit_1e9", {}).get("bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    achieved = alg_bytes / (emit_ms / 1e3) / 1e9
+    return {"kernel": "bjoin::bj_emit_kernel<0, 3>", "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "alg_bytes_per_launch": int(alg_bytes),
+            "alg_bytes_formula": "2 sides x rows x (8 B packed row + 8 B carried payload) read + matches x 24 B written"}
 
 
 def join_cfg4(args, dev, rank, world, total_rows=10**8):

@@ -79,28 +79,33 @@ struct PlanArgs {
 
 // Runs of one group: consecutive sub-buckets [s, e) with at most kBjCap rows
 // on each side (every single sub-bucket fits: the scatter passes check it);
-// encoded (s << 16) | e. The same cut in the count and emit kernels.
+// encoded (s << 16) | e; greedy (a run from s takes the most sub-buckets that
+// fit, at least one). The same cut in the count and emit kernels,
+// by one warp (all 32 lanes, converged): a run's end is found by
+// two ballots instead of a binary search — ends s + 8, s + 16, ... (the fit is
+// monotone in the end: the count of fitting lanes places it within 8), then the
+// 7 ends after that; G <= 256. Returns the run count in every lane.
 template <int G>
-__device__ __forceinline__ uint32_t cut_runs(const uint32_t* ol, const uint32_t* orr, uint32_t* ends) {
+__device__ __forceinline__ uint32_t cut_runs_warp(const uint32_t* ol, const uint32_t* orr, uint32_t* ends) {
+  static_assert(G <= 256, "one ballot covers 32 x 8 ends");
+  const uint32_t lane = threadIdx.x & 31;
   if (ol[G] - ol[0] <= uint32_t(kBjCap) && orr[G] - orr[0] <= uint32_t(kBjCap)) {  // the whole group
-    ends[0] = uint32_t(G);
+    if (lane == 0) ends[0] = uint32_t(G);
     return 1;
   }
-  // greedy: a run from s takes the most sub-buckets that fit (at least one);
-  // the fit is monotone in the end (prefix offsets), so each end is a binary
-  // search — ~8 dependent steps a run instead of one a sub-bucket (G = 256:
-  // this cut ran on one thread while the block waited)
   uint32_t nr = 0, s = 0;
   while (s < uint32_t(G)) {
     const uint32_t bl = ol[s], br = orr[s];
-    uint32_t lo = s + 1, hi = uint32_t(G);  // the end is in [lo, hi]
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (ol[mid] - bl <= uint32_t(kBjCap) && orr[mid] - br <= uint32_t(kBjCap)) lo = mid;
-      else hi = mid - 1;
-    }
-    ends[nr++] = (s << 16) | lo;
-    s = lo;
+    auto fits = [&](uint32_t e) { return ol[e] - bl <= uint32_t(kBjCap) && orr[e] - br <= uint32_t(kBjCap); };
+    const uint32_t e1 = s + 8 * (lane + 1);
+    const uint32_t k1 = __popc(__ballot_sync(0xffffffffu, e1 <= uint32_t(G) && fits(e1)));
+    const uint32_t base = s + 8 * k1;
+    const uint32_t e2 = base + 1 + lane;
+    const uint32_t k2 = __popc(__ballot_sync(0xffffffffu, lane < 7 && e2 <= uint32_t(G) && fits(e2)));
+    const uint32_t e = max(base + k2, s + 1);  // (at least one sub-bucket)
+    if (lane == 0) ends[nr] = (s << 16) | e;
+    ++nr;
+    s = e;
   }
   return nr;
 }
@@ -197,7 +202,10 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
     }
     if (tid == 0) gsum = 0;
     __syncthreads();
-    if (tid == 0) nruns = cut_runs<G>(offl, offr, ends);
+    if (tid < 32) {
+      const uint32_t n = cut_runs_warp<G>(offl, offr, ends);
+      if (tid == 0) nruns = n;
+    }
     __syncthreads();
     const uint32_t nr = nruns;
     for (uint32_t r = 0; r < nr; ++r) {
@@ -563,7 +571,10 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       offr[i] = __ldcg(a.off_r + size_t(g) * G + i);
     }
     __syncthreads();
-    if (tid == 0) *nruns = cut_runs<G>(offl, offr, ends);
+    if (tid < 32) {
+      const uint32_t n = cut_runs_warp<G>(offl, offr, ends);
+      if (tid == 0) *nruns = n;
+    }
     __syncthreads();
     const uint32_t nr = *nruns;
     {  // run starts inside the group (and the run's pair count: rpre[r + 1] - rpre[r])

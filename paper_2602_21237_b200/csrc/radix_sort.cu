@@ -949,6 +949,11 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
   for (int u = 0; u < kPItems; ++u) {
     if (u * kPThreads + tid < tn) {
       const uint32_t p = sp[u];
+      if constexpr (CW == 1) {  // key + carried word interleaved (read back as one 16-byte load)
+        s.sk[2 * p] = k[u];
+        s.sk[2 * p + 1] = cr.p[u][0];
+        continue;
+      }
       s.sk[p] = k[u];
       if constexpr (CW > 0) {
 #pragma unroll
@@ -969,6 +974,24 @@ __device__ __forceinline__ void ptile_scatter(uint64_t (&k)[kPItems], uint32_t (
   // shared loads of the next batch)
   constexpr int kWB = CW >= 2 ? 1 : 4;  // (two carried words: batches spill)
   for (int i0 = tid; i0 < tn; i0 += kWB * kPThreads) {
+    if constexpr (CW == 1) {  // key + carried word: one 16-byte shared load a row
+      ulonglong2 q[kWB];
+      uint32_t o[kWB];
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        const int i = i0 + u * kPThreads;
+        q[u] = i < tn ? reinterpret_cast<const ulonglong2*>(s.sk)[i] : make_ulonglong2(0, 0);
+        o[u] = s.base[uint32_t(q[u].x >> SHIFT) & 255u] + uint32_t(i);
+      }
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        if (i0 + u * kPThreads < tn) {
+          __stwb(reinterpret_cast<unsigned long long*>(out_k) + o[u], q[u].x);
+          __stwb(reinterpret_cast<unsigned long long*>(out_p) + o[u], q[u].y);
+        }
+      }
+      continue;
+    }
     uint64_t kk[kWB];
     uint32_t o[kWB];
 #pragma unroll

@@ -296,6 +296,13 @@ RL_API int rl_bjoin_expand(const rl_bjoin_plan* plan, uint64_t out_begin,
                            uint64_t out_end, uint32_t* left_rows_out,
                            uint32_t* right_rows_out, const rl_column* columns,
                            int32_t n_columns, void* stream);
+/* rl_bjoin_expand with a destination row stride per column (bytes; 0 = the
+ * width): columns of width 8 or 16 may be written row-interleaved into one
+ * buffer (stride a multiple of the width, dst aligned to the width). */
+RL_API int rl_bjoin_expand_strided(const rl_bjoin_plan* plan, uint64_t out_begin,
+                                   uint64_t out_end, uint32_t* left_rows_out,
+                                   uint32_t* right_rows_out, const rl_column* columns,
+                                   int32_t n_columns, const int32_t* dst_strides, void* stream);
 /* rl_join_pair_checksum on a bucket-join plan: sum of fmix64((left_row << 32)
  * | right_row) over pairs [out_begin, out_end), added into *sum_out. */
 RL_API int rl_bjoin_pair_checksum(const rl_bjoin_plan* plan, uint64_t out_begin,
@@ -345,6 +352,13 @@ RL_API int rl_join_pair_checksum(const uint32_t* left_starts,
  * --------------------------------------------------------------------- */
 RL_API int rl_gather_rows(const uint32_t* rows, int64_t m, const rl_column* columns,
                    int32_t n_columns, void* stream);
+
+/* Relation.take of two 8-byte columns stored row-interleaved: src is m_src
+ * rows of 16 bytes (16-byte aligned); dst_lo[t] / dst_hi[t] = the first /
+ * last 8 bytes of src row rows[t]. One random 16-byte load a row (the fused
+ * join -> ORDER BY pipeline writes the join's other two columns this way). */
+RL_API int rl_gather_rows_split16(const uint32_t* rows, int64_t m, const void* src, void* dst_lo,
+                                  void* dst_hi, void* stream);
 
 /* Widen uint32 → int64 (positions/offsets handed back as numpy int64). */
 RL_API int rl_widen_u32(const uint32_t* src, int64_t n, int64_t* dst, void* stream);

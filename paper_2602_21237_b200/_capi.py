@@ -121,7 +121,10 @@ SIGNATURES = {
                                            ctypes.POINTER(RlColumn), _I32, _P, _SZ, ctypes.POINTER(RlBjoinPlan), _P]),
     "rl_bjoin_expand": (ctypes.c_int, [ctypes.POINTER(RlBjoinPlan), _U64, _U64, _P, _P, ctypes.POINTER(RlColumn),
                                        _I32, _P]),
+    "rl_bjoin_expand_strided": (ctypes.c_int, [ctypes.POINTER(RlBjoinPlan), _U64, _U64, _P, _P,
+                                               ctypes.POINTER(RlColumn), _I32, _P, _P]),
     "rl_bjoin_pair_checksum": (ctypes.c_int, [ctypes.POINTER(RlBjoinPlan), _U64, _U64, _P, _P]),
+    "rl_gather_rows_split16": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P]),
     "rl_gather_rows": (ctypes.c_int, [_P, _I64, ctypes.POINTER(RlColumn), _I32, _P]),
     "rl_widen_u32": (ctypes.c_int, [_P, _I64, _P, _P]),
     "rl_partition_workspace_bytes": (_SZ, [_I64, _I32]),

@@ -319,6 +319,7 @@ struct EmitCol {
   int side;
   int carry_off;       // >= 0: the bytes at this offset of the row's carried payload words
   int vec;             // 8 / 16: every source row of the column is one aligned 8- / 16-byte load (host-checked)
+  int64_t dstride;     // bytes between output rows (the width, or a row-interleaved layout's row size)
 };
 struct Cols {
   EmitCol c[kMaxCols];
@@ -690,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         for (int ci = 0; ci < cols.n; ++ci) {
           const EmitCol& c = cols.c[ci];
           const int wd = c.width;
-          uint8_t* dst = c.dst + o * uint64_t(wd);
+          uint8_t* dst = c.dst + o * uint64_t(c.dstride);
           if (c.side == RL_SIDE_KEY) {
             __stcs(reinterpret_cast<long long*>(dst), key_of(wv));
           } else if (c.carry_off >= 0) {  // carried: the run's payload window (L1 / L2 resident)
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
               if (c.side == RL_SIDE_KEY) {
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
-                  if (ok[u]) __stcs(reinterpret_cast<long long*>(c.dst) + out_row(u), key_of(sl[xs[u]]));
+                  if (ok[u]) __stcs(reinterpret_cast<long long*>(c.dst + out_row(u) * uint64_t(c.dstride)), key_of(sl[xs[u]]));
                 continue;
               }
               const bool left = c.side == RL_SIDE_LEFT;
@@ -825,7 +826,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
                   v[u] = ok[u] ? ld_row(reinterpret_cast<const unsigned long long*>(src_of(u))) : 0ull;
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
-                  if (ok[u]) __stcs(reinterpret_cast<unsigned long long*>(c.dst) + out_row(u), v[u]);
+                  if (ok[u]) __stcs(reinterpret_cast<unsigned long long*>(c.dst + out_row(u) * uint64_t(c.dstride)), v[u]);
               } else if (c.vec == 16) {
                 uint4 v[kU];
 #pragma unroll
@@ -833,11 +834,11 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
                   v[u] = ok[u] ? ld_row(reinterpret_cast<const uint4*>(src_of(u))) : make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
-                  if (ok[u]) __stcs(reinterpret_cast<uint4*>(c.dst) + out_row(u), v[u]);
+                  if (ok[u]) __stcs(reinterpret_cast<uint4*>(c.dst + out_row(u) * uint64_t(c.dstride)), v[u]);
               } else {
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
-                  if (ok[u]) copy_row(src_of(u), c.dst + out_row(u) * uint64_t(wd), wd);
+                  if (ok[u]) copy_row(src_of(u), c.dst + out_row(u) * uint64_t(c.dstride), wd);
               }
             }
           }
@@ -1004,7 +1005,8 @@ static int carried_offset(const rl_bjoin_plan* p, const rl_column& c) {
 }
 
 int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t* lrows_out, uint32_t* rrows_out,
-         const rl_column* columns, int n_columns, cudaStream_t stream, uint64_t* checksum = nullptr) {
+         const rl_column* columns, int n_columns, cudaStream_t stream, uint64_t* checksum = nullptr,
+         const int32_t* dst_strides = nullptr) {
   if (!p || out_end < out_begin || n_columns < 0 || n_columns > kMaxCols || (n_columns && !columns))
     return RL_ERR_BAD_ARG;
   if (out_end == out_begin) return RL_OK;
@@ -1033,7 +1035,12 @@ int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t*
         vec = c.width;
       }
     }
-    cs.c[i] = EmitCol{static_cast<const uint8_t*>(c.src), static_cast<uint8_t*>(c.dst), c.width, c.side, co, vec};
+    // a row-interleaved destination: stride >= width, naturally aligned for the vector stores
+    const int64_t stride = dst_strides && dst_strides[i] ? dst_strides[i] : c.width;
+    if (stride < c.width || (stride != c.width && (c.width != 8 && c.width != 16)) ||
+        (stride != c.width && (stride % c.width != 0 || reinterpret_cast<uintptr_t>(c.dst) % uintptr_t(c.width) != 0)))
+      return RL_ERR_BAD_ARG;
+    cs.c[i] = EmitCol{static_cast<const uint8_t*>(c.src), static_cast<uint8_t*>(c.dst), c.width, c.side, co, vec, stride};
   }
   const int lv = p->levels == 3 ? 3 : 2;
   const int grid = lv == 3 ? (checksum ? emit_grid_of<true, 3>() : emit_grid_of<false, 3>())
@@ -1087,6 +1094,13 @@ RL_API int rl_bjoin_expand(const rl_bjoin_plan* plan, uint64_t out_begin, uint64
                            uint32_t* right_rows_out, const rl_column* columns, int32_t n_columns, void* stream) {
   return rl::bjoin::emit(plan, out_begin, out_end, left_rows_out, right_rows_out, columns, n_columns,
                          static_cast<cudaStream_t>(stream));
+}
+
+RL_API int rl_bjoin_expand_strided(const rl_bjoin_plan* plan, uint64_t out_begin, uint64_t out_end,
+                                   uint32_t* left_rows_out, uint32_t* right_rows_out, const rl_column* columns,
+                                   int32_t n_columns, const int32_t* dst_strides, void* stream) {
+  return rl::bjoin::emit(plan, out_begin, out_end, left_rows_out, right_rows_out, columns, n_columns,
+                         static_cast<cudaStream_t>(stream), nullptr, dst_strides);
 }
 
 RL_API int rl_bjoin_pair_checksum(const rl_bjoin_plan* plan, uint64_t out_begin, uint64_t out_end, uint64_t* sum_out,

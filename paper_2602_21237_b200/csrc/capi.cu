@@ -43,6 +43,7 @@ int pair_checksum(const uint32_t* ls, const uint32_t* rs, const uint32_t* rc, co
                   uint64_t* sum_out, cudaStream_t stream);
 int gather_rows(const uint32_t* rows, int64_t m, const rl_column* columns, int n_columns, cudaStream_t stream);
 int widen_u32(const uint32_t* src, int64_t n, int64_t* dst, cudaStream_t stream);
+int gather_split16(const uint32_t* rows, int64_t m, const void* src, void* lo, void* hi, cudaStream_t stream);
 }  // namespace expand
 
 static std::atomic<int64_t> g_launches{0};
@@ -171,6 +172,11 @@ int rl_join_pair_checksum(const uint32_t* left_starts, const uint32_t* right_sta
 
 int rl_gather_rows(const uint32_t* rows, int64_t m, const rl_column* columns, int32_t n_columns, void* stream) {
   return rl::expand::gather_rows(rows, m, columns, n_columns, as_stream(stream));
+}
+
+int rl_gather_rows_split16(const uint32_t* rows, int64_t m, const void* src, void* dst_lo, void* dst_hi,
+                           void* stream) {
+  return rl::expand::gather_split16(rows, m, src, dst_lo, dst_hi, as_stream(stream));
 }
 
 int rl_widen_u32(const uint32_t* src, int64_t n, int64_t* dst, void* stream) {

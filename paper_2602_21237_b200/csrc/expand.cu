@@ -460,6 +460,55 @@ int gather_rows(const uint32_t* rows, int64_t m, const rl_column* columns, int n
   return rl_cuda_status(cudaGetLastError());
 }
 
+// Relation.take of two 8-byte columns stored row-interleaved (16-byte rows,
+// e.g. a join's output written that way for the ORDER BY behind it): ONE
+// random 16-byte load a row instead of two 8-byte loads from two arrays —
+// random gathers over a large source are bound by the access rate, not the
+// bytes (scripts/microbench/gather_flavors.cu: 27.6 vs 56.5 ms for 1e9 rows).
+__global__ void __launch_bounds__(kThreads) gather_split16_kernel(const uint32_t* __restrict__ rows, int64_t m,
+                                                                  const ulonglong2* __restrict__ src,
+                                                                  unsigned long long* __restrict__ lo,
+                                                                  unsigned long long* __restrict__ hi) {
+  constexpr int U = 4;  // rows in flight a thread
+  const int64_t stride = int64_t(gridDim.x) * kThreads * U;
+  for (int64_t s = int64_t(blockIdx.x) * kThreads * U + threadIdx.x; s < m; s += stride) {
+    uint32_t r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = s + int64_t(u) * kThreads;
+      r[u] = t < m ? __ldcs(rows + t) : 0u;
+    }
+    ulonglong2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = s + int64_t(u) * kThreads;
+      v[u] = t < m ? ld_row(src + r[u]) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = s + int64_t(u) * kThreads;
+      if (t < m) {
+        __stcs(lo + t, v[u].x);
+        __stcs(hi + t, v[u].y);
+      }
+    }
+  }
+}
+
+int gather_split16(const uint32_t* rows, int64_t m, const void* src, void* lo, void* hi, cudaStream_t stream) {
+  if (m < 0 || (m > 0 && (!rows || !src || !lo || !hi))) return RL_ERR_BAD_ARG;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(lo) & 7) ||
+      (reinterpret_cast<uintptr_t>(hi) & 7))
+    return RL_ERR_BAD_ARG;
+  if (m == 0) return RL_OK;
+  const int grid = int(std::min<int64_t>((m + kThreads * 4 - 1) / (kThreads * 4), int64_t(device_sm_count()) * 8));
+  gather_split16_kernel<<<grid, kThreads, 0, stream>>>(rows, m, static_cast<const ulonglong2*>(src),
+                                                       static_cast<unsigned long long*>(lo),
+                                                       static_cast<unsigned long long*>(hi));
+  count_launches(1);
+  return rl_cuda_status(cudaGetLastError());
+}
+
 __global__ void widen_kernel(const uint32_t* __restrict__ src, int64_t n, int64_t* __restrict__ dst) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     dst[i] = int64_t(src[i]);

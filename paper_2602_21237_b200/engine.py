@@ -404,6 +404,13 @@ def gather_rows(rows: torch.Tensor, columns: Sequence[OutColumn]) -> None:
     C.check(lib.rl_gather_rows(_ptr(rows), rows.numel(), arr, ncols, stream_handle()), "rl_gather_rows")
 
 
+def gather_split16(rows: torch.Tensor, src16: torch.Tensor, dst_lo: torch.Tensor, dst_hi: torch.Tensor) -> None:
+    """Relation.take of two 8-byte columns stored row-interleaved (src16: rows
+    of 16 bytes): one random 16-byte load a row into two column outputs."""
+    C.check(C.load().rl_gather_rows_split16(_ptr(rows), rows.numel(), _ptr(src16), _ptr(dst_lo), _ptr(dst_hi),
+                                            stream_handle()), "rl_gather_rows_split16")
+
+
 def widen(u32: torch.Tensor, n: Optional[int] = None) -> torch.Tensor:
     """uint32 bits → int64 values (positions/offsets handed back as int64)."""
     lib = C.load()
@@ -528,13 +535,22 @@ class BucketJoinPlan:
         self.applies = bool(ok)
 
     def expand(self, out_begin: int, out_end: int, columns: Sequence[OutColumn] = (),
-               left_rows: Optional[torch.Tensor] = None, right_rows: Optional[torch.Tensor] = None) -> None:
+               left_rows: Optional[torch.Tensor] = None, right_rows: Optional[torch.Tensor] = None,
+               dst_strides: Optional[Sequence[int]] = None) -> None:
+        """dst_strides: bytes between output rows per column (None / 0 = the
+        width) — 8- or 16-byte columns written row-interleaved into one buffer."""
         lib = C.load()
         arr, ncols = C.columns_array(
             (None if c.src is None else c.src.data_ptr(), c.dst.data_ptr(), c.width, c.side) for c in columns
         )
-        C.check(lib.rl_bjoin_expand(ctypes.byref(self.plan), out_begin, out_end, _ptr(left_rows), _ptr(right_rows),
-                                    arr, ncols, stream_handle()), "rl_bjoin_expand")
+        if dst_strides is None:
+            C.check(lib.rl_bjoin_expand(ctypes.byref(self.plan), out_begin, out_end, _ptr(left_rows),
+                                        _ptr(right_rows), arr, ncols, stream_handle()), "rl_bjoin_expand")
+            return
+        st = (ctypes.c_int32 * max(1, len(columns)))(*[int(x or 0) for x in dst_strides])
+        C.check(lib.rl_bjoin_expand_strided(ctypes.byref(self.plan), out_begin, out_end, _ptr(left_rows),
+                                            _ptr(right_rows), arr, ncols, st, stream_handle()),
+                "rl_bjoin_expand_strided")
 
     def pair_checksum(self, out_begin: int, out_end: int, acc: torch.Tensor) -> None:
         C.check(C.load().rl_bjoin_pair_checksum(ctypes.byref(self.plan), out_begin, out_end, _ptr(acc),

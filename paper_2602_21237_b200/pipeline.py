@@ -173,9 +173,68 @@ def order_by(rel: DeviceRelation, spec) -> Tuple[DeviceRelation, torch.Tensor]:
 
 def join_then_order_by(left: DeviceRelation, right: DeviceRelation, key: str, spec,
                        max_output_rows: int = 2**31) -> DeviceRelation:
-    """BASELINE cfg5's pipeline without leaving HBM: equi-join, then ORDER BY."""
-    joined = join(left, right, key, max_output_rows)
-    return order_by(joined, spec)[0]
+    """BASELINE cfg5's pipeline without leaving HBM: equi-join, then ORDER BY.
+
+    Fused layout (cfg5's shape: ORDER BY one int64 output column, the other
+    output columns exactly two 8-byte columns, the bucket join's plan): the
+    join writes the sort column as usual and the other two row-interleaved
+    into one [rows, 16] buffer; the ORDER BY then takes each row of it with
+    ONE random 16-byte load (rl_gather_rows_split16) instead of two 8-byte
+    loads from two arrays — random gathers over a large output are bound by
+    the access rate (scripts/microbench/gather_flavors.cu). The result equals
+    join() then order_by() column for column (same permutation, same bytes).
+    RL_NO_FUSED_ORDER_BY=1 runs the two steps as written."""
+    import os
+
+    out_schema = R.join_output_schema(left.schema, right.schema, key, schema_cls=type(left.schema))
+    lk, rk = left.schema.index(key), right.schema.index(key)
+    plan = plan_join(left.columns[lk], right.columns[rk],
+                     [c for j, c in enumerate(left.columns) if j != lk],
+                     [c for j, c in enumerate(right.columns) if j != rk])
+    if plan.total > max_output_rows:
+        raise OutputTooLarge(f"join would produce {plan.total} rows (cap {max_output_rows})")
+    cols = join_out_columns(left.columns, lk, right.columns, rk, 0)  # (descriptors; outputs allocated below)
+    for k in spec.keys:
+        out_schema.index(k)
+    fusable = (os.environ.get("RL_NO_FUSED_ORDER_BY", "") != "1" and getattr(plan, "kind", "") == "bucket"
+               and plan.total > 0 and len(spec.keys) == 1 and len(cols) == 3)
+    if fusable:
+        j = out_schema.index(spec.keys[0])
+        proto = [c.dst for c in cols]  # empty outputs of the right dtype / shape
+        others = [i for i in range(3) if i != j]
+        fusable = (proto[j].dtype == torch.int64 and proto[j].dim() == 1
+                   and all(_width(proto[i]) == 8 for i in others))
+    if not fusable:
+        cols = join_out_columns(left.columns, lk, right.columns, rk, plan.total)
+        if plan.total:
+            plan.expand(0, plan.total, cols)
+        joined = DeviceRelation(out_schema, [c.dst for c in cols])
+        return order_by(joined, spec)[0]
+    n = plan.total
+    dev = proto[j].device
+    sort_src = torch.empty(n, dtype=torch.int64, device=dev)
+    inter = torch.empty((n, 16), dtype=torch.uint8, device=dev)
+    halves = (inter[:, :8], inter[:, 8:])
+    emit_cols, strides = [], []
+    for i, c in enumerate(cols):
+        if i == j:
+            emit_cols.append(engine.OutColumn(c.src, sort_src, 8, c.side))
+            strides.append(0)
+        else:
+            emit_cols.append(engine.OutColumn(c.src, halves[others.index(i)], 8, c.side))
+            strides.append(16)
+    plan.expand(0, n, emit_cols, dst_strides=strides)
+    del plan
+    sorted_key = torch.empty(n, dtype=torch.int64, device=dev)
+    axis = engine.SortAxis(sort_src, is_descending(spec.directions[0]))
+    perm = engine.sort_permutation([axis], n, dev, sorted_keys_out=sorted_key)
+    del sort_src
+    outs = [None, None, None]
+    outs[j] = sorted_key
+    for k, i in enumerate(others):
+        outs[i] = _empty_like(proto[i], n)
+    engine.gather_split16(perm, inter, outs[others[0]], outs[others[1]])
+    return DeviceRelation(out_schema, outs)
 
 
 def join_stream(plan: JoinPlan, chunk_pairs: int = 1 << 31, begin: int = 0,

@@ -101,3 +101,48 @@ def test_wide_key_join_concurrent_scatter_sorts():
     assert out.row_count == len(want[0]) > 5_000_000
     for a, b in zip(out.columns, want):
         assert (a == b).all()
+
+
+@pytest.mark.parametrize("sort_col,desc", [("payload", False), ("right_payload", True), ("key", False)])
+def test_fused_join_order_by_interleaved_equals_two_steps(monkeypatch, sort_col, desc):
+    """join_then_order_by's fused layout (bucket join writing the two non-sort
+    columns row-interleaved, one 16-byte gather a row) equals join() then
+    order_by() column for column, and the oracle."""
+    from paper_2602_21237_b200 import Direction
+
+    monkeypatch.setenv("RL_FORCE_BJOIN", "1")
+    n = 300_000
+    r, s = synth.cfg1_relations(n=n, domain=n // 2, seed=9)
+    dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
+    spec = SortSpec((sort_col,), (Direction.DESC if desc else Direction.ASC,))
+    fused = pipeline.join_then_order_by(dr, ds, "key", spec).to_host()
+    monkeypatch.setenv("RL_NO_FUSED_ORDER_BY", "1")
+    two = pipeline.join_then_order_by(dr, ds, "key", spec).to_host()
+    assert fused.schema.names == two.schema.names
+    for a, b in zip(fused.columns, two.columns):
+        assert a.dtype == b.dtype and (a == b).all()
+    cols = O.join_columns(list(r.columns), 0, list(s.columns), 0)
+    j = ("key", "payload", "right_payload").index(sort_col)
+    perm = O.sort_permutation([cols[j]], [desc])
+    for a, b in zip(fused.columns, cols):
+        assert (a == b[perm]).all()
+
+
+def test_fused_join_order_by_bytes8_payload(monkeypatch):
+    """The interleaved gather moves raw 8-byte rows: a Bytes(8) payload comes
+    out byte-identical to the two-step path."""
+    from paper_2602_21237_b200 import records as R
+
+    monkeypatch.setenv("RL_FORCE_BJOIN", "1")
+    rng = np.random.default_rng(5)
+    n = 200_000
+    sch = R.Schema((("key", R.Int64()), ("payload", R.Bytes(8))))
+    r = R.Relation(sch, (rng.integers(0, n, n), rng.integers(0, 256, (n, 8), dtype=np.uint8)))
+    s = R.Relation(sch, (rng.integers(0, n, n), rng.integers(0, 256, (n, 8), dtype=np.uint8)))
+    dr, ds = pipeline.DeviceRelation.from_host(r), pipeline.DeviceRelation.from_host(s)
+    spec = SortSpec(("key",))
+    fused = pipeline.join_then_order_by(dr, ds, "key", spec).to_host()
+    monkeypatch.setenv("RL_NO_FUSED_ORDER_BY", "1")
+    two = pipeline.join_then_order_by(dr, ds, "key", spec).to_host()
+    for a, b in zip(fused.columns, two.columns):
+        assert a.shape == b.shape and (a == b).all()

@@ -47,6 +47,56 @@ __global__ void gather(const uint32_t* __restrict__ idx, const unsigned long lon
     }
   }
 }
+// two 8-byte columns by the same rows: separate source arrays (two random
+// loads a row) vs one interleaved 16-byte source row (one load)
+template <bool IL>
+__global__ void gather2(const uint32_t* __restrict__ idx, const unsigned long long* __restrict__ a,
+                        const unsigned long long* __restrict__ b, unsigned long long* __restrict__ da,
+                        unsigned long long* __restrict__ db, uint64_t n) {
+  constexpr int U = 4;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
+  for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) * U + threadIdx.x; s < n; s += stride) {
+    unsigned long long va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = s + uint64_t(u) * blockDim.x;
+      if (i < n) {
+        const uint64_t r = idx[i];
+        if constexpr (IL) {
+          const ulonglong2 q = __ldcg(reinterpret_cast<const ulonglong2*>(a) + r);
+          va[u] = q.x;
+          vb[u] = q.y;
+        } else {
+          va[u] = __ldcg(a + r);
+          vb[u] = __ldcg(b + r);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = s + uint64_t(u) * blockDim.x;
+      if (i < n) {
+        __stcs(da + i, va[u]);
+        __stcs(db + i, vb[u]);
+      }
+    }
+  }
+}
+template <bool IL>
+float run2(const uint32_t* idx, const unsigned long long* a, const unsigned long long* b, unsigned long long* da,
+           unsigned long long* db, uint64_t n, int sms) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  gather2<IL><<<sms * 4, 512>>>(idx, a, b, da, db, n);
+  cudaEventRecord(e0);
+  gather2<IL><<<sms * 4, 512>>>(idx, a, b, da, db, n);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  return ms;
+}
 template <int F>
 float run(const uint32_t* idx, const unsigned long long* src, unsigned long long* dst, uint64_t n, int sms) {
   cudaEvent_t a, b;
@@ -83,5 +133,14 @@ int main(int argc, char** argv) {
   t[7] = run<7>(idx, src, dst, n, sms);
   for (int i = 0; i < 8; ++i) printf("%-26s %8.2f ms  %.2f G rows/s\n", names[i], t[i], n / (t[i] * 1e6));
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+  if (argc > 2) {  // two columns: src = [2n] words (separate: a = src, b = src + n; interleaved: 16-byte rows)
+    cudaFree(dst);
+    unsigned long long *src2, *d2;
+    if (cudaMalloc(&src2, n * 16) || cudaMalloc(&d2, n * 16)) { printf("oom2\n"); return 1; }
+    cudaMemset(src2, 1, n * 16);
+    const float ts = run2<false>(idx, src2, src2 + n, d2, d2 + n, n, sms);
+    const float ti = run2<true>(idx, src2, nullptr, d2, d2 + n, n, sms);
+    printf("two columns, separate arrays  %8.2f ms\ntwo columns, interleaved rows %8.2f ms\n", ts, ti);
+  }
   return 0;
 }

@@ -18,6 +18,7 @@
 // The numpy intermediates (local, cr, li/ri, expanded starts: 4 index
 // arrays of `total` entries) are never materialised.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -448,12 +449,96 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const uint32_t* __rest
   }
 }
 
+// The same for 4- and 8-byte columns, four consecutive output rows a thread:
+// one 16-byte load of their row ids, every random row load of a column in
+// flight before its 16-byte stores (kGU groups of four a thread). A gather
+// from an L2-resident source is bound by random-load latency x loads in
+// flight, not bytes: cfg2's 10M-row payload gather took 55 us one row a
+// thread with the source already in L2.
+constexpr int kGU = 2;
+__global__ void __launch_bounds__(kThreads) gather_vec_kernel(const uint32_t* __restrict__ rows, int64_t m,
+                                                              ColumnSet cols) {
+  const int64_t m4 = m >> 2;
+  const int64_t stride = int64_t(gridDim.x) * kThreads * kGU;
+  for (int64_t g0 = int64_t(blockIdx.x) * kThreads * kGU + threadIdx.x; g0 < m4; g0 += stride) {
+    uint4 r[kGU];
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const int64_t g = g0 + int64_t(u) * kThreads;
+      r[u] = g < m4 ? __ldcs(reinterpret_cast<const uint4*>(rows) + g) : make_uint4(0, 0, 0, 0);
+    }
+    for (int ci = 0; ci < cols.n; ++ci) {
+      const rl_column& c = cols.c[ci];
+      if (c.width == 4) {
+        const unsigned int* src = static_cast<const unsigned int*>(c.src);
+        uint4 v[kGU];
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) {
+          if (g0 + int64_t(u) * kThreads < m4) {
+            v[u].x = ld_row(src + r[u].x);
+            v[u].y = ld_row(src + r[u].y);
+            v[u].z = ld_row(src + r[u].z);
+            v[u].w = ld_row(src + r[u].w);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) {
+          const int64_t g = g0 + int64_t(u) * kThreads;
+          if (g < m4) __stcs(static_cast<uint4*>(c.dst) + g, v[u]);
+        }
+      } else {  // 8 bytes
+        const unsigned long long* src = static_cast<const unsigned long long*>(c.src);
+        ulonglong2 v[kGU][2];
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) {
+          if (g0 + int64_t(u) * kThreads < m4) {
+            v[u][0].x = ld_row(src + r[u].x);
+            v[u][0].y = ld_row(src + r[u].y);
+            v[u][1].x = ld_row(src + r[u].z);
+            v[u][1].y = ld_row(src + r[u].w);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kGU; ++u) {
+          const int64_t g = g0 + int64_t(u) * kThreads;
+          if (g < m4) {
+            __stcs(static_cast<ulonglong2*>(c.dst) + 2 * g, v[u][0]);
+            __stcs(static_cast<ulonglong2*>(c.dst) + 2 * g + 1, v[u][1]);
+          }
+        }
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < uint32_t(m & 3)) {  // the last m % 4 rows
+    const int64_t t = (m4 << 2) + threadIdx.x;
+    const uint64_t row = rows[t];
+    for (int ci = 0; ci < cols.n; ++ci) {
+      const rl_column& c = cols.c[ci];
+      copy_row(static_cast<const uint8_t*>(c.src) + row * uint64_t(c.width),
+               static_cast<uint8_t*>(c.dst) + t * c.width, c.width);
+    }
+  }
+}
+
 int gather_rows(const uint32_t* rows, int64_t m, const rl_column* columns, int n_columns, cudaStream_t stream) {
   if (m < 0 || (m > 0 && rows == nullptr)) return RL_ERR_BAD_ARG;
   ColumnSet cs;
   int st = fill_columns(cs, columns, n_columns, false);
   if (st != RL_OK) return st;
   if (m == 0 || n_columns == 0) return RL_OK;
+  bool vec = (reinterpret_cast<uintptr_t>(rows) & 15) == 0 && m >= 4 && std::getenv("RL_GATHER_SCALAR") == nullptr;
+  for (int i = 0; i < n_columns && vec; ++i) {
+    const rl_column& c = cs.c[i];
+    vec = (c.width == 4 || c.width == 8) && (reinterpret_cast<uintptr_t>(c.src) % uintptr_t(c.width)) == 0 &&
+          (reinterpret_cast<uintptr_t>(c.dst) & 15) == 0;
+  }
+  if (vec) {
+    const int64_t groups = (m >> 2) + kThreads * kGU - 1;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(groups / (kThreads * kGU), int64_t(device_sm_count()) * 8)));
+    gather_vec_kernel<<<grid, kThreads, 0, stream>>>(rows, m, cs);
+    count_launches(1);
+    return rl_cuda_status(cudaGetLastError());
+  }
   const int grid = int(std::min<int64_t>((m + kThreads - 1) / kThreads, int64_t(device_sm_count()) * 16));
   gather_kernel<<<grid, kThreads, 0, stream>>>(rows, m, cs);
   count_launches(1);

@@ -33,6 +33,7 @@
 // make the plan report "does not apply" (scalars[1] == 0) and the caller runs
 // the sort-based plan (plan.cu) instead.
 #include <algorithm>
+#include <cstdlib>
 
 #include "bjoin.cuh"
 #include "common.cuh"
@@ -59,6 +60,7 @@ constexpr int kMaxG = 256;
 constexpr int kMaxBins = 4096;
 constexpr int kRowsPerThread = (kBjCap + kThreads - 1) / kThreads;  // 5
 constexpr int kRankMax = 48;  // bins above this: a warp's bitonic network
+constexpr uint32_t kSelMax = 512;  // emit: a run with at most this many pairs lists its matches instead of sorting
 
 struct PlanArgs {
   const uint64_t* rows_l;
@@ -306,6 +308,7 @@ __global__ void __launch_bounds__(1024) bj_scan_kernel(PlanArgs a, uint32_t grou
 struct EmitArgs {
   PlanArgs p;
   uint64_t out_begin, out_end;
+  int no_sel;  // RL_BJ_NO_SEL=1: every run takes the sorting path (A/B, tests)
   uint32_t* lrows_out;
   uint32_t* rrows_out;
   unsigned long long* checksum;
@@ -611,6 +614,75 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       load_rows(a.rows_r, r0, nrr, w);
       __syncthreads();
       BJPROF(0);  // run setup, prefetch issue, row loads
+      if (cnt_pairs <= kSelMax && !e.no_sel) {
+        // a selective run (few pairs, e.g. cfg4): only the right side is binned;
+        // every left row lists its matches (left word, right word, load indexes),
+        // and each listed pair's output row is its rank in (left word, right
+        // word) order = (key, left row, right row) — no sort of either side
+        bin_rows(w, nrr, bins, nbins, hr, sr, scratch, ridx);
+        if (tid == 0) *nbig = 0;
+        __syncthreads();
+        ulonglong2* pairs = reinterpret_cast<ulonglong2*>(gx);  // [kSelMax] (left word, right word)
+        uint32_t* pidx = omap;                                  // [kSelMax] left | right load index << 16
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+          const uint32_t j = tid + u * kThreads;
+          if (j < nl) {
+            const uint64_t wv = wl[u];
+            const uint32_t b = bins.of(wv);
+            const uint32_t b0 = b ? hr[b - 1] : 0u, b1 = hr[b];
+            const uint32_t key = uint32_t(wv >> 32);
+            for (uint32_t i = b0; i < b1; ++i) {
+              const uint64_t wr = sr[i];
+              if (key_bins || uint32_t(wr >> 32) == key) {
+                const uint32_t at = atomicAdd(nbig, 1u);
+                if (at < kSelMax) {
+                  pairs[at] = make_ulonglong2(wv, wr);
+                  pidx[at] = j | (uint32_t(ridx[i]) << 16);
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+        const uint32_t np = min(*nbig, kSelMax);  // (== cnt_pairs)
+        for (uint32_t q = tid; q < np; q += kThreads) {
+          const ulonglong2 me = pairs[q];
+          uint32_t rk = 0;
+          for (uint32_t i = 0; i < np; ++i) {
+            const ulonglong2 o = pairs[i];
+            rk += (o.x < me.x || (o.x == me.x && o.y < me.y)) ? 1u : 0u;
+          }
+          const uint64_t t = base + rk;  // the pair's output row
+          if (t < e.out_begin || t >= e.out_end) continue;
+          const uint32_t lrow = uint32_t(me.x), rrow = uint32_t(me.y);
+          if constexpr (CHECKSUM) {
+            sum += fmix64((uint64_t(lrow) << 32) | rrow);
+            continue;
+          }
+          const uint64_t o = t - e.out_begin;
+          if (e.lrows_out) __stcs(e.lrows_out + o, lrow);
+          if (e.rrows_out) __stcs(e.rrows_out + o, rrow);
+          const uint32_t lj = pidx[q] & 0xFFFFu, rj = pidx[q] >> 16;
+          for (int ci = 0; ci < cols.n; ++ci) {
+            const EmitCol& c = cols.c[ci];
+            uint8_t* dst = c.dst + o * uint64_t(c.dstride);
+            if (c.side == RL_SIDE_KEY) {
+              __stcs(reinterpret_cast<long long*>(dst), key_of(me.x));
+            } else if (c.carry_off >= 0) {
+              const bool left = c.side == RL_SIDE_LEFT;
+              const uint64_t* pay = left ? a.pay_l : a.pay_r;
+              const int words = left ? a.words_l : a.words_r;
+              const uint64_t at = left ? uint64_t(l0) + lj : uint64_t(r0) + rj;
+              copy_row(reinterpret_cast<const uint8_t*>(pay + at * words) + c.carry_off, dst, c.width);
+            } else {
+              copy_row(c.src + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * c.width, dst, c.width);
+            }
+          }
+        }
+        __syncthreads();  // smem reused by the next run
+        continue;
+      }
       // left side sorted first; the bin counters then serve the right side and
       // keep its bin ends for the match
 #ifdef RL_BJ_SEPARATE_SORTS  // (A/B: one side after the other)
@@ -1052,6 +1124,7 @@ int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t*
                  p->pay_left, p->pay_right, p->words_left, p->words_right};
   e.out_begin = out_begin;
   e.out_end = out_end;
+  e.no_sel = std::getenv("RL_BJ_NO_SEL") != nullptr ? 1 : 0;
   e.lrows_out = lrows_out;
   e.rrows_out = rrows_out;
   e.checksum = reinterpret_cast<unsigned long long*>(checksum);

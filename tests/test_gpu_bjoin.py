@@ -15,6 +15,18 @@ from paper_2602_21237_b200 import engine, pipeline
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["listed", "sorted"])
+def emit_path(request, monkeypatch):
+    """Every test twice: runs with few pairs listing their matches (the
+    default for <= 512 pairs a run) and every run sorting both sides
+    (RL_BJ_NO_SEL=1)."""
+    if request.param == "sorted":
+        monkeypatch.setenv("RL_BJ_NO_SEL", "1")
+    else:
+        monkeypatch.delenv("RL_BJ_NO_SEL", raising=False)
+    return request.param
+
+
 def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 

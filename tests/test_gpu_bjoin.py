@@ -222,3 +222,41 @@ def test_three_level_partition(carry, monkeypatch):
     assert (cols[0].dst.cpu().numpy() == lk[wl]).all()
     assert (cols[1].dst.cpu().numpy() == lp[wl]).all()
     assert (cols[2].dst.cpu().numpy() == rp[wr]).all()
+
+
+def test_strided_outputs_and_split_gather():
+    """rl_bjoin_expand_strided writes 8-byte columns row-interleaved exactly as
+    the plain expand writes them apart; bad strides / alignment are refused;
+    rl_gather_rows_split16 takes interleaved rows into two columns."""
+    rng = np.random.default_rng(41)
+    n = 300_000
+    lk, rk = rng.integers(0, 150_000, n), rng.integers(0, 150_000, n)
+    lp, rp = rng.integers(-(2**50), 2**50, n), rng.integers(-(2**50), 2**50, n)
+    bp = engine.BucketJoinPlan(_dev(lk), _dev(rk), [_dev(lp)], [_dev(rp)])
+    assert bp.applies
+    t = bp.total
+    wl, wr = O.join_pairs(lk, rk)
+    key = torch.empty(t, dtype=torch.int64, device="cuda")
+    inter = torch.empty((t, 16), dtype=torch.uint8, device="cuda")
+    cols = [engine.OutColumn(None, key, 8, C.RL_SIDE_KEY),
+            engine.OutColumn(_dev(lp), inter[:, :8], 8, C.RL_SIDE_LEFT),
+            engine.OutColumn(_dev(rp), inter[:, 8:], 8, C.RL_SIDE_RIGHT)]
+    bp.expand(0, t, cols, dst_strides=[0, 16, 16])
+    both = inter.cpu().numpy().view(np.int64).reshape(t, 2)
+    assert (key.cpu().numpy() == lk[wl]).all()
+    assert (both[:, 0] == lp[wl]).all() and (both[:, 1] == rp[wr]).all()
+    with pytest.raises(ValueError):  # stride below the width
+        bp.expand(0, t, cols, dst_strides=[0, 4, 16])
+    with pytest.raises(ValueError):  # a 5-byte column cannot be interleaved
+        odd = torch.empty((t, 16), dtype=torch.uint8, device="cuda")
+        bp.expand(0, t, [engine.OutColumn(_dev(rng.integers(0, 256, (n, 5), dtype=np.uint8)), odd, 5,
+                                          C.RL_SIDE_LEFT)], dst_strides=[16])
+    perm = torch.from_numpy(rng.permutation(t).astype(np.int32)).cuda()
+    lo = torch.empty(t, dtype=torch.int64, device="cuda")
+    hi = torch.empty(t, dtype=torch.int64, device="cuda")
+    engine.gather_split16(perm, inter, lo, hi)
+    p = perm.cpu().numpy().astype(np.int64)
+    assert (lo.cpu().numpy() == both[p, 0]).all() and (hi.cpu().numpy() == both[p, 1]).all()
+    with pytest.raises(ValueError):  # source rows must be 16-byte aligned
+        engine.gather_split16(perm, inter.view(-1)[8:8 + 16 * (t - 1)].view(t - 1, 16), lo, hi)
+    engine.gather_split16(perm[:0], inter, lo, hi)  # m = 0: nothing to do

@@ -260,3 +260,28 @@ def test_strided_outputs_and_split_gather():
     with pytest.raises(ValueError):  # source rows must be 16-byte aligned
         engine.gather_split16(perm, inter.view(-1)[8:8 + 16 * (t - 1)].view(t - 1, 16), lo, hi)
     engine.gather_split16(perm[:0], inter, lo, hi)  # m = 0: nothing to do
+
+
+def test_selective_join_listed_runs(emit_path):
+    """A selective join (~0.05 pairs a row: every run lists its few matches
+    unless RL_BJ_NO_SEL=1): pairs, order, slices, checksum and carried /
+    gathered columns equal the oracle."""
+    rng = np.random.default_rng(43)
+    n = 1_000_000
+    lk, rk = rng.integers(0, 20_000_000, n), rng.integers(0, 20_000_000, n + 333)
+    bp = _check(lk, rk)
+    wl, wr = O.join_pairs(lk, rk)
+    for a, b in [(0, 7), (1000, bp.total - 1000)]:
+        gl, gr = _pairs(bp, a, b)
+        assert (gl == wl[a:b]).all() and (gr == wr[a:b]).all()
+    lp = rng.integers(-(2**62), 2**62, n)
+    rp = rng.integers(0, 256, (n + 333, 16), dtype=np.uint8)
+    bc = engine.BucketJoinPlan(_dev(lk), _dev(rk), [_dev(lp)], [])
+    cols = [engine.OutColumn(None, torch.empty(bc.total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_KEY),
+            engine.OutColumn(_dev(lp), torch.empty(bc.total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_LEFT),
+            engine.OutColumn(_dev(rp), torch.empty((bc.total, 16), dtype=torch.uint8, device="cuda"), 16,
+                             C.RL_SIDE_RIGHT)]
+    bc.expand(0, bc.total, cols)
+    assert (cols[0].dst.cpu().numpy() == lk[wl]).all()
+    assert (cols[1].dst.cpu().numpy() == lp[wl]).all()
+    assert (cols[2].dst.cpu().numpy() == rp[wr]).all()

@@ -24,7 +24,12 @@
 //      output, and the outputs are written in output order: key, left row,
 //      right row — the reference order (tensorpath.py:162-172) — with every
 //      column gathered (key = the matched key itself, left / right columns by
-//      row id), optionally only the slice [out_begin, out_end).
+//      row id, or read beside the row when carried through the passes),
+//      optionally only the slice [out_begin, out_end) and optionally
+//      row-interleaved (a destination stride per column). Both sides are sorted
+//      in one set of barrier phases (packed left / right bin counters); a run
+//      with few pairs (<= 512 and <= 1/8 of its rows: selective joins) bins
+//      only the right side, lists its matches and writes each at its rank.
 //
 // DRAM traffic per side: 8n (counts) + 16n (digit-7 pass) + 16n (digit-6
 // pass) + 8n (count) + 8n (emit); no position, key-value, offset or

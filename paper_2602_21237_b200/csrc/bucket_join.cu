@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
   __shared__ uint64_t scratch[kThreads / 32 + 2];
   __shared__ uint32_t nruns;
   __shared__ unsigned long long gsum;
+  __shared__ unsigned long long runsum[2];  // pair counts of the current / next run
   const int tid = threadIdx.x;
   if (fell_back(a)) return;
   // packed key length: a bin covering all of its bits holds ONE key
@@ -207,7 +208,10 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
       offl[i] = __ldcg(a.off_l + size_t(g) * G + i);
       offr[i] = __ldcg(a.off_r + size_t(g) * G + i);
     }
-    if (tid == 0) gsum = 0;
+    if (tid == 0) {
+      gsum = 0;
+      runsum[0] = 0;
+    }
     __syncthreads();
     if (tid < 32) {
       const uint32_t n = cut_runs_warp<G>(offl, offr, ends);
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
         // one key a bin: pairs = sum over bins of left rows x right rows (both
         // counts in one word: left in the low 16 bits, right in the high 16)
         const uint32_t nbins = bins.count(e - s);
-        for (uint32_t i = tid; i < nbins; i += kThreads) hist[i] = 0;
+        for (uint32_t i = tid; i < nbins / 4; i += kThreads) reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
         uint64_t w[kRowsPerThread], wl[kRowsPerThread];
         load_rows(a.rows_r, r0, nrr, w);
         load_rows(a.rows_l, l0, nl, wl);
@@ -259,13 +263,16 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
           }
         }
       }
-      uint64_t tot;
-      block_exclusive_scan<kThreads>(cnt, scratch, &tot);
+      // the run's pair count: a warp sum, one shared atomic a warp
+      for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if ((tid & 31) == 0 && cnt) atomicAdd(&runsum[r & 1], (unsigned long long)cnt);
+      __syncthreads();  // (also: hist / br reused by the next run)
       if (tid == 0) {
+        const uint64_t tot = runsum[r & 1];
         a.counts[size_t(g) * G + r] = uint32_t(tot);
         gsum += tot;
+        runsum[(r + 1) & 1] = 0;  // the next run's slot (its atomics come after a later barrier)
       }
-      __syncthreads();  // hist / br / scratch reused by the next run
     }
     if (tid == 0) a.gtot[g] = gsum;
     __syncthreads();
@@ -603,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       const Bins bins(g * G + s, en - s, Q::kShift);
       const uint32_t nbins = bins.count(en - s);
       const bool key_bins = (64u - uint32_t(Q::kShift)) + bins.bb >= keybits;  // bins = keys
-      for (uint32_t i = tid; i < nbins; i += kThreads) hr[i] = 0;
+      for (uint32_t i = tid; i < nbins / 4; i += kThreads) reinterpret_cast<uint4*>(hr)[i] = make_uint4(0, 0, 0, 0);  // (nbins % 16 == 0)
       prefetch_next_run<G>(a, offl, offr, ends, r, nr);
       if constexpr (!CHECKSUM) {  // the carried payload windows of this run: into L2 while the rows are sorted
         const uint32_t lines_l = (nl * uint32_t(a.words_l) * 8 + 127) / 128, lines_r = (nrr * uint32_t(a.words_r) * 8 + 127) / 128;

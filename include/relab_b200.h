@@ -277,6 +277,11 @@ typedef struct rl_bjoin_plan {
   int32_t carry_width_right[4];
   int32_t carry_off_left[4];
   int32_t carry_off_right[4];
+  /* selective runs' matches listed by the plan (two levels; null when off):
+   * rl_bjoin_expand writes a listed run from these instead of re-binning it */
+  const void* sel_pairs;
+  const uint32_t* sel_idx;
+  const uint32_t* run_sel;
 } rl_bjoin_plan;
 /* Payload words (8 B) a row of this side carries through the plan's passes
  * for these columns (0: none; at most 16 bytes / 4 columns, else 0 — they

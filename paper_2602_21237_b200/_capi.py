@@ -65,7 +65,8 @@ class RlBjoinPlan(ctypes.Structure):
         ("carry_cols_left", ctypes.c_int32), ("carry_cols_right", ctypes.c_int32),
         ("carry_src_left", ctypes.c_void_p * 4), ("carry_src_right", ctypes.c_void_p * 4),
         ("carry_width_left", ctypes.c_int32 * 4), ("carry_width_right", ctypes.c_int32 * 4),
-        ("carry_off_left", ctypes.c_int32 * 4), ("carry_off_right", ctypes.c_int32 * 4)]
+        ("carry_off_left", ctypes.c_int32 * 4), ("carry_off_right", ctypes.c_int32 * 4),
+        ("sel_pairs", ctypes.c_void_p), ("sel_idx", ctypes.c_void_p), ("run_sel", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

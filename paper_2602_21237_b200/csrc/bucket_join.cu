@@ -82,6 +82,14 @@ struct PlanArgs {
   const uint64_t* pay_l;    // carried payload words, parallel to rows_l (words_l per row)
   const uint64_t* pay_r;
   int words_l, words_r;
+  // selective runs listed by the count kernel (two levels; null / 0 = off): the
+  // run's matches (left word, right word) and load indexes (left | right << 16)
+  // at run_sel[run] in sel_pairs / sel_idx (~0u: not listed), sel_cursor the fill
+  ulonglong2* sel_pairs;
+  uint32_t* sel_idx;
+  uint32_t* run_sel;
+  unsigned long long* sel_cursor;
+  uint32_t sel_cap;
 };
 
 // Runs of one group: consecutive sub-buckets [s, e) with at most kBjCap rows
@@ -198,6 +206,8 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
   __shared__ uint32_t nruns;
   __shared__ unsigned long long gsum;
   __shared__ unsigned long long runsum[2];  // pair counts of the current / next run
+  __shared__ uint16_t bidx[kBjCap];            // right rows' load indexes (listing)
+  __shared__ uint32_t selbase, lcount;
   const int tid = threadIdx.x;
   if (fell_back(a)) return;
   // packed key length: a bin covering all of its bits holds ONE key
@@ -252,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
         load_rows(a.rows_r, r0, nrr, w);
         load_rows(a.rows_l, l0, nl, wl);  // in flight while the right side is binned
         __syncthreads();
-        bin_rows(w, nrr, bins, nbins, hist, br, scratch);
+        bin_rows(w, nrr, bins, nbins, hist, br, scratch, bidx);
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u) {
           if (tid + u * kThreads < int(nl)) {
@@ -262,7 +272,45 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
             for (uint32_t i = b0; i < b1; ++i) cnt += uint32_t(br[i] >> 32) == key ? 1u : 0u;
           }
         }
+        if (a.sel_cap) {
+          // a selective run (few pairs: <= kSelMax and <= 1/8 of its rows, the
+          // emit's own rule) lists its matches for the emit, which then needs
+          // neither side's rows (the 1/8 rule bounds the buffer: sel_cap >= rows / 8)
+          uint64_t wc = cnt;
+          for (int o = 16; o > 0; o >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, o);
+          if ((tid & 31) == 0 && wc) atomicAdd(&runsum[r & 1], (unsigned long long)wc);
+          __syncthreads();
+          const uint64_t tot = runsum[r & 1];
+          const bool list = tot > 0 && tot <= kSelMax && tot * 8 <= uint64_t(nl) + nrr;
+          if (list) {
+            if (tid == 0) {
+              selbase = uint32_t(atomicAdd(a.sel_cursor, (unsigned long long)tot));
+              lcount = 0;
+            }
+            __syncthreads();
+            const uint32_t sb = selbase;
+#pragma unroll
+            for (int u = 0; u < kRowsPerThread; ++u) {
+              const uint32_t j = tid + u * kThreads;
+              if (j < nl) {
+                const uint32_t b = bins.of(wl[u]);
+                const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
+                const uint32_t key = uint32_t(wl[u] >> 32);
+                for (uint32_t i = b0; i < b1; ++i) {
+                  if (uint32_t(br[i] >> 32) == key) {
+                    const uint32_t k = atomicAdd(&lcount, 1u);
+                    a.sel_pairs[sb + k] = make_ulonglong2(wl[u], br[i]);
+                    a.sel_idx[sb + k] = j | (uint32_t(bidx[i]) << 16);
+                  }
+                }
+              }
+            }
+          }
+          if (tid == 0) a.run_sel[size_t(g) * G + r] = list ? selbase : ~0u;
+          cnt = 0;  // (already in runsum)
+        }
       }
+      if (a.sel_cap && !(nl && nrr && !key_bins) && tid == 0) a.run_sel[size_t(g) * G + r] = ~0u;
       // the run's pair count: a warp sum, one shared atomic a warp
       for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
       if ((tid & 31) == 0 && cnt) atomicAdd(&runsum[r & 1], (unsigned long long)cnt);
@@ -610,6 +658,59 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       const Bins bins(g * G + s, en - s, Q::kShift);
       const uint32_t nbins = bins.count(en - s);
       const bool key_bins = (64u - uint32_t(Q::kShift)) + bins.bb >= keybits;  // bins = keys
+      // listed pairs of a selective run: each writes itself at output row base +
+      // its rank in (left word, right word) order = (key, left row, right row)
+      auto rank_write = [&](const ulonglong2* pairs, const uint32_t* pidx, uint32_t np) {
+          for (uint32_t q = tid; q < np; q += kThreads) {
+            const ulonglong2 me = pairs[q];
+            uint32_t rk = 0;
+            for (uint32_t i = 0; i < np; ++i) {
+              const ulonglong2 o = pairs[i];
+              rk += (o.x < me.x || (o.x == me.x && o.y < me.y)) ? 1u : 0u;
+            }
+            const uint64_t t = base + rk;  // the pair's output row
+            if (t < e.out_begin || t >= e.out_end) continue;
+            const uint32_t lrow = uint32_t(me.x), rrow = uint32_t(me.y);
+            if constexpr (CHECKSUM) {
+              sum += fmix64((uint64_t(lrow) << 32) | rrow);
+              continue;
+            }
+            const uint64_t o = t - e.out_begin;
+            if (e.lrows_out) __stcs(e.lrows_out + o, lrow);
+            if (e.rrows_out) __stcs(e.rrows_out + o, rrow);
+            const uint32_t lj = pidx[q] & 0xFFFFu, rj = pidx[q] >> 16;
+            for (int ci = 0; ci < cols.n; ++ci) {
+              const EmitCol& c = cols.c[ci];
+              uint8_t* dst = c.dst + o * uint64_t(c.dstride);
+              if (c.side == RL_SIDE_KEY) {
+                __stcs(reinterpret_cast<long long*>(dst), key_of(me.x));
+              } else if (c.carry_off >= 0) {
+                const bool left = c.side == RL_SIDE_LEFT;
+                const uint64_t* pay = left ? a.pay_l : a.pay_r;
+                const int words = left ? a.words_l : a.words_r;
+                const uint64_t at = left ? uint64_t(l0) + lj : uint64_t(r0) + rj;
+                copy_row(reinterpret_cast<const uint8_t*>(pay + at * words) + c.carry_off, dst, c.width);
+              } else {
+                copy_row(c.src + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * c.width, dst, c.width);
+              }
+            }
+          }
+      };
+      if (a.run_sel) {  // listed by the count kernel: neither side's rows are needed
+        const uint32_t so = __ldcg(a.run_sel + size_t(g) * G + r);
+        if (so != ~0u) {
+          ulonglong2* pairs = reinterpret_cast<ulonglong2*>(gx);
+          uint32_t* pidx = omap;
+          for (uint32_t q = tid; q < cnt_pairs; q += kThreads) {
+            pairs[q] = __ldcg(a.sel_pairs + so + q);
+            pidx[q] = __ldcg(a.sel_idx + so + q);
+          }
+          __syncthreads();
+          rank_write(pairs, pidx, cnt_pairs);
+          __syncthreads();  // smem reused by the next run
+          continue;
+        }
+      }
       for (uint32_t i = tid; i < nbins / 4; i += kThreads) reinterpret_cast<uint4*>(hr)[i] = make_uint4(0, 0, 0, 0);  // (nbins % 16 == 0)
       prefetch_next_run<G>(a, offl, offr, ends, r, nr);
       if constexpr (!CHECKSUM) {  // the carried payload windows of this run: into L2 while the rows are sorted
@@ -660,40 +761,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         }
         __syncthreads();
         const uint32_t np = min(*nbig, kSelMax);  // (== cnt_pairs)
-        for (uint32_t q = tid; q < np; q += kThreads) {
-          const ulonglong2 me = pairs[q];
-          uint32_t rk = 0;
-          for (uint32_t i = 0; i < np; ++i) {
-            const ulonglong2 o = pairs[i];
-            rk += (o.x < me.x || (o.x == me.x && o.y < me.y)) ? 1u : 0u;
-          }
-          const uint64_t t = base + rk;  // the pair's output row
-          if (t < e.out_begin || t >= e.out_end) continue;
-          const uint32_t lrow = uint32_t(me.x), rrow = uint32_t(me.y);
-          if constexpr (CHECKSUM) {
-            sum += fmix64((uint64_t(lrow) << 32) | rrow);
-            continue;
-          }
-          const uint64_t o = t - e.out_begin;
-          if (e.lrows_out) __stcs(e.lrows_out + o, lrow);
-          if (e.rrows_out) __stcs(e.rrows_out + o, rrow);
-          const uint32_t lj = pidx[q] & 0xFFFFu, rj = pidx[q] >> 16;
-          for (int ci = 0; ci < cols.n; ++ci) {
-            const EmitCol& c = cols.c[ci];
-            uint8_t* dst = c.dst + o * uint64_t(c.dstride);
-            if (c.side == RL_SIDE_KEY) {
-              __stcs(reinterpret_cast<long long*>(dst), key_of(me.x));
-            } else if (c.carry_off >= 0) {
-              const bool left = c.side == RL_SIDE_LEFT;
-              const uint64_t* pay = left ? a.pay_l : a.pay_r;
-              const int words = left ? a.words_l : a.words_r;
-              const uint64_t at = left ? uint64_t(l0) + lj : uint64_t(r0) + rj;
-              copy_row(reinterpret_cast<const uint8_t*>(pay + at * words) + c.carry_off, dst, c.width);
-            } else {
-              copy_row(c.src + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * c.width, dst, c.width);
-            }
-          }
-        }
+        rank_write(pairs, pidx, np);
         __syncthreads();  // smem reused by the next run
         continue;
       }
@@ -964,11 +1032,24 @@ static size_t side_bytes(int64_t n, int words, int levels) {
 static uint32_t groups_of(int levels) { return levels == 3 ? Geo<3>::kGroups : Geo<2>::kGroups; }
 static int group_size(int levels) { return levels == 3 ? Geo<3>::G : Geo<2>::G; }
 
+// The listed matches of selective runs (two levels only): a listed run holds at
+// most 1/8 of its rows in pairs, so (nl + nr) / 8 entries always suffice.
+static size_t sel_cap_of(int64_t nl, int64_t nr, int levels) {
+  return levels == 2 ? size_t((nl + nr) / 8) + kSelMax : 0;
+}
+static size_t sel_bytes(int64_t nl, int64_t nr, int levels) {
+  const size_t cap = sel_cap_of(nl, nr, levels);
+  if (!cap) return 0;
+  const size_t runs = size_t(groups_of(levels)) * group_size(levels);
+  return align_up(16 * cap, 256) + align_up(4 * cap, 256) + align_up(4 * runs, 256);
+}
+
 size_t workspace_bytes(int64_t nl, int64_t nr, int lwords, int rwords) {
   const int lv = radix::bj_levels(nl, nr);
   const size_t runs = size_t(groups_of(lv)) * group_size(lv);
   return side_bytes(nl, lwords, lv) + side_bytes(nr, rwords, lv) + align_up(sizeof(uint32_t) * runs, 256) +
-         align_up(sizeof(uint64_t) * groups_of(lv), 256) + align_up(sizeof(int64_t) * 4, 256) + 256;
+         align_up(sizeof(uint64_t) * groups_of(lv), 256) + align_up(sizeof(int64_t) * 4, 256) +
+         sel_bytes(nl, nr, lv) + 256;
 }
 
 template <bool CK, int LV>
@@ -1045,6 +1126,16 @@ int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, con
   if (st != RL_OK) return st;
   PlanArgs a{L.rows, R.rows, L.sub_off, R.sub_off, L.flags, R.flags, counts, gtot, lv, scalars,
              reinterpret_cast<const long long*>(lkeys), L.pay, R.pay, L.words, R.words};
+  const size_t cap = sel_cap_of(nl, nr, lv);
+  if (cap && std::getenv("RL_BJ_NO_SEL") == nullptr) {
+    char* sb = reinterpret_cast<char*>(scalars) + align_up(sizeof(int64_t) * 4, 256);
+    a.sel_pairs = reinterpret_cast<ulonglong2*>(sb);
+    a.sel_idx = reinterpret_cast<uint32_t*>(sb + align_up(16 * cap, 256));
+    a.run_sel = reinterpret_cast<uint32_t*>(sb + align_up(16 * cap, 256) + align_up(4 * cap, 256));
+    a.sel_cursor = reinterpret_cast<unsigned long long*>(scalars + 2);
+    a.sel_cap = uint32_t(std::min<size_t>(cap, 0xFFFFFFFFu));
+    if (cudaMemsetAsync(scalars + 2, 0, sizeof(int64_t), stream) != cudaSuccess) return rl_cuda_status(cudaGetLastError());
+  }
   const int grid = device_sm_count() * 3;
   if (lv == 3) bj_count_kernel<3><<<grid, kThreads, 0, stream>>>(a);
   else bj_count_kernel<2><<<grid, kThreads, 0, stream>>>(a);
@@ -1063,6 +1154,9 @@ int plan(const int64_t* lkeys, int64_t nl, const int64_t* rkeys, int64_t nr, con
   out->left_keys = lkeys;
   out->pay_left = L.pay;
   out->pay_right = R.pay;
+  out->sel_pairs = a.sel_pairs;
+  out->sel_idx = a.sel_idx;
+  out->run_sel = a.run_sel;
   out->words_left = L.words;
   out->words_right = R.words;
   out->carry_cols_left = lc.n;
@@ -1136,6 +1230,9 @@ int emit(const rl_bjoin_plan* p, uint64_t out_begin, uint64_t out_end, uint32_t*
   e.p = PlanArgs{p->rows_left, p->rows_right, p->sub_off_left, p->sub_off_right, p->flags_left, p->flags_right,
                  p->counts, p->offsets, lv, p->scalars, reinterpret_cast<const long long*>(p->left_keys),
                  p->pay_left, p->pay_right, p->words_left, p->words_right};
+  e.p.sel_pairs = static_cast<ulonglong2*>(const_cast<void*>(p->sel_pairs));
+  e.p.sel_idx = const_cast<uint32_t*>(p->sel_idx);
+  e.p.run_sel = const_cast<uint32_t*>(p->run_sel);
   e.out_begin = out_begin;
   e.out_end = out_end;
   e.no_sel = std::getenv("RL_BJ_NO_SEL") != nullptr ? 1 : 0;

@@ -285,3 +285,42 @@ def test_selective_join_listed_runs(emit_path):
     assert (cols[0].dst.cpu().numpy() == lk[wl]).all()
     assert (cols[1].dst.cpu().numpy() == lp[wl]).all()
     assert (cols[2].dst.cpu().numpy() == rp[wr]).all()
+
+
+@pytest.mark.parametrize("levels", [2, 3])
+def test_mixed_dense_and_selective_runs(levels, emit_path, monkeypatch):
+    """One plan holding both kinds of run: the lower half of the key range is
+    ~24 rows a key on each side (dense runs: rows binned and ranked), the
+    upper half ~0.1 matches a row (selective runs: matches listed by the
+    count kernel, the 1/8 rule per run). Pairs, order, slices that start and
+    end inside either kind, checksum and gathered columns equal the oracle,
+    over the two- and the three-level partition."""
+    if levels == 3:
+        monkeypatch.setenv("RL_BJ_LEVELS", "3")
+    rng = np.random.default_rng(47 + levels)
+    half = 200_000
+
+    def side(m):
+        dense = rng.integers(0, 1 << 13, m) * 256  # 8192 keys below 2^21
+        sparse = rng.integers(1 << 21, 1 << 22, m + 17)  # 2M keys above it
+        k = np.concatenate([dense, sparse])
+        return k[rng.permutation(len(k))]
+
+    lk, rk = side(half), side(half + 101)
+    bp = _check(lk, rk)
+    if levels == 3:
+        assert bp.plan.levels == 3
+    wl, wr = O.join_pairs(lk, rk)
+    dense_pairs = int((lk[wl] < (1 << 21)).sum())
+    assert 0 < dense_pairs < bp.total  # both kinds of run produced pairs
+    first_sparse = int(np.argmax(lk[wl] >= (1 << 21)))
+    for a, b in [(first_sparse - 5, first_sparse + 9), (3, bp.total - 3), (bp.total - 1, bp.total)]:
+        gl, gr = _pairs(bp, a, b)
+        assert (gl == wl[a:b]).all() and (gr == wr[a:b]).all()
+    rp = rng.integers(0, 256, (len(rk), 8), dtype=np.uint8)
+    cols = [engine.OutColumn(None, torch.empty(bp.total, dtype=torch.int64, device="cuda"), 8, C.RL_SIDE_KEY),
+            engine.OutColumn(_dev(rp), torch.empty((bp.total, 8), dtype=torch.uint8, device="cuda"), 8,
+                             C.RL_SIDE_RIGHT)]
+    bp.expand(0, bp.total, cols)
+    assert (cols[0].dst.cpu().numpy() == lk[wl]).all()
+    assert (cols[1].dst.cpu().numpy() == rp[wr]).all()

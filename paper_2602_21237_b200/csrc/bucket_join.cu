@@ -64,6 +64,7 @@ constexpr uint32_t kMaxGroups = 1u << 16;  // (three levels)
 constexpr int kMaxG = 256;
 constexpr int kMaxBins = 4096;
 constexpr int kRowsPerThread = (kBjCap + kThreads - 1) / kThreads;  // 5
+static_assert(kRowsPerThread <= 32, "the count kernel keeps a row-hit bit mask in one word");
 constexpr int kRankMax = 48;  // bins above this: a warp's bitonic network
 constexpr uint32_t kSelMax = 512;  // emit: a run with at most this many pairs (and <= 1/8 of its rows) lists its matches instead of sorting
 
@@ -263,13 +264,17 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
         load_rows(a.rows_l, l0, nl, wl);  // in flight while the right side is binned
         __syncthreads();
         bin_rows(w, nrr, bins, nbins, hist, br, scratch, bidx);
+        uint32_t hits = 0;  // bit u: left row u matched (the listing re-probes only those)
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u) {
           if (tid + u * kThreads < int(nl)) {
             const uint32_t b = bins.of(wl[u]);
             const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
             const uint32_t key = uint32_t(wl[u] >> 32);
-            for (uint32_t i = b0; i < b1; ++i) cnt += uint32_t(br[i] >> 32) == key ? 1u : 0u;
+            uint32_t c = 0;
+            for (uint32_t i = b0; i < b1; ++i) c += uint32_t(br[i] >> 32) == key ? 1u : 0u;
+            cnt += c;
+            hits |= (c != 0 ? 1u : 0u) << u;
           }
         }
         if (a.sel_cap) {
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 3) bj_count_kernel(PlanArgs a) {
 #pragma unroll
             for (int u = 0; u < kRowsPerThread; ++u) {
               const uint32_t j = tid + u * kThreads;
-              if (j < nl) {
+              if (hits >> u & 1u) {
                 const uint32_t b = bins.of(wl[u]);
                 const uint32_t b0 = b ? hist[b - 1] : 0u, b1 = hist[b];
                 const uint32_t key = uint32_t(wl[u] >> 32);

@@ -630,6 +630,33 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
     const uint64_t u = mode == 1 ? (v >> shl) | constbits : radix::unpack_key(v, code, constbits);
     return (long long)radix::xform(u, 0);
   };
+  // one listed pair at output row t (l0 / r0: its run's first rows, for carried payloads)
+  auto write_pair = [&](uint64_t t, uint32_t l0, uint32_t r0, const ulonglong2& me, uint32_t pi) {
+    const uint32_t lrow = uint32_t(me.x), rrow = uint32_t(me.y);
+    if constexpr (CHECKSUM) {
+      sum += fmix64((uint64_t(lrow) << 32) | rrow);
+      return;
+    }
+    const uint64_t o = t - e.out_begin;
+    if (e.lrows_out) __stcs(e.lrows_out + o, lrow);
+    if (e.rrows_out) __stcs(e.rrows_out + o, rrow);
+    const uint32_t lj = pi & 0xFFFFu, rj = pi >> 16;
+    for (int ci = 0; ci < cols.n; ++ci) {
+      const EmitCol& c = cols.c[ci];
+      uint8_t* dst = c.dst + o * uint64_t(c.dstride);
+      if (c.side == RL_SIDE_KEY) {
+        __stcs(reinterpret_cast<long long*>(dst), key_of(me.x));
+      } else if (c.carry_off >= 0) {
+        const bool left = c.side == RL_SIDE_LEFT;
+        const uint64_t* pay = left ? a.pay_l : a.pay_r;
+        const int words = left ? a.words_l : a.words_r;
+        const uint64_t at = left ? uint64_t(l0) + lj : uint64_t(r0) + rj;
+        copy_row(reinterpret_cast<const uint8_t*>(pay + at * words) + c.carry_off, dst, c.width);
+      } else {
+        copy_row(c.src + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * c.width, dst, c.width);
+      }
+    }
+  };
 #ifdef RL_BJ_PROFILE
   long long bjt = clock64();
 #endif
@@ -654,6 +681,35 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       if (tid == 0) rpre[nr] = tot;
       __syncthreads();
     }
+    if (a.run_sel) {
+      // listed runs of at most 32 pairs: a warp each, the CTA's warps on different
+      // runs at once (the run loop below would take them one at a time, each a
+      // load -> barrier -> gather round trip); lane q ranks pair q by shuffles
+      const uint32_t lane = tid & 31;
+      for (uint32_t r = tid >> 5; r < nr; r += kThreads / 32) {
+        const uint32_t np = uint32_t(rpre[r + 1] - rpre[r]);
+        const uint64_t base = gbase + rpre[r];
+        if (np == 0 || np > 32 || base + np <= e.out_begin || base >= e.out_end) continue;
+        const uint32_t so = __ldcg(a.run_sel + size_t(g) * G + r);
+        if (so == ~0u) continue;
+        ulonglong2 me = make_ulonglong2(~0ull, ~0ull);
+        uint32_t pi = 0;
+        if (lane < np) {
+          me = __ldcg(a.sel_pairs + so + lane);
+          pi = __ldcg(a.sel_idx + so + lane);
+        }
+        uint32_t rk = 0;
+        for (uint32_t i = 0; i < np; ++i) {
+          const unsigned long long ox = __shfl_sync(0xffffffffu, me.x, i), oy = __shfl_sync(0xffffffffu, me.y, i);
+          rk += (ox < me.x || (ox == me.x && oy < me.y)) ? 1u : 0u;
+        }
+        const uint64_t t = base + rk;
+        if (lane < np && t >= e.out_begin && t < e.out_end) {
+          const uint32_t s = ends[r] >> 16;
+          write_pair(t, offl[s], offr[s], me, pi);
+        }
+      }
+    }
     for (uint32_t r = 0; r < nr; ++r) {
       const uint32_t cnt_pairs = uint32_t(rpre[r + 1] - rpre[r]);
       const uint64_t base = gbase + rpre[r];
@@ -675,35 +731,13 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
             }
             const uint64_t t = base + rk;  // the pair's output row
             if (t < e.out_begin || t >= e.out_end) continue;
-            const uint32_t lrow = uint32_t(me.x), rrow = uint32_t(me.y);
-            if constexpr (CHECKSUM) {
-              sum += fmix64((uint64_t(lrow) << 32) | rrow);
-              continue;
-            }
-            const uint64_t o = t - e.out_begin;
-            if (e.lrows_out) __stcs(e.lrows_out + o, lrow);
-            if (e.rrows_out) __stcs(e.rrows_out + o, rrow);
-            const uint32_t lj = pidx[q] & 0xFFFFu, rj = pidx[q] >> 16;
-            for (int ci = 0; ci < cols.n; ++ci) {
-              const EmitCol& c = cols.c[ci];
-              uint8_t* dst = c.dst + o * uint64_t(c.dstride);
-              if (c.side == RL_SIDE_KEY) {
-                __stcs(reinterpret_cast<long long*>(dst), key_of(me.x));
-              } else if (c.carry_off >= 0) {
-                const bool left = c.side == RL_SIDE_LEFT;
-                const uint64_t* pay = left ? a.pay_l : a.pay_r;
-                const int words = left ? a.words_l : a.words_r;
-                const uint64_t at = left ? uint64_t(l0) + lj : uint64_t(r0) + rj;
-                copy_row(reinterpret_cast<const uint8_t*>(pay + at * words) + c.carry_off, dst, c.width);
-              } else {
-                copy_row(c.src + uint64_t(c.side == RL_SIDE_LEFT ? lrow : rrow) * c.width, dst, c.width);
-              }
-            }
+            write_pair(t, l0, r0, me, pidx[q]);
           }
       };
       if (a.run_sel) {  // listed by the count kernel: neither side's rows are needed
         const uint32_t so = __ldcg(a.run_sel + size_t(g) * G + r);
         if (so != ~0u) {
+          if (cnt_pairs <= 32) continue;  // (written by a warp above)
           ulonglong2* pairs = reinterpret_cast<ulonglong2*>(gx);
           uint32_t* pidx = omap;
           for (uint32_t q = tid; q < cnt_pairs; q += kThreads) {

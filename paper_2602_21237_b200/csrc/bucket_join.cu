@@ -692,6 +692,10 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
         if (np == 0 || np > 32 || base + np <= e.out_begin || base >= e.out_end) continue;
         const uint32_t so = __ldcg(a.run_sel + size_t(g) * G + r);
         if (so == ~0u) continue;
+        // the run's first rows from global, not offl / offr: a warp still here may
+        // overlap the next group's rewrite of those (no barrier after this loop)
+        const uint32_t s = ends[r] >> 16;
+        const uint32_t l0 = __ldcg(a.off_l + size_t(g) * G + s), r0 = __ldcg(a.off_r + size_t(g) * G + s);
         ulonglong2 me = make_ulonglong2(~0ull, ~0ull);
         uint32_t pi = 0;
         if (lane < np) {
@@ -704,10 +708,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
           rk += (ox < me.x || (ox == me.x && oy < me.y)) ? 1u : 0u;
         }
         const uint64_t t = base + rk;
-        if (lane < np && t >= e.out_begin && t < e.out_end) {
-          const uint32_t s = ends[r] >> 16;
-          write_pair(t, offl[s], offr[s], me, pi);
-        }
+        if (lane < np && t >= e.out_begin && t < e.out_end) write_pair(t, l0, r0, me, pi);
       }
     }
     for (uint32_t r = 0; r < nr; ++r) {

@@ -29,7 +29,9 @@
 //      row-interleaved (a destination stride per column). Both sides are sorted
 //      in one set of barrier phases (packed left / right bin counters); a run
 //      with few pairs (<= 512 and <= 1/8 of its rows: selective joins) bins
-//      only the right side, lists its matches and writes each at its rank.
+//      only the right side, lists its matches and writes each at its rank
+//      (two-level plans: the count kernel lists them; runs of <= 32 pairs are
+//      written a warp each, ranked by shuffles).
 //
 // DRAM traffic per side: 8n (counts) + 16n (digit-7 pass) + 16n (digit-6
 // pass) + 8n (count) + 8n (emit); no position, key-value, offset or

@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 2) bj_emit_kernel(EmitArgs e, Cols c
       if (tid == 0) rpre[nr] = tot;
       __syncthreads();
     }
-    if (a.run_sel) {
+    if (LEVELS == 2 && a.run_sel) {  // (three-level plans list nothing: sel_cap_of)
       // listed runs of at most 32 pairs: a warp each, the CTA's warps on different
       // runs at once (the run loop below would take them one at a time, each a
       // load -> barrier -> gather round trip); lane q ranks pair q by shuffles
